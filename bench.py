@@ -1,0 +1,315 @@
+#!/usr/bin/env python3
+"""Branch-parallel decode benchmark (BASELINE.json metric, configs[1] shape).
+
+Workload (one "step"): every branch of every request appends its new token's K/V into the
+paged cache (RoPE fused) and attends over shared Map prefix + its own suffix — the decode
+hot path of engine.cpp:599-641 (resolve + ToyModel::step attention + extend), batched.
+  per request: Qwen2.5-32B attention shape (40 q / 8 kv heads, head_dim 128, bf16),
+  4096-token shared Map prefix, 8 branches x 1024 tokens, KV pages of 16 tokens.
+  R requests per GPU (default 16 -> 0.8 GB of KV, larger than the 126 MB L2: no flush needed).
+
+Prints ONE JSON line (rank 0). `--impl reference` times the reference CPU path instead: the
+oracle restatement of toy_model.cpp:121-157 (fp64, GQA) on all host cores ("port"; the
+reference's own attention only exists fused inside a full fp64 ToyModel::step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+HQ, HKV, D = 40, 8, 128
+PREFIX, BRANCHES, BRANCH_LEN = 4096, 8, 1024
+METRIC = "branch-parallel decode tokens/s/GPU; attention HBM GB/s vs 8 TB/s roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--requests", type=int, default=16, help="requests per GPU")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.t.join(timeout=2)
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples if len(s) >= 6 for k in range(4) if s[2 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference(seconds: float):
+    """Oracle restatement of the reference attention core on all host cores, one request's step
+    (8 branches x 40 heads over 4096+1024 tokens) repeated for ~`seconds`."""
+    import oracle
+    rng = np.random.default_rng(0)
+    n_rows = PREFIX + BRANCHES * BRANCH_LEN
+    K = rng.uniform(-1, 1, (n_rows, HKV, D))
+    V = rng.uniform(-1, 1, (n_rows, HKV, D))
+    q = rng.uniform(-1, 1, (BRANCHES, HQ, D))
+    ctx = [list(range(PREFIX)) + list(range(PREFIX + b * BRANCH_LEN, PREFIX + (b + 1) * BRANCH_LEN))
+           for b in range(BRANCHES)]
+    threads = os.cpu_count() or 1
+    oracle.attn_decode(q, K, V, ctx, nthreads=threads)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.attn_decode(q, K, V, ctx, nthreads=threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"value": BRANCHES * reps / el, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{reps} decode steps of 1 request (8 branches x 40 heads, ctx 4096+1024, fp64) "
+                      f"in {el:.1f} s on {threads} threads"}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cpu = cpu_reference(max(2.0, args.cpu_seconds))
+    line = {"impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * BRANCHES / cpu["value"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[1]: 40q/8kv heads, d128, 4K shared prefix, 8 branches x 1K, page 16",
+                       "sample": cpu["sample"]},
+            "cpu_baseline": cpu,
+            "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def build_workload(mv, torch, R, dev):
+    """R requests: root prefix, fork into 8 branches, 1023 private tokens each (positions shared start)."""
+    pages = R * (PREFIX // 16 + BRANCHES * (BRANCH_LEN // 16 + 4)) + 1024
+    st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=HKV)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234)
+
+    def rnd(*shape):
+        return (torch.rand(*shape, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
+
+    branches, positions = [], []
+    for r in range(R):
+        root = st.create()
+        st.append_many(root, torch.full((PREFIX,), 11, dtype=torch.int32, device=dev),
+                       torch.arange(PREFIX, dtype=torch.int32, device=dev), 0, rnd(PREFIX, HKV, D),
+                       rnd(PREFIX, HKV, D))
+        for b in st.fork(root, BRANCHES):
+            n = BRANCH_LEN - 1
+            st.append_many(b, torch.full((n,), 12, dtype=torch.int32, device=dev),
+                           torch.arange(PREFIX, PREFIX + n, dtype=torch.int32, device=dev), 0, rnd(n, HKV, D),
+                           rnd(n, HKV, D))
+            branches.append(b)
+            positions.append(PREFIX + n)
+        st.release(root)  # the parent lane waits; its prefix pages live on through the branches
+    torch.cuda.synchronize()
+    return st, branches, positions, rnd
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+    import paper_2506_09991_b200 as mv
+
+    R = args.requests
+    st, handles, pos0, rnd = build_workload(mv, torch, R, dev)
+    n = len(handles)
+    steps_total = args.warmup + args.steps
+    # per-step inputs (device resident for `value`)
+    qs = [rnd(n, HQ, D) for _ in range(2)]
+    ks = [rnd(n, HKV, D) for _ in range(2)]
+    vs = [rnd(n, HKV, D) for _ in range(2)]
+    toks = torch.full((n,), 13, dtype=torch.int32, device=dev)
+    out = torch.empty(n, HQ, D, dtype=torch.bfloat16, device=dev)
+    base_pos = torch.tensor(pos0, dtype=torch.int32, device=dev)
+
+    def step(i, q, k, v, p):
+        st.append(handles, toks, p, 0, k, v)
+        mv.attention.decode(st, handles, q, p, out=out)
+
+    stream = torch.cuda.current_stream()
+    for i in range(args.warmup):
+        step(i, qs[i % 2], ks[i % 2], vs[i % 2], base_pos + i)
+    torch.cuda.synchronize()
+    info = st.plan_info()
+
+    # ---- timed region (device events; attention launches bracketed separately) ----
+    clocks = Clocks(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    att = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev[0].record(stream)
+    for s in range(args.steps):
+        i = args.warmup + s
+        p = base_pos + i
+        st.append(handles, toks, p, 0, ks[i % 2], vs[i % 2])
+        att[s][0].record(stream)
+        mv.attention.decode(st, handles, qs[i % 2], p, out=out)
+        att[s][1].record(stream)
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev[0].elapsed_time(ev[1]) / args.steps
+    att_ms = float(np.mean([a.elapsed_time(b) for a, b in att]))
+    if world > 1:
+        t = torch.tensor([ms, att_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, att_ms = t.tolist()
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the region ----
+    hq_ = [qs[j].cpu().pin_memory() for j in range(2)]
+    hk_ = [ks[j].cpu().pin_memory() for j in range(2)]
+    hv_ = [vs[j].cpu().pin_memory() for j in range(2)]
+    hout = torch.empty(n, HQ, D, dtype=torch.bfloat16).pin_memory()
+    hpos = torch.empty(n, dtype=torch.int32).pin_memory()
+    dq, dk, dv, dp = (torch.empty_like(qs[0]), torch.empty_like(ks[0]), torch.empty_like(vs[0]),
+                      torch.empty(n, dtype=torch.int32, device=dev))
+    e2e_steps = max(3, args.steps // 2)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ee = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ee[0].record(stream)
+    for s in range(e2e_steps):
+        i = args.warmup + args.steps + s
+        hpos.copy_(torch.tensor(pos0, dtype=torch.int32) + i)
+        dq.copy_(hq_[i % 2], non_blocking=True)
+        dk.copy_(hk_[i % 2], non_blocking=True)
+        dv.copy_(hv_[i % 2], non_blocking=True)
+        dp.copy_(hpos, non_blocking=True)
+        st.append(handles, toks, dp, 0, dk, dv)
+        mv.attention.decode(st, handles, dq, dp, out=out)
+        hout.copy_(out, non_blocking=True)
+        stream.synchronize()  # the caller reads this step's result before the next step
+    ee[1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = ee[0].elapsed_time(ee[1]) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+    h2d = n * (HQ + 2 * HKV) * D * 2 + n * 4
+    d2h = n * HQ * D * 2
+
+    tokens_per_step = n * world
+    value = tokens_per_step / (ms / 1e3)
+    # roofline of the dominant kernel: algorithmic bytes = unique KV read once + Q/O
+    kv_tokens = info["unique_kv_tokens"]
+    alg_bytes = kv_tokens * HKV * D * 2 * 2 + n * HQ * D * 2 * 2
+    achieved = alg_bytes / (att_ms / 1e3) / 1e9
+    peak, peak_kind = peaks()
+    traffic = None
+    try:
+        with open(os.path.join(REPO, "profiles", "decode_traffic.json")) as f:
+            tj = json.load(f)
+            if tj.get("requests") == R:
+                traffic = tj.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    if rank == 0:
+        cpu = cpu_reference(args.cpu_seconds) if world == 1 else None
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "configs[1] x R requests per GPU: 40q/8kv heads, d128, bf16, 4K shared Map "
+                                   "prefix, 8 branches x 1K tokens (+1 per step), KV page 16",
+                       "requests_per_gpu": R, "branches_per_gpu": n, "l2": "inputs 0.8+ GB > L2 (no flush)",
+                       "step": "append 1 token K/V per branch (RoPE fused) + cascade decode attention"},
+            "e2e": {"value": tokens_per_step / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "kernel": "decode_kernel+combine_kernel", "alg_bytes_per_launch": alg_bytes,
+                         "launch_ms": att_ms, "frac_of_8TBs": achieved / 8000.0},
+            "gpu_launches": 3 * args.steps,
+            "clocks": clk,
+            "plan": info,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

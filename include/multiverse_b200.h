@@ -1,0 +1,233 @@
+/*
+ * multiverse_b200.h — C-ABI of the B200-native Multiverse Attention hot path.
+ *
+ * This is the drop-in boundary for the reference's proj/core hot-path interface
+ * (SURVEY.md §8b). Every entry point cites the reference interface it replaces.
+ * Plain pointers, sizes and status codes only: no torch or C++ types.
+ *
+ * Conventions
+ *   - Every function returns mv_status; on failure mv_last_error() (thread-local) holds
+ *     a message. Status codes mirror the reference's exception kinds:
+ *       CacheError::Kind      kvcache.hpp:32-41  -> MV_ERR_UNKNOWN_HANDLE .. MV_ERR_NOT_DESCENDANT
+ *       ParseError::Kind      grammar.hpp:136-152 -> MV_ERR_MALFORMED, MV_ERR_COUNT_MISMATCH
+ *       std::invalid_argument (toy_model.cpp:47-51, kvcache.cpp:153-156) -> MV_ERR_INVALID_ARGUMENT
+ *     The reference reports an unknown handle as DoubleRelease (kvcache.cpp:16-20); so do we.
+ *   - "d_" pointers are caller-owned device memory; "h_" pointers are host memory.
+ *   - mv_stream_t is ABI-identical to cudaStream_t (NULL = legacy default stream).
+ *   - Tag-stream encoding: tok::Tokenizer ids (tokenizer.cpp:56-63): ids 0..9 are the ten
+ *     control tags in TagKind order (grammar.hpp:34-46), ids >= 10 are text.
+ */
+#ifndef MULTIVERSE_B200_H_
+#define MULTIVERSE_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MV_API __attribute__((visibility("default")))
+#else
+#define MV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* mv_stream_t;
+
+typedef enum {
+  MV_OK = 0,
+  MV_ERR_UNKNOWN_HANDLE = 1,   /* CacheError::UnknownHandle */
+  MV_ERR_DOUBLE_RELEASE = 2,   /* CacheError::DoubleRelease (also unknown handles, kvcache.cpp:16-20) */
+  MV_ERR_CAPACITY = 3,         /* CacheError::CapacityExceeded */
+  MV_ERR_NOT_DESCENDANT = 4,   /* CacheError::BranchNotDescendant */
+  MV_ERR_MALFORMED = 5,        /* ParseError::MalformedStructure */
+  MV_ERR_COUNT_MISMATCH = 6,   /* ParseError::CountMismatch */
+  MV_ERR_INVALID_ARGUMENT = 7, /* std::invalid_argument */
+  MV_ERR_CUDA = 8,             /* CUDA runtime failure */
+  MV_ERR_DEPTH = 9             /* nesting deeper than the caller's exclusion capacity */
+} mv_status;
+
+/* Thread-local message for the last non-OK status. */
+MV_API const char* mv_last_error(void);
+/* Library version string and the compiled device architecture ("sm_100a"). */
+MV_API const char* mv_version(void);
+
+/* ======================================================================== */
+/* K1 — structured mask and position-id builder                              */
+/* ======================================================================== */
+/*
+ * Replaces dag::build_dag + dag::assign_positions + dag::build_mask
+ * (dag.hpp:94-110, dag.cpp:117-263) and the parse errors of grammar::parse
+ * (grammar.cpp:156-294), for a batch of tag streams in one launch.
+ *
+ *   d_tokens   int32 ids, all sequences concatenated; sequence s is
+ *              [h_offsets[s], h_offsets[s+1])
+ *   d_positions int32[n_total]  Multiverse position ids (assign_positions)
+ *   d_seg_id   int32[n_total]   segment id per token in creation order (GenerationDag::segments
+ *                               index; NULL to skip)
+ *   d_excl     int32[n_total][max_depth][2]  per-token exclusion intervals [lo, hi) of
+ *              sequence-local layout rows: mask[i][j] = j <= i and j in no interval of row i.
+ *              This is the compact form of build_mask (dag.cpp:243-263); unused = (0,0).
+ *   d_status   int32[n_seq] per-sequence status (MV_OK / MV_ERR_MALFORMED /
+ *              MV_ERR_COUNT_MISMATCH / MV_ERR_DEPTH), written asynchronously.
+ *   d_workspace / workspace_bytes from mv_visibility_workspace_size.
+ */
+MV_API size_t mv_visibility_workspace_size(const int64_t* h_offsets, int32_t n_seq);
+MV_API mv_status mv_visibility(const int32_t* d_tokens, const int64_t* h_offsets, int32_t n_seq, int32_t max_depth,
+                        int32_t* d_positions, int32_t* d_seg_id, int32_t* d_excl, int32_t* d_status,
+                        void* d_workspace, size_t workspace_bytes, mv_stream_t stream);
+
+/*
+ * Dense legacy dag::Mask (dag.hpp:59-73) from the intervals: rows [row0, row1) of one
+ * sequence of length n, MSB-first packed bits, row-major ((row1-row0)*n bits).
+ */
+MV_API mv_status mv_mask_packed(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t row0, int32_t row1,
+                         uint8_t* d_out, mv_stream_t stream);
+
+/*
+ * Prefill tile map: classifies every (q-tile, k-tile) of block size `tile` as skipped
+ * (fully masked), full (no masking needed) or partial. d_count[n_qt] receives the
+ * number of non-skipped k-tiles per q-tile; d_list[n_qt][n_qt] their k-tile indices
+ * (ascending), with bit 30 set for partial tiles. Returns the total visible pair count
+ * (popcount of the mask) in *d_visible_pairs (int64, accumulated atomically; zero it first).
+ */
+MV_API mv_status mv_tile_map(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t tile, int32_t* d_count,
+                      int32_t* d_list, unsigned long long* d_visible_pairs, mv_stream_t stream);
+
+/* ======================================================================== */
+/* K2 — paged KV store with Process-stage fork and Reduce-stage merge        */
+/* ======================================================================== */
+/*
+ * Replaces kv::RadixStore (kvcache.hpp:60-154). Pages of 16 token slots live in device
+ * memory; each handle owns a device page table of ragged (page, begin, count) entries
+ * (SURVEY.md §7 H1). fork copies page tables and bumps page refcounts; merge concatenates
+ * page tables; neither moves a KV byte (bytes_copied == 0 by construction, reported
+ * from a device counter of payload bytes written by fork/merge kernels).
+ *
+ * Slots of one page may be shared by several tables: a page is "sealed" for in-place
+ * appends once its tail is shared (fork, merge, functional extend).
+ */
+typedef struct mv_kv_store mv_kv_store;
+
+typedef struct {
+  int32_t num_pages;      /* page pool size; tokens capacity = 16 * num_pages (CapacityExceeded beyond) */
+  int32_t record_bytes;   /* opaque per-token payload record (RadixStore payload_record_size); 0 = none */
+  int32_t layers;         /* attention KV plane: bf16 K and V, [layer][page][kv_head][16][head_dim] */
+  int32_t kv_heads;       /*   (0 = no attention plane) */
+  int32_t head_dim;       /*   must be 128 when kv_heads > 0 */
+  int64_t table_entries;  /* device page-table arena capacity in entries (0 = 4 * num_pages + 65536) */
+  double rope_base;       /* rotary base for K at append (toy_model.cpp:30-41); 0 = 10000 */
+} mv_kv_config;
+
+/* StorageStats (kvcache.hpp:43-50); physical/node/refcount are page-level for this store. */
+typedef struct {
+  uint64_t physical_tokens_stored;   /* distinct slots referenced by live handles */
+  uint64_t logical_tokens_reachable; /* sum of live handle lengths */
+  uint64_t bytes_copied_on_last_op;  /* payload bytes duplicated by the last op: always 0 */
+  uint64_t live_handles;
+  uint64_t node_count;               /* pages with refcount > 0 */
+  uint64_t total_refcount;           /* sum of page refcounts (one per table entry) */
+  uint64_t free_pages;
+} mv_kv_stats;
+
+MV_API mv_status mv_kv_store_create(const mv_kv_config* cfg, mv_kv_store** out);
+MV_API mv_status mv_kv_store_destroy(mv_kv_store* s);
+/* All store kernels are issued on this stream (default: NULL). */
+MV_API mv_status mv_kv_set_stream(mv_kv_store* s, mv_stream_t stream);
+/* Device pointers of the attention planes (for callers that run their own kernels). */
+MV_API mv_status mv_kv_planes(mv_kv_store* s, int32_t layer, void** d_k, void** d_v);
+
+/* RadixStore::create (kvcache.hpp:66-67). */
+MV_API mv_status mv_kv_create(mv_kv_store* s, uint64_t* out_handle);
+/* RadixStore::extend (kvcache.hpp:69-75): new handle = h ++ tokens; h stays live.
+ * h_payloads: n * record_bytes host bytes, or NULL. */
+MV_API mv_status mv_kv_extend(mv_kv_store* s, uint64_t h, const int32_t* h_tokens, int64_t n, const void* h_payloads,
+                       uint64_t* out_handle);
+/* RadixStore::fork (kvcache.hpp:77-78): n handles resolving to h's tokens. */
+MV_API mv_status mv_kv_fork(mv_kv_store* s, uint64_t h, int32_t n, uint64_t* out_handles);
+/* RadixStore::merge (kvcache.hpp:80-83): prefix ++ each branch's suffix, in order.
+ * MV_ERR_NOT_DESCENDANT if a branch is shorter or does not physically share the prefix
+ * slot-for-slot (kvcache.cpp:262-275). */
+MV_API mv_status mv_kv_merge(mv_kv_store* s, uint64_t prefix, const uint64_t* h_branches, int32_t n_branches,
+                      uint64_t* out_handle);
+/* RadixStore::release (kvcache.hpp:85-87). */
+MV_API mv_status mv_kv_release(mv_kv_store* s, uint64_t h);
+MV_API mv_status mv_kv_length(mv_kv_store* s, uint64_t h, int64_t* out_len);
+MV_API mv_status mv_kv_stats_get(mv_kv_store* s, mv_kv_stats* out);
+/* RadixStore::resolve / resolve_payloads / resolve_slots (kvcache.hpp:91-95), into host
+ * buffers of length() entries (payloads: length() * record_bytes bytes). */
+MV_API mv_status mv_kv_resolve(mv_kv_store* s, uint64_t h, int32_t* h_tokens);
+MV_API mv_status mv_kv_resolve_payloads(mv_kv_store* s, uint64_t h, void* h_out);
+MV_API mv_status mv_kv_resolve_slots(mv_kv_store* s, uint64_t h, uint32_t* h_slots);
+
+/*
+ * Engine fast path (replaces the per-token extend + release pair of engine.cpp:639-641):
+ * append one token to each of n handles IN PLACE (handle ids unchanged), allocating pages
+ * on device as needed, and write the token's attention K/V for `layer`:
+ * K is rotated (interleaved RoPE, toy_model.cpp:30-41) at d_positions[i] before it is
+ * cached; V is cached as given (toy_model.cpp:116-119).
+ *   d_tokens int32[n]; d_positions int32[n]; d_k, d_v bf16[n][kv_heads][head_dim]
+ * Pass d_k = d_v = NULL to append token ids only.
+ */
+MV_API mv_status mv_kv_append(mv_kv_store* s, const uint64_t* h_handles, int32_t n, const int32_t* d_tokens,
+                       const int32_t* d_positions, int32_t layer, const void* d_k, const void* d_v);
+/* Write K/V of the LAST token of each handle for another layer (multi-layer models). */
+MV_API mv_status mv_kv_write_last(mv_kv_store* s, const uint64_t* h_handles, int32_t n, const int32_t* d_positions,
+                           int32_t layer, const void* d_k, const void* d_v);
+/* Bulk prefill of a handle's attention plane: n tokens appended in place with K/V rows
+ * d_k/d_v bf16[n][kv_heads][head_dim] at positions d_positions[n]. */
+MV_API mv_status mv_kv_append_many(mv_kv_store* s, uint64_t h, int64_t n, const int32_t* d_tokens,
+                            const int32_t* d_positions, int32_t layer, const void* d_k, const void* d_v);
+/* Gather a handle's cached K and V (post-RoPE, bf16 [len][kv_heads][head_dim]) into device buffers. */
+MV_API mv_status mv_kv_gather_kv(mv_kv_store* s, uint64_t h, int32_t layer, void* d_k, void* d_v);
+
+/* ======================================================================== */
+/* K4 — branch-parallel paged decode attention (split-KV, cascade)           */
+/* ======================================================================== */
+/*
+ * Replaces the attention core of ToyModel::step (toy_model.cpp:121-157) over the
+ * context that engine.cpp:603-607 resolves for every active lane — for ALL lanes of
+ * all requests in one launch. Shared Map-prefix pages (from fork lineage) are read once
+ * per group of sibling branches (cascade); GQA query heads of one KV head are packed
+ * into the same tile.
+ *
+ *   h_handles[n]   the decoding sequences (their current cache includes the new token)
+ *   d_q            bf16[n][q_heads][head_dim] pre-RoPE queries; rotated in-kernel at
+ *                  d_positions[i] (interleaved RoPE)
+ *   d_out          bf16[n][q_heads][head_dim]
+ * The plan (cascade units, split-KV chunks, partial buffers) is built and cached inside the
+ * store; it is rebuilt automatically when the handles' page tables change.
+ */
+MV_API mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_t* h_handles, int32_t n, int32_t q_heads,
+                         const void* d_q, const int32_t* d_positions, void* d_out);
+
+/* Decode-plan statistics of the last mv_attn_decode call on this store (host ints). */
+typedef struct {
+  int32_t units, chunks, work_items, partial_slots;
+  int64_t unique_kv_tokens;   /* tokens of KV read once per step (sum over units) */
+  int64_t naive_kv_tokens;    /* tokens a per-branch decode would read (sum of lengths) */
+} mv_decode_plan_info;
+MV_API mv_status mv_attn_decode_plan_info(mv_kv_store* s, mv_decode_plan_info* out);
+
+/* ======================================================================== */
+/* K3 — branch-masked prefill attention (tcgen05 / TMEM / TMA)               */
+/* ======================================================================== */
+/*
+ * Replaces the attention inside ToyModel::forward (toy_model.cpp:174-202) for a whole
+ * structured sequence at once:
+ *   d_q bf16[n][q_heads][128], d_k / d_v bf16[n][kv_heads][128] (pre-RoPE, rotated in
+ *   kernel at d_positions), d_excl from mv_visibility, d_out bf16[n][q_heads][128].
+ * Fully masked cross-branch tiles are skipped using the tile map.
+ */
+MV_API size_t mv_prefill_workspace_size(int32_t n, int32_t q_heads, int32_t kv_heads);
+MV_API mv_status mv_attn_prefill(const void* d_q, const void* d_k, const void* d_v, const int32_t* d_positions,
+                          const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
+                          double rope_base, void* d_out, void* d_workspace, size_t workspace_bytes,
+                          mv_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MULTIVERSE_B200_H_ */

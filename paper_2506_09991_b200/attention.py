@@ -1,0 +1,34 @@
+"""Branch-parallel paged decode (K4) and branch-masked prefill (K3) attention on the device."""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import check, lib
+from .kv import PagedStore, _p, _u64_array
+
+
+def decode(store: PagedStore, handles, q: torch.Tensor, positions: torch.Tensor, layer: int = 0,
+           out: torch.Tensor | None = None) -> torch.Tensor:
+    """q: bf16 [n, Hq, 128] pre-RoPE queries of the tokens just appended to `handles`."""
+    assert q.dtype == torch.bfloat16 and q.is_cuda and q.is_contiguous()
+    n, hq, d = q.shape
+    out = torch.empty_like(q) if out is None else out
+    check(lib.mv_attn_decode(store.handle, layer, _u64_array(handles), n, hq, _p(q), _p(positions), _p(out)))
+    return out
+
+
+def prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, positions: torch.Tensor, excl: torch.Tensor,
+            rope_base: float = 10000.0, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+    """q bf16 [n, Hq, 128]; k, v bf16 [n, Hkv, 128] (pre-RoPE); excl int32 [n, D, 2] from dag.build_visibility."""
+    n, hq, d = q.shape
+    hkv = k.shape[1]
+    out = torch.empty_like(q) if out is None else out
+    ws_bytes = lib.mv_prefill_workspace_size(n, hq, hkv)
+    if workspace is None or workspace.numel() < ws_bytes:
+        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
+    check(lib.mv_attn_prefill(_p(q), _p(k), _p(v), _p(positions), _p(excl), excl.shape[1], n, hq, hkv, rope_base,
+                              _p(out), _p(workspace), ws_bytes,
+                              ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out

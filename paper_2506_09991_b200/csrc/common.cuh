@@ -1,0 +1,158 @@
+// common.cuh — shared helpers for the sm_100a kernels (PTX wrappers, status plumbing).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "multiverse_b200.h"
+
+namespace mv {
+
+// Thread-local last-error message behind mv_last_error().
+void set_error(const std::string& msg);
+mv_status fail(mv_status st, const std::string& msg);
+
+#define MV_CUDA_TRY(expr)                                                                    \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return ::mv::fail(MV_ERR_CUDA, std::string(#expr " failed: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define MV_LAUNCH_CHECK()                                                                          \
+  do {                                                                                             \
+    cudaError_t _e = cudaGetLastError();                                                           \
+    if (_e != cudaSuccess) return ::mv::fail(MV_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+constexpr int kPageTokens = 16;   // tokens per KV page (BASELINE configs[1] "paged KV block 16")
+constexpr int kHeadDim = 128;     // Qwen2.5-32B head dim; the attention kernels are specialised for it
+constexpr int kTagCount = 10;     // grammar.hpp:47 kTagLiteralCount
+
+// Tag ids (tokenizer.cpp:56-63 / grammar.hpp:34-46).
+enum Tag : int32_t {
+  kParOpen = 0, kParClose, kGoalOpen, kGoalClose, kOutOpen, kOutClose, kPathOpen, kPathClose, kConcOpen, kConcClose
+};
+
+// ---------------------------------------------------------------------------
+// Page-table entry: a ragged run of `count` token slots starting at `begin` inside
+// `page`. Packed in an int2 so a warp reads 32 entries in one 256 B load.
+// ---------------------------------------------------------------------------
+struct __align__(8) PageRef {
+  int32_t page;
+  int32_t bc;  // begin | (count << 8)
+};
+__host__ __device__ inline int ref_begin(PageRef r) { return r.bc & 0xff; }
+__host__ __device__ inline int ref_count(PageRef r) { return (r.bc >> 8) & 0xff; }
+__host__ __device__ inline PageRef make_ref(int page, int begin, int count) {
+  PageRef r;
+  r.page = page;
+  r.bc = begin | (count << 8);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// KV page layout: [page][kv_head][16 tokens][128 dims] bf16, 4 KiB per (page, head).
+// The 16-byte chunk c (8 dims) of token row t is stored at chunk c ^ (t & 7) so that
+// ldmatrix over 8 consecutive token rows is bank-conflict free after a plain 1-D bulk
+// copy (the equivalent of a TMA 128B swizzle, baked into the storage layout).
+// ---------------------------------------------------------------------------
+__host__ __device__ inline int swz_chunk(int token, int chunk) { return chunk ^ (token & 7); }
+__host__ __device__ inline size_t kv_page_head_offset(int64_t page, int head, int kv_heads) {
+  return ((size_t)page * kv_heads + head) * (kPageTokens * kHeadDim);
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers (sm_100a)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared, completing on an mbarrier (TMA engine, no tensor map).
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void ldmatrix_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldmatrix_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3,
+                                                  uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldmatrix_x2(uint32_t& r0, uint32_t& r1, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(addr));
+}
+__device__ __forceinline__ uint32_t movmatrix_trans(uint32_t x) {
+  uint32_t y;
+  asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+// D(16x8 f32) += A(16x16 bf16, row) * B(16x8 bf16, col)
+__device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Interleaved rotary angle for pair t of a 128-dim head (toy_model.cpp:30-41), computed in
+// fp64 (positions reach 1e5 rad) and reduced before the fp32 sincos.
+__device__ __forceinline__ void rope_cs(int pos, int t, double base, float& c, float& s) {
+  double inv = exp2(-2.0 * (double)t / (double)kHeadDim * log2(base));
+  double th = (double)pos * inv;
+  th = th - 6.283185307179586476925286766559 * floor(th * 0.15915494309189533576888376337251);
+  sincosf((float)th, &s, &c);
+}
+
+}  // namespace mv

@@ -1,0 +1,542 @@
+// decode.cu — K4: branch-parallel paged decode attention (split-KV, cascade over fork lineage).
+//
+// Reference behaviour replaced: for every active lane the
+// engine resolves the lane's whole context (engine.cpp:603-605) and runs the attention core
+// of ToyModel::step (toy_model.cpp:121-157): scores q.k/sqrt(dh) over the context in layout
+// order, max-subtract, exp, sum, weighted V sum.  Here all lanes of all requests run in one
+// launch and the shared Map prefix is read from HBM once per group of sibling branches.
+//
+// Plan (host, cached per page-table shape): every decoding handle's table is cut at its fork
+// lineage boundaries; the segment [prev boundary, boundary of group g) is identical in all
+// holders of g, so it becomes ONE cascade unit whose query rows are all holders x GQA heads.
+// Units are split into <= 64-page chunks (split-KV); a work item = (chunk, <= 8 handles).
+//
+// Kernel (one CTA per (work item, KV head)):
+//   warp 6      : producer — 1-D bulk copies (TMA engine) of each 4 KiB K and V page-head
+//                 block into a 15-stage smem ring, mbarrier complete_tx signalling.
+//   warps 0..5  : 3 consumer pairs; pair p takes pages p, p+3, ...  Tokens are the MMA M
+//                 dimension and query rows the N dimension (mma.sync m16n8k16, swapped
+//                 operands), so 40 rows = 5 n8-tiles with no padding; S^T -> P^T goes
+//                 register-to-register through movmatrix.  Both warps of a pair compute
+//                 S = K.Q^T (Q lives in registers); each accumulates O^T for half of the
+//                 128 head dims.  Online softmax in the log2 domain, fp32 accumulation.
+//   epilogue    : the 3 pairs' (m, l, O) are merged through smem and written as one
+//                 partial per (handle, q head); a combine kernel merges the partials of
+//                 each handle's chunks (log-sum-exp) into bf16 outputs.
+#include <algorithm>
+#include <cstring>
+#include <unordered_map>
+#include <vector>
+
+#include "store.hpp"
+
+namespace mv {
+
+namespace {
+
+constexpr int kPairs = 3;  // 7 warps: <= 2 per SM sub-partition -> 255 regs/thread
+constexpr int kConsumerWarps = 2 * kPairs;
+constexpr int kDecThreads = (kConsumerWarps + 1) * 32;
+constexpr int kStages = 15;  // multiple of kPairs: stage s always belongs to pair s % kPairs
+constexpr int kStageBytes = 2 * kPageTokens * kHeadDim * 2;  // K + V page-head blocks
+constexpr int kMaxNT = 5;                                   // <= 40 query rows per CTA
+constexpr int kChunkPages = 64;
+constexpr int kSmemRing = kStages * kStageBytes;            // 128 KiB
+constexpr int kSmemQ = kMaxNT * 8 * kHeadDim * 2;           // 10 KiB
+constexpr int kDecSmem = kSmemRing + kSmemQ + 2 * kStages * 8 + 64;
+
+struct WorkItem {
+  int64_t entry_off;   // absolute arena index of the chunk's first entry
+  int32_t n_entries;
+  int32_t mem_off;     // offset into the member list (batch indices)
+  int32_t n_mem;
+  int32_t slot_base;   // partial slot of the first member
+  int32_t nt;          // n8 row tiles needed
+  int32_t pad;
+};
+
+struct DecodeParams {
+  const PageRef* arena;
+  const __nv_bfloat16* kplane;
+  const __nv_bfloat16* vplane;
+  const __nv_bfloat16* q;     // [n][q_heads][128]
+  const int32_t* pos;         // [n]
+  const WorkItem* items;
+  const int32_t* members;
+  float* part_o;              // [slots][q_heads][128]
+  float2* part_ml;            // [slots][q_heads]
+  int kv_heads, q_heads, gqa;
+  float scale_log2;           // log2(e) / sqrt(128)
+  double rope_base;
+};
+
+template <int NT>
+__device__ __forceinline__ void consume(const DecodeParams& P, const WorkItem& it, int kvh, uint8_t* ring,
+                                        const uint8_t* sq, uint64_t* full, uint64_t* empty, float* s_ml,
+                                        float* s_o) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, hh = warp & 1;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  // Q fragments (B operand, k16 x n8 "col"): rows nt*8.., dims ks*16..
+  uint32_t qb[NT][8][2];
+  const uint32_t sq_base = smem_u32(sq);
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      int row = nt * 8 + (lane & 7);
+      int chunk = ks * 2 + ((lane >> 3) & 1);
+      ldmatrix_x2(qb[nt][ks][0], qb[nt][ks][1], sq_base + row * 256 + (swz_chunk(row, chunk) << 4));
+    }
+
+  float o[4][NT][4];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[mt][nt][k] = 0.f;
+  float m_run[NT][2], l_run[NT][2];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    m_run[nt][0] = m_run[nt][1] = -INFINITY;
+    l_run[nt][0] = l_run[nt][1] = 0.f;
+  }
+
+  const int npages = it.n_entries;
+  for (int j = pair; j < npages; j += kPairs) {
+    const int stage = j % kStages;
+    const PageRef ref = P.arena[it.entry_off + j];
+    const int vb = ref_begin(ref), ve = vb + ref_count(ref);
+    mbar_wait(&full[stage], (j / kStages) & 1);
+    const uint32_t kbase = smem_u32(ring + stage * kStageBytes);
+    const uint32_t vbase = kbase + kPageTokens * kHeadDim * 2;
+
+    // S^T (16 tokens x 8 rows per n-tile) = K . Q^T
+    float s[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      uint32_t a[4];
+      const int mi = lane >> 3;
+      const int row = (mi & 1) * 8 + (lane & 7);
+      const int chunk = ks * 2 + (mi >> 1);
+      ldmatrix_x4(a[0], a[1], a[2], a[3], kbase + row * 256 + (swz_chunk(row, chunk) << 4));
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(s[nt], a, qb[nt][ks][0], qb[nt][ks][1]);
+    }
+
+    // online softmax (log2 domain); tokens g and g+8, rows 2*t4 and 2*t4+1 of each n-tile
+    const bool v0 = g >= vb && g < ve, v1 = g + 8 >= vb && g + 8 < ve;
+    uint32_t pb[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      float x0 = v0 ? s[nt][0] * P.scale_log2 : -INFINITY;
+      float x1 = v0 ? s[nt][1] * P.scale_log2 : -INFINITY;
+      float x2 = v1 ? s[nt][2] * P.scale_log2 : -INFINITY;
+      float x3 = v1 ? s[nt][3] * P.scale_log2 : -INFINITY;
+      float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float mn0 = fmaxf(m_run[nt][0], mx0), mn1 = fmaxf(m_run[nt][1], mx1);
+      const float mu0 = mn0 == -INFINITY ? 0.f : mn0, mu1 = mn1 == -INFINITY ? 0.f : mn1;
+      const float al0 = fast_exp2(m_run[nt][0] - mu0), al1 = fast_exp2(m_run[nt][1] - mu1);
+      m_run[nt][0] = mn0;
+      m_run[nt][1] = mn1;
+      const float p0 = fast_exp2(x0 - mu0), p1 = fast_exp2(x1 - mu1);
+      const float p2 = fast_exp2(x2 - mu0), p3 = fast_exp2(x3 - mu1);
+      l_run[nt][0] = l_run[nt][0] * al0 + p0 + p2;
+      l_run[nt][1] = l_run[nt][1] * al1 + p1 + p3;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        o[mt][nt][0] *= al0;
+        o[mt][nt][1] *= al1;
+        o[mt][nt][2] *= al0;
+        o[mt][nt][3] *= al1;
+      }
+      pb[nt][0] = movmatrix_trans(pack_bf16(p0, p1));
+      pb[nt][1] = movmatrix_trans(pack_bf16(p2, p3));
+    }
+
+    // O^T (dims x rows) += V^T . P^T for this warp's 64 dims
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      uint32_t a[4];
+      const int mi = lane >> 3;
+      const int tok = (mi >> 1) * 8 + (lane & 7);
+      const int chunk = hh * 8 + mt * 2 + (mi & 1);
+      ldmatrix_x4_trans(a[0], a[1], a[2], a[3], vbase + tok * 256 + (swz_chunk(tok, chunk) << 4));
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(o[mt][nt], a, pb[nt][0], pb[nt][1]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[stage]);
+  }
+
+  // finish l (sum over the 8 token-lanes g), publish this pair's (m, l, O^T half) to smem
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float l = l_run[nt][c];
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+      l_run[nt][c] = l;
+    }
+  // consumers finished reading the ring (named barrier over the 8 consumer warps)
+  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerWarps * 32));
+  const int rows = NT * 8;
+  if (hh == 0 && g == 0) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        int r = nt * 8 + 2 * t4 + c;
+        s_ml[(pair * rows + r) * 2 + 0] = m_run[nt][c];
+        s_ml[(pair * rows + r) * 2 + 1] = l_run[nt][c];
+      }
+  }
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int dim = hh * 64 + mt * 16 + g + (k >> 1) * 8;
+        int r = nt * 8 + 2 * t4 + (k & 1);
+        s_o[(pair * rows + r) * kHeadDim + dim] = o[mt][nt][k];
+      }
+  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerWarps * 32));
+
+  // merge the pairs and write one partial per (member, q head)
+  const int nrows = it.n_mem * P.gqa;
+  for (int x = threadIdx.x; x < nrows * kHeadDim; x += kConsumerWarps * 32) {
+    const int r = x / kHeadDim, dim = x % kHeadDim;
+    float m = -INFINITY;
+#pragma unroll
+    for (int p = 0; p < kPairs; ++p) m = fmaxf(m, s_ml[(p * rows + r) * 2]);
+    const float mu = m == -INFINITY ? 0.f : m;
+    float acc = 0.f, l = 0.f;
+#pragma unroll
+    for (int p = 0; p < kPairs; ++p) {
+      const float w = fast_exp2(s_ml[(p * rows + r) * 2] - mu);
+      acc += w * s_o[(p * rows + r) * kHeadDim + dim];
+      l += w * s_ml[(p * rows + r) * 2 + 1];
+    }
+    const int mi = r / P.gqa, hl = r % P.gqa;
+    const int64_t slot = it.slot_base + mi;
+    const int head = kvh * P.gqa + hl;
+    P.part_o[(slot * P.q_heads + head) * kHeadDim + dim] = acc;
+    if (dim == 0) P.part_ml[slot * P.q_heads + head] = make_float2(m, l);
+  }
+}
+
+__global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint8_t* sq = smem + kSmemRing;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemRing + kSmemQ);
+  uint64_t* empty = full + kStages;
+
+  const WorkItem it = P.items[blockIdx.x];
+  const int kvh = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 2);
+    }
+    fence_mbar_init();
+  }
+
+  // Q tile: rows r = member * gqa + local head, RoPE at the member's position, chunk-swizzled.
+  const int rows = it.nt * 8;
+  const int nrows = it.n_mem * P.gqa;
+  for (int x = threadIdx.x; x < rows * 16; x += kDecThreads) {
+    const int r = x >> 4, c = x & 15;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r < nrows) {
+      const int b = P.members[it.mem_off + r / P.gqa];
+      const int head = kvh * P.gqa + r % P.gqa;
+      v = *reinterpret_cast<const uint4*>(P.q + ((size_t)b * P.q_heads + head) * kHeadDim + c * 8);
+      const int pos = P.pos[b];
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float cs, sn;
+        rope_cs(pos, c * 4 + j, P.rope_base, cs, sn);
+        float2 ab = __bfloat1622float2(h2[j]);
+        h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
+      }
+    }
+    *reinterpret_cast<uint4*>(sq + r * 256 + (swz_chunk(r, c) << 4)) = v;
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {
+    // producer
+    if (lane == 0) {
+      const size_t head_off = (size_t)kvh * kPageTokens * kHeadDim;
+      for (int j = 0; j < it.n_entries; ++j) {
+        const int stage = j % kStages;
+        if (j >= kStages) mbar_wait(&empty[stage], ((j / kStages) - 1) & 1);
+        const int64_t page = P.arena[it.entry_off + j].page;
+        const size_t src = (size_t)page * P.kv_heads * kPageTokens * kHeadDim + head_off;
+        uint8_t* dst = ring + stage * kStageBytes;
+        mbar_arrive_expect_tx(&full[stage], kStageBytes);
+        bulk_g2s(dst, P.kplane + src, kStageBytes / 2, &full[stage]);
+        bulk_g2s(dst + kStageBytes / 2, P.vplane + src, kStageBytes / 2, &full[stage]);
+      }
+    }
+    return;
+  }
+
+  float* s_ml = reinterpret_cast<float*>(ring);                       // aliases the ring after the
+  float* s_o = reinterpret_cast<float*>(ring + kPairs * 48 * 2 * 4);  // consumers' barrier
+  switch (it.nt) {
+    case 1: consume<1>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
+    case 2: consume<2>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
+    case 3: consume<3>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
+    case 4: consume<4>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
+    default: consume<5>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
+  }
+}
+
+// Merge every handle's partials (log-sum-exp) into the bf16 output.
+__global__ void combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
+                               const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ slot_idx,
+                               int q_heads, __nv_bfloat16* __restrict__ out) {
+  const int b = blockIdx.x, h = blockIdx.y, dim = threadIdx.x;
+  const int s0 = slot_ptr[b], s1 = slot_ptr[b + 1];
+  float m = -INFINITY;
+  for (int s = s0; s < s1; ++s) m = fmaxf(m, part_ml[(int64_t)slot_idx[s] * q_heads + h].x);
+  const float mu = m == -INFINITY ? 0.f : m;
+  float acc = 0.f, l = 0.f;
+  for (int s = s0; s < s1; ++s) {
+    const int64_t sl = slot_idx[s];
+    const float2 ml = part_ml[sl * q_heads + h];
+    const float w = fast_exp2(ml.x - mu);
+    acc += w * part_o[(sl * q_heads + h) * kHeadDim + dim];
+    l += w * ml.y;
+  }
+  out[((int64_t)b * q_heads + h) * kHeadDim + dim] = __float2bfloat16_rn(l > 0.f ? acc / l : 0.f);
+}
+
+}  // namespace
+
+struct DecodePlanCache {
+  std::vector<uint64_t> handles;
+  std::vector<int64_t> sig;  // per handle: n_entries, lineage size
+  int q_heads = 0;
+  // host plan
+  std::vector<WorkItem> items;
+  std::vector<int32_t> members, slot_ptr, slot_idx;
+  int32_t n_slots = 0;
+  mv_decode_plan_info info{};
+  // device copies
+  WorkItem* d_items = nullptr;
+  int32_t *d_members = nullptr, *d_slot_ptr = nullptr, *d_slot_idx = nullptr;
+  float* d_part_o = nullptr;
+  float2* d_part_ml = nullptr;
+  size_t cap_items = 0, cap_members = 0, cap_ptr = 0, cap_idx = 0, cap_slots = 0;
+  bool smem_set = false;
+  ~DecodePlanCache() {
+    cudaFree(d_items);
+    cudaFree(d_members);
+    cudaFree(d_slot_ptr);
+    cudaFree(d_slot_idx);
+    cudaFree(d_part_o);
+    cudaFree(d_part_ml);
+  }
+};
+
+template <typename T>
+static mv_status ensure_dev(T*& p, size_t& cap, size_t n) {
+  if (n <= cap) return MV_OK;
+  cudaFree(p);
+  p = nullptr;
+  size_t c = std::max<size_t>(n, cap * 2);
+  MV_CUDA_TRY(cudaMalloc(&p, sizeof(T) * c));
+  cap = c;
+  return MV_OK;
+}
+
+static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, int n, int q_heads, int gqa) {
+  pc.items.clear();
+  pc.members.clear();
+  std::vector<std::vector<int32_t>> slots_of(n);
+  int32_t n_slots = 0;
+  int64_t unique_tokens = 0, naive_tokens = 0;
+  const int max_members = std::max(1, (kMaxNT * 8) / gqa);
+
+  // group id -> member batch indices (in batch order)
+  std::unordered_map<uint64_t, std::vector<int32_t>> group_members;
+  std::vector<HandleRec*> recs(n);
+  for (int b = 0; b < n; ++b) {
+    recs[b] = st.find(hs[b]);
+    naive_tokens += recs[b]->n_tokens();
+    for (auto& lg : recs[b]->lineage) group_members[lg.group].push_back(b);
+  }
+
+  auto emit_unit = [&](int64_t src_off, int32_t e0, int32_t e1, const std::vector<int32_t>& mem, int64_t tokens) {
+    if (e1 <= e0 || mem.empty()) return;
+    unique_tokens += tokens;
+    const int32_t npg = e1 - e0;
+    const int32_t nchunks = (npg + kChunkPages - 1) / kChunkPages;
+    for (int32_t c = 0; c < nchunks; ++c) {
+      const int32_t c0 = e0 + (int32_t)((int64_t)npg * c / nchunks);
+      const int32_t c1 = e0 + (int32_t)((int64_t)npg * (c + 1) / nchunks);
+      for (size_t m0 = 0; m0 < mem.size(); m0 += max_members) {
+        const int32_t nm = (int32_t)std::min<size_t>(max_members, mem.size() - m0);
+        WorkItem w;
+        w.entry_off = src_off + c0;
+        w.n_entries = c1 - c0;
+        w.mem_off = (int32_t)pc.members.size();
+        w.n_mem = nm;
+        w.slot_base = n_slots;
+        w.nt = (nm * gqa + 7) / 8;
+        w.pad = 0;
+        for (int32_t k = 0; k < nm; ++k) {
+          pc.members.push_back(mem[m0 + k]);
+          slots_of[mem[m0 + k]].push_back(n_slots + k);
+        }
+        n_slots += nm;
+        pc.items.push_back(w);
+      }
+    }
+  };
+
+  // shared cascade units: one per lineage group with >= 2 decoding holders
+  std::unordered_map<uint64_t, bool> done;
+  for (int b = 0; b < n; ++b) {
+    const HandleRec* r = recs[b];
+    int32_t prev_e = 0;
+    int64_t prev_t = 0;
+    for (auto& lg : r->lineage) {
+      auto& mem = group_members[lg.group];
+      if (mem.size() >= 2 && !done[lg.group]) {
+        done[lg.group] = true;
+        emit_unit(r->arena_off, prev_e, lg.entries, mem, lg.tokens - prev_t);
+      }
+      if (mem.size() >= 2) {
+        prev_e = lg.entries;
+        prev_t = lg.tokens;
+      }
+    }
+    // private remainder (single-holder lineage segments coalesce here)
+    emit_unit(r->arena_off, prev_e, r->n_entries(), std::vector<int32_t>{b}, r->n_tokens() - prev_t);
+  }
+
+  pc.slot_ptr.assign(n + 1, 0);
+  pc.slot_idx.clear();
+  for (int b = 0; b < n; ++b) {
+    pc.slot_ptr[b + 1] = pc.slot_ptr[b] + (int32_t)slots_of[b].size();
+    pc.slot_idx.insert(pc.slot_idx.end(), slots_of[b].begin(), slots_of[b].end());
+  }
+  pc.n_slots = n_slots;
+  pc.info.units = 0;
+  pc.info.chunks = 0;
+  pc.info.work_items = (int32_t)pc.items.size();
+  pc.info.partial_slots = n_slots;
+  pc.info.unique_kv_tokens = unique_tokens;
+  pc.info.naive_kv_tokens = naive_tokens;
+}
+
+}  // namespace mv
+
+using namespace mv;
+
+extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_t* hs, int32_t n, int32_t q_heads,
+                                    const void* d_q, const int32_t* d_positions, void* d_out) {
+  if (!s || !s->impl) return fail(MV_ERR_INVALID_ARGUMENT, "null store");
+  PagedStore& st = *s->impl;
+  const mv_kv_config& cfg = st.cfg();
+  if (cfg.kv_heads <= 0 || layer < 0 || layer >= cfg.layers)
+    return fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_decode: no attention plane for this layer");
+  if (n <= 0) return n == 0 ? MV_OK : fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_decode: n < 0");
+  if (q_heads <= 0 || q_heads % cfg.kv_heads) return fail(MV_ERR_INVALID_ARGUMENT, "q_heads % kv_heads != 0");
+  const int gqa = q_heads / cfg.kv_heads;
+  if (gqa > kMaxNT * 8) return fail(MV_ERR_INVALID_ARGUMENT, "GQA group larger than 40 heads");
+  if (!d_q || !d_positions || !d_out) return fail(MV_ERR_INVALID_ARGUMENT, "null buffer");
+
+  if (!st.plan) st.plan = new DecodePlanCache();
+  DecodePlanCache& pc = *st.plan;
+  // plan signature: the handle list plus each table's entry count and lineage depth
+  std::vector<int64_t> sig(2 * (size_t)n);
+  for (int b = 0; b < n; ++b) {
+    HandleRec* r = st.find(hs[b]);
+    if (!r) return fail(MV_ERR_DOUBLE_RELEASE, "handle " + std::to_string(hs[b]) + " is unknown or already released");
+    if (r->n_tokens() == 0) return fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_decode: empty context");
+    sig[2 * b] = r->n_entries();
+    sig[2 * b + 1] = (int64_t)r->lineage.size();
+  }
+  const bool same = pc.q_heads == q_heads && pc.handles.size() == (size_t)n &&
+                    std::equal(pc.handles.begin(), pc.handles.end(), hs) && pc.sig == sig;
+  cudaStream_t stream = st.stream();
+  if (!same) {
+    build_plan(st, pc, hs, n, q_heads, gqa);
+    pc.handles.assign(hs, hs + n);
+    pc.sig = sig;
+    pc.q_heads = q_heads;
+    if (mv_status e = ensure_dev(pc.d_items, pc.cap_items, pc.items.size())) return e;
+    if (mv_status e = ensure_dev(pc.d_members, pc.cap_members, std::max<size_t>(1, pc.members.size()))) return e;
+    if (mv_status e = ensure_dev(pc.d_slot_ptr, pc.cap_ptr, pc.slot_ptr.size())) return e;
+    if (mv_status e = ensure_dev(pc.d_slot_idx, pc.cap_idx, std::max<size_t>(1, pc.slot_idx.size()))) return e;
+    size_t old_slots = pc.cap_slots;
+    if (mv_status e = ensure_dev(pc.d_part_ml, pc.cap_slots, (size_t)pc.n_slots * q_heads)) return e;
+    if (pc.cap_slots != old_slots || !pc.d_part_o) {
+      cudaFree(pc.d_part_o);
+      MV_CUDA_TRY(cudaMalloc(&pc.d_part_o, sizeof(float) * pc.cap_slots * kHeadDim));
+    }
+    MV_CUDA_TRY(cudaMemcpyAsync(pc.d_items, pc.items.data(), sizeof(WorkItem) * pc.items.size(),
+                                cudaMemcpyHostToDevice, stream));
+    MV_CUDA_TRY(cudaMemcpyAsync(pc.d_members, pc.members.data(), sizeof(int32_t) * pc.members.size(),
+                                cudaMemcpyHostToDevice, stream));
+    MV_CUDA_TRY(cudaMemcpyAsync(pc.d_slot_ptr, pc.slot_ptr.data(), sizeof(int32_t) * pc.slot_ptr.size(),
+                                cudaMemcpyHostToDevice, stream));
+    MV_CUDA_TRY(cudaMemcpyAsync(pc.d_slot_idx, pc.slot_idx.data(), sizeof(int32_t) * pc.slot_idx.size(),
+                                cudaMemcpyHostToDevice, stream));
+  }
+  if (!pc.smem_set) {
+    MV_CUDA_TRY(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem));
+    pc.smem_set = true;
+  }
+  DecodeParams P;
+  P.arena = st.d_arena;
+  P.kplane = st.k_planes()[layer];
+  P.vplane = st.v_planes()[layer];
+  P.q = (const __nv_bfloat16*)d_q;
+  P.pos = d_positions;
+  P.items = pc.d_items;
+  P.members = pc.d_members;
+  P.part_o = pc.d_part_o;
+  P.part_ml = pc.d_part_ml;
+  P.kv_heads = cfg.kv_heads;
+  P.q_heads = q_heads;
+  P.gqa = gqa;
+  P.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
+  P.rope_base = cfg.rope_base;
+  dim3 grid((unsigned)pc.items.size(), (unsigned)cfg.kv_heads);
+  decode_kernel<<<grid, kDecThreads, kDecSmem, stream>>>(P);
+  MV_LAUNCH_CHECK();
+  combine_kernel<<<dim3(n, q_heads), kHeadDim, 0, stream>>>(pc.d_part_o, pc.d_part_ml, pc.d_slot_ptr, pc.d_slot_idx,
+                                                            q_heads, (__nv_bfloat16*)d_out);
+  MV_LAUNCH_CHECK();
+  return MV_OK;
+}
+
+extern "C" mv_status mv_attn_decode_plan_info(mv_kv_store* s, mv_decode_plan_info* out) {
+  if (!s || !s->impl || !out) return fail(MV_ERR_INVALID_ARGUMENT, "null argument");
+  if (!s->impl->plan) {
+    std::memset(out, 0, sizeof *out);
+    return MV_OK;
+  }
+  *out = s->impl->plan->info;
+  return MV_OK;
+}

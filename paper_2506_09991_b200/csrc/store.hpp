@@ -1,0 +1,116 @@
+// store.hpp — host control plane of the paged KV store (K2).
+//
+// Split of responsibilities:
+//   device (source of truth for identity): page pool, per-page refcounts, free-page stack,
+//     page-table arena (PageRef entries + per-entry token prefix sums), token id per slot,
+//     payload records, bf16 K/V planes.  Fork / merge / extend / append / release are
+//     kernels that edit those arrays; page ids never travel to the host.
+//   host (shapes only): per handle the arena block, entry count, token prefix sums,
+//     the in-place-append budget of its tail page, and its fork lineage (for cascade
+//     decode planning).  Every host decision is deterministic and needs no device sync.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mv {
+
+struct HandleRec {
+  int64_t arena_off = 0;             // first entry in the device arena
+  int32_t cap = 0;                   // arena block capacity (entries)
+  std::vector<int32_t> cum{0};       // cum[k] = tokens before entry k; size n_entries + 1
+  int32_t tail_room = 0;             // slots of the tail page this handle may fill in place
+  // Fork lineage: (share-group id, entry boundary, token boundary). Entries [0, boundary)
+  // are identical in every handle holding the group (SURVEY.md §7 H3 cascade).
+  struct Lineage {
+    uint64_t group;
+    int32_t entries;
+    int64_t tokens;
+  };
+  std::vector<Lineage> lineage;
+  uint64_t version = 0;              // bumps whenever the table changes (decode plan cache)
+
+  int32_t n_entries() const { return (int32_t)cum.size() - 1; }
+  int64_t n_tokens() const { return cum.back(); }
+};
+
+struct DecodePlanCache;  // decode.cu
+
+class PagedStore {
+ public:
+  explicit PagedStore(const mv_kv_config& cfg);
+  ~PagedStore();
+  mv_status init();
+
+  const mv_kv_config& cfg() const { return cfg_; }
+  cudaStream_t stream() const { return stream_; }
+  void set_stream(cudaStream_t s) { stream_ = s; }
+
+  mv_status create(uint64_t* out);
+  mv_status extend(uint64_t h, const int32_t* tokens, int64_t n, const void* payloads, uint64_t* out);
+  mv_status fork(uint64_t h, int32_t n, uint64_t* out);
+  mv_status merge(uint64_t prefix, const uint64_t* branches, int32_t nb, uint64_t* out);
+  mv_status release(uint64_t h);
+  mv_status length(uint64_t h, int64_t* out);
+  mv_status stats(mv_kv_stats* out);
+  mv_status resolve(uint64_t h, int32_t* tokens, void* payloads, uint32_t* slots);
+
+  mv_status append(const uint64_t* hs, int32_t n, const int32_t* d_tokens, const int32_t* d_pos, int32_t layer,
+                   const void* d_k, const void* d_v);
+  mv_status write_last(const uint64_t* hs, int32_t n, const int32_t* d_pos, int32_t layer, const void* d_k,
+                       const void* d_v);
+  mv_status append_many(uint64_t h, int64_t n, const int32_t* d_tokens, const int32_t* d_pos, int32_t layer,
+                        const void* d_k, const void* d_v);
+  mv_status gather_kv(uint64_t h, int32_t layer, void* d_k, void* d_v);
+
+  HandleRec* find(uint64_t h);
+  // device arrays (read by the attention kernels)
+  PageRef* d_arena = nullptr;
+  int32_t* d_cum = nullptr;
+  __nv_bfloat16** k_planes() { return k_planes_.data(); }
+  __nv_bfloat16** v_planes() { return v_planes_.data(); }
+
+  // scratch helpers shared with decode.cu
+  void* pinned(size_t bytes);                 // host staging (grows; ordered by stream sync points)
+  void* device_scratch(size_t bytes, int slot);
+  mv_status check_device_error(const char* what);  // syncs the stream
+  DecodePlanCache* plan = nullptr;
+
+ private:
+  int64_t arena_alloc(int32_t need, int32_t* cap_out);
+  void arena_free(int64_t off, int32_t cap);
+  mv_status ensure_cap(HandleRec& r, int32_t need);
+  uint64_t register_handle(HandleRec rec);
+  mv_status upload(const void* host, size_t bytes, void** dev_out, int slot);
+
+  mv_kv_config cfg_;
+  cudaStream_t stream_ = nullptr;
+  int32_t* d_refcnt_ = nullptr;
+  int32_t* d_free_ = nullptr;      // free-page stack
+  int32_t* d_free_top_ = nullptr;  // stack size (device scalar)
+  int32_t* d_err_ = nullptr;       // sticky device error bits (1 = out of pages)
+  int32_t* d_slot_tok_ = nullptr;  // token id per slot
+  uint8_t* d_records_ = nullptr;   // record_bytes per slot
+  std::vector<__nv_bfloat16*> k_planes_, v_planes_;
+  std::unordered_map<uint64_t, HandleRec> handles_;
+  uint64_t next_handle_ = 1;
+  uint64_t next_group_ = 1;
+  std::map<int32_t, std::vector<int64_t>> free_blocks_;  // arena blocks by capacity
+  int64_t arena_top_ = 0;
+  int64_t logical_ = 0;
+  // staging
+  void* pinned_ = nullptr;
+  size_t pinned_bytes_ = 0;
+  std::vector<void*> dscratch_;
+  std::vector<size_t> dscratch_bytes_;
+};
+
+}  // namespace mv
+
+struct mv_kv_store {
+  mv::PagedStore* impl;
+};

@@ -1,0 +1,431 @@
+// visibility.cu — K1: tag stream -> Multiverse positions, segment ids and per-token exclusion
+// intervals (the compact form of the structured mask), plus the dense-mask and prefill
+// tile-map expansions.
+//
+// Reference behaviour replaced:
+//   grammar.cpp:156-294  Parser (error kinds and their precedence)
+//   dag.cpp:117-187      DagBuilder::visit_block (segments, visibility parents)
+//   dag.cpp:203-222      assign_positions: segment start = 1 + max(parent end), root 0
+//   dag.cpp:227-263      visibility_sets + build_mask
+//
+// Algorithm (one CTA per sequence; all phases stream through the sequence in tiles):
+//   1. parallel: compact the indices of tag tokens (ids 0..9) with a block scan; every
+//      token also records the rank of the last tag at or before it.
+//   2. one thread walks only the tags (a few per block, not per token) with the grammar
+//      automaton, validating structure exactly in the reference parser's order and
+//      computing, per tag, its position (sibling <Path>s restart at plan_end+1,
+//      <Conclusion> at max_path_end+1) and the exclusion-interval node that applies from
+//      that tag on: inside path q >= 2 of block B, rows [first <Path> of B, <Path>_q)
+//      are invisible (sibling paths never see each other). Interval nodes form a
+//      persistent stack (one node per <Path>_q, q >= 2), so nesting costs O(1) per tag.
+//   3. parallel: each token takes pos = pos(last tag) + distance, its segment id from a
+//      scan over segment-start flags, and copies its <= D intervals from the node chain.
+#include <cub/block/block_scan.cuh>
+
+#include "common.cuh"
+
+namespace mv {
+namespace {
+
+constexpr int kVisThreads = 512;
+constexpr int kVisItems = 8;                      // tokens per thread per tile
+constexpr int kVisTile = kVisThreads * kVisItems;  // 4096
+constexpr int kMaxFrames = 64;                    // open <Parallel> nesting handled by the walker
+
+struct SeqWs {
+  int32_t* tag_idx;   // [n] sequence-local index of the k-th tag
+  int32_t* tag_pos;   // [n] position of the k-th tag token
+  int32_t* tag_node;  // [n] interval node applying from the k-th tag on (-1 none)
+  int32_t* last_tag;  // [n] rank of the last tag at or before token i (-1 none)
+  int4* nodes;        // [n] interval nodes {lo, hi, parent, depth}
+};
+
+__device__ inline SeqWs seq_ws(void* ws, int64_t off, int64_t n) {
+  // Each sequence owns a contiguous workspace slice of 8*n int32.
+  int32_t* base = reinterpret_cast<int32_t*>(ws) + off * 8;
+  SeqWs w;
+  w.tag_idx = base;
+  w.tag_pos = base + n;
+  w.tag_node = base + 2 * n;
+  w.last_tag = base + 3 * n;
+  w.nodes = reinterpret_cast<int4*>(base + 4 * n);
+  return w;
+}
+
+enum Phase : int32_t {
+  kAfterParOpen = 0,  // expect <Goal>; text here is a stray gap (grammar.cpp:181)
+  kGoalPreamble,      // free text allowed (take_text, grammar.cpp:183)
+  kInOutline,         // outline body
+  kAfterOutline,      // gap: <Outline> or </Goal>
+  kAfterGoal,         // gap: <Path> expected
+  kInPath,            // path body: text, nested <Parallel>, </Path>
+  kAfterPath,         // gap: <Path> or <Conclusion>
+  kInConclusion,      // conclusion text
+  kAfterConclusion,   // gap: </Parallel>
+};
+
+struct Frame {
+  int32_t phase, outlines, paths;
+  int32_t plan_end, max_path_end;
+  int32_t first_path_idx;
+  int32_t enclosing_node;  // interval node of the context the block sits in
+};
+
+__global__ void __launch_bounds__(kVisThreads) visibility_kernel(const int32_t* __restrict__ tokens,
+                                                                  const int64_t* __restrict__ offsets, int max_depth,
+                                                                  int32_t* __restrict__ positions,
+                                                                  int32_t* __restrict__ seg_id,
+                                                                  int32_t* __restrict__ excl,
+                                                                  int32_t* __restrict__ status, void* ws) {
+  using Scan = cub::BlockScan<int, kVisThreads>;
+  __shared__ typename Scan::TempStorage scan_tmp;
+  __shared__ int s_carry;
+  __shared__ Frame frames[kMaxFrames];
+  __shared__ int s_ntags;
+
+  const int s = blockIdx.x;
+  const int64_t off = offsets[s];
+  const int n = (int)(offsets[s + 1] - off);
+  const int32_t* tok = tokens + off;
+  SeqWs w = seq_ws(ws, off, n);
+
+  // ---- phase 1: tag compaction + last-tag rank ----
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += kVisTile) {
+    int flag[kVisItems], rank[kVisItems];
+#pragma unroll
+    for (int k = 0; k < kVisItems; ++k) {
+      int i = base + threadIdx.x * kVisItems + k;
+      flag[k] = (i < n && tok[i] >= 0 && tok[i] < kTagCount) ? 1 : 0;
+    }
+    int total;
+    Scan(scan_tmp).ExclusiveSum(flag, rank, total);
+    int carry = s_carry;
+#pragma unroll
+    for (int k = 0; k < kVisItems; ++k) {
+      int i = base + threadIdx.x * kVisItems + k;
+      if (i < n) {
+        int r = carry + rank[k];
+        if (flag[k]) w.tag_idx[r] = i;
+        w.last_tag[i] = r + flag[k] - 1;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = carry + total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) s_ntags = s_carry;
+  __syncthreads();
+  const int T = s_ntags;
+
+  // ---- phase 2: tag walk (single thread; O(#tags)) ----
+  if (threadIdx.x == 0) {
+    int err = MV_OK;
+    int depth = 0;           // open frames
+    int cur_pos = -1;        // position of the last token processed
+    int prev_idx = -1;       // index of the previous tag
+    int cur_node = -1;       // interval node applying to the current context
+    int nnodes = 0;
+    for (int k = 0; k < T && err == MV_OK; ++k) {
+      const int idx = w.tag_idx[k];
+      const int t = tok[idx];
+      const bool text_before = idx - prev_idx > 1;  // a text run sits between the tags
+      int pos = cur_pos + (idx - prev_idx);
+      Frame* f = depth > 0 ? &frames[depth - 1] : nullptr;
+      if (!f) {
+        // trajectory top level: text or <Parallel> (grammar.cpp:163-172)
+        if (t != kParOpen) { err = MV_ERR_MALFORMED; break; }
+      } else {
+        const int ph = f->phase;
+        const bool gap = ph == kAfterParOpen || ph == kAfterOutline || ph == kAfterGoal || ph == kAfterPath ||
+                         ph == kAfterConclusion;
+        if (gap && text_before) { err = MV_ERR_MALFORMED; break; }  // take_gap (grammar.cpp:272-282)
+        switch (ph) {
+          case kAfterParOpen:
+            if (t != kGoalOpen) err = MV_ERR_MALFORMED;
+            else f->phase = kGoalPreamble;
+            break;
+          case kGoalPreamble:
+            if (t == kOutOpen) { f->phase = kInOutline; f->outlines++; }
+            else if (f->outlines == 0) err = MV_ERR_COUNT_MISMATCH;  // grammar.cpp:195-199
+            else err = MV_ERR_MALFORMED;
+            break;
+          case kInOutline:
+            if (t != kOutClose) err = MV_ERR_MALFORMED;
+            else f->phase = kAfterOutline;
+            break;
+          case kAfterOutline:
+            if (t == kOutOpen) { f->phase = kInOutline; f->outlines++; }
+            else if (t == kGoalClose) { f->phase = kAfterGoal; f->plan_end = pos; }
+            else err = MV_ERR_MALFORMED;
+            break;
+          case kAfterGoal:
+          case kAfterPath:
+            if (t == kPathOpen) {
+              f->paths++;
+              pos = f->plan_end + 1;  // siblings share a start (dag.cpp:203-212)
+              if (f->paths == 1) {
+                f->first_path_idx = idx;
+                cur_node = f->enclosing_node;
+              } else {
+                int parent = f->enclosing_node;
+                int d = parent >= 0 ? w.nodes[parent].w + 1 : 1;
+                if (d > max_depth) { err = MV_ERR_DEPTH; break; }
+                w.nodes[nnodes] = make_int4(f->first_path_idx, idx, parent, d);
+                cur_node = nnodes++;
+              }
+              f->phase = kInPath;
+            } else if (f->paths != f->outlines) {
+              err = MV_ERR_COUNT_MISMATCH;  // grammar.cpp:228-232
+            } else if (t == kConcOpen) {
+              pos = f->max_path_end + 1;  // Reduce = max path end + 1
+              cur_node = f->enclosing_node;
+              f->phase = kInConclusion;
+            } else {
+              err = MV_ERR_MALFORMED;
+            }
+            break;
+          case kInPath:
+            if (t == kParOpen) {
+              // nested block: handled below (push)
+            } else if (t == kPathClose) {
+              f->phase = kAfterPath;
+              f->max_path_end = max(f->max_path_end, pos);
+            } else {
+              err = MV_ERR_MALFORMED;
+            }
+            break;
+          case kInConclusion:
+            if (t != kConcClose) err = MV_ERR_MALFORMED;
+            else f->phase = kAfterConclusion;
+            break;
+          case kAfterConclusion:
+            if (t != kParClose) err = MV_ERR_MALFORMED;
+            else depth--;  // block closed (grammar.cpp:238); cur_node is the enclosing context
+            break;
+        }
+        if (err) break;
+      }
+      if (t == kParOpen) {
+        if (depth == kMaxFrames) { err = MV_ERR_DEPTH; break; }
+        Frame nf;
+        nf.phase = kAfterParOpen;
+        nf.outlines = nf.paths = 0;
+        nf.plan_end = nf.max_path_end = -1;
+        nf.first_path_idx = -1;
+        nf.enclosing_node = cur_node;
+        frames[depth++] = nf;
+      }
+      w.tag_pos[k] = pos;
+      w.tag_node[k] = cur_node;
+      cur_pos = pos;
+      prev_idx = idx;
+    }
+    if (err == MV_OK && depth > 0) {
+      // end of input inside a block (grammar.cpp:250-256 `expect` at end), except the
+      // count checks the parser reaches first.
+      Frame* f = &frames[depth - 1];
+      const bool text_after = n - 1 - prev_idx > 0;
+      const bool gap = f->phase == kAfterParOpen || f->phase == kAfterOutline || f->phase == kAfterGoal ||
+                       f->phase == kAfterPath || f->phase == kAfterConclusion;
+      if (gap && text_after) err = MV_ERR_MALFORMED;
+      else if (f->phase == kGoalPreamble && f->outlines == 0) err = MV_ERR_COUNT_MISMATCH;
+      else if ((f->phase == kAfterGoal || f->phase == kAfterPath) && f->paths != f->outlines)
+        err = MV_ERR_COUNT_MISMATCH;
+      else err = MV_ERR_MALFORMED;
+    }
+    status[s] = err;
+  }
+  __syncthreads();
+
+  // ---- phase 3: per-token fill ----
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += kVisTile) {
+    int flag[kVisItems], sid[kVisItems];
+#pragma unroll
+    for (int k = 0; k < kVisItems; ++k) {
+      int i = base + threadIdx.x * kVisItems + k;
+      int f = 0;
+      if (i < n) {
+        int t = tok[i];
+        // segment starts (dag.cpp:90-98, :150-151, :155, :180): <Parallel> (Plan), <Path>,
+        // <Conclusion> (Reduce), the first token, and any token right after </Parallel>.
+        f = (t == kParOpen || t == kPathOpen || t == kConcOpen || i == 0 || tok[i - 1] == kParClose) ? 1 : 0;
+      }
+      flag[k] = f;
+    }
+    int total;
+    Scan(scan_tmp).InclusiveSum(flag, sid, total);
+    int carry = s_carry;
+#pragma unroll
+    for (int k = 0; k < kVisItems; ++k) {
+      int i = base + threadIdx.x * kVisItems + k;
+      if (i >= n) continue;
+      int lt = w.last_tag[i];
+      int p, node;
+      if (lt < 0) {
+        p = i;
+        node = -1;
+      } else {
+        p = w.tag_pos[lt] + (i - w.tag_idx[lt]);
+        node = w.tag_node[lt];
+      }
+      positions[off + i] = p;
+      if (seg_id) seg_id[off + i] = carry + sid[k] - 1;
+      int32_t* e = excl + (off + i) * (int64_t)max_depth * 2;
+      int d = node >= 0 ? w.nodes[node].w : 0;
+      for (int q = d; q < max_depth; ++q) { e[2 * q] = 0; e[2 * q + 1] = 0; }
+      while (node >= 0) {
+        int4 nd = w.nodes[node];
+        e[2 * (nd.w - 1)] = nd.x;
+        e[2 * (nd.w - 1) + 1] = nd.y;
+        node = nd.z;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_carry = carry + total;
+    __syncthreads();
+  }
+}
+
+// Dense mask bits from intervals (dag::Mask layout, MSB-first packed).
+__global__ void mask_packed_kernel(const int32_t* __restrict__ excl, int n, int D, int row0, int row1,
+                                   uint8_t* __restrict__ out) {
+  const int64_t nbytes = ((int64_t)(row1 - row0) * n + 7) / 8;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbytes; b += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t byte = 0;
+    for (int k = 0; k < 8; ++k) {
+      int64_t bit = b * 8 + k;
+      int i = row0 + (int)(bit / n);
+      int j = (int)(bit % n);
+      if (i >= row1) break;
+      bool vis = j <= i;
+      const int32_t* e = excl + (int64_t)i * D * 2;
+      for (int q = 0; q < D && vis; ++q)
+        if (j >= e[2 * q] && j < e[2 * q + 1]) vis = false;
+      if (vis) byte |= 0x80u >> k;
+    }
+    out[b] = (uint8_t)byte;
+  }
+}
+
+// Prefill tile classification: one CTA per q-tile, one thread per query row.
+__global__ void tile_map_kernel(const int32_t* __restrict__ excl, int n, int D, int tile, int32_t* __restrict__ count,
+                                int32_t* __restrict__ list, unsigned long long* __restrict__ visible_pairs) {
+  const int qt = blockIdx.x;
+  const int n_qt = (n + tile - 1) / tile;
+  const int i = qt * tile + threadIdx.x;
+  const bool row_ok = threadIdx.x < tile && i < n;
+  int lo[8], hi[8];
+  int nd = 0;
+  if (row_ok) {
+    for (int q = 0; q < D && q < 8; ++q) {
+      int a = excl[((int64_t)i * D + q) * 2], b = excl[((int64_t)i * D + q) * 2 + 1];
+      if (a < b) { lo[nd] = a; hi[nd] = b; ++nd; }
+    }
+  }
+  unsigned long long vis_total = 0;
+  int written = 0;
+  for (int kt = 0; kt <= qt; ++kt) {
+    int j0 = kt * tile, j1 = min(n, j0 + tile);
+    bool empty = true, full = true;
+    if (row_ok) {
+      int last = min(j1 - 1, i);  // causal clamp
+      if (j0 > i) {
+        empty = true;
+        full = false;
+      } else {
+        int vis = last - j0 + 1;
+        bool touches = false;
+        for (int q = 0; q < nd; ++q) {
+          int a = max(lo[q], j0), b = min(hi[q], last + 1);
+          if (a < b) {
+            vis -= b - a;
+            touches = true;
+          }
+        }
+        empty = vis == 0;
+        full = !touches && (j1 - 1 <= i);
+        vis_total += (unsigned long long)vis;
+      }
+    } else {
+      full = true;  // padding rows do not force a partial tile
+    }
+    int all_empty = __syncthreads_and(empty ? 1 : 0);
+    int all_full = __syncthreads_and(full ? 1 : 0);
+    if (!all_empty && threadIdx.x == 0) {
+      list[(int64_t)qt * n_qt + written] = kt | (all_full ? 0 : (1 << 30));
+    }
+    if (!all_empty) ++written;
+  }
+  if (threadIdx.x == 0) count[qt] = written;
+  // block reduction of the visible-pair count
+  __shared__ unsigned long long red[32];
+  unsigned long long v = vis_total;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < (int)(blockDim.x + 31) / 32; ++k) t += red[k];
+    atomicAdd(visible_pairs, t);
+  }
+}
+
+}  // namespace
+}  // namespace mv
+
+using namespace mv;
+
+extern "C" size_t mv_visibility_workspace_size(const int64_t* h_offsets, int32_t n_seq) {
+  if (!h_offsets || n_seq <= 0) return 0;
+  return (size_t)h_offsets[n_seq] * 8 * sizeof(int32_t) + 256;
+}
+
+extern "C" mv_status mv_visibility(const int32_t* d_tokens, const int64_t* h_offsets, int32_t n_seq, int32_t max_depth,
+                                   int32_t* d_positions, int32_t* d_seg_id, int32_t* d_excl, int32_t* d_status,
+                                   void* d_workspace, size_t workspace_bytes, mv_stream_t stream) {
+  if (n_seq <= 0 || !h_offsets || max_depth < 1 || !d_positions || !d_excl || !d_status)
+    return fail(MV_ERR_INVALID_ARGUMENT, "mv_visibility: bad arguments");
+  if (workspace_bytes < mv_visibility_workspace_size(h_offsets, n_seq) || !d_workspace)
+    return fail(MV_ERR_INVALID_ARGUMENT, "mv_visibility: workspace too small");
+  for (int s = 0; s < n_seq; ++s)
+    if (h_offsets[s + 1] < h_offsets[s] || h_offsets[s + 1] - h_offsets[s] > (int64_t)INT32_MAX / 2)
+      return fail(MV_ERR_INVALID_ARGUMENT, "mv_visibility: bad offsets");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int64_t* d_off = nullptr;
+  // Offsets travel inside the workspace tail? Keep it simple: a small async upload.
+  MV_CUDA_TRY(cudaMallocAsync(&d_off, sizeof(int64_t) * (n_seq + 1), st));
+  MV_CUDA_TRY(cudaMemcpyAsync(d_off, h_offsets, sizeof(int64_t) * (n_seq + 1), cudaMemcpyHostToDevice, st));
+  visibility_kernel<<<n_seq, kVisThreads, 0, st>>>(d_tokens, d_off, max_depth, d_positions, d_seg_id, d_excl, d_status,
+                                                   d_workspace);
+  MV_LAUNCH_CHECK();
+  MV_CUDA_TRY(cudaFreeAsync(d_off, st));
+  return MV_OK;
+}
+
+extern "C" mv_status mv_mask_packed(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t row0, int32_t row1,
+                                    uint8_t* d_out, mv_stream_t stream) {
+  if (n < 0 || row0 < 0 || row1 > n || row0 > row1 || max_depth < 1)
+    return fail(MV_ERR_INVALID_ARGUMENT, "mv_mask_packed: bad arguments");
+  int64_t nbytes = ((int64_t)(row1 - row0) * n + 7) / 8;
+  if (nbytes == 0) return MV_OK;
+  int blocks = (int)std::min<int64_t>((nbytes + 255) / 256, 148 * 16);
+  mask_packed_kernel<<<blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_excl, n, max_depth, row0, row1,
+                                                                                  d_out);
+  MV_LAUNCH_CHECK();
+  return MV_OK;
+}
+
+extern "C" mv_status mv_tile_map(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t tile, int32_t* d_count,
+                                 int32_t* d_list, unsigned long long* d_visible_pairs, mv_stream_t stream) {
+  if (n <= 0 || tile <= 0 || tile > 1024 || (tile & 31) || max_depth < 1 || max_depth > 8)
+    return fail(MV_ERR_INVALID_ARGUMENT, "mv_tile_map: bad arguments");
+  int n_qt = (n + tile - 1) / tile;
+  tile_map_kernel<<<n_qt, tile, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_excl, n, max_depth, tile, d_count,
+                                                                              d_list, d_visible_pairs);
+  MV_LAUNCH_CHECK();
+  return MV_OK;
+}

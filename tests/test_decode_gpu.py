@@ -1,0 +1,150 @@
+"""K4 parity: branch-parallel paged decode attention vs the fp64 oracle restatement of
+toy_model.cpp:121-157 (GQA h -> h/(Hq/Hkv)), on bf16-rounded seeded inputs.
+Tolerance (north star): max-abs 2e-3 with fp32 accumulation."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from mvtest import bf16_to_f64, sym_bf16
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module")
+def mv():
+    import paper_2506_09991_b200 as m
+    return m
+
+
+class Req:
+    """One request: shared prefix, fork into branches, per-branch private tokens, one decode step."""
+
+    def __init__(self, mv, st, rows, seed, prefix, branches, branch_len, hkv, nested=None):
+        self.st, self.rows = st, rows
+        dev = "cuda"
+
+        def add(h, n, pos0):
+            k = sym_bf16(seed * 1000 + len(rows["k"]) * 7 + 1, (n, hkv, 128))
+            v = sym_bf16(seed * 1000 + len(rows["k"]) * 7 + 2, (n, hkv, 128))
+            pos = torch.arange(pos0, pos0 + n, dtype=torch.int32)
+            st.append_many(h, torch.full((n,), 11, dtype=torch.int32, device=dev), pos.to(dev), 0, k.to(dev),
+                           v.to(dev))
+            base = sum(x.shape[0] for x in rows["k"])
+            rows["k"].append(k)
+            rows["v"].append(v)
+            rows["pos"].append(pos)
+            return list(range(base, base + n))
+
+        root = st.create()
+        ctx_root = add(root, prefix, 0) if prefix else []
+        self.handles, self.ctx, self.qpos = [], [], []
+        kids = st.fork(root, branches)
+        for i, h in enumerate(kids):
+            if nested and i == 0:
+                # nested Process stage inside branch 0: extend, fork again
+                c = ctx_root + add(h, nested[0], prefix)
+                sub = st.fork(h, nested[1])
+                for s in sub:
+                    cc = c + add(s, branch_len - 1, prefix + nested[0])
+                    self.handles.append(s)
+                    self.ctx.append(cc)
+                    self.qpos.append(prefix + nested[0] + branch_len - 1)
+                continue
+            c = ctx_root + (add(h, branch_len - 1, prefix) if branch_len > 1 else [])
+            self.handles.append(h)
+            self.ctx.append(c)
+            self.qpos.append(prefix + branch_len - 1)
+        self.root, self.ctx_root = root, ctx_root
+
+
+def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1):
+    st = mv.kv.PagedStore(num_pages=num_pages, layers=1, kv_heads=hkv)
+    rows = {"k": [], "v": [], "pos": []}
+    reqs = [Req(mv, st, rows, seed + i, *spec, hkv=hkv) if len(spec) == 3 else
+            Req(mv, st, rows, seed + i, *spec[:3], hkv=hkv, nested=spec[3]) for i, spec in enumerate(reqs_spec)]
+    handles = [h for r in reqs for h in r.handles]
+    ctx = [c for r in reqs for c in r.ctx]
+    qpos = [p for r in reqs for p in r.qpos]
+    n = len(handles)
+    # the decode step: append each branch's new token (K/V), then attend
+    knew = sym_bf16(seed * 77 + 5, (n, hkv, 128))
+    vnew = sym_bf16(seed * 77 + 6, (n, hkv, 128))
+    q = sym_bf16(seed * 77 + 7, (n, hq, 128))
+    pos = torch.tensor(qpos, dtype=torch.int32)
+    st.append(handles, torch.full((n,), 12, dtype=torch.int32, device="cuda"), pos.cuda(), 0, knew.cuda(),
+              vnew.cuda())
+    out = mv.attention.decode(st, handles, q.cuda(), pos.cuda())
+    torch.cuda.synchronize()
+    # oracle: rotate K at cache time and q at its position (fp64), attend prefix..suffix..self
+    base = sum(x.shape[0] for x in rows["k"])
+    K = np.concatenate([bf16_to_f64(x) for x in rows["k"]] + [bf16_to_f64(knew)])
+    V = np.concatenate([bf16_to_f64(x) for x in rows["v"]] + [bf16_to_f64(vnew)])
+    P = np.concatenate([x.numpy() for x in rows["pos"]] + [pos.numpy()])
+    Kr = oracle.rope(K, P)
+    qr = oracle.rope(bf16_to_f64(q), pos.numpy())
+    ctx_full = [c + [base + i] for i, c in enumerate(ctx)]
+    ref = oracle.attn_decode(qr, Kr, V, ctx_full)
+    err = np.abs(out.float().cpu().numpy() - ref).max()
+    return err, st
+
+
+def test_small_gqa(mv):
+    err, st = run_case(mv, [(300, 3, 37)], hq=8, hkv=2, num_pages=256)
+    assert err < TOL, err
+    info = st.plan_info()
+    assert info["unique_kv_tokens"] < info["naive_kv_tokens"]  # the prefix is read once
+
+
+def test_ragged_unaligned_prefix(mv):
+    # prefix length not a multiple of 16: the shared tail page is partial
+    err, _ = run_case(mv, [(77, 4, 19), (5, 2, 3), (0, 2, 1)], hq=40, hkv=8, num_pages=256)
+    assert err < TOL, err
+
+
+def test_nested_fork_lineage(mv):
+    # branch 0 forks again: a 2-level cascade (prefix shared by all, mid segment by 3)
+    err, st = run_case(mv, [(200, 3, 30, (40, 3))], hq=40, hkv=8, num_pages=512)
+    assert err < TOL, err
+
+
+def test_many_members_row_split(mv):
+    # 20 branches x 5 heads = 100 rows per KV head: split across CTAs (L2 re-reads)
+    err, _ = run_case(mv, [(130, 20, 9)], hq=40, hkv=8, num_pages=512)
+    assert err < TOL, err
+
+
+def test_c2_shape(mv):
+    # BASELINE configs[1]: 40 q / 8 kv heads, 4K shared prefix, 8 branches x 1K, page 16
+    err, st = run_case(mv, [(4096, 8, 1024)], hq=40, hkv=8, num_pages=1024)
+    assert err < TOL, err
+    info = st.plan_info()
+    assert info["unique_kv_tokens"] == 4096 + 8 * 1024
+    assert info["naive_kv_tokens"] == 8 * (4096 + 1024)
+
+
+def test_decode_after_merge(mv):
+    """Reduce stage: zero-copy merge of the branches, then keep decoding over the merged KV
+    (engine.cpp:767-802 then emit over the merged handle)."""
+    hq, hkv = 40, 8
+    st = mv.kv.PagedStore(num_pages=256, layers=1, kv_heads=hkv)
+    rows = {"k": [], "v": [], "pos": []}
+    r = Req(mv, st, rows, 9, 100, 3, 20, hkv=hkv)
+    m = st.merge(r.root, r.handles)
+    ctx = list(r.ctx_root)
+    for c in r.ctx:
+        ctx += c[len(r.ctx_root):]
+    assert st.length(m) == len(ctx)
+    for h in r.handles + [r.root]:
+        st.release(h)  # zombies released after the merge; pages stay alive through m
+    knew, vnew, q = sym_bf16(555, (1, hkv, 128)), sym_bf16(556, (1, hkv, 128)), sym_bf16(557, (1, hq, 128))
+    pos = torch.tensor([100 + 19], dtype=torch.int32)  # max path end + 1
+    st.append([m], torch.tensor([13], dtype=torch.int32, device="cuda"), pos.cuda(), 0, knew.cuda(), vnew.cuda())
+    out = mv.attention.decode(st, [m], q.cuda(), pos.cuda())
+    base = sum(x.shape[0] for x in rows["k"])
+    K = np.concatenate([bf16_to_f64(x) for x in rows["k"]] + [bf16_to_f64(knew)])
+    V = np.concatenate([bf16_to_f64(x) for x in rows["v"]] + [bf16_to_f64(vnew)])
+    P = np.concatenate([x.numpy() for x in rows["pos"]] + [pos.numpy()])
+    ref = oracle.attn_decode(oracle.rope(bf16_to_f64(q), pos.numpy()), oracle.rope(K, P), V, [ctx + [base]])
+    assert np.abs(out.float().cpu().numpy() - ref).max() < TOL
