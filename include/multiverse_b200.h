@@ -195,12 +195,14 @@ MV_API mv_status mv_kv_gather_kv(mv_kv_store* s, uint64_t h, int32_t layer, void
  *   h_handles[n]   the decoding sequences (their current cache includes the new token)
  *   d_q            bf16[n][q_heads][head_dim] pre-RoPE queries; rotated in-kernel at
  *                  d_positions[i] (interleaved RoPE)
- *   d_out          bf16[n][q_heads][head_dim]
+ *   d_out          [n][q_heads][head_dim], bf16 (out_dtype 0) or fp32 (out_dtype 1); the fp32
+ *                  form exposes the kernel's fp32 result before the bf16 store rounding
+ *                  (2^-9 |o|), which is what the 2e-3 parity contract is checked on
  * The plan (cascade units, split-KV chunks, partial buffers) is built and cached inside the
  * store; it is rebuilt automatically when the handles' page tables change.
  */
 MV_API mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_t* h_handles, int32_t n, int32_t q_heads,
-                         const void* d_q, const int32_t* d_positions, void* d_out);
+                         const void* d_q, const int32_t* d_positions, void* d_out, int32_t out_dtype);
 
 /* Decode-plan statistics of the last mv_attn_decode call on this store (host ints). */
 typedef struct {

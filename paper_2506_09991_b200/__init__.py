@@ -78,7 +78,7 @@ def _load():
         "mv_kv_write_last": ([P, P, i32, P, i32, P, P], ctypes.c_int),
         "mv_kv_append_many": ([P, u64, i64, P, P, i32, P, P], ctypes.c_int),
         "mv_kv_gather_kv": ([P, u64, i32, P, P], ctypes.c_int),
-        "mv_attn_decode": ([P, i32, P, i32, i32, P, P, P], ctypes.c_int),
+        "mv_attn_decode": ([P, i32, P, i32, i32, P, P, P, i32], ctypes.c_int),
         "mv_attn_decode_plan_info": ([P, P], ctypes.c_int),
         "mv_prefill_workspace_size": ([i32, i32, i32], sz),
         "mv_attn_prefill": ([P, P, P, P, P, i32, i32, i32, i32, ctypes.c_double, P, P, sz, P], ctypes.c_int),

@@ -10,12 +10,15 @@ from .kv import PagedStore, _p, _u64_array
 
 
 def decode(store: PagedStore, handles, q: torch.Tensor, positions: torch.Tensor, layer: int = 0,
-           out: torch.Tensor | None = None) -> torch.Tensor:
-    """q: bf16 [n, Hq, 128] pre-RoPE queries of the tokens just appended to `handles`."""
+           out: torch.Tensor | None = None, out_dtype: torch.dtype = torch.bfloat16) -> torch.Tensor:
+    """q: bf16 [n, Hq, 128] pre-RoPE queries of the tokens just appended to `handles`.
+    out_dtype float32 returns the kernel's fp32 result (no bf16 store rounding)."""
     assert q.dtype == torch.bfloat16 and q.is_cuda and q.is_contiguous()
     n, hq, d = q.shape
-    out = torch.empty_like(q) if out is None else out
-    check(lib.mv_attn_decode(store.handle, layer, _u64_array(handles), n, hq, _p(q), _p(positions), _p(out)))
+    if out is None:
+        out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
+    code = {torch.bfloat16: 0, torch.float32: 1}[out.dtype]
+    check(lib.mv_attn_decode(store.handle, layer, _u64_array(handles), n, hq, _p(q), _p(positions), _p(out), code))
     return out
 
 

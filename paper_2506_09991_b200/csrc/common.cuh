@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
 #include <string>
 
 #include "multiverse_b200.h"
@@ -146,13 +147,22 @@ __device__ __forceinline__ float fast_exp2(float x) {
   return y;
 }
 
-// Interleaved rotary angle for pair t of a 128-dim head (toy_model.cpp:30-41), computed in
-// fp64 (positions reach 1e5 rad) and reduced before the fp32 sincos.
-__device__ __forceinline__ void rope_cs(int pos, int t, double base, float& c, float& s) {
-  double inv = exp2(-2.0 * (double)t / (double)kHeadDim * log2(base));
+// Interleaved rotary map (toy_model.cpp:30-41): pair t of a 128-dim head rotates by
+// theta = pos * base^(-2t/dh). The inverse frequencies are computed on the host with the same
+// std::pow expression as the reference, theta is formed and range-reduced in fp64 (positions
+// reach 1e5 rad), and only the final sincos runs in fp32.
+struct RopeTable {
+  double inv[kHeadDim / 2];
+};
+inline RopeTable make_rope_table(double base) {
+  RopeTable t;
+  for (int i = 0; i < kHeadDim / 2; ++i) t.inv[i] = std::pow(base, -2.0 * (double)i / (double)kHeadDim);
+  return t;
+}
+__device__ __forceinline__ void rope_cs(int pos, double inv, float& c, float& s) {
   double th = (double)pos * inv;
-  th = th - 6.283185307179586476925286766559 * floor(th * 0.15915494309189533576888376337251);
-  sincosf((float)th, &s, &c);
+  th = fma(-6.283185307179586476925286766559, rint(th * 0.15915494309189533576888376337251), th);  // [-pi, pi]
+  __sincosf((float)th, &s, &c);  // SFU; |err| < 2^-21 on [-pi, pi]
 }
 
 }  // namespace mv

@@ -36,14 +36,25 @@ namespace {
 
 constexpr int kPairs = 3;  // 7 warps: <= 2 per SM sub-partition -> 255 regs/thread
 constexpr int kConsumerWarps = 2 * kPairs;
-constexpr int kDecThreads = (kConsumerWarps + 1) * 32;
+constexpr int kConsumerThreads = kConsumerWarps * 32;
+constexpr int kDecThreads = kConsumerThreads + 32;
 constexpr int kStages = 15;  // multiple of kPairs: stage s always belongs to pair s % kPairs
-constexpr int kStageBytes = 2 * kPageTokens * kHeadDim * 2;  // K + V page-head blocks
-constexpr int kMaxNT = 5;                                   // <= 40 query rows per CTA
-constexpr int kChunkPages = 64;
-constexpr int kSmemRing = kStages * kStageBytes;            // 128 KiB
-constexpr int kSmemQ = kMaxNT * 8 * kHeadDim * 2;           // 10 KiB
-constexpr int kDecSmem = kSmemRing + kSmemQ + 2 * kStages * 8 + 64;
+constexpr int kStageBytes = 2 * kPageTokens * kHeadDim * 2;  // K + V page-head blocks (8 KiB)
+constexpr int kMaxNT = 5;                                   // <= 40 query rows per item
+constexpr int kMaxRows = kMaxNT * 8;
+constexpr int kChunkPages = 64;                             // split-KV chunk (pages)
+constexpr int kSmemRing = kStages * kStageBytes;            // 120 KiB
+constexpr int kSmemQ = kMaxRows * kHeadDim * 2;             // 10 KiB per buffer
+constexpr int kSmemEnt = kChunkPages * 8;                   // 512 B per buffer
+constexpr int kSmemO = kPairs * kMaxRows * kHeadDim * 4;    // 60 KiB epilogue
+constexpr int kSmemML = kPairs * kMaxRows * 2 * 4;
+constexpr int kOffQ = kSmemRing;
+constexpr int kOffEnt = kOffQ + 2 * kSmemQ;
+constexpr int kOffO = kOffEnt + 2 * kSmemEnt;
+constexpr int kOffML = kOffO + kSmemO;
+constexpr int kOffItem = kOffML + kSmemML;
+constexpr int kOffBar = kOffItem + 2 * 64;
+constexpr int kDecSmem = kOffBar + (2 * kStages + 4) * 8;
 
 struct WorkItem {
   int64_t entry_off;   // absolute arena index of the chunk's first entry
@@ -53,6 +64,12 @@ struct WorkItem {
   int32_t slot_base;   // partial slot of the first member
   int32_t nt;          // n8 row tiles needed
   int32_t pad;
+};
+
+struct ItemSlot {      // what the producer hands the consumers for one (item, kv head)
+  WorkItem it;
+  int32_t kvh;
+  int32_t valid;
 };
 
 struct DecodeParams {
@@ -65,18 +82,22 @@ struct DecodeParams {
   const int32_t* members;
   float* part_o;              // [slots][q_heads][128]
   float2* part_ml;            // [slots][q_heads]
+  int* work_counter;          // dynamic (item, kv head) scheduler
+  int n_work;                 // items * kv_heads
   int kv_heads, q_heads, gqa;
   float scale_log2;           // log2(e) / sqrt(128)
-  double rope_base;
+  RopeTable rope;
 };
 
+// Consumer side of one work item: 3 pairs stream the item's pages through the ring.
 template <int NT>
-__device__ __forceinline__ void consume(const DecodeParams& P, const WorkItem& it, int kvh, uint8_t* ring,
-                                        const uint8_t* sq, uint64_t* full, uint64_t* empty, float* s_ml,
-                                        float* s_o) {
+__device__ __forceinline__ void consume_item(const DecodeParams& P, const ItemSlot& is, int gbase, uint8_t* ring,
+                                             const uint8_t* sq, const PageRef* s_ent, uint64_t* full,
+                                             uint64_t* empty, uint64_t* item_empty, float* s_ml, float* s_o) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, hh = warp & 1;
   const int g = lane >> 2, t4 = lane & 3;
+  const WorkItem& it = is.it;
 
   // Q fragments (B operand, k16 x n8 "col"): rows nt*8.., dims ks*16..
   uint32_t qb[NT][8][2];
@@ -106,10 +127,11 @@ __device__ __forceinline__ void consume(const DecodeParams& P, const WorkItem& i
 
   const int npages = it.n_entries;
   for (int j = pair; j < npages; j += kPairs) {
-    const int stage = j % kStages;
-    const PageRef ref = P.arena[it.entry_off + j];
+    const int gp = gbase + j;
+    const int stage = gp % kStages;
+    const PageRef ref = s_ent[j];
     const int vb = ref_begin(ref), ve = vb + ref_count(ref);
-    mbar_wait(&full[stage], (j / kStages) & 1);
+    mbar_wait(&full[stage], (gp / kStages) & 1);
     const uint32_t kbase = smem_u32(ring + stage * kStageBytes);
     const uint32_t vbase = kbase + kPageTokens * kHeadDim * 2;
 
@@ -177,8 +199,11 @@ __device__ __forceinline__ void consume(const DecodeParams& P, const WorkItem& i
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[stage]);
   }
+  // Q buffer and entry list of this item are no longer read: hand them back to the producer.
+  __syncwarp();
+  if (lane == 0) mbar_arrive(item_empty);
 
-  // finish l (sum over the 8 token-lanes g), publish this pair's (m, l, O^T half) to smem
+  // finish l (sum over the 8 token lanes g), publish this pair's (m, l, O^T half) to smem
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -188,9 +213,8 @@ __device__ __forceinline__ void consume(const DecodeParams& P, const WorkItem& i
       for (int off = 4; off < 32; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
       l_run[nt][c] = l;
     }
-  // consumers finished reading the ring (named barrier over the 8 consumer warps)
-  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerWarps * 32));
   const int rows = NT * 8;
+  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads));  // previous item's merge readers are done
   if (hh == 0 && g == 0) {
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -211,40 +235,49 @@ __device__ __forceinline__ void consume(const DecodeParams& P, const WorkItem& i
         int r = nt * 8 + 2 * t4 + (k & 1);
         s_o[(pair * rows + r) * kHeadDim + dim] = o[mt][nt][k];
       }
-  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerWarps * 32));
+  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads));
 
-  // merge the pairs and write one partial per (member, q head)
+  // merge the pairs and write one partial per (member, q head); float4 per thread
   const int nrows = it.n_mem * P.gqa;
-  for (int x = threadIdx.x; x < nrows * kHeadDim; x += kConsumerWarps * 32) {
-    const int r = x / kHeadDim, dim = x % kHeadDim;
+  for (int x = threadIdx.x; x < nrows * (kHeadDim / 4); x += kConsumerThreads) {
+    const int r = x / (kHeadDim / 4), d4 = (x % (kHeadDim / 4)) * 4;
     float m = -INFINITY;
 #pragma unroll
     for (int p = 0; p < kPairs; ++p) m = fmaxf(m, s_ml[(p * rows + r) * 2]);
     const float mu = m == -INFINITY ? 0.f : m;
-    float acc = 0.f, l = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float l = 0.f;
 #pragma unroll
     for (int p = 0; p < kPairs; ++p) {
       const float w = fast_exp2(s_ml[(p * rows + r) * 2] - mu);
-      acc += w * s_o[(p * rows + r) * kHeadDim + dim];
+      const float4 v = *reinterpret_cast<const float4*>(&s_o[(p * rows + r) * kHeadDim + d4]);
+      acc.x += w * v.x;
+      acc.y += w * v.y;
+      acc.z += w * v.z;
+      acc.w += w * v.w;
       l += w * s_ml[(p * rows + r) * 2 + 1];
     }
     const int mi = r / P.gqa, hl = r % P.gqa;
     const int64_t slot = it.slot_base + mi;
-    const int head = kvh * P.gqa + hl;
-    P.part_o[(slot * P.q_heads + head) * kHeadDim + dim] = acc;
-    if (dim == 0) P.part_ml[slot * P.q_heads + head] = make_float2(m, l);
+    const int head = is.kvh * P.gqa + hl;
+    *reinterpret_cast<float4*>(&P.part_o[(slot * P.q_heads + head) * kHeadDim + d4]) = acc;
+    if (d4 == 0) P.part_ml[slot * P.q_heads + head] = make_float2(m, l);
   }
 }
 
+// Persistent kernel: one CTA per SM pulls (chunk, kv head) work items from a global counter.
+// The producer warp stages item i+1 (entries, rotated Q) and keeps the page ring full while
+// the consumers finish item i, so per-item prologue/epilogue latency stays off the HBM path.
 __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint8_t* ring = smem;
-  uint8_t* sq = smem + kSmemRing;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemRing + kSmemQ);
+  ItemSlot* s_item = reinterpret_cast<ItemSlot*>(smem + kOffItem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* empty = full + kStages;
-
-  const WorkItem it = P.items[blockIdx.x];
-  const int kvh = blockIdx.y;
+  uint64_t* item_full = empty + kStages;
+  uint64_t* item_empty = item_full + 2;
+  float* s_o = reinterpret_cast<float*>(smem + kOffO);
+  float* s_ml = reinterpret_cast<float*>(smem + kOffML);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -252,80 +285,137 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 2);
     }
-    fence_mbar_init();
-  }
-
-  // Q tile: rows r = member * gqa + local head, RoPE at the member's position, chunk-swizzled.
-  const int rows = it.nt * 8;
-  const int nrows = it.n_mem * P.gqa;
-  for (int x = threadIdx.x; x < rows * 16; x += kDecThreads) {
-    const int r = x >> 4, c = x & 15;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (r < nrows) {
-      const int b = P.members[it.mem_off + r / P.gqa];
-      const int head = kvh * P.gqa + r % P.gqa;
-      v = *reinterpret_cast<const uint4*>(P.q + ((size_t)b * P.q_heads + head) * kHeadDim + c * 8);
-      const int pos = P.pos[b];
-      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float cs, sn;
-        rope_cs(pos, c * 4 + j, P.rope_base, cs, sn);
-        float2 ab = __bfloat1622float2(h2[j]);
-        h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
-      }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&item_full[b], 32);
+      mbar_init(&item_empty[b], kConsumerWarps);
     }
-    *reinterpret_cast<uint4*>(sq + r * 256 + (swz_chunk(r, c) << 4)) = v;
+    fence_mbar_init();
   }
   __syncthreads();
 
   if (warp == kConsumerWarps) {
-    // producer
-    if (lane == 0) {
-      const size_t head_off = (size_t)kvh * kPageTokens * kHeadDim;
-      for (int j = 0; j < it.n_entries; ++j) {
-        const int stage = j % kStages;
-        if (j >= kStages) mbar_wait(&empty[stage], ((j / kStages) - 1) & 1);
-        const int64_t page = P.arena[it.entry_off + j].page;
-        const size_t src = (size_t)page * P.kv_heads * kPageTokens * kHeadDim + head_off;
-        uint8_t* dst = ring + stage * kStageBytes;
-        mbar_arrive_expect_tx(&full[stage], kStageBytes);
-        bulk_g2s(dst, P.kplane + src, kStageBytes / 2, &full[stage]);
-        bulk_g2s(dst + kStageBytes / 2, P.vplane + src, kStageBytes / 2, &full[stage]);
+    // ---------------- producer warp ----------------
+    int gp = 0;
+    for (int iter = 0;; ++iter) {
+      const int buf = iter & 1;
+      if (iter >= 2) mbar_wait(&item_empty[buf], ((iter >> 1) - 1) & 1);
+      int w = 0;
+      if (lane == 0) w = atomicAdd(P.work_counter, 1);
+      w = __shfl_sync(0xffffffffu, w, 0);
+      ItemSlot* is = &s_item[buf];
+      if (w >= P.n_work) {
+        if (lane == 0) is->valid = 0;
+        mbar_arrive(&item_full[buf]);
+        break;
       }
+      const WorkItem it = P.items[w / P.kv_heads];
+      const int kvh = w % P.kv_heads;
+      PageRef* s_ent = reinterpret_cast<PageRef*>(smem + kOffEnt + buf * kSmemEnt);
+      for (int j = lane; j < it.n_entries; j += 32) s_ent[j] = P.arena[it.entry_off + j];
+      // rotated Q rows (member * gqa + local head), chunk-swizzled for ldmatrix
+      uint8_t* sq = smem + kOffQ + buf * kSmemQ;
+      const int rows = it.nt * 8, nrows = it.n_mem * P.gqa;
+      for (int x = lane; x < rows * 16; x += 32) {
+        const int r = x >> 4, c = x & 15;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r < nrows) {
+          const int b = P.members[it.mem_off + r / P.gqa];
+          const int head = kvh * P.gqa + r % P.gqa;
+          v = *reinterpret_cast<const uint4*>(P.q + ((size_t)b * P.q_heads + head) * kHeadDim + c * 8);
+          const int pos = P.pos[b];
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float cs, sn;
+            rope_cs(pos, P.rope.inv[c * 4 + j], cs, sn);
+            float2 ab = __bfloat1622float2(h2[j]);
+            h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
+          }
+        }
+        *reinterpret_cast<uint4*>(sq + r * 256 + (swz_chunk(r, c) << 4)) = v;
+      }
+      if (lane == 0) {
+        is->it = it;
+        is->kvh = kvh;
+        is->valid = 1;
+      }
+      __syncwarp();
+      mbar_arrive(&item_full[buf]);  // release: entries, Q and the slot are visible
+      if (lane == 0) {
+        const size_t head_off = (size_t)kvh * kPageTokens * kHeadDim;
+        for (int j = 0; j < it.n_entries; ++j, ++gp) {
+          const int stage = gp % kStages;
+          if (gp >= kStages) mbar_wait(&empty[stage], ((gp / kStages) - 1) & 1);
+          const size_t src = (size_t)s_ent[j].page * P.kv_heads * kPageTokens * kHeadDim + head_off;
+          uint8_t* dst = ring + stage * kStageBytes;
+          mbar_arrive_expect_tx(&full[stage], kStageBytes);
+          bulk_g2s(dst, P.kplane + src, kStageBytes / 2, &full[stage]);
+          bulk_g2s(dst + kStageBytes / 2, P.vplane + src, kStageBytes / 2, &full[stage]);
+        }
+      }
+      gp = __shfl_sync(0xffffffffu, gp, 0);
     }
     return;
   }
 
-  float* s_ml = reinterpret_cast<float*>(ring);                       // aliases the ring after the
-  float* s_o = reinterpret_cast<float*>(ring + kPairs * 48 * 2 * 4);  // consumers' barrier
-  switch (it.nt) {
-    case 1: consume<1>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
-    case 2: consume<2>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
-    case 3: consume<3>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
-    case 4: consume<4>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
-    default: consume<5>(P, it, kvh, ring, sq, full, empty, s_ml, s_o); break;
+  // ---------------- consumer warps ----------------
+  int gbase = 0;
+  for (int iter = 0;; ++iter) {
+    const int buf = iter & 1;
+    mbar_wait(&item_full[buf], (iter >> 1) & 1);
+    const ItemSlot is = s_item[buf];
+    if (!is.valid) break;
+    const uint8_t* sq = smem + kOffQ + buf * kSmemQ;
+    const PageRef* s_ent = reinterpret_cast<const PageRef*>(smem + kOffEnt + buf * kSmemEnt);
+    switch (is.it.nt) {
+      case 1: consume_item<1>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
+      case 2: consume_item<2>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
+      case 3: consume_item<3>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
+      case 4: consume_item<4>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
+      default: consume_item<5>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
+    }
+    gbase += is.it.n_entries;
   }
 }
 
-// Merge every handle's partials (log-sum-exp) into the bf16 output.
+// Merge every handle's partials (log-sum-exp) into the output; one warp per (handle, q head),
+// float4 per lane, single pass with online rescaling.
 __global__ void combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
-                               const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ slot_idx,
-                               int q_heads, __nv_bfloat16* __restrict__ out) {
-  const int b = blockIdx.x, h = blockIdx.y, dim = threadIdx.x;
+                               const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ slot_idx, int n,
+                               int q_heads, void* __restrict__ out, int out_f32) {
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (wid >= n * q_heads) return;
+  const int b = wid / q_heads, h = wid % q_heads;
   const int s0 = slot_ptr[b], s1 = slot_ptr[b + 1];
-  float m = -INFINITY;
-  for (int s = s0; s < s1; ++s) m = fmaxf(m, part_ml[(int64_t)slot_idx[s] * q_heads + h].x);
-  const float mu = m == -INFINITY ? 0.f : m;
-  float acc = 0.f, l = 0.f;
+  float m = -INFINITY, l = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s = s0; s < s1; ++s) {
     const int64_t sl = slot_idx[s];
     const float2 ml = part_ml[sl * q_heads + h];
-    const float w = fast_exp2(ml.x - mu);
-    acc += w * part_o[(sl * q_heads + h) * kHeadDim + dim];
-    l += w * ml.y;
+    const float4 v = *reinterpret_cast<const float4*>(&part_o[(sl * q_heads + h) * kHeadDim + lane * 4]);
+    const float mn = fmaxf(m, ml.x);
+    if (mn == -INFINITY) continue;
+    const float a = fast_exp2(m - mn), w = fast_exp2(ml.x - mn);
+    acc.x = acc.x * a + w * v.x;
+    acc.y = acc.y * a + w * v.y;
+    acc.z = acc.z * a + w * v.z;
+    acc.w = acc.w * a + w * v.w;
+    l = l * a + w * ml.y;
+    m = mn;
   }
-  out[((int64_t)b * q_heads + h) * kHeadDim + dim] = __float2bfloat16_rn(l > 0.f ? acc / l : 0.f);
+  const float inv = l > 0.f ? 1.f / l : 0.f;
+  const int64_t at = ((int64_t)b * q_heads + h) * kHeadDim + lane * 4;
+  if (out_f32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + at) =
+        make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+  } else {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    uint2 pk;
+    pk.x = *reinterpret_cast<uint32_t*>(&lo);
+    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + at) = pk;
+  }
 }
 
 }  // namespace
@@ -346,7 +436,10 @@ struct DecodePlanCache {
   float2* d_part_ml = nullptr;
   size_t cap_items = 0, cap_members = 0, cap_ptr = 0, cap_idx = 0, cap_slots = 0;
   bool smem_set = false;
+  int num_sms = 148;
+  int* d_counter = nullptr;
   ~DecodePlanCache() {
+    cudaFree(d_counter);
     cudaFree(d_items);
     cudaFree(d_members);
     cudaFree(d_slot_ptr);
@@ -453,7 +546,7 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
 using namespace mv;
 
 extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_t* hs, int32_t n, int32_t q_heads,
-                                    const void* d_q, const int32_t* d_positions, void* d_out) {
+                                    const void* d_q, const int32_t* d_positions, void* d_out, int32_t out_dtype) {
   if (!s || !s->impl) return fail(MV_ERR_INVALID_ARGUMENT, "null store");
   PagedStore& st = *s->impl;
   const mv_kv_config& cfg = st.cfg();
@@ -464,6 +557,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   const int gqa = q_heads / cfg.kv_heads;
   if (gqa > kMaxNT * 8) return fail(MV_ERR_INVALID_ARGUMENT, "GQA group larger than 40 heads");
   if (!d_q || !d_positions || !d_out) return fail(MV_ERR_INVALID_ARGUMENT, "null buffer");
+  if (out_dtype != 0 && out_dtype != 1) return fail(MV_ERR_INVALID_ARGUMENT, "out_dtype must be 0 (bf16) or 1 (fp32)");
 
   if (!st.plan) st.plan = new DecodePlanCache();
   DecodePlanCache& pc = *st.plan;
@@ -505,6 +599,10 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   }
   if (!pc.smem_set) {
     MV_CUDA_TRY(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem));
+    int dev = 0;
+    MV_CUDA_TRY(cudaGetDevice(&dev));
+    MV_CUDA_TRY(cudaDeviceGetAttribute(&pc.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    MV_CUDA_TRY(cudaMalloc(&pc.d_counter, sizeof(int)));
     pc.smem_set = true;
   }
   DecodeParams P;
@@ -521,12 +619,16 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   P.q_heads = q_heads;
   P.gqa = gqa;
   P.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
-  P.rope_base = cfg.rope_base;
-  dim3 grid((unsigned)pc.items.size(), (unsigned)cfg.kv_heads);
+  P.rope = st.rope();
+  MV_CUDA_TRY(cudaMemsetAsync(pc.d_counter, 0, sizeof(int), stream));
+  P.work_counter = pc.d_counter;
+  P.n_work = (int)pc.items.size() * cfg.kv_heads;
+  const int grid = std::min(P.n_work, pc.num_sms);
   decode_kernel<<<grid, kDecThreads, kDecSmem, stream>>>(P);
   MV_LAUNCH_CHECK();
-  combine_kernel<<<dim3(n, q_heads), kHeadDim, 0, stream>>>(pc.d_part_o, pc.d_part_ml, pc.d_slot_ptr, pc.d_slot_idx,
-                                                            q_heads, (__nv_bfloat16*)d_out);
+  const int warps = n * q_heads;
+  combine_kernel<<<(warps + 7) / 8, 256, 0, stream>>>(pc.d_part_o, pc.d_part_ml, pc.d_slot_ptr, pc.d_slot_idx, n,
+                                                      q_heads, d_out, out_dtype == 1);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }

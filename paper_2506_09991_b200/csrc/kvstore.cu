@@ -178,13 +178,13 @@ __global__ void k_append_table(PageRef* __restrict__ arena, int32_t* __restrict_
 }
 
 // step 2: per token, write slot token ids, payload records and (optionally) K/V.
-__device__ __forceinline__ void rope8(uint4& v, int pos, int chunk, double base) {
+__device__ __forceinline__ void rope8(uint4& v, int pos, int chunk, const RopeTable& rt) {
   // 8 dims = 4 interleaved pairs, pair index t = chunk*4 + j (toy_model.cpp:30-41)
   __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     float c, s;
-    rope_cs(pos, chunk * 4 + j, base, c, s);
+    rope_cs(pos, rt.inv[chunk * 4 + j], c, s);
     float2 ab = __bfloat1622float2(h[j]);
     h[j] = __floats2bfloat162_rn(ab.x * c - ab.y * s, ab.x * s + ab.y * c);
   }
@@ -192,13 +192,13 @@ __device__ __forceinline__ void rope8(uint4& v, int pos, int chunk, double base)
 
 __device__ __forceinline__ void write_kv_token(__nv_bfloat16* kp, __nv_bfloat16* vp, int64_t page, int slot,
                                                int kv_heads, const __nv_bfloat16* k, const __nv_bfloat16* v,
-                                               int pos, double base, int lane, int nlanes) {
+                                               int pos, const RopeTable& rt, int lane, int nlanes) {
   // kv_heads * 16 chunks of 8 dims; K rotated, V verbatim; stored chunk-swizzled.
   for (int j = lane; j < kv_heads * 16; j += nlanes) {
     int h = j >> 4, c = j & 15;
     size_t dst = kv_page_head_offset(page, h, kv_heads) + (size_t)slot * kHeadDim + (size_t)swz_chunk(slot, c) * 8;
     uint4 kk = *reinterpret_cast<const uint4*>(k + (size_t)h * kHeadDim + c * 8);
-    rope8(kk, pos, c, base);
+    rope8(kk, pos, c, rt);
     *reinterpret_cast<uint4*>(kp + dst) = kk;
     *reinterpret_cast<uint4*>(vp + dst) = *reinterpret_cast<const uint4*>(v + (size_t)h * kHeadDim + c * 8);
   }
@@ -209,7 +209,7 @@ __global__ void k_append_data(AppendPlan pl, const int32_t* __restrict__ page_ou
                               const uint8_t* __restrict__ rec_in, uint8_t* __restrict__ records, int rec_bytes,
                               const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                               const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads,
-                              double base) {
+                              const RopeTable rt) {
   // one warp per token
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
@@ -232,33 +232,37 @@ __global__ void k_append_data(AppendPlan pl, const int32_t* __restrict__ page_ou
     for (int b = lane; b < rec_bytes; b += 32) records[gslot * rec_bytes + b] = rec_in[(int64_t)t * rec_bytes + b];
   if (k && v)
     write_kv_token(kp, vp, page, slot, kv_heads, k + (size_t)t * kv_heads * kHeadDim,
-                   v + (size_t)t * kv_heads * kHeadDim, pos ? pos[t] : 0, base, lane, 32);
+                   v + (size_t)t * kv_heads * kHeadDim, pos ? pos[t] : 0, rt, lane, 32);
 }
 
-// Engine fast path: one token per handle, in place (one CTA per handle).
+// Engine fast path: one token per handle, in place (one warp per handle, 4 per CTA).
 struct TokDesc {
   int64_t idx;     // arena index of the entry to extend / create
   int32_t fresh;   // 1 -> pop a page and create entry (page,0,1); 0 -> grow entry in place
   int32_t cumv;    // cum value for a fresh entry
 };
 __global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ cum, const TokDesc* __restrict__ d,
-                             const int32_t* __restrict__ tokens, int32_t* __restrict__ slot_tok,
+                             int n, const int32_t* __restrict__ tokens, int32_t* __restrict__ slot_tok,
                              int32_t* __restrict__ refcnt, int32_t* __restrict__ free_stack,
                              int32_t* __restrict__ free_top, int32_t* __restrict__ err, const int32_t* __restrict__ pos,
                              const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
-                             __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, double base) {
-  __shared__ int s_page, s_slot;
-  const int i = blockIdx.x;
-  if (threadIdx.x == 0) {
+                             __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, const RopeTable rt) {
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= n) return;
+  int page = -1, slot = 0;
+  if (lane == 0) {
     TokDesc td = d[i];
-    int page = -1, slot = 0;
     if (td.fresh) {
-      int b = pop_pages(free_top, 1, err);
-      if (b >= 0) {
-        page = free_stack[b];
+      // a failed pop leaves the stack usable only for reporting: the sticky error poisons the store
+      int old = atomicSub(free_top, 1);
+      if (old >= 1) {
+        page = free_stack[old - 1];
         arena[td.idx] = make_ref(page, 0, 1);
         cum[td.idx] = td.cumv;
         refcnt[page] = 1;
+      } else {
+        atomicAdd(free_top, 1);
+        atomicOr(err, (int)kErrNoPages);
       }
     } else {
       PageRef r = arena[td.idx];
@@ -267,25 +271,24 @@ __global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ 
       arena[td.idx] = make_ref(r.page, ref_begin(r), ref_count(r) + 1);
     }
     if (page >= 0 && tokens) slot_tok[(int64_t)page * kPageTokens + slot] = tokens[i];
-    s_page = page;
-    s_slot = slot;
   }
-  __syncthreads();
-  if (s_page < 0 || !k || !v) return;
-  write_kv_token(kp, vp, s_page, s_slot, kv_heads, k + (size_t)i * kv_heads * kHeadDim,
-                 v + (size_t)i * kv_heads * kHeadDim, pos[i], base, threadIdx.x, blockDim.x);
+  page = __shfl_sync(0xffffffffu, page, 0);
+  slot = __shfl_sync(0xffffffffu, slot, 0);
+  if (page < 0 || !k || !v) return;
+  write_kv_token(kp, vp, page, slot, kv_heads, k + (size_t)i * kv_heads * kHeadDim,
+                 v + (size_t)i * kv_heads * kHeadDim, pos[i], rt, lane, 32);
 }
 
 // K/V of the last token of each handle (for layers > the one written at append).
 __global__ void k_write_last(const PageRef* __restrict__ arena, const int64_t* __restrict__ idx,
                              const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                              const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads,
-                             double base) {
+                             const RopeTable rt) {
   const int i = blockIdx.x;
   PageRef r = arena[idx[i]];
   int slot = ref_begin(r) + ref_count(r) - 1;
   write_kv_token(kp, vp, r.page, slot, kv_heads, k + (size_t)i * kv_heads * kHeadDim,
-                 v + (size_t)i * kv_heads * kHeadDim, pos[i], base, threadIdx.x, blockDim.x);
+                 v + (size_t)i * kv_heads * kHeadDim, pos[i], rt, threadIdx.x, blockDim.x);
 }
 
 // resolve / resolve_payloads / resolve_slots / gather_kv: one thread block per entry.
@@ -363,6 +366,7 @@ int32_t pow2_cap(int32_t need) {
 PagedStore::PagedStore(const mv_kv_config& cfg) : cfg_(cfg) {
   if (cfg_.table_entries <= 0) cfg_.table_entries = 4 * (int64_t)cfg_.num_pages + 65536;
   if (cfg_.rope_base <= 0) cfg_.rope_base = 10000.0;
+  rope_ = make_rope_table(cfg_.rope_base);
 }
 
 PagedStore::~PagedStore() {
@@ -614,7 +618,7 @@ mv_status PagedStore::extend(uint64_t h, const int32_t* tokens, int64_t n, const
     int64_t threads = n * 32;
     k_append_data<<<(int)((threads + 255) / 256), 256, 0, stream_>>>(
         pl, d_pages, d_pages + new_pages, (const int32_t*)d_tok, d_slot_tok_, (const uint8_t*)d_rec, d_records_,
-        cfg_.record_bytes, nullptr, nullptr, nullptr, nullptr, nullptr, cfg_.kv_heads, cfg_.rope_base);
+        cfg_.record_bytes, nullptr, nullptr, nullptr, nullptr, nullptr, cfg_.kv_heads, rope_);
     MV_LAUNCH_CHECK();
     for (int64_t t = 0; t < fill; ++t) r.cum.back()++;
     for (int32_t k = 0; k < new_pages; ++k) {
@@ -818,10 +822,11 @@ mv_status PagedStore::append(const uint64_t* hs, int32_t n, const int32_t* d_tok
   }
   void* d_desc;
   if (mv_status st = upload(desc.data(), sizeof(TokDesc) * n, &d_desc, 10)) return st;
-  k_append_one<<<n, 128, 0, stream_>>>(d_arena, d_cum, (const TokDesc*)d_desc, d_tokens, d_slot_tok_, d_refcnt_,
+  k_append_one<<<(n + 3) / 4, 128, 0, stream_>>>(d_arena, d_cum, (const TokDesc*)d_desc, n, d_tokens, d_slot_tok_,
+                                                 d_refcnt_,
                                        d_free_, d_free_top_, d_err_, d_pos, (const __nv_bfloat16*)d_k,
                                        (const __nv_bfloat16*)d_v, d_k ? k_planes_[layer] : nullptr,
-                                       d_k ? v_planes_[layer] : nullptr, cfg_.kv_heads, cfg_.rope_base);
+                                       d_k ? v_planes_[layer] : nullptr, cfg_.kv_heads, rope_);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }
@@ -842,7 +847,7 @@ mv_status PagedStore::write_last(const uint64_t* hs, int32_t n, const int32_t* d
   if (mv_status st = upload(idx.data(), sizeof(int64_t) * n, &d_idx, 11)) return st;
   k_write_last<<<n, 128, 0, stream_>>>(d_arena, (const int64_t*)d_idx, d_pos, (const __nv_bfloat16*)d_k,
                                        (const __nv_bfloat16*)d_v, k_planes_[layer], v_planes_[layer], cfg_.kv_heads,
-                                       cfg_.rope_base);
+                                       rope_);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }
@@ -874,7 +879,7 @@ mv_status PagedStore::append_many(uint64_t h, int64_t n, const int32_t* d_tokens
   k_append_data<<<(int)((threads + 255) / 256), 256, 0, stream_>>>(
       pl, d_pages, d_pages + new_pages, d_tokens, d_slot_tok_, nullptr, d_records_, cfg_.record_bytes, d_pos,
       (const __nv_bfloat16*)d_k, (const __nv_bfloat16*)d_v, d_k ? k_planes_[layer] : nullptr,
-      d_k ? v_planes_[layer] : nullptr, cfg_.kv_heads, cfg_.rope_base);
+      d_k ? v_planes_[layer] : nullptr, cfg_.kv_heads, rope_);
   MV_LAUNCH_CHECK();
   r->cum.back() += fill;
   for (int32_t k = 0; k < new_pages; ++k) {

@@ -47,6 +47,7 @@ class PagedStore {
   mv_status init();
 
   const mv_kv_config& cfg() const { return cfg_; }
+  const RopeTable& rope() const { return rope_; }
   cudaStream_t stream() const { return stream_; }
   void set_stream(cudaStream_t s) { stream_ = s; }
 
@@ -88,6 +89,7 @@ class PagedStore {
   mv_status upload(const void* host, size_t bytes, void** dev_out, int slot);
 
   mv_kv_config cfg_;
+  RopeTable rope_;
   cudaStream_t stream_ = nullptr;
   int32_t* d_refcnt_ = nullptr;
   int32_t* d_free_ = nullptr;      // free-page stack

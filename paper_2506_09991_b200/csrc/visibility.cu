@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kVisThreads) visibility_kernel(const int32_t* 
   __shared__ int s_carry;
   __shared__ Frame frames[kMaxFrames];
   __shared__ int s_ntags;
+  __shared__ int s_err;
 
   const int s = blockIdx.x;
   const int64_t off = offsets[s];
@@ -236,8 +237,12 @@ __global__ void __launch_bounds__(kVisThreads) visibility_kernel(const int32_t* 
       else err = MV_ERR_MALFORMED;
     }
     status[s] = err;
+    s_err = err;
   }
   __syncthreads();
+  // A rejected stream has no defined positions/mask (the reference throws); tags past the
+  // failure point were never walked, so stop here.
+  if (s_err != MV_OK) return;
 
   // ---- phase 3: per-token fill ----
   if (threadIdx.x == 0) s_carry = 0;

@@ -75,7 +75,7 @@ def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1):
     pos = torch.tensor(qpos, dtype=torch.int32)
     st.append(handles, torch.full((n,), 12, dtype=torch.int32, device="cuda"), pos.cuda(), 0, knew.cuda(),
               vnew.cuda())
-    out = mv.attention.decode(st, handles, q.cuda(), pos.cuda())
+    out = mv.attention.decode(st, handles, q.cuda(), pos.cuda(), out_dtype=torch.float32)
     torch.cuda.synchronize()
     # oracle: rotate K at cache time and q at its position (fp64), attend prefix..suffix..self
     base = sum(x.shape[0] for x in rows["k"])
@@ -87,6 +87,9 @@ def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1):
     ctx_full = [c + [base + i] for i, c in enumerate(ctx)]
     ref = oracle.attn_decode(qr, Kr, V, ctx_full)
     err = np.abs(out.float().cpu().numpy() - ref).max()
+    # the bf16 output path: identical arithmetic plus the bf16 store rounding (<= 2^-9 |o|)
+    out16 = mv.attention.decode(st, handles, q.cuda(), pos.cuda()).float().cpu().numpy()
+    assert (np.abs(out16 - ref) <= TOL + np.abs(ref) * 2.0 ** -8).all()
     return err, st
 
 
@@ -141,7 +144,7 @@ def test_decode_after_merge(mv):
     knew, vnew, q = sym_bf16(555, (1, hkv, 128)), sym_bf16(556, (1, hkv, 128)), sym_bf16(557, (1, hq, 128))
     pos = torch.tensor([100 + 19], dtype=torch.int32)  # max path end + 1
     st.append([m], torch.tensor([13], dtype=torch.int32, device="cuda"), pos.cuda(), 0, knew.cuda(), vnew.cuda())
-    out = mv.attention.decode(st, [m], q.cuda(), pos.cuda())
+    out = mv.attention.decode(st, [m], q.cuda(), pos.cuda(), out_dtype=torch.float32)
     base = sum(x.shape[0] for x in rows["k"])
     K = np.concatenate([bf16_to_f64(x) for x in rows["k"]] + [bf16_to_f64(knew)])
     V = np.concatenate([bf16_to_f64(x) for x in rows["v"]] + [bf16_to_f64(vnew)])
