@@ -12,8 +12,11 @@
 // Units are split into <= 64-page chunks (split-KV); a work item = (chunk, <= 8 handles).
 //
 // Kernel (one CTA per (work item, KV head)):
-//   warp 6      : producer — 1-D bulk copies (TMA engine) of each 4 KiB K and V page-head
-//                 block into a 15-stage smem ring, mbarrier complete_tx signalling.
+//   warp 6      : TMA warp — 1-D bulk copies (TMA engine) of each 4 KiB K and V page-head
+//                 block into a 15-stage smem ring, mbarrier complete_tx signalling; it runs
+//                 ahead across work-item boundaries (persistent kernel, dynamic item queue).
+//   warp 7      : staging warp — claims the next (chunk, kv head) item and stages its page
+//                 entries and RoPE-rotated Q rows into a double buffer.
 //   warps 0..5  : 3 consumer pairs; pair p takes pages p, p+3, ...  Tokens are the MMA M
 //                 dimension and query rows the N dimension (mma.sync m16n8k16, swapped
 //                 operands), so 40 rows = 5 n8-tiles with no padding; S^T -> P^T goes
@@ -34,27 +37,34 @@ namespace mv {
 
 namespace {
 
-constexpr int kPairs = 3;  // 7 warps: <= 2 per SM sub-partition -> 255 regs/thread
-constexpr int kConsumerWarps = 2 * kPairs;
+constexpr int kConsumerWarps = 6;
 constexpr int kConsumerThreads = kConsumerWarps * 32;
-constexpr int kDecThreads = kConsumerThreads + 32;
-constexpr int kStages = 15;  // multiple of kPairs: stage s always belongs to pair s % kPairs
+constexpr int kDecThreads = kConsumerThreads + 64;  // + TMA warp + staging warp = 8 warps (255 regs)
+constexpr int kStages = 15;
 constexpr int kStageBytes = 2 * kPageTokens * kHeadDim * 2;  // K + V page-head blocks (8 KiB)
 constexpr int kMaxNT = 5;                                   // <= 40 query rows per item
 constexpr int kMaxRows = kMaxNT * 8;
 constexpr int kChunkPages = 64;                             // split-KV chunk (pages)
+constexpr float kLazyRescale = 8.f;                         // log2-domain headroom before O is rescaled
+constexpr int kRowSlots = 144;                              // epilogue rows: 6 streams x 24 or 3 x 40
 constexpr int kSmemRing = kStages * kStageBytes;            // 120 KiB
 constexpr int kSmemQ = kMaxRows * kHeadDim * 2;             // 10 KiB per buffer
 constexpr int kSmemEnt = kChunkPages * 8;                   // 512 B per buffer
-constexpr int kSmemO = kPairs * kMaxRows * kHeadDim * 4;    // 60 KiB epilogue
-constexpr int kSmemML = kPairs * kMaxRows * 2 * 4;
+constexpr int kSmemO = kRowSlots * kHeadDim * 4;            // 72 KiB epilogue
+constexpr int kSmemML = kRowSlots * 2 * 4;
 constexpr int kOffQ = kSmemRing;
 constexpr int kOffEnt = kOffQ + 2 * kSmemQ;
 constexpr int kOffO = kOffEnt + 2 * kSmemEnt;
 constexpr int kOffML = kOffO + kSmemO;
 constexpr int kOffItem = kOffML + kSmemML;
 constexpr int kOffBar = kOffItem + 2 * 64;
-constexpr int kDecSmem = kOffBar + (2 * kStages + 4) * 8;
+constexpr int kOffTag = kOffBar + (2 * kStages + 4) * 8;
+constexpr int kDecSmem = kOffTag + kStages * 4;
+
+// Consumer split of an item with NT row tiles: NT <= 3 -> every warp owns all rows and its own
+// page stream (6 streams); NT 4-5 -> warp pairs split the rows (ceil(NT/2) + floor(NT/2)) and
+// share a page stream (3 streams). No warp repeats another's Q.K^T work.
+__host__ __device__ constexpr int row_groups(int nt) { return nt <= 3 ? 1 : 2; }
 
 struct WorkItem {
   int64_t entry_off;   // absolute arena index of the chunk's first entry
@@ -89,56 +99,61 @@ struct DecodeParams {
   RopeTable rope;
 };
 
-// Consumer side of one work item: 3 pairs stream the item's pages through the ring.
-template <int NT>
-__device__ __forceinline__ void consume_item(const DecodeParams& P, const ItemSlot& is, int gbase, uint8_t* ring,
-                                             const uint8_t* sq, const PageRef* s_ent, uint64_t* full,
-                                             uint64_t* empty, uint64_t* item_empty, float* s_ml, float* s_o) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = warp >> 1, hh = warp & 1;
+// Consumer side of one work item for one warp: rows [nt0*8, (nt0+NTW)*8), pages
+// j = stream, stream + n_streams, ... . S^T = K.Q^T (tokens are the MMA M dimension), online
+// softmax in the log2 domain with lazy rescaling, P^T via movmatrix, O^T += V^T.P^T over all
+// 128 head dims (8 m-tiles).
+template <int NTW>
+__device__ __forceinline__ void consume_rows(const DecodeParams& P, const WorkItem& it, int gbase, int stream,
+                                             int n_streams, int nt0, uint8_t* ring, const uint8_t* sq,
+                                             const PageRef* s_ent, uint64_t* full, uint64_t* empty,
+                                             int empty_count, float* s_ml, float* s_o, const int* s_tag) {
+  const int lane = threadIdx.x & 31;
   const int g = lane >> 2, t4 = lane & 3;
-  const WorkItem& it = is.it;
 
-  // Q fragments (B operand, k16 x n8 "col"): rows nt*8.., dims ks*16..
-  uint32_t qb[NT][8][2];
+  uint32_t qb[NTW][8][2];
   const uint32_t sq_base = smem_u32(sq);
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
+  for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
-      int row = nt * 8 + (lane & 7);
+      int row = (nt0 + nt) * 8 + (lane & 7);
       int chunk = ks * 2 + ((lane >> 3) & 1);
       ldmatrix_x2(qb[nt][ks][0], qb[nt][ks][1], sq_base + row * 256 + (swz_chunk(row, chunk) << 4));
     }
 
-  float o[4][NT][4];
+  float o[8][NTW][4];
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
       for (int k = 0; k < 4; ++k) o[mt][nt][k] = 0.f;
-  float m_run[NT][2], l_run[NT][2];
+  float m_ref[NTW][2], l_run[NTW][2];
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    m_run[nt][0] = m_run[nt][1] = -INFINITY;
+  for (int nt = 0; nt < NTW; ++nt) {
+    m_ref[nt][0] = m_ref[nt][1] = -INFINITY;
     l_run[nt][0] = l_run[nt][1] = 0.f;
   }
 
   const int npages = it.n_entries;
-  for (int j = pair; j < npages; j += kPairs) {
+  for (int j = stream; j < npages; j += n_streams) {
     const int gp = gbase + j;
     const int stage = gp % kStages;
     const PageRef ref = s_ent[j];
     const int vb = ref_begin(ref), ve = vb + ref_count(ref);
+    // Streams consume stages out of order, so a stream may reach page gp while the stage still
+    // holds page gp - kStages in flight; a bare parity wait would then match the previous phase.
+    // The TMA warp tags the stage with gp before issuing it, which pins the phase.
+    while (ld_volatile_s32(&s_tag[stage]) != gp) {
+    }
     mbar_wait(&full[stage], (gp / kStages) & 1);
     const uint32_t kbase = smem_u32(ring + stage * kStageBytes);
     const uint32_t vbase = kbase + kPageTokens * kHeadDim * 2;
 
-    // S^T (16 tokens x 8 rows per n-tile) = K . Q^T
-    float s[NT][4];
+    float s[NTW][4];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+    for (int nt = 0; nt < NTW; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
       uint32_t a[4];
@@ -147,65 +162,75 @@ __device__ __forceinline__ void consume_item(const DecodeParams& P, const ItemSl
       const int chunk = ks * 2 + (mi >> 1);
       ldmatrix_x4(a[0], a[1], a[2], a[3], kbase + row * 256 + (swz_chunk(row, chunk) << 4));
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(s[nt], a, qb[nt][ks][0], qb[nt][ks][1]);
+      for (int nt = 0; nt < NTW; ++nt) mma_bf16_16816(s[nt], a, qb[nt][ks][0], qb[nt][ks][1]);
     }
 
-    // online softmax (log2 domain); tokens g and g+8, rows 2*t4 and 2*t4+1 of each n-tile
     const bool v0 = g >= vb && g < ve, v1 = g + 8 >= vb && g + 8 < ve;
-    uint32_t pb[NT][2];
+    float x[NTW][4], mx[NTW][2];
+    bool need = false;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      float x0 = v0 ? s[nt][0] * P.scale_log2 : -INFINITY;
-      float x1 = v0 ? s[nt][1] * P.scale_log2 : -INFINITY;
-      float x2 = v1 ? s[nt][2] * P.scale_log2 : -INFINITY;
-      float x3 = v1 ? s[nt][3] * P.scale_log2 : -INFINITY;
-      float mx0 = fmaxf(x0, x2), mx1 = fmaxf(x1, x3);
+    for (int nt = 0; nt < NTW; ++nt) {
+      x[nt][0] = v0 ? s[nt][0] * P.scale_log2 : -INFINITY;
+      x[nt][1] = v0 ? s[nt][1] * P.scale_log2 : -INFINITY;
+      x[nt][2] = v1 ? s[nt][2] * P.scale_log2 : -INFINITY;
+      x[nt][3] = v1 ? s[nt][3] * P.scale_log2 : -INFINITY;
+      mx[nt][0] = fmaxf(x[nt][0], x[nt][2]);
+      mx[nt][1] = fmaxf(x[nt][1], x[nt][3]);
 #pragma unroll
       for (int off = 4; off < 32; off <<= 1) {
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        mx[nt][0] = fmaxf(mx[nt][0], __shfl_xor_sync(0xffffffffu, mx[nt][0], off));
+        mx[nt][1] = fmaxf(mx[nt][1], __shfl_xor_sync(0xffffffffu, mx[nt][1], off));
       }
-      const float mn0 = fmaxf(m_run[nt][0], mx0), mn1 = fmaxf(m_run[nt][1], mx1);
-      const float mu0 = mn0 == -INFINITY ? 0.f : mn0, mu1 = mn1 == -INFINITY ? 0.f : mn1;
-      const float al0 = fast_exp2(m_run[nt][0] - mu0), al1 = fast_exp2(m_run[nt][1] - mu1);
-      m_run[nt][0] = mn0;
-      m_run[nt][1] = mn1;
-      const float p0 = fast_exp2(x0 - mu0), p1 = fast_exp2(x1 - mu1);
-      const float p2 = fast_exp2(x2 - mu0), p3 = fast_exp2(x3 - mu1);
-      l_run[nt][0] = l_run[nt][0] * al0 + p0 + p2;
-      l_run[nt][1] = l_run[nt][1] * al1 + p1 + p3;
+      need |= mx[nt][0] > m_ref[nt][0] + kLazyRescale || mx[nt][1] > m_ref[nt][1] + kLazyRescale;
+    }
+    if (__any_sync(0xffffffffu, need)) {
+      // move the reference max (rare after the first pages): rescale l and O
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        o[mt][nt][0] *= al0;
-        o[mt][nt][1] *= al1;
-        o[mt][nt][2] *= al0;
-        o[mt][nt][3] *= al1;
-      }
+      for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const float mn = fmaxf(m_ref[nt][c], mx[nt][c]);
+          const float al = mn == -INFINITY ? 1.f : fast_exp2(m_ref[nt][c] - mn);
+          m_ref[nt][c] = mn;
+          l_run[nt][c] *= al;
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            o[mt][nt][c] *= al;
+            o[mt][nt][2 + c] *= al;
+          }
+        }
+    }
+    uint32_t pb[NTW][2];
+#pragma unroll
+    for (int nt = 0; nt < NTW; ++nt) {
+      const float mu0 = m_ref[nt][0] == -INFINITY ? 0.f : m_ref[nt][0];
+      const float mu1 = m_ref[nt][1] == -INFINITY ? 0.f : m_ref[nt][1];
+      const float p0 = fast_exp2(x[nt][0] - mu0), p1 = fast_exp2(x[nt][1] - mu1);
+      const float p2 = fast_exp2(x[nt][2] - mu0), p3 = fast_exp2(x[nt][3] - mu1);
+      l_run[nt][0] += p0 + p2;
+      l_run[nt][1] += p1 + p3;
       pb[nt][0] = movmatrix_trans(pack_bf16(p0, p1));
       pb[nt][1] = movmatrix_trans(pack_bf16(p2, p3));
     }
 
-    // O^T (dims x rows) += V^T . P^T for this warp's 64 dims
+    // O^T (128 dims x rows) += V^T . P^T
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt) {
+    for (int mt = 0; mt < 8; ++mt) {
       uint32_t a[4];
       const int mi = lane >> 3;
       const int tok = (mi >> 1) * 8 + (lane & 7);
-      const int chunk = hh * 8 + mt * 2 + (mi & 1);
+      const int chunk = mt * 2 + (mi & 1);
       ldmatrix_x4_trans(a[0], a[1], a[2], a[3], vbase + tok * 256 + (swz_chunk(tok, chunk) << 4));
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) mma_bf16_16816(o[mt][nt], a, pb[nt][0], pb[nt][1]);
+      for (int nt = 0; nt < NTW; ++nt) mma_bf16_16816(o[mt][nt], a, pb[nt][0], pb[nt][1]);
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    if (lane == 0) mbar_arrive_n(&empty[stage], empty_count);
   }
-  // Q buffer and entry list of this item are no longer read: hand them back to the producer.
-  __syncwarp();
-  if (lane == 0) mbar_arrive(item_empty);
 
-  // finish l (sum over the 8 token lanes g), publish this pair's (m, l, O^T half) to smem
+  // finish l (sum over the 8 token lanes g) and publish this stream's (m, l, O) rows
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
+  for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       float l = l_run[nt][c];
@@ -213,49 +238,52 @@ __device__ __forceinline__ void consume_item(const DecodeParams& P, const ItemSl
       for (int off = 4; off < 32; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
       l_run[nt][c] = l;
     }
-  const int rows = NT * 8;
+  const int rows = it.nt * 8;
   asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads));  // previous item's merge readers are done
-  if (hh == 0 && g == 0) {
+  if (g == 0) {
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        int r = nt * 8 + 2 * t4 + c;
-        s_ml[(pair * rows + r) * 2 + 0] = m_run[nt][c];
-        s_ml[(pair * rows + r) * 2 + 1] = l_run[nt][c];
+        const int r = (nt0 + nt) * 8 + 2 * t4 + c;
+        s_ml[(stream * rows + r) * 2 + 0] = m_ref[nt][c];
+        s_ml[(stream * rows + r) * 2 + 1] = l_run[nt][c];
       }
   }
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+    for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        int dim = hh * 64 + mt * 16 + g + (k >> 1) * 8;
-        int r = nt * 8 + 2 * t4 + (k & 1);
-        s_o[(pair * rows + r) * kHeadDim + dim] = o[mt][nt][k];
+        const int dim = mt * 16 + g + (k >> 1) * 8;
+        const int r = (nt0 + nt) * 8 + 2 * t4 + (k & 1);
+        s_o[(stream * rows + r) * kHeadDim + dim] = o[mt][nt][k];
       }
-  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads));
+}
 
-  // merge the pairs and write one partial per (member, q head); float4 per thread
+// All consumer warps: merge the streams' partials and write one partial per (member, q head).
+__device__ __forceinline__ void merge_streams(const DecodeParams& P, const ItemSlot& is, int n_streams,
+                                              const float* s_ml, const float* s_o) {
+  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads));
+  const WorkItem& it = is.it;
+  const int rows = it.nt * 8;
   const int nrows = it.n_mem * P.gqa;
   for (int x = threadIdx.x; x < nrows * (kHeadDim / 4); x += kConsumerThreads) {
     const int r = x / (kHeadDim / 4), d4 = (x % (kHeadDim / 4)) * 4;
     float m = -INFINITY;
-#pragma unroll
-    for (int p = 0; p < kPairs; ++p) m = fmaxf(m, s_ml[(p * rows + r) * 2]);
+    for (int st = 0; st < n_streams; ++st) m = fmaxf(m, s_ml[(st * rows + r) * 2]);
     const float mu = m == -INFINITY ? 0.f : m;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float l = 0.f;
-#pragma unroll
-    for (int p = 0; p < kPairs; ++p) {
-      const float w = fast_exp2(s_ml[(p * rows + r) * 2] - mu);
-      const float4 v = *reinterpret_cast<const float4*>(&s_o[(p * rows + r) * kHeadDim + d4]);
+    for (int st = 0; st < n_streams; ++st) {
+      const float w = fast_exp2(s_ml[(st * rows + r) * 2] - mu);
+      const float4 v = *reinterpret_cast<const float4*>(&s_o[(st * rows + r) * kHeadDim + d4]);
       acc.x += w * v.x;
       acc.y += w * v.y;
       acc.z += w * v.z;
       acc.w += w * v.w;
-      l += w * s_ml[(p * rows + r) * 2 + 1];
+      l += w * s_ml[(st * rows + r) * 2 + 1];
     }
     const int mi = r / P.gqa, hl = r % P.gqa;
     const int64_t slot = it.slot_base + mi;
@@ -278,8 +306,10 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
   uint64_t* item_empty = item_full + 2;
   float* s_o = reinterpret_cast<float*>(smem + kOffO);
   float* s_ml = reinterpret_cast<float*>(smem + kOffML);
+  int* s_tag = reinterpret_cast<int*>(smem + kOffTag);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  for (int st = threadIdx.x; st < kStages; st += blockDim.x) s_tag[st] = -1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
@@ -287,15 +317,14 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&item_full[b], 32);
-      mbar_init(&item_empty[b], kConsumerWarps);
+      mbar_init(&item_empty[b], kConsumerWarps + 1);  // consumers + TMA warp
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {
-    // ---------------- producer warp ----------------
-    int gp = 0;
+  if (warp == kConsumerWarps + 1) {
+    // ---------------- staging warp: claims work and stages entries + rotated Q ----------------
     for (int iter = 0;; ++iter) {
       const int buf = iter & 1;
       if (iter >= 2) mbar_wait(&item_empty[buf], ((iter >> 1) - 1) & 1);
@@ -305,6 +334,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
       ItemSlot* is = &s_item[buf];
       if (w >= P.n_work) {
         if (lane == 0) is->valid = 0;
+        __syncwarp();
         mbar_arrive(&item_full[buf]);
         break;
       }
@@ -312,18 +342,34 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
       const int kvh = w % P.kv_heads;
       PageRef* s_ent = reinterpret_cast<PageRef*>(smem + kOffEnt + buf * kSmemEnt);
       for (int j = lane; j < it.n_entries; j += 32) s_ent[j] = P.arena[it.entry_off + j];
-      // rotated Q rows (member * gqa + local head), chunk-swizzled for ldmatrix
+      // rotated Q rows (member * gqa + local head), chunk-swizzled for ldmatrix. All global loads
+      // are issued before any use so the whole item costs ~3 memory round trips, not 20.
+      const int mb = lane < it.n_mem ? P.members[it.mem_off + lane] : 0;
+      const int mpos = lane < it.n_mem ? P.pos[mb] : 0;
       uint8_t* sq = smem + kOffQ + buf * kSmemQ;
       const int rows = it.nt * 8, nrows = it.n_mem * P.gqa;
-      for (int x = lane; x < rows * 16; x += 32) {
+      constexpr int kPer = kMaxRows * 16 / 32;  // 20 chunks of 16 B per lane at most
+      uint4 qv[kPer];
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int x = lane + 32 * k;
         const int r = x >> 4, c = x & 15;
-        uint4 v = make_uint4(0, 0, 0, 0);
+        const int mi = r / P.gqa;
+        const int b = __shfl_sync(0xffffffffu, mb, mi & 31);
+        qv[k] = make_uint4(0, 0, 0, 0);
         if (r < nrows) {
-          const int b = P.members[it.mem_off + r / P.gqa];
           const int head = kvh * P.gqa + r % P.gqa;
-          v = *reinterpret_cast<const uint4*>(P.q + ((size_t)b * P.q_heads + head) * kHeadDim + c * 8);
-          const int pos = P.pos[b];
-          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+          qv[k] = __ldg(reinterpret_cast<const uint4*>(P.q + ((size_t)b * P.q_heads + head) * kHeadDim + c * 8));
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kPer; ++k) {
+        const int x = lane + 32 * k;
+        const int r = x >> 4, c = x & 15;
+        const int pos = __shfl_sync(0xffffffffu, mpos, (r / P.gqa) & 31);
+        if (r >= rows) continue;
+        if (r < nrows) {
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&qv[k]);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float cs, sn;
@@ -332,7 +378,7 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
             h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
           }
         }
-        *reinterpret_cast<uint4*>(sq + r * 256 + (swz_chunk(r, c) << 4)) = v;
+        *reinterpret_cast<uint4*>(sq + r * 256 + (swz_chunk(r, c) << 4)) = qv[k];
       }
       if (lane == 0) {
         is->it = it;
@@ -341,19 +387,34 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
       }
       __syncwarp();
       mbar_arrive(&item_full[buf]);  // release: entries, Q and the slot are visible
-      if (lane == 0) {
-        const size_t head_off = (size_t)kvh * kPageTokens * kHeadDim;
-        for (int j = 0; j < it.n_entries; ++j, ++gp) {
+    }
+    return;
+  }
+
+  if (warp == kConsumerWarps) {
+    // ---------------- TMA warp: keeps the page ring full across item boundaries ----------------
+    if (lane == 0) {
+      int gp = 0;
+      for (int iter = 0;; ++iter) {
+        const int buf = iter & 1;
+        mbar_wait(&item_full[buf], (iter >> 1) & 1);
+        const ItemSlot* is = &s_item[buf];
+        if (!is->valid) break;
+        const PageRef* s_ent = reinterpret_cast<const PageRef*>(smem + kOffEnt + buf * kSmemEnt);
+        const size_t head_off = (size_t)is->kvh * kPageTokens * kHeadDim;
+        const int n_entries = is->it.n_entries;
+        for (int j = 0; j < n_entries; ++j, ++gp) {
           const int stage = gp % kStages;
           if (gp >= kStages) mbar_wait(&empty[stage], ((gp / kStages) - 1) & 1);
+          st_volatile_s32(&s_tag[stage], gp);
           const size_t src = (size_t)s_ent[j].page * P.kv_heads * kPageTokens * kHeadDim + head_off;
           uint8_t* dst = ring + stage * kStageBytes;
           mbar_arrive_expect_tx(&full[stage], kStageBytes);
           bulk_g2s(dst, P.kplane + src, kStageBytes / 2, &full[stage]);
           bulk_g2s(dst + kStageBytes / 2, P.vplane + src, kStageBytes / 2, &full[stage]);
         }
+        mbar_arrive(&item_empty[buf]);  // this item's entry list is no longer read by the TMA warp
       }
-      gp = __shfl_sync(0xffffffffu, gp, 0);
     }
     return;
   }
@@ -367,13 +428,24 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
     if (!is.valid) break;
     const uint8_t* sq = smem + kOffQ + buf * kSmemQ;
     const PageRef* s_ent = reinterpret_cast<const PageRef*>(smem + kOffEnt + buf * kSmemEnt);
-    switch (is.it.nt) {
-      case 1: consume_item<1>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
-      case 2: consume_item<2>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
-      case 3: consume_item<3>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
-      case 4: consume_item<4>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
-      default: consume_item<5>(P, is, gbase, ring, sq, s_ent, full, empty, &item_empty[buf], s_ml, s_o); break;
+    const int nt = is.it.nt;
+    const int G = row_groups(nt);
+    const int n_streams = kConsumerWarps / G;
+    const int stream = warp / G, half = warp % G;
+    const int nta = (nt + 1) / 2;
+    const int nt0 = G == 1 ? 0 : (half ? nta : 0);
+    const int ntw = G == 1 ? nt : (half ? nt - nta : nta);
+    // each stage is released by 2 arrivals: both warps of a pair, or one warp arriving twice
+    const int ecount = G == 1 ? 2 : 1;
+    switch (ntw) {
+      case 1: consume_rows<1>(P, is.it, gbase, stream, n_streams, nt0, ring, sq, s_ent, full, empty, ecount, s_ml, s_o, s_tag); break;
+      case 2: consume_rows<2>(P, is.it, gbase, stream, n_streams, nt0, ring, sq, s_ent, full, empty, ecount, s_ml, s_o, s_tag); break;
+      default: consume_rows<3>(P, is.it, gbase, stream, n_streams, nt0, ring, sq, s_ent, full, empty, ecount, s_ml, s_o, s_tag); break;
     }
+    // Q buffer and entry list of this item are no longer read: hand them back to the stager.
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&item_empty[buf]);
+    merge_streams(P, is, n_streams, s_ml, s_o);
     gbase += is.it.n_entries;
   }
 }

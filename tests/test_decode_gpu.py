@@ -151,3 +151,11 @@ def test_decode_after_merge(mv):
     P = np.concatenate([x.numpy() for x in rows["pos"]] + [pos.numpy()])
     ref = oracle.attn_decode(oracle.rope(bf16_to_f64(q), pos.numpy()), oracle.rope(K, P), V, [ctx + [base]])
     assert np.abs(out.float().cpu().numpy() - ref).max() < TOL
+
+
+def test_many_requests_persistent_mix(mv):
+    # > 148 (item, kv head) work units: every persistent CTA runs several mixed-width items
+    # back to back (cascade prefix items + private items), exercising the ring hand-over.
+    err, st = run_case(mv, [(1024, 8, 200)] * 8 + [(333, 3, 77)] * 3, hq=40, hkv=8, num_pages=2048, seed=5)
+    assert err < TOL, err
+    assert st.plan_info()["work_items"] * 8 > 148
