@@ -27,6 +27,7 @@
 //                 partial per (handle, q head); a combine kernel merges the partials of
 //                 each handle's chunks (log-sum-exp) into bf16 outputs.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <unordered_map>
 #include <vector>
@@ -57,7 +58,8 @@ constexpr int kOffEnt = kOffQ + 2 * kSmemQ;
 constexpr int kOffO = kOffEnt + 2 * kSmemEnt;
 constexpr int kOffML = kOffO + kSmemO;
 constexpr int kOffItem = kOffML + kSmemML;
-constexpr int kOffBar = kOffItem + 2 * 64;
+constexpr int kItemSlotBytes = 128;
+constexpr int kOffBar = kOffItem + 2 * kItemSlotBytes;
 constexpr int kOffTag = kOffBar + (2 * kStages + 4) * 8;
 constexpr int kDecSmem = kOffTag + kStages * 4;
 
@@ -66,15 +68,18 @@ constexpr int kDecSmem = kOffTag + kStages * 4;
 // share a page stream (3 streams). No warp repeats another's Q.K^T work.
 __host__ __device__ constexpr int row_groups(int nt) { return nt <= 3 ? 1 : 2; }
 
-struct WorkItem {
-  int64_t entry_off;   // absolute arena index of the chunk's first entry
+constexpr int kMaxMembers = 8;  // handles per work item (8 x GQA 5 = 40 rows)
+
+struct __align__(16) WorkItem {
+  int64_t entry_off;             // absolute arena index of the chunk's first entry
   int32_t n_entries;
-  int32_t mem_off;     // offset into the member list (batch indices)
-  int32_t n_mem;
-  int32_t slot_base;   // partial slot of the first member
-  int32_t nt;          // n8 row tiles needed
-  int32_t pad;
+  int32_t n_mem;                 // handles (query groups) sharing this chunk
+  int32_t slot_base;             // partial slot of the first member
+  int32_t nt;                    // n8 row tiles (ceil(n_mem * gqa / 8))
+  int32_t members[kMaxMembers];  // batch indices
+  int32_t pad[2];
 };
+static_assert(sizeof(WorkItem) == 64, "WorkItem is one 64 B line");
 
 struct ItemSlot {      // what the producer hands the consumers for one (item, kv head)
   WorkItem it;
@@ -82,20 +87,22 @@ struct ItemSlot {      // what the producer hands the consumers for one (item, k
   int32_t valid;
 };
 
+static_assert(sizeof(ItemSlot) <= kItemSlotBytes, "item slot overflows its smem reservation");
+
 struct DecodeParams {
   const PageRef* arena;
   const __nv_bfloat16* kplane;
   const __nv_bfloat16* vplane;
-  const __nv_bfloat16* q;     // [n][q_heads][128]
-  const int32_t* pos;         // [n]
+  const __nv_bfloat16* q_rot; // [n][q_heads][128], RoPE already applied (rope_q_kernel)
   const WorkItem* items;
-  const int32_t* members;
   float* part_o;              // [slots][q_heads][128]
   float2* part_ml;            // [slots][q_heads]
   int* work_counter;          // dynamic (item, kv head) scheduler
   int n_work;                 // items * kv_heads
   int kv_heads, q_heads, gqa;
   float scale_log2;           // log2(e) / sqrt(128)
+  int diag;                   // diagnostics: 1 = skip math (pipeline only), 2 = skip loads (math only)
+  unsigned long long* trace;  // optional per-item timeline (MV_DECODE_TRACE)
   RopeTable rope;
 };
 
@@ -119,7 +126,8 @@ __device__ __forceinline__ void consume_rows(const DecodeParams& P, const WorkIt
     for (int ks = 0; ks < 8; ++ks) {
       int row = (nt0 + nt) * 8 + (lane & 7);
       int chunk = ks * 2 + ((lane >> 3) & 1);
-      ldmatrix_x2(qb[nt][ks][0], qb[nt][ks][1], sq_base + row * 256 + (swz_chunk(row, chunk) << 4));
+      // Q rows land in smem by bulk copy (unswizzled); 4-way conflicts once per item only
+      ldmatrix_x2(qb[nt][ks][0], qb[nt][ks][1], sq_base + row * 256 + (chunk << 4));
     }
 
   float o[8][NTW][4];
@@ -148,6 +156,11 @@ __device__ __forceinline__ void consume_rows(const DecodeParams& P, const WorkIt
     while (ld_volatile_s32(&s_tag[stage]) != gp) {
     }
     mbar_wait(&full[stage], (gp / kStages) & 1);
+    if (P.diag == 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_n(&empty[stage], empty_count);
+      continue;
+    }
     const uint32_t kbase = smem_u32(ring + stage * kStageBytes);
     const uint32_t vbase = kbase + kPageTokens * kHeadDim * 2;
 
@@ -317,20 +330,21 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&item_full[b], 32);
-      mbar_init(&item_empty[b], kConsumerWarps + 1);  // consumers + TMA warp
+      mbar_init(&item_empty[b], kConsumerWarps + kStages);  // consumer warps + TMA lanes
     }
     fence_mbar_init();
   }
   __syncthreads();
 
   if (warp == kConsumerWarps + 1) {
-    // ---------------- staging warp: claims work and stages entries + rotated Q ----------------
+    // ---------------- staging warp: claims work and stages entries + Q rows ----------------
+    // Critical path per item is ~2 memory round trips: the next claim is issued one item
+    // ahead, Q rows (pre-rotated) arrive by bulk copy on the item barrier itself.
+    int w_next = lane == 0 ? atomicAdd(P.work_counter, 1) : 0;
     for (int iter = 0;; ++iter) {
       const int buf = iter & 1;
       if (iter >= 2) mbar_wait(&item_empty[buf], ((iter >> 1) - 1) & 1);
-      int w = 0;
-      if (lane == 0) w = atomicAdd(P.work_counter, 1);
-      w = __shfl_sync(0xffffffffu, w, 0);
+      const int w = __shfl_sync(0xffffffffu, w_next, 0);
       ItemSlot* is = &s_item[buf];
       if (w >= P.n_work) {
         if (lane == 0) is->valid = 0;
@@ -338,63 +352,42 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
         mbar_arrive(&item_full[buf]);
         break;
       }
+      if (lane == 0) w_next = atomicAdd(P.work_counter, 1);
       const WorkItem it = P.items[w / P.kv_heads];
       const int kvh = w % P.kv_heads;
-      PageRef* s_ent = reinterpret_cast<PageRef*>(smem + kOffEnt + buf * kSmemEnt);
-      for (int j = lane; j < it.n_entries; j += 32) s_ent[j] = P.arena[it.entry_off + j];
-      // rotated Q rows (member * gqa + local head), chunk-swizzled for ldmatrix. All global loads
-      // are issued before any use so the whole item costs ~3 memory round trips, not 20.
-      const int mb = lane < it.n_mem ? P.members[it.mem_off + lane] : 0;
-      const int mpos = lane < it.n_mem ? P.pos[mb] : 0;
       uint8_t* sq = smem + kOffQ + buf * kSmemQ;
-      const int rows = it.nt * 8, nrows = it.n_mem * P.gqa;
-      constexpr int kPer = kMaxRows * 16 / 32;  // 20 chunks of 16 B per lane at most
-      uint4 qv[kPer];
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const int x = lane + 32 * k;
-        const int r = x >> 4, c = x & 15;
-        const int mi = r / P.gqa;
-        const int b = __shfl_sync(0xffffffffu, mb, mi & 31);
-        qv[k] = make_uint4(0, 0, 0, 0);
-        if (r < nrows) {
-          const int head = kvh * P.gqa + r % P.gqa;
-          qv[k] = __ldg(reinterpret_cast<const uint4*>(P.q + ((size_t)b * P.q_heads + head) * kHeadDim + c * 8));
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kPer; ++k) {
-        const int x = lane + 32 * k;
-        const int r = x >> 4, c = x & 15;
-        const int pos = __shfl_sync(0xffffffffu, mpos, (r / P.gqa) & 31);
-        if (r >= rows) continue;
-        if (r < nrows) {
-          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&qv[k]);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            float cs, sn;
-            rope_cs(pos, P.rope.inv[c * 4 + j], cs, sn);
-            float2 ab = __bfloat1622float2(h2[j]);
-            h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
-          }
-        }
-        *reinterpret_cast<uint4*>(sq + r * 256 + (swz_chunk(r, c) << 4)) = qv[k];
-      }
+      const int qbytes = P.gqa * kHeadDim * 2;  // one handle's GQA group of q heads, contiguous
       if (lane == 0) {
         is->it = it;
         is->kvh = kvh;
         is->valid = 1;
+        mbar_arrive_expect_tx(&item_full[buf], it.n_mem * qbytes);
       }
       __syncwarp();
-      mbar_arrive(&item_full[buf]);  // release: entries, Q and the slot are visible
+      if (lane < it.n_mem) {
+        const int b = it.members[lane];
+        bulk_g2s(sq + lane * qbytes, P.q_rot + ((size_t)b * P.q_heads + kvh * P.gqa) * kHeadDim, qbytes,
+                 &item_full[buf]);
+      }
+      PageRef* s_ent = reinterpret_cast<PageRef*>(smem + kOffEnt + buf * kSmemEnt);
+      for (int j = lane; j < it.n_entries; j += 32) s_ent[j] = P.arena[it.entry_off + j];
+      // zero the padding rows of the last n8 tile
+      const int nrows = it.n_mem * P.gqa, rows = it.nt * 8;
+      for (int x = lane; x < (rows - nrows) * 16; x += 32)
+        *reinterpret_cast<uint4*>(sq + nrows * 256 + x * 16) = make_uint4(0, 0, 0, 0);
+      __syncwarp();
+      if (lane != 0) mbar_arrive(&item_full[buf]);  // lane 0 arrived with expect_tx
     }
     return;
   }
 
   if (warp == kConsumerWarps) {
     // ---------------- TMA warp: keeps the page ring full across item boundaries ----------------
-    if (lane == 0) {
-      int gp = 0;
+    // Lane l (< kStages) owns ring stage l and issues every page that maps to it. One issuing
+    // thread per stage matters: a single issuing thread serialises on its empty-barrier waits and
+    // caps a CTA at ~15 GB/s (tools/microbench/mb_tma.cu: 2.3 TB/s vs 7.0 TB/s chip-wide).
+    if (lane < kStages) {
+      int gbase = 0;
       for (int iter = 0;; ++iter) {
         const int buf = iter & 1;
         mbar_wait(&item_full[buf], (iter >> 1) & 1);
@@ -403,17 +396,23 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
         const PageRef* s_ent = reinterpret_cast<const PageRef*>(smem + kOffEnt + buf * kSmemEnt);
         const size_t head_off = (size_t)is->kvh * kPageTokens * kHeadDim;
         const int n_entries = is->it.n_entries;
-        for (int j = 0; j < n_entries; ++j, ++gp) {
-          const int stage = gp % kStages;
-          if (gp >= kStages) mbar_wait(&empty[stage], ((gp / kStages) - 1) & 1);
-          st_volatile_s32(&s_tag[stage], gp);
-          const size_t src = (size_t)s_ent[j].page * P.kv_heads * kPageTokens * kHeadDim + head_off;
-          uint8_t* dst = ring + stage * kStageBytes;
-          mbar_arrive_expect_tx(&full[stage], kStageBytes);
-          bulk_g2s(dst, P.kplane + src, kStageBytes / 2, &full[stage]);
-          bulk_g2s(dst + kStageBytes / 2, P.vplane + src, kStageBytes / 2, &full[stage]);
+        const size_t page_stride = (size_t)P.kv_heads * kPageTokens * kHeadDim;
+        for (int j = ((lane - gbase) % kStages + kStages) % kStages; j < n_entries; j += kStages) {
+          const int gp = gbase + j;
+          if (gp >= kStages) mbar_wait(&empty[lane], ((gp / kStages) - 1) & 1);
+          st_volatile_s32(&s_tag[lane], gp);
+          uint8_t* dst = ring + lane * kStageBytes;
+          if (P.diag == 2) {
+            mbar_arrive(&full[lane]);
+            continue;
+          }
+          const size_t src = (size_t)s_ent[j].page * page_stride + head_off;
+          mbar_arrive_expect_tx(&full[lane], kStageBytes);
+          bulk_g2s(dst, P.kplane + src, kStageBytes / 2, &full[lane]);
+          bulk_g2s(dst + kStageBytes / 2, P.vplane + src, kStageBytes / 2, &full[lane]);
         }
-        mbar_arrive(&item_empty[buf]);  // this item's entry list is no longer read by the TMA warp
+        mbar_arrive(&item_empty[buf]);  // this lane no longer reads the item's entry list
+        gbase += n_entries;
       }
     }
     return;
@@ -421,10 +420,13 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
 
   // ---------------- consumer warps ----------------
   int gbase = 0;
+  unsigned long long* tr = P.trace ? P.trace + (size_t)blockIdx.x * 64 * 4 : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   for (int iter = 0;; ++iter) {
     const int buf = iter & 1;
     mbar_wait(&item_full[buf], (iter >> 1) & 1);
     const ItemSlot is = s_item[buf];
+    if (tr && threadIdx.x == 0 && iter < 62) { tr[4 + iter * 4] = globaltimer(); tr[5 + iter * 4] = is.it.n_entries | ((unsigned long long)is.it.nt << 32); }
     if (!is.valid) break;
     const uint8_t* sq = smem + kOffQ + buf * kSmemQ;
     const PageRef* s_ent = reinterpret_cast<const PageRef*>(smem + kOffEnt + buf * kSmemEnt);
@@ -445,9 +447,33 @@ __global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) 
     // Q buffer and entry list of this item are no longer read: hand them back to the stager.
     __syncwarp();
     if (lane == 0) mbar_arrive(&item_empty[buf]);
+    if (tr && threadIdx.x == 0 && iter < 62) tr[6 + iter * 4] = globaltimer();
     merge_streams(P, is, n_streams, s_ml, s_o);
+    if (tr && threadIdx.x == 0 && iter < 62) tr[7 + iter * 4] = globaltimer();
     gbase += is.it.n_entries;
   }
+}
+
+// RoPE pre-pass: rotate every query once (toy_model.cpp:30-41 at the handle's position) so the
+// decode kernel can bulk-copy Q rows; thread 0 also resets the work-item counter.
+__global__ void rope_q_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pos, int n,
+                              int q_heads, const RopeTable rt, __nv_bfloat16* __restrict__ q_rot, int* counter) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one 16 B chunk (4 pairs)
+  if (x == 0) *counter = 0;
+  if (x >= (int64_t)n * q_heads * 16) return;
+  const int c = (int)(x & 15);
+  const int b = (int)(x / (16 * q_heads));
+  uint4 v = *reinterpret_cast<const uint4*>(q + x * 8);
+  __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+  const int p = pos[b];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float cs, sn;
+    rope_cs(p, rt.inv[c * 4 + j], cs, sn);
+    const float2 ab = __bfloat1622float2(h2[j]);
+    h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
+  }
+  *reinterpret_cast<uint4*>(q_rot + x * 8) = v;
 }
 
 // Merge every handle's partials (log-sum-exp) into the output; one warp per (handle, q head),
@@ -498,22 +524,25 @@ struct DecodePlanCache {
   int q_heads = 0;
   // host plan
   std::vector<WorkItem> items;
-  std::vector<int32_t> members, slot_ptr, slot_idx;
+  std::vector<int32_t> slot_ptr, slot_idx;
   int32_t n_slots = 0;
   mv_decode_plan_info info{};
   // device copies
   WorkItem* d_items = nullptr;
-  int32_t *d_members = nullptr, *d_slot_ptr = nullptr, *d_slot_idx = nullptr;
+  int32_t *d_slot_ptr = nullptr, *d_slot_idx = nullptr;
+  __nv_bfloat16* d_q_rot = nullptr;
   float* d_part_o = nullptr;
   float2* d_part_ml = nullptr;
-  size_t cap_items = 0, cap_members = 0, cap_ptr = 0, cap_idx = 0, cap_slots = 0;
+  size_t cap_items = 0, cap_q_rot = 0, cap_ptr = 0, cap_idx = 0, cap_slots = 0;
   bool smem_set = false;
   int num_sms = 148;
   int* d_counter = nullptr;
+  unsigned long long* d_trace = nullptr;
   ~DecodePlanCache() {
     cudaFree(d_counter);
+    cudaFree(d_trace);
     cudaFree(d_items);
-    cudaFree(d_members);
+    cudaFree(d_q_rot);
     cudaFree(d_slot_ptr);
     cudaFree(d_slot_idx);
     cudaFree(d_part_o);
@@ -534,11 +563,10 @@ static mv_status ensure_dev(T*& p, size_t& cap, size_t n) {
 
 static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, int n, int q_heads, int gqa) {
   pc.items.clear();
-  pc.members.clear();
   std::vector<std::vector<int32_t>> slots_of(n);
   int32_t n_slots = 0;
   int64_t unique_tokens = 0, naive_tokens = 0;
-  const int max_members = std::max(1, (kMaxNT * 8) / gqa);
+  const int max_members = std::max(1, std::min(kMaxMembers, (kMaxNT * 8) / gqa));
 
   // group id -> member batch indices (in batch order)
   std::unordered_map<uint64_t, std::vector<int32_t>> group_members;
@@ -560,15 +588,14 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
       for (size_t m0 = 0; m0 < mem.size(); m0 += max_members) {
         const int32_t nm = (int32_t)std::min<size_t>(max_members, mem.size() - m0);
         WorkItem w;
+        std::memset(&w, 0, sizeof w);
         w.entry_off = src_off + c0;
         w.n_entries = c1 - c0;
-        w.mem_off = (int32_t)pc.members.size();
         w.n_mem = nm;
         w.slot_base = n_slots;
         w.nt = (nm * gqa + 7) / 8;
-        w.pad = 0;
         for (int32_t k = 0; k < nm; ++k) {
-          pc.members.push_back(mem[m0 + k]);
+          w.members[k] = mem[m0 + k];
           slots_of[mem[m0 + k]].push_back(n_slots + k);
         }
         n_slots += nm;
@@ -651,7 +678,6 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     pc.sig = sig;
     pc.q_heads = q_heads;
     if (mv_status e = ensure_dev(pc.d_items, pc.cap_items, pc.items.size())) return e;
-    if (mv_status e = ensure_dev(pc.d_members, pc.cap_members, std::max<size_t>(1, pc.members.size()))) return e;
     if (mv_status e = ensure_dev(pc.d_slot_ptr, pc.cap_ptr, pc.slot_ptr.size())) return e;
     if (mv_status e = ensure_dev(pc.d_slot_idx, pc.cap_idx, std::max<size_t>(1, pc.slot_idx.size()))) return e;
     size_t old_slots = pc.cap_slots;
@@ -661,8 +687,6 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
       MV_CUDA_TRY(cudaMalloc(&pc.d_part_o, sizeof(float) * pc.cap_slots * kHeadDim));
     }
     MV_CUDA_TRY(cudaMemcpyAsync(pc.d_items, pc.items.data(), sizeof(WorkItem) * pc.items.size(),
-                                cudaMemcpyHostToDevice, stream));
-    MV_CUDA_TRY(cudaMemcpyAsync(pc.d_members, pc.members.data(), sizeof(int32_t) * pc.members.size(),
                                 cudaMemcpyHostToDevice, stream));
     MV_CUDA_TRY(cudaMemcpyAsync(pc.d_slot_ptr, pc.slot_ptr.data(), sizeof(int32_t) * pc.slot_ptr.size(),
                                 cudaMemcpyHostToDevice, stream));
@@ -681,10 +705,9 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   P.arena = st.d_arena;
   P.kplane = st.k_planes()[layer];
   P.vplane = st.v_planes()[layer];
-  P.q = (const __nv_bfloat16*)d_q;
-  P.pos = d_positions;
+  if (mv_status e = ensure_dev(pc.d_q_rot, pc.cap_q_rot, (size_t)n * q_heads * kHeadDim)) return e;
+  P.q_rot = pc.d_q_rot;
   P.items = pc.d_items;
-  P.members = pc.d_members;
   P.part_o = pc.d_part_o;
   P.part_ml = pc.d_part_ml;
   P.kv_heads = cfg.kv_heads;
@@ -692,12 +715,36 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   P.gqa = gqa;
   P.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
   P.rope = st.rope();
-  MV_CUDA_TRY(cudaMemsetAsync(pc.d_counter, 0, sizeof(int), stream));
+  {
+    const char* dg = getenv("MV_DECODE_DIAG");
+    P.diag = dg ? atoi(dg) : 0;
+    P.trace = nullptr;
+    if (getenv("MV_DECODE_TRACE")) {
+      if (!pc.d_trace) MV_CUDA_TRY(cudaMalloc(&pc.d_trace, sizeof(unsigned long long) * 148 * 64 * 4 * 2));
+      MV_CUDA_TRY(cudaMemsetAsync(pc.d_trace, 0, sizeof(unsigned long long) * 148 * 64 * 4 * 2, stream));
+      P.trace = pc.d_trace;
+    }
+  }
+  {
+    const int64_t chunks = (int64_t)n * q_heads * 16;
+    rope_q_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(
+        (const __nv_bfloat16*)d_q, d_positions, n, q_heads, st.rope(), pc.d_q_rot, pc.d_counter);
+    MV_LAUNCH_CHECK();
+  }
   P.work_counter = pc.d_counter;
   P.n_work = (int)pc.items.size() * cfg.kv_heads;
   const int grid = std::min(P.n_work, pc.num_sms);
   decode_kernel<<<grid, kDecThreads, kDecSmem, stream>>>(P);
   MV_LAUNCH_CHECK();
+  if (P.trace) {
+    std::vector<unsigned long long> h(148 * 64 * 4);
+    MV_CUDA_TRY(cudaMemcpyAsync(h.data(), pc.d_trace, h.size() * 8, cudaMemcpyDeviceToHost, stream));
+    MV_CUDA_TRY(cudaStreamSynchronize(stream));
+    if (FILE* f = fopen(getenv("MV_DECODE_TRACE"), "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   const int warps = n * q_heads;
   combine_kernel<<<(warps + 7) / 8, 256, 0, stream>>>(pc.d_part_o, pc.d_part_ml, pc.d_slot_ptr, pc.d_slot_idx, n,
                                                       q_heads, d_out, out_dtype == 1);
