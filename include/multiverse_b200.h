@@ -219,14 +219,15 @@ MV_API mv_status mv_attn_decode_plan_info(mv_kv_store* s, mv_decode_plan_info* o
  * Replaces the attention inside ToyModel::forward (toy_model.cpp:174-202) for a whole
  * structured sequence at once:
  *   d_q bf16[n][q_heads][128], d_k / d_v bf16[n][kv_heads][128] (pre-RoPE, rotated in
- *   kernel at d_positions), d_excl from mv_visibility, d_out bf16[n][q_heads][128].
+ *   kernel at d_positions), d_excl from mv_visibility, d_out [n][q_heads][128] bf16
+ *   (out_dtype 0) or fp32 (out_dtype 1).
  * Fully masked cross-branch tiles are skipped using the tile map.
  */
 MV_API size_t mv_prefill_workspace_size(int32_t n, int32_t q_heads, int32_t kv_heads);
 MV_API mv_status mv_attn_prefill(const void* d_q, const void* d_k, const void* d_v, const int32_t* d_positions,
                           const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
-                          double rope_base, void* d_out, void* d_workspace, size_t workspace_bytes,
-                          mv_stream_t stream);
+                          double rope_base, void* d_out, int32_t out_dtype, void* d_workspace,
+                          size_t workspace_bytes, mv_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -127,14 +127,15 @@ def attn_decode(q, K, V, ctx_lists, nthreads: int | None = None) -> np.ndarray:
     return out
 
 
-def attn_prefill(q, K, V, excl, rows, nthreads: int | None = None) -> np.ndarray:
-    """q [n,Hq,D], K/V [n,Hkv,D] post-RoPE fp64; excl [n,D_excl,2] int32; rows: query rows."""
-    q = np.ascontiguousarray(q, np.float64)
+def attn_prefill(q_rows, K, V, excl, rows, nthreads: int | None = None) -> np.ndarray:
+    """q_rows [len(rows),Hq,D] (post-RoPE queries of the sampled rows), K/V [n,Hkv,D] post-RoPE fp64;
+    excl [n,D_excl,2] int32; rows: the sampled query row indices. Returns [len(rows),Hq,D]."""
+    q = np.ascontiguousarray(q_rows, np.float64)
     K = np.ascontiguousarray(K, np.float64)
     V = np.ascontiguousarray(V, np.float64)
     ex = np.ascontiguousarray(excl, np.int32)
     r = np.ascontiguousarray(rows, np.int32)
-    n, hq, dh = q.shape
+    _, hq, dh = q.shape
     out = np.zeros((len(r), hq, dh), np.float64)
     lib().mvo_attn_prefill(_p(q), _p(K), _p(V), hq, K.shape[1], dh, _p(ex), ex.shape[1], _p(r), len(r), _p(out),
                            nthreads or threads())

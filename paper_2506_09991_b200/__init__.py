@@ -81,7 +81,7 @@ def _load():
         "mv_attn_decode": ([P, i32, P, i32, i32, P, P, P, i32], ctypes.c_int),
         "mv_attn_decode_plan_info": ([P, P], ctypes.c_int),
         "mv_prefill_workspace_size": ([i32, i32, i32], sz),
-        "mv_attn_prefill": ([P, P, P, P, P, i32, i32, i32, i32, ctypes.c_double, P, P, sz, P], ctypes.c_int),
+        "mv_attn_prefill": ([P, P, P, P, P, i32, i32, i32, i32, ctypes.c_double, P, i32, P, sz, P], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)

@@ -23,15 +23,18 @@ def decode(store: PagedStore, handles, q: torch.Tensor, positions: torch.Tensor,
 
 
 def prefill(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, positions: torch.Tensor, excl: torch.Tensor,
-            rope_base: float = 10000.0, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None):
+            rope_base: float = 10000.0, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+            out_dtype: torch.dtype = torch.bfloat16):
     """q bf16 [n, Hq, 128]; k, v bf16 [n, Hkv, 128] (pre-RoPE); excl int32 [n, D, 2] from dag.build_visibility."""
     n, hq, d = q.shape
     hkv = k.shape[1]
-    out = torch.empty_like(q) if out is None else out
+    if out is None:
+        out = torch.empty(q.shape, dtype=out_dtype, device=q.device)
+    code = {torch.bfloat16: 0, torch.float32: 1}[out.dtype]
     ws_bytes = lib.mv_prefill_workspace_size(n, hq, hkv)
     if workspace is None or workspace.numel() < ws_bytes:
         workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=q.device)
     check(lib.mv_attn_prefill(_p(q), _p(k), _p(v), _p(positions), _p(excl), excl.shape[1], n, hq, hkv, rope_base,
-                              _p(out), _p(workspace), ws_bytes,
+                              _p(out), code, _p(workspace), ws_bytes,
                               ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
     return out

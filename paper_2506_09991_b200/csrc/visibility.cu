@@ -352,7 +352,7 @@ __global__ void tile_map_kernel(const int32_t* __restrict__ excl, int n, int D, 
           }
         }
         empty = vis == 0;
-        full = !touches && (j1 - 1 <= i);
+        full = !touches && (j1 - 1 <= i) && (j0 + tile <= n);  // tail tiles hold padding tokens
         vis_total += (unsigned long long)vis;
       }
     } else {
