@@ -12,7 +12,9 @@
 //      listed k tiles are visited, the element mask is evaluated only on partial tiles.
 //      K/V tiles stream through a cp.async double buffer (XOR-swizzled rows, conflict-free
 //      ldmatrix); S and P stay in registers (FA2 fragment reuse); online softmax in log2 domain.
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "tc_common.cuh"
 
@@ -257,262 +259,14 @@ __global__ void __launch_bounds__(kPfThreads) prefill_kernel(PrefillParams P) {
   }
 }
 
-// ===========================================================================
-// v1: tcgen05 / TMEM / TMA kernel (one CTA per (128-row q tile, q head))
-// ===========================================================================
-//   warp 0      TMA: Q tile once, then K and V tiles of every listed k tile into a 2-stage ring
-//               (SW128 K-major halves via 3-D tensor maps; OOB rows zero-filled).
-//   warp 1      MMA (one thread): S[b] = Q.K^T (M=128, N=128, 8 x K16) into TMEM, double-
-//               buffered, then O += P.V (P from smem K-major, V MN-major) one tile behind.
-//   warps 4-7   softmax: thread = query row = TMEM lane; S row via tcgen05.ld, interval mask on
-//               partial tiles, lazy O rescale in TMEM (only when the row max grows by > 2^8),
-//               P as bf16 into SW128 smem; epilogue O / l straight from TMEM.
-constexpr int kTM = 128, kTN = 128;
-constexpr int kTcStages = 2;
-constexpr int kTcThreads = 256;
-constexpr int kHalf = kTM * 128;                      // one SW128 half tile: 128 rows x 128 B
-constexpr int kTile = 2 * kHalf;                      // 32 KiB
-constexpr int kOffQ = 0;
-constexpr int kOffK = kOffQ + kTile;
-constexpr int kOffV = kOffK + kTcStages * kTile;
-constexpr int kOffP = kOffV + kTcStages * kTile;
-constexpr int kOffBarTc = kOffP + 2 * kTile;
-constexpr int kTcSmem = kOffBarTc + 256 + 1024;       // barriers + alignment slack
-constexpr uint32_t kIdescQK = tc::idesc_bf16(128, 128, 0, 0);
-constexpr uint32_t kIdescPV = tc::idesc_bf16(128, 128, 0, 1);
-
-struct TcParams {
-  const int32_t* excl;
-  const int32_t* tcount;
-  const int32_t* tlist;
-  void* out;
-  int out_f32;
-  int n, hq, hkv, D, n_qt;
-  float scale_log2;
-};
-
-__global__ void __launch_bounds__(kTcThreads, 1)
-    prefill_tc_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                      const __grid_constant__ CUtensorMap map_v, TcParams P) {
-  extern __shared__ uint8_t tc_smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tc_smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBarTc);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
-  uint64_t* kv_empty = kv_full + kTcStages;
-  uint64_t* s_full = kv_empty + kTcStages;
-  uint64_t* s_free = s_full + 2;
-  uint64_t* p_full = s_free + 2;
-  uint64_t* p_free = p_full + 2;
-  uint64_t* o_done = p_free + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
-
-  const int qt = P.n_qt - 1 - blockIdx.x;  // heaviest (late) q tiles first
-  const int h = blockIdx.y;
-  const int kvh = h / (P.hq / P.hkv);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cnt = P.tcount[qt];
-  const int32_t* lst = P.tlist + (size_t)qt * P.n_qt;
-
-  if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    for (int s = 0; s < kTcStages; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&s_free[b], 128);
-      mbar_init(&p_full[b], 128);
-      mbar_init(&p_free[b], 1);
-    }
-    mbar_init(o_done, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
-  tc::fence_before();
-  __syncthreads();
-  tc::fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      tc::tma_prefetch_desc(&map_q);
-      tc::tma_prefetch_desc(&map_k);
-      tc::tma_prefetch_desc(&map_v);
-      mbar_arrive_expect_tx(q_full, kTile);
-      tc::tma_load_3d(smem + kOffQ, &map_q, 0, h, qt * kTM, q_full);
-      tc::tma_load_3d(smem + kOffQ + kHalf, &map_q, 64, h, qt * kTM, q_full);
-      for (int it = 0; it < cnt; ++it) {
-        const int s = it % kTcStages;
-        if (it >= kTcStages) mbar_wait(&kv_empty[s], ((it / kTcStages) - 1) & 1);
-        const int kt = lst[it] & 0xFFFF;
-        mbar_arrive_expect_tx(&kv_full[s], 2 * kTile);
-        uint8_t* kd = smem + kOffK + s * kTile;
-        uint8_t* vd = smem + kOffV + s * kTile;
-        tc::tma_load_3d(kd, &map_k, 0, kvh, kt * kTN, &kv_full[s]);
-        tc::tma_load_3d(kd + kHalf, &map_k, 64, kvh, kt * kTN, &kv_full[s]);
-        tc::tma_load_3d(vd, &map_v, 0, kvh, kt * kTN, &kv_full[s]);
-        tc::tma_load_3d(vd + kHalf, &map_v, 64, kvh, kt * kTN, &kv_full[s]);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t q_base = smem_u32(smem + kOffQ);
-      auto pv = [&](int j) {
-        const int b = j & 1, s = j % kTcStages;
-        mbar_wait(&p_full[b], (j >> 1) & 1);
-        tc::fence_after();
-        const uint32_t p_base = smem_u32(smem + kOffP + b * kTile);
-        const uint32_t v_base = smem_u32(smem + kOffV + s * kTile);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {  // 16 tokens per MMA
-          const uint64_t ad = tc::sw128_desc(p_base + (k >> 2) * kHalf + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = tc::sw128_desc(v_base + k * 2048, kHalf, 1024);
-          tc::mma_ss(tmem + 256, ad, bd, kIdescPV, (j > 0 || k > 0) ? 1u : 0u);
-        }
-        tc::mma_commit(&p_free[b]);
-        tc::mma_commit(&kv_empty[s]);
-        tc::mma_commit(o_done);
-      };
-      mbar_wait(q_full, 0);
-      tc::fence_after();
-      for (int it = 0; it < cnt; ++it) {
-        const int b = it & 1, s = it % kTcStages;
-        mbar_wait(&kv_full[s], (it / kTcStages) & 1);
-        if (it >= 2) mbar_wait(&s_free[b], ((it >> 1) - 1) & 1);
-        tc::fence_after();
-        const uint32_t k_base = smem_u32(smem + kOffK + s * kTile);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {  // 16 dims per MMA
-          const uint32_t off = (k >> 2) * kHalf + (k & 3) * 32;
-          const uint64_t ad = tc::sw128_desc(q_base + off, 16, 1024);
-          const uint64_t bd = tc::sw128_desc(k_base + off, 16, 1024);
-          tc::mma_ss(tmem + b * 128, ad, bd, kIdescQK, k > 0 ? 1u : 0u);
-        }
-        tc::mma_commit(&s_full[b]);
-        if (it >= 1) pv(it - 1);
-      }
-      if (cnt > 0) pv(cnt - 1);
-    }
-  } else if (warp >= 4) {
-    // ---------------- softmax warpgroup: one query row per thread ----------------
-    const int r = (warp - 4) * 32 + lane;
-    const int i = qt * kTM + r;
-    const uint32_t lane_addr = tmem + ((uint32_t)((warp - 4) * 32) << 16);
-    int elo[kMaxD], ehi[kMaxD];
-#pragma unroll
-    for (int q = 0; q < kMaxD; ++q) {
-      elo[q] = ehi[q] = 0;
-      if (q < P.D && i < P.n) {
-        elo[q] = P.excl[((size_t)i * P.D + q) * 2];
-        ehi[q] = P.excl[((size_t)i * P.D + q) * 2 + 1];
-      }
-    }
-    float m_ref = -INFINITY, l = 0.f;
-    for (int it = 0; it < cnt; ++it) {
-      const int b = it & 1;
-      const int entry = lst[it];
-      const int j0 = (entry & 0xFFFF) * kTN;
-      const bool partial = (entry >> 30) & 1;
-      mbar_wait(&s_full[b], (it >> 1) & 1);
-      tc::fence_after();
-      float x[kTN];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tmem_ld32(lane_addr + b * 128 + c * 32, x + c * 32);
-      tc::tmem_wait_ld();
-      tc::fence_before();
-      mbar_arrive(&s_free[b]);
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < kTN; ++c) {
-        float v = x[c] * P.scale_log2;
-        if (partial) {
-          const int j = j0 + c;
-          bool vis = j <= i && j < P.n;
-#pragma unroll
-          for (int q = 0; q < kMaxD; ++q) vis = vis && !(j >= elo[q] && j < ehi[q]);
-          if (!vis) v = -INFINITY;
-        }
-        x[c] = v;
-        mx = fmaxf(mx, v);
-      }
-      const bool need = mx > m_ref + kLazyRescalePf;
-      if (__any_sync(0xffffffffu, need)) {
-        const float nref = need ? fmaxf(m_ref, mx) : m_ref;
-        const float alpha = need ? fast_exp2(m_ref - nref) : 1.f;  // m_ref = -inf -> 0 (O is still 0)
-        if (it >= 1) {
-          mbar_wait(o_done, (it - 1) & 1);  // PV(it-1) has landed in O
-          tc::fence_after();
-#pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            float o[32];
-            tc::tmem_ld32(lane_addr + 256 + c * 32, o);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= alpha;
-            tc::tmem_st32(lane_addr + 256 + c * 32, o);
-          }
-          tc::tmem_wait_st();
-        }
-        l *= alpha;
-        m_ref = nref;
-      }
-      const float mu = m_ref == -INFINITY ? 0.f : m_ref;
-      if (it >= 2) mbar_wait(&p_free[b], ((it >> 1) - 1) & 1);
-      uint8_t* prow = smem + kOffP + b * kTile + r * 128;
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {  // 8 tokens per 16 B chunk
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float p0 = fast_exp2(x[c * 8 + 2 * e] - mu), p1 = fast_exp2(x[c * 8 + 2 * e + 1] - mu);
-          l += p0 + p1;
-          w[e] = pack_bf16(p0, p1);
-        }
-        const int half = c >> 3, ch = c & 7;
-        *reinterpret_cast<uint4*>(prow + half * kHalf + ((ch ^ (r & 7)) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
-      }
-      tc::fence_proxy_async();
-      mbar_arrive(&p_full[b]);
-    }
-    // epilogue: O / l from TMEM
-    // s_full(cnt-1) already implied PV(cnt-3) landed; step through the last two o_done phases so a
-    // parity wait can never match an older phase.
-    if (cnt >= 2) mbar_wait(o_done, (cnt - 2) & 1);
-    if (cnt >= 1) mbar_wait(o_done, (cnt - 1) & 1);
-    tc::fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      float o[32];
-      tc::tmem_ld32(lane_addr + 256 + c * 32, o);
-      tc::tmem_wait_ld();
-      if (i < P.n) {
-        if (P.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + h) * kHeadDim + c * 32);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + ((size_t)i * P.hq + h) * kHeadDim + c * 32);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
-                                pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
-        }
-      }
-    }
-    tc::fence_before();
-  }
-  __syncthreads();
-  if (warp == 1) {
-    tc::fence_after();
-    tc::tmem_dealloc(tmem, 512);
-  }
-}
-
 }  // namespace
 }  // namespace mv
+
+namespace mv {
+mv_status prefill_tc2_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
+                             const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
+                             void* d_out, int32_t out_dtype, int32_t* tcount, int32_t* tlist, cudaStream_t st);
+}
 
 using namespace mv;
 
@@ -557,35 +311,9 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
   MV_LAUNCH_CHECK();
   MV_CUDA_TRY(cudaMemsetAsync(vis, 0, 8, st));
 
-  if (!getenv("MV_PREFILL_V0")) {
-    // v1: tcgen05 path (tile map at 128)
-    const int n_qt128 = (n + kTM - 1) / kTM;
-    if (mv_status e = mv_tile_map(d_excl, n, max_depth, kTN, tcount, tlist, vis, stream)) return e;
-    CUtensorMap mq, mk, mvv;
-    if (mv_status e = tc::make_rows_map(&mq, q_rot, n, q_heads, kTM)) return e;
-    if (mv_status e = tc::make_rows_map(&mk, k_rot, n, kv_heads, kTN)) return e;
-    if (mv_status e = tc::make_rows_map(&mvv, d_v, n, kv_heads, kTN)) return e;
-    TcParams T;
-    T.excl = d_excl;
-    T.tcount = tcount;
-    T.tlist = tlist;
-    T.out = d_out;
-    T.out_f32 = out_dtype == 1;
-    T.n = n;
-    T.hq = q_heads;
-    T.hkv = kv_heads;
-    T.D = max_depth;
-    T.n_qt = n_qt128;
-    T.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
-    static bool tc_attr = false;
-    if (!tc_attr) {
-      MV_CUDA_TRY(cudaFuncSetAttribute(prefill_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTcSmem));
-      tc_attr = true;
-    }
-    prefill_tc_kernel<<<dim3(n_qt128, q_heads), kTcThreads, kTcSmem, st>>>(mq, mk, mvv, T);
-    MV_LAUNCH_CHECK();
-    return MV_OK;
-  }
+  if (!getenv("MV_PREFILL_V0"))  // tcgen05 path (prefill_tc.cu); v0 kept only for A/B diagnostics
+    return prefill_tc2_launch(q_rot, k_rot, (const __nv_bfloat16*)d_v, d_excl, max_depth, n, q_heads, kv_heads, d_out,
+                              out_dtype, tcount, tlist, st);
   if (mv_status e = mv_tile_map(d_excl, n, max_depth, kBN, tcount, tlist, vis, stream)) return e;
   PrefillParams P;
   P.q = q_rot;

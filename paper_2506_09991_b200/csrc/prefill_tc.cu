@@ -1,0 +1,358 @@
+// prefill_tc.cu — K3 v2: branch-masked prefill on the 5th-gen tensor cores (tcgen05 / TMEM / TMA).
+//
+// One CTA per (256-row query pair, q head); the pair is two 128-row tiles A and B that share
+// every K/V tile, so one MMA thread can ping-pong between them while two softmax warpgroups
+// work (the FlashAttention-4 schedule):
+//
+//   warp 0   TMA  : lane 0 loads Q_A, Q_B once, then K tiles; lane 1 loads V tiles (separate
+//                   rings: K frees after Q.K^T, V only after P.V)
+//   warp 1   MMA  : one thread.  Loop over the pair's k tiles j:
+//                     PV_A(j); QK_A(j+1); PV_B(j); QK_B(j+1)
+//                   S_X = Q_X.K^T (M=128, N=128, 8 x K16, SS operands from SW128 smem) into TMEM;
+//                   O_X += P_X.V with P_X read straight from TMEM (TS operand, aliasing S_X)
+//   warps 2-5 softmax A, warps 6-9 softmax B : thread = query row = TMEM lane.  S row by
+//                   tcgen05.ld, interval mask on partial tiles (128-bit row mask built once per
+//                   tile), lazy O rescale in TMEM only when the row max grows by > 2^8, P as packed
+//                   bf16 back into the S columns by tcgen05.st.  Epilogue O / l from TMEM.
+//
+// TMEM (512 columns): S/P_A 0..127, S/P_B 128..255, O_A 256..383, O_B 384..511.
+// Ordering facts the schedule relies on: tcgen05.mma ops of one thread execute in issue order,
+// so QK_X(j+1) (which overwrites S/P_X) cannot overtake PV_X(j) (which reads P_X), and the
+// commit after QK_X(j+1) also certifies PV_X(j) -> the softmax may rescale O_X after s_full.
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "tc_common.cuh"
+
+namespace mv {
+
+mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
+                    int32_t stride, cudaStream_t stream);
+
+namespace {
+
+constexpr int kT = 128;          // rows per q tile, tokens per k tile
+constexpr int kKSt = 3;          // K ring stages
+constexpr int kVSt = 2;          // V ring stages
+constexpr int kThreads2 = 320;   // 10 warps
+constexpr int kHalf2 = kT * 128;  // SW128 half tile (128 rows x 128 B)
+constexpr int kTile2 = 2 * kHalf2;
+constexpr int kOffQA = 0;
+constexpr int kOffQB = kOffQA + kTile2;
+constexpr int kOffK2 = kOffQB + kTile2;
+constexpr int kOffV2 = kOffK2 + kKSt * kTile2;
+constexpr int kOffBar2 = kOffV2 + kVSt * kTile2;
+constexpr int kSmem2 = kOffBar2 + 256 + 1024;
+constexpr uint32_t kIdQK = tc::idesc_bf16(128, 128, 0, 0);
+constexpr uint32_t kIdPV = tc::idesc_bf16(128, 128, 0, 1);
+constexpr int kMaxD2 = 8;
+constexpr float kLazy2 = 8.f;
+
+struct Tc2Params {
+  const int32_t* excl;
+  const int32_t* tcount;
+  const int32_t* tlist;
+  void* out;
+  int out_f32;
+  int n, hq, hkv, D, n_qp, stride;
+  float scale_log2;
+};
+
+__global__ void __launch_bounds__(kThreads2, 1)
+    prefill_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_v, Tc2Params P) {
+  extern __shared__ uint8_t smem_raw2[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw2) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar2);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = q_full + 1;
+  uint64_t* k_empty = k_full + kKSt;
+  uint64_t* v_full = k_empty + kKSt;
+  uint64_t* v_empty = v_full + kVSt;
+  uint64_t* s_full = v_empty + kVSt;  // [2]: tile A, B
+  uint64_t* p_full = s_full + 2;      // [2]
+  uint64_t* o_fin = p_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_fin + 2);
+
+  const int qp = P.n_qp - 1 - blockIdx.x;  // heaviest pairs first
+  const int h = blockIdx.y;
+  const int kvh = h / (P.hq / P.hkv);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cnt = P.tcount[qp];
+  const int32_t* lst = P.tlist + (size_t)qp * P.stride;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kKSt; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kVSt; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(&s_full[x], 1);
+      mbar_init(&p_full[x], 128);
+      mbar_init(&o_fin[x], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane < 2) {
+      const bool is_k = lane == 0;
+      const CUtensorMap* map = is_k ? &map_k : &map_v;
+      const int nst = is_k ? kKSt : kVSt;
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      uint8_t* ring = smem + (is_k ? kOffK2 : kOffV2);
+      tc::tma_prefetch_desc(map);
+      if (is_k) {
+        tc::tma_prefetch_desc(&map_q);
+        mbar_arrive_expect_tx(q_full, 2 * kTile2);
+        tc::tma_load_3d(smem + kOffQA, &map_q, 0, h, qp * 256, q_full);
+        tc::tma_load_3d(smem + kOffQA + kHalf2, &map_q, 64, h, qp * 256, q_full);
+        tc::tma_load_3d(smem + kOffQB, &map_q, 0, h, qp * 256 + kT, q_full);
+        tc::tma_load_3d(smem + kOffQB + kHalf2, &map_q, 64, h, qp * 256 + kT, q_full);
+      }
+      for (int it = 0; it < cnt; ++it) {
+        const int s = it % nst;
+        if (it >= nst) mbar_wait(&empty[s], ((it / nst) - 1) & 1);
+        const int kt = lst[it] & 0xFFFFF;
+        mbar_arrive_expect_tx(&full[s], kTile2);
+        tc::tma_load_3d(ring + s * kTile2, map, 0, kvh, kt * kT, &full[s]);
+        tc::tma_load_3d(ring + s * kTile2 + kHalf2, map, 64, kvh, kt * kT, &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t qa = smem_u32(smem + kOffQA), qb = smem_u32(smem + kOffQB);
+      auto qk = [&](int x, int j) {  // S_x = Q_x . K(j)^T
+        const int s = j % kKSt;
+        const uint32_t kb = smem_u32(smem + kOffK2 + s * kTile2);
+        const uint32_t qbase = x ? qb : qa;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t off = (k >> 2) * kHalf2 + (k & 3) * 32;
+          tc::mma_ss(tmem + x * 128, tc::sw128_desc(qbase + off, 16, 1024), tc::sw128_desc(kb + off, 16, 1024), kIdQK,
+                     k > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(&s_full[x]);
+      };
+      auto pv = [&](int x, int j) {  // O_x += P_x(tmem) . V(j)
+        const int s = j % kVSt;
+        const uint32_t vb = smem_u32(smem + kOffV2 + s * kTile2);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          tc::mma_ts(tmem + 256 + x * 128, tmem + x * 128 + k * 8, tc::sw128_desc(vb + k * 2048, kHalf2, 1024), kIdPV,
+                     (j > 0 || k > 0) ? 1u : 0u);
+      };
+      mbar_wait(q_full, 0);
+      if (cnt > 0) {
+        mbar_wait(&k_full[0], 0);
+        tc::fence_after();
+        qk(0, 0);
+        qk(1, 0);
+        tc::mma_commit(&k_empty[0]);
+      }
+      for (int j = 0; j < cnt; ++j) {
+        mbar_wait(&v_full[j % kVSt], (j / kVSt) & 1);
+        mbar_wait(&p_full[0], j & 1);
+        tc::fence_after();
+        pv(0, j);
+        const bool more = j + 1 < cnt;
+        if (more) {
+          mbar_wait(&k_full[(j + 1) % kKSt], ((j + 1) / kKSt) & 1);
+          tc::fence_after();
+          qk(0, j + 1);
+        } else {
+          tc::mma_commit(&o_fin[0]);
+        }
+        mbar_wait(&p_full[1], j & 1);
+        tc::fence_after();
+        pv(1, j);
+        tc::mma_commit(&v_empty[j % kVSt]);
+        if (more) {
+          qk(1, j + 1);
+          tc::mma_commit(&k_empty[(j + 1) % kKSt]);
+        } else {
+          tc::mma_commit(&o_fin[1]);
+        }
+      }
+    }
+  } else {
+    // ---------------- softmax warpgroups: warps 2-5 -> tile A, 6-9 -> tile B ----------------
+    const int x = (warp - 2) >> 2;            // tile
+    const int quarter = warp & 3;             // TMEM lane quarter this warp may access
+    const int r = quarter * 32 + lane;        // row within the tile
+    const int i = qp * 256 + x * kT + r;      // sequence row
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    const uint32_t s_col = x * 128, o_col = 256 + x * 128;
+    int elo[kMaxD2], ehi[kMaxD2];
+#pragma unroll
+    for (int q = 0; q < kMaxD2; ++q) {
+      elo[q] = ehi[q] = 0;
+      if (q < P.D && i < P.n) {
+        elo[q] = P.excl[((size_t)i * P.D + q) * 2];
+        ehi[q] = P.excl[((size_t)i * P.D + q) * 2 + 1];
+      }
+    }
+    float m_ref = -INFINITY, l = 0.f;
+    for (int j = 0; j < cnt; ++j) {
+      const int entry = lst[j];
+      const int j0 = (entry & 0xFFFFF) * kT;
+      const int status = (entry >> (20 + 2 * x)) & 3;  // 0 skip, 1 full, 2 partial
+      mbar_wait(&s_full[x], j & 1);
+      tc::fence_after();
+      float v[kT];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tc::tmem_ld32(lane_base + s_col + c * 32, v + c * 32);
+      tc::tmem_wait_ld();
+      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+      if (status != 1) {
+        uint32_t vm[4];
+        const int lim = status == 0 ? -1 : min(i, P.n - 1) - j0;  // last visible column
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int lo = w * 32;
+          vm[w] = lim < lo ? 0u : (lim >= lo + 31 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (31 - (lim - lo))));
+        }
+#pragma unroll
+        for (int q = 0; q < kMaxD2; ++q) {
+          const int a = max(elo[q] - j0, 0), e = min(ehi[q] - j0, kT);
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int lo = max(a - w * 32, 0), hi = min(e - w * 32, 32);
+            if (hi > lo) vm[w] &= ~((hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << lo);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < kT; c += 4) {
+          const uint32_t m = vm[c >> 5] >> (c & 31);
+          v[c] = (m & 1u) ? v[c] : -INFINITY;
+          v[c + 1] = (m & 2u) ? v[c + 1] : -INFINITY;
+          v[c + 2] = (m & 4u) ? v[c + 2] : -INFINITY;
+          v[c + 3] = (m & 8u) ? v[c + 3] : -INFINITY;
+          mx0 = fmaxf(mx0, v[c]); mx1 = fmaxf(mx1, v[c + 1]); mx2 = fmaxf(mx2, v[c + 2]); mx3 = fmaxf(mx3, v[c + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < kT; c += 4) {
+          mx0 = fmaxf(mx0, v[c]); mx1 = fmaxf(mx1, v[c + 1]); mx2 = fmaxf(mx2, v[c + 2]); mx3 = fmaxf(mx3, v[c + 3]);
+        }
+      }
+      // raw-score max; scaled into the log2 domain once (scale > 0 preserves order)
+      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * P.scale_log2;
+      const bool need = mx > m_ref + kLazy2;
+      if (__any_sync(0xffffffffu, need)) {
+        const float nref = need ? fmaxf(m_ref, mx) : m_ref;
+        const float alpha = need ? fast_exp2(m_ref - nref) : 1.f;
+        if (j >= 1) {  // s_full(j) certified PV_x(j-1): O_x is final for tiles < j
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            float o[32];
+            tc::tmem_ld32(lane_base + o_col + c * 32, o);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] *= alpha;
+            tc::tmem_st32(lane_base + o_col + c * 32, o);
+          }
+        }
+        l *= alpha;
+        m_ref = nref;
+      }
+      const float mu = m_ref == -INFINITY ? 0.f : m_ref;
+      float l0 = 0.f, l1 = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {
+        const float p0 = fast_exp2(fmaf(v[2 * c], P.scale_log2, -mu));
+        const float p1 = fast_exp2(fmaf(v[2 * c + 1], P.scale_log2, -mu));
+        l0 += p0;
+        l1 += p1;
+        pk[c] = pack_bf16(p0, p1);
+      }
+      l += l0 + l1;
+      tc::tmem_st32u(lane_base + s_col, pk);
+      tc::tmem_st32u(lane_base + s_col + 32, pk + 32);
+      tc::tmem_wait_st();
+      tc::fence_before();
+      mbar_arrive(&p_full[x]);
+    }
+    // epilogue
+    if (cnt > 0) mbar_wait(&o_fin[x], 0);
+    tc::fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      float o[32];
+      tc::tmem_ld32(lane_base + o_col + c * 32, o);
+      tc::tmem_wait_ld();
+      if (i < P.n) {
+        if (P.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + h) * kHeadDim + c * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + ((size_t)i * P.hq + h) * kHeadDim + c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
+                                pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
+        }
+      }
+    }
+    tc::fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+// Launches the v2 kernel on rotated q/k and the caller's v (all [n][heads][128] bf16).
+mv_status prefill_tc2_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
+                             const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
+                             void* d_out, int32_t out_dtype, int32_t* tcount, int32_t* tlist, cudaStream_t st) {
+  if (max_depth > kMaxD2) return fail(MV_ERR_INVALID_ARGUMENT, "prefill: max_depth > 8");
+  const int n_qp = (n + 255) / 256;
+  const int stride = (n + kT - 1) / kT;
+  if (mv_status e = tile_map2(d_excl, n, max_depth, tcount, tlist, stride, st)) return e;
+  CUtensorMap mq, mk, mvv;
+  if (mv_status e = tc::make_rows_map(&mq, q_rot, n, q_heads, kT)) return e;
+  if (mv_status e = tc::make_rows_map(&mk, k_rot, n, kv_heads, kT)) return e;
+  if (mv_status e = tc::make_rows_map(&mvv, v, n, kv_heads, kT)) return e;
+  Tc2Params T;
+  T.excl = d_excl;
+  T.tcount = tcount;
+  T.tlist = tlist;
+  T.out = d_out;
+  T.out_f32 = out_dtype == 1;
+  T.n = n;
+  T.hq = q_heads;
+  T.hkv = kv_heads;
+  T.D = max_depth;
+  T.n_qp = n_qp;
+  T.stride = stride;
+  T.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
+  static bool attr = false;
+  if (!attr) {
+    MV_CUDA_TRY(cudaFuncSetAttribute(prefill_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
+    attr = true;
+  }
+  prefill_tc2_kernel<<<dim3(n_qp, q_heads), kThreads2, kSmem2, st>>>(mq, mk, mvv, T);
+  MV_LAUNCH_CHECK();
+  return MV_OK;
+}
+
+}  // namespace mv

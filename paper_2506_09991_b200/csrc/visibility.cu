@@ -379,6 +379,71 @@ __global__ void tile_map_kernel(const int32_t* __restrict__ excl, int n, int D, 
   }
 }
 
+
+// Paired tile map for the tcgen05 prefill: one CTA per 256-row q pair (2 x 128-row tiles A and
+// B), one thread per row; for every 128-token k tile it records the status of each half
+// (0 skip, 1 full, 2 partial) and keeps the tile when either half needs it:
+//   list[qp][k] = kt | statusA << 20 | statusB << 22.
+__global__ void tile_map2_kernel(const int32_t* __restrict__ excl, int n, int D, int32_t* __restrict__ count,
+                                 int32_t* __restrict__ list, int stride) {
+  const int qp = blockIdx.x;
+  const int tile = 128;
+  const int i = qp * 256 + threadIdx.x;
+  const bool row_ok = i < n;
+  int lo[8], hi[8];
+  int nd = 0;
+  if (row_ok) {
+    for (int q = 0; q < D && q < 8; ++q) {
+      int a = excl[((int64_t)i * D + q) * 2], b = excl[((int64_t)i * D + q) * 2 + 1];
+      if (a < b) { lo[nd] = a; hi[nd] = b; ++nd; }
+    }
+  }
+  __shared__ int s_flags[2][8];
+  const int half = threadIdx.x >> 7;
+  const int last_kt = min((qp * 256 + 255) / tile, (n - 1) / tile);
+  int written = 0;
+  for (int kt = 0; kt <= last_kt; ++kt) {
+    const int j0 = kt * tile, j1 = min(n, j0 + tile);
+    bool empty = true, full = true;
+    if (row_ok) {
+      const int lastc = min(j1 - 1, i);
+      if (j0 > i) {
+        full = false;
+      } else {
+        int vis = lastc - j0 + 1;
+        bool touches = false;
+        for (int q = 0; q < nd; ++q) {
+          int a = max(lo[q], j0), b = min(hi[q], lastc + 1);
+          if (a < b) { vis -= b - a; touches = true; }
+        }
+        empty = vis == 0;
+        full = !touches && (j1 - 1 <= i) && (j0 + tile <= n);
+      }
+    }
+    // per-half votes (4 warps per half)
+    const unsigned e = __ballot_sync(0xffffffffu, empty), f = __ballot_sync(0xffffffffu, full);
+    if ((threadIdx.x & 31) == 0) {
+      s_flags[0][threadIdx.x >> 5] = e == 0xffffffffu;
+      s_flags[1][threadIdx.x >> 5] = f == 0xffffffffu;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int st[2];
+      for (int hh = 0; hh < 2; ++hh) {
+        bool all_e = true, all_f = true;
+        for (int w = 0; w < 4; ++w) { all_e &= s_flags[0][hh * 4 + w] != 0; all_f &= s_flags[1][hh * 4 + w] != 0; }
+        st[hh] = all_e ? 0 : (all_f ? 1 : 2);
+      }
+      if (st[0] || st[1]) list[(int64_t)qp * stride + written] = kt | (st[0] << 20) | (st[1] << 22);
+      s_flags[0][0] = st[0] || st[1];
+    }
+    __syncthreads();
+    if (s_flags[0][0]) ++written;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) count[qp] = written;
+  (void)half;
+}
 }  // namespace
 }  // namespace mv
 
@@ -434,3 +499,13 @@ extern "C" mv_status mv_tile_map(const int32_t* d_excl, int32_t n, int32_t max_d
   MV_LAUNCH_CHECK();
   return MV_OK;
 }
+
+namespace mv {
+mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
+                    int32_t stride, cudaStream_t stream) {
+  const int n_qp = (n + 255) / 256;
+  tile_map2_kernel<<<n_qp, 256, 0, stream>>>(d_excl, n, max_depth, d_count, d_list, stride);
+  MV_LAUNCH_CHECK();
+  return MV_OK;
+}
+}  // namespace mv
