@@ -21,4 +21,5 @@ for f in dag grammar kvcache synth tokenizer toy_model engine; do
 done
 wait
 $CXX $FLAGS "$HERE/refdrv.cpp" "${objs[@]}" -o "$OUT/refdrv"
+rm -rf "$OUT/src"  # patched copies were build inputs only
 echo "built $OUT/refdrv"
