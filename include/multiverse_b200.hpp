@@ -1,0 +1,340 @@
+// multiverse_b200.hpp — C++20 host shim over the C-ABI (multiverse_b200.h).
+//
+// Mirrors the reference's proj/core hot-path interface so its callers (engine.cpp,
+// tests) can switch by changing the namespace:
+//   multiverse::kv::RadixStore / CacheError / StorageStats / SequenceHandle  (kvcache.hpp:32-101)
+//   multiverse::dag::build_visibility / VisibilitySpec / Mask                 (dag.hpp:59-110)
+//   the attention core of multiverse::toy::ToyModel::step / forward           (toy_model.cpp:121-202)
+// Same method names, argument meaning and exception kinds; values live on the device.
+// Header-only; link with -lmvb200 -lcudart.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "multiverse_b200.h"
+
+namespace multiverse_b200 {
+
+class CudaError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+namespace grammar {
+// grammar::ParseError (grammar.hpp:136-152)
+class ParseError : public std::runtime_error {
+ public:
+  enum class Kind { MalformedStructure, CountMismatch };
+  ParseError(Kind kind, const std::string& what) : std::runtime_error(what), kind_(kind) {}
+  Kind kind() const { return kind_; }
+
+ private:
+  Kind kind_;
+};
+}  // namespace grammar
+
+namespace kv {
+
+using TokenId = std::int32_t;
+
+// kv::CacheError (kvcache.hpp:32-41)
+class CacheError : public std::runtime_error {
+ public:
+  enum class Kind { UnknownHandle, DoubleRelease, CapacityExceeded, BranchNotDescendant };
+  CacheError(Kind kind, const std::string& what) : std::runtime_error(what), kind_(kind) {}
+  Kind kind() const { return kind_; }
+
+ private:
+  Kind kind_;
+};
+
+}  // namespace kv
+
+// Maps a C-ABI status to the reference's exception types (kvcache.hpp:32-41,
+// grammar.hpp:136-152, std::invalid_argument).
+inline void check(mv_status st) {
+  if (st == MV_OK) return;
+  const std::string msg = mv_last_error();
+  switch (st) {
+    case MV_ERR_UNKNOWN_HANDLE: throw kv::CacheError(kv::CacheError::Kind::UnknownHandle, msg);
+    case MV_ERR_DOUBLE_RELEASE: throw kv::CacheError(kv::CacheError::Kind::DoubleRelease, msg);
+    case MV_ERR_CAPACITY: throw kv::CacheError(kv::CacheError::Kind::CapacityExceeded, msg);
+    case MV_ERR_NOT_DESCENDANT: throw kv::CacheError(kv::CacheError::Kind::BranchNotDescendant, msg);
+    case MV_ERR_MALFORMED: throw grammar::ParseError(grammar::ParseError::Kind::MalformedStructure, msg);
+    case MV_ERR_COUNT_MISMATCH: throw grammar::ParseError(grammar::ParseError::Kind::CountMismatch, msg);
+    case MV_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    default: throw CudaError(msg);
+  }
+}
+
+inline void cuda_check(cudaError_t e) {
+  if (e != cudaSuccess) throw CudaError(cudaGetErrorString(e));
+}
+
+// Minimal owning device buffer.
+template <typename T>
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(std::size_t n) : n_(n) {
+    if (n) cuda_check(cudaMalloc(&p_, n * sizeof(T)));
+  }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    return *this;
+  }
+  ~DeviceBuffer() { cudaFree(p_); }
+  T* data() const { return p_; }
+  std::size_t size() const { return n_; }
+  void upload(const T* h, std::size_t n) { cuda_check(cudaMemcpy(p_, h, n * sizeof(T), cudaMemcpyHostToDevice)); }
+  std::vector<T> download() const {
+    std::vector<T> h(n_);
+    if (n_) cuda_check(cudaMemcpy(h.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost));
+    return h;
+  }
+
+ private:
+  T* p_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+namespace kv {
+
+// kv::StorageStats (kvcache.hpp:43-50). node_count / total_refcount are page-level here.
+struct StorageStats {
+  std::size_t physical_tokens_stored = 0;
+  std::size_t logical_tokens_reachable = 0;
+  std::size_t bytes_copied_on_last_op = 0;
+  std::size_t live_handles = 0;
+  std::size_t node_count = 0;
+  std::size_t total_refcount = 0;
+};
+
+// kv::SequenceHandle (kvcache.hpp:52-58)
+struct SequenceHandle {
+  std::uint64_t id = 0;
+  std::size_t length = 0;
+  bool valid() const { return id != 0; }
+};
+
+// kv::RadixStore (kvcache.hpp:60-101) on the device page store. capacity_tokens is
+// rounded up to whole 16-token pages. The attention plane (layers x kv_heads x 128 bf16
+// K and V per token) is optional: kv_heads = 0 gives the payload-only store the
+// reference's engine uses in scripted mode (engine.cpp:444-449).
+class RadixStore {
+ public:
+  explicit RadixStore(std::size_t payload_record_size = 0, std::size_t capacity_tokens = 1u << 20, int layers = 0,
+                      int kv_heads = 0, double rope_base = 10000.0)
+      : record_size_(payload_record_size) {
+    mv_kv_config cfg{};
+    cfg.num_pages = static_cast<int32_t>((capacity_tokens + 15) / 16);
+    cfg.record_bytes = static_cast<int32_t>(payload_record_size);
+    cfg.layers = kv_heads > 0 ? layers : 0;
+    cfg.kv_heads = kv_heads;
+    cfg.head_dim = 128;
+    cfg.rope_base = rope_base;
+    check(mv_kv_store_create(&cfg, &s_));
+  }
+  RadixStore(const RadixStore&) = delete;
+  RadixStore& operator=(const RadixStore&) = delete;
+  ~RadixStore() { mv_kv_store_destroy(s_); }
+
+  std::size_t record_size() const { return record_size_; }
+  mv_kv_store* native() const { return s_; }
+  void set_stream(cudaStream_t st) { check(mv_kv_set_stream(s_, st)); }
+
+  SequenceHandle create() {
+    SequenceHandle h;
+    check(mv_kv_create(s_, &h.id));
+    return h;
+  }
+
+  SequenceHandle extend(const SequenceHandle& h, std::span<const TokenId> tokens,
+                        std::span<const std::byte> payloads = {}) {
+    // same check as kvcache.cpp:153-156 (empty payloads are accepted and stored as zeros)
+    if (record_size_ > 0 && !payloads.empty() && payloads.size() != tokens.size() * record_size_)
+      throw std::invalid_argument("payload byte count does not match token count");
+    SequenceHandle out;
+    check(mv_kv_extend(s_, h.id, tokens.data(), static_cast<int64_t>(tokens.size()),
+                       payloads.empty() ? nullptr : payloads.data(), &out.id));
+    out.length = length_of(out.id);
+    return out;
+  }
+
+  std::vector<SequenceHandle> fork(const SequenceHandle& h, int n) {
+    if (n < 0) throw std::invalid_argument("fork count must be >= 0");
+    std::vector<std::uint64_t> ids(static_cast<std::size_t>(n));
+    check(mv_kv_fork(s_, h.id, n, ids.data()));
+    const std::size_t len = length_of(h.id);
+    std::vector<SequenceHandle> out;
+    out.reserve(ids.size());
+    for (auto id : ids) out.push_back({id, len});
+    return out;
+  }
+
+  SequenceHandle merge(const SequenceHandle& prefix, std::span<const SequenceHandle> branches) {
+    std::vector<std::uint64_t> ids;
+    ids.reserve(branches.size());
+    for (const auto& b : branches) ids.push_back(b.id);
+    SequenceHandle out;
+    check(mv_kv_merge(s_, prefix.id, ids.data(), static_cast<int32_t>(ids.size()), &out.id));
+    out.length = length_of(out.id);
+    return out;
+  }
+
+  void release(const SequenceHandle& h) { check(mv_kv_release(s_, h.id)); }
+
+  StorageStats stats() const {
+    mv_kv_stats st{};
+    check(mv_kv_stats_get(s_, &st));
+    return {st.physical_tokens_stored, st.logical_tokens_reachable, st.bytes_copied_on_last_op,
+            st.live_handles,           st.node_count,               st.total_refcount};
+  }
+
+  std::vector<TokenId> resolve(const SequenceHandle& h) const {
+    std::vector<TokenId> out(length_of(h.id));
+    check(mv_kv_resolve(s_, h.id, out.data()));
+    return out;
+  }
+  std::vector<std::byte> resolve_payloads(const SequenceHandle& h) const {
+    std::vector<std::byte> out(length_of(h.id) * record_size_);
+    check(mv_kv_resolve_payloads(s_, h.id, out.data()));
+    return out;
+  }
+  std::vector<std::uint32_t> resolve_slots(const SequenceHandle& h) const {
+    std::vector<std::uint32_t> out(length_of(h.id));
+    check(mv_kv_resolve_slots(s_, h.id, out.data()));
+    return out;
+  }
+
+  // Engine fast path (engine.cpp:639-641 extend + release of the old handle, in place):
+  // append one token per handle with its attention K/V (device bf16 [n][kv_heads][128]).
+  void append(std::span<const std::uint64_t> handles, const int32_t* d_tokens, const int32_t* d_positions, int layer,
+              const void* d_k, const void* d_v) {
+    check(mv_kv_append(s_, handles.data(), static_cast<int32_t>(handles.size()), d_tokens, d_positions, layer, d_k,
+                       d_v));
+  }
+
+ private:
+  std::size_t length_of(std::uint64_t id) const {
+    int64_t n = 0;
+    check(mv_kv_length(s_, id, &n));
+    return static_cast<std::size_t>(n);
+  }
+
+  mv_kv_store* s_ = nullptr;
+  std::size_t record_size_ = 0;
+};
+
+}  // namespace kv
+
+namespace dag {
+
+// dag::Mask (dag.hpp:59-73), dense, materialised from the device intervals.
+class Mask {
+ public:
+  Mask() = default;
+  explicit Mask(std::size_t n) : n_(n), bits_(n * n, 0) {}
+  std::size_t size() const { return n_; }
+  bool at(std::size_t i, std::size_t j) const { return bits_[i * n_ + j] != 0; }
+  void set(std::size_t i, std::size_t j, bool v) { bits_[i * n_ + j] = v ? 1 : 0; }
+  bool operator==(const Mask&) const = default;
+
+ private:
+  std::size_t n_ = 0;
+  std::vector<std::uint8_t> bits_;
+};
+
+// dag::VisibilitySpec (dag.hpp:104-110) plus the compact device form the kernels use.
+struct VisibilitySpec {
+  std::vector<int> positions;
+  Mask mask;
+};
+
+struct DeviceVisibility {
+  int n = 0, max_depth = 0;
+  DeviceBuffer<int32_t> positions;  // int32[n]
+  DeviceBuffer<int32_t> seg_id;     // int32[n]
+  DeviceBuffer<int32_t> excl;       // int32[n][max_depth][2]
+};
+
+// Tag-stream token ids (tok::Tokenizer ids, tokenizer.cpp:56-63) -> device positions and
+// exclusion intervals. Throws grammar::ParseError like grammar::parse (grammar.cpp:156-294).
+inline DeviceVisibility build_visibility_device(std::span<const int32_t> tokens, int max_depth = 4,
+                                                cudaStream_t stream = nullptr) {
+  DeviceVisibility v;
+  v.n = static_cast<int>(tokens.size());
+  v.max_depth = max_depth;
+  const std::size_t n = std::max<std::size_t>(tokens.size(), 1);
+  DeviceBuffer<int32_t> d_tok(n);
+  if (!tokens.empty()) d_tok.upload(tokens.data(), tokens.size());
+  v.positions = DeviceBuffer<int32_t>(n);
+  v.seg_id = DeviceBuffer<int32_t>(n);
+  v.excl = DeviceBuffer<int32_t>(n * static_cast<std::size_t>(max_depth) * 2);
+  DeviceBuffer<int32_t> status(1);
+  const int64_t offs[2] = {0, static_cast<int64_t>(tokens.size())};
+  const std::size_t ws_bytes = mv_visibility_workspace_size(offs, 1);
+  DeviceBuffer<std::uint8_t> ws(std::max<std::size_t>(ws_bytes, 1));
+  check(mv_visibility(d_tok.data(), offs, 1, max_depth, v.positions.data(), v.seg_id.data(), v.excl.data(),
+                      status.data(), ws.data(), ws_bytes, stream));
+  cuda_check(cudaStreamSynchronize(stream));
+  check(static_cast<mv_status>(status.download()[0]));
+  return v;
+}
+
+// dag::build_visibility (dag.hpp:104-110): host positions + dense mask.
+inline VisibilitySpec build_visibility(std::span<const int32_t> tokens, int max_depth = 4) {
+  DeviceVisibility v = build_visibility_device(tokens, max_depth);
+  VisibilitySpec out;
+  const std::size_t n = tokens.size();
+  out.mask = Mask(n);
+  if (n == 0) return out;
+  auto pos = v.positions.download();
+  out.positions.assign(pos.begin(), pos.begin() + static_cast<std::ptrdiff_t>(n));
+  DeviceBuffer<std::uint8_t> bits((n * n + 7) / 8);
+  check(mv_mask_packed(v.excl.data(), v.n, max_depth, 0, v.n, bits.data(), nullptr));
+  auto h = bits.download();
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t j = 0; j < n; ++j) {
+      const std::size_t b = i * n + j;
+      out.mask.set(i, j, (h[b >> 3] >> (7 - (b & 7))) & 1);
+    }
+  return out;
+}
+
+}  // namespace dag
+
+namespace attn {
+
+// Attention core of ToyModel::step (toy_model.cpp:121-157) for every lane in one launch:
+// q bf16 [n][q_heads][128] (pre-RoPE, rotated at d_positions), out bf16 or fp32.
+inline void decode(kv::RadixStore& store, int layer, std::span<const std::uint64_t> handles, int q_heads,
+                   const void* d_q, const int32_t* d_positions, void* d_out, bool out_f32 = false) {
+  check(mv_attn_decode(store.native(), layer, handles.data(), static_cast<int32_t>(handles.size()), q_heads, d_q,
+                       d_positions, d_out, out_f32 ? 1 : 0));
+}
+
+// Attention inside ToyModel::forward (toy_model.cpp:174-202) for a whole structured sequence.
+inline void prefill(const void* d_q, const void* d_k, const void* d_v, const dag::DeviceVisibility& vis, int q_heads,
+                    int kv_heads, void* d_out, bool out_f32 = false, double rope_base = 10000.0,
+                    cudaStream_t stream = nullptr) {
+  const std::size_t ws_bytes = mv_prefill_workspace_size(vis.n, q_heads, kv_heads);
+  DeviceBuffer<std::uint8_t> ws(std::max<std::size_t>(ws_bytes, 1));
+  check(mv_attn_prefill(d_q, d_k, d_v, vis.positions.data(), vis.excl.data(), vis.max_depth, vis.n, q_heads, kv_heads,
+                        rope_base, d_out, out_f32 ? 1 : 0, ws.data(), ws_bytes, stream));
+}
+
+}  // namespace attn
+
+}  // namespace multiverse_b200
