@@ -56,12 +56,18 @@ __host__ __device__ inline PageRef make_ref(int page, int begin, int count) {
 }
 
 // ---------------------------------------------------------------------------
-// KV page layout: [page][kv_head][16 tokens][128 dims] bf16, 4 KiB per (page, head).
-// The 16-byte chunk c (8 dims) of token row t is stored at chunk c ^ (t & 7) so that
-// ldmatrix over 8 consecutive token rows is bank-conflict free after a plain 1-D bulk
-// copy (the equivalent of a TMA 128B swizzle, baked into the storage layout).
+// KV page layout: [page][kv_head][2 halves][16 tokens][64 dims] bf16, 4 KiB per (page, head).
+// Half h holds dims 64h..64h+63 as 128-byte token rows, and the 16-byte chunk c of token row t
+// sits at chunk c ^ (t & 7): each half is exactly the canonical UMMA SWIZZLE_128B atom pair
+// (8 rows x 128 B, 1024 B apart), so a plain 1-D bulk copy of a page-head block lands an
+// operand the tcgen05 tensor core reads directly — K-major for Q.K^T (N = tokens) and
+// MN-major for P.V (N = dims) — with no shared-memory re-layout.
 // ---------------------------------------------------------------------------
 __host__ __device__ inline int swz_chunk(int token, int chunk) { return chunk ^ (token & 7); }
+// element offset of 16-byte chunk c (dims 8c..8c+7) of token slot t inside a page-head block
+__host__ __device__ inline int kv_chunk_offset(int t, int c) {
+  return (c >> 3) * (kPageTokens * 64) + t * 64 + (((c & 7) ^ (t & 7)) << 3);
+}
 __host__ __device__ inline size_t kv_page_head_offset(int64_t page, int head, int kv_heads) {
   return ((size_t)page * kv_heads + head) * (kPageTokens * kHeadDim);
 }

@@ -1,4 +1,5 @@
-// decode.cu — K4: branch-parallel paged decode attention (split-KV, cascade over fork lineage).
+// decode.cu — K4: branch-parallel paged decode attention on the 5th-gen tensor cores
+// (tcgen05 / TMEM, 1-D TMA bulk copies), split-KV with cascade over the fork lineage.
 //
 // Reference behaviour replaced: for every active lane the
 // engine resolves the lane's whole context (engine.cpp:603-605) and runs the attention core
@@ -9,23 +10,30 @@
 // Plan (host, cached per page-table shape): every decoding handle's table is cut at its fork
 // lineage boundaries; the segment [prev boundary, boundary of group g) is identical in all
 // holders of g, so it becomes ONE cascade unit whose query rows are all holders x GQA heads.
-// Units are split into <= 64-page chunks (split-KV); a work item = (chunk, <= 8 handles).
+// Units are split into <= 64-page chunks (split-KV); a work unit = (chunk, <= 16 handles,
+// KV head), ordered longest-first for the persistent scheduler.
 //
-// Kernel (one CTA per (work item, KV head)):
-//   warp 6      : TMA warp — 1-D bulk copies (TMA engine) of each 4 KiB K and V page-head
-//                 block into a 15-stage smem ring, mbarrier complete_tx signalling; it runs
-//                 ahead across work-item boundaries (persistent kernel, dynamic item queue).
-//   warp 7      : staging warp — claims the next (chunk, kv head) item and stages its page
-//                 entries and RoPE-rotated Q rows into a double buffer.
-//   warps 0..5  : 3 consumer pairs; pair p takes pages p, p+3, ...  Tokens are the MMA M
-//                 dimension and query rows the N dimension (mma.sync m16n8k16, swapped
-//                 operands), so 40 rows = 5 n8-tiles with no padding; S^T -> P^T goes
-//                 register-to-register through movmatrix.  Both warps of a pair compute
-//                 S = K.Q^T (Q lives in registers); each accumulates O^T for half of the
-//                 128 head dims.  Online softmax in the log2 domain, fp32 accumulation.
-//   epilogue    : the 3 pairs' (m, l, O) are merged through smem and written as one
-//                 partial per (handle, q head); a combine kernel merges the partials of
-//                 each handle's chunks (log-sum-exp) into bf16 outputs.
+// Kernel: persistent, one CTA per SM, 16 warps, dynamic work queue.
+//   warp 2  TMA     : one thread; 1-D bulk copies of the K and V page-head blocks (already in
+//                     UMMA SWIZZLE_128B layout in HBM, common.cuh) of 4-page blocks into a 4-slot
+//                     ring (mbarrier complete_tx), plus L2 prefetches further ahead.  Runs ahead
+//                     across work units.
+//   warp 3  MMA     : one thread. Per unit: Q smem -> TMEM (tcgen05.cp).  Per block: S = Q.K_blk^T
+//                     (M=128 query rows, N=64 tokens, K=128; A = Q from TMEM) into a TMEM S buffer; after softmax, per page
+//                     O += P_page.V_page (TS: P read from TMEM, aliasing S; N=128 dims).  Two S
+//                     buffers (64 columns) and two O buffers (one per in-flight unit).
+//   warp 0  stager  : claims the next unit, copies its page entries, and bulk-copies the
+//                     members' RoPE'd Q rows (pre-swizzled by rope_q_tile_kernel) into one of
+//                     two Q buffers.
+//   warps 4-11 softmax: two warpgroups ping-pong over even / odd blocks, each with its own S
+//                     buffer, O buffer and (m, l): thread = query row = TMEM lane.  Masks ragged
+//                     page slots, log2-domain online softmax against a lazily moved reference
+//                     (no per-block max), P as packed bf16 back into TMEM.
+//   warps 12-15 epilogue: merges the two parity partials of each row from TMEM -> final output
+//                     (single-chunk handles) or an fp32 split-KV partial, merged afterwards by
+//                     combine_kernel (log-sum-exp over the handle's chunks).
+// Query rows: member m of a unit owns TMEM lanes [m*R, m*R + gqa), R = gqa rounded up to a
+// power of two >= 8, so every member's rows share the swizzle phase and a 1 KiB-aligned slot.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -33,473 +41,530 @@
 #include <vector>
 
 #include "store.hpp"
+#include "tc_common.cuh"
 
 namespace mv {
 
 namespace {
 
-constexpr int kConsumerWarps = 6;
-constexpr int kConsumerThreads = kConsumerWarps * 32;
-constexpr int kDecThreads = kConsumerThreads + 64;  // + TMA warp + staging warp = 8 warps (255 regs)
-constexpr int kStages = 15;
-constexpr int kStageBytes = 2 * kPageTokens * kHeadDim * 2;  // K + V page-head blocks (8 KiB)
-constexpr int kMaxNT = 5;                                   // <= 40 query rows per item
-constexpr int kMaxRows = kMaxNT * 8;
-constexpr int kChunkPages = 64;                             // split-KV chunk (pages)
-constexpr float kLazyRescale = 8.f;                         // log2-domain headroom before O is rescaled
-constexpr int kRowSlots = 144;                              // epilogue rows: 6 streams x 24 or 3 x 40
-constexpr int kSmemRing = kStages * kStageBytes;            // 120 KiB
-constexpr int kSmemQ = kMaxRows * kHeadDim * 2;             // 10 KiB per buffer
-constexpr int kSmemEnt = kChunkPages * 8;                   // 512 B per buffer
-constexpr int kSmemO = kRowSlots * kHeadDim * 4;            // 72 KiB epilogue
-constexpr int kSmemML = kRowSlots * 2 * 4;
-constexpr int kOffQ = kSmemRing;
-constexpr int kOffEnt = kOffQ + 2 * kSmemQ;
-constexpr int kOffO = kOffEnt + 2 * kSmemEnt;
-constexpr int kOffML = kOffO + kSmemO;
-constexpr int kOffItem = kOffML + kSmemML;
-constexpr int kItemSlotBytes = 128;
-constexpr int kOffBar = kOffItem + 2 * kItemSlotBytes;
-constexpr int kOffTag = kOffBar + (2 * kStages + 4) * 8;
-constexpr int kDecSmem = kOffTag + kStages * 4;
-
-// Consumer split of an item with NT row tiles: NT <= 3 -> every warp owns all rows and its own
-// page stream (6 streams); NT 4-5 -> warp pairs split the rows (ceil(NT/2) + floor(NT/2)) and
-// share a page stream (3 streams). No warp repeats another's Q.K^T work.
-__host__ __device__ constexpr int row_groups(int nt) { return nt <= 3 ? 1 : 2; }
-
-constexpr int kMaxMembers = 8;  // handles per work item (8 x GQA 5 = 40 rows)
+constexpr int kThreads = 512;                               // 16 warps
+// Warp w issues on SM sub-partition w % 4, shared with softmax / epilogue warps of TMEM lane
+// quadrant w % 4.  Query rows fill quadrants from 0, so the latency-critical MMA issuer sits on
+// sub-partition 3 (idle unless a unit has > 96 rows) and the TMA issuer on 2.
+constexpr int kWarpStage = 0, kWarpTma = 2, kWarpMma = 3;
+constexpr int kPageBytes = kPageTokens * kHeadDim * 2;      // 4 KiB page-head block
+constexpr int kBlkPages = 4;                                // pages per block (one QK MMA chain)
+constexpr int kBlkCols = kBlkPages * kPageTokens;           // 64 S columns per block
+constexpr int kSlots = 4;                                   // ring slots, one block (K + V) each
+constexpr int kSlotK = kBlkPages * kPageBytes;              // K: [2 halves][64 tokens][128 B]
+constexpr int kSlotBytes = 2 * kSlotK;                      // + V: 4 page-head blocks as stored
+constexpr int kMaxEntries = 64;                             // pages per work unit (split-KV chunk)
+constexpr int kMaxMem = 16;                                 // handles per work unit
+constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dims] bf16
+constexpr int kQBytes = 2 * kQHalf;
+constexpr float kSumLimit = 4096.f;                        // block mass that moves the softmax reference
+constexpr int kPrefetch = 24;                               // L2 prefetch distance (pages)
+constexpr int kColS = 0;                                    // TMEM: S0, S1 (64 cols each)
+constexpr int kColO = 2 * kBlkCols;                         //       O0, O1 (128 cols each)
+constexpr int kColQ = kColO + 256;                          //       Q0, Q1 (64 cols: 128 bf16 dims)
+constexpr int kTmemCols = 512;
 
 struct __align__(16) WorkItem {
   int64_t entry_off;             // absolute arena index of the chunk's first entry
-  int32_t n_entries;
-  int32_t n_mem;                 // handles (query groups) sharing this chunk
-  int32_t slot_base;             // partial slot of the first member
-  int32_t nt;                    // n8 row tiles (ceil(n_mem * gqa / 8))
-  int32_t members[kMaxMembers];  // batch indices
-  int32_t pad[2];
-};
-static_assert(sizeof(WorkItem) == 64, "WorkItem is one 64 B line");
-
-struct ItemSlot {      // what the producer hands the consumers for one (item, kv head)
-  WorkItem it;
-  int32_t kvh;
+  int32_t n_entries;             // pages (1..64)
+  int32_t n_mem;                 // handles sharing the chunk
+  int32_t slot_base;             // partial slot of member 0 (member m -> slot_base + m)
+  int32_t kvh;                   // KV head
   int32_t valid;
+  int32_t pad;
+  int32_t members[kMaxMem];      // batch indices
 };
+static_assert(sizeof(WorkItem) == 96, "WorkItem layout");
+constexpr int kItemInts = sizeof(WorkItem) / 4;
 
-static_assert(sizeof(ItemSlot) <= kItemSlotBytes, "item slot overflows its smem reservation");
+constexpr int kOffQ = 0;
+constexpr int kOffRing = kOffQ + 2 * kQBytes;
+constexpr int kOffEnt = kOffRing + kSlots * kSlotBytes;
+constexpr int kOffItem = kOffEnt + 2 * kMaxEntries * 8;
+constexpr int kOffEp = kOffItem + 2 * sizeof(WorkItem);
+constexpr int kOffStat = kOffEp + 2 * sizeof(WorkItem);
+constexpr int kOffFlag = kOffStat + 2 * 128 * 8;
+constexpr int kOffBar = kOffFlag + 128 * 4;
+constexpr int kNumBars = 4 + 2 * kSlots + 10;
+constexpr int kOffTmem = kOffBar + kNumBars * 8;
+constexpr int kSmem = kOffTmem + 16 + 1024;  // + 1 KiB alignment slack
+static_assert(kSmem <= 227 * 1024, "decode smem");
+
+constexpr uint32_t kIdQK = tc::idesc_bf16(128, kBlkCols, 0, 0);  // S(128 x 64) = Q . K_blk^T
+constexpr uint32_t kIdPV = tc::idesc_bf16(128, 128, 0, 1);  // O(128 x 128) += P_page . V_page
 
 struct DecodeParams {
   const PageRef* arena;
   const __nv_bfloat16* kplane;
   const __nv_bfloat16* vplane;
-  const __nv_bfloat16* q_rot; // [n][q_heads][128], RoPE already applied (rope_q_kernel)
-  const WorkItem* items;
-  float* part_o;              // [slots][q_heads][128]
-  float2* part_ml;            // [slots][q_heads]
-  int* work_counter;          // dynamic (item, kv head) scheduler
-  int n_work;                 // items * kv_heads
-  int kv_heads, q_heads, gqa;
-  float scale_log2;           // log2(e) / sqrt(128)
-  int diag;                   // diagnostics: 1 = skip math (pipeline only), 2 = skip loads (math only)
-  unsigned long long* trace;  // optional per-item timeline (MV_DECODE_TRACE)
-  RopeTable rope;
+  const __nv_bfloat16* q_tile;  // [n][kv_heads][2][R][64] RoPE'd, swizzled (rope_q_tile_kernel)
+  const WorkItem* units;
+  int n_units;
+  int* work_counter;
+  float* part_o;                // [slots][q_heads][128]
+  float2* part_ml;              // [slots][q_heads] (log2-domain reference max, sum)
+  const int32_t* slot_cnt;      // [n] partial slots per handle
+  const int32_t* slot_ptr;      // [n + 1]
+  const int32_t* slot_idx;
+  void* out;
+  int out_f32;
+  int kv_heads, q_heads, gqa, R;
+  float scale_log2;
+  unsigned long long* trace;    // optional timeline [cta][kTraceWords] (MV_DECODE_TRACE)
 };
 
-// Consumer side of one work item for one warp: rows [nt0*8, (nt0+NTW)*8), pages
-// j = stream, stream + n_streams, ... . S^T = K.Q^T (tokens are the MMA M dimension), online
-// softmax in the log2 domain with lazy rescaling, P^T via movmatrix, O^T += V^T.P^T over all
-// 128 head dims (8 m-tiles).
-template <int NTW>
-__device__ __forceinline__ void consume_rows(const DecodeParams& P, const WorkItem& it, int gbase, int stream,
-                                             int n_streams, int nt0, uint8_t* ring, const uint8_t* sq,
-                                             const PageRef* s_ent, uint64_t* full, uint64_t* empty,
-                                             int empty_count, float* s_ml, float* s_o, const int* s_tag) {
-  const int lane = threadIdx.x & 31;
-  const int g = lane >> 2, t4 = lane & 3;
+constexpr int kTraceWords = 544;
 
-  uint32_t qb[NTW][8][2];
-  const uint32_t sq_base = smem_u32(sq);
+__device__ __forceinline__ void store_row(const DecodeParams& P, int64_t row, int c, const float* o, float inv) {
+  if (P.out_f32) {
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + row * kHeadDim + c * 32);
 #pragma unroll
-  for (int nt = 0; nt < NTW; ++nt)
+    for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + row * kHeadDim + c * 32);
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      int row = (nt0 + nt) * 8 + (lane & 7);
-      int chunk = ks * 2 + ((lane >> 3) & 1);
-      // Q rows land in smem by bulk copy (unswizzled); 4-way conflicts once per item only
-      ldmatrix_x2(qb[nt][ks][0], qb[nt][ks][1], sq_base + row * 256 + (chunk << 4));
-    }
-
-  float o[8][NTW][4];
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NTW; ++nt)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) o[mt][nt][k] = 0.f;
-  float m_ref[NTW][2], l_run[NTW][2];
-#pragma unroll
-  for (int nt = 0; nt < NTW; ++nt) {
-    m_ref[nt][0] = m_ref[nt][1] = -INFINITY;
-    l_run[nt][0] = l_run[nt][1] = 0.f;
-  }
-
-  const int npages = it.n_entries;
-  for (int j = stream; j < npages; j += n_streams) {
-    const int gp = gbase + j;
-    const int stage = gp % kStages;
-    const PageRef ref = s_ent[j];
-    const int vb = ref_begin(ref), ve = vb + ref_count(ref);
-    // Streams consume stages out of order, so a stream may reach page gp while the stage still
-    // holds page gp - kStages in flight; a bare parity wait would then match the previous phase.
-    // The TMA warp tags the stage with gp before issuing it, which pins the phase.
-    while (ld_volatile_s32(&s_tag[stage]) != gp) {
-    }
-    mbar_wait(&full[stage], (gp / kStages) & 1);
-    if (P.diag == 1) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive_n(&empty[stage], empty_count);
-      continue;
-    }
-    const uint32_t kbase = smem_u32(ring + stage * kStageBytes);
-    const uint32_t vbase = kbase + kPageTokens * kHeadDim * 2;
-
-    float s[NTW][4];
-#pragma unroll
-    for (int nt = 0; nt < NTW; ++nt) s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
-      uint32_t a[4];
-      const int mi = lane >> 3;
-      const int row = (mi & 1) * 8 + (lane & 7);
-      const int chunk = ks * 2 + (mi >> 1);
-      ldmatrix_x4(a[0], a[1], a[2], a[3], kbase + row * 256 + (swz_chunk(row, chunk) << 4));
-#pragma unroll
-      for (int nt = 0; nt < NTW; ++nt) mma_bf16_16816(s[nt], a, qb[nt][ks][0], qb[nt][ks][1]);
-    }
-
-    const bool v0 = g >= vb && g < ve, v1 = g + 8 >= vb && g + 8 < ve;
-    float x[NTW][4], mx[NTW][2];
-    bool need = false;
-#pragma unroll
-    for (int nt = 0; nt < NTW; ++nt) {
-      x[nt][0] = v0 ? s[nt][0] * P.scale_log2 : -INFINITY;
-      x[nt][1] = v0 ? s[nt][1] * P.scale_log2 : -INFINITY;
-      x[nt][2] = v1 ? s[nt][2] * P.scale_log2 : -INFINITY;
-      x[nt][3] = v1 ? s[nt][3] * P.scale_log2 : -INFINITY;
-      mx[nt][0] = fmaxf(x[nt][0], x[nt][2]);
-      mx[nt][1] = fmaxf(x[nt][1], x[nt][3]);
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
-        mx[nt][0] = fmaxf(mx[nt][0], __shfl_xor_sync(0xffffffffu, mx[nt][0], off));
-        mx[nt][1] = fmaxf(mx[nt][1], __shfl_xor_sync(0xffffffffu, mx[nt][1], off));
-      }
-      need |= mx[nt][0] > m_ref[nt][0] + kLazyRescale || mx[nt][1] > m_ref[nt][1] + kLazyRescale;
-    }
-    if (__any_sync(0xffffffffu, need)) {
-      // move the reference max (rare after the first pages): rescale l and O
-#pragma unroll
-      for (int nt = 0; nt < NTW; ++nt)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const float mn = fmaxf(m_ref[nt][c], mx[nt][c]);
-          const float al = mn == -INFINITY ? 1.f : fast_exp2(m_ref[nt][c] - mn);
-          m_ref[nt][c] = mn;
-          l_run[nt][c] *= al;
-#pragma unroll
-          for (int mt = 0; mt < 8; ++mt) {
-            o[mt][nt][c] *= al;
-            o[mt][nt][2 + c] *= al;
-          }
-        }
-    }
-    uint32_t pb[NTW][2];
-#pragma unroll
-    for (int nt = 0; nt < NTW; ++nt) {
-      const float mu0 = m_ref[nt][0] == -INFINITY ? 0.f : m_ref[nt][0];
-      const float mu1 = m_ref[nt][1] == -INFINITY ? 0.f : m_ref[nt][1];
-      const float p0 = fast_exp2(x[nt][0] - mu0), p1 = fast_exp2(x[nt][1] - mu1);
-      const float p2 = fast_exp2(x[nt][2] - mu0), p3 = fast_exp2(x[nt][3] - mu1);
-      l_run[nt][0] += p0 + p2;
-      l_run[nt][1] += p1 + p3;
-      pb[nt][0] = movmatrix_trans(pack_bf16(p0, p1));
-      pb[nt][1] = movmatrix_trans(pack_bf16(p2, p3));
-    }
-
-    // O^T (128 dims x rows) += V^T . P^T
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      uint32_t a[4];
-      const int mi = lane >> 3;
-      const int tok = (mi >> 1) * 8 + (lane & 7);
-      const int chunk = mt * 2 + (mi & 1);
-      ldmatrix_x4_trans(a[0], a[1], a[2], a[3], vbase + tok * 256 + (swz_chunk(tok, chunk) << 4));
-#pragma unroll
-      for (int nt = 0; nt < NTW; ++nt) mma_bf16_16816(o[mt][nt], a, pb[nt][0], pb[nt][1]);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive_n(&empty[stage], empty_count);
-  }
-
-  // finish l (sum over the 8 token lanes g) and publish this stream's (m, l, O) rows
-#pragma unroll
-  for (int nt = 0; nt < NTW; ++nt)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      float l = l_run[nt][c];
-#pragma unroll
-      for (int off = 4; off < 32; off <<= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
-      l_run[nt][c] = l;
-    }
-  const int rows = it.nt * 8;
-  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads));  // previous item's merge readers are done
-  if (g == 0) {
-#pragma unroll
-    for (int nt = 0; nt < NTW; ++nt)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int r = (nt0 + nt) * 8 + 2 * t4 + c;
-        s_ml[(stream * rows + r) * 2 + 0] = m_ref[nt][c];
-        s_ml[(stream * rows + r) * 2 + 1] = l_run[nt][c];
-      }
-  }
-#pragma unroll
-  for (int mt = 0; mt < 8; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NTW; ++nt)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int dim = mt * 16 + g + (k >> 1) * 8;
-        const int r = (nt0 + nt) * 8 + 2 * t4 + (k & 1);
-        s_o[(stream * rows + r) * kHeadDim + dim] = o[mt][nt][k];
-      }
-}
-
-// All consumer warps: merge the streams' partials and write one partial per (member, q head).
-__device__ __forceinline__ void merge_streams(const DecodeParams& P, const ItemSlot& is, int n_streams,
-                                              const float* s_ml, const float* s_o) {
-  asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads));
-  const WorkItem& it = is.it;
-  const int rows = it.nt * 8;
-  const int nrows = it.n_mem * P.gqa;
-  for (int x = threadIdx.x; x < nrows * (kHeadDim / 4); x += kConsumerThreads) {
-    const int r = x / (kHeadDim / 4), d4 = (x % (kHeadDim / 4)) * 4;
-    float m = -INFINITY;
-    for (int st = 0; st < n_streams; ++st) m = fmaxf(m, s_ml[(st * rows + r) * 2]);
-    const float mu = m == -INFINITY ? 0.f : m;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    float l = 0.f;
-    for (int st = 0; st < n_streams; ++st) {
-      const float w = fast_exp2(s_ml[(st * rows + r) * 2] - mu);
-      const float4 v = *reinterpret_cast<const float4*>(&s_o[(st * rows + r) * kHeadDim + d4]);
-      acc.x += w * v.x;
-      acc.y += w * v.y;
-      acc.z += w * v.z;
-      acc.w += w * v.w;
-      l += w * s_ml[(st * rows + r) * 2 + 1];
-    }
-    const int mi = r / P.gqa, hl = r % P.gqa;
-    const int64_t slot = it.slot_base + mi;
-    const int head = is.kvh * P.gqa + hl;
-    *reinterpret_cast<float4*>(&P.part_o[(slot * P.q_heads + head) * kHeadDim + d4]) = acc;
-    if (d4 == 0) P.part_ml[slot * P.q_heads + head] = make_float2(m, l);
+    for (int e = 0; e < 4; ++e)
+      dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
+                          pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
   }
 }
 
-// Persistent kernel: one CTA per SM pulls (chunk, kv head) work items from a global counter.
-// The producer warp stages item i+1 (entries, rotated Q) and keeps the page ring full while
-// the consumers finish item i, so per-item prologue/epilogue latency stays off the HBM path.
-__global__ void __launch_bounds__(kDecThreads, 1) decode_kernel(DecodeParams P) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* ring = smem;
-  ItemSlot* s_item = reinterpret_cast<ItemSlot*>(smem + kOffItem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  uint64_t* empty = full + kStages;
-  uint64_t* item_full = empty + kStages;
-  uint64_t* item_empty = item_full + 2;
-  float* s_o = reinterpret_cast<float*>(smem + kOffO);
-  float* s_ml = reinterpret_cast<float*>(smem + kOffML);
-  int* s_tag = reinterpret_cast<int*>(smem + kOffTag);
+template <bool TRACE>
+__global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodeParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* ring = smem + kOffRing;
+  WorkItem* s_item = reinterpret_cast<WorkItem*>(smem + kOffItem);
+  WorkItem* s_ep = reinterpret_cast<WorkItem*>(smem + kOffEp);
+  PageRef* s_ent0 = reinterpret_cast<PageRef*>(smem + kOffEnt);
+  float2* s_stat = reinterpret_cast<float2*>(smem + kOffStat);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* item_full = bars;             // [2] stager -> TMA / MMA / softmax (count 1 + Q tx)
+  uint64_t* slot_empty = bars + 2;        // [2] TMA + MMA commit + 8 softmax warps -> stager
+  uint64_t* full = bars + 4;              // [kSlots] TMA -> MMA
+  uint64_t* empty = full + kSlots;        // [kSlots] MMA commit -> TMA
+  uint64_t* s_full = empty + kSlots;      // [2] MMA commit -> softmax
+  uint64_t* p_full = s_full + 2;          // [2] softmax warps -> MMA
+  uint64_t* o_full = p_full + 2;          // MMA commit -> epilogue (unit's O_0 / O_1 final)
+  uint64_t* o_empty = o_full + 2;         // epilogue warps -> MMA / softmax
+  uint64_t* stat_full = o_empty + 2;      // 8 softmax warps -> epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  for (int st = threadIdx.x; st < kStages; st += blockDim.x) s_tag[st] = -1;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 2);
-    }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&item_full[b], 32);
-      mbar_init(&item_empty[b], kConsumerWarps + kStages);  // consumer warps + TMA lanes
+      mbar_init(&item_full[b], 1);
+      mbar_init(&slot_empty[b], 10);
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 4);
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 4);
+      mbar_init(&stat_full[b], 8);
+    }
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
     }
     fence_mbar_init();
   }
+  if (warp == kWarpMma) tc::tmem_alloc(tmem_slot, kTmemCols);
+  tc::fence_before();
   __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tmem_slot;
 
-  if (warp == kConsumerWarps + 1) {
-    // ---------------- staging warp: claims work and stages entries + Q rows ----------------
-    // Critical path per item is ~2 memory round trips: the next claim is issued one item
-    // ahead, Q rows (pre-rotated) arrive by bulk copy on the item barrier itself.
+  if (warp == kWarpStage) {
+    // ---------------- stager: claim, entries, Q rows ----------------
     int w_next = lane == 0 ? atomicAdd(P.work_counter, 1) : 0;
-    for (int iter = 0;; ++iter) {
-      const int buf = iter & 1;
-      if (iter >= 2) mbar_wait(&item_empty[buf], ((iter >> 1) - 1) & 1);
+    for (int i = 0;; ++i) {
+      const int buf = i & 1;
+      if (i >= 2) mbar_wait(&slot_empty[buf], ((i >> 1) - 1) & 1);
       const int w = __shfl_sync(0xffffffffu, w_next, 0);
-      ItemSlot* is = &s_item[buf];
-      if (w >= P.n_work) {
-        if (lane == 0) is->valid = 0;
+      WorkItem* si = &s_item[buf];
+      if (w >= P.n_units) {
+        if (lane == 0) si->valid = 0;
         __syncwarp();
-        mbar_arrive(&item_full[buf]);
+        if (lane == 0) mbar_arrive(&item_full[buf]);
         break;
       }
       if (lane == 0) w_next = atomicAdd(P.work_counter, 1);
-      const WorkItem it = P.items[w / P.kv_heads];
-      const int kvh = w % P.kv_heads;
-      uint8_t* sq = smem + kOffQ + buf * kSmemQ;
-      const int qbytes = P.gqa * kHeadDim * 2;  // one handle's GQA group of q heads, contiguous
-      if (lane == 0) {
-        is->it = it;
-        is->kvh = kvh;
-        is->valid = 1;
-        mbar_arrive_expect_tx(&item_full[buf], it.n_mem * qbytes);
-      }
+      if (TRACE && lane == 0 && i < 32) P.trace[blockIdx.x * kTraceWords + 320 + i] = globaltimer();
+      if (lane < kItemInts) reinterpret_cast<int*>(si)[lane] = reinterpret_cast<const int*>(P.units + w)[lane];
       __syncwarp();
-      if (lane < it.n_mem) {
-        const int b = it.members[lane];
-        bulk_g2s(sq + lane * qbytes, P.q_rot + ((size_t)b * P.q_heads + kvh * P.gqa) * kHeadDim, qbytes,
-                 &item_full[buf]);
-      }
-      PageRef* s_ent = reinterpret_cast<PageRef*>(smem + kOffEnt + buf * kSmemEnt);
-      for (int j = lane; j < it.n_entries; j += 32) s_ent[j] = P.arena[it.entry_off + j];
-      // zero the padding rows of the last n8 tile
-      const int nrows = it.n_mem * P.gqa, rows = it.nt * 8;
-      for (int x = lane; x < (rows - nrows) * 16; x += 32)
-        *reinterpret_cast<uint4*>(sq + nrows * 256 + x * 16) = make_uint4(0, 0, 0, 0);
-      __syncwarp();
-      if (lane != 0) mbar_arrive(&item_full[buf]);  // lane 0 arrived with expect_tx
-    }
-    return;
-  }
-
-  if (warp == kConsumerWarps) {
-    // ---------------- TMA warp: keeps the page ring full across item boundaries ----------------
-    // Lane l (< kStages) owns ring stage l and issues every page that maps to it. One issuing
-    // thread per stage matters: a single issuing thread serialises on its empty-barrier waits and
-    // caps a CTA at ~15 GB/s (tools/microbench/mb_tma.cu: 2.3 TB/s vs 7.0 TB/s chip-wide).
-    if (lane < kStages) {
-      int gbase = 0;
-      for (int iter = 0;; ++iter) {
-        const int buf = iter & 1;
-        mbar_wait(&item_full[buf], (iter >> 1) & 1);
-        const ItemSlot* is = &s_item[buf];
-        if (!is->valid) break;
-        const PageRef* s_ent = reinterpret_cast<const PageRef*>(smem + kOffEnt + buf * kSmemEnt);
-        const size_t head_off = (size_t)is->kvh * kPageTokens * kHeadDim;
-        const int n_entries = is->it.n_entries;
-        const size_t page_stride = (size_t)P.kv_heads * kPageTokens * kHeadDim;
-        for (int j = ((lane - gbase) % kStages + kStages) % kStages; j < n_entries; j += kStages) {
-          const int gp = gbase + j;
-          if (gp >= kStages) mbar_wait(&empty[lane], ((gp / kStages) - 1) & 1);
-          st_volatile_s32(&s_tag[lane], gp);
-          uint8_t* dst = ring + lane * kStageBytes;
-          if (P.diag == 2) {
-            mbar_arrive(&full[lane]);
-            continue;
-          }
-          const size_t src = (size_t)s_ent[j].page * page_stride + head_off;
-          mbar_arrive_expect_tx(&full[lane], kStageBytes);
-          bulk_g2s(dst, P.kplane + src, kStageBytes / 2, &full[lane]);
-          bulk_g2s(dst + kStageBytes / 2, P.vplane + src, kStageBytes / 2, &full[lane]);
+      const int n_ent = si->n_entries, n_mem = si->n_mem, kvh = si->kvh;
+      const int64_t eoff = si->entry_off;
+      PageRef* se = s_ent0 + buf * kMaxEntries;
+      for (int j = lane; j < n_ent; j += 32) {
+        const PageRef ref = P.arena[eoff + j];
+        se[j] = ref;
+        if (j < kPrefetch) {  // the TMA thread prefetches the rest, kPrefetch pages ahead
+          const size_t pf = ((size_t)ref.page * P.kv_heads + kvh) * kPageTokens * kHeadDim;
+          prefetch_l2(P.kplane + pf, kPageBytes);
+          prefetch_l2(P.vplane + pf, kPageBytes);
         }
-        mbar_arrive(&item_empty[buf]);  // this lane no longer reads the item's entry list
-        gbase += n_entries;
+      }
+      __syncwarp();
+      const uint32_t half_bytes = (uint32_t)P.R * 128;
+      if (lane == 0) mbar_arrive_expect_tx(&item_full[buf], 2u * half_bytes * (uint32_t)n_mem);
+      __syncwarp();
+      if (lane < 2 * n_mem) {
+        const int m = lane >> 1, h = lane & 1;
+        const int b = si->members[m];
+        uint8_t* dst = smem + kOffQ + buf * kQBytes + h * kQHalf + m * half_bytes;
+        const __nv_bfloat16* src = P.q_tile + (((size_t)b * P.kv_heads + kvh) * 2 + h) * (size_t)P.R * 64;
+        bulk_g2s(dst, src, half_bytes, &item_full[buf]);
       }
     }
-    return;
-  }
-
-  // ---------------- consumer warps ----------------
-  int gbase = 0;
-  unsigned long long* tr = P.trace ? P.trace + (size_t)blockIdx.x * 64 * 4 : nullptr;
-  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
-  for (int iter = 0;; ++iter) {
-    const int buf = iter & 1;
-    mbar_wait(&item_full[buf], (iter >> 1) & 1);
-    const ItemSlot is = s_item[buf];
-    if (tr && threadIdx.x == 0 && iter < 62) { tr[4 + iter * 4] = globaltimer(); tr[5 + iter * 4] = is.it.n_entries | ((unsigned long long)is.it.nt << 32); }
-    if (!is.valid) break;
-    const uint8_t* sq = smem + kOffQ + buf * kSmemQ;
-    const PageRef* s_ent = reinterpret_cast<const PageRef*>(smem + kOffEnt + buf * kSmemEnt);
-    const int nt = is.it.nt;
-    const int G = row_groups(nt);
-    const int n_streams = kConsumerWarps / G;
-    const int stream = warp / G, half = warp % G;
-    const int nta = (nt + 1) / 2;
-    const int nt0 = G == 1 ? 0 : (half ? nta : 0);
-    const int ntw = G == 1 ? nt : (half ? nt - nta : nta);
-    // each stage is released by 2 arrivals: both warps of a pair, or one warp arriving twice
-    const int ecount = G == 1 ? 2 : 1;
-    switch (ntw) {
-      case 1: consume_rows<1>(P, is.it, gbase, stream, n_streams, nt0, ring, sq, s_ent, full, empty, ecount, s_ml, s_o, s_tag); break;
-      case 2: consume_rows<2>(P, is.it, gbase, stream, n_streams, nt0, ring, sq, s_ent, full, empty, ecount, s_ml, s_o, s_tag); break;
-      default: consume_rows<3>(P, is.it, gbase, stream, n_streams, nt0, ring, sq, s_ent, full, empty, ecount, s_ml, s_o, s_tag); break;
+  } else if (warp == kWarpTma) {
+    // ---------------- TMA: keeps the block ring full across work units ----------------
+    // One issuing thread, in consumption order.  A block = up to 4 pages: each page's K half-rows
+    // land contiguously per half ([2][64 tokens][128 B], one N=64 UMMA operand), V page-head blocks
+    // as stored.  HBM latency beyond the ring is hidden by L2 prefetches kPrefetch pages ahead.
+    if (lane == 0) {
+      int g = 0;
+      const size_t page_stride = (size_t)P.kv_heads * kPageTokens * kHeadDim;
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        mbar_wait(&item_full[buf], (i >> 1) & 1);
+        const WorkItem* si = &s_item[buf];
+        if (!si->valid) break;
+        const int n_ent = si->n_entries;
+        const size_t head_off = (size_t)si->kvh * kPageTokens * kHeadDim;
+        const PageRef* se = s_ent0 + buf * kMaxEntries;
+        for (int e0 = 0; e0 < n_ent; e0 += kBlkPages, ++g) {
+          const int sl = g % kSlots, np = min(kBlkPages, n_ent - e0);
+          for (int j = e0 + kPrefetch; j < min(e0 + kPrefetch + kBlkPages, n_ent); ++j) {
+            const size_t pf = (size_t)se[j].page * page_stride + head_off;
+            prefetch_l2(P.kplane + pf, kPageBytes);
+            prefetch_l2(P.vplane + pf, kPageBytes);
+          }
+          if (g >= kSlots) mbar_wait(&empty[sl], ((g / kSlots) - 1) & 1);
+          uint8_t* dk = ring + sl * kSlotBytes;
+          mbar_arrive_expect_tx(&full[sl], (uint32_t)np * 2 * kPageBytes);
+          for (int p = 0; p < np; ++p) {
+            const size_t src = (size_t)se[e0 + p].page * page_stride + head_off;
+            bulk_g2s(dk + p * (kPageBytes / 2), P.kplane + src, kPageBytes / 2, &full[sl]);
+            bulk_g2s(dk + kSlotK / 2 + p * (kPageBytes / 2), P.kplane + src + kPageTokens * 64, kPageBytes / 2,
+                     &full[sl]);
+            bulk_g2s(dk + kSlotK + p * kPageBytes, P.vplane + src, kPageBytes, &full[sl]);
+          }
+        }
+        mbar_arrive(&slot_empty[buf]);
+      }
     }
-    // Q buffer and entry list of this item are no longer read: hand them back to the stager.
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&item_empty[buf]);
-    if (tr && threadIdx.x == 0 && iter < 62) tr[6 + iter * 4] = globaltimer();
-    merge_streams(P, is, n_streams, s_ml, s_o);
-    if (tr && threadIdx.x == 0 && iter < 62) tr[7 + iter * 4] = globaltimer();
-    gbase += is.it.n_entries;
-  }
-}
-
-// RoPE pre-pass: rotate every query once (toy_model.cpp:30-41 at the handle's position) so the
-// decode kernel can bulk-copy Q rows; thread 0 also resets the work-item counter.
-__global__ void rope_q_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pos, int n,
-                              int q_heads, const RopeTable rt, __nv_bfloat16* __restrict__ q_rot, int* counter) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one 16 B chunk (4 pairs)
-  if (x == 0) *counter = 0;
-  if (x >= (int64_t)n * q_heads * 16) return;
-  const int c = (int)(x & 15);
-  const int b = (int)(x / (16 * q_heads));
-  uint4 v = *reinterpret_cast<const uint4*>(q + x * 8);
-  __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
-  const int p = pos[b];
+  } else if (warp == kWarpMma) {
+    // ---------------- MMA issuer (one thread; kept tight: ~50 cycles per tcgen05.mma) ----------------
+    if (lane == 0) {
+      const uint64_t qdesc0 = tc::sw128_desc(smem_u32(smem + kOffQ), 16, 1024);
+      const uint64_t kdesc0 = tc::sw128_desc(smem_u32(ring), 16, 1024);
+      const uint64_t vdesc0 = tc::sw128_desc(smem_u32(ring + kSlotK), kPageBytes / 2, 1024);
+      // units opened by the QK cursor are remembered for the PV cursor (QK runs <= 2 blocks ahead)
+      int f_ent[4], f_valid[4];
+      int q_i = -1, q_blk = 0, q_nblk = 0, q_valid = 1;
+      int qg = 0;  // global block index of the next QK
+      auto issue_qk = [&]() {
+        while (q_valid && q_blk >= q_nblk) {
+          ++q_i;
+          const int ub = q_i & 1;
+          mbar_wait(&item_full[ub], (q_i >> 1) & 1);
+          const WorkItem* si = &s_item[ub];
+          q_valid = si->valid;
+          const int ne = q_valid ? si->n_entries : 0;
+          q_nblk = (ne + kBlkPages - 1) / kBlkPages;
+          q_blk = 0;
+          f_ent[q_i & 3] = ne;
+          f_valid[q_i & 3] = q_valid;
+          if (q_valid) {
+            // the unit's Q tile smem -> TMEM once (QK then reads A from TMEM: no per-block re-read
+            // of Q from shared memory)
+            tc::fence_after();
+            const uint64_t qd = qdesc0 + (uint64_t)((ub * kQBytes) >> 4);
+            const uint32_t qt = tmem + kColQ + ub * 64;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    float cs, sn;
-    rope_cs(p, rt.inv[c * 4 + j], cs, sn);
-    const float2 ab = __bfloat1622float2(h2[j]);
-    h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
+            for (int k = 0; k < 8; ++k)
+              tc::cp_128x256b(qt + k * 8, qd + (uint64_t)(((k >> 2) * kQHalf + (k & 3) * 32) >> 4));
+          }
+        }
+        if (!q_valid) return;
+        const int sl = qg % kSlots;
+        if (TRACE && qg < 64) P.trace[blockIdx.x * kTraceWords + 128 + qg] = globaltimer();
+        mbar_wait(&full[sl], (qg / kSlots) & 1);
+        tc::fence_after();
+        const uint32_t qt = tmem + kColQ + (q_i & 1) * 64;
+        const uint64_t kd = kdesc0 + (uint64_t)(sl * (kSlotBytes >> 4));
+        const uint32_t dcol = tmem + kColS + (qg & 1) * kBlkCols;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          tc::mma_ts(dcol, qt + k * 8, kd + (uint64_t)(((k >> 2) * (kSlotK / 2) + (k & 3) * 32) >> 4), kIdQK,
+                     k > 0 ? 1u : 0u);
+        tc::mma_commit(&s_full[qg & 1]);
+        if (q_blk == q_nblk - 1) tc::mma_commit(&slot_empty[q_i & 1]);  // Q buffer no longer read
+        if (TRACE && qg < 64) P.trace[blockIdx.x * kTraceWords + 192 + qg] = globaltimer();
+        ++q_blk;
+        ++qg;
+      };
+      issue_qk();
+      issue_qk();
+      int p_i = 0, p_blk = 0;
+      for (int pg = 0;; ++pg) {
+        // PV cursor: next block (units already opened by the QK cursor)
+        while (f_valid[p_i & 3] && p_blk * kBlkPages >= f_ent[p_i & 3]) {
+          ++p_i;
+          p_blk = 0;
+        }
+        if (!f_valid[p_i & 3]) break;
+        const int n_ent = f_ent[p_i & 3];
+        mbar_wait(&p_full[pg & 1], (pg >> 1) & 1);
+        if (TRACE && pg < 64) P.trace[blockIdx.x * kTraceWords + 480 + pg] = globaltimer();
+        if (p_blk == 0 && p_i >= 1) mbar_wait(o_empty, (p_i - 1) & 1);  // epilogue drained O
+        tc::fence_after();
+        const uint32_t ocol = tmem + kColO + (pg & 1) * 128;  // O of this block parity
+        const uint32_t pcol = tmem + kColS + (pg & 1) * kBlkCols;
+        const uint64_t vd = vdesc0 + (uint64_t)((pg % kSlots) * (kSlotBytes >> 4));
+        const int np = n_ent - p_blk * kBlkPages;
+        // blocks 0 and 1 of a unit open O_0 / O_1
+        tc::mma_ts(ocol, pcol, vd, kIdPV, p_blk >= 2 ? 1u : 0u);
+        if (np > 1) tc::mma_ts(ocol, pcol + 8, vd + (uint64_t)(kPageBytes >> 4), kIdPV, 1u);
+        if (np > 2) tc::mma_ts(ocol, pcol + 16, vd + (uint64_t)((2 * kPageBytes) >> 4), kIdPV, 1u);
+        if (np > 3) tc::mma_ts(ocol, pcol + 24, vd + (uint64_t)((3 * kPageBytes) >> 4), kIdPV, 1u);
+        tc::mma_commit(&empty[pg % kSlots]);  // also certifies PV(pg) to the softmax (O rescale)
+        if (np <= kBlkPages) tc::mma_commit(o_full);  // last block of the unit
+        ++p_blk;
+        issue_qk();
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // ---------------- softmax: two warpgroups ping-pong over the block parity ----------------
+    // WG par (warps 4-7: par 0, 8-11: par 1) owns blocks g with g & 1 == par: S buffer par,
+    // O buffer par and its own (m, l) per row.  Thread = query row = TMEM lane.
+    const int par = (warp >> 2) - 1;
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    const uint32_t ocol = lane_base + kColO + par * 128;
+    const uint32_t scol = lane_base + kColS + par * kBlkCols;
+    int g = 0;
+    for (int i = 0;; ++i) {
+      const int buf = i & 1;
+      mbar_wait(&item_full[buf], (i >> 1) & 1);
+      const WorkItem* si = &s_item[buf];
+      if (!si->valid) {
+        if (i >= 1) mbar_wait(o_empty, (i - 1) & 1);
+        if (par == 0 && q == 0 && lane == 0) s_ep->valid = 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(stat_full);
+        break;
+      }
+      const int n_ent = si->n_entries, n_mem = si->n_mem;
+      const bool warp_active = q * 32 < n_mem * P.R;
+      const int mi = r / P.R, hl = r % P.R;
+      const bool row_active = mi < n_mem && hl < P.gqa;
+      const PageRef* se = s_ent0 + buf * kMaxEntries;
+      const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
+      float m_ref = -INFINITY, l = 0.f;
+      bool first = true;  // first block of this parity in the unit: O_par not yet written
+      for (int blk = 0; blk < nblk; ++blk, ++g) {
+        if ((g & 1) != par) continue;
+        mbar_wait(&s_full[par], (g >> 1) & 1);
+        tc::fence_after();
+        if (TRACE && q == 0 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + g] = globaltimer();
+        if (warp_active) {
+          const int e0 = blk * kBlkPages;
+          // valid slots per page: ragged unit head / tail pages and partial pages; rows without a
+          // query see nothing
+          uint32_t vm[kBlkPages];
+          bool full_blk = row_active;
+#pragma unroll
+          for (int p = 0; p < kBlkPages; ++p) {
+            vm[p] = 0u;
+            if (row_active && e0 + p < n_ent) {
+              const PageRef ref = se[e0 + p];
+              vm[p] = ((1u << ref_count(ref)) - 1u) << ref_begin(ref);
+            }
+            full_blk &= vm[p] == 0xFFFFu;
+          }
+          const bool masked = !__all_sync(0xffffffffu, full_blk);
+          // S in two 32-column halves (register budget); masked slots -> -inf
+          auto load_half = [&](int h, float* v) {
+            tc::tmem_ld32(scol + h * 32, v);
+            tc::tmem_wait_ld();
+            if (masked) {
+#pragma unroll
+              for (int t = 0; t < 32; ++t) v[t] = ((vm[2 * h + (t >> 4)] >> (t & 15)) & 1u) ? v[t] : -INFINITY;
+            }
+          };
+          uint32_t pk[kBlkCols / 2];
+          auto exp_block = [&](float mu) {
+            float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float v[32];
+              load_half(h, v);
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const float p0 = fast_exp2(fmaf(v[2 * c], P.scale_log2, -mu));
+                const float p1 = fast_exp2(fmaf(v[2 * c + 1], P.scale_log2, -mu));
+                l0 += p0;
+                l1 += p1;
+                pk[h * 16 + c] = pack_bf16(p0, p1);
+              }
+            }
+            return l0 + l1;
+          };
+          // Fast path: exponentiate against the row's current reference; the reference moves only
+          // on the first block or when a block's mass exceeds kSumLimit (P <= kSumLimit is exact
+          // enough in bf16 and far from fp32 overflow), so no per-block max is needed.  S stays
+          // intact in TMEM until P is stored, so the slow path can re-read it.
+          bool need = row_active && m_ref == -INFINITY;
+          float ls = 0.f;
+          if (!__any_sync(0xffffffffu, need)) {
+            ls = exp_block(row_active ? m_ref : 0.f);
+            need = ls > kSumLimit;
+          }
+          if (__any_sync(0xffffffffu, need)) {
+            float mx = -INFINITY;
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+              float v[32];
+              load_half(h, v);
+#pragma unroll
+              for (int c = 0; c < 32; ++c) mx = fmaxf(mx, v[c]);
+            }
+            mx *= P.scale_log2;  // raw-score max into the log2 domain (scale > 0 keeps order)
+            const float nref = need ? fmaxf(m_ref, mx) : m_ref;
+            const bool resc = need && m_ref != -INFINITY;
+            const float alpha = resc ? fast_exp2(m_ref - nref) : 1.f;
+            if (!first && __any_sync(0xffffffffu, resc)) {
+              // O_par holds this parity's earlier blocks once PV(g-2) has completed (its slot's empty commit)
+              mbar_wait(&empty[(g - 2) % kSlots], ((g - 2) / kSlots) & 1);
+              tc::fence_after();
+#pragma unroll 1
+              for (int c = 0; c < 4; ++c) {
+                float o[32];
+                tc::tmem_ld32(ocol + c * 32, o);
+                tc::tmem_wait_ld();
+#pragma unroll
+                for (int e = 0; e < 32; ++e) o[e] *= alpha;
+                tc::tmem_st32(ocol + c * 32, o);
+              }
+            }
+            l *= alpha;
+            m_ref = nref;
+            ls = exp_block(m_ref == -INFINITY ? 0.f : m_ref);
+          }
+          l += ls;
+          tc::tmem_st32u(scol, pk);
+          tc::tmem_wait_st();
+        }
+        first = false;
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[par]);
+        if (TRACE && q == 0 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 64 + g] = globaltimer();
+      }
+      // hand (m, l) and the unit header to the epilogue, release the unit slot
+      if (i >= 1) mbar_wait(o_empty, (i - 1) & 1);
+      s_stat[par * 128 + r] = make_float2(m_ref, first ? 0.f : l);
+      if (par == 0 && q == 0 && lane < kItemInts) reinterpret_cast<int*>(s_ep)[lane] = reinterpret_cast<const int*>(si)[lane];
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(stat_full);
+        mbar_arrive(&slot_empty[buf]);
+      }
+    }
+  } else if (warp >= 12) {
+    // ---------------- epilogue warpgroup: merge O_0 / O_1, output or split-KV partial ----------------
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    for (int i = 0;; ++i) {
+      mbar_wait(stat_full, i & 1);
+      if (!s_ep->valid) break;
+      const int n_mem = s_ep->n_mem, kvh = s_ep->kvh;
+      const int mi = r / P.R, hl = r % P.R;
+      const bool active = mi < n_mem && hl < P.gqa;
+      const bool warp_active = q * 32 < n_mem * P.R;
+      const int b = active ? s_ep->members[mi] : 0;
+      const int64_t slot = s_ep->slot_base + mi;
+      const float2 ml0 = s_stat[r], ml1 = s_stat[128 + r];
+      mbar_wait(o_full, i & 1);
+      tc::fence_after();
+      if (TRACE && r == 0 && i < 32) P.trace[blockIdx.x * kTraceWords + 256 + i] = globaltimer();
+      // merge the two parity partials of this row (a parity without blocks has l == 0)
+      const bool h0 = ml0.y > 0.f, h1 = ml1.y > 0.f;
+      const float mm = fmaxf(h0 ? ml0.x : -INFINITY, h1 ? ml1.x : -INFINITY);
+      const float w0 = h0 ? fast_exp2(ml0.x - mm) : 0.f, w1 = h1 ? fast_exp2(ml1.x - mm) : 0.f;
+      const float2 ml = make_float2(mm, w0 * ml0.y + w1 * ml1.y);
+      const int head = kvh * P.gqa + hl;
+      const int nslots = active ? P.slot_cnt[b] : 0;
+      const int64_t orow = (int64_t)b * P.q_heads + head;
+      if (warp_active) {
+        const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float o[32], o1[32];
+          tc::tmem_ld32(lane_base + kColO + c * 32, o);
+          tc::tmem_ld32(lane_base + kColO + 128 + c * 32, o1);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = (h0 ? w0 * o[e] : 0.f) + (h1 ? w1 * o1[e] : 0.f);
+          if (active) {
+            if (nslots == 1) {
+              store_row(P, orow, c, o, inv);
+            } else {
+              float4* dst = reinterpret_cast<float4*>(P.part_o + (slot * P.q_heads + head) * kHeadDim + c * 32);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) __stcg(dst + e, make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]));
+            }
+          }
+        }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(o_empty);
+      if (active && nslots > 1) __stcg(P.part_ml + slot * P.q_heads + head, ml);
+      if (TRACE && r == 0 && i < 32) P.trace[blockIdx.x * kTraceWords + 288 + i] = globaltimer();
+    }
   }
-  *reinterpret_cast<uint4*>(q_rot + x * 8) = v;
+  tc::fence_before();
+  __syncthreads();
+  if (warp == kWarpMma) {
+    tc::fence_after();
+    tc::tmem_dealloc(tmem, kTmemCols);
+  }
 }
 
-// Merge every handle's partials (log-sum-exp) into the output; one warp per (handle, q head),
-// float4 per lane, single pass with online rescaling.
+// Split-KV combine for handles with more than one partial slot: one warp per (handle, q head),
+// float4 per lane, log-sum-exp over the handle's slots (single-slot handles were written by the
+// decode epilogue directly).
 __global__ void combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
-                               const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ slot_idx, int n,
-                               int q_heads, void* __restrict__ out, int out_f32) {
+                               const int32_t* __restrict__ multi, int n_multi, const int32_t* __restrict__ slot_ptr,
+                               const int32_t* __restrict__ slot_idx, int q_heads, void* __restrict__ out,
+                               int out_f32) {
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= n * q_heads) return;
-  const int b = wid / q_heads, h = wid % q_heads;
+  if (wid >= n_multi * q_heads) return;
+  const int b = multi[wid / q_heads], h = wid % q_heads;
   const int s0 = slot_ptr[b], s1 = slot_ptr[b + 1];
-  float m = -INFINITY, l = 0.f;
+  float m = -INFINITY;
+  for (int s = s0; s < s1; ++s) m = fmaxf(m, part_ml[(int64_t)slot_idx[s] * q_heads + h].x);
+  const float mu = m == -INFINITY ? 0.f : m;
+  float l = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s = s0; s < s1; ++s) {
     const int64_t sl = slot_idx[s];
     const float2 ml = part_ml[sl * q_heads + h];
+    const float w = fast_exp2(ml.x - mu);
     const float4 v = *reinterpret_cast<const float4*>(&part_o[(sl * q_heads + h) * kHeadDim + lane * 4]);
-    const float mn = fmaxf(m, ml.x);
-    if (mn == -INFINITY) continue;
-    const float a = fast_exp2(m - mn), w = fast_exp2(ml.x - mn);
-    acc.x = acc.x * a + w * v.x;
-    acc.y = acc.y * a + w * v.y;
-    acc.z = acc.z * a + w * v.z;
-    acc.w = acc.w * a + w * v.w;
-    l = l * a + w * ml.y;
-    m = mn;
+    acc.x += w * v.x;
+    acc.y += w * v.y;
+    acc.z += w * v.z;
+    acc.w += w * v.w;
+    l += w * ml.y;
   }
   const float inv = l > 0.f ? 1.f / l : 0.f;
   const int64_t at = ((int64_t)b * q_heads + h) * kHeadDim + lane * 4;
@@ -507,13 +572,45 @@ __global__ void combine_kernel(const float* __restrict__ part_o, const float2* _
     *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + at) =
         make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
   } else {
-    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
     uint2 pk;
-    pk.x = *reinterpret_cast<uint32_t*>(&lo);
-    pk.y = *reinterpret_cast<uint32_t*>(&hi);
+    pk.x = pack_bf16(acc.x * inv, acc.y * inv);
+    pk.y = pack_bf16(acc.z * inv, acc.w * inv);
     *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + at) = pk;
   }
+}
+
+// RoPE pre-pass: rotates every query once (toy_model.cpp:30-41 at the handle's position) and
+// writes it as the decode kernel's Q operand tile [n][kv_heads][2 halves][R rows][64 dims],
+// SWIZZLE_128B (chunk c of row hl at c ^ (hl & 7)); rows hl >= gqa are zero.  Thread 0 also
+// resets the work counter.  One thread per 16-byte chunk.
+__global__ void rope_q_tile_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pos, int n,
+                                   int kv_heads, int gqa, int R, const RopeTable rt, __nv_bfloat16* __restrict__ tile,
+                                   int* counter) {
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x == 0) *counter = 0;
+  const int64_t total = (int64_t)n * kv_heads * R * 16;
+  if (x >= total) return;
+  const int c = (int)(x & 15);           // 16-byte chunk of the 128-dim row
+  const int hl = (int)((x >> 4) % R);
+  const int64_t bk = (x >> 4) / R;       // b * kv_heads + kvh
+  const int b = (int)(bk / kv_heads), kvh = (int)(bk % kv_heads);
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (hl < gqa) {
+    const int head = kvh * gqa + hl;
+    v = *reinterpret_cast<const uint4*>(q + ((int64_t)b * kv_heads * gqa + head) * kHeadDim + c * 8);
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+    const int p = pos[b];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float cs, sn;
+      rope_cs(p, rt.inv[c * 4 + j], cs, sn);
+      const float2 ab = __bfloat1622float2(h2[j]);
+      h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
+    }
+  }
+  const int half = c >> 3, cc = c & 7;
+  const int64_t dst = ((bk * 2 + half) * R + hl) * 64 + ((cc ^ (hl & 7)) << 3);
+  *reinterpret_cast<uint4*>(tile + dst) = v;
 }
 
 }  // namespace
@@ -523,32 +620,36 @@ struct DecodePlanCache {
   std::vector<int64_t> sig;  // per handle: n_entries, lineage size
   int q_heads = 0;
   // host plan
-  std::vector<WorkItem> items;
-  std::vector<int32_t> slot_ptr, slot_idx;
+  std::vector<WorkItem> units;
+  std::vector<int32_t> slot_ptr, slot_idx, slot_cnt, multi;  // multi: handles with > 1 slot
   int32_t n_slots = 0;
   mv_decode_plan_info info{};
   // device copies
-  WorkItem* d_items = nullptr;
-  int32_t *d_slot_ptr = nullptr, *d_slot_idx = nullptr;
-  __nv_bfloat16* d_q_rot = nullptr;
+  WorkItem* d_units = nullptr;
+  int32_t *d_slot_ptr = nullptr, *d_slot_idx = nullptr, *d_slot_cnt = nullptr, *d_multi = nullptr;
+  __nv_bfloat16* d_q_tile = nullptr;
   float* d_part_o = nullptr;
   float2* d_part_ml = nullptr;
-  size_t cap_items = 0, cap_q_rot = 0, cap_ptr = 0, cap_idx = 0, cap_slots = 0;
+  size_t cap_units = 0, cap_q = 0, cap_ptr = 0, cap_idx = 0, cap_cnt = 0, cap_multi = 0, cap_slots = 0;
   bool smem_set = false;
   int num_sms = 148;
   int* d_counter = nullptr;
   unsigned long long* d_trace = nullptr;
   ~DecodePlanCache() {
-    cudaFree(d_counter);
     cudaFree(d_trace);
-    cudaFree(d_items);
-    cudaFree(d_q_rot);
+    cudaFree(d_counter);
+    cudaFree(d_units);
+    cudaFree(d_q_tile);
     cudaFree(d_slot_ptr);
     cudaFree(d_slot_idx);
+    cudaFree(d_slot_cnt);
+    cudaFree(d_multi);
     cudaFree(d_part_o);
     cudaFree(d_part_ml);
   }
 };
+
+void destroy_plan(DecodePlanCache* p) { delete p; }
 
 template <typename T>
 static mv_status ensure_dev(T*& p, size_t& cap, size_t n) {
@@ -561,12 +662,20 @@ static mv_status ensure_dev(T*& p, size_t& cap, size_t n) {
   return MV_OK;
 }
 
-static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, int n, int q_heads, int gqa) {
-  pc.items.clear();
+static int rows_per_member(int gqa) {
+  int R = 8;
+  while (R < gqa) R *= 2;
+  return R;
+}
+
+static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, int n, int kv_heads, int gqa,
+                       int num_sms) {
+  pc.units.clear();
   std::vector<std::vector<int32_t>> slots_of(n);
   int32_t n_slots = 0;
   int64_t unique_tokens = 0, naive_tokens = 0;
-  const int max_members = std::max(1, std::min(kMaxMembers, (kMaxNT * 8) / gqa));
+  const int R = rows_per_member(gqa);
+  const int max_members = std::max(1, std::min(kMaxMem, 128 / R));
 
   // group id -> member batch indices (in batch order)
   std::unordered_map<uint64_t, std::vector<int32_t>> group_members;
@@ -577,34 +686,20 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
     for (auto& lg : recs[b]->lineage) group_members[lg.group].push_back(b);
   }
 
-  auto emit_unit = [&](int64_t src_off, int32_t e0, int32_t e1, const std::vector<int32_t>& mem, int64_t tokens) {
+  // cascade units: (arena offset, entry range, members)
+  struct Seg {
+    int64_t off;
+    int32_t e0, e1;
+    std::vector<int32_t> mem;
+  };
+  std::vector<Seg> segs;
+  int64_t total_pages = 0;
+  auto add_seg = [&](int64_t off, int32_t e0, int32_t e1, std::vector<int32_t> mem, int64_t tokens) {
     if (e1 <= e0 || mem.empty()) return;
     unique_tokens += tokens;
-    const int32_t npg = e1 - e0;
-    const int32_t nchunks = (npg + kChunkPages - 1) / kChunkPages;
-    for (int32_t c = 0; c < nchunks; ++c) {
-      const int32_t c0 = e0 + (int32_t)((int64_t)npg * c / nchunks);
-      const int32_t c1 = e0 + (int32_t)((int64_t)npg * (c + 1) / nchunks);
-      for (size_t m0 = 0; m0 < mem.size(); m0 += max_members) {
-        const int32_t nm = (int32_t)std::min<size_t>(max_members, mem.size() - m0);
-        WorkItem w;
-        std::memset(&w, 0, sizeof w);
-        w.entry_off = src_off + c0;
-        w.n_entries = c1 - c0;
-        w.n_mem = nm;
-        w.slot_base = n_slots;
-        w.nt = (nm * gqa + 7) / 8;
-        for (int32_t k = 0; k < nm; ++k) {
-          w.members[k] = mem[m0 + k];
-          slots_of[mem[m0 + k]].push_back(n_slots + k);
-        }
-        n_slots += nm;
-        pc.items.push_back(w);
-      }
-    }
+    total_pages += e1 - e0;
+    segs.push_back({off, e0, e1, std::move(mem)});
   };
-
-  // shared cascade units: one per lineage group with >= 2 decoding holders
   std::unordered_map<uint64_t, bool> done;
   for (int b = 0; b < n; ++b) {
     const HandleRec* r = recs[b];
@@ -614,7 +709,7 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
       auto& mem = group_members[lg.group];
       if (mem.size() >= 2 && !done[lg.group]) {
         done[lg.group] = true;
-        emit_unit(r->arena_off, prev_e, lg.entries, mem, lg.tokens - prev_t);
+        add_seg(r->arena_off, prev_e, lg.entries, mem, lg.tokens - prev_t);
       }
       if (mem.size() >= 2) {
         prev_e = lg.entries;
@@ -622,19 +717,67 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
       }
     }
     // private remainder (single-holder lineage segments coalesce here)
-    emit_unit(r->arena_off, prev_e, r->n_entries(), std::vector<int32_t>{b}, r->n_tokens() - prev_t);
+    add_seg(r->arena_off, prev_e, r->n_entries(), std::vector<int32_t>{b}, r->n_tokens() - prev_t);
   }
 
+  // split-KV chunk size: <= 64 pages, small enough for >= ~6 waves of work over the SMs
+  const int64_t target_units = (int64_t)num_sms * 6;
+  int chunk = kMaxEntries;
+  while (chunk > 16 && total_pages * kv_heads / chunk < target_units) chunk /= 2;
+
+  std::vector<WorkItem> items;
+  for (const Seg& s : segs) {
+    const int32_t npg = s.e1 - s.e0;
+    const int32_t nchunks = (npg + chunk - 1) / chunk;
+    for (int32_t c = 0; c < nchunks; ++c) {
+      const int32_t c0 = s.e0 + (int32_t)((int64_t)npg * c / nchunks);
+      const int32_t c1 = s.e0 + (int32_t)((int64_t)npg * (c + 1) / nchunks);
+      const int ngroups = (int)((s.mem.size() + max_members - 1) / max_members);
+      for (int gi = 0; gi < ngroups; ++gi) {
+        // balanced member groups
+        const size_t m0 = s.mem.size() * gi / ngroups, m1 = s.mem.size() * (gi + 1) / ngroups;
+        WorkItem w;
+        std::memset(&w, 0, sizeof w);
+        w.entry_off = s.off + c0;
+        w.n_entries = c1 - c0;
+        w.n_mem = (int32_t)(m1 - m0);
+        w.slot_base = n_slots;
+        w.valid = 1;
+        for (size_t k = m0; k < m1; ++k) {
+          w.members[k - m0] = s.mem[k];
+          slots_of[s.mem[k]].push_back(n_slots + (int32_t)(k - m0));
+        }
+        n_slots += w.n_mem;
+        items.push_back(w);
+      }
+    }
+  }
+  // longest-first (then widest-first) for the dynamic queue: the tail is made of the smallest units
+  std::stable_sort(items.begin(), items.end(), [](const WorkItem& a, const WorkItem& b) {
+    return a.n_entries != b.n_entries ? a.n_entries > b.n_entries : a.n_mem > b.n_mem;
+  });
+  pc.units.reserve(items.size() * kv_heads);
+  for (const WorkItem& w : items)
+    for (int h = 0; h < kv_heads; ++h) {
+      WorkItem u = w;
+      u.kvh = h;
+      pc.units.push_back(u);
+    }
+
   pc.slot_ptr.assign(n + 1, 0);
+  pc.slot_cnt.assign(n, 0);
   pc.slot_idx.clear();
+  pc.multi.clear();
   for (int b = 0; b < n; ++b) {
-    pc.slot_ptr[b + 1] = pc.slot_ptr[b] + (int32_t)slots_of[b].size();
+    pc.slot_cnt[b] = (int32_t)slots_of[b].size();
+    pc.slot_ptr[b + 1] = pc.slot_ptr[b] + pc.slot_cnt[b];
+    if (pc.slot_cnt[b] > 1) pc.multi.push_back(b);
     pc.slot_idx.insert(pc.slot_idx.end(), slots_of[b].begin(), slots_of[b].end());
   }
   pc.n_slots = n_slots;
-  pc.info.units = 0;
-  pc.info.chunks = 0;
-  pc.info.work_items = (int32_t)pc.items.size();
+  pc.info.units = (int32_t)segs.size();
+  pc.info.chunks = chunk;
+  pc.info.work_items = (int32_t)items.size();
   pc.info.partial_slots = n_slots;
   pc.info.unique_kv_tokens = unique_tokens;
   pc.info.naive_kv_tokens = naive_tokens;
@@ -654,12 +797,21 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   if (n <= 0) return n == 0 ? MV_OK : fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_decode: n < 0");
   if (q_heads <= 0 || q_heads % cfg.kv_heads) return fail(MV_ERR_INVALID_ARGUMENT, "q_heads % kv_heads != 0");
   const int gqa = q_heads / cfg.kv_heads;
-  if (gqa > kMaxNT * 8) return fail(MV_ERR_INVALID_ARGUMENT, "GQA group larger than 40 heads");
+  if (gqa > 128) return fail(MV_ERR_INVALID_ARGUMENT, "GQA group larger than 128 heads");
   if (!d_q || !d_positions || !d_out) return fail(MV_ERR_INVALID_ARGUMENT, "null buffer");
   if (out_dtype != 0 && out_dtype != 1) return fail(MV_ERR_INVALID_ARGUMENT, "out_dtype must be 0 (bf16) or 1 (fp32)");
 
   if (!st.plan) st.plan = new DecodePlanCache();
   DecodePlanCache& pc = *st.plan;
+  if (!pc.smem_set) {
+    MV_CUDA_TRY(cudaFuncSetAttribute(decode_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    MV_CUDA_TRY(cudaFuncSetAttribute(decode_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    int dev = 0;
+    MV_CUDA_TRY(cudaGetDevice(&dev));
+    MV_CUDA_TRY(cudaDeviceGetAttribute(&pc.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    MV_CUDA_TRY(cudaMalloc(&pc.d_counter, sizeof(int)));
+    pc.smem_set = true;
+  }
   // plan signature: the handle list plus each table's entry count and lineage depth
   std::vector<int64_t> sig(2 * (size_t)n);
   for (int b = 0; b < n; ++b) {
@@ -673,82 +825,92 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
                     std::equal(pc.handles.begin(), pc.handles.end(), hs) && pc.sig == sig;
   cudaStream_t stream = st.stream();
   if (!same) {
-    build_plan(st, pc, hs, n, q_heads, gqa);
+    build_plan(st, pc, hs, n, cfg.kv_heads, gqa, pc.num_sms);
     pc.handles.assign(hs, hs + n);
     pc.sig = sig;
     pc.q_heads = q_heads;
-    if (mv_status e = ensure_dev(pc.d_items, pc.cap_items, pc.items.size())) return e;
+    if (mv_status e = ensure_dev(pc.d_units, pc.cap_units, pc.units.size())) return e;
     if (mv_status e = ensure_dev(pc.d_slot_ptr, pc.cap_ptr, pc.slot_ptr.size())) return e;
     if (mv_status e = ensure_dev(pc.d_slot_idx, pc.cap_idx, std::max<size_t>(1, pc.slot_idx.size()))) return e;
-    size_t old_slots = pc.cap_slots;
-    if (mv_status e = ensure_dev(pc.d_part_ml, pc.cap_slots, (size_t)pc.n_slots * q_heads)) return e;
+    if (mv_status e = ensure_dev(pc.d_slot_cnt, pc.cap_cnt, pc.slot_cnt.size())) return e;
+    if (mv_status e = ensure_dev(pc.d_multi, pc.cap_multi, std::max<size_t>(1, pc.multi.size()))) return e;
+    if (!pc.multi.empty())
+      MV_CUDA_TRY(cudaMemcpyAsync(pc.d_multi, pc.multi.data(), sizeof(int32_t) * pc.multi.size(),
+                                  cudaMemcpyHostToDevice, stream));
+    const size_t old_slots = pc.cap_slots;
+    if (mv_status e = ensure_dev(pc.d_part_ml, pc.cap_slots, std::max<size_t>(1, (size_t)pc.n_slots * q_heads)))
+      return e;
     if (pc.cap_slots != old_slots || !pc.d_part_o) {
       cudaFree(pc.d_part_o);
+      pc.d_part_o = nullptr;
       MV_CUDA_TRY(cudaMalloc(&pc.d_part_o, sizeof(float) * pc.cap_slots * kHeadDim));
     }
-    MV_CUDA_TRY(cudaMemcpyAsync(pc.d_items, pc.items.data(), sizeof(WorkItem) * pc.items.size(),
+    MV_CUDA_TRY(cudaMemcpyAsync(pc.d_units, pc.units.data(), sizeof(WorkItem) * pc.units.size(),
                                 cudaMemcpyHostToDevice, stream));
     MV_CUDA_TRY(cudaMemcpyAsync(pc.d_slot_ptr, pc.slot_ptr.data(), sizeof(int32_t) * pc.slot_ptr.size(),
                                 cudaMemcpyHostToDevice, stream));
     MV_CUDA_TRY(cudaMemcpyAsync(pc.d_slot_idx, pc.slot_idx.data(), sizeof(int32_t) * pc.slot_idx.size(),
                                 cudaMemcpyHostToDevice, stream));
+    MV_CUDA_TRY(cudaMemcpyAsync(pc.d_slot_cnt, pc.slot_cnt.data(), sizeof(int32_t) * pc.slot_cnt.size(),
+                                cudaMemcpyHostToDevice, stream));
+    // the host vectors must outlive the async copies: synchronise once per re-plan
+    MV_CUDA_TRY(cudaStreamSynchronize(stream));
   }
-  if (!pc.smem_set) {
-    MV_CUDA_TRY(cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDecSmem));
-    int dev = 0;
-    MV_CUDA_TRY(cudaGetDevice(&dev));
-    MV_CUDA_TRY(cudaDeviceGetAttribute(&pc.num_sms, cudaDevAttrMultiProcessorCount, dev));
-    MV_CUDA_TRY(cudaMalloc(&pc.d_counter, sizeof(int)));
-    pc.smem_set = true;
+  const int R = rows_per_member(gqa);
+  if (mv_status e = ensure_dev(pc.d_q_tile, pc.cap_q, (size_t)n * cfg.kv_heads * 2 * R * 64)) return e;
+  {
+    const int64_t chunks = (int64_t)n * cfg.kv_heads * R * 16;
+    rope_q_tile_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(
+        (const __nv_bfloat16*)d_q, d_positions, n, cfg.kv_heads, gqa, R, st.rope(), pc.d_q_tile, pc.d_counter);
+    MV_LAUNCH_CHECK();
   }
   DecodeParams P;
   P.arena = st.d_arena;
   P.kplane = st.k_planes()[layer];
   P.vplane = st.v_planes()[layer];
-  if (mv_status e = ensure_dev(pc.d_q_rot, pc.cap_q_rot, (size_t)n * q_heads * kHeadDim)) return e;
-  P.q_rot = pc.d_q_rot;
-  P.items = pc.d_items;
+  P.q_tile = pc.d_q_tile;
+  P.units = pc.d_units;
+  P.n_units = (int)pc.units.size();
+  P.work_counter = pc.d_counter;
   P.part_o = pc.d_part_o;
   P.part_ml = pc.d_part_ml;
+  P.slot_cnt = pc.d_slot_cnt;
+  P.slot_ptr = pc.d_slot_ptr;
+  P.slot_idx = pc.d_slot_idx;
+  P.out = d_out;
+  P.out_f32 = out_dtype == 1;
   P.kv_heads = cfg.kv_heads;
   P.q_heads = q_heads;
   P.gqa = gqa;
+  P.R = R;
   P.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
-  P.rope = st.rope();
-  {
-    const char* dg = getenv("MV_DECODE_DIAG");
-    P.diag = dg ? atoi(dg) : 0;
-    P.trace = nullptr;
-    if (getenv("MV_DECODE_TRACE")) {
-      if (!pc.d_trace) MV_CUDA_TRY(cudaMalloc(&pc.d_trace, sizeof(unsigned long long) * 148 * 64 * 4 * 2));
-      MV_CUDA_TRY(cudaMemsetAsync(pc.d_trace, 0, sizeof(unsigned long long) * 148 * 64 * 4 * 2, stream));
-      P.trace = pc.d_trace;
-    }
+  const int grid = std::min(P.n_units, pc.num_sms);
+  P.trace = nullptr;
+  const char* trace_path = getenv("MV_DECODE_TRACE");
+  const size_t trace_words = (size_t)pc.num_sms * kTraceWords;
+  if (trace_path) {
+    if (!pc.d_trace) MV_CUDA_TRY(cudaMalloc(&pc.d_trace, sizeof(unsigned long long) * trace_words));
+    MV_CUDA_TRY(cudaMemsetAsync(pc.d_trace, 0, sizeof(unsigned long long) * trace_words, stream));
+    P.trace = pc.d_trace;
   }
-  {
-    const int64_t chunks = (int64_t)n * q_heads * 16;
-    rope_q_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(
-        (const __nv_bfloat16*)d_q, d_positions, n, q_heads, st.rope(), pc.d_q_rot, pc.d_counter);
+  if (P.trace) decode_tc_kernel<true><<<grid, kThreads, kSmem, stream>>>(P);
+  else decode_tc_kernel<false><<<grid, kThreads, kSmem, stream>>>(P);
+  MV_LAUNCH_CHECK();
+  if (!pc.multi.empty()) {
+    const int warps = (int)pc.multi.size() * q_heads;
+    combine_kernel<<<(warps + 7) / 8, 256, 0, stream>>>(pc.d_part_o, pc.d_part_ml, pc.d_multi, (int)pc.multi.size(),
+                                                        pc.d_slot_ptr, pc.d_slot_idx, q_heads, d_out, out_dtype == 1);
     MV_LAUNCH_CHECK();
   }
-  P.work_counter = pc.d_counter;
-  P.n_work = (int)pc.items.size() * cfg.kv_heads;
-  const int grid = std::min(P.n_work, pc.num_sms);
-  decode_kernel<<<grid, kDecThreads, kDecSmem, stream>>>(P);
-  MV_LAUNCH_CHECK();
-  if (P.trace) {
-    std::vector<unsigned long long> h(148 * 64 * 4);
+  if (trace_path) {
+    std::vector<unsigned long long> h(trace_words);
     MV_CUDA_TRY(cudaMemcpyAsync(h.data(), pc.d_trace, h.size() * 8, cudaMemcpyDeviceToHost, stream));
     MV_CUDA_TRY(cudaStreamSynchronize(stream));
-    if (FILE* f = fopen(getenv("MV_DECODE_TRACE"), "wb")) {
+    if (FILE* f = fopen(trace_path, "wb")) {
       fwrite(h.data(), 8, h.size(), f);
       fclose(f);
     }
   }
-  const int warps = n * q_heads;
-  combine_kernel<<<(warps + 7) / 8, 256, 0, stream>>>(pc.d_part_o, pc.d_part_ml, pc.d_slot_ptr, pc.d_slot_idx, n,
-                                                      q_heads, d_out, out_dtype == 1);
-  MV_LAUNCH_CHECK();
   return MV_OK;
 }
 

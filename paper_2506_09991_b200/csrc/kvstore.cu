@@ -196,7 +196,7 @@ __device__ __forceinline__ void write_kv_token(__nv_bfloat16* kp, __nv_bfloat16*
   // kv_heads * 16 chunks of 8 dims; K rotated, V verbatim; stored chunk-swizzled.
   for (int j = lane; j < kv_heads * 16; j += nlanes) {
     int h = j >> 4, c = j & 15;
-    size_t dst = kv_page_head_offset(page, h, kv_heads) + (size_t)slot * kHeadDim + (size_t)swz_chunk(slot, c) * 8;
+    size_t dst = kv_page_head_offset(page, h, kv_heads) + (size_t)kv_chunk_offset(slot, c);
     uint4 kk = *reinterpret_cast<const uint4*>(k + (size_t)h * kHeadDim + c * 8);
     rope8(kk, pos, c, rt);
     *reinterpret_cast<uint4*>(kp + dst) = kk;
@@ -313,7 +313,7 @@ __global__ void k_resolve(const PageRef* __restrict__ arena, const int32_t* __re
       for (int x = threadIdx.x; x < cnt * kv_heads * 16; x += blockDim.x) {
         int t = x / (kv_heads * 16), h = (x / 16) % kv_heads, c = x % 16;
         int slot = b + t;
-        size_t src = kv_page_head_offset(r.page, h, kv_heads) + (size_t)slot * kHeadDim + swz_chunk(slot, c) * 8;
+        size_t src = kv_page_head_offset(r.page, h, kv_heads) + (size_t)kv_chunk_offset(slot, c);
         size_t dst = ((size_t)(c0 + t) * kv_heads + h) * kHeadDim + c * 8;
         *reinterpret_cast<uint4*>(k_out + dst) = *reinterpret_cast<const uint4*>(kp + src);
         *reinterpret_cast<uint4*>(v_out + dst) = *reinterpret_cast<const uint4*>(vp + src);
@@ -383,6 +383,7 @@ PagedStore::~PagedStore() {
   for (auto* p : v_planes_) cudaFree(p);
   for (auto* p : dscratch_) cudaFree(p);
   if (pinned_) cudaFreeHost(pinned_);
+  destroy_plan(plan);
 }
 
 mv_status PagedStore::init() {

@@ -39,6 +39,7 @@ struct HandleRec {
 };
 
 struct DecodePlanCache;  // decode.cu
+void destroy_plan(DecodePlanCache* p);
 
 class PagedStore {
  public:
