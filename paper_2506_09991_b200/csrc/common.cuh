@@ -56,17 +56,18 @@ __host__ __device__ inline PageRef make_ref(int page, int begin, int count) {
 }
 
 // ---------------------------------------------------------------------------
-// KV page layout: [page][kv_head][2 halves][16 tokens][64 dims] bf16, 4 KiB per (page, head).
-// Half h holds dims 64h..64h+63 as 128-byte token rows, and the 16-byte chunk c of token row t
-// sits at chunk c ^ (t & 7): each half is exactly the canonical UMMA SWIZZLE_128B atom pair
-// (8 rows x 128 B, 1024 B apart), so a plain 1-D bulk copy of a page-head block lands an
-// operand the tcgen05 tensor core reads directly — K-major for Q.K^T (N = tokens) and
-// MN-major for P.V (N = dims) — with no shared-memory re-layout.
+// KV page layout: [page][kv_head][4 KiB block]; the block holds token t, dim d at
+//   atom (t >> 3, d >> 6) of 1 KiB = 8 token rows x 128 B, atoms ordered [t >> 3][d >> 6],
+//   16-byte chunk c of row r stored at chunk c ^ r   (SWIZZLE_128B within each atom).
+// Consecutive page-head blocks of one KV head therefore form canonical UMMA operands with
+// one 1-D bulk copy per page: K-major for Q.K^T (N = tokens: 8-row groups 2048 B apart, dims
+// 64..127 at +1024 B) and MN-major for P.V (N = dims: atoms 1024 B apart, K = tokens: 8-row
+// groups 2048 B apart) — no shared-memory re-layout.
 // ---------------------------------------------------------------------------
 __host__ __device__ inline int swz_chunk(int token, int chunk) { return chunk ^ (token & 7); }
 // element offset of 16-byte chunk c (dims 8c..8c+7) of token slot t inside a page-head block
 __host__ __device__ inline int kv_chunk_offset(int t, int c) {
-  return (c >> 3) * (kPageTokens * 64) + t * 64 + (((c & 7) ^ (t & 7)) << 3);
+  return ((((t >> 3) * 2 + (c >> 3)) * 8 + (t & 7)) * 64) + ((((c & 7) ^ (t & 7))) << 3);
 }
 __host__ __device__ inline size_t kv_page_head_offset(int64_t page, int head, int kv_heads) {
   return ((size_t)page * kv_heads + head) * (kPageTokens * kHeadDim);

@@ -49,24 +49,25 @@ namespace {
 
 constexpr int kThreads = 512;                               // 16 warps
 // Warp w issues on SM sub-partition w % 4, shared with softmax / epilogue warps of TMEM lane
-// quadrant w % 4.  Query rows fill quadrants from 0, so the latency-critical MMA issuer sits on
-// sub-partition 3 (idle unless a unit has > 96 rows) and the TMA issuer on 2.
-constexpr int kWarpStage = 0, kWarpTma = 2, kWarpMma = 3;
+// quadrant w % 4.  Query rows fill quadrants from 0, so the latency-critical MMA issuers sit on
+// sub-partitions 3 (QK) and 2 (PV), idle unless a unit has > 64 rows.
+constexpr int kWarpStage = 0, kWarpTma = 1, kWarpPv = 2, kWarpQk = 3;
 constexpr int kPageBytes = kPageTokens * kHeadDim * 2;      // 4 KiB page-head block
 constexpr int kBlkPages = 4;                                // pages per block (one QK MMA chain)
 constexpr int kBlkCols = kBlkPages * kPageTokens;           // 64 S columns per block
-constexpr int kSlots = 4;                                   // ring slots, one block (K + V) each
-constexpr int kSlotK = kBlkPages * kPageBytes;              // K: [2 halves][64 tokens][128 B]
-constexpr int kSlotBytes = 2 * kSlotK;                      // + V: 4 page-head blocks as stored
+constexpr int kKSlots = 5, kVSlots = 6;                     // K / V rings, one block (4 pages) per slot
+constexpr int kSlotBytes = kBlkPages * kPageBytes;          // 4 page-head blocks as stored (16 KiB)
 constexpr int kMaxEntries = 64;                             // pages per work unit (split-KV chunk)
 constexpr int kMaxMem = 16;                                 // handles per work unit
 constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dims] bf16
 constexpr int kQBytes = 2 * kQHalf;
 constexpr float kSumLimit = 4096.f;                        // block mass that moves the softmax reference
-constexpr int kPrefetch = 24;                               // L2 prefetch distance (pages)
-constexpr int kColS = 0;                                    // TMEM: S0, S1 (64 cols each)
-constexpr int kColO = 2 * kBlkCols;                         //       O0, O1 (128 cols each)
-constexpr int kColQ = kColO + 256;                          //       Q0, Q1 (64 cols: 128 bf16 dims)
+constexpr int kPrefetch = 32;                               // pages of a unit prefetched into L2 at staging
+constexpr int kSBufs = 3;                                   // S / P buffers in flight
+constexpr int kColS = 0;                                    // TMEM: S0..S2 (64 cols each)
+constexpr int kColO = kSBufs * kBlkCols;                    //       O0, O1 (128 cols each)
+constexpr int kColQ = kColO + 256;                          //       Q (64 cols: 128 bf16 dims)
+static_assert(kColQ + 64 <= 512, "TMEM budget");
 constexpr int kTmemCols = 512;
 
 struct __align__(16) WorkItem {
@@ -83,14 +84,15 @@ static_assert(sizeof(WorkItem) == 96, "WorkItem layout");
 constexpr int kItemInts = sizeof(WorkItem) / 4;
 
 constexpr int kOffQ = 0;
-constexpr int kOffRing = kOffQ + 2 * kQBytes;
-constexpr int kOffEnt = kOffRing + kSlots * kSlotBytes;
+constexpr int kOffRing = kOffQ + kQBytes;  // one Q staging tile: TMEM holds the live copy
+constexpr int kOffVRing = kOffRing + kKSlots * kSlotBytes;
+constexpr int kOffEnt = kOffVRing + kVSlots * kSlotBytes;
 constexpr int kOffItem = kOffEnt + 2 * kMaxEntries * 8;
 constexpr int kOffEp = kOffItem + 2 * sizeof(WorkItem);
 constexpr int kOffStat = kOffEp + 2 * sizeof(WorkItem);
 constexpr int kOffFlag = kOffStat + 2 * 128 * 8;
 constexpr int kOffBar = kOffFlag + 128 * 4;
-constexpr int kNumBars = 4 + 2 * kSlots + 10;
+constexpr int kNumBars = 4 + 2 * (kKSlots + kVSlots) + 3 * kSBufs + 4;
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
 constexpr int kSmem = kOffTmem + 16 + 1024;  // + 1 KiB alignment slack
 static_assert(kSmem <= 227 * 1024, "decode smem");
@@ -118,7 +120,7 @@ struct DecodeParams {
   unsigned long long* trace;    // optional timeline [cta][kTraceWords] (MV_DECODE_TRACE)
 };
 
-constexpr int kTraceWords = 544;
+constexpr int kTraceWords = 672;
 
 __device__ __forceinline__ void store_row(const DecodeParams& P, int64_t row, int c, const float* o, float inv) {
   if (P.out_f32) {
@@ -134,6 +136,28 @@ __device__ __forceinline__ void store_row(const DecodeParams& P, int64_t row, in
   }
 }
 
+// MMA issue helpers with compile-time TMEM operands: the issuing thread then needs no per-MMA
+// register -> uniform-register moves (which the compiler otherwise wraps in an ELECT loop).
+template <int SB>
+__device__ __forceinline__ void issue_qk_mmas(uint64_t kd) {  // S_SB = Q . K_blk^T (A = Q in TMEM)
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    tc::mma_ts(kColS + SB * kBlkCols, kColQ + k * 8, kd + (uint64_t)(((k >> 2) * 1024 + (k & 3) * 32) >> 4), kIdQK,
+               k > 0 ? 1u : 0u);
+}
+template <int PAR, int SB>
+__device__ __forceinline__ void issue_pv_mmas(uint64_t vd, int np, uint32_t acc0) {  // O_PAR += P_SB . V_blk
+  constexpr uint32_t ocol = kColO + PAR * 128, pcol = kColS + SB * kBlkCols;
+  tc::mma_ts(ocol, pcol, vd, kIdPV, acc0);
+  if (np > 1) tc::mma_ts(ocol, pcol + 8, vd + (uint64_t)(kPageBytes >> 4), kIdPV, 1u);
+  if (np > 2) tc::mma_ts(ocol, pcol + 16, vd + (uint64_t)((2 * kPageBytes) >> 4), kIdPV, 1u);
+  if (np > 3) tc::mma_ts(ocol, pcol + 24, vd + (uint64_t)((3 * kPageBytes) >> 4), kIdPV, 1u);
+}
+__device__ __forceinline__ void issue_q_copy(uint64_t qd) {  // Q tile smem -> TMEM
+#pragma unroll
+  for (int k = 0; k < 8; ++k) tc::cp_128x256b(kColQ + k * 8, qd + (uint64_t)(((k >> 2) * kQHalf + (k & 3) * 32) >> 4));
+}
+
 template <bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodeParams P) {
   extern __shared__ uint8_t smem_raw[];
@@ -146,37 +170,52 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* item_full = bars;             // [2] stager -> TMA / MMA / softmax (count 1 + Q tx)
   uint64_t* slot_empty = bars + 2;        // [2] TMA + MMA commit + 8 softmax warps -> stager
-  uint64_t* full = bars + 4;              // [kSlots] TMA -> MMA
-  uint64_t* empty = full + kSlots;        // [kSlots] MMA commit -> TMA
-  uint64_t* s_full = empty + kSlots;      // [2] MMA commit -> softmax
-  uint64_t* p_full = s_full + 2;          // [2] softmax warps -> MMA
-  uint64_t* o_full = p_full + 2;          // MMA commit -> epilogue (unit's O_0 / O_1 final)
-  uint64_t* o_empty = o_full + 2;         // epilogue warps -> MMA / softmax
-  uint64_t* stat_full = o_empty + 2;      // 8 softmax warps -> epilogue
+  uint64_t* kfull = bars + 4;             // [kKSlots] TMA -> QK issuer
+  uint64_t* kempty = kfull + kKSlots;     // [kKSlots] QK commit -> TMA
+  uint64_t* vfull = kempty + kKSlots;     // [kVSlots] TMA -> PV issuer
+  uint64_t* vempty = vfull + kVSlots;     // [kVSlots] PV commit -> TMA (and softmax O rescale)
+  uint64_t* s_full = vempty + kVSlots;    // [kSBufs] QK commit -> softmax
+  uint64_t* p_full = s_full + kSBufs;     // [kSBufs] softmax warps -> PV issuer
+  uint64_t* pv_done = p_full + kSBufs;    // [kSBufs] PV commit -> QK issuer (S buffer free)
+  uint64_t* o_full = pv_done + kSBufs;    // PV commit -> epilogue (unit's O_0 / O_1 final)
+  uint64_t* o_empty = o_full + 1;         // epilogue warps -> PV issuer / softmax
+  uint64_t* stat_full = o_empty + 1;      // 8 softmax warps -> epilogue
+  uint64_t* q_free = stat_full + 1;       // QK issuer commit (Q tile copied to TMEM) -> stager
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&item_full[b], 1);
-      mbar_init(&slot_empty[b], 10);
+      mbar_init(&slot_empty[b], 12);  // 2 TMA lanes + QK commit + PV issuer + 8 softmax warps
+    }
+    for (int b = 0; b < kSBufs; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 4);
-      mbar_init(&o_full[b], 1);
-      mbar_init(&o_empty[b], 4);
-      mbar_init(&stat_full[b], 8);
+      mbar_init(&pv_done[b], 1);
     }
-    for (int s = 0; s < kSlots; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    mbar_init(o_full, 1);
+    mbar_init(o_empty, 4);
+    mbar_init(stat_full, 8);
+    mbar_init(q_free, 1);
+    for (int s = 0; s < kKSlots; ++s) {
+      mbar_init(&kfull[s], 1);
+      mbar_init(&kempty[s], 1);
+    }
+    for (int s = 0; s < kVSlots; ++s) {
+      mbar_init(&vfull[s], 1);
+      mbar_init(&vempty[s], 1);
     }
     fence_mbar_init();
   }
-  if (warp == kWarpMma) tc::tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kWarpQk) tc::tmem_alloc(tmem_slot, kTmemCols);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // One CTA per SM allocates all 512 columns, so the allocation starts at lane 0 / column 0.  A
+  // compile-time base keeps every TMEM operand uniform (no per-MMA R2UR waterfall in the issuer).
+  constexpr uint32_t tmem = 0;
+  if (*tmem_slot != tmem) __trap();
 
   if (warp == kWarpStage) {
     // ---------------- stager: claim, entries, Q rows ----------------
@@ -202,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       for (int j = lane; j < n_ent; j += 32) {
         const PageRef ref = P.arena[eoff + j];
         se[j] = ref;
-        if (j < kPrefetch) {  // the TMA thread prefetches the rest, kPrefetch pages ahead
+        if (j < kPrefetch) {  // the unit's head now; its tail once the unit has started (below)
           const size_t pf = ((size_t)ref.page * P.kv_heads + kvh) * kPageTokens * kHeadDim;
           prefetch_l2(P.kplane + pf, kPageBytes);
           prefetch_l2(P.vplane + pf, kPageBytes);
@@ -210,24 +249,41 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       }
       __syncwarp();
       const uint32_t half_bytes = (uint32_t)P.R * 128;
+      if (i >= 1) {
+        mbar_wait(q_free, (i - 1) & 1);  // the previous unit's Q tile is in TMEM: it has started
+        // stream the rest of the previous unit into L2 (its page list is still staged)
+        const WorkItem* sp = &s_item[buf ^ 1];
+        const PageRef* pe = s_ent0 + (buf ^ 1) * kMaxEntries;
+        for (int j = kPrefetch + lane; j < sp->n_entries; j += 32) {
+          const size_t pf = ((size_t)pe[j].page * P.kv_heads + sp->kvh) * kPageTokens * kHeadDim;
+          prefetch_l2(P.kplane + pf, kPageBytes);
+          prefetch_l2(P.vplane + pf, kPageBytes);
+        }
+      }
       if (lane == 0) mbar_arrive_expect_tx(&item_full[buf], 2u * half_bytes * (uint32_t)n_mem);
       __syncwarp();
       if (lane < 2 * n_mem) {
         const int m = lane >> 1, h = lane & 1;
         const int b = si->members[m];
-        uint8_t* dst = smem + kOffQ + buf * kQBytes + h * kQHalf + m * half_bytes;
+        uint8_t* dst = smem + kOffQ + h * kQHalf + m * half_bytes;
         const __nv_bfloat16* src = P.q_tile + (((size_t)b * P.kv_heads + kvh) * 2 + h) * (size_t)P.R * 64;
         bulk_g2s(dst, src, half_bytes, &item_full[buf]);
       }
     }
   } else if (warp == kWarpTma) {
-    // ---------------- TMA: keeps the block ring full across work units ----------------
-    // One issuing thread, in consumption order.  A block = up to 4 pages: each page's K half-rows
-    // land contiguously per half ([2][64 tokens][128 B], one N=64 UMMA operand), V page-head blocks
-    // as stored.  HBM latency beyond the ring is hidden by L2 prefetches kPrefetch pages ahead.
-    if (lane == 0) {
-      int g = 0;
+    // ---------------- TMA: keeps the K and V rings full across work units ----------------
+    // Two independent streams on two lanes (their issue latencies overlap): lane 0 copies K
+    // blocks, lane 1 V blocks (one 4 KiB bulk copy per page-head).  K slots free after Q.K^T,
+    // V slots after P.V.  L2 prefetching is the stager's job.
+    if (lane < 2) {
       const size_t page_stride = (size_t)P.kv_heads * kPageTokens * kHeadDim;
+      const bool is_k = lane == 0;
+      const int nsl = is_k ? kKSlots : kVSlots;
+      uint64_t* fb = is_k ? kfull : vfull;
+      uint64_t* eb = is_k ? kempty : vempty;
+      uint8_t* rb = is_k ? ring : smem + kOffVRing;
+      const __nv_bfloat16* plane = is_k ? P.kplane : P.vplane;
+      int g = 0;
       for (int i = 0;; ++i) {
         const int buf = i & 1;
         mbar_wait(&item_full[buf], (i >> 1) & 1);
@@ -237,105 +293,92 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         const size_t head_off = (size_t)si->kvh * kPageTokens * kHeadDim;
         const PageRef* se = s_ent0 + buf * kMaxEntries;
         for (int e0 = 0; e0 < n_ent; e0 += kBlkPages, ++g) {
-          const int sl = g % kSlots, np = min(kBlkPages, n_ent - e0);
-          for (int j = e0 + kPrefetch; j < min(e0 + kPrefetch + kBlkPages, n_ent); ++j) {
-            const size_t pf = (size_t)se[j].page * page_stride + head_off;
-            prefetch_l2(P.kplane + pf, kPageBytes);
-            prefetch_l2(P.vplane + pf, kPageBytes);
-          }
-          if (g >= kSlots) mbar_wait(&empty[sl], ((g / kSlots) - 1) & 1);
-          uint8_t* dk = ring + sl * kSlotBytes;
-          mbar_arrive_expect_tx(&full[sl], (uint32_t)np * 2 * kPageBytes);
-          for (int p = 0; p < np; ++p) {
-            const size_t src = (size_t)se[e0 + p].page * page_stride + head_off;
-            bulk_g2s(dk + p * (kPageBytes / 2), P.kplane + src, kPageBytes / 2, &full[sl]);
-            bulk_g2s(dk + kSlotK / 2 + p * (kPageBytes / 2), P.kplane + src + kPageTokens * 64, kPageBytes / 2,
-                     &full[sl]);
-            bulk_g2s(dk + kSlotK + p * kPageBytes, P.vplane + src, kPageBytes, &full[sl]);
-          }
+          const int sl = g % nsl, np = min(kBlkPages, n_ent - e0);
+          if (TRACE && is_k && g < 64) P.trace[blockIdx.x * kTraceWords + 544 + g] = globaltimer();
+          if (g >= nsl) mbar_wait(&eb[sl], ((g / nsl) - 1) & 1);
+          uint8_t* dst = rb + sl * kSlotBytes;
+          mbar_arrive_expect_tx(&fb[sl], (uint32_t)np * kPageBytes);
+          for (int p = 0; p < np; ++p)
+            bulk_g2s(dst + p * kPageBytes, plane + (size_t)se[e0 + p].page * page_stride + head_off, kPageBytes,
+                     &fb[sl]);
         }
-        mbar_arrive(&slot_empty[buf]);
+        mbar_arrive(&slot_empty[buf]);  // this stream no longer reads the unit's entries
       }
     }
-  } else if (warp == kWarpMma) {
-    // ---------------- MMA issuer (one thread; kept tight: ~50 cycles per tcgen05.mma) ----------------
+  } else if (warp == kWarpQk) {
+    // ---------------- QK issuer: Q -> TMEM per unit, S_g = Q . K_g^T per block ----------------
     if (lane == 0) {
       const uint64_t qdesc0 = tc::sw128_desc(smem_u32(smem + kOffQ), 16, 1024);
-      const uint64_t kdesc0 = tc::sw128_desc(smem_u32(ring), 16, 1024);
-      const uint64_t vdesc0 = tc::sw128_desc(smem_u32(ring + kSlotK), kPageBytes / 2, 1024);
-      // units opened by the QK cursor are remembered for the PV cursor (QK runs <= 2 blocks ahead)
-      int f_ent[4], f_valid[4];
-      int q_i = -1, q_blk = 0, q_nblk = 0, q_valid = 1;
-      int qg = 0;  // global block index of the next QK
-      auto issue_qk = [&]() {
-        while (q_valid && q_blk >= q_nblk) {
-          ++q_i;
-          const int ub = q_i & 1;
-          mbar_wait(&item_full[ub], (q_i >> 1) & 1);
-          const WorkItem* si = &s_item[ub];
-          q_valid = si->valid;
-          const int ne = q_valid ? si->n_entries : 0;
-          q_nblk = (ne + kBlkPages - 1) / kBlkPages;
-          q_blk = 0;
-          f_ent[q_i & 3] = ne;
-          f_valid[q_i & 3] = q_valid;
-          if (q_valid) {
-            // the unit's Q tile smem -> TMEM once (QK then reads A from TMEM: no per-block re-read
-            // of Q from shared memory)
-            tc::fence_after();
-            const uint64_t qd = qdesc0 + (uint64_t)((ub * kQBytes) >> 4);
-            const uint32_t qt = tmem + kColQ + ub * 64;
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              tc::cp_128x256b(qt + k * 8, qd + (uint64_t)(((k >> 2) * kQHalf + (k & 3) * 32) >> 4));
+      const uint64_t kdesc0 = tc::sw128_desc(smem_u32(ring), 16, 2048);
+      int g = 0;
+      for (int i = 0;; ++i) {
+        const int ub = i & 1;
+        mbar_wait(&item_full[ub], (i >> 1) & 1);
+        const WorkItem* si = &s_item[ub];
+        if (!si->valid) break;
+        const int nblk = (si->n_entries + kBlkPages - 1) / kBlkPages;
+        tc::fence_after();
+        // the unit's Q tile smem -> TMEM (ordered after the previous unit's QK MMAs)
+        issue_q_copy(qdesc0);
+        tc::mma_commit(q_free);
+        for (int blk = 0; blk < nblk; ++blk, ++g) {
+          const int sb = g % kSBufs, sl = g % kKSlots;
+          if (TRACE && g < 64) P.trace[blockIdx.x * kTraceWords + 128 + g] = globaltimer();
+          if (g >= kSBufs) mbar_wait(&pv_done[sb], ((g - kSBufs) / kSBufs) & 1);  // P(g-3) consumed
+          mbar_wait(&kfull[sl], (g / kKSlots) & 1);
+          tc::fence_after();
+          const long long c0 = TRACE ? clock64() : 0;
+          const uint64_t kd = kdesc0 + (uint64_t)(sl * (kSlotBytes >> 4));
+          if (sb == 0) issue_qk_mmas<0>(kd);
+          else if (sb == 1) issue_qk_mmas<1>(kd);
+          else issue_qk_mmas<2>(kd);
+          tc::mma_commit(&s_full[sb]);
+          tc::mma_commit(&kempty[sl]);
+          if (TRACE && g < 64) {
+            P.trace[blockIdx.x * kTraceWords + 192 + g] = globaltimer();
+            P.trace[blockIdx.x * kTraceWords + 352 + g] = clock64() - c0;  // QK issue cycles (data ready)
           }
         }
-        if (!q_valid) return;
-        const int sl = qg % kSlots;
-        if (TRACE && qg < 64) P.trace[blockIdx.x * kTraceWords + 128 + qg] = globaltimer();
-        mbar_wait(&full[sl], (qg / kSlots) & 1);
-        tc::fence_after();
-        const uint32_t qt = tmem + kColQ + (q_i & 1) * 64;
-        const uint64_t kd = kdesc0 + (uint64_t)(sl * (kSlotBytes >> 4));
-        const uint32_t dcol = tmem + kColS + (qg & 1) * kBlkCols;
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          tc::mma_ts(dcol, qt + k * 8, kd + (uint64_t)(((k >> 2) * (kSlotK / 2) + (k & 3) * 32) >> 4), kIdQK,
-                     k > 0 ? 1u : 0u);
-        tc::mma_commit(&s_full[qg & 1]);
-        if (q_blk == q_nblk - 1) tc::mma_commit(&slot_empty[q_i & 1]);  // Q buffer no longer read
-        if (TRACE && qg < 64) P.trace[blockIdx.x * kTraceWords + 192 + qg] = globaltimer();
-        ++q_blk;
-        ++qg;
-      };
-      issue_qk();
-      issue_qk();
-      int p_i = 0, p_blk = 0;
-      for (int pg = 0;; ++pg) {
-        // PV cursor: next block (units already opened by the QK cursor)
-        while (f_valid[p_i & 3] && p_blk * kBlkPages >= f_ent[p_i & 3]) {
-          ++p_i;
-          p_blk = 0;
+        tc::mma_commit(&slot_empty[ub]);  // Q smem tile consumed
+      }
+    }
+  } else if (warp == kWarpPv) {
+    // ---------------- PV issuer: O_par += P_g . V_g per block ----------------
+    if (lane == 0) {
+      const uint64_t vdesc0 = tc::sw128_desc(smem_u32(smem + kOffVRing), 1024, 2048);
+      int g = 0;
+      for (int i = 0;; ++i) {
+        const int ub = i & 1;
+        mbar_wait(&item_full[ub], (i >> 1) & 1);
+        const WorkItem* si = &s_item[ub];
+        const int valid = si->valid, n_ent = si->n_entries;
+        mbar_arrive(&slot_empty[ub]);  // header read
+        if (!valid) break;
+        const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
+        for (int blk = 0; blk < nblk; ++blk, ++g) {
+          const int sb = g % kSBufs;
+          mbar_wait(&p_full[sb], (g / kSBufs) & 1);
+          if (TRACE && g < 64) P.trace[blockIdx.x * kTraceWords + 480 + g] = globaltimer();
+          if (blk == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue drained O
+          mbar_wait(&vfull[g % kVSlots], (g / kVSlots) & 1);
+          tc::fence_after();
+          const long long c1 = TRACE ? clock64() : 0;
+          const uint64_t vd = vdesc0 + (uint64_t)((g % kVSlots) * (kSlotBytes >> 4));
+          const int np = n_ent - blk * kBlkPages;
+          const uint32_t acc0 = blk >= 2 ? 1u : 0u;  // blocks 0 and 1 of a unit open O_0 / O_1
+          switch (g % 6) {  // (parity, S buffer)
+            case 0: issue_pv_mmas<0, 0>(vd, np, acc0); break;
+            case 1: issue_pv_mmas<1, 1>(vd, np, acc0); break;
+            case 2: issue_pv_mmas<0, 2>(vd, np, acc0); break;
+            case 3: issue_pv_mmas<1, 0>(vd, np, acc0); break;
+            case 4: issue_pv_mmas<0, 1>(vd, np, acc0); break;
+            default: issue_pv_mmas<1, 2>(vd, np, acc0); break;
+          }
+          tc::mma_commit(&vempty[g % kVSlots]);  // also certifies PV(g) to the softmax (O rescale)
+          tc::mma_commit(&pv_done[sb]);
+          if (blk == nblk - 1) tc::mma_commit(o_full);
+          if (TRACE && g < 64) P.trace[blockIdx.x * kTraceWords + 416 + g] = clock64() - c1;  // PV issue cycles
         }
-        if (!f_valid[p_i & 3]) break;
-        const int n_ent = f_ent[p_i & 3];
-        mbar_wait(&p_full[pg & 1], (pg >> 1) & 1);
-        if (TRACE && pg < 64) P.trace[blockIdx.x * kTraceWords + 480 + pg] = globaltimer();
-        if (p_blk == 0 && p_i >= 1) mbar_wait(o_empty, (p_i - 1) & 1);  // epilogue drained O
-        tc::fence_after();
-        const uint32_t ocol = tmem + kColO + (pg & 1) * 128;  // O of this block parity
-        const uint32_t pcol = tmem + kColS + (pg & 1) * kBlkCols;
-        const uint64_t vd = vdesc0 + (uint64_t)((pg % kSlots) * (kSlotBytes >> 4));
-        const int np = n_ent - p_blk * kBlkPages;
-        // blocks 0 and 1 of a unit open O_0 / O_1
-        tc::mma_ts(ocol, pcol, vd, kIdPV, p_blk >= 2 ? 1u : 0u);
-        if (np > 1) tc::mma_ts(ocol, pcol + 8, vd + (uint64_t)(kPageBytes >> 4), kIdPV, 1u);
-        if (np > 2) tc::mma_ts(ocol, pcol + 16, vd + (uint64_t)((2 * kPageBytes) >> 4), kIdPV, 1u);
-        if (np > 3) tc::mma_ts(ocol, pcol + 24, vd + (uint64_t)((3 * kPageBytes) >> 4), kIdPV, 1u);
-        tc::mma_commit(&empty[pg % kSlots]);  // also certifies PV(pg) to the softmax (O rescale)
-        if (np <= kBlkPages) tc::mma_commit(o_full);  // last block of the unit
-        ++p_blk;
-        issue_qk();
       }
     }
   } else if (warp >= 4 && warp < 12) {
@@ -347,7 +390,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
     const int r = q * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     const uint32_t ocol = lane_base + kColO + par * 128;
-    const uint32_t scol = lane_base + kColS + par * kBlkCols;
     int g = 0;
     for (int i = 0;; ++i) {
       const int buf = i & 1;
@@ -370,7 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       bool first = true;  // first block of this parity in the unit: O_par not yet written
       for (int blk = 0; blk < nblk; ++blk, ++g) {
         if ((g & 1) != par) continue;
-        mbar_wait(&s_full[par], (g >> 1) & 1);
+        const int sb = g % kSBufs;
+        const uint32_t scol = lane_base + kColS + sb * kBlkCols;
+        mbar_wait(&s_full[sb], (g / kSBufs) & 1);
         tc::fence_after();
         if (TRACE && q == 0 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + g] = globaltimer();
         if (warp_active) {
@@ -441,7 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
             const float alpha = resc ? fast_exp2(m_ref - nref) : 1.f;
             if (!first && __any_sync(0xffffffffu, resc)) {
               // O_par holds this parity's earlier blocks once PV(g-2) has completed (its slot's empty commit)
-              mbar_wait(&empty[(g - 2) % kSlots], ((g - 2) / kSlots) & 1);
+              mbar_wait(&vempty[(g - 2) % kVSlots], ((g - 2) / kVSlots) & 1);
               tc::fence_after();
 #pragma unroll 1
               for (int c = 0; c < 4; ++c) {
@@ -464,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         first = false;
         tc::fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[par]);
+        if (lane == 0) mbar_arrive(&p_full[sb]);
         if (TRACE && q == 0 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 64 + g] = globaltimer();
       }
       // hand (m, l) and the unit header to the epilogue, release the unit slot
@@ -533,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == kWarpMma) {
+  if (warp == kWarpQk) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, kTmemCols);
   }

@@ -7,7 +7,7 @@ import sys
 
 import numpy as np
 
-W = 544
+W = 672
 t = np.fromfile(sys.argv[1], dtype=np.uint64).astype(np.int64)
 t = t.reshape(-1, W)
 valid = t[:, 320] > 0
@@ -34,9 +34,12 @@ stat("MMA QK page wait (start -> commit)", pairs(qk_s, qk_e))
 stat("QK commit -> softmax saw S", pairs(qk_e, sm_seen))
 stat("block period (softmax seen g -> g+1)", pairs(sm_seen[:, :-1], sm_seen[:, 1:]))
 qw = t[:, 352:416].astype(np.float64) / 1.965
-stat("MMA full-wait time within QK (ns @1965MHz)", qw[qk_e > 0] * 1.0)
+stat("MMA QK issue (data ready) ns @1965MHz", qw[qk_e > 0] * 1.0)
 ow = t[:, 416:480].astype(np.float64) / 1.965
-stat("MMA o_empty wait before PV (ns)", ow[sm_rel > 0] * 1.0)
+stat("MMA PV issue ns @1965MHz", ow[sm_rel > 0] * 1.0)
+tw = t[:, 608:672].astype(np.float64) / 1.965
+stat("TMA issue per block ns (after empty)", tw[t[:, 544:608] > 0] * 1.0)
+stat("TMA block issue -> QK commit", pairs(t[:, 544:608], qk_e))
 stat("epilogue (incl. combine)", pairs(ep_s, ep_e))
 stat("unit period (claim i -> i+1)", pairs(claim[:, :-1], claim[:, 1:]))
 stat("first S after first claim", sm_seen[:, 0] - claim[:, 0])
@@ -47,7 +50,7 @@ print(f"CTA last epilogue end after t0: min {((last - t0).min())/1e3:.1f} med {n
 if len(sys.argv) > 2:
     c = int(sys.argv[2])
     base = claim[c, 0]
-    print(f"CTA {c} timeline (us after first claim): g | S seen | P released | MMA got P | QK start | QK commit")
+    print(f"CTA {c} timeline (us after first claim): g | TMA start | S seen | P released | MMA got P | QK start | QK commit")
     for g in range(40):
-        row = [t[c, g], t[c, 64 + g], t[c, 480 + g], t[c, 128 + g], t[c, 192 + g]]
+        row = [t[c, 544 + g], t[c, g], t[c, 64 + g], t[c, 480 + g], t[c, 128 + g], t[c, 192 + g]]
         print(f"  {g:2d} " + " ".join(f"{(x - base) / 1e3:8.3f}" if x > 0 else "       -" for x in row))
