@@ -25,11 +25,12 @@
 //   warp 0  stager  : claims the next unit, copies its page entries, and bulk-copies the
 //                     members' RoPE'd Q rows (pre-swizzled by rope_q_tile_kernel) into one of
 //                     two Q buffers.
-//   warps 4-11 softmax: two warpgroups ping-pong over even / odd blocks, each with its own S
-//                     buffer, O buffer and (m, l): thread = query row = TMEM lane.  Masks ragged
-//                     page slots, log2-domain online softmax against a lazily moved reference
-//                     (no per-block max), P as packed bf16 back into TMEM.
-//   warps 12-15 epilogue: merges the two parity partials of each row from TMEM -> final output
+//   warps 4-11 softmax: thread = query row = TMEM lane; the two warps of a lane quadrant split
+//                     each block's columns and share the row's reference max (barrier-reduced),
+//                     so every block accumulates into one O.  Masks ragged page slots, log2-domain
+//                     online softmax against a lazily moved reference (no per-block max), P as
+//                     packed bf16 back into TMEM (5 S/P buffers in flight).
+//   warps 12-15 epilogue: O row from TMEM -> final output
 //                     (single-chunk handles) or an fp32 split-KV partial, merged afterwards by
 //                     combine_kernel (log-sum-exp over the handle's chunks).
 // Query rows: member m of a unit owns TMEM lanes [m*R, m*R + gqa), R = gqa rounded up to a
@@ -63,10 +64,10 @@ constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dim
 constexpr int kQBytes = 2 * kQHalf;
 constexpr float kSumLimit = 4096.f;                        // block mass that moves the softmax reference
 constexpr int kPrefetch = 32;                               // pages of a unit prefetched into L2 at staging
-constexpr int kSBufs = 3;                                   // S / P buffers in flight
-constexpr int kColS = 0;                                    // TMEM: S0..S2 (64 cols each)
-constexpr int kColO = kSBufs * kBlkCols;                    //       O0, O1 (128 cols each)
-constexpr int kColQ = kColO + 256;                          //       Q (64 cols: 128 bf16 dims)
+constexpr int kSBufs = 5;                                   // S / P buffers in flight
+constexpr int kColS = 0;                                    // TMEM: S0..S4 (64 cols each)
+constexpr int kColO = kSBufs * kBlkCols;                    //       O (128 cols)
+constexpr int kColQ = kColO + 128;                          //       Q (64 cols: 128 bf16 dims)
 static_assert(kColQ + 64 <= 512, "TMEM budget");
 constexpr int kTmemCols = 512;
 
@@ -90,8 +91,8 @@ constexpr int kOffEnt = kOffVRing + kVSlots * kSlotBytes;
 constexpr int kOffItem = kOffEnt + 2 * kMaxEntries * 8;
 constexpr int kOffEp = kOffItem + 2 * sizeof(WorkItem);
 constexpr int kOffStat = kOffEp + 2 * sizeof(WorkItem);
-constexpr int kOffFlag = kOffStat + 2 * 128 * 8;
-constexpr int kOffBar = kOffFlag + 128 * 4;
+constexpr int kOffFlag = kOffStat + 2 * 128 * 8;  // pair max exchange [4][2][32] floats
+constexpr int kOffBar = kOffFlag + 4 * 2 * 32 * 4;
 constexpr int kNumBars = 4 + 2 * (kKSlots + kVSlots) + 3 * kSBufs + 4;
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
 constexpr int kSmem = kOffTmem + 16 + 1024;  // + 1 KiB alignment slack
@@ -120,7 +121,7 @@ struct DecodeParams {
   unsigned long long* trace;    // optional timeline [cta][kTraceWords] (MV_DECODE_TRACE)
 };
 
-constexpr int kTraceWords = 672;
+constexpr int kTraceWords = 864;
 
 __device__ __forceinline__ void store_row(const DecodeParams& P, int64_t row, int c, const float* o, float inv) {
   if (P.out_f32) {
@@ -145,14 +146,25 @@ __device__ __forceinline__ void issue_qk_mmas(uint64_t kd) {  // S_SB = Q . K_bl
     tc::mma_ts(kColS + SB * kBlkCols, kColQ + k * 8, kd + (uint64_t)(((k >> 2) * 1024 + (k & 3) * 32) >> 4), kIdQK,
                k > 0 ? 1u : 0u);
 }
-template <int PAR, int SB>
-__device__ __forceinline__ void issue_pv_mmas(uint64_t vd, int np, uint32_t acc0) {  // O_PAR += P_SB . V_blk
-  constexpr uint32_t ocol = kColO + PAR * 128, pcol = kColS + SB * kBlkCols;
+template <int SB>
+__device__ __forceinline__ void issue_pv_mmas(uint64_t vd, int np, uint32_t acc0) {  // O += P_SB . V_blk
+  constexpr uint32_t ocol = kColO, pcol = kColS + SB * kBlkCols;
   tc::mma_ts(ocol, pcol, vd, kIdPV, acc0);
   if (np > 1) tc::mma_ts(ocol, pcol + 8, vd + (uint64_t)(kPageBytes >> 4), kIdPV, 1u);
   if (np > 2) tc::mma_ts(ocol, pcol + 16, vd + (uint64_t)((2 * kPageBytes) >> 4), kIdPV, 1u);
   if (np > 3) tc::mma_ts(ocol, pcol + 24, vd + (uint64_t)((3 * kPageBytes) >> 4), kIdPV, 1u);
 }
+// barrier over the two softmax warps of one TMEM lane quadrant, OR-reducing a predicate
+__device__ __forceinline__ bool pair_any(int q, bool pred) {
+  uint32_t out;
+  asm volatile(
+      "{\n.reg .pred pi, po;\nsetp.ne.u32 pi, %1, 0;\nbarrier.cta.red.or.pred po, %2, 64, pi;\nselp.u32 %0, 1, 0, po;\n}\n"
+      : "=r"(out)
+      : "r"((uint32_t)pred), "r"(2 + q)
+      : "memory");
+  return out != 0;
+}
+__device__ __forceinline__ void pair_sync(int q) { asm volatile("barrier.cta.sync %0, 64;" ::"r"(2 + q) : "memory"); }
 __device__ __forceinline__ void issue_q_copy(uint64_t qd) {  // Q tile smem -> TMEM
 #pragma unroll
   for (int k = 0; k < 8; ++k) tc::cp_128x256b(kColQ + k * 8, qd + (uint64_t)(((k >> 2) * kQHalf + (k & 3) * 32) >> 4));
@@ -175,9 +187,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
   uint64_t* vfull = kempty + kKSlots;     // [kVSlots] TMA -> PV issuer
   uint64_t* vempty = vfull + kVSlots;     // [kVSlots] PV commit -> TMA (and softmax O rescale)
   uint64_t* s_full = vempty + kVSlots;    // [kSBufs] QK commit -> softmax
-  uint64_t* p_full = s_full + kSBufs;     // [kSBufs] softmax warps -> PV issuer
+  uint64_t* p_full = s_full + kSBufs;     // [kSBufs] 8 softmax warps -> PV issuer
   uint64_t* pv_done = p_full + kSBufs;    // [kSBufs] PV commit -> QK issuer (S buffer free)
-  uint64_t* o_full = pv_done + kSBufs;    // PV commit -> epilogue (unit's O_0 / O_1 final)
+  uint64_t* o_full = pv_done + kSBufs;    // PV commit -> epilogue (unit's O final)
   uint64_t* o_empty = o_full + 1;         // epilogue warps -> PV issuer / softmax
   uint64_t* stat_full = o_empty + 1;      // 8 softmax warps -> epilogue
   uint64_t* q_free = stat_full + 1;       // QK issuer commit (Q tile copied to TMEM) -> stager
@@ -191,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
     }
     for (int b = 0; b < kSBufs; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 4);
+      mbar_init(&p_full[b], 8);
       mbar_init(&pv_done[b], 1);
     }
     mbar_init(o_full, 1);
@@ -324,14 +336,18 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         for (int blk = 0; blk < nblk; ++blk, ++g) {
           const int sb = g % kSBufs, sl = g % kKSlots;
           if (TRACE && g < 64) P.trace[blockIdx.x * kTraceWords + 128 + g] = globaltimer();
-          if (g >= kSBufs) mbar_wait(&pv_done[sb], ((g - kSBufs) / kSBufs) & 1);  // P(g-3) consumed
+          if (g >= kSBufs) mbar_wait(&pv_done[sb], ((g - kSBufs) / kSBufs) & 1);  // P(g - kSBufs) consumed
           mbar_wait(&kfull[sl], (g / kKSlots) & 1);
           tc::fence_after();
           const long long c0 = TRACE ? clock64() : 0;
           const uint64_t kd = kdesc0 + (uint64_t)(sl * (kSlotBytes >> 4));
-          if (sb == 0) issue_qk_mmas<0>(kd);
-          else if (sb == 1) issue_qk_mmas<1>(kd);
-          else issue_qk_mmas<2>(kd);
+          switch (sb) {
+            case 0: issue_qk_mmas<0>(kd); break;
+            case 1: issue_qk_mmas<1>(kd); break;
+            case 2: issue_qk_mmas<2>(kd); break;
+            case 3: issue_qk_mmas<3>(kd); break;
+            default: issue_qk_mmas<4>(kd); break;
+          }
           tc::mma_commit(&s_full[sb]);
           tc::mma_commit(&kempty[sl]);
           if (TRACE && g < 64) {
@@ -365,14 +381,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           const long long c1 = TRACE ? clock64() : 0;
           const uint64_t vd = vdesc0 + (uint64_t)((g % kVSlots) * (kSlotBytes >> 4));
           const int np = n_ent - blk * kBlkPages;
-          const uint32_t acc0 = blk >= 2 ? 1u : 0u;  // blocks 0 and 1 of a unit open O_0 / O_1
-          switch (g % 6) {  // (parity, S buffer)
-            case 0: issue_pv_mmas<0, 0>(vd, np, acc0); break;
-            case 1: issue_pv_mmas<1, 1>(vd, np, acc0); break;
-            case 2: issue_pv_mmas<0, 2>(vd, np, acc0); break;
-            case 3: issue_pv_mmas<1, 0>(vd, np, acc0); break;
-            case 4: issue_pv_mmas<0, 1>(vd, np, acc0); break;
-            default: issue_pv_mmas<1, 2>(vd, np, acc0); break;
+          const uint32_t acc0 = blk > 0 ? 1u : 0u;  // the unit's first block opens O
+          switch (sb) {
+            case 0: issue_pv_mmas<0>(vd, np, acc0); break;
+            case 1: issue_pv_mmas<1>(vd, np, acc0); break;
+            case 2: issue_pv_mmas<2>(vd, np, acc0); break;
+            case 3: issue_pv_mmas<3>(vd, np, acc0); break;
+            default: issue_pv_mmas<4>(vd, np, acc0); break;
           }
           tc::mma_commit(&vempty[g % kVSlots]);  // also certifies PV(g) to the softmax (O rescale)
           tc::mma_commit(&pv_done[sb]);
@@ -382,14 +397,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       }
     }
   } else if (warp >= 4 && warp < 12) {
-    // ---------------- softmax: two warpgroups ping-pong over the block parity ----------------
-    // WG par (warps 4-7: par 0, 8-11: par 1) owns blocks g with g & 1 == par: S buffer par,
-    // O buffer par and its own (m, l) per row.  Thread = query row = TMEM lane.
-    const int par = (warp >> 2) - 1;
-    const int q = warp & 3;
+    // ---------------- softmax: 8 warps, one block at a time ----------------
+    // Thread = query row = TMEM lane; the two warps of a lane quadrant split the block's 64
+    // columns (half h: pages 2h, 2h+1) and share the row's reference max, so P of every block
+    // is on one scale and all blocks accumulate into one O.
+    const int q = warp & 3, half = (warp - 4) >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t ocol = lane_base + kColO + par * 128;
+    const uint32_t ocol = lane_base + kColO + half * 64;  // this warp's half of O (rescale)
+    float* pmax = reinterpret_cast<float*>(smem + kOffFlag) + q * 64;
     int g = 0;
     for (int i = 0;; ++i) {
       const int buf = i & 1;
@@ -397,98 +413,85 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       const WorkItem* si = &s_item[buf];
       if (!si->valid) {
         if (i >= 1) mbar_wait(o_empty, (i - 1) & 1);
-        if (par == 0 && q == 0 && lane == 0) s_ep->valid = 0;
+        if (warp == 4 && lane == 0) s_ep->valid = 0;
         __syncwarp();
         if (lane == 0) mbar_arrive(stat_full);
         break;
       }
       const int n_ent = si->n_entries, n_mem = si->n_mem;
-      const bool warp_active = q * 32 < n_mem * P.R;
+      const bool warp_active = q * 32 < n_mem * P.R;  // same for both warps of the pair
       const int mi = r / P.R, hl = r % P.R;
       const bool row_active = mi < n_mem && hl < P.gqa;
       const PageRef* se = s_ent0 + buf * kMaxEntries;
       const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
       float m_ref = -INFINITY, l = 0.f;
-      bool first = true;  // first block of this parity in the unit: O_par not yet written
       for (int blk = 0; blk < nblk; ++blk, ++g) {
-        if ((g & 1) != par) continue;
         const int sb = g % kSBufs;
         const uint32_t scol = lane_base + kColS + sb * kBlkCols;
         mbar_wait(&s_full[sb], (g / kSBufs) & 1);
         tc::fence_after();
-        if (TRACE && q == 0 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + g] = globaltimer();
+        float v[32];
+        if (warp_active) tc::tmem_ld32(scol + half * 32, v);
+        if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + g] = globaltimer();
         if (warp_active) {
-          const int e0 = blk * kBlkPages;
-          // valid slots per page: ragged unit head / tail pages and partial pages; rows without a
-          // query see nothing
-          uint32_t vm[kBlkPages];
-          bool full_blk = row_active;
+          const long long sc0 = TRACE ? clock64() : 0;
+          // valid slots of this half's two pages (ragged unit head / tail, partial pages)
+          const int e0 = blk * kBlkPages + 2 * half;
+          uint32_t vm = 0u;
+          if (row_active) {
 #pragma unroll
-          for (int p = 0; p < kBlkPages; ++p) {
-            vm[p] = 0u;
-            if (row_active && e0 + p < n_ent) {
-              const PageRef ref = se[e0 + p];
-              vm[p] = ((1u << ref_count(ref)) - 1u) << ref_begin(ref);
-            }
-            full_blk &= vm[p] == 0xFFFFu;
+            for (int p = 0; p < 2; ++p)
+              if (e0 + p < n_ent) {
+                const PageRef ref = se[e0 + p];
+                vm |= (((1u << ref_count(ref)) - 1u) << ref_begin(ref)) << (16 * p);
+              }
           }
-          const bool masked = !__all_sync(0xffffffffu, full_blk);
-          // S in two 32-column halves (register budget); masked slots -> -inf
-          auto load_half = [&](int h, float* v) {
-            tc::tmem_ld32(scol + h * 32, v);
-            tc::tmem_wait_ld();
-            if (masked) {
+          tc::tmem_wait_ld();
+          if (!__all_sync(0xffffffffu, vm == 0xFFFFFFFFu)) {
 #pragma unroll
-              for (int t = 0; t < 32; ++t) v[t] = ((vm[2 * h + (t >> 4)] >> (t & 15)) & 1u) ? v[t] : -INFINITY;
-            }
-          };
-          uint32_t pk[kBlkCols / 2];
-          auto exp_block = [&](float mu) {
+            for (int t = 0; t < 32; ++t) v[t] = ((vm >> t) & 1u) ? v[t] : -INFINITY;
+          }
+          uint32_t pk[16];
+          auto exp_half = [&](float mu) {
             float l0 = 0.f, l1 = 0.f;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              float v[32];
-              load_half(h, v);
-#pragma unroll
-              for (int c = 0; c < 16; ++c) {
-                const float p0 = fast_exp2(fmaf(v[2 * c], P.scale_log2, -mu));
-                const float p1 = fast_exp2(fmaf(v[2 * c + 1], P.scale_log2, -mu));
-                l0 += p0;
-                l1 += p1;
-                pk[h * 16 + c] = pack_bf16(p0, p1);
-              }
+            for (int c = 0; c < 16; ++c) {
+              const float p0 = fast_exp2(fmaf(v[2 * c], P.scale_log2, -mu));
+              const float p1 = fast_exp2(fmaf(v[2 * c + 1], P.scale_log2, -mu));
+              l0 += p0;
+              l1 += p1;
+              pk[c] = pack_bf16(p0, p1);
             }
             return l0 + l1;
           };
-          // Fast path: exponentiate against the row's current reference; the reference moves only
-          // on the first block or when a block's mass exceeds kSumLimit (P <= kSumLimit is exact
-          // enough in bf16 and far from fp32 overflow), so no per-block max is needed.  S stays
-          // intact in TMEM until P is stored, so the slow path can re-read it.
+          // Fast path: exponentiate against the row's shared reference; it moves only on the
+          // unit's first block or when a half-block's mass exceeds kSumLimit / 2 (P stays exact
+          // enough in bf16 and far from fp32 overflow), so no per-block max is needed.
           bool need = row_active && m_ref == -INFINITY;
           float ls = 0.f;
           if (!__any_sync(0xffffffffu, need)) {
-            ls = exp_block(row_active ? m_ref : 0.f);
-            need = ls > kSumLimit;
+            ls = exp_half(row_active ? m_ref : 0.f);
+            need = ls > 0.5f * kSumLimit;
           }
-          if (__any_sync(0xffffffffu, need)) {
+          if (pair_any(q, need)) {
+            // slow path (both warps): pair-wide row max, move the reference, rescale O
             float mx = -INFINITY;
-#pragma unroll 1
-            for (int h = 0; h < 2; ++h) {
-              float v[32];
-              load_half(h, v);
 #pragma unroll
-              for (int c = 0; c < 32; ++c) mx = fmaxf(mx, v[c]);
-            }
-            mx *= P.scale_log2;  // raw-score max into the log2 domain (scale > 0 keeps order)
-            const float nref = need ? fmaxf(m_ref, mx) : m_ref;
-            const bool resc = need && m_ref != -INFINITY;
+            for (int t = 0; t < 32; ++t) mx = fmaxf(mx, v[t]);
+            pmax[half * 32 + lane] = mx;
+            pair_sync(q);
+            mx = fmaxf(mx, pmax[(half ^ 1) * 32 + lane]) * P.scale_log2;
+            pair_sync(q);  // both read before the next exchange overwrites
+            const bool move = row_active && (m_ref == -INFINITY || mx > m_ref + 8.f);
+            const float nref = move ? mx : m_ref;
+            const bool resc = move && m_ref != -INFINITY;
             const float alpha = resc ? fast_exp2(m_ref - nref) : 1.f;
-            if (!first && __any_sync(0xffffffffu, resc)) {
-              // O_par holds this parity's earlier blocks once PV(g-2) has completed (its slot's empty commit)
-              mbar_wait(&vempty[(g - 2) % kVSlots], ((g - 2) / kVSlots) & 1);
+            if (blk > 0 && __any_sync(0xffffffffu, resc)) {
+              // O holds blocks < blk of this unit once PV(g-1) has completed (its V slot commit)
+              mbar_wait(&vempty[(g - 1) % kVSlots], ((g - 1) / kVSlots) & 1);
               tc::fence_after();
 #pragma unroll 1
-              for (int c = 0; c < 4; ++c) {
+              for (int c = 0; c < 2; ++c) {
                 float o[32];
                 tc::tmem_ld32(ocol + c * 32, o);
                 tc::tmem_wait_ld();
@@ -499,22 +502,23 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
             }
             l *= alpha;
             m_ref = nref;
-            ls = exp_block(m_ref == -INFINITY ? 0.f : m_ref);
+            ls = exp_half(m_ref == -INFINITY ? 0.f : m_ref);
           }
           l += ls;
-          tc::tmem_st32u(scol, pk);
+          if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 672 + g] = clock64() - sc0;
+          tc::tmem_st16u(scol + half * 16, pk);
           tc::tmem_wait_st();
+          if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 800 + g] = clock64() - sc0;
         }
-        first = false;
         tc::fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[sb]);
-        if (TRACE && q == 0 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 64 + g] = globaltimer();
+        if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 64 + g] = globaltimer();
       }
-      // hand (m, l) and the unit header to the epilogue, release the unit slot
+      // hand (m, l_half) and the unit header to the epilogue, release the unit slot
       if (i >= 1) mbar_wait(o_empty, (i - 1) & 1);
-      s_stat[par * 128 + r] = make_float2(m_ref, first ? 0.f : l);
-      if (par == 0 && q == 0 && lane < kItemInts) reinterpret_cast<int*>(s_ep)[lane] = reinterpret_cast<const int*>(si)[lane];
+      s_stat[half * 128 + r] = make_float2(m_ref, l);
+      if (warp == 4 && lane < kItemInts) reinterpret_cast<int*>(s_ep)[lane] = reinterpret_cast<const int*>(si)[lane];
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(stat_full);
@@ -539,11 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       mbar_wait(o_full, i & 1);
       tc::fence_after();
       if (TRACE && r == 0 && i < 32) P.trace[blockIdx.x * kTraceWords + 256 + i] = globaltimer();
-      // merge the two parity partials of this row (a parity without blocks has l == 0)
-      const bool h0 = ml0.y > 0.f, h1 = ml1.y > 0.f;
-      const float mm = fmaxf(h0 ? ml0.x : -INFINITY, h1 ? ml1.x : -INFINITY);
-      const float w0 = h0 ? fast_exp2(ml0.x - mm) : 0.f, w1 = h1 ? fast_exp2(ml1.x - mm) : 0.f;
-      const float2 ml = make_float2(mm, w0 * ml0.y + w1 * ml1.y);
+      const float2 ml = make_float2(ml0.x, ml0.y + ml1.y);  // both halves share the reference
       const int head = kvh * P.gqa + hl;
       const int nslots = active ? P.slot_cnt[b] : 0;
       const int64_t orow = (int64_t)b * P.q_heads + head;
@@ -551,12 +551,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
-          float o[32], o1[32];
+          float o[32];
           tc::tmem_ld32(lane_base + kColO + c * 32, o);
-          tc::tmem_ld32(lane_base + kColO + 128 + c * 32, o1);
           tc::tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = (h0 ? w0 * o[e] : 0.f) + (h1 ? w1 * o1[e] : 0.f);
           if (active) {
             if (nslots == 1) {
               store_row(P, orow, c, o, inv);

@@ -7,7 +7,7 @@ import sys
 
 import numpy as np
 
-W = 672
+W = 864
 t = np.fromfile(sys.argv[1], dtype=np.uint64).astype(np.int64)
 t = t.reshape(-1, W)
 valid = t[:, 320] > 0
@@ -40,6 +40,9 @@ stat("MMA PV issue ns @1965MHz", ow[sm_rel > 0] * 1.0)
 tw = t[:, 608:672].astype(np.float64) / 1.965
 stat("TMA issue per block ns (after empty)", tw[t[:, 544:608] > 0] * 1.0)
 stat("TMA block issue -> QK commit", pairs(t[:, 544:608], qk_e))
+for nm, o in (("softmax: masks+ld+exp (fast path) ns", 672), ("softmax: P store+wait ns", 736), ("softmax: compute total ns", 800)):
+    x = t[:, o:o + 64].astype(np.float64) / 1.965
+    stat(nm, x[x > 0] * 1.0)
 stat("epilogue (incl. combine)", pairs(ep_s, ep_e))
 stat("unit period (claim i -> i+1)", pairs(claim[:, :-1], claim[:, 1:]))
 stat("first S after first claim", sm_seen[:, 0] - claim[:, 0])
