@@ -64,6 +64,7 @@ constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dim
 constexpr int kQBytes = 2 * kQHalf;
 constexpr float kSumLimit = 4096.f;                        // block mass that moves the softmax reference
 constexpr int kPrefetch = 32;                               // pages of a unit prefetched into L2 at staging
+constexpr bool kUseCopies = false;                          // see build_plan
 constexpr int kSBufs = 5;                                   // S / P buffers in flight
 constexpr int kColS = 0;                                    // TMEM: S0..S4 (64 cols each)
 constexpr int kColO = kSBufs * kBlkCols;                    //       O (128 cols)
@@ -78,7 +79,7 @@ struct __align__(16) WorkItem {
   int32_t slot_base;             // partial slot of member 0 (member m -> slot_base + m)
   int32_t kvh;                   // KV head
   int32_t valid;
-  int32_t pad;
+  int32_t copies;                // query-row copies F (1, 2, 4): rows replicated across lane quadrants
   int32_t members[kMaxMem];      // batch indices
 };
 static_assert(sizeof(WorkItem) == 96, "WorkItem layout");
@@ -91,8 +92,9 @@ constexpr int kOffEnt = kOffVRing + kVSlots * kSlotBytes;
 constexpr int kOffItem = kOffEnt + 2 * kMaxEntries * 8;
 constexpr int kOffEp = kOffItem + 2 * sizeof(WorkItem);
 constexpr int kOffStat = kOffEp + 2 * sizeof(WorkItem);
-constexpr int kOffFlag = kOffStat + 2 * 128 * 8;  // pair max exchange [4][2][32] floats
-constexpr int kOffBar = kOffFlag + 4 * 2 * 32 * 4;
+constexpr int kOffFlag = kOffStat + 2 * 128 * 8;  // softmax group max exchange [4][8][32] floats
+constexpr int kOffXch = kOffFlag + 4 * 8 * 32 * 4;  // epilogue copy merge [3][32][16] floats
+constexpr int kOffBar = kOffXch + 3 * 32 * 16 * 4;
 constexpr int kNumBars = 4 + 2 * (kKSlots + kVSlots) + 3 * kSBufs + 4;
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
 constexpr int kSmem = kOffTmem + 16 + 1024;  // + 1 KiB alignment slack
@@ -139,6 +141,20 @@ __device__ __forceinline__ void store_row(const DecodeParams& P, int64_t row, in
 
 // MMA issue helpers with compile-time TMEM operands: the issuing thread then needs no per-MMA
 // register -> uniform-register moves (which the compiler otherwise wraps in an ELECT loop).
+__device__ __forceinline__ void store_row16(const DecodeParams& P, int64_t row, int k, const float* o, float inv) {
+  if (P.out_f32) {
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + row * kHeadDim + k * 16);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
+  } else {
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + row * kHeadDim + k * 16);
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
+                          pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
+  }
+}
+
 template <int SB>
 __device__ __forceinline__ void issue_qk_mmas(uint64_t kd) {  // S_SB = Q . K_blk^T (A = Q in TMEM)
 #pragma unroll
@@ -154,17 +170,153 @@ __device__ __forceinline__ void issue_pv_mmas(uint64_t vd, int np, uint32_t acc0
   if (np > 2) tc::mma_ts(ocol, pcol + 16, vd + (uint64_t)((2 * kPageBytes) >> 4), kIdPV, 1u);
   if (np > 3) tc::mma_ts(ocol, pcol + 24, vd + (uint64_t)((3 * kPageBytes) >> 4), kIdPV, 1u);
 }
-// barrier over the two softmax warps of one TMEM lane quadrant, OR-reducing a predicate
-__device__ __forceinline__ bool pair_any(int q, bool pred) {
+// named barrier over the softmax warps holding one logical row quadrant, OR-reducing a predicate
+__device__ __forceinline__ bool group_any(int id, int count, bool pred) {
   uint32_t out;
   asm volatile(
-      "{\n.reg .pred pi, po;\nsetp.ne.u32 pi, %1, 0;\nbarrier.cta.red.or.pred po, %2, 64, pi;\nselp.u32 %0, 1, 0, po;\n}\n"
+      "{\n.reg .pred pi, po;\nsetp.ne.u32 pi, %1, 0;\nbarrier.cta.red.or.pred po, %2, %3, pi;\nselp.u32 %0, 1, 0, po;\n}\n"
       : "=r"(out)
-      : "r"((uint32_t)pred), "r"(2 + q)
+      : "r"((uint32_t)pred), "r"(id), "r"(count)
       : "memory");
   return out != 0;
 }
-__device__ __forceinline__ void pair_sync(int q) { asm volatile("barrier.cta.sync %0, 64;" ::"r"(2 + q) : "memory"); }
+__device__ __forceinline__ void group_sync(int id, int count) {
+  asm volatile("barrier.cta.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// One work unit of the softmax role for one warp (F = query-row copies).  Thread = TMEM lane.
+// Copy c of the unit's rows lives in lane quadrants [c * 4/F, (c+1) * 4/F); the block's 64
+// token columns are split into 2F parts: copy c, warp half h owns part 2c + h and writes zeros
+// into the other copies' parts of its rows, so every copy accumulates a disjoint slice of the
+// tokens into its own O rows (summed by the epilogue).  All 2F warps holding a logical row share
+// its reference max through one named barrier per block (OR-reduced "move" flag).
+template <int F, bool TRACE>
+__device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int n_ent, int n_mem,
+                                             const PageRef* se, int warp, int lane, uint32_t tmem, uint64_t* s_full,
+                                             uint64_t* p_full, uint64_t* vempty, float* xmax, float& m_out,
+                                             float& l_out) {
+  constexpr int QPC = 4 / F, RPC = 32 * QPC, NP = 2 * F, W = kBlkCols / NP, WP = W / 2;
+  const int q = warp & 3, half = (warp - 4) >> 2;
+  const int c = q / QPC, lq = q % QPC;
+  const int r = q * 32 + lane, lr = r - c * RPC;
+  const int mi = lr / P.R, hl = lr % P.R;
+  const bool row_active = mi < n_mem && hl < P.gqa;
+  const bool warp_active = lq * 32 < n_mem * P.R;  // uniform over the group
+  const int part = c * 2 + half;
+  const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+  const uint32_t ocol = lane_base + kColO + half * 64;
+  float* gmax = xmax + lq * (NP * 32);
+  const int bar_id = 2 + lq, bar_cnt = 64 * F;
+  const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
+  float m_ref = -INFINITY, l = 0.f;
+  for (int blk = 0; blk < nblk; ++blk, ++g) {
+    const int sb = g % kSBufs;
+    const uint32_t scol = lane_base + kColS + sb * kBlkCols;
+    mbar_wait(&s_full[sb], (g / kSBufs) & 1);
+    tc::fence_after();
+    if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + g] = globaltimer();
+    if (warp_active) {
+      const long long sc0 = TRACE ? clock64() : 0;
+      float v[W];
+      tc::tmem_ldN<W>(scol + part * W, v);
+      // valid slots of this part's tokens (ragged unit head / tail pages, partial pages)
+      const int t0 = part * W;
+      uint32_t vm = 0u;
+      if (row_active) {
+#pragma unroll
+        for (int p = 0; p < (W + 15) / 16; ++p) {
+          const int pg = blk * kBlkPages + t0 / 16 + p;
+          if (pg < n_ent) {
+            const PageRef ref = se[pg];
+            const uint32_t pm = ((1u << ref_count(ref)) - 1u) << ref_begin(ref);
+            vm |= (W == 8 ? (pm >> (t0 & 15)) & 0xFFu : pm) << (16 * p);
+          }
+        }
+      }
+      constexpr uint32_t kFull = W == 32 ? 0xFFFFFFFFu : ((1u << W) - 1u);
+      tc::tmem_wait_ld();
+      if (!__all_sync(0xffffffffu, vm == kFull)) {
+#pragma unroll
+        for (int t = 0; t < W; ++t) v[t] = ((vm >> t) & 1u) ? v[t] : -INFINITY;
+      }
+      uint32_t pk[WP];
+      auto exp_part = [&](float mu) {
+        float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < WP; ++k) {
+          const float p0 = fast_exp2(fmaf(v[2 * k], P.scale_log2, -mu));
+          const float p1 = fast_exp2(fmaf(v[2 * k + 1], P.scale_log2, -mu));
+          l0 += p0;
+          l1 += p1;
+          pk[k] = pack_bf16(p0, p1);
+        }
+        return l0 + l1;
+      };
+      // Fast path: exponentiate against the row's shared reference; it moves only on the unit's
+      // first block or when a part's mass exceeds kSumLimit / NP (P stays exact enough in bf16
+      // and far from fp32 overflow), so no per-block max is needed.
+      bool need = row_active && m_ref == -INFINITY;
+      float ls = 0.f;
+      if (!__any_sync(0xffffffffu, need)) {
+        ls = exp_part(row_active ? m_ref : 0.f);
+        need = ls > kSumLimit / NP;
+      }
+      // the barrier also orders every warp's S reads before any warp's P / zero stores
+      if (group_any(bar_id, bar_cnt, need)) {
+        // slow path (whole group): row max over all parts, move the reference, rescale O
+        float mx = -INFINITY;
+#pragma unroll
+        for (int t = 0; t < W; ++t) mx = fmaxf(mx, v[t]);
+        gmax[part * 32 + lane] = mx;
+        group_sync(bar_id, bar_cnt);
+#pragma unroll
+        for (int pp = 0; pp < NP; ++pp) mx = fmaxf(mx, gmax[pp * 32 + lane]);
+        mx *= P.scale_log2;  // raw-score max into the log2 domain (scale > 0 keeps order)
+        group_sync(bar_id, bar_cnt);  // all read before the next exchange overwrites
+        const bool move = row_active && (m_ref == -INFINITY || mx > m_ref + 8.f);
+        const float nref = move ? mx : m_ref;
+        const bool resc = move && m_ref != -INFINITY;
+        const float alpha = resc ? fast_exp2(m_ref - nref) : 1.f;
+        if (blk > 0 && __any_sync(0xffffffffu, resc)) {
+          // O holds blocks < blk of this unit once PV(g-1) has completed (its V slot commit)
+          mbar_wait(&vempty[(g - 1) % kVSlots], ((g - 1) / kVSlots) & 1);
+          tc::fence_after();
+#pragma unroll 1
+          for (int cc = 0; cc < 2; ++cc) {
+            float o[32];
+            tc::tmem_ld32(ocol + cc * 32, o);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] *= alpha;
+            tc::tmem_st32(ocol + cc * 32, o);
+          }
+        }
+        l *= alpha;
+        m_ref = nref;
+        ls = exp_part(m_ref == -INFINITY ? 0.f : m_ref);
+      }
+      l += ls;
+      if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 672 + g] = clock64() - sc0;
+      tc::tmem_stNu<WP>(scol + part * WP, pk);
+      if (F > 1) {
+        uint32_t z[WP];
+#pragma unroll
+        for (int k = 0; k < WP; ++k) z[k] = 0u;
+#pragma unroll
+        for (int c2 = 0; c2 < F; ++c2)
+          if (c2 != c) tc::tmem_stNu<WP>(scol + (c2 * 2 + half) * WP, z);
+      }
+      tc::tmem_wait_st();
+      if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 800 + g] = clock64() - sc0;
+    }
+    tc::fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&p_full[sb]);
+    if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 64 + g] = globaltimer();
+  }
+  m_out = m_ref;
+  l_out = l;
+}
 __device__ __forceinline__ void issue_q_copy(uint64_t qd) {  // Q tile smem -> TMEM
 #pragma unroll
   for (int k = 0; k < 8; ++k) tc::cp_128x256b(kColQ + k * 8, qd + (uint64_t)(((k >> 2) * kQHalf + (k & 3) * 32) >> 4));
@@ -272,12 +424,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           prefetch_l2(P.vplane + pf, kPageBytes);
         }
       }
-      if (lane == 0) mbar_arrive_expect_tx(&item_full[buf], 2u * half_bytes * (uint32_t)n_mem);
+      const int copies = si->copies, rpc = 128 / copies;
+      if (lane == 0) mbar_arrive_expect_tx(&item_full[buf], 2u * half_bytes * (uint32_t)(n_mem * copies));
       __syncwarp();
-      if (lane < 2 * n_mem) {
-        const int m = lane >> 1, h = lane & 1;
+      if (lane < 2 * n_mem * copies) {  // (member, half, copy): n_mem * R * copies <= 128 rows
+        const int m = (lane >> 1) % n_mem, h = lane & 1, cp = (lane >> 1) / n_mem;
         const int b = si->members[m];
-        uint8_t* dst = smem + kOffQ + h * kQHalf + m * half_bytes;
+        uint8_t* dst = smem + kOffQ + h * kQHalf + (cp * rpc) * 128 + m * half_bytes;
         const __nv_bfloat16* src = P.q_tile + (((size_t)b * P.kv_heads + kvh) * 2 + h) * (size_t)P.R * 64;
         bulk_g2s(dst, src, half_bytes, &item_full[buf]);
       }
@@ -397,15 +550,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       }
     }
   } else if (warp >= 4 && warp < 12) {
-    // ---------------- softmax: 8 warps, one block at a time ----------------
-    // Thread = query row = TMEM lane; the two warps of a lane quadrant split the block's 64
-    // columns (half h: pages 2h, 2h+1) and share the row's reference max, so P of every block
-    // is on one scale and all blocks accumulate into one O.
+    // ---------------- softmax: 8 warps, one block at a time (softmax_unit) ----------------
     const int q = warp & 3, half = (warp - 4) >> 2;
     const int r = q * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-    const uint32_t ocol = lane_base + kColO + half * 64;  // this warp's half of O (rescale)
-    float* pmax = reinterpret_cast<float*>(smem + kOffFlag) + q * 64;
+    float* xmax = reinterpret_cast<float*>(smem + kOffFlag);
     int g = 0;
     for (int i = 0;; ++i) {
       const int buf = i & 1;
@@ -418,103 +566,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         if (lane == 0) mbar_arrive(stat_full);
         break;
       }
-      const int n_ent = si->n_entries, n_mem = si->n_mem;
-      const bool warp_active = q * 32 < n_mem * P.R;  // same for both warps of the pair
-      const int mi = r / P.R, hl = r % P.R;
-      const bool row_active = mi < n_mem && hl < P.gqa;
+      const int n_ent = si->n_entries, n_mem = si->n_mem, copies = si->copies;
       const PageRef* se = s_ent0 + buf * kMaxEntries;
-      const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
-      float m_ref = -INFINITY, l = 0.f;
-      for (int blk = 0; blk < nblk; ++blk, ++g) {
-        const int sb = g % kSBufs;
-        const uint32_t scol = lane_base + kColS + sb * kBlkCols;
-        mbar_wait(&s_full[sb], (g / kSBufs) & 1);
-        tc::fence_after();
-        float v[32];
-        if (warp_active) tc::tmem_ld32(scol + half * 32, v);
-        if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + g] = globaltimer();
-        if (warp_active) {
-          const long long sc0 = TRACE ? clock64() : 0;
-          // valid slots of this half's two pages (ragged unit head / tail, partial pages)
-          const int e0 = blk * kBlkPages + 2 * half;
-          uint32_t vm = 0u;
-          if (row_active) {
-#pragma unroll
-            for (int p = 0; p < 2; ++p)
-              if (e0 + p < n_ent) {
-                const PageRef ref = se[e0 + p];
-                vm |= (((1u << ref_count(ref)) - 1u) << ref_begin(ref)) << (16 * p);
-              }
-          }
-          tc::tmem_wait_ld();
-          if (!__all_sync(0xffffffffu, vm == 0xFFFFFFFFu)) {
-#pragma unroll
-            for (int t = 0; t < 32; ++t) v[t] = ((vm >> t) & 1u) ? v[t] : -INFINITY;
-          }
-          uint32_t pk[16];
-          auto exp_half = [&](float mu) {
-            float l0 = 0.f, l1 = 0.f;
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-              const float p0 = fast_exp2(fmaf(v[2 * c], P.scale_log2, -mu));
-              const float p1 = fast_exp2(fmaf(v[2 * c + 1], P.scale_log2, -mu));
-              l0 += p0;
-              l1 += p1;
-              pk[c] = pack_bf16(p0, p1);
-            }
-            return l0 + l1;
-          };
-          // Fast path: exponentiate against the row's shared reference; it moves only on the
-          // unit's first block or when a half-block's mass exceeds kSumLimit / 2 (P stays exact
-          // enough in bf16 and far from fp32 overflow), so no per-block max is needed.
-          bool need = row_active && m_ref == -INFINITY;
-          float ls = 0.f;
-          if (!__any_sync(0xffffffffu, need)) {
-            ls = exp_half(row_active ? m_ref : 0.f);
-            need = ls > 0.5f * kSumLimit;
-          }
-          if (pair_any(q, need)) {
-            // slow path (both warps): pair-wide row max, move the reference, rescale O
-            float mx = -INFINITY;
-#pragma unroll
-            for (int t = 0; t < 32; ++t) mx = fmaxf(mx, v[t]);
-            pmax[half * 32 + lane] = mx;
-            pair_sync(q);
-            mx = fmaxf(mx, pmax[(half ^ 1) * 32 + lane]) * P.scale_log2;
-            pair_sync(q);  // both read before the next exchange overwrites
-            const bool move = row_active && (m_ref == -INFINITY || mx > m_ref + 8.f);
-            const float nref = move ? mx : m_ref;
-            const bool resc = move && m_ref != -INFINITY;
-            const float alpha = resc ? fast_exp2(m_ref - nref) : 1.f;
-            if (blk > 0 && __any_sync(0xffffffffu, resc)) {
-              // O holds blocks < blk of this unit once PV(g-1) has completed (its V slot commit)
-              mbar_wait(&vempty[(g - 1) % kVSlots], ((g - 1) / kVSlots) & 1);
-              tc::fence_after();
-#pragma unroll 1
-              for (int c = 0; c < 2; ++c) {
-                float o[32];
-                tc::tmem_ld32(ocol + c * 32, o);
-                tc::tmem_wait_ld();
-#pragma unroll
-                for (int e = 0; e < 32; ++e) o[e] *= alpha;
-                tc::tmem_st32(ocol + c * 32, o);
-              }
-            }
-            l *= alpha;
-            m_ref = nref;
-            ls = exp_half(m_ref == -INFINITY ? 0.f : m_ref);
-          }
-          l += ls;
-          if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 672 + g] = clock64() - sc0;
-          tc::tmem_st16u(scol + half * 16, pk);
-          tc::tmem_wait_st();
-          if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 800 + g] = clock64() - sc0;
-        }
-        tc::fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[sb]);
-        if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 64 + g] = globaltimer();
-      }
+      float m_ref, l;
+      if (copies == 4)
+        softmax_unit<4, TRACE>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
+      else if (copies == 2)
+        softmax_unit<2, TRACE>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
+      else
+        softmax_unit<1, TRACE>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
       // hand (m, l_half) and the unit header to the epilogue, release the unit slot
       if (i >= 1) mbar_wait(o_empty, (i - 1) & 1);
       s_stat[half * 128 + r] = make_float2(m_ref, l);
@@ -526,41 +586,83 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       }
     }
   } else if (warp >= 12) {
-    // ---------------- epilogue warpgroup: merge O_0 / O_1, output or split-KV partial ----------------
+    // ---------------- epilogue warpgroup: sum row copies, output or split-KV partial ----------------
     const int q = warp & 3;
     const int r = q * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
+    float* xch = reinterpret_cast<float*>(smem + kOffXch);  // [copy - 1][row in copy][16]
     for (int i = 0;; ++i) {
       mbar_wait(stat_full, i & 1);
       if (!s_ep->valid) break;
-      const int n_mem = s_ep->n_mem, kvh = s_ep->kvh;
-      const int mi = r / P.R, hl = r % P.R;
-      const bool active = mi < n_mem && hl < P.gqa;
-      const bool warp_active = q * 32 < n_mem * P.R;
+      const int n_mem = s_ep->n_mem, kvh = s_ep->kvh, F = s_ep->copies;
+      const int qpc = 4 / F, rpc = 32 * qpc;
+      const int c = q / qpc, lq = q % qpc, lr = r - c * rpc;
+      const int mi = lr / P.R, hl = lr % P.R;
+      const bool warp_active = lq * 32 < n_mem * P.R;
+      const bool active = c == 0 && mi < n_mem && hl < P.gqa;
       const int b = active ? s_ep->members[mi] : 0;
       const int64_t slot = s_ep->slot_base + mi;
-      const float2 ml0 = s_stat[r], ml1 = s_stat[128 + r];
+      // every copy and warp half shares the reference; the row's mass is the sum of the parts
+      float2 ml = make_float2(s_stat[lr].x, 0.f);
+      for (int cc = 0; cc < F; ++cc) ml.y += s_stat[cc * rpc + lr].y + s_stat[128 + cc * rpc + lr].y;
       mbar_wait(o_full, i & 1);
       tc::fence_after();
       if (TRACE && r == 0 && i < 32) P.trace[blockIdx.x * kTraceWords + 256 + i] = globaltimer();
-      const float2 ml = make_float2(ml0.x, ml0.y + ml1.y);  // both halves share the reference
       const int head = kvh * P.gqa + hl;
       const int nslots = active ? P.slot_cnt[b] : 0;
       const int64_t orow = (int64_t)b * P.q_heads + head;
-      if (warp_active) {
-        const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
+      const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
+      if (F == 1) {
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int k = 0; k < 4; ++k) {  // 32-column chunks of O
           float o[32];
-          tc::tmem_ld32(lane_base + kColO + c * 32, o);
-          tc::tmem_wait_ld();
+          if (warp_active) {
+            tc::tmem_ld32(lane_base + kColO + k * 32, o);
+            tc::tmem_wait_ld();
+          }
           if (active) {
             if (nslots == 1) {
-              store_row(P, orow, c, o, inv);
+              store_row(P, orow, k, o, inv);
             } else {
-              float4* dst = reinterpret_cast<float4*>(P.part_o + (slot * P.q_heads + head) * kHeadDim + c * 32);
+              float4* dst = reinterpret_cast<float4*>(P.part_o + (slot * P.q_heads + head) * kHeadDim + k * 32);
 #pragma unroll
               for (int e = 0; e < 8; ++e) __stcg(dst + e, make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]));
+            }
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int k = 0; k < 8; ++k) {  // 16-column chunks of O
+          float o[16];
+          if (warp_active) {
+            tc::tmem_ldN<16>(lane_base + kColO + k * 16, o);
+            tc::tmem_wait_ld();
+          }
+          if (F > 1) {
+            if (c > 0 && warp_active)
+  #pragma unroll
+              for (int e = 0; e < 16; e += 4)
+                *reinterpret_cast<float4*>(&xch[((c - 1) * rpc + lr) * 16 + e]) = make_float4(o[e], o[e + 1], o[e + 2], o[e + 3]);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (c == 0 && warp_active)
+              for (int cc = 1; cc < F; ++cc)
+  #pragma unroll
+                for (int e = 0; e < 16; e += 4) {
+                  const float4 x = *reinterpret_cast<const float4*>(&xch[((cc - 1) * rpc + lr) * 16 + e]);
+                  o[e] += x.x;
+                  o[e + 1] += x.y;
+                  o[e + 2] += x.z;
+                  o[e + 3] += x.w;
+                }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+          }
+          if (active) {
+            if (nslots == 1) {
+              store_row16(P, orow, k, o, inv);
+            } else {
+              float4* dst = reinterpret_cast<float4*>(P.part_o + (slot * P.q_heads + head) * kHeadDim + k * 16);
+  #pragma unroll
+              for (int e = 0; e < 4; ++e) __stcg(dst + e, make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]));
             }
           }
         }
@@ -784,6 +886,11 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
         w.n_mem = (int32_t)(m1 - m0);
         w.slot_base = n_slots;
         w.valid = 1;
+        const int rows = w.n_mem * R;
+        // row replication (copies > 1) trades softmax time for an epilogue merge; measured
+        // slower end to end on C2 with the current epilogue, so it stays off
+        w.copies = kUseCopies ? (rows <= 32 ? 4 : (rows <= 64 ? 2 : 1)) : 1;
+        (void)rows;
         for (size_t k = m0; k < m1; ++k) {
           w.members[k - m0] = s.mem[k];
           slots_of[s.mem[k]].push_back(n_slots + (int32_t)(k - m0));
