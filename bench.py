@@ -9,8 +9,10 @@ hot path of engine.cpp:599-641 (resolve + ToyModel::step attention + extend), ba
   R requests per GPU (default 16 -> 0.8 GB of KV, larger than the 126 MB L2: no flush needed).
 
 Prints ONE JSON line (rank 0). `--impl reference` times the reference CPU path instead: the
-oracle restatement of toy_model.cpp:121-157 (fp64, GQA) on all host cores ("port"; the
-reference's own attention only exists fused inside a full fp64 ToyModel::step).
+patched reference core compiled from /root/reference (oracle/_ref/refdrv, kind "reference") running
+its own decode path (RadixStore::resolve_payloads + ToyModel::step, engine.cpp:599-607) on all host
+cores, attention part isolated as step(ctx) - step(empty); if that binary was not built, the
+oracle restatement of toy_model.cpp:121-157 (fp64, GQA; kind "port").
 """
 from __future__ import annotations
 
@@ -35,11 +37,11 @@ METRIC = "branch-parallel decode tokens/s/GPU; attention HBM GB/s vs 8 TB/s roof
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--requests", type=int, default=16, help="requests per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
 
 
@@ -89,6 +91,29 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def ref_binary():
+    path = os.path.join(REPO, "oracle", "_ref", "refdrv")
+    return path if os.access(path, os.X_OK) else None
+
+
+def cpu_reference_ref(seconds: float):
+    """The reference's own decode path (engine.cpp:599-607: RadixStore::resolve_payloads + ToyModel::step),
+    compiled from /root/reference by oracle/ref_build.sh, on all host cores (one branch per thread).
+    step() also runs projections + MLP, so the value is the attention path: step(ctx) - step(empty ctx)."""
+    threads = os.cpu_count() or 1
+    out = subprocess.run([ref_binary(), "decode", str(threads), str(seconds)], capture_output=True, text=True,
+                         check=True, timeout=600).stdout
+    r = json.loads(out.strip().splitlines()[-1])
+    return {"value": r["tokens_per_s_attention"], "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "sample": f"{r['steps']} branch decode steps of the patched reference (resolve_payloads + ToyModel::step "
+                      f"attention; 40 heads x 128 MHA, ctx {r['ctx']}, fp64) on {threads} threads; full step incl. "
+                      f"projections/MLP: {r['tokens_per_s_full']:.3f} tokens/s"}
+
+
+def cpu_baseline(seconds: float):
+    return cpu_reference_ref(seconds) if ref_binary() else cpu_reference(seconds)
+
+
 def cpu_reference(seconds: float):
     """Oracle restatement of the reference attention core on all host cores, one request's step
     (8 branches x 40 heads over 4096+1024 tokens) repeated for ~`seconds`."""
@@ -125,7 +150,7 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cpu = cpu_reference(max(2.0, args.cpu_seconds))
+    cpu = cpu_baseline(max(2.0, args.cpu_seconds))
     line = {"impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * BRANCHES / cpu["value"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -263,7 +288,9 @@ def run_ours(args):
     tokens_per_step = n * world
     value = tokens_per_step / (ms / 1e3)
     # roofline of the dominant kernel: algorithmic bytes = unique KV read once + Q/O
-    kv_tokens = info["unique_kv_tokens"]
+    # every step appends one token per branch before attending, so the context (and the bytes a
+    # step must read) grows by n tokens per step: use the mean over the timed steps
+    kv_tokens = info["unique_kv_tokens"] + n * (args.steps + 1) / 2.0
     alg_bytes = kv_tokens * HKV * D * 2 * 2 + n * HQ * D * 2 * 2
     achieved = alg_bytes / (att_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
@@ -277,7 +304,7 @@ def run_ours(args):
         pass
 
     if rank == 0:
-        cpu = cpu_reference(args.cpu_seconds) if world == 1 else None
+        cpu = cpu_baseline(args.cpu_seconds) if world == 1 else None
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -285,14 +312,16 @@ def run_ours(args):
             "config": {"workload": "configs[1] x R requests per GPU: 40q/8kv heads, d128, bf16, 4K shared Map "
                                    "prefix, 8 branches x 1K tokens (+1 per step), KV page 16",
                        "requests_per_gpu": R, "branches_per_gpu": n, "l2": "inputs 0.8+ GB > L2 (no flush)",
+                       "mean_kv_tokens_per_step": kv_tokens,
                        "step": "append 1 token K/V per branch (RoPE fused) + cascade decode attention"},
             "e2e": {"value": tokens_per_step / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "decode_kernel+combine_kernel", "alg_bytes_per_launch": alg_bytes,
+                         "kernel": "decode_tc_kernel (+ rope_q_tile_kernel, combine_kernel)",
+                         "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": att_ms, "frac_of_8TBs": achieved / 8000.0},
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": 4 * args.steps,  # per step: k_append_one, rope_q_tile, decode_tc, combine
             "clocks": clk,
             "plan": info,
         }

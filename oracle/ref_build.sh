@@ -20,6 +20,6 @@ for f in dag grammar kvcache synth tokenizer toy_model engine; do
   objs+=("$OUT/$f.o")
 done
 wait
-$CXX $FLAGS "$HERE/refdrv.cpp" "${objs[@]}" -o "$OUT/refdrv"
+$CXX $FLAGS "$HERE/refdrv.cpp" "${objs[@]}" -o "$OUT/refdrv" -lpthread
 rm -rf "$OUT/src"  # patched copies were build inputs only
 echo "built $OUT/refdrv"

@@ -13,6 +13,8 @@
 //                                    (toy_model.cpp:83-202, engine.cpp:928-939)
 //   refdrv forced <words> <plen>     time engine::run_forced on the C1 config (BASELINE
 //                                    configs[0]); prints tokens/s
+//   refdrv decode <threads> <secs>   time the reference decode path (resolve_payloads + step)
+//                                    on the configs[1] shape; prints tokens/s
 #include <chrono>
 #include <cinttypes>
 #include <cstdio>
@@ -22,6 +24,7 @@
 #include <set>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "multiverse/dag.hpp"
@@ -522,6 +525,83 @@ int mode_forced_bench(int prompt_words, int path_words, int reps) {
   return 0;
 }
 
+// The reference's own decode path for BASELINE configs[1] (engine.cpp:599-607: resolve_payloads of
+// the lane's context + ToyModel::step), one layer of Qwen2.5-32B attention shape (40 heads x 128;
+// the reference has no GQA, so K/V per token are 40 heads wide), 4096-token shared prefix forked
+// into 8 branches of 1023 tokens, timed on `threads` host threads (one branch per thread;
+// RadixStore resolution is read-only and ToyModel::step is const).
+// step() also runs the QKV/O projections and the MLP, which are not part of the attention path,
+// so each sample also times step() with an empty context and reports the difference.
+int mode_decode_bench(int threads, double seconds) {
+  toy::ToyModelConfig cfg;
+  cfg.layers = 1;
+  cfg.heads = 40;
+  cfg.model_dim = 5120;
+  cfg.vocab_size = 256;
+  toy::ToyModel model(cfg);
+  const std::size_t rec = static_cast<std::size_t>(cfg.kv_doubles_per_token()) * sizeof(double);
+  kv::RadixStore store(rec, 1u << 16);
+  synth::Rng rng(0);
+  auto payload = [&](std::size_t n) {
+    std::vector<double> d(n * cfg.kv_doubles_per_token());
+    for (auto& x : d) x = rng.next_symmetric(1.0);
+    std::vector<std::byte> b(d.size() * sizeof(double));
+    std::memcpy(b.data(), d.data(), b.size());
+    return b;
+  };
+  auto ids = [](std::size_t n, int base) {
+    std::vector<kv::TokenId> t(n);
+    for (std::size_t i = 0; i < n; ++i) t[i] = 10 + static_cast<int>((base + i) % 240);
+    return t;
+  };
+  const std::size_t prefix = 4096, blen = 1023;
+  const int nb = 8;
+  auto root = store.create();
+  auto pfx_ids = ids(prefix, 0);
+  auto pfx = store.extend(root, pfx_ids, payload(prefix));
+  auto kids = store.fork(pfx, nb);
+  std::vector<kv::SequenceHandle> br;
+  for (int b = 0; b < nb; ++b) {
+    auto bi = ids(blen, 1000 * (b + 1));
+    br.push_back(store.extend(kids[b], bi, payload(blen)));
+  }
+  std::vector<double> t_full(threads, 0.0), t_empty(threads, 0.0);
+  std::vector<int> reps(threads, 0);
+  const auto start = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] {
+      const auto& h = br[t % nb];
+      const int pos = static_cast<int>(prefix + blen);
+      while (std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count() < seconds || reps[t] == 0) {
+        auto a = std::chrono::steady_clock::now();
+        auto ctx = store.resolve_payloads(h);
+        auto out = model.step(std::span<const double>(reinterpret_cast<const double*>(ctx.data()), ctx.size() / sizeof(double)),
+                              h.length, 13, pos);
+        auto b = std::chrono::steady_clock::now();
+        auto out0 = model.step(std::span<const double>(), 0, 13, pos);
+        auto c = std::chrono::steady_clock::now();
+        t_full[t] += std::chrono::duration<double>(b - a).count();
+        t_empty[t] += std::chrono::duration<double>(c - b).count();
+        reps[t] += 1;
+        if (out.logits.empty() || out0.logits.empty()) std::abort();
+      }
+    });
+  for (auto& th : pool) th.join();
+  double full = 0, empty = 0;
+  int n = 0;
+  for (int t = 0; t < threads; ++t) {
+    full += t_full[t];
+    empty += t_empty[t];
+    n += reps[t];
+  }
+  const double per_full = full / n, per_attn = (full - empty) / n;
+  std::printf("{\"kind\":\"decode_bench\",\"threads\":%d,\"steps\":%d,\"ctx\":%zu,\"s_per_token_full\":%.6f,"
+              "\"s_per_token_attention\":%.6f,\"tokens_per_s_full\":%.4f,\"tokens_per_s_attention\":%.4f}\n",
+              threads, n, prefix + blen, per_full, per_attn, threads / per_full, threads / per_attn);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -535,6 +615,7 @@ int main(int argc, char** argv) {
     return mode_kv(std::stoull(argv[2]), std::stoi(argv[3]), static_cast<std::size_t>(std::stoul(argv[4])));
   if (mode == "toy") return mode_toy();
   if (mode == "forced" && argc >= 5) return mode_forced_bench(std::stoi(argv[2]), std::stoi(argv[3]), std::stoi(argv[4]));
+  if (mode == "decode" && argc >= 4) return mode_decode_bench(std::stoi(argv[2]), std::stod(argv[3]));
   std::fprintf(stderr, "bad arguments\n");
   return 1;
 }

@@ -58,7 +58,8 @@ constexpr int kBlkPages = 4;                                // pages per block (
 constexpr int kBlkCols = kBlkPages * kPageTokens;           // 64 S columns per block
 constexpr int kKSlots = 5, kVSlots = 6;                     // K / V rings, one block (4 pages) per slot
 constexpr int kSlotBytes = kBlkPages * kPageBytes;          // 4 page-head blocks as stored (16 KiB)
-constexpr int kMaxEntries = 64;                             // pages per work unit (split-KV chunk)
+constexpr int kMaxChunk = 64;                               // split-KV chunk target (pages)
+constexpr int kMaxEntries = 80;                             // pages per work unit (a tail chunk grows in place)
 constexpr int kMaxMem = 16;                                 // handles per work unit
 constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dims] bf16
 constexpr int kQBytes = 2 * kQHalf;
@@ -765,6 +766,7 @@ struct DecodePlanCache {
   // host plan
   std::vector<WorkItem> units;
   std::vector<int32_t> slot_ptr, slot_idx, slot_cnt, multi;  // multi: handles with > 1 slot
+  std::vector<int32_t> tail_item, tail_c0;  // per handle: item holding its private tail chunk (-1 none)
   int32_t n_slots = 0;
   mv_decode_plan_info info{};
   // device copies
@@ -777,8 +779,17 @@ struct DecodePlanCache {
   bool smem_set = false;
   int num_sms = 148;
   int* d_counter = nullptr;
+  // pinned double-buffered staging for in-place plan updates (no implicit stream sync)
+  WorkItem* h_stage[2] = {nullptr, nullptr};
+  size_t cap_stage = 0;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  int stage_k = 0;
   unsigned long long* d_trace = nullptr;
   ~DecodePlanCache() {
+    for (int k = 0; k < 2; ++k) {
+      if (h_stage[k]) cudaFreeHost(h_stage[k]);
+      if (stage_ev[k]) cudaEventDestroy(stage_ev[k]);
+    }
     cudaFree(d_trace);
     cudaFree(d_counter);
     cudaFree(d_units);
@@ -834,14 +845,15 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
     int64_t off;
     int32_t e0, e1;
     std::vector<int32_t> mem;
+    int32_t tail_of;  // handle whose private tail this segment is (-1: shared segment)
   };
   std::vector<Seg> segs;
   int64_t total_pages = 0;
-  auto add_seg = [&](int64_t off, int32_t e0, int32_t e1, std::vector<int32_t> mem, int64_t tokens) {
+  auto add_seg = [&](int64_t off, int32_t e0, int32_t e1, std::vector<int32_t> mem, int64_t tokens, int32_t tail_of) {
     if (e1 <= e0 || mem.empty()) return;
     unique_tokens += tokens;
     total_pages += e1 - e0;
-    segs.push_back({off, e0, e1, std::move(mem)});
+    segs.push_back({off, e0, e1, std::move(mem), tail_of});
   };
   std::unordered_map<uint64_t, bool> done;
   for (int b = 0; b < n; ++b) {
@@ -852,7 +864,7 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
       auto& mem = group_members[lg.group];
       if (mem.size() >= 2 && !done[lg.group]) {
         done[lg.group] = true;
-        add_seg(r->arena_off, prev_e, lg.entries, mem, lg.tokens - prev_t);
+        add_seg(r->arena_off, prev_e, lg.entries, mem, lg.tokens - prev_t, -1);
       }
       if (mem.size() >= 2) {
         prev_e = lg.entries;
@@ -860,15 +872,16 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
       }
     }
     // private remainder (single-holder lineage segments coalesce here)
-    add_seg(r->arena_off, prev_e, r->n_entries(), std::vector<int32_t>{b}, r->n_tokens() - prev_t);
+    add_seg(r->arena_off, prev_e, r->n_entries(), std::vector<int32_t>{b}, r->n_tokens() - prev_t, b);
   }
 
   // split-KV chunk size: <= 64 pages, small enough for >= ~6 waves of work over the SMs
   const int64_t target_units = (int64_t)num_sms * 6;
-  int chunk = kMaxEntries;
+  int chunk = kMaxChunk;
   while (chunk > 16 && total_pages * kv_heads / chunk < target_units) chunk /= 2;
 
   std::vector<WorkItem> items;
+  std::vector<int32_t> tags, tag_c0;  // per item: handle whose private tail it ends (-1), its first entry
   for (const Seg& s : segs) {
     const int32_t npg = s.e1 - s.e0;
     const int32_t nchunks = (npg + chunk - 1) / chunk;
@@ -897,20 +910,33 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
         }
         n_slots += w.n_mem;
         items.push_back(w);
+        tags.push_back(s.tail_of >= 0 && c == nchunks - 1 ? s.tail_of : -1);
+        tag_c0.push_back(c0);
       }
     }
   }
   // longest-first (then widest-first) for the dynamic queue: the tail is made of the smallest units
-  std::stable_sort(items.begin(), items.end(), [](const WorkItem& a, const WorkItem& b) {
+  std::vector<int32_t> order(items.size());
+  for (size_t k = 0; k < order.size(); ++k) order[k] = (int32_t)k;
+  std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+    const WorkItem &a = items[x], &b = items[y];
     return a.n_entries != b.n_entries ? a.n_entries > b.n_entries : a.n_mem > b.n_mem;
   });
+  pc.tail_item.assign(n, -1);
+  pc.tail_c0.assign(n, 0);
   pc.units.reserve(items.size() * kv_heads);
-  for (const WorkItem& w : items)
+  for (size_t k = 0; k < order.size(); ++k) {
+    const int32_t it = order[k];
+    if (tags[it] >= 0) {
+      pc.tail_item[tags[it]] = (int32_t)k;
+      pc.tail_c0[tags[it]] = tag_c0[it];
+    }
     for (int h = 0; h < kv_heads; ++h) {
-      WorkItem u = w;
+      WorkItem u = items[it];
       u.kvh = h;
       pc.units.push_back(u);
     }
+  }
 
   pc.slot_ptr.assign(n + 1, 0);
   pc.slot_cnt.assign(n, 0);
@@ -961,17 +987,54 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     pc.smem_set = true;
   }
   // plan signature: the handle list plus each table's entry count and lineage depth
-  std::vector<int64_t> sig(2 * (size_t)n);
+  std::vector<int64_t> sig(3 * (size_t)n);
   for (int b = 0; b < n; ++b) {
     HandleRec* r = st.find(hs[b]);
     if (!r) return fail(MV_ERR_DOUBLE_RELEASE, "handle " + std::to_string(hs[b]) + " is unknown or already released");
     if (r->n_tokens() == 0) return fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_decode: empty context");
-    sig[2 * b] = r->n_entries();
-    sig[2 * b + 1] = (int64_t)r->lineage.size();
+    sig[3 * b] = r->n_entries();
+    sig[3 * b + 1] = (int64_t)r->lineage.size();
+    sig[3 * b + 2] = r->arena_off;
   }
-  const bool same = pc.q_heads == q_heads && pc.handles.size() == (size_t)n &&
-                    std::equal(pc.handles.begin(), pc.handles.end(), hs) && pc.sig == sig;
+  const bool same_set = pc.q_heads == q_heads && pc.handles.size() == (size_t)n &&
+                        std::equal(pc.handles.begin(), pc.handles.end(), hs) && pc.sig.size() == sig.size();
+  bool same = same_set && pc.sig == sig;
   cudaStream_t stream = st.stream();
+  if (same_set && !same) {
+    // Decode appends grow only each branch's private tail: bump its tail chunk in place (one upload,
+    // no re-plan) while the chunk fits; anything else (new lineage, moved table) re-plans.
+    bool incr = true;
+    for (int b = 0; b < n && incr; ++b) {
+      if (sig[3 * b + 1] != pc.sig[3 * b + 1] || sig[3 * b + 2] != pc.sig[3 * b + 2] || sig[3 * b] < pc.sig[3 * b]) incr = false;
+      else if (sig[3 * b] != pc.sig[3 * b] && (pc.tail_item[b] < 0 || sig[3 * b] - pc.tail_c0[b] > kMaxEntries)) incr = false;
+    }
+    if (incr) {
+      for (int b = 0; b < n; ++b) {
+        if (sig[3 * b] == pc.sig[3 * b]) continue;
+        const int it = pc.tail_item[b];
+        for (int h = 0; h < cfg.kv_heads; ++h) pc.units[(size_t)it * cfg.kv_heads + h].n_entries = (int32_t)(sig[3 * b] - pc.tail_c0[b]);
+      }
+      // pinned double-buffered staging: an async copy that does not drain the stream
+      if (pc.cap_stage < pc.units.size()) {
+        for (int k = 0; k < 2; ++k) {
+          if (pc.h_stage[k]) cudaFreeHost(pc.h_stage[k]);
+          pc.h_stage[k] = nullptr;
+          MV_CUDA_TRY(cudaMallocHost(&pc.h_stage[k], sizeof(WorkItem) * pc.units.size()));
+          if (!pc.stage_ev[k]) MV_CUDA_TRY(cudaEventCreateWithFlags(&pc.stage_ev[k], cudaEventDisableTiming));
+        }
+        pc.cap_stage = pc.units.size();
+      }
+      const int k = pc.stage_k;
+      pc.stage_k ^= 1;
+      MV_CUDA_TRY(cudaEventSynchronize(pc.stage_ev[k]));  // the copy that last used this buffer
+      std::memcpy(pc.h_stage[k], pc.units.data(), sizeof(WorkItem) * pc.units.size());
+      MV_CUDA_TRY(cudaMemcpyAsync(pc.d_units, pc.h_stage[k], sizeof(WorkItem) * pc.units.size(),
+                                  cudaMemcpyHostToDevice, stream));
+      MV_CUDA_TRY(cudaEventRecord(pc.stage_ev[k], stream));
+      pc.sig = sig;
+      same = true;
+    }
+  }
   if (!same) {
     build_plan(st, pc, hs, n, cfg.kv_heads, gqa, pc.num_sms);
     pc.handles.assign(hs, hs + n);
@@ -1001,8 +1064,8 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
                                 cudaMemcpyHostToDevice, stream));
     MV_CUDA_TRY(cudaMemcpyAsync(pc.d_slot_cnt, pc.slot_cnt.data(), sizeof(int32_t) * pc.slot_cnt.size(),
                                 cudaMemcpyHostToDevice, stream));
-    // the host vectors must outlive the async copies: synchronise once per re-plan
-    MV_CUDA_TRY(cudaStreamSynchronize(stream));
+    // pageable sources: each copy is staged before its call returns (it drains the stream, which is
+    // acceptable for a full re-plan; in-place updates above use pinned staging)
   }
   const int R = rows_per_member(gqa);
   if (mv_status e = ensure_dev(pc.d_q_tile, pc.cap_q, (size_t)n * cfg.kv_heads * 2 * R * 64)) return e;

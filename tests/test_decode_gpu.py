@@ -159,3 +159,37 @@ def test_many_requests_persistent_mix(mv):
     err, st = run_case(mv, [(1024, 8, 200)] * 8 + [(333, 3, 77)] * 3, hq=40, hkv=8, num_pages=2048, seed=5)
     assert err < TOL, err
     assert st.plan_info()["work_items"] * 8 > 148
+
+
+def test_multi_step_decode_growing_tables(mv):
+    """Engine loop: 40 decode steps per branch (append then attend), crossing page boundaries, so
+    the cached decode plan is updated in place (tail chunks grow) and re-planned when a chunk fills;
+    every step is checked against the oracle."""
+    hq, hkv = 40, 8
+    st = mv.kv.PagedStore(num_pages=512, layers=1, kv_heads=hkv)
+    rows = {"k": [], "v": [], "pos": []}
+    r = Req(mv, st, rows, 11, 1000, 4, 1013, hkv=hkv)  # tails end 3 tokens before a page boundary
+    handles, ctx, qpos = list(r.handles), [list(c) for c in r.ctx], list(r.qpos)
+    n = len(handles)
+    for step in range(40):
+        knew = sym_bf16(9000 + step * 3, (n, hkv, 128))
+        vnew = sym_bf16(9001 + step * 3, (n, hkv, 128))
+        q = sym_bf16(9002 + step * 3, (n, hq, 128))
+        pos = torch.tensor(qpos, dtype=torch.int32)
+        st.append(handles, torch.full((n,), 12, dtype=torch.int32, device="cuda"), pos.cuda(), 0, knew.cuda(),
+                  vnew.cuda())
+        base = sum(x.shape[0] for x in rows["k"])
+        rows["k"].append(knew)
+        rows["v"].append(vnew)
+        rows["pos"].append(pos)
+        for i in range(n):
+            ctx[i].append(base + i)
+        out = mv.attention.decode(st, handles, q.cuda(), pos.cuda(), out_dtype=torch.float32)
+        if step % 7 == 0 or step == 39:
+            K = np.concatenate([bf16_to_f64(x) for x in rows["k"]])
+            V = np.concatenate([bf16_to_f64(x) for x in rows["v"]])
+            P = np.concatenate([x.numpy() for x in rows["pos"]])
+            ref = oracle.attn_decode(oracle.rope(bf16_to_f64(q), pos.numpy()), oracle.rope(K, P), V, ctx)
+            err = np.abs(out.float().cpu().numpy() - ref).max()
+            assert err < TOL, (step, err)
+        qpos = [p + 1 for p in qpos]
