@@ -121,6 +121,7 @@ struct DecodeParams {
   int out_f32;
   int kv_heads, q_heads, gqa, R;
   float scale_log2;
+  int pf_head, pf_tail;          // L2 prefetch: pages of a unit's head at staging; its tail once started
   unsigned long long* trace;    // optional timeline [cta][kTraceWords] (MV_DECODE_TRACE)
 };
 
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       for (int j = lane; j < n_ent; j += 32) {
         const PageRef ref = P.arena[eoff + j];
         se[j] = ref;
-        if (j < kPrefetch) {  // the unit's head now; its tail once the unit has started (below)
+        if (j < P.pf_head) {  // the unit's head now; its tail once the unit has started (below)
           const size_t pf = ((size_t)ref.page * P.kv_heads + kvh) * kPageTokens * kHeadDim;
           prefetch_l2(P.kplane + pf, kPageBytes);
           prefetch_l2(P.vplane + pf, kPageBytes);
@@ -419,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         // stream the rest of the previous unit into L2 (its page list is still staged)
         const WorkItem* sp = &s_item[buf ^ 1];
         const PageRef* pe = s_ent0 + (buf ^ 1) * kMaxEntries;
-        for (int j = kPrefetch + lane; j < sp->n_entries; j += 32) {
+        for (int j = P.pf_head + lane; P.pf_tail && j < sp->n_entries; j += 32) {
           const size_t pf = ((size_t)pe[j].page * P.kv_heads + sp->kvh) * kPageTokens * kHeadDim;
           prefetch_l2(P.kplane + pf, kPageBytes);
           prefetch_l2(P.vplane + pf, kPageBytes);
@@ -1095,6 +1096,12 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   P.gqa = gqa;
   P.R = R;
   P.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
+  {
+    const char* pfh = getenv("MV_DECODE_PF_HEAD");
+    const char* pft = getenv("MV_DECODE_PF_TAIL");
+    P.pf_head = pfh ? atoi(pfh) : 0;  // measured: L2 prefetching only adds DRAM traffic (tools/pf_sweep.sh)
+    P.pf_tail = pft ? atoi(pft) : 0;
+  }
   const int grid = std::min(P.n_units, pc.num_sms);
   P.trace = nullptr;
   const char* trace_path = getenv("MV_DECODE_TRACE");
