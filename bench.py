@@ -244,7 +244,10 @@ def run_ours(args):
         dist.barrier()
     clk = clocks.stop()
     ms = ev[0].elapsed_time(ev[1]) / args.steps
-    att_ms = float(np.mean([a.elapsed_time(b) for a, b in att]))
+    att_each = [a.elapsed_time(b) for a, b in att]
+    att_ms = float(np.mean(att_each))
+    if os.environ.get("MV_BENCH_DUMP"):
+        np.save(os.environ["MV_BENCH_DUMP"], np.array(att_each))
     if world > 1:
         t = torch.tensor([ms, att_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -36,6 +36,7 @@
 // Query rows: member m of a unit owns TMEM lanes [m*R, m*R + gqa), R = gqa rounded up to a
 // power of two >= 8, so every member's rows share the swizzle phase and a 1 KiB-aligned slot.
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <unordered_map>
@@ -811,7 +812,7 @@ static mv_status ensure_dev(T*& p, size_t& cap, size_t n) {
   if (n <= cap) return MV_OK;
   cudaFree(p);
   p = nullptr;
-  size_t c = std::max<size_t>(n, cap * 2);
+  size_t c = std::max<size_t>(2 * n, cap * 2);  // headroom: re-plans of growing tables rarely reallocate
   MV_CUDA_TRY(cudaMalloc(&p, sizeof(T) * c));
   cap = c;
   return MV_OK;
@@ -1009,6 +1010,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
       if (sig[3 * b + 1] != pc.sig[3 * b + 1] || sig[3 * b + 2] != pc.sig[3 * b + 2] || sig[3 * b] < pc.sig[3 * b]) incr = false;
       else if (sig[3 * b] != pc.sig[3 * b] && (pc.tail_item[b] < 0 || sig[3 * b] - pc.tail_c0[b] > kMaxEntries)) incr = false;
     }
+    if (getenv("MV_DECODE_LOG")) fprintf(stderr, "[mv decode] plan %s\n", incr ? "grow tail in place" : "rebuild");
     if (incr) {
       for (int b = 0; b < n; ++b) {
         if (sig[3 * b] == pc.sig[3 * b]) continue;
@@ -1037,7 +1039,11 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     }
   }
   if (!same) {
+    const auto t_plan = std::chrono::steady_clock::now();
     build_plan(st, pc, hs, n, cfg.kv_heads, gqa, pc.num_sms);
+    if (getenv("MV_DECODE_LOG"))
+      fprintf(stderr, "[mv decode] build_plan (%d handles): %.3f ms host\n", n,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_plan).count());
     pc.handles.assign(hs, hs + n);
     pc.sig = sig;
     pc.q_heads = q_heads;
@@ -1050,7 +1056,8 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
       MV_CUDA_TRY(cudaMemcpyAsync(pc.d_multi, pc.multi.data(), sizeof(int32_t) * pc.multi.size(),
                                   cudaMemcpyHostToDevice, stream));
     const size_t old_slots = pc.cap_slots;
-    if (mv_status e = ensure_dev(pc.d_part_ml, pc.cap_slots, std::max<size_t>(1, (size_t)pc.n_slots * q_heads)))
+    // 2x headroom: later re-plans split growing tails into more chunks (more partial slots)
+    if (mv_status e = ensure_dev(pc.d_part_ml, pc.cap_slots, std::max<size_t>(1, (size_t)pc.n_slots * q_heads * 2)))
       return e;
     if (pc.cap_slots != old_slots || !pc.d_part_o) {
       cudaFree(pc.d_part_o);

@@ -382,6 +382,11 @@ PagedStore::~PagedStore() {
   for (auto* p : k_planes_) cudaFree(p);
   for (auto* p : v_planes_) cudaFree(p);
   for (auto* p : dscratch_) cudaFree(p);
+  for (auto& sg : stage_)
+    for (int k = 0; k < 2; ++k) {
+      if (sg.buf[k]) cudaFreeHost(sg.buf[k]);
+      if (sg.ev[k]) cudaEventDestroy(sg.ev[k]);
+    }
   if (pinned_) cudaFreeHost(pinned_);
   destroy_plan(plan);
 }
@@ -495,10 +500,28 @@ void* PagedStore::device_scratch(size_t bytes, int slot) {
   return dscratch_[slot];
 }
 
+// Host -> device staging of small per-call arrays (page-table descriptors): copied into one of two
+// pinned buffers per slot (ping-pong, guarded by an event), so the async copy neither drains the
+// stream (as a pageable source would) nor races a copy still in flight.
 mv_status PagedStore::upload(const void* host, size_t bytes, void** dev_out, int slot) {
   void* d = device_scratch(bytes, slot);
   if (!d) return fail(MV_ERR_CUDA, "device scratch allocation failed");
-  if (bytes) MV_CUDA_TRY(cudaMemcpyAsync(d, host, bytes, cudaMemcpyHostToDevice, stream_));
+  if (bytes) {
+    if ((int)stage_.size() <= slot) stage_.resize(slot + 1);
+    Stage& sg = stage_[slot];
+    const int k = sg.next;
+    sg.next ^= 1;
+    if (sg.ev[k]) MV_CUDA_TRY(cudaEventSynchronize(sg.ev[k]));
+    else MV_CUDA_TRY(cudaEventCreateWithFlags(&sg.ev[k], cudaEventDisableTiming));
+    if (sg.bytes[k] < bytes) {
+      if (sg.buf[k]) cudaFreeHost(sg.buf[k]);
+      sg.bytes[k] = std::max<size_t>(bytes, 4096);
+      MV_CUDA_TRY(cudaMallocHost(&sg.buf[k], sg.bytes[k]));
+    }
+    std::memcpy(sg.buf[k], host, bytes);
+    MV_CUDA_TRY(cudaMemcpyAsync(d, sg.buf[k], bytes, cudaMemcpyHostToDevice, stream_));
+    MV_CUDA_TRY(cudaEventRecord(sg.ev[k], stream_));
+  }
   *dev_out = d;
   return MV_OK;
 }

@@ -109,6 +109,13 @@ class PagedStore {
   void* pinned_ = nullptr;
   size_t pinned_bytes_ = 0;
   std::vector<void*> dscratch_;
+  struct Stage {
+    void* buf[2] = {nullptr, nullptr};
+    size_t bytes[2] = {0, 0};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int next = 0;
+  };
+  std::vector<Stage> stage_;  // pinned ping-pong staging per upload slot
   std::vector<size_t> dscratch_bytes_;
 };
 
