@@ -57,6 +57,7 @@ struct Tc2Params {
   int out_f32;
   int n, hq, hkv, D, n_qp, stride;
   float scale_log2;
+  unsigned long long* trace;  // optional timeline (MV_PREFILL_TRACE): head 0, [qp][272]
 };
 
 __global__ void __launch_bounds__(kThreads2, 1)
@@ -80,6 +81,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
   const int kvh = h / (P.hq / P.hkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cnt = P.tcount[qp];
+  unsigned long long* tr = (P.trace && blockIdx.y == 0) ? P.trace + (size_t)qp * 272 : nullptr;
+  if (tr && threadIdx.x == 0) { tr[0] = globaltimer(); tr[1] = cnt; }
   const int32_t* lst = P.tlist + (size_t)qp * P.stride;
 
   if (threadIdx.x == 0) {
@@ -165,6 +168,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       for (int j = 0; j < cnt; ++j) {
         mbar_wait(&v_full[j % kVSt], (j / kVSt) & 1);
         mbar_wait(&p_full[0], j & 1);
+        if (tr && j < 32) tr[16 + j * 8 + 0] = globaltimer();
         tc::fence_after();
         pv(0, j);
         const bool more = j + 1 < cnt;
@@ -175,7 +179,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
         } else {
           tc::mma_commit(&o_fin[0]);
         }
+        if (tr && j < 32) tr[16 + j * 8 + 1] = globaltimer();
         mbar_wait(&p_full[1], j & 1);
+        if (tr && j < 32) tr[16 + j * 8 + 2] = globaltimer();
         tc::fence_after();
         pv(1, j);
         tc::mma_commit(&v_empty[j % kVSt]);
@@ -185,6 +191,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         } else {
           tc::mma_commit(&o_fin[1]);
         }
+        if (tr && j < 32) tr[16 + j * 8 + 3] = globaltimer();
       }
     }
   } else {
@@ -210,6 +217,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       const int j0 = (entry & 0xFFFFF) * kT;
       const int status = (entry >> (20 + 2 * x)) & 3;  // 0 skip, 1 full, 2 partial
       mbar_wait(&s_full[x], j & 1);
+      if (tr && quarter == 0 && lane == 0 && j < 32) tr[16 + j * 8 + 4 + 2 * x] = globaltimer();
       tc::fence_after();
       float v[kT];
 #pragma unroll
@@ -285,6 +293,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tc::tmem_wait_st();
       tc::fence_before();
       mbar_arrive(&p_full[x]);
+      if (tr && quarter == 0 && lane == 0 && j < 32) tr[16 + j * 8 + 5 + 2 * x] = globaltimer();
     }
     // epilogue
     if (cnt > 0) mbar_wait(&o_fin[x], 0);
@@ -345,6 +354,14 @@ mv_status prefill_tc2_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_
   T.n_qp = n_qp;
   T.stride = stride;
   T.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
+  T.trace = nullptr;
+  static unsigned long long* d_trace = nullptr;
+  const char* tp = getenv("MV_PREFILL_TRACE");
+  if (tp) {
+    if (!d_trace) MV_CUDA_TRY(cudaMalloc(&d_trace, sizeof(unsigned long long) * 272 * 1024));
+    MV_CUDA_TRY(cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long) * 272 * 1024, st));
+    T.trace = d_trace;
+  }
   static bool attr = false;
   if (!attr) {
     MV_CUDA_TRY(cudaFuncSetAttribute(prefill_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
@@ -352,6 +369,15 @@ mv_status prefill_tc2_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_
   }
   prefill_tc2_kernel<<<dim3(n_qp, q_heads), kThreads2, kSmem2, st>>>(mq, mk, mvv, T);
   MV_LAUNCH_CHECK();
+  if (tp && n_qp <= 1024) {
+    std::vector<unsigned long long> h((size_t)272 * n_qp);
+    MV_CUDA_TRY(cudaMemcpyAsync(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    MV_CUDA_TRY(cudaStreamSynchronize(st));
+    if (FILE* f = fopen(tp, "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   return MV_OK;
 }
 
