@@ -161,12 +161,13 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def build_workload(mv, torch, R, dev):
-    """R requests: root prefix, fork into 8 branches, 1023 private tokens each (positions shared start)."""
+def build_workload(mv, torch, R, dev, first_request=0):
+    """R requests: root prefix, fork into 8 branches, 1023 private tokens each (positions shared start).
+    Request r's data is seeded by its global id, so every rank holds distinct requests."""
     pages = R * (PREFIX // 16 + BRANCHES * (BRANCH_LEN // 16 + 4)) + 1024
     st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=HKV)
     gen = torch.Generator(device=dev)
-    gen.manual_seed(1234)
+    gen.manual_seed(1234 + first_request)
 
     def rnd(*shape):
         return (torch.rand(*shape, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
@@ -200,8 +201,11 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     import paper_2506_09991_b200 as mv
 
-    R = args.requests
-    st, handles, pos0, rnd = build_workload(mv, torch, R, dev)
+    from paper_2506_09991_b200.shard import shard_requests, max_over_ranks
+    # weak scaling: R requests per GPU, sharded by request (no collective in attention)
+    shard = shard_requests(args.requests * world, HKV, world, rank)
+    R = len(shard.requests)
+    st, handles, pos0, rnd = build_workload(mv, torch, R, dev, shard.requests[0])
     n = len(handles)
     steps_total = args.warmup + args.steps
     # per-step inputs (device resident for `value`)
@@ -248,10 +252,7 @@ def run_ours(args):
     att_ms = float(np.mean(att_each))
     if os.environ.get("MV_BENCH_DUMP"):
         np.save(os.environ["MV_BENCH_DUMP"], np.array(att_each))
-    if world > 1:
-        t = torch.tensor([ms, att_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, att_ms = t.tolist()
+    ms, att_ms = max_over_ranks([ms, att_ms], device=dev)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the region ----
     hq_ = [qs[j].cpu().pin_memory() for j in range(2)]
@@ -281,10 +282,7 @@ def run_ours(args):
     ee[1].record(stream)
     torch.cuda.synchronize()
     e2e_ms = ee[0].elapsed_time(ee[1]) / e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = t.item()
+    (e2e_ms,) = max_over_ranks([e2e_ms], device=dev)
     h2d = n * (HQ + 2 * HKV) * D * 2 + n * 4
     d2h = n * HQ * D * 2
 

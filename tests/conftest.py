@@ -12,6 +12,7 @@ if str(REPO) not in sys.path:
 GOLDEN = REPO / "tests" / "golden"
 
 
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); runs through the C-ABI library")
 

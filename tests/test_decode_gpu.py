@@ -193,3 +193,67 @@ def test_multi_step_decode_growing_tables(mv):
             err = np.abs(out.float().cpu().numpy() - ref).max()
             assert err < TOL, (step, err)
         qpos = [p + 1 for p in qpos]
+
+
+def test_reduce_merge_stress_then_decode(mv):
+    """BASELINE configs[4] in miniature: R rounds of {fork B branches; each branch appends a path;
+    zero-copy merge in ordinal order; append the Reduce tokens}, then decode over the merged KV
+    (engine.cpp:679-725 spawn, :767-802 merge).  Checks 0 bytes copied and no page allocated by
+    fork / merge, refcount conservation, and decode parity against the oracle."""
+    hq, hkv, B, R, path, red = 40, 8, 24, 4, 17, 5
+    st = mv.kv.PagedStore(num_pages=2048, layers=1, kv_heads=hkv)
+    rows = {"k": [], "v": [], "pos": []}
+    seed = [100]
+
+    def add(h, n, pos0):
+        seed[0] += 2
+        k = sym_bf16(seed[0], (n, hkv, 128))
+        v = sym_bf16(seed[0] + 1, (n, hkv, 128))
+        pos = torch.arange(pos0, pos0 + n, dtype=torch.int32)
+        st.append_many(h, torch.full((n,), 11, dtype=torch.int32, device="cuda"), pos.cuda(), 0, k.cuda(), v.cuda())
+        base = sum(x.shape[0] for x in rows["k"])
+        rows["k"].append(k)
+        rows["v"].append(v)
+        rows["pos"].append(pos)
+        return list(range(base, base + n))
+
+    cur = st.create()
+    ctx = add(cur, 250, 0)
+    L = 250
+    for _ in range(R):
+        kids = st.fork(cur, B)
+        s0 = st.stats()
+        assert s0.bytes_copied_on_last_op == 0
+        kid_ctx = [add(k, path, L) for k in kids]  # sibling paths share their start position
+        free_before = st.stats().free_pages
+        m = st.merge(cur, kids)
+        s1 = st.stats()
+        assert s1.bytes_copied_on_last_op == 0 and s1.free_pages == free_before  # merge moves no KV, allocates no page
+        ctx = ctx + [r for kc in kid_ctx for r in kc]
+        for h in [cur] + kids:
+            st.release(h)
+        L += path  # Reduce starts at max path end + 1 (SPEC.md:195)
+        ctx = ctx + add(m, red, L)
+        L += red
+        cur = m
+        assert st.length(cur) == len(ctx)
+    assert st.resolve_slots(cur) is not None
+    for step in range(3):
+        knew, vnew, q = sym_bf16(7000 + step, (1, hkv, 128)), sym_bf16(7100 + step, (1, hkv, 128)), sym_bf16(7200 + step, (1, hq, 128))
+        pos = torch.tensor([L], dtype=torch.int32)
+        st.append([cur], torch.tensor([13], dtype=torch.int32, device="cuda"), pos.cuda(), 0, knew.cuda(), vnew.cuda())
+        base = sum(x.shape[0] for x in rows["k"])
+        rows["k"].append(knew)
+        rows["v"].append(vnew)
+        rows["pos"].append(pos)
+        ctx = ctx + [base]
+        out = mv.attention.decode(st, [cur], q.cuda(), pos.cuda(), out_dtype=torch.float32)
+        K = np.concatenate([bf16_to_f64(x) for x in rows["k"]])
+        V = np.concatenate([bf16_to_f64(x) for x in rows["v"]])
+        P = np.concatenate([x.numpy() for x in rows["pos"]])
+        ref = oracle.attn_decode(oracle.rope(bf16_to_f64(q), pos.numpy()), oracle.rope(K, P), V, [ctx])
+        assert np.abs(out.float().cpu().numpy() - ref).max() < TOL
+        L += 1
+    st.release(cur)
+    s = st.stats()
+    assert s.live_handles == 0 and s.total_refcount == 0 and s.free_pages == 2048
