@@ -20,6 +20,7 @@
 // so QK_X(j+1) (which overwrites S/P_X) cannot overtake PV_X(j) (which reads P_X), and the
 // commit after QK_X(j+1) also certifies PV_X(j) -> the softmax may rescale O_X after s_full.
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <vector>
 
@@ -43,7 +44,7 @@ constexpr int kOffQB = kOffQA + kTile2;
 constexpr int kOffK2 = kOffQB + kTile2;
 constexpr int kOffV2 = kOffK2 + kKSt * kTile2;
 constexpr int kOffBar2 = kOffV2 + kVSt * kTile2;
-constexpr int kSmem2 = kOffBar2 + 256 + 1024;
+constexpr int kSmem2 = kOffBar2 + 512 + 1024;
 constexpr uint32_t kIdQK = tc::idesc_bf16(128, 128, 0, 0);
 constexpr uint32_t kIdPV = tc::idesc_bf16(128, 128, 0, 1);
 constexpr int kMaxD2 = 8;
@@ -57,36 +58,42 @@ struct Tc2Params {
   int out_f32;
   int n, hq, hkv, D, n_qp, stride;
   float scale_log2;
-  unsigned long long* trace;  // optional timeline (MV_PREFILL_TRACE): head 0, [qp][272]
+  int n_items;          // (q-tile pair, q head) work items, heaviest pairs first
+  int* counters;        // [0] work queue, [1] finished CTAs (the last one re-arms the queue)
 };
 
+struct __align__(16) PfItem {
+  int qp, h, cnt, valid;
+};
+
+// Persistent: one CTA per SM pulls (q-tile pair, q head) items from a queue and keeps its TMA /
+// tensor-core / softmax pipeline running across items (K/V rings, S/P and mbarrier phases
+// continue; the next item's Q tile loads while the previous item finishes).
 __global__ void __launch_bounds__(kThreads2, 1)
     prefill_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, Tc2Params P) {
   extern __shared__ uint8_t smem_raw2[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw2) + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar2);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = q_full + 1;
+  uint64_t* q_full = bars;                 // Q tiles of the current item landed (tx)
+  uint64_t* q_empty = q_full + 1;          // MMA commit: the item's last Q.K^T done -> next Q may land
+  uint64_t* k_full = q_empty + 1;
   uint64_t* k_empty = k_full + kKSt;
   uint64_t* v_full = k_empty + kKSt;
   uint64_t* v_empty = v_full + kVSt;
-  uint64_t* s_full = v_empty + kVSt;  // [2]: tile A, B
-  uint64_t* p_full = s_full + 2;      // [2]
-  uint64_t* o_fin = p_full + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_fin + 2);
+  uint64_t* s_full = v_empty + kVSt;       // [2]: tile A, B
+  uint64_t* p_full = s_full + 2;           // [2]
+  uint64_t* o_fin = p_full + 2;            // [2] MMA commit: O_X of the item final
+  uint64_t* o_empty = o_fin + 2;           // [2] softmax WG X read O_X (epilogue)
+  uint64_t* item_full = o_empty + 2;       // [2] scheduler -> all roles
+  uint64_t* slot_empty = item_full + 2;    // [2] V lane + MMA + 8 softmax warps -> scheduler
+  PfItem* s_item = reinterpret_cast<PfItem*>(slot_empty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_item + 2);
 
-  const int qp = P.n_qp - 1 - blockIdx.x;  // heaviest pairs first
-  const int h = blockIdx.y;
-  const int kvh = h / (P.hq / P.hkv);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cnt = P.tcount[qp];
-  unsigned long long* tr = (P.trace && blockIdx.y == 0) ? P.trace + (size_t)qp * 272 : nullptr;
-  if (tr && threadIdx.x == 0) { tr[0] = globaltimer(); tr[1] = cnt; }
-  const int32_t* lst = P.tlist + (size_t)qp * P.stride;
-
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int s = 0; s < kKSt; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&k_empty[s], 1);
@@ -99,6 +106,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
       mbar_init(&s_full[x], 1);
       mbar_init(&p_full[x], 128);
       mbar_init(&o_fin[x], 1);
+      mbar_init(&o_empty[x], 128);
+      mbar_init(&item_full[x], 1);
+      mbar_init(&slot_empty[x], 10);
     }
     fence_mbar_init();
   }
@@ -106,40 +116,73 @@ __global__ void __launch_bounds__(kThreads2, 1)
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // one CTA per SM allocates all 512 columns, so the base is lane 0 / column 0
+  constexpr uint32_t tmem = 0;
+  if (*tmem_slot != tmem) __trap();
 
   if (warp == 0) {
-    if (lane < 2) {
-      const bool is_k = lane == 0;
-      const CUtensorMap* map = is_k ? &map_k : &map_v;
-      const int nst = is_k ? kKSt : kVSt;
-      uint64_t* full = is_k ? k_full : v_full;
-      uint64_t* empty = is_k ? k_empty : v_empty;
-      uint8_t* ring = smem + (is_k ? kOffK2 : kOffV2);
-      tc::tma_prefetch_desc(map);
-      if (is_k) {
-        tc::tma_prefetch_desc(&map_q);
+    if (lane == 0) {
+      // ---------------- scheduler + Q / K loader ----------------
+      tc::tma_prefetch_desc(&map_q);
+      tc::tma_prefetch_desc(&map_k);
+      int gk = 0;
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        if (i >= 2) mbar_wait(&slot_empty[buf], ((i >> 1) - 1) & 1);
+        const int w = atomicAdd(&P.counters[0], 1);
+        PfItem it;
+        it.valid = w < P.n_items;
+        it.qp = it.valid ? P.n_qp - 1 - w / P.hq : 0;
+        it.h = it.valid ? w % P.hq : 0;
+        it.cnt = it.valid ? P.tcount[it.qp] : 0;
+        s_item[buf] = it;
+        mbar_arrive(&item_full[buf]);
+        if (!it.valid) break;
+        if (i >= 1) mbar_wait(q_empty, (i - 1) & 1);
         mbar_arrive_expect_tx(q_full, 2 * kTile2);
-        tc::tma_load_3d(smem + kOffQA, &map_q, 0, h, qp * 256, q_full);
-        tc::tma_load_3d(smem + kOffQA + kHalf2, &map_q, 64, h, qp * 256, q_full);
-        tc::tma_load_3d(smem + kOffQB, &map_q, 0, h, qp * 256 + kT, q_full);
-        tc::tma_load_3d(smem + kOffQB + kHalf2, &map_q, 64, h, qp * 256 + kT, q_full);
+        tc::tma_load_3d(smem + kOffQA, &map_q, 0, it.h, it.qp * 256, q_full);
+        tc::tma_load_3d(smem + kOffQA + kHalf2, &map_q, 64, it.h, it.qp * 256, q_full);
+        tc::tma_load_3d(smem + kOffQB, &map_q, 0, it.h, it.qp * 256 + kT, q_full);
+        tc::tma_load_3d(smem + kOffQB + kHalf2, &map_q, 64, it.h, it.qp * 256 + kT, q_full);
+        const int kvh = it.h / (P.hq / P.hkv);
+        const int32_t* lst = P.tlist + (size_t)it.qp * P.stride;
+        for (int j = 0; j < it.cnt; ++j, ++gk) {
+          const int s = gk % kKSt;
+          if (gk >= kKSt) mbar_wait(&k_empty[s], ((gk / kKSt) - 1) & 1);
+          const int kt = lst[j] & 0xFFFFF;
+          mbar_arrive_expect_tx(&k_full[s], kTile2);
+          tc::tma_load_3d(smem + kOffK2 + s * kTile2, &map_k, 0, kvh, kt * kT, &k_full[s]);
+          tc::tma_load_3d(smem + kOffK2 + s * kTile2 + kHalf2, &map_k, 64, kvh, kt * kT, &k_full[s]);
+        }
       }
-      for (int it = 0; it < cnt; ++it) {
-        const int s = it % nst;
-        if (it >= nst) mbar_wait(&empty[s], ((it / nst) - 1) & 1);
-        const int kt = lst[it] & 0xFFFFF;
-        mbar_arrive_expect_tx(&full[s], kTile2);
-        tc::tma_load_3d(ring + s * kTile2, map, 0, kvh, kt * kT, &full[s]);
-        tc::tma_load_3d(ring + s * kTile2 + kHalf2, map, 64, kvh, kt * kT, &full[s]);
+    } else if (lane == 1) {
+      // ---------------- V loader ----------------
+      tc::tma_prefetch_desc(&map_v);
+      int gv = 0;
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        mbar_wait(&item_full[buf], (i >> 1) & 1);
+        const PfItem it = s_item[buf];
+        mbar_arrive(&slot_empty[buf]);
+        if (!it.valid) break;
+        const int kvh = it.h / (P.hq / P.hkv);
+        const int32_t* lst = P.tlist + (size_t)it.qp * P.stride;
+        for (int j = 0; j < it.cnt; ++j, ++gv) {
+          const int s = gv % kVSt;
+          if (gv >= kVSt) mbar_wait(&v_empty[s], ((gv / kVSt) - 1) & 1);
+          const int kt = lst[j] & 0xFFFFF;
+          mbar_arrive_expect_tx(&v_full[s], kTile2);
+          tc::tma_load_3d(smem + kOffV2 + s * kTile2, &map_v, 0, kvh, kt * kT, &v_full[s]);
+          tc::tma_load_3d(smem + kOffV2 + s * kTile2 + kHalf2, &map_v, 64, kvh, kt * kT, &v_full[s]);
+        }
       }
     }
   } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
     if (lane == 0) {
       const uint32_t qa = smem_u32(smem + kOffQA), qb = smem_u32(smem + kOffQB);
-      auto qk = [&](int x, int j) {  // S_x = Q_x . K(j)^T
-        const int s = j % kKSt;
-        const uint32_t kb = smem_u32(smem + kOffK2 + s * kTile2);
+      auto qk = [&](int x, int g) {  // S_x = Q_x . K(g)^T
+        const uint32_t kb = smem_u32(smem + kOffK2 + (g % kKSt) * kTile2);
         const uint32_t qbase = x ? qb : qa;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
@@ -149,49 +192,61 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
         tc::mma_commit(&s_full[x]);
       };
-      auto pv = [&](int x, int j) {  // O_x += P_x(tmem) . V(j)
-        const int s = j % kVSt;
-        const uint32_t vb = smem_u32(smem + kOffV2 + s * kTile2);
+      auto pv = [&](int x, int g, bool first) {  // O_x += P_x(tmem) . V(g)
+        const uint32_t vb = smem_u32(smem + kOffV2 + (g % kVSt) * kTile2);
 #pragma unroll
         for (int k = 0; k < 8; ++k)
           tc::mma_ts(tmem + 256 + x * 128, tmem + x * 128 + k * 8, tc::sw128_desc(vb + k * 2048, kHalf2, 1024), kIdPV,
-                     (j > 0 || k > 0) ? 1u : 0u);
+                     (!first || k > 0) ? 1u : 0u);
       };
-      mbar_wait(q_full, 0);
-      if (cnt > 0) {
-        mbar_wait(&k_full[0], 0);
-        tc::fence_after();
-        qk(0, 0);
-        qk(1, 0);
-        tc::mma_commit(&k_empty[0]);
-      }
-      for (int j = 0; j < cnt; ++j) {
-        mbar_wait(&v_full[j % kVSt], (j / kVSt) & 1);
-        mbar_wait(&p_full[0], j & 1);
-        if (tr && j < 32) tr[16 + j * 8 + 0] = globaltimer();
-        tc::fence_after();
-        pv(0, j);
-        const bool more = j + 1 < cnt;
-        if (more) {
-          mbar_wait(&k_full[(j + 1) % kKSt], ((j + 1) / kKSt) & 1);
+      int g = 0;
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        mbar_wait(&item_full[buf], (i >> 1) & 1);
+        const PfItem it = s_item[buf];
+        mbar_arrive(&slot_empty[buf]);
+        if (!it.valid) break;
+        mbar_wait(q_full, i & 1);
+        const int cnt = it.cnt;
+        if (cnt > 0) {
+          mbar_wait(&k_full[g % kKSt], (g / kKSt) & 1);
           tc::fence_after();
-          qk(0, j + 1);
+          qk(0, g);
+          qk(1, g);
+          tc::mma_commit(&k_empty[g % kKSt]);
+          if (cnt == 1) tc::mma_commit(q_empty);
         } else {
+          tc::mma_commit(q_empty);
           tc::mma_commit(&o_fin[0]);
-        }
-        if (tr && j < 32) tr[16 + j * 8 + 1] = globaltimer();
-        mbar_wait(&p_full[1], j & 1);
-        if (tr && j < 32) tr[16 + j * 8 + 2] = globaltimer();
-        tc::fence_after();
-        pv(1, j);
-        tc::mma_commit(&v_empty[j % kVSt]);
-        if (more) {
-          qk(1, j + 1);
-          tc::mma_commit(&k_empty[(j + 1) % kKSt]);
-        } else {
           tc::mma_commit(&o_fin[1]);
         }
-        if (tr && j < 32) tr[16 + j * 8 + 3] = globaltimer();
+        for (int j = 0; j < cnt; ++j, ++g) {
+          const bool more = j + 1 < cnt;
+          mbar_wait(&v_full[g % kVSt], (g / kVSt) & 1);
+          mbar_wait(&p_full[0], g & 1);
+          if (j == 0 && i >= 1) mbar_wait(&o_empty[0], (i - 1) & 1);  // epilogue drained O_A
+          tc::fence_after();
+          pv(0, g, j == 0);
+          if (more) {
+            mbar_wait(&k_full[(g + 1) % kKSt], ((g + 1) / kKSt) & 1);
+            tc::fence_after();
+            qk(0, g + 1);
+          } else {
+            tc::mma_commit(&o_fin[0]);
+          }
+          mbar_wait(&p_full[1], g & 1);
+          if (j == 0 && i >= 1) mbar_wait(&o_empty[1], (i - 1) & 1);
+          tc::fence_after();
+          pv(1, g, j == 0);
+          tc::mma_commit(&v_empty[g % kVSt]);
+          if (more) {
+            qk(1, g + 1);
+            tc::mma_commit(&k_empty[(g + 1) % kKSt]);
+            if (j + 2 == cnt) tc::mma_commit(q_empty);  // the item's last Q.K^T
+          } else {
+            tc::mma_commit(&o_fin[1]);
+          }
+        }
       }
     }
   } else {
@@ -199,128 +254,144 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int x = (warp - 2) >> 2;            // tile
     const int quarter = warp & 3;             // TMEM lane quarter this warp may access
     const int r = quarter * 32 + lane;        // row within the tile
-    const int i = qp * 256 + x * kT + r;      // sequence row
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const uint32_t s_col = x * 128, o_col = 256 + x * 128;
-    int elo[kMaxD2], ehi[kMaxD2];
+    int gs = 0;
+    for (int it_i = 0;; ++it_i) {
+      const int buf = it_i & 1;
+      mbar_wait(&item_full[buf], (it_i >> 1) & 1);
+      const PfItem it = s_item[buf];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slot_empty[buf]);
+      if (!it.valid) break;
+      const int qp = it.qp, h = it.h, cnt = it.cnt;
+      const int32_t* lst = P.tlist + (size_t)qp * P.stride;
+      const int i = qp * 256 + x * kT + r;  // sequence row
+      int elo[kMaxD2], ehi[kMaxD2];
 #pragma unroll
-    for (int q = 0; q < kMaxD2; ++q) {
-      elo[q] = ehi[q] = 0;
-      if (q < P.D && i < P.n) {
-        elo[q] = P.excl[((size_t)i * P.D + q) * 2];
-        ehi[q] = P.excl[((size_t)i * P.D + q) * 2 + 1];
+      for (int q = 0; q < kMaxD2; ++q) {
+        elo[q] = ehi[q] = 0;
+        if (q < P.D && i < P.n) {
+          elo[q] = P.excl[((size_t)i * P.D + q) * 2];
+          ehi[q] = P.excl[((size_t)i * P.D + q) * 2 + 1];
+        }
       }
-    }
-    float m_ref = -INFINITY, l = 0.f;
-    for (int j = 0; j < cnt; ++j) {
-      const int entry = lst[j];
-      const int j0 = (entry & 0xFFFFF) * kT;
-      const int status = (entry >> (20 + 2 * x)) & 3;  // 0 skip, 1 full, 2 partial
-      mbar_wait(&s_full[x], j & 1);
-      if (tr && quarter == 0 && lane == 0 && j < 32) tr[16 + j * 8 + 4 + 2 * x] = globaltimer();
+        float m_ref = -INFINITY, l = 0.f;
+        for (int j = 0; j < cnt; ++j) {
+          const int entry = lst[j];
+          const int j0 = (entry & 0xFFFFF) * kT;
+          const int status = (entry >> (20 + 2 * x)) & 3;  // 0 skip, 1 full, 2 partial
+          mbar_wait(&s_full[x], gs & 1);
+          ++gs;
+          tc::fence_after();
+          float v[kT];
+    #pragma unroll
+          for (int c = 0; c < 4; ++c) tc::tmem_ld32(lane_base + s_col + c * 32, v + c * 32);
+          tc::tmem_wait_ld();
+          float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+          if (status != 1) {
+            uint32_t vm[4];
+            const int lim = status == 0 ? -1 : min(i, P.n - 1) - j0;  // last visible column
+    #pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              const int lo = w * 32;
+              vm[w] = lim < lo ? 0u : (lim >= lo + 31 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (31 - (lim - lo))));
+            }
+    #pragma unroll
+            for (int q = 0; q < kMaxD2; ++q) {
+              const int a = max(elo[q] - j0, 0), e = min(ehi[q] - j0, kT);
+    #pragma unroll
+              for (int w = 0; w < 4; ++w) {
+                const int lo = max(a - w * 32, 0), hi = min(e - w * 32, 32);
+                if (hi > lo) vm[w] &= ~((hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << lo);
+              }
+            }
+    #pragma unroll
+            for (int c = 0; c < kT; c += 4) {
+              const uint32_t m = vm[c >> 5] >> (c & 31);
+              v[c] = (m & 1u) ? v[c] : -INFINITY;
+              v[c + 1] = (m & 2u) ? v[c + 1] : -INFINITY;
+              v[c + 2] = (m & 4u) ? v[c + 2] : -INFINITY;
+              v[c + 3] = (m & 8u) ? v[c + 3] : -INFINITY;
+              mx0 = fmaxf(mx0, v[c]); mx1 = fmaxf(mx1, v[c + 1]); mx2 = fmaxf(mx2, v[c + 2]); mx3 = fmaxf(mx3, v[c + 3]);
+            }
+          } else {
+    #pragma unroll
+            for (int c = 0; c < kT; c += 4) {
+              mx0 = fmaxf(mx0, v[c]); mx1 = fmaxf(mx1, v[c + 1]); mx2 = fmaxf(mx2, v[c + 2]); mx3 = fmaxf(mx3, v[c + 3]);
+            }
+          }
+          // raw-score max; scaled into the log2 domain once (scale > 0 preserves order)
+          const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * P.scale_log2;
+          const bool need = mx > m_ref + kLazy2;
+          if (__any_sync(0xffffffffu, need)) {
+            const float nref = need ? fmaxf(m_ref, mx) : m_ref;
+            const float alpha = need ? fast_exp2(m_ref - nref) : 1.f;
+            if (j >= 1) {  // s_full(j) certified PV_x(j-1): O_x is final for tiles < j
+    #pragma unroll 1
+              for (int c = 0; c < 4; ++c) {
+                float o[32];
+                tc::tmem_ld32(lane_base + o_col + c * 32, o);
+                tc::tmem_wait_ld();
+    #pragma unroll
+                for (int e = 0; e < 32; ++e) o[e] *= alpha;
+                tc::tmem_st32(lane_base + o_col + c * 32, o);
+              }
+            }
+            l *= alpha;
+            m_ref = nref;
+          }
+          const float mu = m_ref == -INFINITY ? 0.f : m_ref;
+          float l0 = 0.f, l1 = 0.f;
+          uint32_t pk[64];
+    #pragma unroll
+          for (int c = 0; c < 64; ++c) {
+            const float p0 = fast_exp2(fmaf(v[2 * c], P.scale_log2, -mu));
+            const float p1 = fast_exp2(fmaf(v[2 * c + 1], P.scale_log2, -mu));
+            l0 += p0;
+            l1 += p1;
+            pk[c] = pack_bf16(p0, p1);
+          }
+          l += l0 + l1;
+          tc::tmem_st32u(lane_base + s_col, pk);
+          tc::tmem_st32u(lane_base + s_col + 32, pk + 32);
+          tc::tmem_wait_st();
+          tc::fence_before();
+          mbar_arrive(&p_full[x]);
+        }
+      // epilogue: O_x / l, then hand O_x back to the MMA issuer
+      if (cnt > 0) mbar_wait(&o_fin[x], it_i & 1);
       tc::fence_after();
-      float v[kT];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tmem_ld32(lane_base + s_col + c * 32, v + c * 32);
-      tc::tmem_wait_ld();
-      float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
-      if (status != 1) {
-        uint32_t vm[4];
-        const int lim = status == 0 ? -1 : min(i, P.n - 1) - j0;  // last visible column
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int lo = w * 32;
-          vm[w] = lim < lo ? 0u : (lim >= lo + 31 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (31 - (lim - lo))));
-        }
-#pragma unroll
-        for (int q = 0; q < kMaxD2; ++q) {
-          const int a = max(elo[q] - j0, 0), e = min(ehi[q] - j0, kT);
-#pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            const int lo = max(a - w * 32, 0), hi = min(e - w * 32, 32);
-            if (hi > lo) vm[w] &= ~((hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << lo);
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < kT; c += 4) {
-          const uint32_t m = vm[c >> 5] >> (c & 31);
-          v[c] = (m & 1u) ? v[c] : -INFINITY;
-          v[c + 1] = (m & 2u) ? v[c + 1] : -INFINITY;
-          v[c + 2] = (m & 4u) ? v[c + 2] : -INFINITY;
-          v[c + 3] = (m & 8u) ? v[c + 3] : -INFINITY;
-          mx0 = fmaxf(mx0, v[c]); mx1 = fmaxf(mx1, v[c + 1]); mx2 = fmaxf(mx2, v[c + 2]); mx3 = fmaxf(mx3, v[c + 3]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < kT; c += 4) {
-          mx0 = fmaxf(mx0, v[c]); mx1 = fmaxf(mx1, v[c + 1]); mx2 = fmaxf(mx2, v[c + 2]); mx3 = fmaxf(mx3, v[c + 3]);
-        }
-      }
-      // raw-score max; scaled into the log2 domain once (scale > 0 preserves order)
-      const float mx = fmaxf(fmaxf(mx0, mx1), fmaxf(mx2, mx3)) * P.scale_log2;
-      const bool need = mx > m_ref + kLazy2;
-      if (__any_sync(0xffffffffu, need)) {
-        const float nref = need ? fmaxf(m_ref, mx) : m_ref;
-        const float alpha = need ? fast_exp2(m_ref - nref) : 1.f;
-        if (j >= 1) {  // s_full(j) certified PV_x(j-1): O_x is final for tiles < j
+      const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            float o[32];
-            tc::tmem_ld32(lane_base + o_col + c * 32, o);
-            tc::tmem_wait_ld();
+      for (int c = 0; c < 4; ++c) {
+        float o[32];
+        tc::tmem_ld32(lane_base + o_col + c * 32, o);
+        tc::tmem_wait_ld();
+        if (i < P.n) {
+          if (P.out_f32) {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + h) * kHeadDim + c * 32);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] *= alpha;
-            tc::tmem_st32(lane_base + o_col + c * 32, o);
+            for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + ((size_t)i * P.hq + h) * kHeadDim + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
+                                  pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
           }
         }
-        l *= alpha;
-        m_ref = nref;
       }
-      const float mu = m_ref == -INFINITY ? 0.f : m_ref;
-      float l0 = 0.f, l1 = 0.f;
-      uint32_t pk[64];
-#pragma unroll
-      for (int c = 0; c < 64; ++c) {
-        const float p0 = fast_exp2(fmaf(v[2 * c], P.scale_log2, -mu));
-        const float p1 = fast_exp2(fmaf(v[2 * c + 1], P.scale_log2, -mu));
-        l0 += p0;
-        l1 += p1;
-        pk[c] = pack_bf16(p0, p1);
-      }
-      l += l0 + l1;
-      tc::tmem_st32u(lane_base + s_col, pk);
-      tc::tmem_st32u(lane_base + s_col + 32, pk + 32);
-      tc::tmem_wait_st();
       tc::fence_before();
-      mbar_arrive(&p_full[x]);
-      if (tr && quarter == 0 && lane == 0 && j < 32) tr[16 + j * 8 + 5 + 2 * x] = globaltimer();
+      mbar_arrive(&o_empty[x]);
     }
-    // epilogue
-    if (cnt > 0) mbar_wait(&o_fin[x], 0);
-    tc::fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
-      float o[32];
-      tc::tmem_ld32(lane_base + o_col + c * 32, o);
-      tc::tmem_wait_ld();
-      if (i < P.n) {
-        if (P.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + h) * kHeadDim + c * 32);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + ((size_t)i * P.hq + h) * kHeadDim + c * 32);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
-                                pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
-        }
-      }
-    }
-    tc::fence_before();
   }
+  tc::fence_before();
   __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&P.counters[1], 1) == (int)gridDim.x - 1) {
+    P.counters[0] = 0;  // every CTA has stopped claiming: re-arm the queue for the next launch
+    P.counters[1] = 0;
+  }
   if (warp == 1) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, 512);
@@ -354,30 +425,24 @@ mv_status prefill_tc2_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_
   T.n_qp = n_qp;
   T.stride = stride;
   T.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
-  T.trace = nullptr;
-  static unsigned long long* d_trace = nullptr;
-  const char* tp = getenv("MV_PREFILL_TRACE");
-  if (tp) {
-    if (!d_trace) MV_CUDA_TRY(cudaMalloc(&d_trace, sizeof(unsigned long long) * 272 * 1024));
-    MV_CUDA_TRY(cudaMemsetAsync(d_trace, 0, sizeof(unsigned long long) * 272 * 1024, st));
-    T.trace = d_trace;
+  T.n_items = n_qp * q_heads;
+  static int* d_counters = nullptr;
+  static int num_sms = 0;
+  if (!d_counters) {
+    MV_CUDA_TRY(cudaMalloc(&d_counters, 2 * sizeof(int)));
+    MV_CUDA_TRY(cudaMemsetAsync(d_counters, 0, 2 * sizeof(int), st));
+    int dev = 0;
+    MV_CUDA_TRY(cudaGetDevice(&dev));
+    MV_CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  T.counters = d_counters;
   static bool attr = false;
   if (!attr) {
     MV_CUDA_TRY(cudaFuncSetAttribute(prefill_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
     attr = true;
   }
-  prefill_tc2_kernel<<<dim3(n_qp, q_heads), kThreads2, kSmem2, st>>>(mq, mk, mvv, T);
+  prefill_tc2_kernel<<<std::min(T.n_items, num_sms), kThreads2, kSmem2, st>>>(mq, mk, mvv, T);
   MV_LAUNCH_CHECK();
-  if (tp && n_qp <= 1024) {
-    std::vector<unsigned long long> h((size_t)272 * n_qp);
-    MV_CUDA_TRY(cudaMemcpyAsync(h.data(), d_trace, h.size() * 8, cudaMemcpyDeviceToHost, st));
-    MV_CUDA_TRY(cudaStreamSynchronize(st));
-    if (FILE* f = fopen(tp, "wb")) {
-      fwrite(h.data(), 8, h.size(), f);
-      fclose(f);
-    }
-  }
   return MV_OK;
 }
 
