@@ -62,6 +62,23 @@ struct Tc2Params {
   int* counters;        // [0] work queue, [1] finished CTAs (the last one re-arms the queue)
 };
 
+// MMA issue with compile-time TMEM operands (tile X: S/P at column 128X, O at 256 + 128X) and
+// descriptors advanced by constants, so the issuing thread does little besides UTCHMMA
+template <int X>
+__device__ __forceinline__ void pf_qk(uint64_t qd, uint64_t kd) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint64_t off = (uint64_t)(((k >> 2) * kHalf2 + (k & 3) * 32) >> 4);
+    tc::mma_ss(X * 128, qd + off, kd + off, kIdQK, k > 0 ? 1u : 0u);
+  }
+}
+template <int X>
+__device__ __forceinline__ void pf_pv(uint64_t vd, bool first) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    tc::mma_ts(256 + X * 128, X * 128 + k * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV, (!first || k > 0) ? 1u : 0u);
+}
+
 struct __align__(16) PfItem {
   int qp, h, cnt, valid;
 };
@@ -180,24 +197,20 @@ __global__ void __launch_bounds__(kThreads2, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      const uint32_t qa = smem_u32(smem + kOffQA), qb = smem_u32(smem + kOffQB);
+      const uint64_t qdA = tc::sw128_desc(smem_u32(smem + kOffQA), 16, 1024);
+      const uint64_t qdB = tc::sw128_desc(smem_u32(smem + kOffQB), 16, 1024);
+      const uint64_t kd0 = tc::sw128_desc(smem_u32(smem + kOffK2), 16, 1024);
+      const uint64_t vd0 = tc::sw128_desc(smem_u32(smem + kOffV2), kHalf2, 1024);
       auto qk = [&](int x, int g) {  // S_x = Q_x . K(g)^T
-        const uint32_t kb = smem_u32(smem + kOffK2 + (g % kKSt) * kTile2);
-        const uint32_t qbase = x ? qb : qa;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t off = (k >> 2) * kHalf2 + (k & 3) * 32;
-          tc::mma_ss(tmem + x * 128, tc::sw128_desc(qbase + off, 16, 1024), tc::sw128_desc(kb + off, 16, 1024), kIdQK,
-                     k > 0 ? 1u : 0u);
-        }
+        const uint64_t kd = kd0 + (uint64_t)(((g % kKSt) * kTile2) >> 4);
+        if (x) pf_qk<1>(qdB, kd);
+        else pf_qk<0>(qdA, kd);
         tc::mma_commit(&s_full[x]);
       };
       auto pv = [&](int x, int g, bool first) {  // O_x += P_x(tmem) . V(g)
-        const uint32_t vb = smem_u32(smem + kOffV2 + (g % kVSt) * kTile2);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          tc::mma_ts(tmem + 256 + x * 128, tmem + x * 128 + k * 8, tc::sw128_desc(vb + k * 2048, kHalf2, 1024), kIdPV,
-                     (!first || k > 0) ? 1u : 0u);
+        const uint64_t vd = vd0 + (uint64_t)(((g % kVSt) * kTile2) >> 4);
+        if (x) pf_pv<1>(vd, first);
+        else pf_pv<0>(vd, first);
       };
       int g = 0;
       for (int i = 0;; ++i) {
