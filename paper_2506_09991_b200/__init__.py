@@ -14,10 +14,11 @@ call runs on the GPU.
 from __future__ import annotations
 
 import ctypes
+import os
 import pathlib
 
 PKG = pathlib.Path(__file__).resolve().parent
-LIB_PATH = PKG / "libmvb200.so"
+LIB_PATH = pathlib.Path(os.environ["MV_LIB"]) if os.environ.get("MV_LIB") else PKG / "libmvb200.so"  # MV_LIB: A/B builds
 
 
 class MvError(RuntimeError):

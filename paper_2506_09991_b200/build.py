@@ -10,12 +10,12 @@ import sys
 PKG = pathlib.Path(__file__).resolve().parent
 REPO = PKG.parent
 CSRC = PKG / "csrc"
-OUT = PKG / "libmvb200.so"
-OBJ = PKG / "build"
+OUT = pathlib.Path(os.environ.get("MV_BUILD_OUT", PKG / "libmvb200.so"))
+OBJ = pathlib.Path(os.environ.get("MV_BUILD_OBJ", PKG / "build"))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "--expt-relaxed-constexpr", f"-I{REPO / 'include'}", f"-I{CSRC}"]
+         "--expt-relaxed-constexpr", f"-I{REPO / 'include'}", f"-I{CSRC}"] + os.environ.get("MV_NVCC_EXTRA", "").split()
 
 
 def sources():

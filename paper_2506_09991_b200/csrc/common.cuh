@@ -198,6 +198,15 @@ inline RopeTable make_rope_table(double base) {
   for (int i = 0; i < kHeadDim / 2; ++i) t.inv[i] = std::pow(base, -2.0 * (double)i / (double)kHeadDim);
   return t;
 }
+// Stages the frequency table in shared memory.  Indexing the by-value kernel-parameter copy
+// with a lane-dependent index serialises in the constant cache (16 distinct addresses per
+// warp), which made the RoPE passes ~4x slower than their HBM bound.  Call before any early
+// return (it contains a block barrier).
+__device__ __forceinline__ const double* rope_stage(const RopeTable& rt, double* s_inv) {
+  for (int t = threadIdx.x; t < kHeadDim / 2; t += blockDim.x) s_inv[t] = rt.inv[t];
+  __syncthreads();
+  return s_inv;
+}
 __device__ __forceinline__ void rope_cs(int pos, double inv, float& c, float& s) {
   double th = (double)pos * inv;
   th = fma(-6.283185307179586476925286766559, rint(th * 0.15915494309189533576888376337251), th);  // [-pi, pi]

@@ -732,6 +732,8 @@ __global__ void combine_kernel(const float* __restrict__ part_o, const float2* _
 __global__ void rope_q_tile_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pos, int n,
                                    int kv_heads, int gqa, int R, const RopeTable rt, __nv_bfloat16* __restrict__ tile,
                                    int* counter) {
+  __shared__ double s_inv[kHeadDim / 2];
+  const double* inv = rope_stage(rt, s_inv);
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (x == 0) *counter = 0;
   const int64_t total = (int64_t)n * kv_heads * R * 16;
@@ -749,7 +751,7 @@ __global__ void rope_q_tile_kernel(const __nv_bfloat16* __restrict__ q, const in
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       float cs, sn;
-      rope_cs(p, rt.inv[c * 4 + j], cs, sn);
+      rope_cs(p, inv[c * 4 + j], cs, sn);
       const float2 ab = __bfloat1622float2(h2[j]);
       h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
     }

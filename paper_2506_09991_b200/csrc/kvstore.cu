@@ -178,13 +178,13 @@ __global__ void k_append_table(PageRef* __restrict__ arena, int32_t* __restrict_
 }
 
 // step 2: per token, write slot token ids, payload records and (optionally) K/V.
-__device__ __forceinline__ void rope8(uint4& v, int pos, int chunk, const RopeTable& rt) {
+__device__ __forceinline__ void rope8(uint4& v, int pos, int chunk, const double* inv) {
   // 8 dims = 4 interleaved pairs, pair index t = chunk*4 + j (toy_model.cpp:30-41)
   __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     float c, s;
-    rope_cs(pos, rt.inv[chunk * 4 + j], c, s);
+    rope_cs(pos, inv[chunk * 4 + j], c, s);
     float2 ab = __bfloat1622float2(h[j]);
     h[j] = __floats2bfloat162_rn(ab.x * c - ab.y * s, ab.x * s + ab.y * c);
   }
@@ -192,13 +192,13 @@ __device__ __forceinline__ void rope8(uint4& v, int pos, int chunk, const RopeTa
 
 __device__ __forceinline__ void write_kv_token(__nv_bfloat16* kp, __nv_bfloat16* vp, int64_t page, int slot,
                                                int kv_heads, const __nv_bfloat16* k, const __nv_bfloat16* v,
-                                               int pos, const RopeTable& rt, int lane, int nlanes) {
+                                               int pos, const double* inv, int lane, int nlanes) {
   // kv_heads * 16 chunks of 8 dims; K rotated, V verbatim; stored chunk-swizzled.
   for (int j = lane; j < kv_heads * 16; j += nlanes) {
     int h = j >> 4, c = j & 15;
     size_t dst = kv_page_head_offset(page, h, kv_heads) + (size_t)kv_chunk_offset(slot, c);
     uint4 kk = *reinterpret_cast<const uint4*>(k + (size_t)h * kHeadDim + c * 8);
-    rope8(kk, pos, c, rt);
+    rope8(kk, pos, c, inv);
     *reinterpret_cast<uint4*>(kp + dst) = kk;
     *reinterpret_cast<uint4*>(vp + dst) = *reinterpret_cast<const uint4*>(v + (size_t)h * kHeadDim + c * 8);
   }
@@ -210,6 +210,8 @@ __global__ void k_append_data(AppendPlan pl, const int32_t* __restrict__ page_ou
                               const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                               const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads,
                               const RopeTable rt) {
+  __shared__ double s_inv[kHeadDim / 2];
+  const double* inv = rope_stage(rt, s_inv);
   // one warp per token
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
@@ -232,7 +234,7 @@ __global__ void k_append_data(AppendPlan pl, const int32_t* __restrict__ page_ou
     for (int b = lane; b < rec_bytes; b += 32) records[gslot * rec_bytes + b] = rec_in[(int64_t)t * rec_bytes + b];
   if (k && v)
     write_kv_token(kp, vp, page, slot, kv_heads, k + (size_t)t * kv_heads * kHeadDim,
-                   v + (size_t)t * kv_heads * kHeadDim, pos ? pos[t] : 0, rt, lane, 32);
+                   v + (size_t)t * kv_heads * kHeadDim, pos ? pos[t] : 0, inv, lane, 32);
 }
 
 // Engine fast path: one token per handle, in place (one warp per handle, 4 per CTA).
@@ -247,6 +249,8 @@ __global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ 
                              int32_t* __restrict__ free_top, int32_t* __restrict__ err, const int32_t* __restrict__ pos,
                              const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                              __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, const RopeTable rt) {
+  __shared__ double s_inv[kHeadDim / 2];
+  const double* inv = rope_stage(rt, s_inv);
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= n) return;
   int page = -1, slot = 0;
@@ -276,7 +280,7 @@ __global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ 
   slot = __shfl_sync(0xffffffffu, slot, 0);
   if (page < 0 || !k || !v) return;
   write_kv_token(kp, vp, page, slot, kv_heads, k + (size_t)i * kv_heads * kHeadDim,
-                 v + (size_t)i * kv_heads * kHeadDim, pos[i], rt, lane, 32);
+                 v + (size_t)i * kv_heads * kHeadDim, pos[i], inv, lane, 32);
 }
 
 // K/V of the last token of each handle (for layers > the one written at append).
@@ -284,11 +288,13 @@ __global__ void k_write_last(const PageRef* __restrict__ arena, const int64_t* _
                              const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                              const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads,
                              const RopeTable rt) {
+  __shared__ double s_inv[kHeadDim / 2];
+  const double* inv = rope_stage(rt, s_inv);
   const int i = blockIdx.x;
   PageRef r = arena[idx[i]];
   int slot = ref_begin(r) + ref_count(r) - 1;
   write_kv_token(kp, vp, r.page, slot, kv_heads, k + (size_t)i * kv_heads * kHeadDim,
-                 v + (size_t)i * kv_heads * kHeadDim, pos[i], rt, threadIdx.x, blockDim.x);
+                 v + (size_t)i * kv_heads * kHeadDim, pos[i], inv, threadIdx.x, blockDim.x);
 }
 
 // resolve / resolve_payloads / resolve_slots / gather_kv: one thread block per entry.

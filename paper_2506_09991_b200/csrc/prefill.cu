@@ -27,29 +27,34 @@ constexpr int kPfThreads = 128;  // 4 warps x 16 rows
 constexpr int kMaxD = 8;         // exclusion intervals per row supported by the kernel
 constexpr float kLazyRescalePf = 8.f;  // log2-domain headroom before O is rescaled
 
-__global__ void rope_qk_kernel(const __nv_bfloat16* __restrict__ q, const __nv_bfloat16* __restrict__ k,
-                               const int32_t* __restrict__ pos, int n, int hq, int hkv, const RopeTable rt,
-                               __nv_bfloat16* __restrict__ q_rot, __nv_bfloat16* __restrict__ k_rot) {
-  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // one 16 B chunk (4 pairs)
+__global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __restrict__ q,
+                                                      const __nv_bfloat16* __restrict__ k,
+                                                      const int32_t* __restrict__ pos, int n, int hq, int hkv,
+                                                      const RopeTable rt, __nv_bfloat16* __restrict__ q_rot,
+                                                      __nv_bfloat16* __restrict__ k_rot) {
+  __shared__ double s_inv[kHeadDim / 2];
+  const double* inv = rope_stage(rt, s_inv);
   const int64_t nq = (int64_t)n * hq * 16, nk = (int64_t)n * hkv * 16;
-  if (x >= nq + nk) return;
-  const bool isq = x < nq;
-  const int64_t y = isq ? x : x - nq;
-  const int c = (int)(y & 15);
-  const int row = (int)(y / (16 * (isq ? hq : hkv)));
-  const __nv_bfloat16* src = isq ? q : k;
-  __nv_bfloat16* dst = isq ? q_rot : k_rot;
-  uint4 v = *reinterpret_cast<const uint4*>(src + y * 8);
-  __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
-  const int p = pos[row];
+  // grid-stride over 16-byte chunks (4 interleaved pairs each)
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nq + nk; x += (int64_t)gridDim.x * blockDim.x) {
+    const bool isq = x < nq;
+    const int64_t y = isq ? x : x - nq;
+    const int c = (int)(y & 15);
+    const int row = (int)((y >> 4) / (isq ? hq : hkv));
+    const __nv_bfloat16* src = isq ? q : k;
+    __nv_bfloat16* dst = isq ? q_rot : k_rot;
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(src + y * 8));
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+    const int p = __ldg(pos + row);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    float cs, sn;
-    rope_cs(p, rt.inv[c * 4 + j], cs, sn);
-    const float2 ab = __bfloat1622float2(h2[j]);
-    h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
+    for (int j = 0; j < 4; ++j) {
+      float cs, sn;
+      rope_cs(p, inv[c * 4 + j], cs, sn);
+      const float2 ab = __bfloat1622float2(h2[j]);
+      h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
+    }
+    *reinterpret_cast<uint4*>(dst + y * 8) = v;
   }
-  *reinterpret_cast<uint4*>(dst + y * 8) = v;
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
@@ -306,7 +311,7 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
 
   const RopeTable rt = make_rope_table(rope_base > 0 ? rope_base : 10000.0);
   const int64_t chunks = (int64_t)n * (q_heads + kv_heads) * 16;
-  rope_qk_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, st>>>(
+  rope_qk_kernel<<<(unsigned)std::min<int64_t>((chunks + 255) / 256, 148 * 8), 256, 0, st>>>(
       (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_k, d_positions, n, q_heads, kv_heads, rt, q_rot, k_rot);
   MV_LAUNCH_CHECK();
   MV_CUDA_TRY(cudaMemsetAsync(vis, 0, 8, st));

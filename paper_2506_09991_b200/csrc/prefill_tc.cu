@@ -79,6 +79,15 @@ __device__ __forceinline__ void pf_pv(uint64_t vd, bool first) {
     tc::mma_ts(256 + X * 128, X * 128 + k * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV, (!first || k > 0) ? 1u : 0u);
 }
 
+// bits [lo, hi) of a 32-bit word, lo/hi clamped to [0, 32] (bmsk: one instruction)
+__device__ __forceinline__ uint32_t bit_range(int lo, int hi) {
+  lo = max(lo, 0);
+  const int w = max(min(hi, 32) - lo, 0);
+  uint32_t m;
+  asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(m) : "r"(lo), "r"(w));
+  return m;
+}
+
 struct __align__(16) PfItem {
   int qp, h, cnt, valid;
 };
@@ -280,15 +289,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
       const int qp = it.qp, h = it.h, cnt = it.cnt;
       const int32_t* lst = P.tlist + (size_t)qp * P.stride;
       const int i = qp * 256 + x * kT + r;  // sequence row
-      int elo[kMaxD2], ehi[kMaxD2];
-#pragma unroll
-      for (int q = 0; q < kMaxD2; ++q) {
-        elo[q] = ehi[q] = 0;
-        if (q < P.D && i < P.n) {
-          elo[q] = P.excl[((size_t)i * P.D + q) * 2];
-          ehi[q] = P.excl[((size_t)i * P.D + q) * 2 + 1];
-        }
-      }
+      // the row's exclusion intervals are re-read (L1) on partial tiles only: keeping 2 x 8 of
+      // them in registers next to the 128 scores forced spills
+      const int2* exr = reinterpret_cast<const int2*>(P.excl) + (size_t)min(i, P.n - 1) * P.D;
         float m_ref = -INFINITY, l = 0.f;
         for (int j = 0; j < cnt; ++j) {
           const int entry = lst[j];
@@ -297,27 +300,31 @@ __global__ void __launch_bounds__(kThreads2, 1)
           mbar_wait(&s_full[x], gs & 1);
           ++gs;
           tc::fence_after();
+#if MV_PF_NOSOFT
+          if (true) { mbar_arrive(&p_full[x]); continue; }
+#endif
           float v[kT];
     #pragma unroll
           for (int c = 0; c < 4; ++c) tc::tmem_ld32(lane_base + s_col + c * 32, v + c * 32);
           tc::tmem_wait_ld();
           float mx0 = -INFINITY, mx1 = -INFINITY, mx2 = -INFINITY, mx3 = -INFINITY;
+#if MV_PF_NOMASK
+          if (false) {
+#else
           if (status != 1) {
+#endif
             uint32_t vm[4];
             const int lim = status == 0 ? -1 : min(i, P.n - 1) - j0;  // last visible column
     #pragma unroll
-            for (int w = 0; w < 4; ++w) {
-              const int lo = w * 32;
-              vm[w] = lim < lo ? 0u : (lim >= lo + 31 ? 0xFFFFFFFFu : (0xFFFFFFFFu >> (31 - (lim - lo))));
-            }
+            for (int w = 0; w < 4; ++w) vm[w] = bit_range(0, lim + 1 - w * 32);
     #pragma unroll
             for (int q = 0; q < kMaxD2; ++q) {
-              const int a = max(elo[q] - j0, 0), e = min(ehi[q] - j0, kT);
+              if (q >= P.D) break;  // uniform across the CTA
+              const int2 ex = __ldg(exr + q);
+              const int a = ex.x - j0, e = ex.y - j0;
+              if (a >= kT || e <= 0) continue;  // interval misses this k tile
     #pragma unroll
-              for (int w = 0; w < 4; ++w) {
-                const int lo = max(a - w * 32, 0), hi = min(e - w * 32, 32);
-                if (hi > lo) vm[w] &= ~((hi - lo == 32 ? 0xFFFFFFFFu : ((1u << (hi - lo)) - 1u)) << lo);
-              }
+              for (int w = 0; w < 4; ++w) vm[w] &= ~bit_range(a - w * 32, e - w * 32);
             }
     #pragma unroll
             for (int c = 0; c < kT; c += 4) {
@@ -355,19 +362,26 @@ __global__ void __launch_bounds__(kThreads2, 1)
             m_ref = nref;
           }
           const float mu = m_ref == -INFINITY ? 0.f : m_ref;
-          float l0 = 0.f, l1 = 0.f;
-          uint32_t pk[64];
+          // packed f32x2 FMA / add (FFMA2, FADD2) halve the scale and row-sum instructions; P
+          // (bf16 pairs) overwrites S's first 64 columns 16 packed columns at a time, so only 16
+          // packed registers are live next to the 128 scores
+          const float2 sc2 = make_float2(P.scale_log2, P.scale_log2), nmu2 = make_float2(-mu, -mu);
+          float2 l2 = make_float2(0.f, 0.f), l2b = make_float2(0.f, 0.f);
     #pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            const float p0 = fast_exp2(fmaf(v[2 * c], P.scale_log2, -mu));
-            const float p1 = fast_exp2(fmaf(v[2 * c + 1], P.scale_log2, -mu));
-            l0 += p0;
-            l1 += p1;
-            pk[c] = pack_bf16(p0, p1);
+          for (int c16 = 0; c16 < 4; ++c16) {
+            uint32_t pk[16];
+    #pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const int c = c16 * 16 + u;
+              const float2 xy = __ffma2_rn(make_float2(v[2 * c], v[2 * c + 1]), sc2, nmu2);
+              const float2 pp = make_float2(fast_exp2(xy.x), fast_exp2(xy.y));
+              if (u & 1) l2b = __fadd2_rn(l2b, pp);
+              else l2 = __fadd2_rn(l2, pp);
+              pk[u] = pack_bf16(pp.x, pp.y);
+            }
+            tc::tmem_stNu<16>(lane_base + s_col + c16 * 16, pk);
           }
-          l += l0 + l1;
-          tc::tmem_st32u(lane_base + s_col, pk);
-          tc::tmem_st32u(lane_base + s_col + 32, pk + 32);
+          l += (l2.x + l2b.x) + (l2.y + l2b.y);
           tc::tmem_wait_st();
           tc::fence_before();
           mbar_arrive(&p_full[x]);

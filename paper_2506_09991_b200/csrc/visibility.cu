@@ -384,11 +384,17 @@ __global__ void tile_map_kernel(const int32_t* __restrict__ excl, int n, int D, 
 // B), one thread per row; for every 128-token k tile it records the status of each half
 // (0 skip, 1 full, 2 partial) and keeps the tile when either half needs it:
 //   list[qp][k] = kt | statusA << 20 | statusB << 22.
-__global__ void tile_map2_kernel(const int32_t* __restrict__ excl, int n, int D, int32_t* __restrict__ count,
-                                 int32_t* __restrict__ list, int stride) {
+constexpr int kTm2Chunk = 1024;  // k tiles classified per pass (flags in shared memory)
+constexpr int kTm2Threads = 1024;  // 4 groups of 256 (one thread per row) share the k tiles
+
+__global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* __restrict__ excl, int n, int D,
+                                                                int32_t* __restrict__ count,
+                                                                int32_t* __restrict__ list, int stride) {
   const int qp = blockIdx.x;
   const int tile = 128;
-  const int i = qp * 256 + threadIdx.x;
+  const int r = threadIdx.x & 255, grp = threadIdx.x >> 8;
+  const int i = qp * 256 + r;
+  const int rw = r >> 5, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool row_ok = i < n;
   int lo[8], hi[8];
   int nd = 0;
@@ -398,51 +404,70 @@ __global__ void tile_map2_kernel(const int32_t* __restrict__ excl, int n, int D,
       if (a < b) { lo[nd] = a; hi[nd] = b; ++nd; }
     }
   }
-  __shared__ int s_flags[2][8];
-  const int half = threadIdx.x >> 7;
+  // per 32-row warp and k tile: all rows empty / all rows full (no block barrier per k tile)
+  __shared__ uint8_t s_e[8][kTm2Chunk], s_f[8][kTm2Chunk];
+  __shared__ int s_warp_sum[kTm2Threads / 32];
   const int last_kt = min((qp * 256 + 255) / tile, (n - 1) / tile);
   int written = 0;
-  for (int kt = 0; kt <= last_kt; ++kt) {
-    const int j0 = kt * tile, j1 = min(n, j0 + tile);
-    bool empty = true, full = true;
-    if (row_ok) {
-      const int lastc = min(j1 - 1, i);
-      if (j0 > i) {
-        full = false;
-      } else {
-        int vis = lastc - j0 + 1;
-        bool touches = false;
-        for (int q = 0; q < nd; ++q) {
-          int a = max(lo[q], j0), b = min(hi[q], lastc + 1);
-          if (a < b) { vis -= b - a; touches = true; }
+  for (int kt0 = 0; kt0 <= last_kt; kt0 += kTm2Chunk) {
+    const int kt1 = min(last_kt + 1, kt0 + kTm2Chunk);
+    for (int kt = kt0 + grp; kt < kt1; kt += kTm2Threads / 256) {
+      const int j0 = kt * tile, j1 = min(n, j0 + tile);
+      bool empty = true, full = true;
+      if (row_ok) {
+        const int lastc = min(j1 - 1, i);
+        if (j0 > i) {
+          full = false;
+        } else {
+          int vis = lastc - j0 + 1;
+          bool touches = false;
+          for (int q = 0; q < nd; ++q) {
+            int a = max(lo[q], j0), b = min(hi[q], lastc + 1);
+            if (a < b) { vis -= b - a; touches = true; }
+          }
+          empty = vis == 0;
+          full = !touches && (j1 - 1 <= i) && (j0 + tile <= n);
         }
-        empty = vis == 0;
-        full = !touches && (j1 - 1 <= i) && (j0 + tile <= n);
+      }
+      const bool we = __all_sync(0xffffffffu, empty), wf = __all_sync(0xffffffffu, full);
+      if (lane == 0) {
+        s_e[rw][kt - kt0] = we;
+        s_f[rw][kt - kt0] = wf;
       }
     }
-    // per-half votes (4 warps per half)
-    const unsigned e = __ballot_sync(0xffffffffu, empty), f = __ballot_sync(0xffffffffu, full);
-    if ((threadIdx.x & 31) == 0) {
-      s_flags[0][threadIdx.x >> 5] = e == 0xffffffffu;
-      s_flags[1][threadIdx.x >> 5] = f == 0xffffffffu;
-    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // status per k tile (row warps 0-3 -> half A, 4-7 -> half B); one tile per thread
+    const int kt = kt0 + threadIdx.x;
+    int ent = -1;
+    if (kt < kt1) {
       int st[2];
+#pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         bool all_e = true, all_f = true;
-        for (int w = 0; w < 4; ++w) { all_e &= s_flags[0][hh * 4 + w] != 0; all_f &= s_flags[1][hh * 4 + w] != 0; }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          all_e &= s_e[hh * 4 + w][kt - kt0] != 0;
+          all_f &= s_f[hh * 4 + w][kt - kt0] != 0;
+        }
         st[hh] = all_e ? 0 : (all_f ? 1 : 2);
       }
-      if (st[0] || st[1]) list[(int64_t)qp * stride + written] = kt | (st[0] << 20) | (st[1] << 22);
-      s_flags[0][0] = st[0] || st[1];
+      if (st[0] || st[1]) ent = kt | (st[0] << 20) | (st[1] << 22);
     }
+    // ordered compaction
+    const unsigned keep = __ballot_sync(0xffffffffu, ent >= 0);
+    if (lane == 0) s_warp_sum[warp] = __popc(keep);
     __syncthreads();
-    if (s_flags[0][0]) ++written;
-    __syncthreads();
+    int base = written, total = 0;
+    for (int w = 0; w < kTm2Threads / 32; ++w) {
+      const int c = s_warp_sum[w];
+      if (w < warp) base += c;
+      total += c;
+    }
+    if (ent >= 0) list[(int64_t)qp * stride + base + __popc(keep & ((1u << lane) - 1u))] = ent;
+    written += total;
+    __syncthreads();  // s_e / s_f / s_warp_sum reused by the next pass
   }
   if (threadIdx.x == 0) count[qp] = written;
-  (void)half;
 }
 }  // namespace
 }  // namespace mv
@@ -504,7 +529,7 @@ namespace mv {
 mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
                     int32_t stride, cudaStream_t stream) {
   const int n_qp = (n + 255) / 256;
-  tile_map2_kernel<<<n_qp, 256, 0, stream>>>(d_excl, n, max_depth, d_count, d_list, stride);
+  tile_map2_kernel<<<n_qp, kTm2Threads, 0, stream>>>(d_excl, n, max_depth, d_count, d_list, stride);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }
