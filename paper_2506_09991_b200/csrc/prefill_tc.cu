@@ -1,24 +1,34 @@
 // prefill_tc.cu — K3 v2: branch-masked prefill on the 5th-gen tensor cores (tcgen05 / TMEM / TMA).
 //
-// One CTA per (256-row query pair, q head); the pair is two 128-row tiles A and B that share
-// every K/V tile, so one MMA thread can ping-pong between them while two softmax warpgroups
-// work (the FlashAttention-4 schedule):
+// Persistent: one CTA per SM pulls (256-row query pair, q head) items from a queue (heaviest
+// pairs first).  The pair is two 128-row tiles A and B that share every K/V tile, so one MMA
+// thread can ping-pong between them while two softmax warpgroups work (the FlashAttention-4
+// schedule):
 //
-//   warp 0   TMA  : lane 0 loads Q_A, Q_B once, then K tiles; lane 1 loads V tiles (separate
-//                   rings: K frees after Q.K^T, V only after P.V)
-//   warp 1   MMA  : one thread.  Loop over the pair's k tiles j:
+//   warp 0   lane 0: scheduler + TMA for Q_A, Q_B (once per item) and the K ring; lane 1: V ring
+//                   (separate rings: K frees after Q.K^T, V only after P.V)
+//   warp 1   MMA  : one thread.  Loop over the pair's listed k tiles j:
 //                     PV_A(j); QK_A(j+1); PV_B(j); QK_B(j+1)
 //                   S_X = Q_X.K^T (M=128, N=128, 8 x K16, SS operands from SW128 smem) into TMEM;
-//                   O_X += P_X.V with P_X read straight from TMEM (TS operand, aliasing S_X)
+//                   O_X += P_X.V with P_X read straight from TMEM (TS operand, aliasing S_X).
+//                   P arrives in two halves (k tokens 0-63, 64-127) so the first four P.V MMAs
+//                   start while the softmax finishes the second half.
 //   warps 2-5 softmax A, warps 6-9 softmax B : thread = query row = TMEM lane.  S row by
-//                   tcgen05.ld, interval mask on partial tiles (128-bit row mask built once per
-//                   tile), lazy O rescale in TMEM only when the row max grows by > 2^8, P as packed
-//                   bf16 back into the S columns by tcgen05.st.  Epilogue O / l from TMEM.
+//                   tcgen05.ld, interval mask on partial tiles (bmsk-built 128-bit row mask),
+//                   lazy O rescale in TMEM only when the row max grows by > 2^8, P as packed
+//                   bf16 back into the S columns by tcgen05.st (FFMA2 / FADD2 for scale and
+//                   row sum).  Epilogue O / l from TMEM.
 //
 // TMEM (512 columns): S/P_A 0..127, S/P_B 128..255, O_A 256..383, O_B 384..511.
 // Ordering facts the schedule relies on: tcgen05.mma ops of one thread execute in issue order,
 // so QK_X(j+1) (which overwrites S/P_X) cannot overtake PV_X(j) (which reads P_X), and the
 // commit after QK_X(j+1) also certifies PV_X(j) -> the softmax may rescale O_X after s_full.
+//
+// Measured bound (tools/trace_prefill.py, C3): the per-tile chain is PV_X(j) + QK_X(j+1) on the
+// tensor core (16 MMAs at the 64-cycle N=128 tensor rate, ~1.4k cycles) followed by softmax X
+// (~2k cycles: 128 MUFU.EX2 per row at 16 lanes/clk/SM, tools/microbench/mb_exp.cu).  S/P
+// aliasing (TMEM is full: 2 x S + 2 x O) keeps QK_X(j+1) behind PV_X(j), so the tensor core
+// idles ~1/3 of each step.
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
@@ -72,10 +82,12 @@ __device__ __forceinline__ void pf_qk(uint64_t qd, uint64_t kd) {
     tc::mma_ss(X * 128, qd + off, kd + off, kIdQK, k > 0 ? 1u : 0u);
   }
 }
-template <int X>
+// P.V over k tokens [64 H, 64 H + 64): the softmax releases P in two halves so the first four
+// MMAs run while it still computes the second half
+template <int X, int H>
 __device__ __forceinline__ void pf_pv(uint64_t vd, bool first) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
+  for (int k = 4 * H; k < 4 * H + 4; ++k)
     tc::mma_ts(256 + X * 128, X * 128 + k * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV, (!first || k > 0) ? 1u : 0u);
 }
 
@@ -108,8 +120,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
   uint64_t* v_full = k_empty + kKSt;
   uint64_t* v_empty = v_full + kVSt;
   uint64_t* s_full = v_empty + kVSt;       // [2]: tile A, B
-  uint64_t* p_full = s_full + 2;           // [2]
-  uint64_t* o_fin = p_full + 2;            // [2] MMA commit: O_X of the item final
+  uint64_t* p_full = s_full + 2;           // [2] P_X columns for k tokens 0-63 written
+  uint64_t* p_hi = p_full + 2;             // [2] P_X columns for k tokens 64-127 written
+  uint64_t* o_fin = p_hi + 2;              // [2] MMA commit: O_X of the item final
   uint64_t* o_empty = o_fin + 2;           // [2] softmax WG X read O_X (epilogue)
   uint64_t* item_full = o_empty + 2;       // [2] scheduler -> all roles
   uint64_t* slot_empty = item_full + 2;    // [2] V lane + MMA + 8 softmax warps -> scheduler
@@ -131,6 +144,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     for (int x = 0; x < 2; ++x) {
       mbar_init(&s_full[x], 1);
       mbar_init(&p_full[x], 128);
+      mbar_init(&p_hi[x], 128);
       mbar_init(&o_fin[x], 1);
       mbar_init(&o_empty[x], 128);
       mbar_init(&item_full[x], 1);
@@ -216,10 +230,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
         else pf_qk<0>(qdA, kd);
         tc::mma_commit(&s_full[x]);
       };
-      auto pv = [&](int x, int g, bool first) {  // O_x += P_x(tmem) . V(g)
+      auto pv = [&](int x, int g, bool first) {  // O_x += P_x(tmem) . V(g), P in two halves
         const uint64_t vd = vd0 + (uint64_t)(((g % kVSt) * kTile2) >> 4);
-        if (x) pf_pv<1>(vd, first);
-        else pf_pv<0>(vd, first);
+        if (x) pf_pv<1, 0>(vd, first);
+        else pf_pv<0, 0>(vd, first);
+        mbar_wait(&p_hi[x], g & 1);
+        tc::fence_after();
+        if (x) pf_pv<1, 1>(vd, first);
+        else pf_pv<0, 1>(vd, first);
       };
       int g = 0;
       for (int i = 0;; ++i) {
@@ -301,7 +319,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           ++gs;
           tc::fence_after();
 #if MV_PF_NOSOFT
-          if (true) { mbar_arrive(&p_full[x]); continue; }
+          if (true) { mbar_arrive(&p_full[x]); mbar_arrive(&p_hi[x]); continue; }
 #endif
           float v[kT];
     #pragma unroll
@@ -380,11 +398,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
               pk[u] = pack_bf16(pp.x, pp.y);
             }
             tc::tmem_stNu<16>(lane_base + s_col + c16 * 16, pk);
+            if (c16 == 1 || c16 == 3) {  // P for k tokens 0-63, then 64-127
+              tc::tmem_wait_st();
+              tc::fence_before();
+              mbar_arrive(c16 == 1 ? &p_full[x] : &p_hi[x]);
+            }
           }
           l += (l2.x + l2b.x) + (l2.y + l2b.y);
-          tc::tmem_wait_st();
-          tc::fence_before();
-          mbar_arrive(&p_full[x]);
         }
       // epilogue: O_x / l, then hand O_x back to the MMA issuer
       if (cnt > 0) mbar_wait(&o_fin[x], it_i & 1);
