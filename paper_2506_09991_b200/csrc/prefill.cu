@@ -271,6 +271,12 @@ namespace mv {
 mv_status prefill_tc2_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
                              const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
                              void* d_out, int32_t out_dtype, int32_t* tcount, int32_t* tlist, cudaStream_t st);
+mv_status prefill_tc3_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
+                             const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
+                             void* d_out, int32_t out_dtype, const int32_t* hcount, const int32_t* tlist,
+                             int32_t stride, cudaStream_t st);
+mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
+                    int32_t stride, cudaStream_t stream, int32_t* d_hcount);
 }
 
 using namespace mv;
@@ -316,7 +322,15 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
   MV_LAUNCH_CHECK();
   MV_CUDA_TRY(cudaMemsetAsync(vis, 0, 8, st));
 
-  if (!getenv("MV_PREFILL_V0"))  // tcgen05 path (prefill_tc.cu); v0 kept only for A/B diagnostics
+  if (!getenv("MV_PREFILL_V0") && !getenv("MV_PREFILL_TC2")) {  // tcgen05 v3 (prefill_tc3.cu)
+    // pair lists + per-128-row-tile processed counts (hcount after the n_qp pair counts)
+    const int n_qp = (n + 255) / 256, stride = (n + 127) / 128;
+    int32_t* hcount = tcount + n_qp;
+    if (mv_status e = tile_map2(d_excl, n, max_depth, tcount, tlist, stride, st, hcount)) return e;
+    return prefill_tc3_launch(q_rot, k_rot, (const __nv_bfloat16*)d_v, d_excl, max_depth, n, q_heads, kv_heads, d_out,
+                              out_dtype, hcount, tlist, stride, st);
+  }
+  if (!getenv("MV_PREFILL_V0"))  // tcgen05 v2 (prefill_tc.cu) and v0 kept for A/B diagnostics
     return prefill_tc2_launch(q_rot, k_rot, (const __nv_bfloat16*)d_v, d_excl, max_depth, n, q_heads, kv_heads, d_out,
                               out_dtype, tcount, tlist, st);
   if (mv_status e = mv_tile_map(d_excl, n, max_depth, kBN, tcount, tlist, vis, stream)) return e;

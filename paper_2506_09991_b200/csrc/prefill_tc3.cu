@@ -1,0 +1,501 @@
+// prefill_tc3.cu — K3 v3: branch-masked prefill, one 128-row query tile per work item with the
+// S tile double-buffered in TMEM and the softmax split by columns over two warpgroups.
+//
+// Why (tools/trace_prefill.py on v2, prefill_tc.cu): with two q tiles per CTA, TMEM holds
+// 2 x S + 2 x O = 512 columns, P aliases S, and Q.K^T(j+1) has to queue behind P.V(j); each
+// tile's chain was 16 tensor MMAs + a full-row softmax (~3.9k cycles per k step) and the tensor
+// core idled a third of the time.  Here TMEM holds three S buffers and one O, so Q.K^T(j+1)
+// and Q.K^T(j+2) are issued while the softmax of tile j works, and the softmax of tile j+1
+// starts the moment it finishes tile j (with two buffers it still waited on P.V(j-1) + Q.K^T(j+1)
+// behind the P(j-1) handoff).  Each row's 128 scores are split over
+// two warps of the same TMEM lane quarter (64 columns each): half the per-thread latency,
+// both warps of an SMSP pair busy, row max / sum exchanged through shared memory.
+//
+// Persistent: one CTA per SM pulls (128-row q tile, q head) items from a queue, heaviest
+// (last) tiles first.  Roles:
+//   warp 0 lane 0: scheduler + TMA for the item's Q tile and the K ring
+//   warp 0 lane 1: TMA for the V ring
+//   warp 1 lane 0: MMA issuer.  Per item with m processed k tiles (status != 0):
+//                    QK(0); QK(1); QK(2); for j: [P(j)] PV(j); QK(j+3)
+//                  S(j) = Q.K(j)^T into S buffer j % 3 (SS, M=128 N=128, 8 x K16);
+//                  O += P(j).V(j) (TS: P read from TMEM where it overwrote S(j)).
+//   warps 2-5 (columns 0-63) and 6-9 (columns 64-127): softmax, thread = row = TMEM lane.
+//                  Lazy O rescale (only when the row max grows by > 2^8), after P.V(j-1) is
+//                  certified by the V ring's empty barrier.  Epilogue: O / l for its 64 dims.
+// Tile lists come from tile_map2 (pairs of 128-row tiles): item tile t reads the pair list of
+// t / 2 and skips entries whose status for half t & 1 is 0; hcount[t] (written by tile_map2)
+// is the number of processed entries.
+#include <cstdio>
+#include <algorithm>
+#include <cstdlib>
+#include <vector>
+
+#include "tc_common.cuh"
+
+namespace mv {
+namespace {
+
+constexpr int kT3 = 128;
+constexpr int kKSt3 = 3;
+constexpr int kVSt3 = 2;
+constexpr int kThreads3 = 320;
+constexpr int kHalf3 = kT3 * 128;  // SW128 half tile: 128 rows x 64 dims
+constexpr int kTile3 = 2 * kHalf3;
+constexpr int kOffQ3 = 0;  // one Q tile: the next item's loads once this item's last Q.K^T is issued
+constexpr int kOffK3 = kOffQ3 + kTile3;
+constexpr int kOffV3 = kOffK3 + kKSt3 * kTile3;
+constexpr int kOffBar3 = kOffV3 + kVSt3 * kTile3;
+constexpr int kOffX3 = kOffBar3 + 256;  // row max / sum exchange: [2 parity][2 WG][128 rows] f32
+constexpr int kSmem3 = kOffX3 + 2 * 2 * 128 * 4 + 1024;
+constexpr uint32_t kIdQK3 = tc::idesc_bf16(128, 128, 0, 0);
+constexpr uint32_t kIdPV3 = tc::idesc_bf16(128, 128, 0, 1);
+constexpr float kLazy3 = 8.f;
+// TMEM columns: three S buffers (S(g) in buffer g % 3) and one O
+constexpr int kSB = 3;
+constexpr uint32_t kS0 = 0, kO0 = 384;
+
+struct Tc3Params {
+  const int32_t* excl;
+  const int32_t* hcount;  // [n_qt] processed k tiles per 128-row q tile
+  const int32_t* tlist;   // [n_qp][stride] pair lists from tile_map2
+  void* out;
+  int out_f32;
+  int n, hq, hkv, D, n_qt, stride;
+  float scale_log2;
+  int n_items;
+  int* counters;
+  unsigned long long* trace;  // MV_PF_TRACE builds only: CTA 0 timeline, [tile][8] clock64
+};
+
+#ifndef MV_PF_TRACE
+#define MV_PF_TRACE 0
+#endif
+constexpr int kTrace3 = 1024;
+#define PF3_TRACE(step, k)                                             \
+  do {                                                                 \
+    if (MV_PF_TRACE && blockIdx.x == 0 && (step) < kTrace3)            \
+      P.trace[(step) * 8 + (k)] = clock64();                           \
+  } while (0)
+
+struct __align__(16) Item3 {
+  int t, h, m, valid;
+};
+
+template <int B>
+__device__ __forceinline__ void qk3(uint64_t qd, uint64_t kd) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint64_t off = (uint64_t)(((k >> 2) * kHalf3 + (k & 3) * 32) >> 4);
+    tc::mma_ss(kS0 + B * 128, qd + off, kd + off, kIdQK3, k > 0 ? 1u : 0u);
+  }
+}
+template <int B>
+__device__ __forceinline__ void pv3(uint64_t vd, bool first) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    tc::mma_ts(kO0, kS0 + B * 128 + k * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV3, (!first || k > 0) ? 1u : 0u);
+}
+
+__device__ __forceinline__ uint32_t bit_range3(int lo, int hi) {
+  lo = max(lo, 0);
+  const int w = max(min(hi, 32) - lo, 0);
+  uint32_t m;
+  asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(m) : "r"(lo), "r"(w));
+  return m;
+}
+__device__ __forceinline__ void pair_sync(int q) {  // the two softmax warps of lane quarter q
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads3, 1)
+    prefill_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
+                       const __grid_constant__ CUtensorMap map_v, Tc3Params P) {
+  extern __shared__ uint8_t smem_raw3[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw3) + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar3);
+  uint64_t* q_full = bars;               // Q tile landed (tx)
+  uint64_t* q_empty = q_full + 1;        // MMA commit after the item's last Q.K^T
+  uint64_t* k_full = q_empty + 1;        // [3]
+  uint64_t* k_empty = k_full + kKSt3;    // [3]
+  uint64_t* v_full = k_empty + kKSt3;    // [2]
+  uint64_t* v_empty = v_full + kVSt3;    // [2] MMA commit after P.V (also certifies O for the rescale)
+  uint64_t* s_full = v_empty + kVSt3;    // [3] S buffer b written
+  uint64_t* p_full = s_full + kSB;       // [3] 256 softmax threads wrote P into S buffer b
+  uint64_t* o_fin = p_full + kSB;        // O final for the item
+  uint64_t* o_empty = o_fin + 1;         // epilogue read O (256 threads)
+  uint64_t* item_full = o_empty + 1;     // [2]
+  uint64_t* slot_empty = item_full + 2;  // [2] V lane + MMA + 8 softmax warps
+  Item3* s_item = reinterpret_cast<Item3*>(slot_empty + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_item + 2);
+  float* s_x = reinterpret_cast<float*>(smem + kOffX3);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    mbar_init(o_fin, 1);
+    mbar_init(o_empty, 256);
+    for (int b = 0; b < kSB; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&p_full[b], 256);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&item_full[b], 1);
+      mbar_init(&slot_empty[b], 10);
+    }
+    for (int s = 0; s < kKSt3; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < kVSt3; ++s) {
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  if (*tmem_slot != 0) __trap();  // one CTA per SM owns all 512 columns
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- scheduler + Q / K loader ----------------
+      tc::tma_prefetch_desc(&map_q);
+      tc::tma_prefetch_desc(&map_k);
+      int gk = 0;
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        if (i >= 2) mbar_wait(&slot_empty[buf], ((i >> 1) - 1) & 1);
+        const int w = atomicAdd(&P.counters[0], 1);
+        Item3 it;
+        it.valid = w < P.n_items;
+        it.t = it.valid ? P.n_qt - 1 - w / P.hq : 0;
+        it.h = it.valid ? w % P.hq : 0;
+        it.m = it.valid ? P.hcount[it.t] : 0;
+        s_item[buf] = it;
+        mbar_arrive(&item_full[buf]);
+        if (!it.valid) break;
+        if (i >= 1) mbar_wait(q_empty, (i - 1) & 1);
+        mbar_arrive_expect_tx(q_full, kTile3);
+        tc::tma_load_3d(smem + kOffQ3, &map_q, 0, it.h, it.t * kT3, q_full);
+        tc::tma_load_3d(smem + kOffQ3 + kHalf3, &map_q, 64, it.h, it.t * kT3, q_full);
+        const int kvh = it.h / (P.hq / P.hkv);
+        const int32_t* lst = P.tlist + (size_t)(it.t >> 1) * P.stride;
+        const int sh = 20 + 2 * (it.t & 1);
+        for (int j = 0, done = 0; done < it.m; ++j) {
+          const int e = lst[j];
+          if (((e >> sh) & 3) == 0) continue;
+          const int s = gk % kKSt3;
+          if (gk >= kKSt3) mbar_wait(&k_empty[s], ((gk / kKSt3) - 1) & 1);
+          const int kt = e & 0xFFFFF;
+          mbar_arrive_expect_tx(&k_full[s], kTile3);
+          tc::tma_load_3d(smem + kOffK3 + s * kTile3, &map_k, 0, kvh, kt * kT3, &k_full[s]);
+          tc::tma_load_3d(smem + kOffK3 + s * kTile3 + kHalf3, &map_k, 64, kvh, kt * kT3, &k_full[s]);
+          ++gk;
+          ++done;
+        }
+      }
+    } else if (lane == 1) {
+      // ---------------- V loader ----------------
+      tc::tma_prefetch_desc(&map_v);
+      int gv = 0;
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        mbar_wait(&item_full[buf], (i >> 1) & 1);
+        const Item3 it = s_item[buf];
+        mbar_arrive(&slot_empty[buf]);
+        if (!it.valid) break;
+        const int kvh = it.h / (P.hq / P.hkv);
+        const int32_t* lst = P.tlist + (size_t)(it.t >> 1) * P.stride;
+        const int sh = 20 + 2 * (it.t & 1);
+        for (int j = 0, done = 0; done < it.m; ++j) {
+          const int e = lst[j];
+          if (((e >> sh) & 3) == 0) continue;
+          const int s = gv % kVSt3;
+          if (gv >= kVSt3) mbar_wait(&v_empty[s], ((gv / kVSt3) - 1) & 1);
+          const int kt = e & 0xFFFFF;
+          mbar_arrive_expect_tx(&v_full[s], kTile3);
+          tc::tma_load_3d(smem + kOffV3 + s * kTile3, &map_v, 0, kvh, kt * kT3, &v_full[s]);
+          tc::tma_load_3d(smem + kOffV3 + s * kTile3 + kHalf3, &map_v, 64, kvh, kt * kT3, &v_full[s]);
+          ++gv;
+          ++done;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      const uint64_t qd0 = tc::sw128_desc(smem_u32(smem + kOffQ3), 16, 1024);
+      const uint64_t kd0 = tc::sw128_desc(smem_u32(smem + kOffK3), 16, 1024);
+      const uint64_t vd0 = tc::sw128_desc(smem_u32(smem + kOffV3), kHalf3, 1024);
+      int g = 0;  // processed k tiles so far (K/V ring index, S buffer = g % 3)
+      auto qk = [&](uint64_t qd, int gg) {  // S(gg % 3) = Q . K(gg)^T
+        mbar_wait(&k_full[gg % kKSt3], (gg / kKSt3) & 1);
+        tc::fence_after();
+        const uint64_t kd = kd0 + (uint64_t)(((gg % kKSt3) * kTile3) >> 4);
+        const int b = gg % kSB;
+        if (b == 0) qk3<0>(qd, kd);
+        else if (b == 1) qk3<1>(qd, kd);
+        else qk3<2>(qd, kd);
+        tc::mma_commit(&s_full[b]);
+        tc::mma_commit(&k_empty[gg % kKSt3]);
+      };
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        mbar_wait(&item_full[buf], (i >> 1) & 1);
+        const Item3 it = s_item[buf];
+        mbar_arrive(&slot_empty[buf]);
+        if (!it.valid) break;
+        const int m = it.m;
+        const uint64_t qd = qd0;
+        mbar_wait(q_full, i & 1);
+        for (int u = 0; u < kSB && u < m; ++u) qk(qd, g + u);
+        if (m <= kSB) tc::mma_commit(q_empty);
+        for (int j = 0; j < m; ++j, ++g) {
+          mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
+          mbar_wait(&p_full[g % kSB], (g / kSB) & 1);
+          PF3_TRACE(g, 0);
+          if (j == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue of item i-1 read O
+          tc::fence_after();
+          const uint64_t vd = vd0 + (uint64_t)(((g % kVSt3) * kTile3) >> 4);
+          const int b = g % kSB;
+          if (b == 0) pv3<0>(vd, j == 0);
+          else if (b == 1) pv3<1>(vd, j == 0);
+          else pv3<2>(vd, j == 0);
+          tc::mma_commit(&v_empty[g % kVSt3]);
+          if (j + kSB < m) {
+            qk(qd, g + kSB);  // S buffer g % 3 again: in order behind P.V(g)
+            if (j + kSB + 1 == m) tc::mma_commit(q_empty);
+          }
+          PF3_TRACE(g, 1);
+        }
+        if (m == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);
+        tc::mma_commit(o_fin);
+      }
+    }
+  } else {
+    // ---------------- softmax: warps 2-5 columns 0-63, warps 6-9 columns 64-127 ----------------
+    const int c = (warp - 2) >> 2;      // column half
+    const int quarter = warp & 3;       // TMEM lane quarter
+    const int r = quarter * 32 + lane;  // row within the tile
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    int g = 0;
+    for (int it_i = 0;; ++it_i) {
+      const int buf = it_i & 1;
+      mbar_wait(&item_full[buf], (it_i >> 1) & 1);
+      const Item3 it = s_item[buf];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slot_empty[buf]);
+      if (!it.valid) break;
+      const int i = it.t * kT3 + r;  // sequence row
+      const int2* exr = reinterpret_cast<const int2*>(P.excl) + (size_t)min(i, P.n - 1) * P.D;
+      const int32_t* lst = P.tlist + (size_t)(it.t >> 1) * P.stride;
+      const int sh = 20 + 2 * (it.t & 1);
+      const uint32_t o_col = kO0 + c * 64;
+      float m_ref = -INFINITY, l = 0.f;
+      // the list entry of the next tile is loaded one tile ahead (its L2 latency used to sit
+      // between releasing P and waiting for the next S)
+      int j = 0;
+      int nx = it.m > 0 ? lst[0] : 0;
+      for (int done = 0; done < it.m; ++done, ++g) {
+        int e = nx;
+        ++j;
+        while (((e >> sh) & 3) == 0) e = lst[j++];
+        nx = done + 1 < it.m ? lst[j] : 0;
+        const int j0 = (e & 0xFFFFF) * kT3;
+        const int status = (e >> sh) & 3;
+        const uint32_t s_col = kS0 + (g % kSB) * 128;
+        mbar_wait(&s_full[g % kSB], (g / kSB) & 1);
+        const bool tr = r == 0;
+        if (tr) PF3_TRACE(g, c ? 6 : 2);
+        tc::fence_after();
+        float v[64];
+        tc::tmem_ld32(lane_base + s_col + c * 64, v);
+        tc::tmem_ld32(lane_base + s_col + c * 64 + 32, v + 32);
+        tc::tmem_wait_ld();
+        if (tr && !c) PF3_TRACE(g, 3);
+        float mx0 = -INFINITY, mx1 = -INFINITY;
+        if (status != 1) {
+          const int lim = min(i, P.n - 1) - j0;  // last visible column
+          uint32_t vm[2];
+#pragma unroll
+          for (int w = 0; w < 2; ++w) vm[w] = bit_range3(0, lim + 1 - (2 * c + w) * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            if (q >= P.D) break;
+            const int2 ex = __ldg(exr + q);
+            const int a = ex.x - j0, b = ex.y - j0;
+            if (a >= kT3 || b <= 0) continue;
+#pragma unroll
+            for (int w = 0; w < 2; ++w) vm[w] &= ~bit_range3(a - (2 * c + w) * 32, b - (2 * c + w) * 32);
+          }
+#pragma unroll
+          for (int k = 0; k < 64; k += 2) {
+            const uint32_t mm = vm[k >> 5] >> (k & 31);
+            v[k] = (mm & 1u) ? v[k] : -INFINITY;
+            v[k + 1] = (mm & 2u) ? v[k + 1] : -INFINITY;
+            mx0 = fmaxf(mx0, v[k]);
+            mx1 = fmaxf(mx1, v[k + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 64; k += 2) {
+            mx0 = fmaxf(mx0, v[k]);
+            mx1 = fmaxf(mx1, v[k + 1]);
+          }
+        }
+        // row max over both column halves (the pair barrier also orders both warps' S loads
+        // before either writes P into the S columns)
+        float* xs = s_x + (g & 1) * 256;
+        xs[c * 128 + r] = fmaxf(mx0, mx1);
+        pair_sync(quarter);
+        const float mx = fmaxf(xs[r], xs[128 + r]) * P.scale_log2;
+        if (tr && !c) PF3_TRACE(g, 4);
+        const bool need = mx > m_ref + kLazy3;
+        if (__any_sync(0xffffffffu, need)) {
+          const float nref = need ? fmaxf(m_ref, mx) : m_ref;
+          const float alpha = need ? fast_exp2(m_ref - nref) : 1.f;
+          if (done >= 1) {
+            // O holds P.V of the previous tile (g - 1): its V slot's release certifies it
+            mbar_wait(&v_empty[(g - 1) % kVSt3], ((g - 1) / kVSt3) & 1);
+            tc::fence_after();
+#pragma unroll 1
+            for (int cc = 0; cc < 2; ++cc) {
+              float o[32];
+              tc::tmem_ld32(lane_base + o_col + cc * 32, o);
+              tc::tmem_wait_ld();
+#pragma unroll
+              for (int k = 0; k < 32; ++k) o[k] *= alpha;
+              tc::tmem_st32(lane_base + o_col + cc * 32, o);
+            }
+          }
+          l *= alpha;
+          m_ref = nref;
+        }
+        const float mu = m_ref == -INFINITY ? 0.f : m_ref;
+        const float2 sc2 = make_float2(P.scale_log2, P.scale_log2), nmu2 = make_float2(-mu, -mu);
+        float2 la = make_float2(0.f, 0.f), lb = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c16 = 0; c16 < 2; ++c16) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            const int k = c16 * 32 + 2 * u;
+            const float2 xy = __ffma2_rn(make_float2(v[k], v[k + 1]), sc2, nmu2);
+            const float2 pp = make_float2(fast_exp2(xy.x), fast_exp2(xy.y));
+            if (u & 1) lb = __fadd2_rn(lb, pp);
+            else la = __fadd2_rn(la, pp);
+            pk[u] = pack_bf16(pp.x, pp.y);
+          }
+          // P for k tokens [64c, 64c + 64) -> packed columns [32c, 32c + 32) of the S buffer
+          tc::tmem_stNu<16>(lane_base + s_col + c * 32 + c16 * 16, pk);
+        }
+        l += (la.x + lb.x) + (la.y + lb.y);
+        tc::tmem_wait_st();
+        tc::fence_before();
+        if (tr) PF3_TRACE(g, c ? 7 : 5);
+        mbar_arrive(&p_full[g % kSB]);
+      }
+      // epilogue: row sum over both halves, O / l for this warp's 64 dims
+      mbar_wait(o_fin, it_i & 1);
+      tc::fence_after();
+      float* ls = s_x + (g & 1) * 256;  // the next tile's max slot: free until this pair syncs again
+      ls[c * 128 + r] = l;
+      pair_sync(quarter);
+      const float lt = ls[r] + ls[128 + r];
+      pair_sync(quarter);  // both read before the slot is reused by the next tile's max
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+#pragma unroll 1
+      for (int cc = 0; cc < 2; ++cc) {
+        float o[32];
+        tc::tmem_ld32(lane_base + o_col + cc * 32, o);
+        tc::tmem_wait_ld();
+        if (i < P.n) {
+          const int d0 = c * 64 + cc * 32;
+          if (P.out_f32) {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + it.h) * kHeadDim + d0);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + ((size_t)i * P.hq + it.h) * kHeadDim + d0);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
+                                  pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
+          }
+        }
+      }
+      tc::fence_before();
+      mbar_arrive(o_empty);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(&P.counters[1], 1) == (int)gridDim.x - 1) {
+    P.counters[0] = 0;  // every CTA has stopped claiming: re-arm the queue for the next launch
+    P.counters[1] = 0;
+  }
+  if (warp == 1) {
+    tc::fence_after();
+    tc::tmem_dealloc(0, 512);
+  }
+}
+
+}  // namespace
+
+// v3 launch on rotated q/k and the caller's v; tcount / tlist / hcount from tile_map2.
+mv_status prefill_tc3_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
+                             const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
+                             void* d_out, int32_t out_dtype, const int32_t* hcount, const int32_t* tlist,
+                             int32_t stride, cudaStream_t st) {
+  if (max_depth > 8) return fail(MV_ERR_INVALID_ARGUMENT, "prefill: max_depth > 8");
+  CUtensorMap mq, mk, mvv;
+  if (mv_status e = tc::make_rows_map(&mq, q_rot, n, q_heads, kT3)) return e;
+  if (mv_status e = tc::make_rows_map(&mk, k_rot, n, kv_heads, kT3)) return e;
+  if (mv_status e = tc::make_rows_map(&mvv, v, n, kv_heads, kT3)) return e;
+  Tc3Params T;
+  T.excl = d_excl;
+  T.hcount = hcount;
+  T.tlist = tlist;
+  T.out = d_out;
+  T.out_f32 = out_dtype == 1;
+  T.n = n;
+  T.hq = q_heads;
+  T.hkv = kv_heads;
+  T.D = max_depth;
+  T.n_qt = (n + kT3 - 1) / kT3;
+  T.stride = stride;
+  T.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
+  T.n_items = T.n_qt * q_heads;
+  static int* d_counters = nullptr;
+  static int num_sms = 0;
+  if (!d_counters) {
+    MV_CUDA_TRY(cudaMalloc(&d_counters, 2 * sizeof(int)));
+    MV_CUDA_TRY(cudaMemsetAsync(d_counters, 0, 2 * sizeof(int), st));
+    int dev = 0;
+    MV_CUDA_TRY(cudaGetDevice(&dev));
+    MV_CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    MV_CUDA_TRY(cudaFuncSetAttribute(prefill_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem3));
+  }
+  T.counters = d_counters;
+  T.trace = nullptr;
+  if (MV_PF_TRACE) {
+    static unsigned long long* d_trace = nullptr;
+    const size_t tb = kTrace3 * 8 * sizeof(unsigned long long);
+    if (!d_trace) MV_CUDA_TRY(cudaMalloc(&d_trace, tb));
+    if (const char* f = getenv("MV_PREFILL_TRACE")) {  // the previous launch's timeline
+      std::vector<unsigned long long> h(kTrace3 * 8);
+      MV_CUDA_TRY(cudaMemcpy(h.data(), d_trace, tb, cudaMemcpyDeviceToHost));
+      if (FILE* fp = fopen(f, "wb")) { fwrite(h.data(), 8, h.size(), fp); fclose(fp); }
+    }
+    MV_CUDA_TRY(cudaMemsetAsync(d_trace, 0, tb, st));
+    T.trace = d_trace;
+  }
+  prefill_tc3_kernel<<<std::min(T.n_items, num_sms), kThreads3, kSmem3, st>>>(mq, mk, mvv, T);
+  MV_LAUNCH_CHECK();
+  return MV_OK;
+}
+
+}  // namespace mv

@@ -389,7 +389,8 @@ constexpr int kTm2Threads = 1024;  // 4 groups of 256 (one thread per row) share
 
 __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* __restrict__ excl, int n, int D,
                                                                 int32_t* __restrict__ count,
-                                                                int32_t* __restrict__ list, int stride) {
+                                                                int32_t* __restrict__ list, int stride,
+                                                                int32_t* __restrict__ hcount) {
   const int qp = blockIdx.x;
   const int tile = 128;
   const int r = threadIdx.x & 255, grp = threadIdx.x >> 8;
@@ -408,7 +409,7 @@ __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* _
   __shared__ uint8_t s_e[8][kTm2Chunk], s_f[8][kTm2Chunk];
   __shared__ int s_warp_sum[kTm2Threads / 32];
   const int last_kt = min((qp * 256 + 255) / tile, (n - 1) / tile);
-  int written = 0;
+  int written = 0, nA = 0, nB = 0;
   for (int kt0 = 0; kt0 <= last_kt; kt0 += kTm2Chunk) {
     const int kt1 = min(last_kt + 1, kt0 + kTm2Chunk);
     for (int kt = kt0 + grp; kt < kt1; kt += kTm2Threads / 256) {
@@ -453,6 +454,9 @@ __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* _
       }
       if (st[0] || st[1]) ent = kt | (st[0] << 20) | (st[1] << 22);
     }
+    // per-half processed counts (k tiles whose status for that 128-row half is not 0)
+    nA += __syncthreads_count(ent >= 0 && ((ent >> 20) & 3) != 0);
+    nB += __syncthreads_count(ent >= 0 && ((ent >> 22) & 3) != 0);
     // ordered compaction
     const unsigned keep = __ballot_sync(0xffffffffu, ent >= 0);
     if (lane == 0) s_warp_sum[warp] = __popc(keep);
@@ -467,7 +471,13 @@ __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* _
     written += total;
     __syncthreads();  // s_e / s_f / s_warp_sum reused by the next pass
   }
-  if (threadIdx.x == 0) count[qp] = written;
+  if (threadIdx.x == 0) {
+    count[qp] = written;
+    if (hcount) {
+      hcount[2 * qp] = nA;
+      hcount[2 * qp + 1] = nB;
+    }
+  }
 }
 }  // namespace
 }  // namespace mv
@@ -527,9 +537,9 @@ extern "C" mv_status mv_tile_map(const int32_t* d_excl, int32_t n, int32_t max_d
 
 namespace mv {
 mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
-                    int32_t stride, cudaStream_t stream) {
+                    int32_t stride, cudaStream_t stream, int32_t* d_hcount) {
   const int n_qp = (n + 255) / 256;
-  tile_map2_kernel<<<n_qp, kTm2Threads, 0, stream>>>(d_excl, n, max_depth, d_count, d_list, stride);
+  tile_map2_kernel<<<n_qp, kTm2Threads, 0, stream>>>(d_excl, n, max_depth, d_count, d_list, stride, d_hcount);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }
