@@ -97,6 +97,13 @@ __device__ __forceinline__ void mbar_arrive_n(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 // non-blocking probe: has the phase with this parity completed?
+// 1024-byte-aligned view of dynamic shared memory that keeps the shared address space: pointer
+// arithmetic on the __shared__ array itself, so data accesses compile to LDS / STS (an integer
+// round trip through uintptr_t made them generic LD / ST).
+__device__ __forceinline__ uint8_t* smem_align1024(uint8_t* raw) {
+  return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u);
+}
+
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(

@@ -328,7 +328,7 @@ __device__ __forceinline__ void issue_q_copy(uint64_t qd) {  // Q tile smem -> T
 template <bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodeParams P) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* ring = smem + kOffRing;
   WorkItem* s_item = reinterpret_cast<WorkItem*>(smem + kOffItem);
   WorkItem* s_ep = reinterpret_cast<WorkItem*>(smem + kOffEp);

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     prefill_tc2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, Tc2Params P) {
   extern __shared__ uint8_t smem_raw2[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw2) + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_align1024(smem_raw2);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar2);
   uint64_t* q_full = bars;                 // Q tiles of the current item landed (tx)
   uint64_t* q_empty = q_full + 1;          // MMA commit: the item's last Q.K^T done -> next Q may land

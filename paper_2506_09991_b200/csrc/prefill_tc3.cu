@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
     prefill_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, Tc3Params P) {
   extern __shared__ uint8_t smem_raw3[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw3) + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = smem_align1024(smem_raw3);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar3);
   uint64_t* q_full = bars;               // Q tile landed (tx)
   uint64_t* q_empty = q_full + 1;        // MMA commit after the item's last Q.K^T
@@ -311,6 +311,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
         const bool tr = r == 0;
         if (tr) PF3_TRACE(g, c ? 6 : 2);
         tc::fence_after();
+#if MV_PF_NOSOFT
+        if (true) { mbar_arrive(&p_full[g % kSB]); continue; }
+#endif
         float v[64];
         tc::tmem_ld32(lane_base + s_col + c * 64, v);
         tc::tmem_ld32(lane_base + s_col + c * 64 + 32, v + 32);
