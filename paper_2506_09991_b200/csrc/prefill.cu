@@ -27,6 +27,9 @@ constexpr int kPfThreads = 128;  // 4 warps x 16 rows
 constexpr int kMaxD = 8;         // exclusion intervals per row supported by the kernel
 constexpr float kLazyRescalePf = 8.f;  // log2-domain headroom before O is rescaled
 
+// One thread per (row, 16-byte chunk): the 4 (cos, sin) pairs of the chunk depend only on the
+// row's position, so they are computed once and applied to the chunk in every q and k head
+// (hq + hkv heads, 256 B apart; a warp covers two rows' 512 contiguous bytes per head).
 __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __restrict__ q,
                                                       const __nv_bfloat16* __restrict__ k,
                                                       const int32_t* __restrict__ pos, int n, int hq, int hkv,
@@ -34,27 +37,37 @@ __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __res
                                                       __nv_bfloat16* __restrict__ k_rot) {
   __shared__ double s_inv[kHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
-  const int64_t nq = (int64_t)n * hq * 16, nk = (int64_t)n * hkv * 16;
-  // grid-stride over 16-byte chunks (4 interleaved pairs each)
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < nq + nk; x += (int64_t)gridDim.x * blockDim.x) {
-    const bool isq = x < nq;
-    const int64_t y = isq ? x : x - nq;
-    const int c = (int)(y & 15);
-    const int row = (int)((y >> 4) / (isq ? hq : hkv));
-    const __nv_bfloat16* src = isq ? q : k;
-    __nv_bfloat16* dst = isq ? q_rot : k_rot;
-    uint4 v = __ldg(reinterpret_cast<const uint4*>(src + y * 8));
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (x >= (int64_t)n * 16) return;
+  const int row = (int)(x >> 4), c = (int)(x & 15);
+  const int p = __ldg(pos + row);
+  float cs[4], sn[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) rope_cs(p, inv[c * 4 + j], cs[j], sn[j]);
+  auto rot = [&](uint4 v) {
     __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
-    const int p = __ldg(pos + row);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      float cs, sn;
-      rope_cs(p, inv[c * 4 + j], cs, sn);
       const float2 ab = __bfloat1622float2(h2[j]);
-      h2[j] = __floats2bfloat162_rn(ab.x * cs - ab.y * sn, ab.x * sn + ab.y * cs);
+      h2[j] = __floats2bfloat162_rn(ab.x * cs[j] - ab.y * sn[j], ab.x * sn[j] + ab.y * cs[j]);
     }
-    *reinterpret_cast<uint4*>(dst + y * 8) = v;
+    return v;
+  };
+  const uint4* qs = reinterpret_cast<const uint4*>(q + (size_t)row * hq * kHeadDim) + c;
+  uint4* qd = reinterpret_cast<uint4*>(q_rot + (size_t)row * hq * kHeadDim) + c;
+  int h = 0;
+  for (; h + 4 <= hq; h += 4) {  // 4 independent 16-byte loads in flight per thread
+    uint4 v0 = __ldg(qs + (h + 0) * 16), v1 = __ldg(qs + (h + 1) * 16), v2 = __ldg(qs + (h + 2) * 16),
+          v3 = __ldg(qs + (h + 3) * 16);
+    qd[(h + 0) * 16] = rot(v0);
+    qd[(h + 1) * 16] = rot(v1);
+    qd[(h + 2) * 16] = rot(v2);
+    qd[(h + 3) * 16] = rot(v3);
   }
+  for (; h < hq; ++h) qd[h * 16] = rot(__ldg(qs + h * 16));
+  const uint4* ks = reinterpret_cast<const uint4*>(k + (size_t)row * hkv * kHeadDim) + c;
+  uint4* kd = reinterpret_cast<uint4*>(k_rot + (size_t)row * hkv * kHeadDim) + c;
+  for (h = 0; h < hkv; ++h) kd[h * 16] = rot(__ldg(ks + h * 16));
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
@@ -316,20 +329,34 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
   unsigned long long* vis = reinterpret_cast<unsigned long long*>(ws);
 
   const RopeTable rt = make_rope_table(rope_base > 0 ? rope_base : 10000.0);
-  const int64_t chunks = (int64_t)n * (q_heads + kv_heads) * 16;
-  rope_qk_kernel<<<(unsigned)std::min<int64_t>((chunks + 255) / 256, 148 * 8), 256, 0, st>>>(
+  const bool v3 = !getenv("MV_PREFILL_V0") && !getenv("MV_PREFILL_TC2");
+  const int n_qp = (n + 255) / 256, stride = (n + 127) / 128;
+  int32_t* hcount = tcount + n_qp;  // per-128-row-tile processed counts after the n_qp pair counts
+  // The tile map (latency-bound, n/256 CTAs) runs on a side stream next to the HBM-bound RoPE
+  // pass; the main stream joins it before the attention kernel.
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (v3 && !side) {
+    MV_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    MV_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    MV_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  if (v3) {
+    MV_CUDA_TRY(cudaEventRecord(ev_fork, st));
+    MV_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
+    if (mv_status e = tile_map2(d_excl, n, max_depth, tcount, tlist, stride, side, hcount)) return e;
+    MV_CUDA_TRY(cudaEventRecord(ev_join, side));
+  }
+  rope_qk_kernel<<<(unsigned)(((int64_t)n * 16 + 255) / 256), 256, 0, st>>>(
       (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_k, d_positions, n, q_heads, kv_heads, rt, q_rot, k_rot);
   MV_LAUNCH_CHECK();
-  MV_CUDA_TRY(cudaMemsetAsync(vis, 0, 8, st));
 
-  if (!getenv("MV_PREFILL_V0") && !getenv("MV_PREFILL_TC2")) {  // tcgen05 v3 (prefill_tc3.cu)
-    // pair lists + per-128-row-tile processed counts (hcount after the n_qp pair counts)
-    const int n_qp = (n + 255) / 256, stride = (n + 127) / 128;
-    int32_t* hcount = tcount + n_qp;
-    if (mv_status e = tile_map2(d_excl, n, max_depth, tcount, tlist, stride, st, hcount)) return e;
+  if (v3) {  // tcgen05 v3 (prefill_tc3.cu)
+    MV_CUDA_TRY(cudaStreamWaitEvent(st, ev_join, 0));
     return prefill_tc3_launch(q_rot, k_rot, (const __nv_bfloat16*)d_v, d_excl, max_depth, n, q_heads, kv_heads, d_out,
                               out_dtype, hcount, tlist, stride, st);
   }
+  MV_CUDA_TRY(cudaMemsetAsync(vis, 0, 8, st));
   if (!getenv("MV_PREFILL_V0"))  // tcgen05 v2 (prefill_tc.cu) and v0 kept for A/B diagnostics
     return prefill_tc2_launch(q_rot, k_rot, (const __nv_bfloat16*)d_v, d_excl, max_depth, n, q_heads, kv_heads, d_out,
                               out_dtype, tcount, tlist, st);
