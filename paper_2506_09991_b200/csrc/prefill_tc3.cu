@@ -50,9 +50,15 @@ constexpr int kSmem3 = kOffX3 + 2 * 2 * 128 * 4 + 1024;
 constexpr uint32_t kIdQK3 = tc::idesc_bf16(128, 128, 0, 0);
 constexpr uint32_t kIdPV3 = tc::idesc_bf16(128, 128, 0, 1);
 constexpr float kLazy3 = 8.f;
-// TMEM columns: three S buffers (S(g) in buffer g % 3) and one O
-constexpr int kSB = 3;
-constexpr uint32_t kS0 = 0, kO0 = 384;
+#ifndef MV_PF_QTMEM
+#define MV_PF_QTMEM 0
+#endif
+// TMEM columns: three S buffers (S(g) in buffer g % 3) and one O; or, with Q in TMEM (A operand
+// of Q.K^T read from TMEM: halves the smem operand traffic of the SS form), two S buffers, O and
+// the Q tile (64 packed columns).
+constexpr bool kQT = MV_PF_QTMEM != 0;
+constexpr int kSB = kQT ? 2 : 3;
+constexpr uint32_t kS0 = 0, kO0 = kSB * 128, kQ0 = kO0 + 128;
 
 struct Tc3Params {
   const int32_t* excl;
@@ -86,7 +92,8 @@ __device__ __forceinline__ void qk3(uint64_t qd, uint64_t kd) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint64_t off = (uint64_t)(((k >> 2) * kHalf3 + (k & 3) * 32) >> 4);
-    tc::mma_ss(kS0 + B * 128, qd + off, kd + off, kIdQK3, k > 0 ? 1u : 0u);
+    if (kQT) tc::mma_ts(kS0 + B * 128, kQ0 + k * 8, kd + off, kIdQK3, k > 0 ? 1u : 0u);
+    else tc::mma_ss(kS0 + B * 128, qd + off, kd + off, kIdQK3, k > 0 ? 1u : 0u);
   }
 }
 template <int B>
@@ -258,7 +265,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
         const int b = gg % kSB;
         if (b == 0) qk3<0>(qd, kd);
         else if (b == 1) qk3<1>(qd, kd);
-        else qk3<2>(qd, kd);
+        else if (kSB > 2) qk3<2 % kSB>(qd, kd);
         tc::mma_commit(&s_full[b]);
         tc::mma_commit(&k_empty[gg % kKSt3]);
       };
@@ -271,8 +278,15 @@ __global__ void __launch_bounds__(kThreads3, 1)
         const int m = it.m;
         const uint64_t qd = qd0;
         mbar_wait(q_full, i & 1);
+        if (kQT) {  // Q tile smem -> TMEM (in order behind the previous item's Q.K^T), smem freed
+          tc::fence_after();
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            tc::cp_128x256b(kQ0 + k * 8, qd + (uint64_t)(((k >> 2) * kHalf3 + (k & 3) * 32) >> 4));
+          tc::mma_commit(q_empty);
+        }
         for (int u = 0; u < kSB && u < m; ++u) qk(qd, g + u);
-        if (m <= kSB) tc::mma_commit(q_empty);
+        if (!kQT && m <= kSB) tc::mma_commit(q_empty);
         for (int j = 0; j < m; ++j, ++g) {
           mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
           mbar_wait(&p_full[g % kSB], (g / kSB) & 1);
@@ -283,11 +297,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
           const int b = g % kSB;
           if (b == 0) pv3<0>(vd, j == 0);
           else if (b == 1) pv3<1>(vd, j == 0);
-          else pv3<2>(vd, j == 0);
+          else if (kSB > 2) pv3<2 % kSB>(vd, j == 0);
           tc::mma_commit(&v_empty[g % kVSt3]);
           if (j + kSB < m) {
             qk(qd, g + kSB);  // S buffer g % 3 again: in order behind P.V(g)
-            if (j + kSB + 1 == m) tc::mma_commit(q_empty);
+            if (!kQT && j + kSB + 1 == m) tc::mma_commit(q_empty);
           }
           PF3_TRACE(g, 1);
         }
