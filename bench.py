@@ -234,10 +234,12 @@ def run_ours(args):
     torch.cuda.synchronize()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     att = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    pos_steps = [base_pos + (args.warmup + s) for s in range(args.steps)]  # inputs resident before timing
+    torch.cuda.synchronize()
     ev[0].record(stream)
     for s in range(args.steps):
         i = args.warmup + s
-        p = base_pos + i
+        p = pos_steps[s]
         st.append(handles, toks, p, 0, ks[i % 2], vs[i % 2])
         att[s][0].record(stream)
         mv.attention.decode(st, handles, qs[i % 2], p, out=out)

@@ -97,6 +97,12 @@ __device__ __forceinline__ void mbar_arrive_n(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 // non-blocking probe: has the phase with this parity completed?
+// Programmatic dependent launch (PDL): the dependent grid may be scheduled once every CTA of
+// this grid has called launch_dependents; pdl_wait blocks until the predecessor grid completed
+// and its memory is visible (a no-op when the launch carried no programmatic dependency).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 1024-byte-aligned view of dynamic shared memory that keeps the shared address space: pointer
 // arithmetic on the __shared__ array itself, so data accesses compile to LDS / STS (an integer
 // round trip through uintptr_t made them generic LD / ST).

@@ -383,6 +383,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
   // compile-time base keeps every TMEM operand uniform (no per-MMA R2UR waterfall in the issuer).
   constexpr uint32_t tmem = 0;
   if (*tmem_slot != tmem) __trap();
+  // programmatic launch: the prologue above overlapped rope_q_tile_kernel; its Q tile and the
+  // work-counter reset are visible after this wait
+  pdl_wait();
+  pdl_launch_dependents();
 
   if (warp == kWarpStage) {
     // ---------------- stager: claim, entries, Q rows ----------------
@@ -692,6 +696,7 @@ __global__ void combine_kernel(const float* __restrict__ part_o, const float2* _
                                const int32_t* __restrict__ multi, int n_multi, const int32_t* __restrict__ slot_ptr,
                                const int32_t* __restrict__ slot_idx, int q_heads, void* __restrict__ out,
                                int out_f32) {
+  pdl_wait();  // programmatic launch behind decode_tc_kernel: its partials are visible after this
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (wid >= n_multi * q_heads) return;
   const int b = multi[wid / q_heads], h = wid % q_heads;
@@ -732,6 +737,7 @@ __global__ void combine_kernel(const float* __restrict__ part_o, const float2* _
 __global__ void rope_q_tile_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pos, int n,
                                    int kv_heads, int gqa, int R, const RopeTable rt, __nv_bfloat16* __restrict__ tile,
                                    int* counter) {
+  pdl_launch_dependents();  // decode_tc may start its prologue (every CTA of this grid is running)
   __shared__ double s_inv[kHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1120,13 +1126,29 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     MV_CUDA_TRY(cudaMemsetAsync(pc.d_trace, 0, sizeof(unsigned long long) * trace_words, stream));
     P.trace = pc.d_trace;
   }
-  if (P.trace) decode_tc_kernel<true><<<grid, kThreads, kSmem, stream>>>(P);
-  else decode_tc_kernel<false><<<grid, kThreads, kSmem, stream>>>(P);
+  // decode_tc and combine are launched programmatically dependent on the kernel before them
+  // (PDL): their launch latency and prologue overlap the predecessor's tail
+  cudaLaunchAttribute pdl[1];
+  pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(kThreads);
+  lc.dynamicSmemBytes = kSmem;
+  lc.stream = stream;
+  lc.attrs = pdl;
+  lc.numAttrs = 1;
+  if (P.trace) MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel<true>, P));
+  else MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel<false>, P));
   MV_LAUNCH_CHECK();
   if (!pc.multi.empty()) {
     const int warps = (int)pc.multi.size() * q_heads;
-    combine_kernel<<<(warps + 7) / 8, 256, 0, stream>>>(pc.d_part_o, pc.d_part_ml, pc.d_multi, (int)pc.multi.size(),
-                                                        pc.d_slot_ptr, pc.d_slot_idx, q_heads, d_out, out_dtype == 1);
+    lc.gridDim = dim3((warps + 7) / 8);
+    lc.blockDim = dim3(256);
+    lc.dynamicSmemBytes = 0;
+    MV_CUDA_TRY(cudaLaunchKernelEx(&lc, combine_kernel, (const float*)pc.d_part_o, (const float2*)pc.d_part_ml,
+                                   (const int32_t*)pc.d_multi, (int)pc.multi.size(), (const int32_t*)pc.d_slot_ptr,
+                                   (const int32_t*)pc.d_slot_idx, q_heads, d_out, (int)(out_dtype == 1)));
     MV_LAUNCH_CHECK();
   }
   if (trace_path) {
