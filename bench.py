@@ -31,6 +31,11 @@ sys.path.insert(0, REPO)
 
 HQ, HKV, D = 40, 8, 128
 PREFIX, BRANCHES, BRANCH_LEN = 4096, 8, 1024
+# --workload: c2 = configs[1] (the metric's config, R requests per GPU, weak scaling);
+# c4 = configs[3] (64 requests x 32 branches, 16K shared prefix + 32 x 512 = 32K unique tokens per
+# request, sharded by request across the GPUs: strong scaling)
+WORKLOADS = {"c2": dict(prefix=4096, branches=8, branch_len=1024),
+             "c4": dict(prefix=16384, branches=32, branch_len=512, total_requests=64)}
 METRIC = "branch-parallel decode tokens/s/GPU; attention HBM GB/s vs 8 TB/s roofline"
 
 
@@ -39,7 +44,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--requests", type=int, default=16, help="requests per GPU")
+    ap.add_argument("--requests", type=int, default=16, help="requests per GPU (c2)")
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -161,11 +167,17 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def build_workload(mv, torch, R, dev, first_request=0):
-    """R requests: root prefix, fork into 8 branches, 1023 private tokens each (positions shared start).
-    Request r's data is seeded by its global id, so every rank holds distinct requests."""
-    pages = R * (PREFIX // 16 + BRANCHES * (BRANCH_LEN // 16 + 4)) + 1024
-    st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=HKV)
+def build_workload(mv, torch, R, dev, first_request=0, prefix=PREFIX, branches_per_req=BRANCHES,
+                   branch_len=BRANCH_LEN, steps_total=0):
+    """R requests: root prefix, fork into B branches, branch_len - 1 private tokens each (positions
+    shared start).  Request r's data is seeded by its global id, so every rank holds distinct
+    requests.  The pool has room for steps_total appended tokens per branch."""
+    PREFIX, BRANCHES, BRANCH_LEN = prefix, branches_per_req, branch_len  # noqa: N806
+    pages = R * (PREFIX // 16 + 1 + BRANCHES * ((BRANCH_LEN + steps_total) // 16 + 3)) + 1024
+    # page-table arena: every branch holds its own span list (prefix entries + private tail), with
+    # the store's capacity doubling on growth
+    table = 2 * R * (BRANCHES + 1) * (PREFIX // 16 + (BRANCH_LEN + steps_total) // 16 + 8) + 65536
+    st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=HKV, table_entries=table)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + first_request)
 
@@ -203,9 +215,14 @@ def run_ours(args):
 
     from paper_2506_09991_b200.shard import shard_requests, max_over_ranks
     # weak scaling: R requests per GPU, sharded by request (no collective in attention)
-    shard = shard_requests(args.requests * world, HKV, world, rank)
+    wl = WORKLOADS[args.workload]
+    total = wl.get("total_requests", args.requests * world)
+    shard = shard_requests(total, HKV, world, rank)
     R = len(shard.requests)
-    st, handles, pos0, rnd = build_workload(mv, torch, R, dev, shard.requests[0])
+    steps_total = args.warmup + args.steps
+    steps_total += max(3, args.steps // 2)  # the e2e leg appends too
+    st, handles, pos0, rnd = build_workload(mv, torch, R, dev, shard.requests[0], wl["prefix"], wl["branches"],
+                                            wl["branch_len"], steps_total)
     n = len(handles)
     steps_total = args.warmup + args.steps
     # per-step inputs (device resident for `value`)
@@ -307,13 +324,20 @@ def run_ours(args):
         pass
 
     if rank == 0:
-        cpu = cpu_baseline(args.cpu_seconds) if world == 1 else None
+        cpu = cpu_baseline(args.cpu_seconds) if world == 1 and args.workload == "c2" else None
+        if args.workload == "c4":
+            wl_text = ("configs[3]: 64 requests x 32 branches sharded by request over the GPUs, 40q/8kv heads, "
+                       "d128, bf16, 16K shared prefix + 32 x 512 branch tokens (32K unique per request, +1 per "
+                       "branch per step), KV page 16")
+        else:
+            wl_text = ("configs[1] x R requests per GPU: 40q/8kv heads, d128, bf16, 4K shared Map prefix, 8 "
+                       "branches x 1K tokens (+1 per step), KV page 16")
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if args.workload == "c4" else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "configs[1] x R requests per GPU: 40q/8kv heads, d128, bf16, 4K shared Map "
-                                   "prefix, 8 branches x 1K tokens (+1 per step), KV page 16",
+            "config": {"workload": wl_text,
                        "requests_per_gpu": R, "branches_per_gpu": n, "l2": "inputs 0.8+ GB > L2 (no flush)",
                        "mean_kv_tokens_per_step": kv_tokens,
                        "step": "append 1 token K/V per branch (RoPE fused) + cascade decode attention"},

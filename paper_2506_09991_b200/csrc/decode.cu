@@ -59,8 +59,8 @@ constexpr int kBlkPages = 4;                                // pages per block (
 constexpr int kBlkCols = kBlkPages * kPageTokens;           // 64 S columns per block
 constexpr int kKSlots = 5, kVSlots = 6;                     // K / V rings, one block (4 pages) per slot
 constexpr int kSlotBytes = kBlkPages * kPageBytes;          // 4 page-head blocks as stored (16 KiB)
-constexpr int kMaxChunk = 64;                               // split-KV chunk target (pages)
-constexpr int kMaxEntries = 80;                             // pages per work unit (a tail chunk grows in place)
+constexpr int kMaxChunk = 256;                              // split-KV chunk cap (pages); the planner halves it down to 64-16 when work is scarce
+constexpr int kMaxEntries = kMaxChunk + 16;                 // pages per work unit (a tail chunk grows in place)
 constexpr int kMaxMem = 16;                                 // handles per work unit
 constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dims] bf16
 constexpr int kQBytes = 2 * kQHalf;
@@ -1016,7 +1016,9 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     bool incr = true;
     for (int b = 0; b < n && incr; ++b) {
       if (sig[3 * b + 1] != pc.sig[3 * b + 1] || sig[3 * b + 2] != pc.sig[3 * b + 2] || sig[3 * b] < pc.sig[3 * b]) incr = false;
-      else if (sig[3 * b] != pc.sig[3 * b] && (pc.tail_item[b] < 0 || sig[3 * b] - pc.tail_c0[b] > kMaxEntries)) incr = false;
+      else if (sig[3 * b] != pc.sig[3 * b] &&
+               (pc.tail_item[b] < 0 || sig[3 * b] - pc.tail_c0[b] > std::min(kMaxEntries, pc.info.chunks + 16)))
+        incr = false;  // a tail chunk may outgrow the plan's chunk size by 16 pages before a re-plan
     }
     if (getenv("MV_DECODE_LOG")) fprintf(stderr, "[mv decode] plan %s\n", incr ? "grow tail in place" : "rebuild");
     if (incr) {
