@@ -257,3 +257,117 @@ def test_reduce_merge_stress_then_decode(mv):
     st.release(cur)
     s = st.stats()
     assert s.live_handles == 0 and s.total_refcount == 0 and s.free_pages == 2048
+
+
+def test_c4_full_scale_sampled(mv):
+    """BASELINE configs[3] at full size on one GPU: 64 requests x 32 branches, 16K shared prefix +
+    32 x 512 branch tokens (32K unique per request, 8.6 GB of bf16 K/V), one decode step for all
+    2,048 branches.  Size-independent checks on the whole batch (plan reads every unique token
+    once per member group, finite outputs), oracle parity on a seeded sample of branches."""
+    hq, hkv, R, B, prefix, blen = 40, 8, 64, 32, 16384, 512
+    pages = R * (prefix // 16 + 1 + B * (blen // 16 + 3)) + 1024
+    table = 2 * R * (B + 1) * (prefix // 16 + blen // 16 + 8) + 65536
+    st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=hkv, table_entries=table)
+    sample = {3: [0, 17, 31], 50: [5, 30]}  # request -> branches checked against the oracle
+    kept = {}
+    handles, qpos = [], []
+    for r in range(R):
+        g = torch.Generator(device="cuda")
+        g.manual_seed(4242 + r)
+        rnd = lambda *s: (torch.rand(*s, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)  # noqa: E731
+        kp, vp = rnd(prefix, hkv, 128), rnd(prefix, hkv, 128)
+        root = st.create()
+        st.append_many(root, torch.full((prefix,), 11, dtype=torch.int32, device="cuda"),
+                       torch.arange(prefix, dtype=torch.int32, device="cuda"), 0, kp, vp)
+        kids = st.fork(root, B)
+        st.release(root)
+        for bi, h in enumerate(kids):
+            kb, vb = rnd(blen - 1, hkv, 128), rnd(blen - 1, hkv, 128)
+            st.append_many(h, torch.full((blen - 1,), 12, dtype=torch.int32, device="cuda"),
+                           torch.arange(prefix, prefix + blen - 1, dtype=torch.int32, device="cuda"), 0, kb, vb)
+            if bi in sample.get(r, []):
+                kept[(r, bi)] = (kp.cpu(), vp.cpu(), kb.cpu(), vb.cpu(), len(handles))
+            handles.append(h)
+            qpos.append(prefix + blen - 1)
+    n = len(handles)
+    knew, vnew, q = sym_bf16(31, (n, hkv, 128)), sym_bf16(32, (n, hkv, 128)), sym_bf16(33, (n, hq, 128))
+    pos = torch.tensor(qpos, dtype=torch.int32)
+    st.append(handles, torch.full((n,), 13, dtype=torch.int32, device="cuda"), pos.cuda(), 0, knew.cuda(), vnew.cuda())
+    out = mv.attention.decode(st, handles, q.cuda(), pos.cuda(), out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    info = st.plan_info()
+    assert info["unique_kv_tokens"] == R * (prefix + B * blen)
+    o = out.cpu().numpy()
+    assert np.isfinite(o).all()
+    for (r, bi), (kp, vp, kb, vb, idx) in kept.items():
+        K = np.concatenate([bf16_to_f64(kp), bf16_to_f64(kb), bf16_to_f64(knew[idx:idx + 1])])
+        V = np.concatenate([bf16_to_f64(vp), bf16_to_f64(vb), bf16_to_f64(vnew[idx:idx + 1])])
+        P = np.concatenate([np.arange(prefix), np.arange(prefix, prefix + blen - 1), [qpos[idx]]]).astype(np.int32)
+        ref = oracle.attn_decode(oracle.rope(bf16_to_f64(q[idx:idx + 1]), pos[idx:idx + 1].numpy()), oracle.rope(K, P), V,
+                                 [list(range(len(P)))])
+        err = np.abs(o[idx:idx + 1] - ref).max()
+        assert err < TOL, ((r, bi), err)
+
+
+def test_c5_reduce_merge_full_scale(mv):
+    """BASELINE configs[4] at full size: 4,096-token prefix, 16 rounds of {fork 128; append 64
+    tokens per branch; zero-copy merge in ordinal order; append 16 Reduce tokens}, then decode
+    steps over the merged 135,424-token context.  Every fork / merge moves 0 KV bytes and
+    allocates no page; the final decode matches the oracle."""
+    hq, hkv, B, rounds, path, red, prefix = 40, 8, 128, 16, 64, 16, 4096
+    total = prefix + rounds * (B * path + red)
+    assert total == 135424
+    pages = total // 16 + rounds * B * 2 + 4096
+    # every fork gives each of the 128 children its own copy of the parent's span list (as the
+    # reference does, kvcache.cpp:245-252): ~2 x 128 x 8.5K entries in the last round
+    st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=hkv, table_entries=1 << 23)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(555)
+    ks, vs, ps = [], [], []
+
+    def add(h, n, pos0):
+        k = (torch.rand(n, hkv, 128, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+        v = (torch.rand(n, hkv, 128, generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+        p = torch.arange(pos0, pos0 + n, dtype=torch.int32, device="cuda")
+        st.append_many(h, torch.full((n,), 11, dtype=torch.int32, device="cuda"), p, 0, k, v)
+        ks.append(k)
+        vs.append(v)
+        ps.append(p)
+
+    cur = st.create()
+    add(cur, prefix, 0)
+    L = prefix
+    for _ in range(rounds):
+        kids = st.fork(cur, B)
+        assert st.stats().bytes_copied_on_last_op == 0
+        for k in kids:
+            add(k, path, L)  # siblings share their start position
+        free_before = st.stats().free_pages
+        m = st.merge(cur, kids)
+        s = st.stats()
+        assert s.bytes_copied_on_last_op == 0 and s.free_pages == free_before
+        for h in [cur] + kids:
+            st.release(h)
+        L += path
+        add(m, red, L)
+        L += red
+        cur = m
+    assert st.length(cur) == total
+    for step in range(4):
+        kn, vn = sym_bf16(8800 + step, (1, hkv, 128)), sym_bf16(8900 + step, (1, hkv, 128))
+        q = sym_bf16(9900 + step, (1, hq, 128))
+        pos = torch.tensor([L], dtype=torch.int32)
+        st.append([cur], torch.tensor([13], dtype=torch.int32, device="cuda"), pos.cuda(), 0, kn.cuda(), vn.cuda())
+        ks.append(kn.cuda())
+        vs.append(vn.cuda())
+        ps.append(pos.cuda())
+        out = mv.attention.decode(st, [cur], q.cuda(), pos.cuda(), out_dtype=torch.float32)
+        L += 1
+    K = bf16_to_f64(torch.cat(ks).cpu())
+    V = bf16_to_f64(torch.cat(vs).cpu())
+    P = torch.cat(ps).cpu().numpy()
+    ref = oracle.attn_decode(oracle.rope(bf16_to_f64(q), pos.numpy()), oracle.rope(K, P), V, [list(range(len(P)))])
+    assert np.abs(out.float().cpu().numpy() - ref).max() < TOL
+    st.release(cur)
+    s = st.stats()
+    assert s.live_handles == 0 and s.total_refcount == 0 and s.free_pages == pages
