@@ -15,6 +15,9 @@
 //                                    configs[0]); prints tokens/s
 //   refdrv decode <threads> <secs>   time the reference decode path (resolve_payloads + step)
 //                                    on the configs[1] shape; prints tokens/s
+//   refdrv c5 <rounds> <rec_bytes>   time RadixStore fork / extend / merge / release on the
+//                                    configs[4] protocol (prefix 4096; per round fork 128,
+//                                    64 tokens per branch, ordinal merge, 16 Reduce tokens)
 #include <chrono>
 #include <cinttypes>
 #include <cstdio>
@@ -602,6 +605,56 @@ int mode_decode_bench(int threads, double seconds) {
   return 0;
 }
 
+int mode_c5(int rounds, std::size_t rec) {
+  using clk = std::chrono::steady_clock;
+  kv::RadixStore store(rec, 1u << 20);
+  std::vector<std::byte> zeros(rec * 4096);
+  auto ids = [](std::size_t n, int base) {
+    std::vector<kv::TokenId> t(n);
+    for (std::size_t i = 0; i < n; ++i) t[i] = 10 + static_cast<int>((base + 7 * i) % 240);
+    return t;
+  };
+  auto us = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+  auto root = store.create();
+  auto cur = store.extend(root, ids(4096, 0), std::span<const std::byte>(zeros.data(), rec * 4096));
+  store.release(root);
+  double t_fork = 0, t_ext = 0, t_merge = 0, t_rel = 0, t_red = 0;
+  int n_ext = 0, n_rel = 0;
+  for (int r = 0; r < rounds; ++r) {
+    auto a = clk::now();
+    auto kids = store.fork(cur, 128);
+    auto b = clk::now();
+    t_fork += us(a, b);
+    std::vector<kv::SequenceHandle> ext;
+    for (int k = 0; k < 128; ++k) {
+      auto c = clk::now();
+      ext.push_back(store.extend(kids[k], ids(64, 1000 * (r + 1) + 13 * k), std::span<const std::byte>(zeros.data(), rec * 64)));
+      t_ext += us(c, clk::now());
+      ++n_ext;
+    }
+    auto d = clk::now();
+    auto m = store.merge(cur, ext);
+    auto e = clk::now();
+    t_merge += us(d, e);
+    auto f = clk::now();
+    store.release(cur);
+    for (auto& h : kids) store.release(h);
+    for (auto& h : ext) store.release(h);
+    t_rel += us(f, clk::now());
+    n_rel += 1 + 256;
+    auto g = clk::now();
+    auto nm = store.extend(m, ids(16, 7), std::span<const std::byte>(zeros.data(), rec * 16));
+    store.release(m);
+    t_red += us(g, clk::now());
+    cur = nm;
+  }
+  std::printf("{\"kind\":\"c5\",\"rounds\":%d,\"final_len\":%zu,\"fork128_us\":%.3f,\"extend64_us\":%.3f,"
+              "\"merge128_us\":%.3f,\"release_us\":%.3f,\"reduce_extend16_us\":%.3f}\n",
+              rounds, cur.length, t_fork / rounds, t_ext / n_ext, t_merge / rounds, t_rel / n_rel, t_red / rounds);
+  store.release(cur);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -616,6 +669,7 @@ int main(int argc, char** argv) {
   if (mode == "toy") return mode_toy();
   if (mode == "forced" && argc >= 5) return mode_forced_bench(std::stoi(argv[2]), std::stoi(argv[3]), std::stoi(argv[4]));
   if (mode == "decode" && argc >= 4) return mode_decode_bench(std::stoi(argv[2]), std::stod(argv[3]));
+  if (mode == "c5" && argc >= 4) return mode_c5(std::stoi(argv[2]), static_cast<std::size_t>(std::stoul(argv[3])));
   std::fprintf(stderr, "bad arguments\n");
   return 1;
 }
