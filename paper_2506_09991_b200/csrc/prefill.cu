@@ -55,19 +55,23 @@ __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __res
   };
   const uint4* qs = reinterpret_cast<const uint4*>(q + (size_t)row * hq * kHeadDim) + c;
   uint4* qd = reinterpret_cast<uint4*>(q_rot + (size_t)row * hq * kHeadDim) + c;
-  int h = 0;
-  for (; h + 4 <= hq; h += 4) {  // 4 independent 16-byte loads in flight per thread
-    uint4 v0 = __ldg(qs + (h + 0) * 16), v1 = __ldg(qs + (h + 1) * 16), v2 = __ldg(qs + (h + 2) * 16),
-          v3 = __ldg(qs + (h + 3) * 16);
-    qd[(h + 0) * 16] = rot(v0);
-    qd[(h + 1) * 16] = rot(v1);
-    qd[(h + 2) * 16] = rot(v2);
-    qd[(h + 3) * 16] = rot(v3);
-  }
-  for (; h < hq; ++h) qd[h * 16] = rot(__ldg(qs + h * 16));
+  // q heads then k heads as one sequence of 16-byte chunks, 8 independent loads in flight
   const uint4* ks = reinterpret_cast<const uint4*>(k + (size_t)row * hkv * kHeadDim) + c;
   uint4* kd = reinterpret_cast<uint4*>(k_rot + (size_t)row * hkv * kHeadDim) + c;
-  for (h = 0; h < hkv; ++h) kd[h * 16] = rot(__ldg(ks + h * 16));
+  const int nh = hq + hkv;
+  for (int h0 = 0; h0 < nh; h0 += 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int h = h0 + u;
+      if (h < nh) v[u] = __ldg(h < hq ? qs + h * 16 : ks + (h - hq) * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int h = h0 + u;
+      if (h < nh) *(h < hq ? qd + h * 16 : kd + (h - hq) * 16) = rot(v[u]);
+    }
+  }
 }
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
