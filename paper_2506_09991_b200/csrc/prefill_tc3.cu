@@ -45,7 +45,7 @@ constexpr int kOffQ3 = 0;  // one Q tile: the next item's loads once this item's
 constexpr int kOffK3 = kOffQ3 + kTile3;
 constexpr int kOffV3 = kOffK3 + kKSt3 * kTile3;
 constexpr int kOffBar3 = kOffV3 + kVSt3 * kTile3;
-constexpr int kOffX3 = kOffBar3 + 256;  // row max / sum exchange: [2 parity][2 WG][128 rows] f32
+constexpr int kOffX3 = kOffBar3 + 512;  // row max / sum exchange: [2 parity][2 WG][128 rows] f32
 constexpr int kSmem3 = kOffX3 + 2 * 2 * 128 * 4 + 1024;
 constexpr uint32_t kIdQK3 = tc::idesc_bf16(128, 128, 0, 0);
 constexpr uint32_t kIdPV3 = tc::idesc_bf16(128, 128, 0, 1);
@@ -85,6 +85,7 @@ constexpr int kTrace3 = 1024;
 
 struct __align__(16) Item3 {
   int t, h, m, valid;
+  int e0, pad0, pad1, pad2;  // e0: first raw entry of the tile's pair list (read ahead by the scheduler)
 };
 
 template <int B>
@@ -192,18 +193,27 @@ __global__ void __launch_bounds__(kThreads3, 1)
       tc::tma_prefetch_desc(&map_q);
       tc::tma_prefetch_desc(&map_k);
       int gk = 0;
-      for (int i = 0;; ++i) {
-        const int buf = i & 1;
-        if (i >= 2) mbar_wait(&slot_empty[buf], ((i >> 1) - 1) & 1);
+      // the next item is claimed (and its count / first list entry loaded) one item ahead, so
+      // the queue atomic and the two global loads overlap this item's K loads
+      auto claim = [&](Item3& it) {
         const int w = atomicAdd(&P.counters[0], 1);
-        Item3 it;
         it.valid = w < P.n_items;
         it.t = it.valid ? P.n_qt - 1 - w / P.hq : 0;
         it.h = it.valid ? w % P.hq : 0;
         it.m = it.valid ? P.hcount[it.t] : 0;
+        it.e0 = it.valid ? P.tlist[(size_t)(it.t >> 1) * P.stride] : 0;
+        it.pad0 = it.pad1 = it.pad2 = 0;
+      };
+      Item3 nxt;
+      claim(nxt);
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        if (i >= 2) mbar_wait(&slot_empty[buf], ((i >> 1) - 1) & 1);
+        const Item3 it = nxt;
         s_item[buf] = it;
         mbar_arrive(&item_full[buf]);
         if (!it.valid) break;
+        claim(nxt);
         if (i >= 1) mbar_wait(q_empty, (i - 1) & 1);
         mbar_arrive_expect_tx(q_full, kTile3);
         tc::tma_load_3d(smem + kOffQ3, &map_q, 0, it.h, it.t * kT3, q_full);
@@ -325,6 +335,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
       if (!it.valid) break;
       const int i = it.t * kT3 + r;  // sequence row
       const int2* exr = reinterpret_cast<const int2*>(P.excl) + (size_t)min(i, P.n - 1) * P.D;
+      // the row's exclusion intervals, in registers for the whole item (partial tiles only use them)
+      int2 exv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) exv[q] = q < P.D ? __ldg(exr + q) : make_int2(0, 0);
       const int32_t* lst = P.tlist + (size_t)(it.t >> 1) * P.stride;
       const int sh = 20 + 2 * (it.t & 1);
       const uint32_t o_col = kO0 + c * 64;
@@ -332,7 +346,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       // the list entry of the next tile is loaded one tile ahead (its L2 latency used to sit
       // between releasing P and waiting for the next S)
       int j = 0;
-      int nx = it.m > 0 ? lst[0] : 0;
+      int nx = it.e0;
       for (int done = 0; done < it.m; ++done, ++g) {
         int e = nx;
         ++j;
@@ -362,8 +376,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             if (q >= P.D) break;
-            const int2 ex = __ldg(exr + q);
-            const int a = ex.x - j0, b = ex.y - j0;
+            const int a = exv[q].x - j0, b = exv[q].y - j0;
             if (a >= kT3 || b <= 0) continue;
 #pragma unroll
             for (int w = 0; w < 2; ++w) vm[w] &= ~bit_range3(a - (2 * c + w) * 32, b - (2 * c + w) * 32);
