@@ -25,7 +25,6 @@ constexpr int kBM = 64;          // query rows per CTA
 constexpr int kBN = 64;          // key tokens per tile
 constexpr int kPfThreads = 128;  // 4 warps x 16 rows
 constexpr int kMaxD = 8;         // exclusion intervals per row supported by the kernel
-constexpr float kLazyRescalePf = 8.f;  // log2-domain headroom before O is rescaled
 
 // One thread per (row, 16-byte chunk): the 4 (cos, sin) pairs of the chunk depend only on the
 // row's position, so they are computed once and applied to the chunk in every q and k head
@@ -293,7 +292,7 @@ mv_status prefill_tc3_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_
                              void* d_out, int32_t out_dtype, const int32_t* hcount, const int32_t* tlist,
                              int32_t stride, cudaStream_t st);
 mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
-                    int32_t stride, cudaStream_t stream, int32_t* d_hcount);
+                    int32_t stride, cudaStream_t stream, int32_t* d_hcount, int32_t* d_hlist);
 }
 
 using namespace mv;
@@ -348,7 +347,9 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
   if (v3) {
     MV_CUDA_TRY(cudaEventRecord(ev_fork, st));
     MV_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
-    if (mv_status e = tile_map2(d_excl, n, max_depth, tcount, tlist, stride, side, hcount)) return e;
+    // per-128-row-tile lists after the pair lists (capacity (n/64)^2 >= 3 n^2 / 2^15 entries)
+    if (mv_status e = tile_map2(d_excl, n, max_depth, tcount, tlist, stride, side, hcount, tlist + (size_t)n_qp * stride))
+      return e;
     MV_CUDA_TRY(cudaEventRecord(ev_join, side));
   }
   rope_qk_kernel<<<(unsigned)(((int64_t)n * 16 + 255) / 256), 256, 0, st>>>(
@@ -358,7 +359,7 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
   if (v3) {  // tcgen05 v3 (prefill_tc3.cu)
     MV_CUDA_TRY(cudaStreamWaitEvent(st, ev_join, 0));
     return prefill_tc3_launch(q_rot, k_rot, (const __nv_bfloat16*)d_v, d_excl, max_depth, n, q_heads, kv_heads, d_out,
-                              out_dtype, hcount, tlist, stride, st);
+                              out_dtype, hcount, tlist + (size_t)n_qp * stride, stride, st);
   }
   MV_CUDA_TRY(cudaMemsetAsync(vis, 0, 8, st));
   if (!getenv("MV_PREFILL_V0"))  // tcgen05 v2 (prefill_tc.cu) and v0 kept for A/B diagnostics

@@ -39,7 +39,7 @@
 namespace mv {
 
 mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
-                    int32_t stride, cudaStream_t stream, int32_t* d_hcount = nullptr);
+                    int32_t stride, cudaStream_t stream, int32_t* d_hcount = nullptr, int32_t* d_hlist = nullptr);
 
 namespace {
 

@@ -22,9 +22,9 @@
 //   warps 2-5 (columns 0-63) and 6-9 (columns 64-127): softmax, thread = row = TMEM lane.
 //                  Lazy O rescale (only when the row max grows by > 2^8), after P.V(j-1) is
 //                  certified by the V ring's empty barrier.  Epilogue: O / l for its 64 dims.
-// Tile lists come from tile_map2 (pairs of 128-row tiles): item tile t reads the pair list of
-// t / 2 and skips entries whose status for half t & 1 is 0; hcount[t] (written by tile_map2)
-// is the number of processed entries.
+// Tile lists come from tile_map2: item tile t reads its own list (the k tiles whose status for
+// that 128-row tile is not 0, hcount[t] of them; entries keep the pair layout kt | stA << 20 |
+// stB << 22, so the status of tile t sits at bit 20 + 2 (t & 1)).
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
@@ -63,7 +63,7 @@ constexpr uint32_t kS0 = 0, kO0 = kSB * 128, kQ0 = kO0 + 128;
 struct Tc3Params {
   const int32_t* excl;
   const int32_t* hcount;  // [n_qt] processed k tiles per 128-row q tile
-  const int32_t* tlist;   // [n_qp][stride] pair lists from tile_map2
+  const int32_t* tlist;   // [n_qt][stride] per-tile lists from tile_map2
   void* out;
   int out_f32;
   int n, hq, hkv, D, n_qt, stride;
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
         it.t = it.valid ? P.n_qt - 1 - w / P.hq : 0;
         it.h = it.valid ? w % P.hq : 0;
         it.m = it.valid ? P.hcount[it.t] : 0;
-        it.e0 = it.valid ? P.tlist[(size_t)(it.t >> 1) * P.stride] : 0;
+        it.e0 = it.valid ? P.tlist[(size_t)it.t * P.stride] : 0;
         it.pad0 = it.pad1 = it.pad2 = 0;
       };
       Item3 nxt;
@@ -219,11 +219,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
         tc::tma_load_3d(smem + kOffQ3, &map_q, 0, it.h, it.t * kT3, q_full);
         tc::tma_load_3d(smem + kOffQ3 + kHalf3, &map_q, 64, it.h, it.t * kT3, q_full);
         const int kvh = it.h / (P.hq / P.hkv);
-        const int32_t* lst = P.tlist + (size_t)(it.t >> 1) * P.stride;
-        const int sh = 20 + 2 * (it.t & 1);
-        for (int j = 0, done = 0; done < it.m; ++j) {
+        const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
+        for (int j = 0; j < it.m; ++j) {
           const int e = lst[j];
-          if (((e >> sh) & 3) == 0) continue;
           const int s = gk % kKSt3;
           if (gk >= kKSt3) mbar_wait(&k_empty[s], ((gk / kKSt3) - 1) & 1);
           const int kt = e & 0xFFFFF;
@@ -231,7 +229,6 @@ __global__ void __launch_bounds__(kThreads3, 1)
           tc::tma_load_3d(smem + kOffK3 + s * kTile3, &map_k, 0, kvh, kt * kT3, &k_full[s]);
           tc::tma_load_3d(smem + kOffK3 + s * kTile3 + kHalf3, &map_k, 64, kvh, kt * kT3, &k_full[s]);
           ++gk;
-          ++done;
         }
       }
     } else if (lane == 1) {
@@ -245,11 +242,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
         mbar_arrive(&slot_empty[buf]);
         if (!it.valid) break;
         const int kvh = it.h / (P.hq / P.hkv);
-        const int32_t* lst = P.tlist + (size_t)(it.t >> 1) * P.stride;
-        const int sh = 20 + 2 * (it.t & 1);
-        for (int j = 0, done = 0; done < it.m; ++j) {
+        const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
+        for (int j = 0; j < it.m; ++j) {
           const int e = lst[j];
-          if (((e >> sh) & 3) == 0) continue;
           const int s = gv % kVSt3;
           if (gv >= kVSt3) mbar_wait(&v_empty[s], ((gv / kVSt3) - 1) & 1);
           const int kt = e & 0xFFFFF;
@@ -257,7 +252,6 @@ __global__ void __launch_bounds__(kThreads3, 1)
           tc::tma_load_3d(smem + kOffV3 + s * kTile3, &map_v, 0, kvh, kt * kT3, &v_full[s]);
           tc::tma_load_3d(smem + kOffV3 + s * kTile3 + kHalf3, &map_v, 64, kvh, kt * kT3, &v_full[s]);
           ++gv;
-          ++done;
         }
       }
     }
@@ -339,19 +333,16 @@ __global__ void __launch_bounds__(kThreads3, 1)
       int2 exv[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) exv[q] = q < P.D ? __ldg(exr + q) : make_int2(0, 0);
-      const int32_t* lst = P.tlist + (size_t)(it.t >> 1) * P.stride;
+      const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
       const int sh = 20 + 2 * (it.t & 1);
       const uint32_t o_col = kO0 + c * 64;
       float m_ref = -INFINITY, l = 0.f;
       // the list entry of the next tile is loaded one tile ahead (its L2 latency used to sit
       // between releasing P and waiting for the next S)
-      int j = 0;
       int nx = it.e0;
       for (int done = 0; done < it.m; ++done, ++g) {
         int e = nx;
-        ++j;
-        while (((e >> sh) & 3) == 0) e = lst[j++];
-        nx = done + 1 < it.m ? lst[j] : 0;
+        nx = done + 1 < it.m ? lst[done + 1] : 0;
         const int j0 = (e & 0xFFFFF) * kT3;
         const int status = (e >> sh) & 3;
         const uint32_t s_col = kS0 + (g % kSB) * 128;

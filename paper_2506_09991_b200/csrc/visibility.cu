@@ -390,7 +390,8 @@ constexpr int kTm2Threads = 1024;  // 4 groups of 256 (one thread per row) share
 __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* __restrict__ excl, int n, int D,
                                                                 int32_t* __restrict__ count,
                                                                 int32_t* __restrict__ list, int stride,
-                                                                int32_t* __restrict__ hcount) {
+                                                                int32_t* __restrict__ hcount,
+                                                                int32_t* __restrict__ hlist) {
   const int qp = blockIdx.x;
   const int tile = 128;
   const int r = threadIdx.x & 255, grp = threadIdx.x >> 8;
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* _
   }
   // per 32-row warp and k tile: all rows empty / all rows full (no block barrier per k tile)
   __shared__ uint8_t s_e[8][kTm2Chunk], s_f[8][kTm2Chunk];
-  __shared__ int s_warp_sum[kTm2Threads / 32];
+  __shared__ int s_warp_sum[3][kTm2Threads / 32];
   const int last_kt = min((qp * 256 + 255) / tile, (n - 1) / tile);
   int written = 0, nA = 0, nB = 0;
   for (int kt0 = 0; kt0 <= last_kt; kt0 += kTm2Chunk) {
@@ -454,21 +455,34 @@ __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* _
       }
       if (st[0] || st[1]) ent = kt | (st[0] << 20) | (st[1] << 22);
     }
-    // per-half processed counts (k tiles whose status for that 128-row half is not 0)
-    nA += __syncthreads_count(ent >= 0 && ((ent >> 20) & 3) != 0);
-    nB += __syncthreads_count(ent >= 0 && ((ent >> 22) & 3) != 0);
-    // ordered compaction
-    const unsigned keep = __ballot_sync(0xffffffffu, ent >= 0);
-    if (lane == 0) s_warp_sum[warp] = __popc(keep);
-    __syncthreads();
-    int base = written, total = 0;
-    for (int w = 0; w < kTm2Threads / 32; ++w) {
-      const int c = s_warp_sum[w];
-      if (w < warp) base += c;
-      total += c;
+    // ordered compactions: the pair list, and (for the one-tile-per-item kernel) one list per
+    // 128-row half holding only the k tiles whose status for that half is not 0
+    const bool kp[3] = {ent >= 0, ent >= 0 && ((ent >> 20) & 3) != 0, ent >= 0 && ((ent >> 22) & 3) != 0};
+    unsigned keep[3];
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      keep[x] = __ballot_sync(0xffffffffu, kp[x]);
+      if (lane == 0) s_warp_sum[x][warp] = __popc(keep[x]);
     }
-    if (ent >= 0) list[(int64_t)qp * stride + base + __popc(keep & ((1u << lane) - 1u))] = ent;
-    written += total;
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+      int base = 0, total = 0;
+      for (int w = 0; w < kTm2Threads / 32; ++w) {
+        const int c = s_warp_sum[x][w];
+        if (w < warp) base += c;
+        total += c;
+      }
+      const int at = base + __popc(keep[x] & ((1u << lane) - 1u));
+      if (x == 0) {
+        if (kp[0]) list[(int64_t)qp * stride + written + at] = ent;
+        written += total;
+      } else {
+        if (kp[x] && hlist) hlist[(int64_t)(2 * qp + x - 1) * stride + (x == 1 ? nA : nB) + at] = ent;
+        if (x == 1) nA += total;
+        else nB += total;
+      }
+    }
     __syncthreads();  // s_e / s_f / s_warp_sum reused by the next pass
   }
   if (threadIdx.x == 0) {
@@ -537,9 +551,9 @@ extern "C" mv_status mv_tile_map(const int32_t* d_excl, int32_t n, int32_t max_d
 
 namespace mv {
 mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
-                    int32_t stride, cudaStream_t stream, int32_t* d_hcount) {
+                    int32_t stride, cudaStream_t stream, int32_t* d_hcount, int32_t* d_hlist) {
   const int n_qp = (n + 255) / 256;
-  tile_map2_kernel<<<n_qp, kTm2Threads, 0, stream>>>(d_excl, n, max_depth, d_count, d_list, stride, d_hcount);
+  tile_map2_kernel<<<n_qp, kTm2Threads, 0, stream>>>(d_excl, n, max_depth, d_count, d_list, stride, d_hcount, d_hlist);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }
