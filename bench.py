@@ -254,6 +254,7 @@ def run_ours(args):
     pos_steps = [base_pos + (args.warmup + s) for s in range(args.steps)]  # inputs resident before timing
     torch.cuda.synchronize()
     ev[0].record(stream)
+    t_host0 = time.perf_counter()
     for s in range(args.steps):
         i = args.warmup + s
         p = pos_steps[s]
@@ -262,6 +263,7 @@ def run_ours(args):
         mv.attention.decode(st, handles, qs[i % 2], p, out=out)
         att[s][1].record(stream)
     ev[1].record(stream)
+    host_ms = (time.perf_counter() - t_host0) * 1e3 / args.steps  # enqueue cost per step (host)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -339,7 +341,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl_text,
                        "requests_per_gpu": R, "branches_per_gpu": n, "l2": "inputs 0.8+ GB > L2 (no flush)",
-                       "mean_kv_tokens_per_step": kv_tokens,
+                       "mean_kv_tokens_per_step": kv_tokens, "host_enqueue_ms_per_step": host_ms,
                        "step": "append 1 token K/V per branch (RoPE fused) + cascade decode attention"},
             "e2e": {"value": tokens_per_step / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},

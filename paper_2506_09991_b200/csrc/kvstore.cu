@@ -192,9 +192,9 @@ __device__ __forceinline__ void rope8(uint4& v, int pos, int chunk, const double
 
 __device__ __forceinline__ void write_kv_token(__nv_bfloat16* kp, __nv_bfloat16* vp, int64_t page, int slot,
                                                int kv_heads, const __nv_bfloat16* k, const __nv_bfloat16* v,
-                                               int pos, const double* inv, int lane, int nlanes) {
-  // kv_heads * 16 chunks of 8 dims; K rotated, V verbatim; stored chunk-swizzled.
-  for (int j = lane; j < kv_heads * 16; j += nlanes) {
+                                               int pos, const double* inv, int lane, int nlanes, int first = 0) {
+  // kv_heads * 16 chunks of 8 dims (from chunk `first`); K rotated, V verbatim; stored chunk-swizzled.
+  for (int j = first + lane; j < kv_heads * 16; j += nlanes) {
     int h = j >> 4, c = j & 15;
     size_t dst = kv_page_head_offset(page, h, kv_heads) + (size_t)kv_chunk_offset(slot, c);
     uint4 kk = *reinterpret_cast<const uint4*>(k + (size_t)h * kHeadDim + c * 8);
@@ -243,19 +243,41 @@ struct TokDesc {
   int32_t fresh;   // 1 -> pop a page and create entry (page,0,1); 0 -> grow entry in place
   int32_t cumv;    // cum value for a fresh entry
 };
-__global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ cum, const TokDesc* __restrict__ d,
-                             int n, const int32_t* __restrict__ tokens, int32_t* __restrict__ slot_tok,
-                             int32_t* __restrict__ refcnt, int32_t* __restrict__ free_stack,
-                             int32_t* __restrict__ free_top, int32_t* __restrict__ err, const int32_t* __restrict__ pos,
-                             const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
-                             __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, const RopeTable rt) {
-  __shared__ double s_inv[kHeadDim / 2];
-  const double* inv = rope_stage(rt, s_inv);
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (i >= n) return;
+// Descriptors of up to kDescInline tokens travel in the launch's parameter space (no separate
+// host->device copy in the stream); larger batches use an uploaded array.
+constexpr int kDescInline = 240;
+struct TokDescInline {
+  TokDesc d[kDescInline];
+};
+
+// One warp per token.  The token's K/V chunks (<= 4 per lane for <= 8 kv heads) are loaded and
+// rotated before lane 0's page-table update resolves the destination, so the two latency
+// chains overlap; the stores follow the shuffle of (page, slot).
+__device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef* __restrict__ arena,
+                                                int32_t* __restrict__ cum, const int32_t* __restrict__ tokens,
+                                                int32_t* __restrict__ slot_tok, int32_t* __restrict__ refcnt,
+                                                int32_t* __restrict__ free_stack, int32_t* __restrict__ free_top,
+                                                int32_t* __restrict__ err, const int32_t* __restrict__ pos,
+                                                const __nv_bfloat16* __restrict__ k,
+                                                const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp,
+                                                __nv_bfloat16* vp, int kv_heads, const double* inv) {
+  const int lane = threadIdx.x & 31;
+  const bool kv = k && v;
+  const int nch = kv ? kv_heads * 16 : 0;  // 16-byte chunks of the token's K (and V)
+  const __nv_bfloat16* kt = kv ? k + (size_t)i * kv_heads * kHeadDim : nullptr;
+  const __nv_bfloat16* vt = kv ? v + (size_t)i * kv_heads * kHeadDim : nullptr;
+  uint4 kk[4], vv[4];
+  const int p = kv ? __ldg(pos + i) : 0;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = lane + 32 * u;
+    if (j < nch) {
+      kk[u] = __ldg(reinterpret_cast<const uint4*>(kt) + j);
+      vv[u] = __ldg(reinterpret_cast<const uint4*>(vt) + j);
+    }
+  }
   int page = -1, slot = 0;
   if (lane == 0) {
-    TokDesc td = d[i];
     if (td.fresh) {
       // a failed pop leaves the stack usable only for reporting: the sticky error poisons the store
       int old = atomicSub(free_top, 1);
@@ -276,11 +298,51 @@ __global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ 
     }
     if (page >= 0 && tokens) slot_tok[(int64_t)page * kPageTokens + slot] = tokens[i];
   }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (lane + 32 * u < nch) rope8(kk[u], p, (lane + 32 * u) & 15, inv);
   page = __shfl_sync(0xffffffffu, page, 0);
   slot = __shfl_sync(0xffffffffu, slot, 0);
-  if (page < 0 || !k || !v) return;
-  write_kv_token(kp, vp, page, slot, kv_heads, k + (size_t)i * kv_heads * kHeadDim,
-                 v + (size_t)i * kv_heads * kHeadDim, pos[i], inv, lane, 32);
+  if (page < 0 || !kv) return;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int j = lane + 32 * u;
+    if (j < nch) {
+      const size_t dst = kv_page_head_offset(page, j >> 4, kv_heads) + (size_t)kv_chunk_offset(slot, j & 15);
+      *reinterpret_cast<uint4*>(kp + dst) = kk[u];
+      *reinterpret_cast<uint4*>(vp + dst) = vv[u];
+    }
+  }
+  if (nch > 128)  // more than 8 kv heads: the remaining chunks after the destination is known
+    write_kv_token(kp, vp, page, slot, kv_heads, kt, vt, p, inv, lane, 32, 128);
+}
+
+__global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ cum, const TokDesc* __restrict__ d,
+                             int n, const int32_t* __restrict__ tokens, int32_t* __restrict__ slot_tok,
+                             int32_t* __restrict__ refcnt, int32_t* __restrict__ free_stack,
+                             int32_t* __restrict__ free_top, int32_t* __restrict__ err, const int32_t* __restrict__ pos,
+                             const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
+                             __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, const RopeTable rt) {
+  __shared__ double s_inv[kHeadDim / 2];
+  const double* inv = rope_stage(rt, s_inv);
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  append_one_warp((threadIdx.x & 31) == 0 ? d[i] : TokDesc{0, 0, 0}, i, arena, cum, tokens, slot_tok, refcnt,
+                  free_stack, free_top, err, pos, k, v, kp, vp, kv_heads, inv);
+}
+__global__ void k_append_one_inline(PageRef* __restrict__ arena, int32_t* __restrict__ cum, const TokDescInline d,
+                                    int n, const int32_t* __restrict__ tokens, int32_t* __restrict__ slot_tok,
+                                    int32_t* __restrict__ refcnt, int32_t* __restrict__ free_stack,
+                                    int32_t* __restrict__ free_top, int32_t* __restrict__ err,
+                                    const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
+                                    const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp,
+                                    int kv_heads, const RopeTable rt) {
+  __shared__ double s_inv[kHeadDim / 2];
+  const double* inv = rope_stage(rt, s_inv);
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  append_one_warp(d.d[i], i, arena, cum, tokens, slot_tok, refcnt, free_stack, free_top, err, pos, k, v, kp, vp,
+                  kv_heads, inv);
 }
 
 // K/V of the last token of each handle (for layers > the one written at append).
@@ -850,13 +912,23 @@ mv_status PagedStore::append(const uint64_t* hs, int32_t n, const int32_t* d_tok
     r->version++;
     logical_ += 1;
   }
-  void* d_desc;
-  if (mv_status st = upload(desc.data(), sizeof(TokDesc) * n, &d_desc, 10)) return st;
-  k_append_one<<<(n + 3) / 4, 128, 0, stream_>>>(d_arena, d_cum, (const TokDesc*)d_desc, n, d_tokens, d_slot_tok_,
-                                                 d_refcnt_,
-                                       d_free_, d_free_top_, d_err_, d_pos, (const __nv_bfloat16*)d_k,
-                                       (const __nv_bfloat16*)d_v, d_k ? k_planes_[layer] : nullptr,
-                                       d_k ? v_planes_[layer] : nullptr, cfg_.kv_heads, rope_);
+  __nv_bfloat16* kpl = d_k ? k_planes_[layer] : nullptr;
+  __nv_bfloat16* vpl = d_k ? v_planes_[layer] : nullptr;
+  if (n <= kDescInline) {  // descriptors ride in the launch parameters: no copy in the stream
+    TokDescInline inl;
+    std::memcpy(inl.d, desc.data(), sizeof(TokDesc) * n);
+    k_append_one_inline<<<(n + 3) / 4, 128, 0, stream_>>>(d_arena, d_cum, inl, n, d_tokens, d_slot_tok_, d_refcnt_,
+                                                          d_free_, d_free_top_, d_err_, d_pos,
+                                                          (const __nv_bfloat16*)d_k, (const __nv_bfloat16*)d_v, kpl,
+                                                          vpl, cfg_.kv_heads, rope_);
+  } else {
+    void* d_desc;
+    if (mv_status st = upload(desc.data(), sizeof(TokDesc) * n, &d_desc, 10)) return st;
+    k_append_one<<<(n + 3) / 4, 128, 0, stream_>>>(d_arena, d_cum, (const TokDesc*)d_desc, n, d_tokens, d_slot_tok_,
+                                                   d_refcnt_, d_free_, d_free_top_, d_err_, d_pos,
+                                                   (const __nv_bfloat16*)d_k, (const __nv_bfloat16*)d_v, kpl, vpl,
+                                                   cfg_.kv_heads, rope_);
+  }
   MV_LAUNCH_CHECK();
   return MV_OK;
 }
