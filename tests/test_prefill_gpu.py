@@ -63,3 +63,61 @@ def test_c3_nested_16k_sampled(mv):
     rows = np.sort(np.concatenate([rng.choice(16384, 60, replace=False), [0, 1, 16383, 2048, 2049]]))
     err, spec = run_prefill(mv, toks, hq=40, hkv=8, rows=rows)
     assert err < TOL, err
+
+
+def nested_tokens(depth, paths, path_words, seed=0, prefix=100):
+    """A tag stream with Parallel blocks nested `depth` deep (every path of a block holds another
+    block until the innermost level): many exclusion intervals per row, interval ends inside k
+    tiles, and short sibling paths that share a 128-token tile."""
+    rng = np.random.default_rng(seed)
+    words = lambda k: [int(x) for x in 10 + rng.integers(0, 4000, size=k)]  # noqa: E731
+    P_OPEN, P_CLOSE, G_OPEN, G_CLOSE, O_OPEN, O_CLOSE, PATH, PATH_C, C_OPEN, C_CLOSE = range(10)
+
+    def block(d):
+        t = [P_OPEN, G_OPEN]
+        for _ in range(paths):
+            t += [O_OPEN] + words(3) + [O_CLOSE]
+        t += [G_CLOSE]
+        for _ in range(paths):
+            body = words(path_words)
+            if d > 1:
+                body += block(d - 1) + words(max(1, path_words // 2))
+            t += [PATH] + body + [PATH_C]
+        return t + [C_OPEN] + words(5) + [C_CLOSE, P_CLOSE]
+
+    return words(prefix) + block(depth) + words(7)
+
+
+@pytest.mark.parametrize("depth,paths,pw", [(3, 3, 20), (4, 2, 9), (2, 6, 5)])
+def test_deep_nesting_all_rows(mv, depth, paths, pw):
+    toks = nested_tokens(depth, paths, pw, seed=depth * 10 + paths)
+    err, spec = run_prefill(mv, toks, hq=40, hkv=8, seed=depth)
+    assert spec.excl.shape[1] >= depth - 1
+    assert err < TOL, (len(toks), err)
+
+
+@pytest.mark.parametrize("hq,hkv", [(4, 4), (16, 2), (8, 8)])
+def test_gqa_ratios(mv, dag_golden, hq, hkv):
+    c = next(c for c in dag_golden if c["name"].startswith("random4x6") and c["error"] == -1)
+    err, _ = run_prefill(mv, c["tokens"], hq=hq, hkv=hkv, seed=hq + hkv)
+    assert err < TOL, err
+
+
+def test_bf16_output_matches_fp32(mv):
+    toks = nested_tokens(3, 3, 40, seed=7)
+    n = len(toks)
+    spec = mv.dag.build_visibility(toks)
+    q, k, v = sym_bf16(71, (n, 40, 128)).cuda(), sym_bf16(72, (n, 8, 128)).cuda(), sym_bf16(73, (n, 8, 128)).cuda()
+    o32 = mv.attention.prefill(q, k, v, spec.positions, spec.excl, out_dtype=torch.float32)
+    o16 = mv.attention.prefill(q, k, v, spec.positions, spec.excl)
+    # identical arithmetic, then the bf16 store rounding (<= 2^-9 relative)
+    d = (o16.float() - o32).abs()
+    assert bool((d <= o32.abs() * 2.0 ** -8 + 1e-6).all())
+
+
+def test_sequence_lengths_around_tiles(mv):
+    # lengths that leave a partial last q tile / k tile, including n < 128 and n = 128 * k + 1
+    for n_extra in (0, 1, 127, 129, 255, 383):
+        toks = nested_tokens(2, 2, 8, seed=n_extra, prefix=50 + n_extra)
+        err, _ = run_prefill(mv, toks, hq=8, hkv=2, seed=n_extra + 1)
+        assert err < TOL, (len(toks), err)
