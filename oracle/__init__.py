@@ -150,9 +150,12 @@ class Toy:
         self.h = lib().mvo_toy_new(layers, heads, model_dim, vocab, seed, init, rope)
 
     def __del__(self):
-        if getattr(self, "h", None):
-            lib().mvo_toy_free(self.h)
-            self.h = None
+        try:
+            if getattr(self, "h", None):
+                lib().mvo_toy_free(self.h)
+                self.h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     @property
     def rec(self):

@@ -7,6 +7,7 @@ it with ctypes and mirrors the reference's proj/core interface names for this pa
     kv.PagedStore         <- multiverse::kv::RadixStore (kvcache.hpp:60-101)
     attention.decode      <- attention core of ToyModel::step (toy_model.cpp:121-157)
     attention.prefill     <- attention inside ToyModel::forward (toy_model.cpp:174-202)
+    toy.ToyModel          <- ToyModel forward / engine::run_forced around those kernels (configs[0])
 
 There is no CPU fallback: importing fails loudly when the library is missing, and every
 call runs on the GPU.
@@ -116,4 +117,4 @@ def check(status: int) -> None:
     raise MvError(status, msg)
 
 
-from . import dag, kv, attention  # noqa: E402,F401
+from . import dag, kv, attention, toy  # noqa: E402,F401

@@ -1,0 +1,107 @@
+"""BASELINE configs[0] (C1) end to end on the GPU: the reference's toy transformer (2 layers,
+d=256, 4 heads of 64) with this package's kernels for the attention (prefill for
+ToyModel::forward, paged fork / merge / append + decode for engine::run_forced), against the
+reference's own logits (tests/golden/toy.jsonl.gz, written by the compiled reference) and the
+fp64 oracle restatement for the full C1-sized trajectory.
+
+Tolerance: the attention inputs are bf16 (the kernels' contract), the layer algebra fp64, so
+logits differ from the fp64 reference by the bf16 rounding of q / k / v propagated through two
+layers; LOGIT_TOL bounds it (measured 1.7e-5 max-abs on the 692-token C1 trajectory, logits of
+magnitude <= 0.067 at init 0.05) and the greedy argmax must agree."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2506_09991_b200.host.tokenize import tokenize
+
+pytestmark = pytest.mark.gpu
+LOGIT_TOL = 2e-4
+
+
+@pytest.fixture(scope="module")
+def mv():
+    import paper_2506_09991_b200 as m
+    return m
+
+
+def gpu_toy(mv, c):
+    ref = oracle.Toy(c["layers"], c["heads"], c["model_dim"], c["vocab"], c["seed"], c["init"], c["rope"])
+    L = c["layers"]
+    w = {"emb": ref.weight("emb"), "unemb": ref.weight("unemb")}
+    for k in ("wq", "wk", "wv", "wo", "up", "down"):
+        w[k] = [ref.weight(k, l) for l in range(L)]
+    return ref, mv.toy.ToyModel(w, L, c["heads"], c["model_dim"], c["vocab"], c["rope"])
+
+
+def check_logits(got, want, what):
+    got = got.cpu().numpy().reshape(want.shape)
+    err = np.abs(got - want).max()
+    agree = (got.argmax(-1) == want.argmax(-1)).mean()
+    assert err < LOGIT_TOL, (what, err)
+    assert agree == 1.0, (what, agree)
+    return err
+
+
+def test_forward_matches_reference_golden(mv, toy_golden):
+    for name in ("t1_small", "t1_c1"):
+        g = toy_golden[name]
+        _, toy = gpu_toy(mv, g)
+        check_logits(toy.forward(g["tokens"]), np.array(g["logits"]).reshape(len(g["tokens"]), -1), name)
+
+
+def test_run_forced_matches_reference_engine(mv, toy_golden):
+    # engine::run_forced logits (per-lane decode with the KV in the store) from the reference
+    for name, cfg in (("forced_t1_small", "t1_small"), ("forced_c1_mini", "t1_c1")):
+        g, c = toy_golden[name], toy_golden[cfg]
+        _, toy = gpu_toy(mv, c)
+        ids = tokenize(g["text"])
+        logits, stats = toy.run_forced(ids)
+        want = np.array(g["logits"]).reshape(len(ids), -1)
+        check_logits(logits, want, name)
+        assert stats["forks"] == 1 and stats["merges"] == 1 and stats["length"] == len(ids)
+        assert stats["store"].live_handles == 1  # the root only, released after the stats read
+
+
+def c1_text(seed=0, prompt_words=512, path_words=64, concl_words=32):
+    """configs[0] shape: 512-word prompt, one block of 2 outlines, paths of 64 words, conclusion 32."""
+    rng = np.random.default_rng(seed)
+    lex = ["value", "residue", "the", "terms", "area", "bound", "compute", "apply", "prime", "result", "of",
+           "case", "digits", "total", "lemma", "sum", "factor", "check", "ratio", "segment", "series", "count",
+           "root", "length"]
+    w = lambda k: " ".join(rng.choice(lex, size=k))  # noqa: E731
+    return (w(prompt_words) + " <Parallel> <Goal> <Outline> 1: first </Outline> <Outline> 2: second </Outline> "
+            "</Goal> <Path> 1: " + w(path_words) + " </Path> <Path> 2: " + w(path_words) + " </Path> <Conclusion> "
+            + w(concl_words) + " </Conclusion> </Parallel>")
+
+
+def test_c1_full_forward_and_run_forced(mv, toy_golden):
+    c = toy_golden["t1_c1"]  # configs[0] model: 2 layers, d 256, 4 heads, vocab 256, seed 0
+    ref, toy = gpu_toy(mv, c)
+    ids = tokenize(c1_text())
+    err, pos, _, _ = oracle.build_dag(ids)
+    assert err == 0 and len(ids) > 600
+    want = ref.forward(ids, pos, oracle.mask_dense(ids))
+    check_logits(toy.forward(ids), want, "C1 forward")
+    logits, stats = toy.run_forced(ids)
+    check_logits(logits, want, "C1 run_forced")
+    assert stats["steps"] < len(ids)  # the two path lanes stepped together
+
+
+def test_nested_run_forced_equals_forward(mv, toy_golden):
+    # nested Process stages: a lane per inner path, forks inside forked lanes, merges inside out
+    c = toy_golden["t1_c1"]
+    ref, toy = gpu_toy(mv, c)
+    text = ("intro words here <Parallel> <Goal> <Outline> 1: a </Outline> <Outline> 2: b </Outline> "
+            "<Outline> 3: c </Outline> </Goal> <Path> 1: x x <Parallel> <Goal> <Outline> 1: u </Outline> "
+            "<Outline> 2: v </Outline> </Goal> <Path> 1: p q r </Path> <Path> 2: s t </Path> <Conclusion> w "
+            "</Conclusion> </Parallel> y </Path> <Path> 2: z z z z </Path> <Path> 3: k </Path> <Conclusion> "
+            "done now </Conclusion> </Parallel> tail")
+    ids = tokenize(text)
+    err, pos, _, _ = oracle.build_dag(ids)
+    assert err == 0
+    want = ref.forward(ids, pos, oracle.mask_dense(ids))
+    logits, stats = toy.run_forced(ids)
+    assert stats["forks"] == 2 and stats["merges"] == 2
+    check_logits(logits, want, "nested run_forced")
+    check_logits(toy.forward(ids), want, "nested forward")
