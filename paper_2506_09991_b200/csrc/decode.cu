@@ -66,7 +66,13 @@ constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dim
 constexpr int kQBytes = 2 * kQHalf;
 constexpr float kSumLimit = 4096.f;                        // block mass that moves the softmax reference
 constexpr int kPrefetch = 32;                               // pages of a unit prefetched into L2 at staging
-constexpr bool kUseCopies = false;                          // see build_plan
+// Row replication across lane quadrants (copies > 1) is an experiment kept behind
+// -DMV_DEC_COPIES=1: measured 7% slower on C2 and NOT parity-clean (tests/test_decode_gpu.py
+// fails with it); the product build never plans copies.
+#ifndef MV_DEC_COPIES
+#define MV_DEC_COPIES 0
+#endif
+constexpr bool kUseCopies = MV_DEC_COPIES != 0;
 constexpr int kSBufs = 5;                                   // S / P buffers in flight
 constexpr int kColS = 0;                                    // TMEM: S0..S4 (64 cols each)
 constexpr int kColO = kSBufs * kBlkCols;                    //       O (128 cols)
