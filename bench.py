@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--requests", type=int, default=16, help="requests per GPU (c2)")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--shard", default="requests", choices=["requests", "heads"],
+                    help="heads: every rank serves all requests for its KV-head group and the head-sharded "
+                         "outputs are all-gathered over NCCL each step (the layer-level bench, SURVEY.md §8e)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     return ap.parse_args()
@@ -168,7 +171,7 @@ def run_reference(args):
 
 
 def build_workload(mv, torch, R, dev, first_request=0, prefix=PREFIX, branches_per_req=BRANCHES,
-                   branch_len=BRANCH_LEN, steps_total=0):
+                   branch_len=BRANCH_LEN, steps_total=0, hkv=HKV):
     """R requests: root prefix, fork into B branches, branch_len - 1 private tokens each (positions
     shared start).  Request r's data is seeded by its global id, so every rank holds distinct
     requests.  The pool has room for steps_total appended tokens per branch."""
@@ -177,6 +180,7 @@ def build_workload(mv, torch, R, dev, first_request=0, prefix=PREFIX, branches_p
     # page-table arena: every branch holds its own span list (prefix entries + private tail), with
     # the store's capacity doubling on growth
     table = 2 * R * (BRANCHES + 1) * (PREFIX // 16 + (BRANCH_LEN + steps_total) // 16 + 8) + 65536
+    HKV = hkv  # noqa: N806  (this rank's KV-head group)
     st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=HKV, table_entries=table)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + first_request)
@@ -213,24 +217,38 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     import paper_2506_09991_b200 as mv
 
-    from paper_2506_09991_b200.shard import shard_requests, max_over_ranks
+    from paper_2506_09991_b200.shard import shard_heads, shard_requests, max_over_ranks
     # weak scaling: R requests per GPU, sharded by request (no collective in attention)
     wl = WORKLOADS[args.workload]
-    total = wl.get("total_requests", args.requests * world)
-    shard = shard_requests(total, HKV, world, rank)
+    heads_mode = args.shard == "heads"
+    if heads_mode:
+        # layer-level bench: all ranks serve the same requests, each for its KV-head group
+        total = wl.get("total_requests", args.requests)
+        shard = shard_heads(total, HKV, world, rank)
+    else:
+        total = wl.get("total_requests", args.requests * world)
+        shard = shard_requests(total, HKV, world, rank)
     R = len(shard.requests)
+    hkv_l = shard.kv_heads[1] - shard.kv_heads[0]
+    hq_l = hkv_l * (HQ // HKV)
     steps_total = args.warmup + args.steps
     steps_total += max(3, args.steps // 2)  # the e2e leg appends too
-    st, handles, pos0, rnd = build_workload(mv, torch, R, dev, shard.requests[0], wl["prefix"], wl["branches"],
-                                            wl["branch_len"], steps_total)
+    # a head-sharded rank seeds its data by (first request, head group): synthetic values per shard
+    seed_id = shard.requests[0] * 64 + shard.kv_heads[0]
+    st, handles, pos0, rnd = build_workload(mv, torch, R, dev, seed_id, wl["prefix"], wl["branches"],
+                                            wl["branch_len"], steps_total, hkv=hkv_l)
     n = len(handles)
     steps_total = args.warmup + args.steps
     # per-step inputs (device resident for `value`)
-    qs = [rnd(n, HQ, D) for _ in range(2)]
-    ks = [rnd(n, HKV, D) for _ in range(2)]
-    vs = [rnd(n, HKV, D) for _ in range(2)]
+    qs = [rnd(n, hq_l, D) for _ in range(2)]
+    ks = [rnd(n, hkv_l, D) for _ in range(2)]
+    vs = [rnd(n, hkv_l, D) for _ in range(2)]
     toks = torch.full((n,), 13, dtype=torch.int32, device=dev)
-    out = torch.empty(n, HQ, D, dtype=torch.bfloat16, device=dev)
+    out = torch.empty(n, hq_l, D, dtype=torch.bfloat16, device=dev)
+    # head-sharded outputs of all ranks: [world][n][hq_l][D] (NCCL all-gather each step)
+    gathered = torch.empty(world, n, hq_l, D, dtype=torch.bfloat16, device=dev) if heads_mode and world > 1 else None
+    ag = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)] if gathered is not None else []
     base_pos = torch.tensor(pos0, dtype=torch.int32, device=dev)
 
     def step(i, q, k, v, p):
@@ -262,6 +280,10 @@ def run_ours(args):
         att[s][0].record(stream)
         mv.attention.decode(st, handles, qs[i % 2], p, out=out)
         att[s][1].record(stream)
+        if gathered is not None:  # layer-level: every rank assembles all heads of every token
+            ag[s][0].record(stream)
+            dist.all_gather_into_tensor(gathered, out)
+            ag[s][1].record(stream)
     ev[1].record(stream)
     host_ms = (time.perf_counter() - t_host0) * 1e3 / args.steps  # enqueue cost per step (host)
     torch.cuda.synchronize()
@@ -271,13 +293,14 @@ def run_ours(args):
     ms = ev[0].elapsed_time(ev[1]) / args.steps
     att_each = [a.elapsed_time(b) for a, b in att]
     att_ms = float(np.mean(att_each))
+    ag_ms = float(np.mean([a.elapsed_time(b) for a, b in ag])) if ag else 0.0
     if os.environ.get("MV_BENCH_DUMP"):
         np.save(os.environ["MV_BENCH_DUMP"], np.array(att_each))
-    ms, att_ms = max_over_ranks([ms, att_ms], device=dev)
+    ms, att_ms, ag_ms = max_over_ranks([ms, att_ms, ag_ms], device=dev)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the region ----
     # one pinned host block per step input set [q | k | v | positions] -> one H2D copy per step
-    nq, nk = n * HQ * D * 2, n * HKV * D * 2
+    nq, nk = n * hq_l * D * 2, n * hkv_l * D * 2
     blk = nq + 2 * nk + n * 4
     hin = [torch.empty(blk, dtype=torch.uint8).pin_memory() for _ in range(2)]
     for j in range(2):
@@ -286,11 +309,11 @@ def run_ours(args):
         hin[j][nq + nk:nq + 2 * nk].copy_(vs[j].cpu().view(torch.uint8).reshape(-1))
     hpos = [hin[j][nq + 2 * nk:].view(torch.int32) for j in range(2)]
     din = torch.empty(blk, dtype=torch.uint8, device=dev)
-    dq = din[:nq].view(torch.bfloat16).view(n, HQ, D)
-    dk = din[nq:nq + nk].view(torch.bfloat16).view(n, HKV, D)
-    dv = din[nq + nk:nq + 2 * nk].view(torch.bfloat16).view(n, HKV, D)
+    dq = din[:nq].view(torch.bfloat16).view(n, hq_l, D)
+    dk = din[nq:nq + nk].view(torch.bfloat16).view(n, hkv_l, D)
+    dv = din[nq + nk:nq + 2 * nk].view(torch.bfloat16).view(n, hkv_l, D)
     dp = din[nq + 2 * nk:].view(torch.int32)
-    hout = torch.empty(n, HQ, D, dtype=torch.bfloat16).pin_memory()
+    hout = torch.empty(n, hq_l, D, dtype=torch.bfloat16).pin_memory()
     pos0_np = np.asarray(pos0, dtype=np.int32)
     e2e_steps = max(3, args.steps // 2)
     if world > 1:
@@ -310,16 +333,16 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = ee[0].elapsed_time(ee[1]) / e2e_steps
     (e2e_ms,) = max_over_ranks([e2e_ms], device=dev)
-    h2d = n * (HQ + 2 * HKV) * D * 2 + n * 4
-    d2h = n * HQ * D * 2
+    h2d = n * (hq_l + 2 * hkv_l) * D * 2 + n * 4
+    d2h = n * hq_l * D * 2
 
-    tokens_per_step = n * world
+    tokens_per_step = n if heads_mode else n * world  # head-sharded ranks share their tokens
     value = tokens_per_step / (ms / 1e3)
     # roofline of the dominant kernel: algorithmic bytes = unique KV read once + Q/O
     # every step appends one token per branch before attending, so the context (and the bytes a
     # step must read) grows by n tokens per step: use the mean over the timed steps
     kv_tokens = info["unique_kv_tokens"] + n * (args.steps + 1) / 2.0
-    alg_bytes = kv_tokens * HKV * D * 2 * 2 + n * HQ * D * 2 * 2
+    alg_bytes = kv_tokens * hkv_l * D * 2 * 2 + n * hq_l * D * 2 * 2
     achieved = alg_bytes / (att_ms / 1e3) / 1e9
     peak, peak_kind = peaks()
     traffic = None
@@ -343,11 +366,14 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if args.workload == "c4" else "weak",
+            "scaling": "strong" if (args.workload == "c4" or heads_mode) else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": wl_text,
                        "requests_per_gpu": R, "branches_per_gpu": n, "l2": "inputs 0.8+ GB > L2 (no flush)",
                        "mean_kv_tokens_per_step": kv_tokens, "host_enqueue_ms_per_step": host_ms,
+                       "parallelism": (f"kv-head groups x{world} + NCCL all-gather of outputs" if heads_mode
+                                       else f"requests x{world}, no collective"),
+                       "kv_heads_per_gpu": hkv_l, "allgather_ms_per_step": ag_ms if heads_mode else None,
                        "step": "append 1 token K/V per branch (RoPE fused) + cascade decode attention"},
             "e2e": {"value": tokens_per_step / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},

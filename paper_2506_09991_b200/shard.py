@@ -33,6 +33,17 @@ def shard_requests(total_requests: int, kv_heads: int, world: int, rank: int) ->
     return Shard((req,), (g * step, (g + 1) * step))
 
 
+def shard_heads(total_requests: int, kv_heads: int, world: int, rank: int) -> Shard:
+    """Layer-level sharding: every rank serves all requests for one contiguous KV-head group (and
+    its GQA query heads); the head-sharded outputs are all-gathered afterwards."""
+    if world < 1 or not 0 <= rank < world or total_requests < 1 or kv_heads < 1:
+        raise ValueError("bad shard arguments")
+    if kv_heads % world:
+        raise ValueError(f"{kv_heads} KV heads do not split into {world} groups")
+    step = kv_heads // world
+    return Shard(tuple(range(total_requests)), (rank * step, (rank + 1) * step))
+
+
 def max_over_ranks(values, device=None):
     """Element-wise max of a list of floats over all ranks (identity when not distributed)."""
     import torch
