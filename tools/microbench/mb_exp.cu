@@ -29,6 +29,8 @@ __global__ void bench(float* out, long long* cyc, float s) {
         acc += r;
       } else if (MODE == 4) {
         asm volatile("add.f32 %0, %0, %1;" : "+f"(a[k]) : "f"(s));
+      } else if (MODE == 5) {  // ex2 with only 8 of 32 lanes active (divergent branch)
+        if ((threadIdx.x & 31) < 8) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a[k]));
       }
     }
   }
@@ -65,6 +67,7 @@ int main() {
     run<2>("fmnmx3", w);
     run<3>("f2fp", w);
     run<4>("fadd", w);
+    run<5>("ex2 8/32", w);
   }
   return 0;
 }
