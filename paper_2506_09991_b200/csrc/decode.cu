@@ -103,7 +103,7 @@ constexpr int kOffStat = kOffEp + 2 * sizeof(WorkItem);
 constexpr int kOffFlag = kOffStat + 2 * 128 * 8;  // softmax group max exchange [4][8][32] floats
 constexpr int kOffXch = kOffFlag + 4 * 8 * 32 * 4;  // epilogue copy merge [3][32][16] floats
 constexpr int kOffBar = kOffXch + 3 * 32 * 16 * 4;
-constexpr int kNumBars = 4 + 2 * (kKSlots + kVSlots) + 3 * kSBufs + 4;
+constexpr int kNumBars = 4 + 2 * (kKSlots + kVSlots) + 3 * kSBufs + 4 + 2;
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
 constexpr int kSmem = kOffTmem + 16 + 1024;  // + 1 KiB alignment slack
 static_assert(kSmem <= 227 * 1024, "decode smem");
@@ -354,11 +354,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
   uint64_t* o_empty = o_full + 1;         // epilogue warps -> PV issuer / softmax
   uint64_t* stat_full = o_empty + 1;      // 8 softmax warps -> epilogue
   uint64_t* q_free = stat_full + 1;       // QK issuer commit (Q tile copied to TMEM) -> stager
+  uint64_t* ent_full = q_free + 1;        // [2] stager -> TMA lanes: header + page entries staged (no Q)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int b = 0; b < 2; ++b) {
+      mbar_init(&ent_full[b], 1);
       mbar_init(&item_full[b], 1);
       mbar_init(&slot_empty[b], 12);  // 2 TMA lanes + QK commit + PV issuer + 8 softmax warps
     }
@@ -389,9 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
   // compile-time base keeps every TMEM operand uniform (no per-MMA R2UR waterfall in the issuer).
   constexpr uint32_t tmem = 0;
   if (*tmem_slot != tmem) __trap();
-  // programmatic launch: the prologue above overlapped rope_q_tile_kernel; its Q tile and the
-  // work-counter reset are visible after this wait
-  pdl_wait();
+  // programmatic launch: everything but the Q tile (written by rope_q_tile_kernel, the kernel
+  // this one may overlap) is ready, so only the stager waits (before its first Q copy); the page
+  // tables and K/V planes were final before rope_q_tile_kernel started
   pdl_launch_dependents();
 
   if (warp == kWarpStage) {
@@ -405,7 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       if (w >= P.n_units) {
         if (lane == 0) si->valid = 0;
         __syncwarp();
-        if (lane == 0) mbar_arrive(&item_full[buf]);
+        if (lane == 0) {
+          mbar_arrive(&ent_full[buf]);
+          mbar_arrive(&item_full[buf]);
+        }
         break;
       }
       if (lane == 0) w_next = atomicAdd(P.work_counter, 1);
@@ -425,7 +430,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         }
       }
       __syncwarp();
+      if (lane == 0) mbar_arrive(&ent_full[buf]);  // the TMA lanes may stream this unit's pages
       const uint32_t half_bytes = (uint32_t)P.R * 128;
+      if (i == 0) pdl_wait();  // the Q tile of this launch is complete and visible
       if (i >= 1) {
         mbar_wait(q_free, (i - 1) & 1);  // the previous unit's Q tile is in TMEM: it has started
         // stream the rest of the previous unit into L2 (its page list is still staged)
@@ -464,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       int g = 0;
       for (int i = 0;; ++i) {
         const int buf = i & 1;
-        mbar_wait(&item_full[buf], (i >> 1) & 1);
+        mbar_wait(&ent_full[buf], (i >> 1) & 1);
         const WorkItem* si = &s_item[buf];
         if (!si->valid) break;
         const int n_ent = si->n_entries;
@@ -689,6 +696,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
   }
   tc::fence_before();
   __syncthreads();
+  if (threadIdx.x == 0 && atomicAdd(P.work_counter + 1, 1) == (int)gridDim.x - 1) {
+    P.work_counter[0] = 0;  // every CTA has stopped claiming: re-arm the queue for the next launch
+    P.work_counter[1] = 0;
+  }
   if (warp == kWarpQk) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, kTmemCols);
@@ -738,16 +749,14 @@ __global__ void combine_kernel(const float* __restrict__ part_o, const float2* _
 
 // RoPE pre-pass: rotates every query once (toy_model.cpp:30-41 at the handle's position) and
 // writes it as the decode kernel's Q operand tile [n][kv_heads][2 halves][R rows][64 dims],
-// SWIZZLE_128B (chunk c of row hl at c ^ (hl & 7)); rows hl >= gqa are zero.  Thread 0 also
-// resets the work counter.  One thread per 16-byte chunk.
+// SWIZZLE_128B (chunk c of row hl at c ^ (hl & 7)); rows hl >= gqa are zero.  One thread per
+// 16-byte chunk.
 __global__ void rope_q_tile_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pos, int n,
-                                   int kv_heads, int gqa, int R, const RopeTable rt, __nv_bfloat16* __restrict__ tile,
-                                   int* counter) {
+                                   int kv_heads, int gqa, int R, const RopeTable rt, __nv_bfloat16* __restrict__ tile) {
   pdl_launch_dependents();  // decode_tc may start its prologue (every CTA of this grid is running)
   __shared__ double s_inv[kHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x == 0) *counter = 0;
   const int64_t total = (int64_t)n * kv_heads * R * 16;
   if (x >= total) return;
   const int c = (int)(x & 15);           // 16-byte chunk of the 128-dim row
@@ -1001,7 +1010,8 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     int dev = 0;
     MV_CUDA_TRY(cudaGetDevice(&dev));
     MV_CUDA_TRY(cudaDeviceGetAttribute(&pc.num_sms, cudaDevAttrMultiProcessorCount, dev));
-    MV_CUDA_TRY(cudaMalloc(&pc.d_counter, sizeof(int)));
+    MV_CUDA_TRY(cudaMalloc(&pc.d_counter, 2 * sizeof(int)));  // [0] work queue, [1] finished CTAs
+    MV_CUDA_TRY(cudaMemset(pc.d_counter, 0, 2 * sizeof(int)));
     pc.smem_set = true;
   }
   // plan signature: the handle list plus each table's entry count and lineage depth
@@ -1098,7 +1108,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   {
     const int64_t chunks = (int64_t)n * cfg.kv_heads * R * 16;
     rope_q_tile_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(
-        (const __nv_bfloat16*)d_q, d_positions, n, cfg.kv_heads, gqa, R, st.rope(), pc.d_q_tile, pc.d_counter);
+        (const __nv_bfloat16*)d_q, d_positions, n, cfg.kv_heads, gqa, R, st.rope(), pc.d_q_tile);
     MV_LAUNCH_CHECK();
   }
   DecodeParams P;
