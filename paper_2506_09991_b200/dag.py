@@ -60,7 +60,12 @@ def build_visibility_batch(token_lists, max_depth: int = DEFAULT_MAX_DEPTH, devi
         offs.append(offs[-1] + L)
     total = offs[-1]
     h_offs = (ctypes.c_int64 * len(offs))(*offs)
-    flat = torch.tensor([x for t in token_lists for x in t] or [0], dtype=torch.int32, device=device)
+    if lens and all(isinstance(t, torch.Tensor) for t in token_lists):  # no host round trip per token
+        flat = torch.cat([t.reshape(-1).to(device=device, dtype=torch.int32) for t in token_lists])
+        if flat.numel() == 0:
+            flat = torch.zeros(1, dtype=torch.int32, device=device)
+    else:
+        flat = torch.tensor([int(x) for t in token_lists for x in t] or [0], dtype=torch.int32, device=device)
     pos = torch.empty(max(total, 1), dtype=torch.int32, device=device)
     seg = torch.empty(max(total, 1), dtype=torch.int32, device=device)
     excl = torch.empty((max(total, 1), max_depth, 2), dtype=torch.int32, device=device)
@@ -81,7 +86,8 @@ def build_visibility_batch(token_lists, max_depth: int = DEFAULT_MAX_DEPTH, devi
 
 def build_visibility(tokens, max_depth: int = DEFAULT_MAX_DEPTH, device="cuda") -> VisibilitySpec:
     """Positions + compact mask of one tag stream; raises ParseError like grammar::parse."""
-    res, st = build_visibility_batch([list(tokens)], max_depth, device)
+    res, st = build_visibility_batch([tokens if isinstance(tokens, torch.Tensor) else list(tokens)], max_depth,
+                                     device)
     if st[0] != 0:
         check(st[0]) if st[0] not in ParseError.KINDS else None
         raise ParseError(st[0], f"tag stream rejected: {ParseError.KINDS.get(st[0], st[0])}")
