@@ -349,8 +349,8 @@ def run_ours(args):
     try:
         with open(os.path.join(REPO, "profiles", "decode_traffic.json")) as f:
             tj = json.load(f)
-            if tj.get("requests") == R:
-                traffic = tj.get("dram_bytes_per_launch")
+            if tj.get("requests") == R and args.workload == "c2" and not heads_mode:
+                traffic = tj["per_kernel_bytes"].get(tj.get("dominant_kernel", ""), tj.get("dram_bytes_per_launch"))
     except Exception:
         pass
 
