@@ -460,9 +460,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
     // Two independent streams on two lanes (their issue latencies overlap): lane 0 copies K
     // blocks, lane 1 V blocks (one 4 KiB bulk copy per page-head).  K slots free after Q.K^T,
     // V slots after P.V.  L2 prefetching is the stager's job.
-    if (lane < 2) {
+    if (lane < 8) {
+      // lanes 0-3 stream K, lanes 4-7 stream V; lane p of a group copies page p of each 4-page
+      // block (tools/microbench/mb_gather.cu: random 4 KiB bulk copies need several issuing
+      // lanes to approach the HBM bandwidth)
       const size_t page_stride = (size_t)P.kv_heads * kPageTokens * kHeadDim;
-      const bool is_k = lane == 0;
+      const bool is_k = lane < 4;
+      const int sub = lane & 3;
+      const unsigned gmask = is_k ? 0x0Fu : 0xF0u;
       const int nsl = is_k ? kKSlots : kVSlots;
       uint64_t* fb = is_k ? kfull : vfull;
       uint64_t* eb = is_k ? kempty : vempty;
@@ -479,15 +484,17 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         const PageRef* se = s_ent0 + buf * kMaxEntries;
         for (int e0 = 0; e0 < n_ent; e0 += kBlkPages, ++g) {
           const int sl = g % nsl, np = min(kBlkPages, n_ent - e0);
-          if (TRACE && is_k && g < 64) P.trace[blockIdx.x * kTraceWords + 544 + g] = globaltimer();
+          if (TRACE && is_k && sub == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 544 + g] = globaltimer();
           if (g >= nsl) mbar_wait(&eb[sl], ((g / nsl) - 1) & 1);
           uint8_t* dst = rb + sl * kSlotBytes;
-          mbar_arrive_expect_tx(&fb[sl], (uint32_t)np * kPageBytes);
-          for (int p = 0; p < np; ++p)
-            bulk_g2s(dst + p * kPageBytes, plane + (size_t)se[e0 + p].page * page_stride + head_off, kPageBytes,
+          if (sub == 0) mbar_arrive_expect_tx(&fb[sl], (uint32_t)np * kPageBytes);
+          __syncwarp(gmask);  // the expected bytes are registered before any copy can complete
+          if (sub < np)
+            bulk_g2s(dst + sub * kPageBytes, plane + (size_t)se[e0 + sub].page * page_stride + head_off, kPageBytes,
                      &fb[sl]);
         }
-        mbar_arrive(&slot_empty[buf]);  // this stream no longer reads the unit's entries
+        __syncwarp(gmask);
+        if (sub == 0) mbar_arrive(&slot_empty[buf]);  // this stream no longer reads the unit's entries
       }
     }
   } else if (warp == kWarpQk) {
