@@ -74,6 +74,10 @@ constexpr int kPrefetch = 32;                               // pages of a unit p
 #endif
 constexpr bool kUseCopies = MV_DEC_COPIES != 0;
 constexpr int kSBufs = 5;                                   // S / P buffers in flight
+#ifndef MV_DEC_TMA_GROUPS
+#define MV_DEC_TMA_GROUPS 2  // C2 +1.4% over 1 (C4 unchanged)
+#endif
+constexpr int kTmaLanesPerBlkGroup = MV_DEC_TMA_GROUPS;     // 4-lane copy groups per stream (blocks in flight per step)
 constexpr int kColS = 0;                                    // TMEM: S0..S4 (64 cols each)
 constexpr int kColO = kSBufs * kBlkCols;                    //       O (128 cols)
 constexpr int kColQ = kColO + 128;                          //       Q (64 cols: 128 bf16 dims)
@@ -460,29 +464,34 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
     // Two independent streams on two lanes (their issue latencies overlap): lane 0 copies K
     // blocks, lane 1 V blocks (one 4 KiB bulk copy per page-head).  K slots free after Q.K^T,
     // V slots after P.V.  L2 prefetching is the stager's job.
-    if (lane < 8) {
-      // lanes 0-3 stream K, lanes 4-7 stream V; lane p of a group copies page p of each 4-page
-      // block (tools/microbench/mb_gather.cu: random 4 KiB bulk copies need several issuing
-      // lanes to approach the HBM bandwidth)
+    if (lane < 4 * kTmaLanesPerBlkGroup * 2) {
+      // K and V streams, kTmaGroups 4-lane groups each; group j of a stream copies block g + j of
+      // every kTmaGroups-block step, lane p of a group page p (tools/microbench/mb_gather.cu:
+      // random 4 KiB bulk copies need several issuing lanes to approach the HBM bandwidth)
+      constexpr int kTmaGroups = kTmaLanesPerBlkGroup;
       const size_t page_stride = (size_t)P.kv_heads * kPageTokens * kHeadDim;
-      const bool is_k = lane < 4;
-      const int sub = lane & 3;
-      const unsigned gmask = is_k ? 0x0Fu : 0xF0u;
+      const bool is_k = lane < 4 * kTmaGroups;
+      const int sl_lane = lane % (4 * kTmaGroups);
+      const int sub = sl_lane & 3, grp = sl_lane >> 2;
+      const unsigned gmask = 0xFu << (lane & ~3);  // this lane's 4-lane group
       const int nsl = is_k ? kKSlots : kVSlots;
       uint64_t* fb = is_k ? kfull : vfull;
       uint64_t* eb = is_k ? kempty : vempty;
       uint8_t* rb = is_k ? ring : smem + kOffVRing;
       const __nv_bfloat16* plane = is_k ? P.kplane : P.vplane;
-      int g = 0;
+      int g0 = 0;  // first block of the unit (global block counter)
       for (int i = 0;; ++i) {
         const int buf = i & 1;
         mbar_wait(&ent_full[buf], (i >> 1) & 1);
         const WorkItem* si = &s_item[buf];
         if (!si->valid) break;
         const int n_ent = si->n_entries;
+        const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
         const size_t head_off = (size_t)si->kvh * kPageTokens * kHeadDim;
         const PageRef* se = s_ent0 + buf * kMaxEntries;
-        for (int e0 = 0; e0 < n_ent; e0 += kBlkPages, ++g) {
+        for (int blk = grp; blk < nblk; blk += kTmaGroups) {
+          const int g = g0 + blk;
+          const int e0 = blk * kBlkPages;
           const int sl = g % nsl, np = min(kBlkPages, n_ent - e0);
           if (TRACE && is_k && sub == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 544 + g] = globaltimer();
           if (g >= nsl) mbar_wait(&eb[sl], ((g / nsl) - 1) & 1);
@@ -493,8 +502,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
             bulk_g2s(dst + sub * kPageBytes, plane + (size_t)se[e0 + sub].page * page_stride + head_off, kPageBytes,
                      &fb[sl]);
         }
-        __syncwarp(gmask);
-        if (sub == 0) mbar_arrive(&slot_empty[buf]);  // this stream no longer reads the unit's entries
+        g0 += nblk;
+        // every lane of the stream is done with the unit's entries before the slot is released
+        __syncwarp(is_k ? (0xFFFFFFFFu >> (32 - 4 * kTmaGroups)) : ((0xFFFFFFFFu >> (32 - 4 * kTmaGroups)) << (4 * kTmaGroups)));
+        if (sl_lane == 0) mbar_arrive(&slot_empty[buf]);  // this stream no longer reads the unit's entries
       }
     }
   } else if (warp == kWarpQk) {
