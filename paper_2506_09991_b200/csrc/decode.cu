@@ -727,31 +727,51 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
 // Split-KV combine for handles with more than one partial slot: one warp per (handle, q head),
 // float4 per lane, log-sum-exp over the handle's slots (single-slot handles were written by the
 // decode epilogue directly).
-__global__ void combine_kernel(const float* __restrict__ part_o, const float2* __restrict__ part_ml,
-                               const int32_t* __restrict__ multi, int n_multi, const int32_t* __restrict__ slot_ptr,
-                               const int32_t* __restrict__ slot_idx, int q_heads, void* __restrict__ out,
-                               int out_f32) {
+constexpr int kCombineWarps = 4;
+__global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(
+    const float* __restrict__ part_o, const float2* __restrict__ part_ml, const int32_t* __restrict__ multi,
+    int n_multi, const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ slot_idx, int q_heads,
+    void* __restrict__ out, int out_f32) {
   pdl_wait();  // programmatic launch behind decode_tc_kernel: its partials are visible after this
-  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (wid >= n_multi * q_heads) return;
-  const int b = multi[wid / q_heads], h = wid % q_heads;
+  // one CTA per (handle, q head); warp w merges slots w, w + 4, ... online (log-sum-exp), two
+  // slots' loads in flight, then warp 0 merges the four partial states (a long single context
+  // has one slot per split-KV chunk: 132 at the 135K-token C5 context)
+  __shared__ float s_m[kCombineWarps], s_l[kCombineWarps];
+  __shared__ float4 s_acc[kCombineWarps][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = multi[blockIdx.x / q_heads], h = blockIdx.x % q_heads;
   const int s0 = slot_ptr[b], s1 = slot_ptr[b + 1];
-  float m = -INFINITY;
-  for (int s = s0; s < s1; ++s) m = fmaxf(m, part_ml[(int64_t)slot_idx[s] * q_heads + h].x);
-  const float mu = m == -INFINITY ? 0.f : m;
-  float l = 0.f;
+  float m = -INFINITY, l = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int s = s0; s < s1; ++s) {
-    const int64_t sl = slot_idx[s];
-    const float2 ml = part_ml[sl * q_heads + h];
-    const float w = fast_exp2(ml.x - mu);
-    const float4 v = *reinterpret_cast<const float4*>(&part_o[(sl * q_heads + h) * kHeadDim + lane * 4]);
-    acc.x += w * v.x;
-    acc.y += w * v.y;
-    acc.z += w * v.z;
-    acc.w += w * v.w;
-    l += w * ml.y;
+  auto merge = [&](float2 ml, float4 v) {
+    if (ml.x == -INFINITY) return;
+    const float nm = fmaxf(m, ml.x);
+    const float a = m == -INFINITY ? 0.f : fast_exp2(m - nm), w = fast_exp2(ml.x - nm);
+    acc = make_float4(acc.x * a + w * v.x, acc.y * a + w * v.y, acc.z * a + w * v.z, acc.w * a + w * v.w);
+    l = l * a + w * ml.y;
+    m = nm;
+  };
+  for (int s = s0 + warp; s < s1; s += 2 * kCombineWarps) {
+    const int64_t sa = slot_idx[s];
+    const bool two = s + kCombineWarps < s1;
+    const int64_t sb = two ? slot_idx[s + kCombineWarps] : sa;
+    const float2 mla = part_ml[sa * q_heads + h], mlb = part_ml[sb * q_heads + h];
+    const float4 va = *reinterpret_cast<const float4*>(&part_o[(sa * q_heads + h) * kHeadDim + lane * 4]);
+    const float4 vb = *reinterpret_cast<const float4*>(&part_o[(sb * q_heads + h) * kHeadDim + lane * 4]);
+    merge(mla, va);
+    if (two) merge(mlb, vb);
   }
+  if (lane == 0) {
+    s_m[warp] = m;
+    s_l[warp] = l;
+  }
+  s_acc[warp][lane] = acc;
+  __syncthreads();
+  if (warp != 0) return;
+  m = -INFINITY;
+  l = 0.f;
+  acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int w = 0; w < kCombineWarps; ++w) merge(make_float2(s_m[w], s_l[w]), s_acc[w][lane]);
   const float inv = l > 0.f ? 1.f / l : 0.f;
   const int64_t at = ((int64_t)b * q_heads + h) * kHeadDim + lane * 4;
   if (out_f32) {
@@ -1180,9 +1200,8 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   else MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel<false>, P));
   MV_LAUNCH_CHECK();
   if (!pc.multi.empty()) {
-    const int warps = (int)pc.multi.size() * q_heads;
-    lc.gridDim = dim3((warps + 7) / 8);
-    lc.blockDim = dim3(256);
+    lc.gridDim = dim3((unsigned)(pc.multi.size() * q_heads));  // one CTA per (handle, q head)
+    lc.blockDim = dim3(32 * kCombineWarps);
     lc.dynamicSmemBytes = 0;
     MV_CUDA_TRY(cudaLaunchKernelEx(&lc, combine_kernel, (const float*)pc.d_part_o, (const float2*)pc.d_part_ml,
                                    (const int32_t*)pc.d_multi, (int)pc.multi.size(), (const int32_t*)pc.d_slot_ptr,
