@@ -938,9 +938,10 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
     add_seg(r->arena_off, prev_e, r->n_entries(), std::vector<int32_t>{b}, r->n_tokens() - prev_t, b);
   }
 
-  // split-KV chunk: the largest power of two <= 256 pages that still gives >= 4 waves of units
-  // over the SMs (C2 sweep: 96-256 pages 1.3% faster than 64; 32-48 slower: more partials)
-  const int64_t target_units = (int64_t)num_sms * 4;
+  // split-KV chunk: the largest power of two <= 256 pages that still gives >= 1.5 waves of units
+  // over the SMs.  Sweeps (with the parallel combine): C5's single 135K context 0.123 ms at 256
+  // pages vs 0.138 at 64; C2 and C4 best at 128-256.  Fewer, longer units mean fewer partials.
+  const int64_t target_units = (int64_t)num_sms * 3 / 2;
   int chunk = kMaxChunk;
   while (chunk > 16 && total_pages * kv_heads / chunk < target_units) chunk /= 2;
   if (const char* e = getenv("MV_DECODE_CHUNK")) chunk = std::max(4, std::min(kMaxChunk, atoi(e)));  // A/B knob
