@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __res
                                                       const __nv_bfloat16* __restrict__ k,
                                                       const int32_t* __restrict__ pos, int n, int hq, int hkv,
                                                       const RopeTable rt, __nv_bfloat16* __restrict__ q_rot,
-                                                      __nv_bfloat16* __restrict__ k_rot) {
+                                                      __nv_bfloat16* __restrict__ k_rot, float2* __restrict__ table) {
   __shared__ double s_inv[kHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -43,6 +43,11 @@ __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __res
   float cs[4], sn[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) rope_cs(p, inv[c * 4 + j], cs[j], sn[j]);
+  if (table) {  // (cos, sin) per row and pair for the prefill kernel's in-place Q rotation
+    float4* tb = reinterpret_cast<float4*>(table + (size_t)row * 64 + c * 4);
+    tb[0] = make_float4(cs[0], sn[0], cs[1], sn[1]);
+    tb[1] = make_float4(cs[2], sn[2], cs[3], sn[3]);
+  }
   auto rot = [&](uint4 v) {
     __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
 #pragma unroll
@@ -57,18 +62,19 @@ __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __res
   // q heads then k heads as one sequence of 16-byte chunks, 8 independent loads in flight
   const uint4* ks = reinterpret_cast<const uint4*>(k + (size_t)row * hkv * kHeadDim) + c;
   uint4* kd = reinterpret_cast<uint4*>(k_rot + (size_t)row * hkv * kHeadDim) + c;
-  const int nh = hq + hkv;
+  const int nq = q_rot ? hq : 0;  // without q_rot only K is rotated (Q rotates in the kernel)
+  const int nh = nq + hkv;
   for (int h0 = 0; h0 < nh; h0 += 8) {
     uint4 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int h = h0 + u;
-      if (h < nh) v[u] = __ldg(h < hq ? qs + h * 16 : ks + (h - hq) * 16);
+      if (h < nh) v[u] = __ldg(h < nq ? qs + h * 16 : ks + (h - nq) * 16);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int h = h0 + u;
-      if (h < nh) *(h < hq ? qd + h * 16 : kd + (h - hq) * 16) = rot(v[u]);
+      if (h < nh) *(h < nq ? qd + h * 16 : kd + (h - nq) * 16) = rot(v[u]);
     }
   }
 }
@@ -287,10 +293,10 @@ namespace mv {
 mv_status prefill_tc2_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
                              const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
                              void* d_out, int32_t out_dtype, int32_t* tcount, int32_t* tlist, cudaStream_t st);
-mv_status prefill_tc3_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
-                             const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
-                             void* d_out, int32_t out_dtype, const int32_t* hcount, const int32_t* tlist,
-                             int32_t stride, cudaStream_t st);
+mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
+                             const float2* cs, const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
+                             int32_t kv_heads, void* d_out, int32_t out_dtype, const int32_t* hcount,
+                             const int32_t* tlist, int32_t stride, cudaStream_t st);
 mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
                     int32_t stride, cudaStream_t stream, int32_t* d_hcount, int32_t* d_hlist);
 }
@@ -301,7 +307,9 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 extern "C" size_t mv_prefill_workspace_size(int32_t n, int32_t q_heads, int32_t kv_heads) {
   const size_t n_qt = (size_t)(n + kBM - 1) / kBM;
-  return align256((size_t)n * q_heads * kHeadDim * 2) + align256((size_t)n * kv_heads * kHeadDim * 2) +
+  // region 1: rotated Q (v0 / v2) or the per-row RoPE (cos, sin) table (v3: n x 64 float2)
+  return align256(std::max((size_t)n * q_heads * kHeadDim * 2, (size_t)n * 64 * sizeof(float2))) +
+         align256((size_t)n * kv_heads * kHeadDim * 2) +
          align256(n_qt * 4) + align256(n_qt * n_qt * 4) + align256(8);
 }
 
@@ -322,7 +330,7 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
   const int n_qt = (n + kBM - 1) / kBM;
   uint8_t* ws = reinterpret_cast<uint8_t*>(d_workspace);
   __nv_bfloat16* q_rot = reinterpret_cast<__nv_bfloat16*>(ws);
-  ws += align256((size_t)n * q_heads * kHeadDim * 2);
+  ws += align256(std::max((size_t)n * q_heads * kHeadDim * 2, (size_t)n * 64 * sizeof(float2)));
   __nv_bfloat16* k_rot = reinterpret_cast<__nv_bfloat16*>(ws);
   ws += align256((size_t)n * kv_heads * kHeadDim * 2);
   int32_t* tcount = reinterpret_cast<int32_t*>(ws);
@@ -352,14 +360,18 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
       return e;
     MV_CUDA_TRY(cudaEventRecord(ev_join, side));
   }
+  // v3 rotates Q in the kernel from a per-row (cos, sin) table (written into the q_rot region)
+  float2* cs_table = reinterpret_cast<float2*>(q_rot);
   rope_qk_kernel<<<(unsigned)(((int64_t)n * 16 + 255) / 256), 256, 0, st>>>(
-      (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_k, d_positions, n, q_heads, kv_heads, rt, q_rot, k_rot);
+      (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_k, d_positions, n, q_heads, kv_heads, rt,
+      v3 ? nullptr : q_rot, k_rot, v3 ? cs_table : nullptr);
   MV_LAUNCH_CHECK();
 
   if (v3) {  // tcgen05 v3 (prefill_tc3.cu)
     MV_CUDA_TRY(cudaStreamWaitEvent(st, ev_join, 0));
-    return prefill_tc3_launch(q_rot, k_rot, (const __nv_bfloat16*)d_v, d_excl, max_depth, n, q_heads, kv_heads, d_out,
-                              out_dtype, hcount, tlist + (size_t)n_qp * stride, stride, st);
+    return prefill_tc3_launch((const __nv_bfloat16*)d_q, k_rot, (const __nv_bfloat16*)d_v, cs_table, d_excl, max_depth,
+                              n, q_heads, kv_heads, d_out, out_dtype, hcount, tlist + (size_t)n_qp * stride, stride,
+                              st);
   }
   MV_CUDA_TRY(cudaMemsetAsync(vis, 0, 8, st));
   if (!getenv("MV_PREFILL_V0"))  // tcgen05 v2 (prefill_tc.cu) and v0 kept for A/B diagnostics

@@ -38,32 +38,30 @@ namespace {
 constexpr int kT3 = 128;
 constexpr int kKSt3 = 3;
 constexpr int kVSt3 = 2;
-constexpr int kThreads3 = 320;
+constexpr int kThreads3 = 384;   // 12 warps: loader, MMA, 8 softmax, 2 Q rotators
+constexpr int kRotWarp0 = 10;    // warps 10-11 rotate each item's raw Q tile in shared memory
 constexpr int kHalf3 = kT3 * 128;  // SW128 half tile: 128 rows x 64 dims
 constexpr int kTile3 = 2 * kHalf3;
-constexpr int kOffQ3 = 0;  // one Q tile: the next item's loads once this item's last Q.K^T is issued
-constexpr int kOffK3 = kOffQ3 + kTile3;
+constexpr int kOffQ3 = 0;  // two Q tiles: item i loads and rotates into tile i & 1
+constexpr int kOffK3 = kOffQ3 + 2 * kTile3;
 constexpr int kOffV3 = kOffK3 + kKSt3 * kTile3;
 constexpr int kOffBar3 = kOffV3 + kVSt3 * kTile3;
 constexpr int kOffX3 = kOffBar3 + 512;  // row max / sum exchange: [2 parity][2 WG][128 rows] f32
-constexpr int kSmem3 = kOffX3 + 2 * 2 * 128 * 4 + 1024;
+// no alignment slack: the dynamic shared memory base is 1024-aligned here (checked at entry)
+constexpr int kSmem3 = kOffX3 + 2 * 2 * 128 * 4;
+static_assert(kSmem3 <= 227 * 1024, "prefill v3 smem");
 constexpr uint32_t kIdQK3 = tc::idesc_bf16(128, 128, 0, 0);
 constexpr uint32_t kIdPV3 = tc::idesc_bf16(128, 128, 0, 1);
 constexpr float kLazy3 = 8.f;
-#ifndef MV_PF_QTMEM
-#define MV_PF_QTMEM 0
-#endif
-// TMEM columns: three S buffers (S(g) in buffer g % 3) and one O; or, with Q in TMEM (A operand
-// of Q.K^T read from TMEM: halves the smem operand traffic of the SS form), two S buffers, O and
-// the Q tile (64 packed columns).
-constexpr bool kQT = MV_PF_QTMEM != 0;
-constexpr int kSB = kQT ? 2 : 3;
-constexpr uint32_t kS0 = 0, kO0 = kSB * 128, kQ0 = kO0 + 128;
+// TMEM columns: three S buffers (S(g) in buffer g % 3) and one O
+constexpr int kSB = 3;
+constexpr uint32_t kS0 = 0, kO0 = kSB * 128;
 
 struct Tc3Params {
   const int32_t* excl;
   const int32_t* hcount;  // [n_qt] processed k tiles per 128-row q tile
   const int32_t* tlist;   // [n_qt][stride] per-tile lists from tile_map2
+  const float2* cs;        // [n][64] RoPE (cos, sin) per row and pair, from the K pre-pass
   void* out;
   int out_f32;
   int n, hq, hkv, D, n_qt, stride;
@@ -93,8 +91,7 @@ __device__ __forceinline__ void qk3(uint64_t qd, uint64_t kd) {
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint64_t off = (uint64_t)(((k >> 2) * kHalf3 + (k & 3) * 32) >> 4);
-    if (kQT) tc::mma_ts(kS0 + B * 128, kQ0 + k * 8, kd + off, kIdQK3, k > 0 ? 1u : 0u);
-    else tc::mma_ss(kS0 + B * 128, qd + off, kd + off, kIdQK3, k > 0 ? 1u : 0u);
+    tc::mma_ss(kS0 + B * 128, qd + off, kd + off, kIdQK3, k > 0 ? 1u : 0u);
   }
 }
 template <int B>
@@ -140,10 +137,12 @@ __global__ void __launch_bounds__(kThreads3, 1)
                        const __grid_constant__ CUtensorMap map_v, Tc3Params P) {
   extern __shared__ uint8_t smem_raw3[];
   uint8_t* smem = smem_align1024(smem_raw3);
+  if (smem != smem_raw3) __trap();  // no slack was allocated for alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar3);
-  uint64_t* q_full = bars;               // Q tile landed (tx)
-  uint64_t* q_empty = q_full + 1;        // MMA commit after the item's last Q.K^T
-  uint64_t* k_full = q_empty + 1;        // [3]
+  uint64_t* q_loaded = bars;             // [2] raw Q tile landed (tx)
+  uint64_t* q_full = q_loaded + 2;       // [2] Q tile rotated (2 rotator warps)
+  uint64_t* q_empty = q_full + 2;        // [2] MMA commit after the item's last Q.K^T
+  uint64_t* k_full = q_empty + 2;        // [3]
   uint64_t* k_empty = k_full + kKSt3;    // [3]
   uint64_t* v_full = k_empty + kKSt3;    // [2]
   uint64_t* v_empty = v_full + kVSt3;    // [2] MMA commit after P.V (also certifies O for the rescale)
@@ -159,8 +158,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&q_loaded[b], 1);
+      mbar_init(&q_full[b], 2);
+      mbar_init(&q_empty[b], 1);
+    }
     mbar_init(o_fin, 1);
     mbar_init(o_empty, 256);
     for (int b = 0; b < kSB; ++b) {
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&item_full[b], 1);
-      mbar_init(&slot_empty[b], 10);
+      mbar_init(&slot_empty[b], 12);  // V lane, MMA, 8 softmax warps, 2 rotator warps
     }
     for (int s = 0; s < kKSt3; ++s) {
       mbar_init(&k_full[s], 1);
@@ -214,10 +216,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
         mbar_arrive(&item_full[buf]);
         if (!it.valid) break;
         claim(nxt);
-        if (i >= 1) mbar_wait(q_empty, (i - 1) & 1);
-        mbar_arrive_expect_tx(q_full, kTile3);
-        tc::tma_load_3d(smem + kOffQ3, &map_q, 0, it.h, it.t * kT3, q_full);
-        tc::tma_load_3d(smem + kOffQ3 + kHalf3, &map_q, 64, it.h, it.t * kT3, q_full);
+        // raw (pre-RoPE) Q into tile buf once item i-2's last Q.K^T has read it
+        if (i >= 2) mbar_wait(&q_empty[buf], ((i >> 1) - 1) & 1);
+        mbar_arrive_expect_tx(&q_loaded[buf], kTile3);
+        tc::tma_load_3d(smem + kOffQ3 + buf * kTile3, &map_q, 0, it.h, it.t * kT3, &q_loaded[buf]);
+        tc::tma_load_3d(smem + kOffQ3 + buf * kTile3 + kHalf3, &map_q, 64, it.h, it.t * kT3, &q_loaded[buf]);
         const int kvh = it.h / (P.hq / P.hkv);
         const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
         for (int j = 0; j < it.m; ++j) {
@@ -280,17 +283,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
         mbar_arrive(&slot_empty[buf]);
         if (!it.valid) break;
         const int m = it.m;
-        const uint64_t qd = qd0;
-        mbar_wait(q_full, i & 1);
-        if (kQT) {  // Q tile smem -> TMEM (in order behind the previous item's Q.K^T), smem freed
-          tc::fence_after();
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
-            tc::cp_128x256b(kQ0 + k * 8, qd + (uint64_t)(((k >> 2) * kHalf3 + (k & 3) * 32) >> 4));
-          tc::mma_commit(q_empty);
-        }
+        const uint64_t qd = qd0 + (uint64_t)((buf * kTile3) >> 4);
+        mbar_wait(&q_full[buf], (i >> 1) & 1);  // rotated by warps 10-11 (generic -> async proxy fenced)
         for (int u = 0; u < kSB && u < m; ++u) qk(qd, g + u);
-        if (!kQT && m <= kSB) tc::mma_commit(q_empty);
+        if (m <= kSB) tc::mma_commit(&q_empty[buf]);
         for (int j = 0; j < m; ++j, ++g) {
           mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
           mbar_wait(&p_full[g % kSB], (g / kSB) & 1);
@@ -305,13 +301,49 @@ __global__ void __launch_bounds__(kThreads3, 1)
           tc::mma_commit(&v_empty[g % kVSt3]);
           if (j + kSB < m) {
             qk(qd, g + kSB);  // S buffer g % 3 again: in order behind P.V(g)
-            if (!kQT && j + kSB + 1 == m) tc::mma_commit(q_empty);
+            if (j + kSB + 1 == m) tc::mma_commit(&q_empty[buf]);
           }
           PF3_TRACE(g, 1);
         }
         if (m == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);
         tc::mma_commit(o_fin);
       }
+    }
+  } else if (warp >= kRotWarp0) {
+    // ---------------- Q rotators: interleaved RoPE of the raw Q tile, in place ----------------
+    // thread = 16-byte chunk (4 dim pairs) of a row; SW128: chunk c of row r sits at c ^ (r & 7)
+    // of the row's 128 B in half c >> 3.  Same fp32 arithmetic as the pre-pass (rope_cs values
+    // from the per-row table), so rotated Q is bit-identical to rope_qk_kernel's.
+    const int rt = threadIdx.x - kRotWarp0 * 32;  // 0..63
+    for (int it_i = 0;; ++it_i) {
+      const int buf = it_i & 1;
+      mbar_wait(&item_full[buf], (it_i >> 1) & 1);
+      const Item3 it = s_item[buf];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slot_empty[buf]);
+      if (!it.valid) break;
+      mbar_wait(&q_loaded[buf], (it_i >> 1) & 1);
+      uint8_t* qt = smem + kOffQ3 + buf * kTile3;
+#pragma unroll 4
+      for (int ch = rt; ch < kT3 * 16; ch += 64) {
+        const int row = ch >> 4, c = ch & 15;
+        const int grow = min(it.t * kT3 + row, P.n - 1);  // rows past n are zero-filled: any angle
+        uint4* q4 = reinterpret_cast<uint4*>(qt + (c >> 3) * kHalf3 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
+        const float4* tb = reinterpret_cast<const float4*>(P.cs + (size_t)grow * 64 + c * 4);
+        const float4 t01 = __ldg(tb), t23 = __ldg(tb + 1);
+        uint4 v = *q4;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+        const float cs[4] = {t01.x, t01.z, t23.x, t23.z}, sn[4] = {t01.y, t01.w, t23.y, t23.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 ab = __bfloat1622float2(h2[j]);
+          h2[j] = __floats2bfloat162_rn(ab.x * cs[j] - ab.y * sn[j], ab.x * sn[j] + ab.y * cs[j]);
+        }
+        *q4 = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&q_full[buf]);
     }
   } else {
     // ---------------- softmax: warps 2-5 columns 0-63, warps 6-9 columns 64-127 ----------------
@@ -489,19 +521,20 @@ __global__ void __launch_bounds__(kThreads3, 1)
 }  // namespace
 
 // v3 launch on rotated q/k and the caller's v; tcount / tlist / hcount from tile_map2.
-mv_status prefill_tc3_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
-                             const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
-                             void* d_out, int32_t out_dtype, const int32_t* hcount, const int32_t* tlist,
-                             int32_t stride, cudaStream_t st) {
+mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
+                             const float2* cs, const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
+                             int32_t kv_heads, void* d_out, int32_t out_dtype, const int32_t* hcount,
+                             const int32_t* tlist, int32_t stride, cudaStream_t st) {
   if (max_depth > 8) return fail(MV_ERR_INVALID_ARGUMENT, "prefill: max_depth > 8");
   CUtensorMap mq, mk, mvv;
-  if (mv_status e = tc::make_rows_map(&mq, q_rot, n, q_heads, kT3)) return e;
+  if (mv_status e = tc::make_rows_map(&mq, q_raw, n, q_heads, kT3)) return e;
   if (mv_status e = tc::make_rows_map(&mk, k_rot, n, kv_heads, kT3)) return e;
   if (mv_status e = tc::make_rows_map(&mvv, v, n, kv_heads, kT3)) return e;
   Tc3Params T;
   T.excl = d_excl;
   T.hcount = hcount;
   T.tlist = tlist;
+  T.cs = cs;
   T.out = d_out;
   T.out_f32 = out_dtype == 1;
   T.n = n;
