@@ -416,36 +416,40 @@ __global__ void tile_map_kernel(const int32_t* __restrict__ excl, int n, int D, 
 // B), one thread per row; for every 128-token k tile it records the status of each half
 // (0 skip, 1 full, 2 partial) and keeps the tile when either half needs it:
 //   list[qp][k] = kt | statusA << 20 | statusB << 22.
-constexpr int kTm2Chunk = 1024;  // k tiles classified per pass (flags in shared memory)
-constexpr int kTm2Threads = 1024;  // 4 groups of 256 (one thread per row) share the k tiles
+// Paired tile map in two kernels: (A) status of every (256-row q pair, k tile) on many CTAs,
+// (B) one CTA per q pair compacts the statuses into the ordered lists.
+constexpr int kTm2Split = 8;        // k-tile ranges per q pair in kernel A
+constexpr int kTm2Chunk = 1024;     // k tiles compacted per pass in kernel B
+constexpr int kTm2Threads = 1024;
 
-__global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* __restrict__ excl, int n, int D,
-                                                                int32_t* __restrict__ count,
-                                                                int32_t* __restrict__ list, int stride,
-                                                                int32_t* __restrict__ hcount,
-                                                                int32_t* __restrict__ hlist) {
-  const int qp = blockIdx.x;
+// A: thread = row of the pair (256 per CTA), CTA = (q pair, k-tile range); per warp and k tile
+// the rows vote all-empty / all-full, the block combines the 4 warps of each 128-row half.
+// status[qp][kt] = stA | stB << 2 (0 skip, 1 full, 2 partial).
+__global__ void __launch_bounds__(256) tile_status_kernel(const int32_t* __restrict__ excl, int n, int D,
+                                                          uint8_t* __restrict__ status, int stride) {
+  const int qp = blockIdx.x, part = blockIdx.y;
   const int tile = 128;
-  const int r = threadIdx.x & 255, grp = threadIdx.x >> 8;
+  const int r = threadIdx.x, warp = r >> 5, lane = r & 31;
   const int i = qp * 256 + r;
-  const int rw = r >> 5, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool row_ok = i < n;
+  // the row's intervals in registers (fixed trip count); empty intervals never intersect
   int lo[8], hi[8];
-  int nd = 0;
-  if (row_ok) {
-    for (int q = 0; q < D && q < 8; ++q) {
-      int a = excl[((int64_t)i * D + q) * 2], b = excl[((int64_t)i * D + q) * 2 + 1];
-      if (a < b) { lo[nd] = a; hi[nd] = b; ++nd; }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    lo[q] = hi[q] = 0;
+    if (row_ok && q < D) {
+      lo[q] = excl[((int64_t)i * D + q) * 2];
+      hi[q] = excl[((int64_t)i * D + q) * 2 + 1];
     }
   }
-  // per 32-row warp and k tile: all rows empty / all rows full (no block barrier per k tile)
-  __shared__ uint8_t s_e[8][kTm2Chunk], s_f[8][kTm2Chunk];
-  __shared__ int s_warp_sum[3][kTm2Threads / 32];
-  const int last_kt = min((qp * 256 + 255) / tile, (n - 1) / tile);
-  int written = 0, nA = 0, nB = 0;
-  for (int kt0 = 0; kt0 <= last_kt; kt0 += kTm2Chunk) {
-    const int kt1 = min(last_kt + 1, kt0 + kTm2Chunk);
-    for (int kt = kt0 + grp; kt < kt1; kt += kTm2Threads / 256) {
+  const int n_kt = min((qp * 256 + 255) / tile, (n - 1) / tile) + 1;
+  const int per = (n_kt + kTm2Split - 1) / kTm2Split;
+  const int kt0 = part * per, kt1 = min(n_kt, kt0 + per);
+  __shared__ uint8_t s_e[8][64], s_f[8][64];
+  for (int base = kt0; base < kt1; base += 64) {
+    const int cnt = min(64, kt1 - base);
+    for (int u = 0; u < cnt; ++u) {
+      const int kt = base + u;
       const int j0 = kt * tile, j1 = min(n, j0 + tile);
       bool empty = true, full = true;
       if (row_ok) {
@@ -455,8 +459,9 @@ __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* _
         } else {
           int vis = lastc - j0 + 1;
           bool touches = false;
-          for (int q = 0; q < nd; ++q) {
-            int a = max(lo[q], j0), b = min(hi[q], lastc + 1);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int a = max(lo[q], j0), b = min(hi[q], lastc + 1);
             if (a < b) { vis -= b - a; touches = true; }
           }
           empty = vis == 0;
@@ -465,30 +470,49 @@ __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* _
       }
       const bool we = __all_sync(0xffffffffu, empty), wf = __all_sync(0xffffffffu, full);
       if (lane == 0) {
-        s_e[rw][kt - kt0] = we;
-        s_f[rw][kt - kt0] = wf;
+        s_e[warp][u] = we;
+        s_f[warp][u] = wf;
       }
     }
     __syncthreads();
-    // status per k tile (row warps 0-3 -> half A, 4-7 -> half B); one tile per thread
-    const int kt = kt0 + threadIdx.x;
-    int ent = -1;
-    if (kt < kt1) {
+    if (r < cnt) {
       int st[2];
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         bool all_e = true, all_f = true;
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          all_e &= s_e[hh * 4 + w][kt - kt0] != 0;
-          all_f &= s_f[hh * 4 + w][kt - kt0] != 0;
+          all_e &= s_e[hh * 4 + w][r] != 0;
+          all_f &= s_f[hh * 4 + w][r] != 0;
         }
         st[hh] = all_e ? 0 : (all_f ? 1 : 2);
       }
-      if (st[0] || st[1]) ent = kt | (st[0] << 20) | (st[1] << 22);
+      status[(int64_t)qp * stride + base + r] = (uint8_t)(st[0] | (st[1] << 2));
     }
-    // ordered compactions: the pair list, and (for the one-tile-per-item kernel) one list per
-    // 128-row half holding only the k tiles whose status for that half is not 0
+    __syncthreads();
+  }
+}
+
+// B: ordered compactions of one q pair's statuses: the pair list, and one list per 128-row half
+// holding only the k tiles whose status for that half is not 0 (with the per-half counts).
+//   list[qp][k] = kt | statusA << 20 | statusB << 22.
+__global__ void __launch_bounds__(kTm2Threads) tile_list_kernel(const uint8_t* __restrict__ status, int n,
+                                                                int32_t* __restrict__ count,
+                                                                int32_t* __restrict__ list, int stride,
+                                                                int32_t* __restrict__ hcount,
+                                                                int32_t* __restrict__ hlist) {
+  const int qp = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_warp_sum[3][kTm2Threads / 32];
+  const int n_kt = min((qp * 256 + 255) / 128, (n - 1) / 128) + 1;
+  int written = 0, nA = 0, nB = 0;
+  for (int kt0 = 0; kt0 < n_kt; kt0 += kTm2Chunk) {
+    const int kt = kt0 + threadIdx.x;
+    int ent = -1;
+    if (kt < n_kt) {
+      const int st = status[(int64_t)qp * stride + kt];
+      if (st) ent = kt | ((st & 3) << 20) | ((st >> 2) << 22);
+    }
     const bool kp[3] = {ent >= 0, ent >= 0 && ((ent >> 20) & 3) != 0, ent >= 0 && ((ent >> 22) & 3) != 0};
     unsigned keep[3];
 #pragma unroll
@@ -515,7 +539,7 @@ __global__ void __launch_bounds__(kTm2Threads) tile_map2_kernel(const int32_t* _
         else nB += total;
       }
     }
-    __syncthreads();  // s_e / s_f / s_warp_sum reused by the next pass
+    __syncthreads();  // s_warp_sum reused by the next pass
   }
   if (threadIdx.x == 0) {
     count[qp] = written;
@@ -592,7 +616,18 @@ namespace mv {
 mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
                     int32_t stride, cudaStream_t stream, int32_t* d_hcount, int32_t* d_hlist) {
   const int n_qp = (n + 255) / 256;
-  tile_map2_kernel<<<n_qp, kTm2Threads, 0, stream>>>(d_excl, n, max_depth, d_count, d_list, stride, d_hcount, d_hlist);
+  // statuses in a scratch byte array [n_qp][stride] (persistent per device, grown on demand)
+  static uint8_t* d_status = nullptr;
+  static size_t status_bytes = 0;
+  const size_t need = (size_t)n_qp * stride;
+  if (need > status_bytes) {
+    if (d_status) MV_CUDA_TRY(cudaFree(d_status));
+    MV_CUDA_TRY(cudaMalloc(&d_status, need));
+    status_bytes = need;
+  }
+  tile_status_kernel<<<dim3(n_qp, kTm2Split), 256, 0, stream>>>(d_excl, n, max_depth, d_status, stride);
+  MV_LAUNCH_CHECK();
+  tile_list_kernel<<<n_qp, kTm2Threads, 0, stream>>>(d_status, n, d_count, d_list, stride, d_hcount, d_hlist);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }
