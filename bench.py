@@ -238,6 +238,7 @@ def run_ours(args):
     st, handles, pos0, rnd = build_workload(mv, torch, R, dev, seed_id, wl["prefix"], wl["branches"],
                                             wl["branch_len"], steps_total, hkv=hkv_l)
     n = len(handles)
+    handles = mv.kv.handle_array(handles)  # uint64 array: no per-call list conversion
     steps_total = args.warmup + args.steps
     # per-step inputs (device resident for `value`)
     qs = [rnd(n, hq_l, D) for _ in range(2)]

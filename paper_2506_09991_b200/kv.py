@@ -43,7 +43,15 @@ class StorageStats:
     free_pages: int
 
 
+def handle_array(hs) -> np.ndarray:
+    """Handles as a contiguous uint64 array: pass it (instead of a list) to the per-step calls
+    (append, write_last, attention.decode) to skip the per-call list -> C array conversion."""
+    return np.ascontiguousarray(np.asarray([int(h) for h in hs], dtype=np.uint64))
+
+
 def _u64_array(hs):
+    if isinstance(hs, np.ndarray) and hs.dtype == np.uint64 and hs.flags["C_CONTIGUOUS"]:
+        return ctypes.c_void_p(hs.ctypes.data)  # zero-copy view
     return (ctypes.c_uint64 * len(hs))(*[int(h) for h in hs])
 
 
