@@ -733,6 +733,7 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(
     int n_multi, const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ slot_idx, int q_heads,
     void* __restrict__ out, int out_f32) {
   pdl_wait();  // programmatic launch behind decode_tc_kernel: its partials are visible after this
+  pdl_launch_dependents();  // the next step's append may start its loads
   // one CTA per (handle, q head); warp w merges slots w, w + 4, ... online (log-sum-exp), two
   // slots' loads in flight, then warp 0 merges the four partial states (a long single context
   // has one slot per split-KV chunk: 132 at the 135K-token C5 context)

@@ -276,6 +276,9 @@ __device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef
       vv[u] = __ldg(reinterpret_cast<const uint4*>(vt) + j);
     }
   }
+  // programmatic launch (engine fast path): the loads above overlapped the previous kernel;
+  // the page tables and planes it may still read are written only after it completed
+  pdl_wait();
   int page = -1, slot = 0;
   if (lane == 0) {
     if (td.fresh) {
@@ -917,10 +920,19 @@ mv_status PagedStore::append(const uint64_t* hs, int32_t n, const int32_t* d_tok
   if (n <= kDescInline) {  // descriptors ride in the launch parameters: no copy in the stream
     TokDescInline inl;
     std::memcpy(inl.d, desc.data(), sizeof(TokDesc) * n);
-    k_append_one_inline<<<(n + 3) / 4, 128, 0, stream_>>>(d_arena, d_cum, inl, n, d_tokens, d_slot_tok_, d_refcnt_,
-                                                          d_free_, d_free_top_, d_err_, d_pos,
-                                                          (const __nv_bfloat16*)d_k, (const __nv_bfloat16*)d_v, kpl,
-                                                          vpl, cfg_.kv_heads, rope_);
+    // programmatic dependent launch: the K/V loads and RoPE overlap the previous kernel's tail
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((n + 3) / 4);
+    lc.blockDim = dim3(128);
+    lc.stream = stream_;
+    lc.attrs = pdl;
+    lc.numAttrs = 1;
+    MV_CUDA_TRY(cudaLaunchKernelEx(&lc, k_append_one_inline, d_arena, d_cum, inl, n, d_tokens, d_slot_tok_, d_refcnt_,
+                                   d_free_, d_free_top_, d_err_, d_pos, (const __nv_bfloat16*)d_k,
+                                   (const __nv_bfloat16*)d_v, kpl, vpl, (int)cfg_.kv_heads, rope_));
   } else {
     void* d_desc;
     if (mv_status st = upload(desc.data(), sizeof(TokDesc) * n, &d_desc, 10)) return st;
