@@ -391,7 +391,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
         tc::tmem_wait_ld();
         if (tr && !c) PF3_TRACE(g, 3);
         float mx0 = -INFINITY, mx1 = -INFINITY;
+#if MV_PF_NOMASK  // timing experiment only (wrong results): every tile treated as full
+        if (false) {
+#else
         if (status != 1) {
+#endif
           const int lim = min(i, P.n - 1) - j0;  // last visible column
           uint32_t vm[2];
 #pragma unroll
