@@ -106,21 +106,6 @@ __device__ __forceinline__ void pv3(uint64_t vd, bool first) {
 #endif
 constexpr int kPolyMod3 = MV_PF_POLY;  // every kPolyMod3-th score pair takes poly_exp2x2 (0: none)
 
-// 2^x for a pair on the FMA pipe (FA4-style MUFU offload): x = j + f with j = rint(x) by the
-// 1.5 * 2^23 magic add, 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (relative error
-// 1.1e-4, below bf16's rounding of P), j added into the exponent field.
-__device__ __forceinline__ float2 poly_exp2x2(float2 x) {
-  x = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));  // keeps j + exponent(p) >= 0
-  const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
-  const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
-  const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);
-  float2 p = __ffma2_rn(make_float2(0.05592212f, 0.05592212f), f, make_float2(0.24264069f, 0.24264069f));
-  p = __ffma2_rn(p, f, make_float2(0.69312102f, 0.69312102f));
-  p = __ffma2_rn(p, f, make_float2(0.99992444f, 0.99992444f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
-}
-
 __device__ __forceinline__ uint32_t bit_range3(int lo, int hi) {
   lo = max(lo, 0);
   const int w = max(min(hi, 32) - lo, 0);
