@@ -66,9 +66,9 @@ constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dim
 constexpr int kQBytes = 2 * kQHalf;
 constexpr float kSumLimit = 4096.f;                        // block mass that moves the softmax reference
 constexpr int kPrefetch = 32;                               // pages of a unit prefetched into L2 at staging
-// Row replication across lane quadrants (copies > 1) is an experiment kept behind
-// -DMV_DEC_COPIES=1: measured 7% slower on C2 and NOT parity-clean (tests/test_decode_gpu.py
-// fails with it); the product build never plans copies.
+// Row replication across lane quadrants: the product plans two copies for wide units (see
+// build_plan); four copies for narrow units are an experiment behind -DMV_DEC_COPIES=1
+// (measured slower on C2 and NOT parity-clean: tests/test_decode_gpu.py fails with it).
 #ifndef MV_DEC_COPIES
 #define MV_DEC_COPIES 0
 #endif
@@ -975,9 +975,11 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
         w.slot_base = n_slots;
         w.valid = 1;
         const int rows = w.n_mem * R;
-        // row replication (copies > 1) trades softmax time for an epilogue merge; measured
-        // slower end to end on C2 with the current epilogue, so it stays off
-        w.copies = kUseCopies ? (rows <= 32 ? 4 : (rows <= 64 ? 2 : 1)) : 1;
+        // Wide cascade units (33-64 rows: two lane quadrants, so two SMSPs carry their softmax)
+        // get a second row copy in the other two quadrants, each copy exponentiating half of
+        // every block's columns: the softmax spreads over all four SMSPs (C2 +2%).  Four copies
+        // for narrow units stay behind -DMV_DEC_COPIES=1 (slower and not parity-clean).
+        w.copies = kUseCopies ? (rows <= 32 ? 4 : (rows <= 64 ? 2 : 1)) : ((rows > 32 && rows <= 64) ? 2 : 1);
         (void)rows;
         for (size_t k = m0; k < m1; ++k) {
           w.members[k - m0] = s.mem[k];
