@@ -262,6 +262,10 @@ __device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef
                                                 const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp,
                                                 __nv_bfloat16* vp, int kv_heads, const double* inv) {
   const int lane = threadIdx.x & 31;
+  // programmatic launch: the inputs (k, v, positions, tokens) may be produced by the kernel
+  // this one overlaps (e.g. the caller's projection GEMM), so nothing is read before this wait;
+  // only the launch latency and the frequency staging overlap the predecessor
+  pdl_wait();
   const bool kv = k && v;
   const int nch = kv ? kv_heads * 16 : 0;  // 16-byte chunks of the token's K (and V)
   const __nv_bfloat16* kt = kv ? k + (size_t)i * kv_heads * kHeadDim : nullptr;
@@ -276,9 +280,6 @@ __device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef
       vv[u] = __ldg(reinterpret_cast<const uint4*>(vt) + j);
     }
   }
-  // programmatic launch (engine fast path): the loads above overlapped the previous kernel;
-  // the page tables and planes it may still read are written only after it completed
-  pdl_wait();
   int page = -1, slot = 0;
   if (lane == 0) {
     if (td.fresh) {
@@ -920,7 +921,8 @@ mv_status PagedStore::append(const uint64_t* hs, int32_t n, const int32_t* d_tok
   if (n <= kDescInline) {  // descriptors ride in the launch parameters: no copy in the stream
     TokDescInline inl;
     std::memcpy(inl.d, desc.data(), sizeof(TokDesc) * n);
-    // programmatic dependent launch: the K/V loads and RoPE overlap the previous kernel's tail
+    // programmatic dependent launch: launch latency and frequency staging overlap the
+    // previous kernel (every input read follows griddepcontrol.wait)
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
