@@ -97,6 +97,15 @@ __device__ __forceinline__ void mbar_arrive_n(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 // non-blocking probe: has the phase with this parity completed?
+// Lazily created per-device state (streams, scratch, function attributes) is indexed by the
+// current device, so one process may drive several GPUs.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d < kMaxDevices ? d : kMaxDevices - 1;
+}
+
 // Programmatic dependent launch (PDL): the dependent grid may be scheduled once every CTA of
 // this grid has called launch_dependents; pdl_wait blocks until the predecessor grid completed
 // and its memory is visible (a no-op when the launch carried no programmatic dependency).

@@ -345,13 +345,16 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
   int32_t* hcount = tcount + n_qp;  // per-128-row-tile processed counts after the n_qp pair counts
   // The tile map (latency-bound, n/256 CTAs) runs on a side stream next to the HBM-bound RoPE
   // pass; the main stream joins it before the attention kernel.
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (v3 && !side) {
-    MV_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    MV_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    MV_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  static cudaStream_t sides[kMaxDevices] = {};
+  static cudaEvent_t forks[kMaxDevices] = {}, joins[kMaxDevices] = {};
+  const int dev = current_device();
+  if (v3 && !sides[dev]) {
+    MV_CUDA_TRY(cudaStreamCreateWithFlags(&sides[dev], cudaStreamNonBlocking));
+    MV_CUDA_TRY(cudaEventCreateWithFlags(&forks[dev], cudaEventDisableTiming));
+    MV_CUDA_TRY(cudaEventCreateWithFlags(&joins[dev], cudaEventDisableTiming));
   }
+  cudaStream_t side = sides[dev];
+  cudaEvent_t ev_fork = forks[dev], ev_join = joins[dev];
   if (v3) {
     MV_CUDA_TRY(cudaEventRecord(ev_fork, st));
     MV_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
@@ -393,10 +396,10 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
   P.D = max_depth;
   P.n_qt = n_qt;
   P.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kMaxDevices] = {};
+  if (!attr_set[current_device()]) {
     MV_CUDA_TRY(cudaFuncSetAttribute(prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPfSmem));
-    attr_set = true;
+    attr_set[current_device()] = true;
   }
   prefill_kernel<<<dim3(n_qt, q_heads), kPfThreads, kPfSmem, st>>>(P);
   MV_LAUNCH_CHECK();

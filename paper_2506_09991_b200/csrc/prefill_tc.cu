@@ -473,8 +473,11 @@ mv_status prefill_tc2_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_
   T.stride = stride;
   T.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
   T.n_items = n_qp * q_heads;
-  static int* d_counters = nullptr;
-  static int num_sms = 0;
+  static int* counters_dev[kMaxDevices] = {};
+  static int sms_dev[kMaxDevices] = {};
+  const int cur = current_device();
+  int*& d_counters = counters_dev[cur];
+  int& num_sms = sms_dev[cur];
   if (!d_counters) {
     MV_CUDA_TRY(cudaMalloc(&d_counters, 2 * sizeof(int)));
     MV_CUDA_TRY(cudaMemsetAsync(d_counters, 0, 2 * sizeof(int), st));
@@ -483,10 +486,10 @@ mv_status prefill_tc2_launch(const __nv_bfloat16* q_rot, const __nv_bfloat16* k_
     MV_CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
   T.counters = d_counters;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr_dev[kMaxDevices] = {};
+  if (!attr_dev[cur]) {
     MV_CUDA_TRY(cudaFuncSetAttribute(prefill_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
-    attr = true;
+    attr_dev[cur] = true;
   }
   prefill_tc2_kernel<<<std::min(T.n_items, num_sms), kThreads2, kSmem2, st>>>(mq, mk, mvv, T);
   MV_LAUNCH_CHECK();

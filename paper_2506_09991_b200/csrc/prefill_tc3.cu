@@ -534,8 +534,11 @@ mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_
   T.stride = stride;
   T.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
   T.n_items = T.n_qt * q_heads;
-  static int* d_counters = nullptr;
-  static int num_sms = 0;
+  static int* counters_dev[kMaxDevices] = {};
+  static int sms_dev[kMaxDevices] = {};
+  const int cur = current_device();
+  int*& d_counters = counters_dev[cur];
+  int& num_sms = sms_dev[cur];
   if (!d_counters) {
     MV_CUDA_TRY(cudaMalloc(&d_counters, 2 * sizeof(int)));
     MV_CUDA_TRY(cudaMemsetAsync(d_counters, 0, 2 * sizeof(int), st));
@@ -547,7 +550,8 @@ mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_
   T.counters = d_counters;
   T.trace = nullptr;
   if (MV_PF_TRACE) {
-    static unsigned long long* d_trace = nullptr;
+    static unsigned long long* trace_dev[kMaxDevices] = {};
+    unsigned long long*& d_trace = trace_dev[cur];
     const size_t tb = kTrace3 * 8 * sizeof(unsigned long long);
     if (!d_trace) MV_CUDA_TRY(cudaMalloc(&d_trace, tb));
     if (const char* f = getenv("MV_PREFILL_TRACE")) {  // the previous launch's timeline

@@ -617,8 +617,10 @@ mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t
                     int32_t stride, cudaStream_t stream, int32_t* d_hcount, int32_t* d_hlist) {
   const int n_qp = (n + 255) / 256;
   // statuses in a scratch byte array [n_qp][stride] (persistent per device, grown on demand)
-  static uint8_t* d_status = nullptr;
-  static size_t status_bytes = 0;
+  static uint8_t* status_dev[kMaxDevices] = {};
+  static size_t status_bytes_dev[kMaxDevices] = {};
+  uint8_t*& d_status = status_dev[current_device()];
+  size_t& status_bytes = status_bytes_dev[current_device()];
   const size_t need = (size_t)n_qp * stride;
   if (need > status_bytes) {
     if (d_status) MV_CUDA_TRY(cudaFree(d_status));
