@@ -10,29 +10,32 @@
 // Plan (host, cached per page-table shape): every decoding handle's table is cut at its fork
 // lineage boundaries; the segment [prev boundary, boundary of group g) is identical in all
 // holders of g, so it becomes ONE cascade unit whose query rows are all holders x GQA heads.
-// Units are split into <= 64-page chunks (split-KV); a work unit = (chunk, <= 16 handles,
-// KV head), ordered longest-first for the persistent scheduler.
+// Segments are split into chunks of up to 256 pages (split-KV, >= 1.5 waves of units); a work
+// unit = (chunk, <= 16 handles, KV head), ordered longest-first for the persistent scheduler;
+// units of 33-64 rows carry a second row copy in the idle lane quadrants.
 //
-// Kernel: persistent, one CTA per SM, 16 warps, dynamic work queue.
-//   warp 2  TMA     : one thread; 1-D bulk copies of the K and V page-head blocks (already in
-//                     UMMA SWIZZLE_128B layout in HBM, common.cuh) of 4-page blocks into a 4-slot
-//                     ring (mbarrier complete_tx), plus L2 prefetches further ahead.  Runs ahead
-//                     across work units.
-//   warp 3  MMA     : one thread. Per unit: Q smem -> TMEM (tcgen05.cp).  Per block: S = Q.K_blk^T
-//                     (M=128 query rows, N=64 tokens, K=128; A = Q from TMEM) into a TMEM S buffer; after softmax, per page
-//                     O += P_page.V_page (TS: P read from TMEM, aliasing S; N=128 dims).  Two S
-//                     buffers (64 columns) and two O buffers (one per in-flight unit).
-//   warp 0  stager  : claims the next unit, copies its page entries, and bulk-copies the
-//                     members' RoPE'd Q rows (pre-swizzled by rope_q_tile_kernel) into one of
-//                     two Q buffers.
+// Kernel: persistent, one CTA per SM, 16 warps, dynamic work queue (re-armed by the last CTA),
+// launched programmatically dependent on rope_q_tile_kernel.
+//   warp 0  stager  : claims the next unit, stages its page entries (the TMA lanes may start
+//                     streaming), then bulk-copies the members' RoPE'd Q rows (pre-swizzled by
+//                     rope_q_tile_kernel; the first copy waits on griddepcontrol) into the Q tile.
+//   warp 1  TMA     : lanes 0-7 K, lanes 8-15 V; two 4-lane groups per stream, lane p of a group
+//                     copies page p of a 4-page block (1-D bulk copies of the page-head blocks,
+//                     already in UMMA SWIZZLE_128B layout in HBM, common.cuh) into 5 K / 6 V ring
+//                     slots (mbarrier complete_tx).  Runs ahead across work units.
+//   warp 3  QK      : one thread.  Per unit: Q smem -> TMEM (tcgen05.cp).  Per block:
+//                     S = Q.K_blk^T (M=128 query rows, N=64 tokens, K=128; A = Q from TMEM) into
+//                     one of 5 TMEM S buffers.
+//   warp 2  PV      : one thread.  After the softmax, per page O += P_page.V_page (TS: P read
+//                     from TMEM, aliasing S; N=128 dims).
 //   warps 4-11 softmax: thread = query row = TMEM lane; the two warps of a lane quadrant split
-//                     each block's columns and share the row's reference max (barrier-reduced),
-//                     so every block accumulates into one O.  Masks ragged page slots, log2-domain
-//                     online softmax against a lazily moved reference (no per-block max), P as
-//                     packed bf16 back into TMEM (5 S/P buffers in flight).
-//   warps 12-15 epilogue: O row from TMEM -> final output
-//                     (single-chunk handles) or an fp32 split-KV partial, merged afterwards by
-//                     combine_kernel (log-sum-exp over the handle's chunks).
+//                     each block's columns and share the row's reference max (barrier-reduced).
+//                     Masks ragged page slots, log2-domain softmax against a lazily moved
+//                     reference (no per-block max), one score pair in four on the FMA pipe,
+//                     P as packed bf16 back into TMEM.
+//   warps 12-15 epilogue: sums row copies; O row from TMEM -> final output (single-chunk
+//                     handles) or an fp32 split-KV partial, merged afterwards by combine_kernel
+//                     (log-sum-exp over the handle's chunks, one CTA per (handle, q head)).
 // Query rows: member m of a unit owns TMEM lanes [m*R, m*R + gqa), R = gqa rounded up to a
 // power of two >= 8, so every member's rows share the swizzle phase and a 1 KiB-aligned slot.
 #include <algorithm>
