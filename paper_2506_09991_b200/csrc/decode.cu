@@ -60,7 +60,13 @@ constexpr int kWarpStage = 0, kWarpTma = 1, kWarpPv = 2, kWarpQk = 3;
 constexpr int kPageBytes = kPageTokens * kHeadDim * 2;      // 4 KiB page-head block
 constexpr int kBlkPages = 4;                                // pages per block (one QK MMA chain)
 constexpr int kBlkCols = kBlkPages * kPageTokens;           // 64 S columns per block
-constexpr int kKSlots = 5, kVSlots = 6;                     // K / V rings, one block (4 pages) per slot
+#ifndef MV_DEC_KS
+#define MV_DEC_KS 5
+#endif
+#ifndef MV_DEC_VS
+#define MV_DEC_VS 6
+#endif
+constexpr int kKSlots = MV_DEC_KS, kVSlots = MV_DEC_VS;                     // K / V rings, one block (4 pages) per slot
 constexpr int kSlotBytes = kBlkPages * kPageBytes;          // 4 page-head blocks as stored (16 KiB)
 constexpr int kMaxChunk = 256;                              // split-KV chunk cap (pages); the planner halves it down to 64-16 when work is scarce
 constexpr int kMaxEntries = kMaxChunk + 16;                 // pages per work unit (a tail chunk grows in place)
