@@ -54,7 +54,7 @@ int main() {
   int sms = 148;
   unsigned long long* d_bytes;
   cudaMalloc(&d_bytes, 8);
-  for (int page_bytes : {4096, 8192, 16384}) {
+  for (int page_bytes : {4096}) {
     const size_t n_pages_pool = pool_bytes / page_bytes;
     const int per_cta = (int)((1ull << 30) / page_bytes / sms);  // 1 GB moved in total
     std::vector<uint32_t> h((size_t)per_cta * sms);
@@ -63,13 +63,13 @@ int main() {
     uint32_t* d_pages;
     cudaMalloc(&d_pages, h.size() * 4);
     cudaMemcpy(d_pages, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
-    for (int slot_kb : {16, 32}) {
+    for (int slot_kb : {16}) {
       const int pps = std::max(1, slot_kb * 1024 / page_bytes);
-      for (int issuers : {1, 2, 4, 8})
-      for (int slots : {6}) {
+      for (int issuers : {4})
+      for (int slots : {6, 9, 11, 12}) {
         if (issuers > pps) continue;
         const int smem = slots * pps * page_bytes;
-        if (smem > 200 * 1024) continue;
+        if (smem > 220 * 1024) continue;
         cudaFuncSetAttribute(gather, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
