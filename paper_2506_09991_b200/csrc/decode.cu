@@ -590,6 +590,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           const uint64_t vd = vdesc0 + (uint64_t)((g % kVSlots) * (kSlotBytes >> 4));
           const int np = n_ent - blk * kBlkPages;
           const uint32_t acc0 = blk > 0 ? 1u : 0u;  // the unit's first block opens O
+#if MV_DEC_FAKE_NOPV  // timing experiment only (wrong results): no P.V MMAs
+          if (false)
+#endif
           switch (sb) {
             case 0: issue_pv_mmas<0>(vd, np, acc0); break;
             case 1: issue_pv_mmas<1>(vd, np, acc0); break;
