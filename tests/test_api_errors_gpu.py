@@ -70,3 +70,24 @@ def test_prefill_rejects_bad_arguments(mv):
     out = mv.attention.prefill(q, k, v, spec.positions, spec.excl)
     torch.cuda.synchronize()
     assert bool(torch.isfinite(out.float()).all())
+
+
+def test_handle_arrays_match_lists(mv):
+    """kv.handle_array (zero-copy uint64 handles) and plain lists give identical results."""
+    import numpy as np
+    outs = []
+    for as_array in (False, True):
+        st = mv.kv.PagedStore(num_pages=128, layers=1, kv_heads=2)
+        root = st.create()
+        k, v = sym_bf16(11, (40, 2, 128)).cuda(), sym_bf16(12, (40, 2, 128)).cuda()
+        st.append_many(root, torch.full((40,), 11, dtype=torch.int32, device="cuda"),
+                       torch.arange(40, dtype=torch.int32, device="cuda"), 0, k, v)
+        kids = st.fork(root, 3)
+        hs = mv.kv.handle_array(kids) if as_array else list(kids)
+        pos = torch.full((3,), 40, dtype=torch.int32, device="cuda")
+        st.append(hs, torch.full((3,), 12, dtype=torch.int32, device="cuda"), pos, 0,
+                  sym_bf16(13, (3, 2, 128)).cuda(), sym_bf16(14, (3, 2, 128)).cuda())
+        outs.append(mv.attention.decode(st, hs, sym_bf16(15, (3, 4, 128)).cuda(), pos, out_dtype=torch.float32))
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
+    assert isinstance(mv.kv.handle_array([1, 2]), np.ndarray)
