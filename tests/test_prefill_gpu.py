@@ -96,7 +96,7 @@ def test_deep_nesting_all_rows(mv, depth, paths, pw):
     assert err < TOL, (len(toks), err)
 
 
-@pytest.mark.parametrize("hq,hkv", [(4, 4), (16, 2), (8, 8)])
+@pytest.mark.parametrize("hq,hkv", [(4, 4), (16, 2), (8, 8), (1, 1)])
 def test_gqa_ratios(mv, dag_golden, hq, hkv):
     c = next(c for c in dag_golden if c["name"].startswith("random4x6") and c["error"] == -1)
     err, _ = run_prefill(mv, c["tokens"], hq=hq, hkv=hkv, seed=hq + hkv)
