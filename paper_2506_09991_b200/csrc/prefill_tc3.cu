@@ -39,7 +39,10 @@ constexpr int kT3 = 128;
 constexpr int kKSt3 = 3;
 constexpr int kVSt3 = 2;
 constexpr int kThreads3 = 384;   // 12 warps: loader, MMA, 8 softmax, 2 Q rotators
-constexpr int kRotWarp0 = 10;    // warps 10-11 rotate each item's raw Q tile in shared memory
+constexpr int kRotWarp0 = 10;
+#ifndef MV_PF_NOROT
+#define MV_PF_NOROT 0
+#endif    // warps 10-11 rotate each item's raw Q tile in shared memory
 constexpr int kHalf3 = kT3 * 128;  // SW128 half tile: 128 rows x 64 dims
 constexpr int kTile3 = 2 * kHalf3;
 constexpr int kOffQ3 = 0;  // two Q tiles: item i loads and rotates into tile i & 1
@@ -310,7 +313,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       mbar_wait(&q_loaded[buf], (it_i >> 1) & 1);
       uint8_t* qt = smem + kOffQ3 + buf * kTile3;
 #pragma unroll 4
-      for (int ch = rt; ch < kT3 * 16; ch += 64) {
+      for (int ch = rt; ch < (MV_PF_NOROT ? 0 : kT3 * 16); ch += 64) {  // NOROT: timing experiment
         const int row = ch >> 4, c = ch & 15;
         const int grow = min(it.t * kT3 + row, P.n - 1);  // rows past n are zero-filled: any angle
         uint4* q4 = reinterpret_cast<uint4*>(qt + (c >> 3) * kHalf3 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
