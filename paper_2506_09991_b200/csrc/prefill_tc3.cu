@@ -312,22 +312,35 @@ __global__ void __launch_bounds__(kThreads3, 1)
       if (!it.valid) break;
       mbar_wait(&q_loaded[buf], (it_i >> 1) & 1);
       uint8_t* qt = smem + kOffQ3 + buf * kTile3;
-#pragma unroll 4
-      for (int ch = rt; ch < (MV_PF_NOROT ? 0 : kT3 * 16); ch += 64) {  // NOROT: timing experiment
-        const int row = ch >> 4, c = ch & 15;
-        const int grow = min(it.t * kT3 + row, P.n - 1);  // rows past n are zero-filled: any angle
-        uint4* q4 = reinterpret_cast<uint4*>(qt + (c >> 3) * kHalf3 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
-        const float4* tb = reinterpret_cast<const float4*>(P.cs + (size_t)grow * 64 + c * 4);
-        const float4 t01 = __ldg(tb), t23 = __ldg(tb + 1);
-        uint4 v = *q4;
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
-        const float cs[4] = {t01.x, t01.z, t23.x, t23.z}, sn[4] = {t01.y, t01.w, t23.y, t23.w};
+      // 32 chunks per thread in 4 batches of 8: all table loads of a batch are in flight together
+      // (the table comes from L2; a light item's rotation is otherwise on the MMA's critical path)
+      constexpr int kBatch = 8;
+      for (int b0 = 0; b0 < (MV_PF_NOROT ? 0 : kT3 * 16 / 64); b0 += kBatch) {
+        float4 t01[kBatch], t23[kBatch];
+        uint4* q4[kBatch];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float2 ab = __bfloat1622float2(h2[j]);
-          h2[j] = __floats2bfloat162_rn(ab.x * cs[j] - ab.y * sn[j], ab.x * sn[j] + ab.y * cs[j]);
+        for (int u = 0; u < kBatch; ++u) {
+          const int ch = rt + 64 * (b0 + u);
+          const int row = ch >> 4, c = ch & 15;
+          const int grow = min(it.t * kT3 + row, P.n - 1);  // rows past n are zero-filled: any angle
+          q4[u] = reinterpret_cast<uint4*>(qt + (c >> 3) * kHalf3 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
+          const float4* tb = reinterpret_cast<const float4*>(P.cs + (size_t)grow * 64 + c * 4);
+          t01[u] = __ldg(tb);
+          t23[u] = __ldg(tb + 1);
         }
-        *q4 = v;
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          uint4 v = *q4[u];
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
+          const float cs[4] = {t01[u].x, t01[u].z, t23[u].x, t23[u].z};
+          const float sn[4] = {t01[u].y, t01[u].w, t23[u].y, t23[u].w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 ab = __bfloat1622float2(h2[j]);
+            h2[j] = __floats2bfloat162_rn(ab.x * cs[j] - ab.y * sn[j], ab.x * sn[j] + ab.y * cs[j]);
+          }
+          *q4[u] = v;
+        }
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
       __syncwarp();
