@@ -36,7 +36,11 @@ namespace mv {
 namespace {
 
 constexpr int kT3 = 128;
-constexpr int kKSt3 = 3;
+#ifndef MV_PF_QBUF
+#define MV_PF_QBUF 2
+#endif
+constexpr int kQB3 = MV_PF_QBUF;       // Q tiles (item i uses tile i % kQB3)
+constexpr int kKSt3 = 5 - kQB3;        // K ring slots (Q tiles + K slots share 5 x 32 KiB)
 constexpr int kVSt3 = 2;
 constexpr int kThreads3 = 384;   // 12 warps: loader, MMA, 8 softmax, 2 Q rotators
 constexpr int kRotWarp0 = 10;
@@ -46,7 +50,7 @@ constexpr int kRotWarp0 = 10;
 constexpr int kHalf3 = kT3 * 128;  // SW128 half tile: 128 rows x 64 dims
 constexpr int kTile3 = 2 * kHalf3;
 constexpr int kOffQ3 = 0;  // two Q tiles: item i loads and rotates into tile i & 1
-constexpr int kOffK3 = kOffQ3 + 2 * kTile3;
+constexpr int kOffK3 = kOffQ3 + kQB3 * kTile3;
 constexpr int kOffV3 = kOffK3 + kKSt3 * kTile3;
 constexpr int kOffBar3 = kOffV3 + kVSt3 * kTile3;
 constexpr int kOffX3 = kOffBar3 + 512;  // row max / sum exchange: [2 parity][2 WG][128 rows] f32
@@ -127,10 +131,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
   uint8_t* smem = smem_align1024(smem_raw3);
   if (smem != smem_raw3) __trap();  // no slack was allocated for alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar3);
-  uint64_t* q_loaded = bars;             // [2] raw Q tile landed (tx)
-  uint64_t* q_full = q_loaded + 2;       // [2] Q tile rotated (2 rotator warps)
-  uint64_t* q_empty = q_full + 2;        // [2] MMA commit after the item's last Q.K^T
-  uint64_t* k_full = q_empty + 2;        // [3]
+  uint64_t* q_loaded = bars;             // [kQB3] raw Q tile landed (tx)
+  uint64_t* q_full = q_loaded + kQB3;    // [kQB3] Q tile rotated (2 rotator warps)
+  uint64_t* q_empty = q_full + kQB3;     // [kQB3] MMA commit after the item's last Q.K^T
+  uint64_t* k_full = q_empty + kQB3;     // [kKSt3]
   uint64_t* k_empty = k_full + kKSt3;    // [3]
   uint64_t* v_full = k_empty + kKSt3;    // [2]
   uint64_t* v_empty = v_full + kVSt3;    // [2] MMA commit after P.V (also certifies O for the rescale)
@@ -140,13 +144,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
   uint64_t* o_empty = o_fin + 1;         // epilogue read O (256 threads)
   uint64_t* item_full = o_empty + 1;     // [2]
   uint64_t* slot_empty = item_full + 2;  // [2] V lane + MMA + 8 softmax warps
-  Item3* s_item = reinterpret_cast<Item3*>(slot_empty + 2);
+  static_assert(3 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 2 * kSB + 6 <= 32, "barrier block");
+  Item3* s_item = reinterpret_cast<Item3*>(smem + kOffBar3 + 256);  // after <= 32 barriers, 16 B aligned
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_item + 2);
   float* s_x = reinterpret_cast<float*>(smem + kOffX3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < kQB3; ++b) {
       mbar_init(&q_loaded[b], 1);
       mbar_init(&q_full[b], 2);
       mbar_init(&q_empty[b], 1);
@@ -205,10 +210,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
         if (!it.valid) break;
         claim(nxt);
         // raw (pre-RoPE) Q into tile buf once item i-2's last Q.K^T has read it
-        if (i >= 2) mbar_wait(&q_empty[buf], ((i >> 1) - 1) & 1);
-        mbar_arrive_expect_tx(&q_loaded[buf], kTile3);
-        tc::tma_load_3d(smem + kOffQ3 + buf * kTile3, &map_q, 0, it.h, it.t * kT3, &q_loaded[buf]);
-        tc::tma_load_3d(smem + kOffQ3 + buf * kTile3 + kHalf3, &map_q, 64, it.h, it.t * kT3, &q_loaded[buf]);
+        const int qb = i % kQB3;
+        if (i >= kQB3) mbar_wait(&q_empty[qb], ((i / kQB3) - 1) & 1);
+        mbar_arrive_expect_tx(&q_loaded[qb], kTile3);
+        tc::tma_load_3d(smem + kOffQ3 + qb * kTile3, &map_q, 0, it.h, it.t * kT3, &q_loaded[qb]);
+        tc::tma_load_3d(smem + kOffQ3 + qb * kTile3 + kHalf3, &map_q, 64, it.h, it.t * kT3, &q_loaded[qb]);
         const int kvh = it.h / (P.hq / P.hkv);
         const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
         for (int j = 0; j < it.m; ++j) {
@@ -271,10 +277,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
         mbar_arrive(&slot_empty[buf]);
         if (!it.valid) break;
         const int m = it.m;
-        const uint64_t qd = qd0 + (uint64_t)((buf * kTile3) >> 4);
-        mbar_wait(&q_full[buf], (i >> 1) & 1);  // rotated by warps 10-11 (generic -> async proxy fenced)
+        const int qb = i % kQB3;
+        const uint64_t qd = qd0 + (uint64_t)((qb * kTile3) >> 4);
+        mbar_wait(&q_full[qb], (i / kQB3) & 1);  // rotated by warps 10-11 (generic -> async proxy fenced)
         for (int u = 0; u < kSB && u < m; ++u) qk(qd, g + u);
-        if (m <= kSB) tc::mma_commit(&q_empty[buf]);
+        if (m <= kSB) tc::mma_commit(&q_empty[qb]);
         for (int j = 0; j < m; ++j, ++g) {
           mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
           mbar_wait(&p_full[g % kSB], (g / kSB) & 1);
@@ -289,7 +296,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
           tc::mma_commit(&v_empty[g % kVSt3]);
           if (j + kSB < m) {
             qk(qd, g + kSB);  // S buffer g % 3 again: in order behind P.V(g)
-            if (j + kSB + 1 == m) tc::mma_commit(&q_empty[buf]);
+            if (j + kSB + 1 == m) tc::mma_commit(&q_empty[qb]);
           }
           PF3_TRACE(g, 1);
         }
@@ -310,8 +317,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&slot_empty[buf]);
       if (!it.valid) break;
-      mbar_wait(&q_loaded[buf], (it_i >> 1) & 1);
-      uint8_t* qt = smem + kOffQ3 + buf * kTile3;
+      const int qb = it_i % kQB3;
+      mbar_wait(&q_loaded[qb], (it_i / kQB3) & 1);
+      uint8_t* qt = smem + kOffQ3 + qb * kTile3;
       // 32 chunks per thread in 4 batches of 8: all table loads of a batch are in flight together
       // (the table comes from L2; a light item's rotation is otherwise on the MMA's critical path)
       constexpr int kBatch = 8;
@@ -344,7 +352,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
       __syncwarp();
-      if (lane == 0) mbar_arrive(&q_full[buf]);
+      if (lane == 0) mbar_arrive(&q_full[qb]);
     }
   } else {
     // ---------------- softmax: warps 2-5 columns 0-63, warps 6-9 columns 64-127 ----------------
