@@ -371,3 +371,12 @@ def test_c5_reduce_merge_full_scale(mv):
     st.release(cur)
     s = st.stats()
     assert s.live_handles == 0 and s.total_refcount == 0 and s.free_pages == pages
+
+
+@pytest.mark.parametrize("hq,hkv,branches", [(40, 1, 3), (8, 8, 5), (16, 4, 9), (32, 8, 12)])
+def test_gqa_and_copy_layouts(mv, hq, hkv, branches):
+    """Row layouts across GQA ratios: one KV head with 40 query heads (64-row members), MHA,
+    and member counts that make 33-64-row cascade units (planned with a second row copy) and
+    > 64-row units."""
+    err, _ = run_case(mv, [(200, branches, 45)], hq=hq, hkv=hkv, num_pages=512, seed=hq + branches)
+    assert err < TOL, err
