@@ -232,7 +232,10 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
   const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
   const uint32_t ocol = lane_base + kColO + half * 64;
   float* gmax = xmax + lq * (NP * 32);
-  const int bar_id = 2 + lq, bar_cnt = 64 * F;
+  // named barrier per (copy layout, row quadrant group): units with different F never share an
+  // id, so warps that run ahead into the next unit (inactive ones skip barriers) cannot mix
+  // arrivals of differently sized barriers (ids 2-5: F = 1, 6-7: F = 2, 8: F = 4; 1: epilogue)
+  const int bar_id = (F == 1 ? 2 : (F == 2 ? 6 : 8)) + lq, bar_cnt = 64 * F;
   const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
   float m_ref = -INFINITY, l = 0.f;
   for (int blk = 0; blk < nblk; ++blk, ++g) {

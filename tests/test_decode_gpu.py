@@ -380,3 +380,12 @@ def test_gqa_and_copy_layouts(mv, hq, hkv, branches):
     > 64-row units."""
     err, _ = run_case(mv, [(200, branches, 45)], hq=hq, hkv=hkv, num_pages=512, seed=hq + branches)
     assert err < TOL, err
+
+
+def test_row_copy_layouts_after_plain_units(mv):
+    """Long private chunks (1 member, plain layout) are scheduled before short cascade chunks of
+    6 members (48 rows: planned with row copies), so CTAs switch from plain to copied units
+    while some softmax warps of the previous unit are still running."""
+    err, st = run_case(mv, [(64, 6, 1500)] * 6, hq=40, hkv=8, num_pages=8192, seed=77)
+    assert err < TOL, err
+    assert st.plan_info()["work_items"] >= 6 * 7
