@@ -121,3 +121,16 @@ def test_sequence_lengths_around_tiles(mv):
         toks = nested_tokens(2, 2, 8, seed=n_extra, prefix=50 + n_extra)
         err, _ = run_prefill(mv, toks, hq=8, hkv=2, seed=n_extra + 1)
         assert err < TOL, (len(toks), err)
+
+
+def test_32k_nested_sampled(mv):
+    """A ~33K-token stream (twice configs[2]; two top-level blocks, three nesting levels): tile
+    lists, the RoPE table and the persistent queue beyond the benchmark size; sampled rows
+    against the oracle."""
+    toks = nested_tokens(3, 4, 290, seed=32, prefix=2000) + nested_tokens(2, 3, 300, seed=33, prefix=100)
+    rng = np.random.default_rng(3)
+    n = len(toks)
+    assert 30000 < n < 40000, n
+    rows = np.sort(np.concatenate([rng.choice(n, 48, replace=False), [0, n - 1]]))
+    err, spec = run_prefill(mv, toks, hq=40, hkv=8, rows=rows, seed=9)
+    assert err < TOL, (n, err)
