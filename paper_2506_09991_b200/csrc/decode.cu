@@ -821,6 +821,10 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(
 // 16-byte chunk.
 __global__ void rope_q_tile_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pos, int n,
                                    int kv_heads, int gqa, int R, const RopeTable rt, __nv_bfloat16* __restrict__ tile) {
+  // launched PDL-dependent on the append: wait for it (and, transitively, everything before it)
+  // BEFORE releasing decode_tc, whose TMA lanes read the page tables and KV planes ahead of their
+  // own griddepcontrol.wait
+  pdl_wait();
   pdl_launch_dependents();  // decode_tc may start its prologue (every CTA of this grid is running)
   __shared__ double s_inv[kHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
@@ -1178,8 +1182,17 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   if (mv_status e = ensure_dev(pc.d_q_tile, pc.cap_q, (size_t)n * cfg.kv_heads * 2 * R * 64)) return e;
   {
     const int64_t chunks = (int64_t)n * cfg.kv_heads * R * 16;
-    rope_q_tile_kernel<<<(unsigned)((chunks + 255) / 256), 256, 0, stream>>>(
-        (const __nv_bfloat16*)d_q, d_positions, n, cfg.kv_heads, gqa, R, st.rope(), pc.d_q_tile);
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)((chunks + 255) / 256));
+    lc.blockDim = dim3(256);
+    lc.stream = stream;
+    lc.attrs = pdl;
+    lc.numAttrs = 1;
+    MV_CUDA_TRY(cudaLaunchKernelEx(&lc, rope_q_tile_kernel, (const __nv_bfloat16*)d_q, d_positions, n,
+                                   cfg.kv_heads, gqa, R, st.rope(), pc.d_q_tile));
     MV_LAUNCH_CHECK();
   }
   DecodeParams P;

@@ -341,6 +341,9 @@ __global__ void k_append_one_inline(PageRef* __restrict__ arena, int32_t* __rest
                                     const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                                     const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp,
                                     int kv_heads, const RopeTable rt) {
+  // the RoPE pre-pass after this kernel may launch now: it waits (griddepcontrol.wait) for this
+  // grid to complete before touching anything, and only then releases decode_tc
+  pdl_launch_dependents();
   __shared__ double s_inv[kHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
