@@ -84,7 +84,7 @@ constexpr int kPrefetch = 32;                               // pages of a unit p
 constexpr bool kUseCopies = MV_DEC_COPIES != 0;
 constexpr int kSBufs = 5;                                   // S / P buffers in flight
 #ifndef MV_DEC_POLY
-#define MV_DEC_POLY 4  // C2 +4.5% (1/8: +2.4%, 1/3 ~ 1/4, 1/2 no gain)
+#define MV_DEC_POLY 4  // C2 +4.5% (1/8: +2.4%, 1/3 ~ 1/4, 1/2 no gain); C4: 1/2 -3.5%, 1/3 -0.5%, 1/6 -2%
 #endif
 constexpr int kDecPoly = MV_DEC_POLY;                       // every kDecPoly-th score pair on the FMA pipe
 #ifndef MV_DEC_TMA_GROUPS

@@ -389,3 +389,51 @@ def test_row_copy_layouts_after_plain_units(mv):
     err, st = run_case(mv, [(64, 6, 1500)] * 6, hq=40, hkv=8, num_pages=8192, seed=77)
     assert err < TOL, err
     assert st.plan_info()["work_items"] >= 6 * 7
+
+
+def test_device_produced_inputs_without_sync(mv):
+    """Engine-style stream ordering: every step's K/V, positions and queries are written by a
+    device kernel into the SAME buffers right before the append / decode that read them (holding
+    the previous step's values until then), behind a long GEMM, with no host synchronisation
+    across 12 steps.  The append, the RoPE pre-pass and decode_tc are launched programmatically
+    dependent (PDL): a read issued ahead of its griddepcontrol.wait would see the stale values."""
+    hq, hkv, steps = 40, 8, 12
+    st = mv.kv.PagedStore(num_pages=512, layers=1, kv_heads=hkv)
+    rows = {"k": [], "v": [], "pos": []}
+    r = Req(mv, st, rows, 21, 300, 4, 40, hkv=hkv)
+    handles, ctx, qpos = list(r.handles), [list(c) for c in r.ctx], list(r.qpos)
+    n = len(handles)
+    ks = [sym_bf16(7000 + s * 3, (n, hkv, 128)) for s in range(steps)]
+    vs = [sym_bf16(7001 + s * 3, (n, hkv, 128)) for s in range(steps)]
+    qs = [sym_bf16(7002 + s * 3, (n, hq, 128)) for s in range(steps)]
+    ks_d, vs_d, qs_d = [x.cuda() for x in ks], [x.cuda() for x in vs], [x.cuda() for x in qs]
+    kbuf, vbuf, qbuf = torch.empty_like(ks_d[0]), torch.empty_like(vs_d[0]), torch.empty_like(qs_d[0])
+    pbuf = torch.tensor(qpos, dtype=torch.int32, device="cuda") - 1
+    toks = torch.full((n,), 12, dtype=torch.int32, device="cuda")
+    big = torch.randn(4096, 4096, dtype=torch.bfloat16, device="cuda")
+    outs = []
+    torch.cuda.synchronize()
+    for s in range(steps):
+        _ = big @ big  # keeps the GPU busy so PDL launches start early
+        torch.add(pbuf, 1, out=pbuf)
+        torch.mul(ks_d[s], 1, out=kbuf)
+        torch.mul(vs_d[s], 1, out=vbuf)
+        st.append(handles, toks, pbuf, 0, kbuf, vbuf)
+        _ = big @ big
+        torch.mul(qs_d[s], 1, out=qbuf)
+        outs.append(mv.attention.decode(st, handles, qbuf, pbuf, out_dtype=torch.float32))
+    torch.cuda.synchronize()
+    for s in range(steps):
+        pos = torch.tensor([p + s for p in qpos], dtype=torch.int32)
+        base = sum(x.shape[0] for x in rows["k"])
+        rows["k"].append(ks[s])
+        rows["v"].append(vs[s])
+        rows["pos"].append(pos)
+        for i in range(n):
+            ctx[i].append(base + i)
+        K = np.concatenate([bf16_to_f64(x) for x in rows["k"]])
+        V = np.concatenate([bf16_to_f64(x) for x in rows["v"]])
+        P = np.concatenate([x.numpy() for x in rows["pos"]])
+        ref = oracle.attn_decode(oracle.rope(bf16_to_f64(qs[s]), pos.numpy()), oracle.rope(K, P), V, ctx)
+        err = np.abs(outs[s].cpu().numpy() - ref).max()
+        assert err < TOL, (s, err)
