@@ -229,6 +229,44 @@ MV_API mv_status mv_attn_prefill(const void* d_q, const void* d_k, const void* d
                           double rope_base, void* d_out, int32_t out_dtype, void* d_workspace,
                           size_t workspace_bytes, mv_stream_t stream);
 
+/*
+ * K5 — per-lane tag interpreter (replaces engine.cpp:323-415 feed_interpreter, with the BUG-2
+ * fix, and the merge-completion reset at engine.cpp:793).
+ * d_state: MV_INTERP_STATE_WORDS int32 per lane (opaque), set up by mv_interp_init; d_is_child
+ * (nullable: all root lanes) marks worker lanes (LaneRuntime::parent >= 0).
+ * mv_interp_feed walks d_events [n_steps][n_lanes] (token ids, 0..9 the tags in TagKind order;
+ * MV_INTERP_IDLE: no call this step; MV_INTERP_MERGED: the lane's paths were merged) and writes
+ * d_action [n_steps][n_lanes] (MV_ACT_*) and d_arg (spawn count for MV_ACT_SPAWN, MV_VIOL_* for
+ * MV_ACT_VIOLATION, else 0). A violation leaves the lane state unchanged, as the reference does.
+ * Optional d_spawns: (step, lane, count) triples appended in no particular order at
+ * *d_n_spawns (caller-zeroed, device memory).
+ */
+#define MV_INTERP_STATE_WORDS 2
+#define MV_INTERP_IDLE (-1)
+#define MV_INTERP_MERGED (-2)
+#define MV_ACT_NONE 0
+#define MV_ACT_SPAWN 1
+#define MV_ACT_WORKER_DONE 2
+#define MV_ACT_VIOLATION 3
+#define MV_VIOL_PATH_CLOSE_OUTSIDE 1          /* "</Path> outside any path" */
+#define MV_VIOL_UNEXPECTED_SEQUENTIAL 2       /* "unexpected <tag> in sequential decode" */
+#define MV_VIOL_EXPECTED_GOAL 3               /* "expected <Goal> after <Parallel>" */
+#define MV_VIOL_TEXT_BETWEEN_OUTLINES 4       /* "text between outlines" */
+#define MV_VIOL_NESTED_OUTLINE 5              /* "nested <Outline>" */
+#define MV_VIOL_OUTLINE_CLOSE_WITHOUT_OPEN 6  /* "</Outline> without <Outline>" */
+#define MV_VIOL_GOAL_CLOSE_IN_OUTLINE 7       /* "</Goal> inside <Outline>" */
+#define MV_VIOL_ZERO_OUTLINES 8               /* "</Goal> with zero outlines" */
+#define MV_VIOL_UNEXPECTED_IN_GOAL 9          /* "unexpected <tag> inside <Goal>" */
+#define MV_VIOL_WAITING 10                    /* "token while waiting for paths" */
+#define MV_VIOL_EXPECTED_CONCLUSION 11        /* "expected <Conclusion> after merge" */
+#define MV_VIOL_UNEXPECTED_IN_CONCLUSION 12   /* "unexpected <tag> inside <Conclusion>" */
+#define MV_VIOL_EXPECTED_PARALLEL_CLOSE 13    /* "expected </Parallel> after </Conclusion>" */
+#define MV_VIOL_MERGE_NO_BLOCK 14             /* merge with no open block (undefined in the reference) */
+MV_API mv_status mv_interp_init(int32_t* d_state, int32_t n_lanes, const int32_t* d_is_child, mv_stream_t stream);
+MV_API mv_status mv_interp_feed(int32_t* d_state, int32_t n_lanes, const int32_t* d_events, int32_t n_steps,
+                                int32_t* d_action, int32_t* d_arg, int32_t* d_spawns, int32_t* d_n_spawns,
+                                mv_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

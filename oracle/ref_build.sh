@@ -21,5 +21,8 @@ for f in dag grammar kvcache synth tokenizer toy_model engine; do
 done
 wait
 $CXX $FLAGS "$HERE/refdrv.cpp" "${objs[@]}" -o "$OUT/refdrv" -lpthread
+# the reference's own per-lane tag interpreter (engine.cpp:323-415), for tests/golden/interp.jsonl.gz
+$CXX $FLAGS -I"$OUT/src/src" "$HERE/interp_drv.cpp" "$OUT"/{dag,grammar,kvcache,synth,tokenizer,toy_model}.o \
+  -o "$OUT/interp_drv"
 rm -rf "$OUT/src"  # patched copies were build inputs only
 echo "built $OUT/refdrv"

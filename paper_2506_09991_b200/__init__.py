@@ -8,6 +8,7 @@ it with ctypes and mirrors the reference's proj/core interface names for this pa
     attention.decode      <- attention core of ToyModel::step (toy_model.cpp:121-157)
     attention.prefill     <- attention inside ToyModel::forward (toy_model.cpp:174-202)
     toy.ToyModel          <- ToyModel forward / engine::run_forced around those kernels (configs[0])
+    interp.TagInterpreter <- the engine's per-lane feed_interpreter (engine.cpp:323-415)
 
 There is no CPU fallback: importing fails loudly when the library is missing, and every
 call runs on the GPU.
@@ -84,6 +85,8 @@ def _load():
         "mv_attn_decode_plan_info": ([P, P], ctypes.c_int),
         "mv_prefill_workspace_size": ([i32, i32, i32], sz),
         "mv_attn_prefill": ([P, P, P, P, P, i32, i32, i32, i32, ctypes.c_double, P, i32, P, sz, P], ctypes.c_int),
+        "mv_interp_init": ([P, i32, P, P], ctypes.c_int),
+        "mv_interp_feed": ([P, i32, P, i32, P, P, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -101,6 +104,7 @@ EXPORTED = (
     "mv_kv_fork", "mv_kv_merge", "mv_kv_release", "mv_kv_length", "mv_kv_stats_get", "mv_kv_resolve",
     "mv_kv_resolve_payloads", "mv_kv_resolve_slots", "mv_kv_append", "mv_kv_write_last", "mv_kv_append_many",
     "mv_kv_gather_kv", "mv_attn_decode", "mv_attn_decode_plan_info", "mv_prefill_workspace_size", "mv_attn_prefill",
+    "mv_interp_init", "mv_interp_feed",
 )
 
 
@@ -117,4 +121,4 @@ def check(status: int) -> None:
     raise MvError(status, msg)
 
 
-from . import dag, kv, attention, toy  # noqa: E402,F401
+from . import dag, kv, attention, toy, interp  # noqa: E402,F401
