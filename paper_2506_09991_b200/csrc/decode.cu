@@ -60,13 +60,7 @@ constexpr int kWarpStage = 0, kWarpTma = 1, kWarpPv = 2, kWarpQk = 3;
 constexpr int kPageBytes = kPageTokens * kHeadDim * 2;      // 4 KiB page-head block
 constexpr int kBlkPages = 4;                                // pages per block (one QK MMA chain)
 constexpr int kBlkCols = kBlkPages * kPageTokens;           // 64 S columns per block
-#ifndef MV_DEC_KS
-#define MV_DEC_KS 5
-#endif
-#ifndef MV_DEC_VS
-#define MV_DEC_VS 6
-#endif
-constexpr int kKSlots = MV_DEC_KS, kVSlots = MV_DEC_VS;                     // K / V rings, one block (4 pages) per slot
+constexpr int kKSlots = 5, kVSlots = 6;                     // K / V rings, one block (4 pages) per slot (5/6 measured best against 4/7, 6/5, 3/8)
 constexpr int kSlotBytes = kBlkPages * kPageBytes;          // 4 page-head blocks as stored (16 KiB)
 constexpr int kMaxChunk = 256;                              // split-KV chunk cap (pages); the planner halves it down to 64-16 when work is scarce
 constexpr int kMaxEntries = kMaxChunk + 16;                 // pages per work unit (a tail chunk grows in place)
@@ -74,23 +68,11 @@ constexpr int kMaxMem = 16;                                 // handles per work 
 constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dims] bf16
 constexpr int kQBytes = 2 * kQHalf;
 constexpr float kSumLimit = 4096.f;                        // block mass that moves the softmax reference
-constexpr int kPrefetch = 32;                               // pages of a unit prefetched into L2 at staging
-// Row replication across lane quadrants: the product plans two copies for wide units (see
-// build_plan); four copies for narrow units are an experiment behind -DMV_DEC_COPIES=1
-// (measured slower on C2 and NOT parity-clean: tests/test_decode_gpu.py fails with it).
-#ifndef MV_DEC_COPIES
-#define MV_DEC_COPIES 0
-#endif
-constexpr bool kUseCopies = MV_DEC_COPIES != 0;
 constexpr int kSBufs = 5;                                   // S / P buffers in flight
-#ifndef MV_DEC_POLY
-#define MV_DEC_POLY 4  // C2 +4.5% (1/8: +2.4%, 1/3 ~ 1/4, 1/2 no gain); C4: 1/2 -3.5%, 1/3 -0.5%, 1/6 -2%
-#endif
-constexpr int kDecPoly = MV_DEC_POLY;                       // every kDecPoly-th score pair on the FMA pipe
-#ifndef MV_DEC_TMA_GROUPS
-#define MV_DEC_TMA_GROUPS 2  // C2 +1.4% over 1 (C4 unchanged)
-#endif
-constexpr int kTmaLanesPerBlkGroup = MV_DEC_TMA_GROUPS;     // 4-lane copy groups per stream (blocks in flight per step)
+// every kDecPoly-th score pair on the FMA pipe: C2 +4.5% (1/8: +2.4%, 1/3 ~ 1/4, 1/2 no gain);
+// C4: 1/2 -3.5%, 1/3 -0.5%, 1/6 -2%
+constexpr int kDecPoly = 4;
+constexpr int kTmaLanesPerBlkGroup = 2;  // 4-lane copy groups per stream (blocks in flight per step): C2 +1.4% over 1
 constexpr int kColS = 0;                                    // TMEM: S0..S4 (64 cols each)
 constexpr int kColO = kSBufs * kBlkCols;                    //       O (128 cols)
 constexpr int kColQ = kColO + 128;                          //       Q (64 cols: 128 bf16 dims)
@@ -145,11 +127,7 @@ struct DecodeParams {
   int out_f32;
   int kv_heads, q_heads, gqa, R;
   float scale_log2;
-  int pf_head, pf_tail;          // L2 prefetch: pages of a unit's head at staging; its tail once started
-  unsigned long long* trace;    // optional timeline [cta][kTraceWords] (MV_DECODE_TRACE)
 };
-
-constexpr int kTraceWords = 864;
 
 __device__ __forceinline__ void store_row(const DecodeParams& P, int64_t row, int c, const float* o, float inv) {
   if (P.out_f32) {
@@ -216,7 +194,7 @@ __device__ __forceinline__ void group_sync(int id, int count) {
 // into the other copies' parts of its rows, so every copy accumulates a disjoint slice of the
 // tokens into its own O rows (summed by the epilogue).  All 2F warps holding a logical row share
 // its reference max through one named barrier per block (OR-reduced "move" flag).
-template <int F, bool TRACE>
+template <int F>
 __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int n_ent, int n_mem,
                                              const PageRef* se, int warp, int lane, uint32_t tmem, uint64_t* s_full,
                                              uint64_t* p_full, uint64_t* vempty, float* xmax, float& m_out,
@@ -243,9 +221,7 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
     const uint32_t scol = lane_base + kColS + sb * kBlkCols;
     mbar_wait(&s_full[sb], (g / kSBufs) & 1);
     tc::fence_after();
-    if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + g] = globaltimer();
     if (warp_active) {
-      const long long sc0 = TRACE ? clock64() : 0;
       float v[W];
       tc::tmem_ldN<W>(scol + part * W, v);
       // valid slots of this part's tokens (ragged unit head / tail pages, partial pages)
@@ -329,7 +305,6 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
         ls = exp_part(m_ref == -INFINITY ? 0.f : m_ref);
       }
       l += ls;
-      if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 672 + g] = clock64() - sc0;
       tc::tmem_stNu<WP>(scol + part * WP, pk);
       if (F > 1) {
         uint32_t z[WP];
@@ -340,12 +315,10 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
           if (c2 != c) tc::tmem_stNu<WP>(scol + (c2 * 2 + half) * WP, z);
       }
       tc::tmem_wait_st();
-      if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 800 + g] = clock64() - sc0;
     }
     tc::fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&p_full[sb]);
-    if (TRACE && warp == 4 && lane == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 64 + g] = globaltimer();
   }
   m_out = m_ref;
   l_out = l;
@@ -355,7 +328,6 @@ __device__ __forceinline__ void issue_q_copy(uint64_t qd) {  // Q tile smem -> T
   for (int k = 0; k < 8; ++k) tc::cp_128x256b(kColQ + k * 8, qd + (uint64_t)(((k >> 2) * kQHalf + (k & 3) * 32) >> 4));
 }
 
-template <bool TRACE>
 __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodeParams P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
@@ -438,7 +410,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         break;
       }
       if (lane == 0) w_next = atomicAdd(P.work_counter, 1);
-      if (TRACE && lane == 0 && i < 32) P.trace[blockIdx.x * kTraceWords + 320 + i] = globaltimer();
       if (lane < kItemInts) reinterpret_cast<int*>(si)[lane] = reinterpret_cast<const int*>(P.units + w)[lane];
       __syncwarp();
       const int n_ent = si->n_entries, n_mem = si->n_mem, kvh = si->kvh;
@@ -446,28 +417,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       PageRef* se = s_ent0 + buf * kMaxEntries;
       for (int j = lane; j < n_ent; j += 32) {
         const PageRef ref = P.arena[eoff + j];
-        se[j] = ref;
-        if (j < P.pf_head) {  // the unit's head now; its tail once the unit has started (below)
-          const size_t pf = ((size_t)ref.page * P.kv_heads + kvh) * kPageTokens * kHeadDim;
-          prefetch_l2(P.kplane + pf, kPageBytes);
-          prefetch_l2(P.vplane + pf, kPageBytes);
-        }
+        se[j] = ref.page >= 0 ? ref : make_ref(0, 0, 0);  // an unset entry reads no token (never expected)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ent_full[buf]);  // the TMA lanes may stream this unit's pages
       const uint32_t half_bytes = (uint32_t)P.R * 128;
       if (i == 0) pdl_wait();  // the Q tile of this launch is complete and visible
-      if (i >= 1) {
-        mbar_wait(q_free, (i - 1) & 1);  // the previous unit's Q tile is in TMEM: it has started
-        // stream the rest of the previous unit into L2 (its page list is still staged)
-        const WorkItem* sp = &s_item[buf ^ 1];
-        const PageRef* pe = s_ent0 + (buf ^ 1) * kMaxEntries;
-        for (int j = P.pf_head + lane; P.pf_tail && j < sp->n_entries; j += 32) {
-          const size_t pf = ((size_t)pe[j].page * P.kv_heads + sp->kvh) * kPageTokens * kHeadDim;
-          prefetch_l2(P.kplane + pf, kPageBytes);
-          prefetch_l2(P.vplane + pf, kPageBytes);
-        }
-      }
+      if (i >= 1) mbar_wait(q_free, (i - 1) & 1);  // the previous unit's Q tile is in TMEM
       const int copies = si->copies, rpc = 128 / copies;
       if (lane == 0) mbar_arrive_expect_tx(&item_full[buf], 2u * half_bytes * (uint32_t)(n_mem * copies));
       __syncwarp();
@@ -513,7 +469,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           const int g = g0 + blk;
           const int e0 = blk * kBlkPages;
           const int sl = g % nsl, np = min(kBlkPages, n_ent - e0);
-          if (TRACE && is_k && sub == 0 && g < 64) P.trace[blockIdx.x * kTraceWords + 544 + g] = globaltimer();
           if (g >= nsl) mbar_wait(&eb[sl], ((g / nsl) - 1) & 1);
           uint8_t* dst = rb + sl * kSlotBytes;
           if (sub == 0) mbar_arrive_expect_tx(&fb[sl], (uint32_t)np * kPageBytes);
@@ -546,11 +501,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         tc::mma_commit(q_free);
         for (int blk = 0; blk < nblk; ++blk, ++g) {
           const int sb = g % kSBufs, sl = g % kKSlots;
-          if (TRACE && g < 64) P.trace[blockIdx.x * kTraceWords + 128 + g] = globaltimer();
           if (g >= kSBufs) mbar_wait(&pv_done[sb], ((g - kSBufs) / kSBufs) & 1);  // P(g - kSBufs) consumed
           mbar_wait(&kfull[sl], (g / kKSlots) & 1);
           tc::fence_after();
-          const long long c0 = TRACE ? clock64() : 0;
           const uint64_t kd = kdesc0 + (uint64_t)(sl * (kSlotBytes >> 4));
           switch (sb) {
             case 0: issue_qk_mmas<0>(kd); break;
@@ -561,10 +514,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           }
           tc::mma_commit(&s_full[sb]);
           tc::mma_commit(&kempty[sl]);
-          if (TRACE && g < 64) {
-            P.trace[blockIdx.x * kTraceWords + 192 + g] = globaltimer();
-            P.trace[blockIdx.x * kTraceWords + 352 + g] = clock64() - c0;  // QK issue cycles (data ready)
-          }
         }
         tc::mma_commit(&slot_empty[ub]);  // Q smem tile consumed
       }
@@ -585,17 +534,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         for (int blk = 0; blk < nblk; ++blk, ++g) {
           const int sb = g % kSBufs;
           mbar_wait(&p_full[sb], (g / kSBufs) & 1);
-          if (TRACE && g < 64) P.trace[blockIdx.x * kTraceWords + 480 + g] = globaltimer();
           if (blk == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue drained O
           mbar_wait(&vfull[g % kVSlots], (g / kVSlots) & 1);
           tc::fence_after();
-          const long long c1 = TRACE ? clock64() : 0;
           const uint64_t vd = vdesc0 + (uint64_t)((g % kVSlots) * (kSlotBytes >> 4));
           const int np = n_ent - blk * kBlkPages;
           const uint32_t acc0 = blk > 0 ? 1u : 0u;  // the unit's first block opens O
-#if MV_DEC_FAKE_NOPV  // timing experiment only (wrong results): no P.V MMAs
-          if (false)
-#endif
           switch (sb) {
             case 0: issue_pv_mmas<0>(vd, np, acc0); break;
             case 1: issue_pv_mmas<1>(vd, np, acc0); break;
@@ -606,7 +550,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           tc::mma_commit(&vempty[g % kVSlots]);  // also certifies PV(g) to the softmax (O rescale)
           tc::mma_commit(&pv_done[sb]);
           if (blk == nblk - 1) tc::mma_commit(o_full);
-          if (TRACE && g < 64) P.trace[blockIdx.x * kTraceWords + 416 + g] = clock64() - c1;  // PV issue cycles
         }
       }
     }
@@ -630,12 +573,10 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       const int n_ent = si->n_entries, n_mem = si->n_mem, copies = si->copies;
       const PageRef* se = s_ent0 + buf * kMaxEntries;
       float m_ref, l;
-      if (copies == 4)
-        softmax_unit<4, TRACE>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
-      else if (copies == 2)
-        softmax_unit<2, TRACE>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
+      if (copies == 2)
+        softmax_unit<2>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
       else
-        softmax_unit<1, TRACE>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
+        softmax_unit<1>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
       // hand (m, l_half) and the unit header to the epilogue, release the unit slot
       if (i >= 1) mbar_wait(o_empty, (i - 1) & 1);
       s_stat[half * 128 + r] = make_float2(m_ref, l);
@@ -668,7 +609,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       for (int cc = 0; cc < F; ++cc) ml.y += s_stat[cc * rpc + lr].y + s_stat[128 + cc * rpc + lr].y;
       mbar_wait(o_full, i & 1);
       tc::fence_after();
-      if (TRACE && r == 0 && i < 32) P.trace[blockIdx.x * kTraceWords + 256 + i] = globaltimer();
       const int head = kvh * P.gqa + hl;
       const int nslots = active ? P.slot_cnt[b] : 0;
       const int64_t orow = (int64_t)b * P.q_heads + head;
@@ -732,7 +672,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       __syncwarp();
       if (lane == 0) mbar_arrive(o_empty);
       if (active && nslots > 1) __stcg(P.part_ml + slot * P.q_heads + head, ml);
-      if (TRACE && r == 0 && i < 32) P.trace[blockIdx.x * kTraceWords + 288 + i] = globaltimer();
     }
   }
   tc::fence_before();
@@ -881,13 +820,11 @@ struct DecodePlanCache {
   size_t cap_stage = 0;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   int stage_k = 0;
-  unsigned long long* d_trace = nullptr;
   ~DecodePlanCache() {
     for (int k = 0; k < 2; ++k) {
       if (h_stage[k]) cudaFreeHost(h_stage[k]);
       if (stage_ev[k]) cudaEventDestroy(stage_ev[k]);
     }
-    cudaFree(d_trace);
     cudaFree(d_counter);
     cudaFree(d_units);
     cudaFree(d_q_tile);
@@ -978,7 +915,6 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
   const int64_t target_units = (int64_t)num_sms * 3 / 2;
   int chunk = kMaxChunk;
   while (chunk > 16 && total_pages * kv_heads / chunk < target_units) chunk /= 2;
-  if (const char* e = getenv("MV_DECODE_CHUNK")) chunk = std::max(4, std::min(kMaxChunk, atoi(e)));  // A/B knob
 
   std::vector<WorkItem> items;
   std::vector<int32_t> tags, tag_c0;  // per item: handle whose private tail it ends (-1), its first entry
@@ -1002,10 +938,8 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
         const int rows = w.n_mem * R;
         // Wide cascade units (33-64 rows: two lane quadrants, so two SMSPs carry their softmax)
         // get a second row copy in the other two quadrants, each copy exponentiating half of
-        // every block's columns: the softmax spreads over all four SMSPs (C2 +2%).  Four copies
-        // for narrow units stay behind -DMV_DEC_COPIES=1 (slower and not parity-clean).
-        w.copies = kUseCopies ? (rows <= 32 ? 4 : (rows <= 64 ? 2 : 1)) : ((rows > 32 && rows <= 64) ? 2 : 1);
-        (void)rows;
+        // every block's columns: the softmax spreads over all four SMSPs (C2 +2%).
+        w.copies = (rows > 32 && rows <= 64) ? 2 : 1;
         for (size_t k = m0; k < m1; ++k) {
           w.members[k - m0] = s.mem[k];
           slots_of[s.mem[k]].push_back(n_slots + (int32_t)(k - m0));
@@ -1080,8 +1014,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   if (!st.plan) st.plan = new DecodePlanCache();
   DecodePlanCache& pc = *st.plan;
   if (!pc.smem_set) {
-    MV_CUDA_TRY(cudaFuncSetAttribute(decode_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
-    MV_CUDA_TRY(cudaFuncSetAttribute(decode_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    MV_CUDA_TRY(cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     int dev = 0;
     MV_CUDA_TRY(cudaGetDevice(&dev));
     MV_CUDA_TRY(cudaDeviceGetAttribute(&pc.num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1113,7 +1046,6 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
                (pc.tail_item[b] < 0 || sig[3 * b] - pc.tail_c0[b] > std::min(kMaxEntries, pc.info.chunks + 16)))
         incr = false;  // a tail chunk may outgrow the plan's chunk size by 16 pages before a re-plan
     }
-    if (getenv("MV_DECODE_LOG")) fprintf(stderr, "[mv decode] plan %s\n", incr ? "grow tail in place" : "rebuild");
     if (incr) {
       for (int b = 0; b < n; ++b) {
         if (sig[3 * b] == pc.sig[3 * b]) continue;
@@ -1142,11 +1074,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     }
   }
   if (!same) {
-    const auto t_plan = std::chrono::steady_clock::now();
     build_plan(st, pc, hs, n, cfg.kv_heads, gqa, pc.num_sms);
-    if (getenv("MV_DECODE_LOG"))
-      fprintf(stderr, "[mv decode] build_plan (%d handles): %.3f ms host\n", n,
-              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_plan).count());
     pc.handles.assign(hs, hs + n);
     pc.sig = sig;
     pc.q_heads = q_heads;
@@ -1215,21 +1143,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   P.gqa = gqa;
   P.R = R;
   P.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
-  {
-    const char* pfh = getenv("MV_DECODE_PF_HEAD");
-    const char* pft = getenv("MV_DECODE_PF_TAIL");
-    P.pf_head = pfh ? atoi(pfh) : 0;  // measured: L2 prefetching only adds DRAM traffic (tools/pf_sweep.sh)
-    P.pf_tail = pft ? atoi(pft) : 0;
-  }
   const int grid = std::min(P.n_units, pc.num_sms);
-  P.trace = nullptr;
-  const char* trace_path = getenv("MV_DECODE_TRACE");
-  const size_t trace_words = (size_t)pc.num_sms * kTraceWords;
-  if (trace_path) {
-    if (!pc.d_trace) MV_CUDA_TRY(cudaMalloc(&pc.d_trace, sizeof(unsigned long long) * trace_words));
-    MV_CUDA_TRY(cudaMemsetAsync(pc.d_trace, 0, sizeof(unsigned long long) * trace_words, stream));
-    P.trace = pc.d_trace;
-  }
   // decode_tc and combine are launched programmatically dependent on the kernel before them
   // (PDL): their launch latency and prologue overlap the predecessor's tail
   cudaLaunchAttribute pdl[1];
@@ -1242,8 +1156,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   lc.stream = stream;
   lc.attrs = pdl;
   lc.numAttrs = 1;
-  if (P.trace) MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel<true>, P));
-  else MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel<false>, P));
+  MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel, P));
   MV_LAUNCH_CHECK();
   if (!pc.multi.empty()) {
     int max_slots = 0;
@@ -1257,15 +1170,6 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
                                    (const int32_t*)pc.d_multi, (int)pc.multi.size(), (const int32_t*)pc.d_slot_ptr,
                                    (const int32_t*)pc.d_slot_idx, q_heads, d_out, (int)(out_dtype == 1), wide));
     MV_LAUNCH_CHECK();
-  }
-  if (trace_path) {
-    std::vector<unsigned long long> h(trace_words);
-    MV_CUDA_TRY(cudaMemcpyAsync(h.data(), pc.d_trace, h.size() * 8, cudaMemcpyDeviceToHost, stream));
-    MV_CUDA_TRY(cudaStreamSynchronize(stream));
-    if (FILE* f = fopen(trace_path, "wb")) {
-      fwrite(h.data(), 8, h.size(), f);
-      fclose(f);
-    }
   }
   return MV_OK;
 }

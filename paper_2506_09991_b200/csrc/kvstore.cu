@@ -238,11 +238,6 @@ __global__ void k_append_data(AppendPlan pl, const int32_t* __restrict__ page_ou
 }
 
 // Engine fast path: one token per handle, in place (one warp per handle, 4 per CTA).
-struct TokDesc {
-  int64_t idx;     // arena index of the entry to extend / create
-  int32_t fresh;   // 1 -> pop a page and create entry (page,0,1); 0 -> grow entry in place
-  int32_t cumv;    // cum value for a fresh entry
-};
 // Descriptors of up to kDescInline tokens travel in the launch's parameter space (no separate
 // host->device copy in the stream); larger batches use an uploaded array.
 constexpr int kDescInline = 240;
@@ -283,7 +278,8 @@ __device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef
   int page = -1, slot = 0;
   if (lane == 0) {
     if (td.fresh) {
-      // a failed pop leaves the stack usable only for reporting: the sticky error poisons the store
+      // the host reserved this page (PagedStore::reserve_pages), so the pop cannot fail; a failure
+      // is a reservation bug, reported through err at the next reservation sync
       int old = atomicSub(free_top, 1);
       if (old >= 1) {
         page = free_stack[old - 1];
@@ -498,6 +494,7 @@ mv_status PagedStore::init() {
   k_init_free<<<grid_for(cfg_.num_pages, 256), 256, 0, stream_>>>(d_free_, cfg_.num_pages, d_free_top_);
   MV_LAUNCH_CHECK();
   MV_CUDA_TRY(cudaStreamSynchronize(stream_));
+  free_lb_ = cfg_.num_pages;
   return MV_OK;
 }
 
@@ -616,13 +613,24 @@ void* PagedStore::pinned(size_t bytes) {
   return pinned_;
 }
 
-mv_status PagedStore::check_device_error(const char* what) {
-  int32_t e = 0;
-  MV_CUDA_TRY(cudaMemcpyAsync(&e, d_err_, sizeof e, cudaMemcpyDeviceToHost, stream_));
-  MV_CUDA_TRY(cudaStreamSynchronize(stream_));
-  if (e & (int)kErrNoPages)
-    return fail(MV_ERR_CAPACITY, std::string(what) + ": store capacity of " +
-                                     std::to_string((int64_t)cfg_.num_pages * kPageTokens) + " tokens exceeded");
+mv_status PagedStore::reserve_pages(int64_t m, const char* what) {
+  if (m <= 0) return MV_OK;
+  if (m > free_lb_) {
+    // the bound says the pool may run out: wait for the queued pops / releases and re-read the stack
+    int32_t top = 0, e = 0;
+    MV_CUDA_TRY(cudaMemcpyAsync(&top, d_free_top_, sizeof top, cudaMemcpyDeviceToHost, stream_));
+    MV_CUDA_TRY(cudaMemcpyAsync(&e, d_err_, sizeof e, cudaMemcpyDeviceToHost, stream_));
+    MV_CUDA_TRY(cudaStreamSynchronize(stream_));
+    if (e) {
+      MV_CUDA_TRY(cudaMemsetAsync(d_err_, 0, sizeof(int32_t), stream_));
+      return fail(MV_ERR_CUDA, std::string(what) + ": internal error: a device page pop failed");
+    }
+    free_lb_ = top;
+    if (m > free_lb_)
+      return fail(MV_ERR_CAPACITY, std::string(what) + ": store capacity of " +
+                                       std::to_string((int64_t)cfg_.num_pages * kPageTokens) + " tokens exceeded");
+  }
+  free_lb_ -= m;
   return MV_OK;
 }
 
@@ -658,7 +666,7 @@ mv_status PagedStore::fork(uint64_t h, int32_t n, uint64_t* out) {
     c.cum = src->cum;
     c.tail_room = 0;  // the parent keeps the in-place budget of the shared tail page
     c.lineage = src->lineage;
-    c.lineage.push_back({group, src->n_entries(), src->n_tokens()});
+    c.lineage.push_back({group, src->n_entries(), src->n_tokens(), h, src->version});
     offs[k] = off;
   }
   if (src->n_entries() > 0) {
@@ -677,14 +685,19 @@ mv_status PagedStore::extend(uint64_t h, const int32_t* tokens, int64_t n, const
   HandleRec* src = find(h);
   if (!src) return unknown(h);
   HandleRec r;
-  r.cum = src->cum;
-  r.lineage = src->lineage;
   const int32_t fill = (int32_t)std::min<int64_t>(src->tail_room, n);
   const int64_t rest = n - fill;
   const int32_t new_pages = (int32_t)((rest + kPageTokens - 1) / kPageTokens);
+  // capacity first (kvcache.cpp:37-41 throws before the store changes)
+  if (mv_status st = reserve_pages(new_pages, "extend")) return st;
   int32_t cap;
   int64_t off = arena_alloc(src->n_entries() + new_pages + 1, &cap);
-  if (off < 0) return fail(MV_ERR_CAPACITY, "page-table arena exhausted");
+  if (off < 0) {
+    unreserve_pages(new_pages);
+    return fail(MV_ERR_CAPACITY, "page-table arena exhausted");
+  }
+  r.cum = src->cum;
+  r.lineage = src->lineage;
   r.arena_off = off;
   r.cap = cap;
   // 1) copy the source table (shares every page; one ref per copied entry)
@@ -706,6 +719,7 @@ mv_status PagedStore::extend(uint64_t h, const int32_t* tokens, int64_t n, const
   pl.tok_base = (int32_t)src->n_tokens();
   if (n > 0) {
     void *d_tok = nullptr, *d_rec = nullptr;
+    // (a CUDA failure from here on leaves the store unusable, as any CUDA error does)
     if (mv_status st = upload(tokens, sizeof(int32_t) * n, &d_tok, 1)) return st;
     if (payloads && cfg_.record_bytes > 0)
       if (mv_status st = upload(payloads, (size_t)n * cfg_.record_bytes, &d_rec, 2)) return st;
@@ -730,11 +744,6 @@ mv_status PagedStore::extend(uint64_t h, const int32_t* tokens, int64_t n, const
       r.tail_room = src->tail_room - fill;
     }
     src->tail_room = 0;
-    if (new_pages > 0)
-      if (mv_status st = check_device_error("extend")) {
-        arena_free(r.arena_off, r.cap);
-        return st;
-      }
   } else {
     // zero-token extend: a second handle on the same tail; nobody may fill it in place now
     r.tail_room = 0;
@@ -756,11 +765,18 @@ mv_status PagedStore::merge(uint64_t prefix, const uint64_t* branches, int32_t n
   r.lineage = p->lineage;
   segs.push_back({p->arena_off, 0, 0, 0, 0, 0, 0});
   int32_t out_n = p->n_entries();
+  bool all_proven = true;
   for (int b = 0; b < nb; ++b) {
     HandleRec* br = find(branches[b]);
     if (!br) return unknown(branches[b]);
     if (br->n_tokens() < plen)
       return fail(MV_ERR_NOT_DESCENDANT, "branch shorter than the merge prefix");  // kvcache.cpp:262-265
+    // host proof of the slot-identity precondition: the branch descends from a fork of `prefix`
+    // taken while `prefix` was exactly as it is now (its version is unchanged since)
+    bool proven = br == p;
+    for (auto& lg : br->lineage)
+      if (lg.src == prefix && lg.src_version == p->version && lg.tokens == plen) proven = true;
+    all_proven = all_proven && proven;
     bdesc.push_back({br->arena_off, br->n_entries(), 0});
     if (br->n_tokens() == plen) continue;
     // first branch entry holding token `plen`
@@ -781,8 +797,9 @@ mv_status PagedStore::merge(uint64_t prefix, const uint64_t* branches, int32_t n
     }
     out_n += br->n_entries() - k;
   }
-  // slot-identity precondition, checked on device (synchronous: merge throws like the reference)
-  if (nb > 0 && plen > 0) {
+  // slot-identity precondition (kvcache.cpp:268-274) for branches the lineage does not prove:
+  // checked on the device, synchronously (merge throws like the reference)
+  if (nb > 0 && plen > 0 && !all_proven) {
     void* d_b;
     if (mv_status st = upload(bdesc.data(), sizeof(BranchDesc) * bdesc.size(), &d_b, 4)) return st;
     int32_t* d_bad = (int32_t*)device_scratch(sizeof(int32_t), 5);
@@ -863,6 +880,7 @@ mv_status PagedStore::stats(mv_kv_stats* out) {
   MV_CUDA_TRY(cudaMemcpyAsync(host, cnt, sizeof host, cudaMemcpyDeviceToHost, stream_));
   MV_CUDA_TRY(cudaMemcpyAsync(&top, d_free_top_, sizeof top, cudaMemcpyDeviceToHost, stream_));
   MV_CUDA_TRY(cudaStreamSynchronize(stream_));
+  free_lb_ = top;  // exact after the sync
   out->physical_tokens_stored = host[0];
   out->logical_tokens_reachable = (uint64_t)logical_;
   out->bytes_copied_on_last_op = 0;
@@ -902,23 +920,41 @@ mv_status PagedStore::append(const uint64_t* hs, int32_t n, const int32_t* d_tok
   if (n <= 0) return n == 0 ? MV_OK : fail(MV_ERR_INVALID_ARGUMENT, "append: n < 0");
   if ((d_k || d_v) && (cfg_.kv_heads == 0 || layer < 0 || layer >= cfg_.layers || !d_pos))
     return fail(MV_ERR_INVALID_ARGUMENT, "append: no attention plane for this layer / positions missing");
-  std::vector<TokDesc> desc(n);
+  // pass 1 validates everything before any state changes: unknown handles, a handle listed twice
+  // (two warps would extend the same entry), table capacity, and the pages this call pops
+  std::vector<HandleRec*>& recs = append_recs_;
+  recs.resize(n);
+  const uint64_t stamp = ++call_stamp_;
+  int64_t fresh = 0;
   for (int i = 0; i < n; ++i) {
     HandleRec* r = find(hs[i]);
     if (!r) return unknown(hs[i]);
+    if (r->stamp == stamp) return fail(MV_ERR_INVALID_ARGUMENT, "append: handle " + std::to_string(hs[i]) + " listed twice");
+    r->stamp = stamp;
+    recs[i] = r;
+    if (r->tail_room == 0) {
+      ++fresh;
+      if (mv_status st = ensure_cap(*r, r->n_entries() + 1)) return st;  // moves the table only
+    }
+  }
+  if (mv_status st = reserve_pages(fresh, "append")) return st;
+  // pass 2 commits the host metadata (cannot fail)
+  std::vector<TokDesc>& desc = append_desc_;
+  desc.resize(n);
+  for (int i = 0; i < n; ++i) {
+    HandleRec* r = recs[i];
     if (r->tail_room > 0) {
       desc[i] = {r->arena_off + r->n_entries() - 1, 0, 0};
       r->tail_room--;
       r->cum.back()++;
     } else {
-      if (mv_status st = ensure_cap(*r, r->n_entries() + 1)) return st;
       desc[i] = {r->arena_off + r->n_entries(), 1, (int32_t)r->n_tokens()};
       r->cum.push_back(r->cum.back() + 1);
       r->tail_room = kPageTokens - 1;
     }
     r->version++;
-    logical_ += 1;
   }
+  logical_ += n;
   __nv_bfloat16* kpl = d_k ? k_planes_[layer] : nullptr;
   __nv_bfloat16* vpl = d_k ? v_planes_[layer] : nullptr;
   if (n <= kDescInline) {  // descriptors ride in the launch parameters: no copy in the stream
@@ -981,7 +1017,11 @@ mv_status PagedStore::append_many(uint64_t h, int64_t n, const int32_t* d_tokens
   const int32_t fill = (int32_t)std::min<int64_t>(r->tail_room, n);
   const int64_t rest = n - fill;
   const int32_t new_pages = (int32_t)((rest + kPageTokens - 1) / kPageTokens);
-  if (mv_status st = ensure_cap(*r, r->n_entries() + new_pages + 1)) return st;
+  if (mv_status st = reserve_pages(new_pages, "append_many")) return st;
+  if (mv_status st = ensure_cap(*r, r->n_entries() + new_pages + 1)) {
+    unreserve_pages(new_pages);
+    return st;
+  }
   AppendPlan pl;
   pl.tail_idx = fill > 0 ? r->arena_off + r->n_entries() - 1 : -1;
   pl.new_idx = r->arena_off + r->n_entries();

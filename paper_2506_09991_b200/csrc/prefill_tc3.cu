@@ -25,10 +25,8 @@
 // Tile lists come from tile_map2: item tile t reads its own list (the k tiles whose status for
 // that 128-row tile is not 0, hcount[t] of them; entries keep the pair layout kt | stA << 20 |
 // stB << 22, so the status of tile t sits at bit 20 + 2 (t & 1)).
-#include <cstdio>
 #include <algorithm>
-#include <cstdlib>
-#include <vector>
+#include <mutex>
 
 #include "tc_common.cuh"
 
@@ -36,17 +34,11 @@ namespace mv {
 namespace {
 
 constexpr int kT3 = 128;
-#ifndef MV_PF_QBUF
-#define MV_PF_QBUF 2
-#endif
-constexpr int kQB3 = MV_PF_QBUF;       // Q tiles (item i uses tile i % kQB3)
+constexpr int kQB3 = 2;                // Q tiles (item i uses tile i % kQB3; 3 Q tiles + 2 K slots measured 3% slower)
 constexpr int kKSt3 = 5 - kQB3;        // K ring slots (Q tiles + K slots share 5 x 32 KiB)
 constexpr int kVSt3 = 2;
 constexpr int kThreads3 = 384;   // 12 warps: loader, MMA, 8 softmax, 2 Q rotators
 constexpr int kRotWarp0 = 10;
-#ifndef MV_PF_NOROT
-#define MV_PF_NOROT 0
-#endif    // warps 10-11 rotate each item's raw Q tile in shared memory
 constexpr int kHalf3 = kT3 * 128;  // SW128 half tile: 128 rows x 64 dims
 constexpr int kTile3 = 2 * kHalf3;
 constexpr int kOffQ3 = 0;  // two Q tiles: item i loads and rotates into tile i & 1
@@ -74,19 +66,8 @@ struct Tc3Params {
   int n, hq, hkv, D, n_qt, stride;
   float scale_log2;
   int n_items;
-  int* counters;
-  unsigned long long* trace;  // MV_PF_TRACE builds only: CTA 0 timeline, [tile][8] clock64
+  int* counters;           // [2] work queue / finished CTAs, in the caller's workspace (zeroed by the RoPE pass)
 };
-
-#ifndef MV_PF_TRACE
-#define MV_PF_TRACE 0
-#endif
-constexpr int kTrace3 = 1024;
-#define PF3_TRACE(step, k)                                             \
-  do {                                                                 \
-    if (MV_PF_TRACE && blockIdx.x == 0 && (step) < kTrace3)            \
-      P.trace[(step) * 8 + (k)] = clock64();                           \
-  } while (0)
 
 struct __align__(16) Item3 {
   int t, h, m, valid;
@@ -108,10 +89,8 @@ __device__ __forceinline__ void pv3(uint64_t vd, bool first) {
     tc::mma_ts(kO0, kS0 + B * 128 + k * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV3, (!first || k > 0) ? 1u : 0u);
 }
 
-#ifndef MV_PF_POLY
-#define MV_PF_POLY 8  // 1 pair in 8: +2.5% on C3 (16 and 4..6 measured no better)
-#endif
-constexpr int kPolyMod3 = MV_PF_POLY;  // every kPolyMod3-th score pair takes poly_exp2x2 (0: none)
+// every kPolyMod3-th score pair takes poly_exp2x2: 1 pair in 8 gave +2.5% on C3 (16 and 4..6 no better)
+constexpr int kPolyMod3 = 8;
 
 __device__ __forceinline__ uint32_t bit_range3(int lo, int hi) {
   lo = max(lo, 0);
@@ -285,7 +264,6 @@ __global__ void __launch_bounds__(kThreads3, 1)
         for (int j = 0; j < m; ++j, ++g) {
           mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
           mbar_wait(&p_full[g % kSB], (g / kSB) & 1);
-          PF3_TRACE(g, 0);
           if (j == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue of item i-1 read O
           tc::fence_after();
           const uint64_t vd = vd0 + (uint64_t)(((g % kVSt3) * kTile3) >> 4);
@@ -298,7 +276,6 @@ __global__ void __launch_bounds__(kThreads3, 1)
             qk(qd, g + kSB);  // S buffer g % 3 again: in order behind P.V(g)
             if (j + kSB + 1 == m) tc::mma_commit(&q_empty[qb]);
           }
-          PF3_TRACE(g, 1);
         }
         if (m == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);
         tc::mma_commit(o_fin);
@@ -323,7 +300,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       // 32 chunks per thread in 4 batches of 8: all table loads of a batch are in flight together
       // (the table comes from L2; a light item's rotation is otherwise on the MMA's critical path)
       constexpr int kBatch = 8;
-      for (int b0 = 0; b0 < (MV_PF_NOROT ? 0 : kT3 * 16 / 64); b0 += kBatch) {
+      for (int b0 = 0; b0 < kT3 * 16 / 64; b0 += kBatch) {
         float4 t01[kBatch], t23[kBatch];
         uint4* q4[kBatch];
 #pragma unroll
@@ -388,23 +365,13 @@ __global__ void __launch_bounds__(kThreads3, 1)
         const int status = (e >> sh) & 3;
         const uint32_t s_col = kS0 + (g % kSB) * 128;
         mbar_wait(&s_full[g % kSB], (g / kSB) & 1);
-        const bool tr = r == 0;
-        if (tr) PF3_TRACE(g, c ? 6 : 2);
         tc::fence_after();
-#if MV_PF_NOSOFT
-        if (true) { mbar_arrive(&p_full[g % kSB]); continue; }
-#endif
         float v[64];
         tc::tmem_ld32(lane_base + s_col + c * 64, v);
         tc::tmem_ld32(lane_base + s_col + c * 64 + 32, v + 32);
         tc::tmem_wait_ld();
-        if (tr && !c) PF3_TRACE(g, 3);
         float mx0 = -INFINITY, mx1 = -INFINITY;
-#if MV_PF_NOMASK  // timing experiment only (wrong results): every tile treated as full
-        if (false) {
-#else
         if (status != 1) {
-#endif
           const int lim = min(i, P.n - 1) - j0;  // last visible column
           uint32_t vm[2];
 #pragma unroll
@@ -438,7 +405,6 @@ __global__ void __launch_bounds__(kThreads3, 1)
         xs[c * 128 + r] = fmaxf(mx0, mx1);
         pair_sync(quarter);
         const float mx = fmaxf(xs[r], xs[128 + r]) * P.scale_log2;
-        if (tr && !c) PF3_TRACE(g, 4);
         const bool need = mx > m_ref + kLazy3;
         if (__any_sync(0xffffffffu, need)) {
           const float nref = need ? fmaxf(m_ref, mx) : m_ref;
@@ -483,7 +449,6 @@ __global__ void __launch_bounds__(kThreads3, 1)
         l += (la.x + lb.x) + (la.y + lb.y);
         tc::tmem_wait_st();
         tc::fence_before();
-        if (tr) PF3_TRACE(g, c ? 7 : 5);
         mbar_arrive(&p_full[g % kSB]);
       }
       // epilogue: row sum over both halves, O / l for this warp's 64 dims
@@ -521,10 +486,6 @@ __global__ void __launch_bounds__(kThreads3, 1)
   }
   tc::fence_before();
   __syncthreads();
-  if (threadIdx.x == 0 && atomicAdd(&P.counters[1], 1) == (int)gridDim.x - 1) {
-    P.counters[0] = 0;  // every CTA has stopped claiming: re-arm the queue for the next launch
-    P.counters[1] = 0;
-  }
   if (warp == 1) {
     tc::fence_after();
     tc::tmem_dealloc(0, 512);
@@ -537,7 +498,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
 mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
                              const float2* cs, const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
                              int32_t kv_heads, void* d_out, int32_t out_dtype, const int32_t* hcount,
-                             const int32_t* tlist, int32_t stride, cudaStream_t st) {
+                             const int32_t* tlist, int32_t stride, int32_t* counters, cudaStream_t st) {
   if (max_depth > 8) return fail(MV_ERR_INVALID_ARGUMENT, "prefill: max_depth > 8");
   CUtensorMap mq, mk, mvv;
   if (mv_status e = tc::make_rows_map(&mq, q_raw, n, q_heads, kT3)) return e;
@@ -558,34 +519,18 @@ mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_
   T.stride = stride;
   T.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
   T.n_items = T.n_qt * q_heads;
-  static int* counters_dev[kMaxDevices] = {};
+  static std::once_flag attr_once[kMaxDevices];
   static int sms_dev[kMaxDevices] = {};
   const int cur = current_device();
-  int*& d_counters = counters_dev[cur];
-  int& num_sms = sms_dev[cur];
-  if (!d_counters) {
-    MV_CUDA_TRY(cudaMalloc(&d_counters, 2 * sizeof(int)));
-    MV_CUDA_TRY(cudaMemsetAsync(d_counters, 0, 2 * sizeof(int), st));
-    int dev = 0;
-    MV_CUDA_TRY(cudaGetDevice(&dev));
-    MV_CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
-    MV_CUDA_TRY(cudaFuncSetAttribute(prefill_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem3));
-  }
-  T.counters = d_counters;
-  T.trace = nullptr;
-  if (MV_PF_TRACE) {
-    static unsigned long long* trace_dev[kMaxDevices] = {};
-    unsigned long long*& d_trace = trace_dev[cur];
-    const size_t tb = kTrace3 * 8 * sizeof(unsigned long long);
-    if (!d_trace) MV_CUDA_TRY(cudaMalloc(&d_trace, tb));
-    if (const char* f = getenv("MV_PREFILL_TRACE")) {  // the previous launch's timeline
-      std::vector<unsigned long long> h(kTrace3 * 8);
-      MV_CUDA_TRY(cudaMemcpy(h.data(), d_trace, tb, cudaMemcpyDeviceToHost));
-      if (FILE* fp = fopen(f, "wb")) { fwrite(h.data(), 8, h.size(), fp); fclose(fp); }
-    }
-    MV_CUDA_TRY(cudaMemsetAsync(d_trace, 0, tb, st));
-    T.trace = d_trace;
-  }
+  cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once[cur], [&] {
+    attr_err = cudaDeviceGetAttribute(&sms_dev[cur], cudaDevAttrMultiProcessorCount, cur);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(prefill_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem3);
+  });
+  MV_CUDA_TRY(attr_err);
+  const int num_sms = sms_dev[cur] > 0 ? sms_dev[cur] : 148;
+  T.counters = counters;
   prefill_tc3_kernel<<<std::min(T.n_items, num_sms), kThreads3, kSmem3, st>>>(mq, mk, mvv, T);
   MV_LAUNCH_CHECK();
   return MV_OK;

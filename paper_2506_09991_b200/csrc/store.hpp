@@ -26,16 +26,29 @@ struct HandleRec {
   int32_t tail_room = 0;             // slots of the tail page this handle may fill in place
   // Fork lineage: (share-group id, entry boundary, token boundary). Entries [0, boundary)
   // are identical in every handle holding the group (SURVEY.md §7 H3 cascade).
+  // src / src_version: the forked handle and its version at the fork; while that handle is
+  // unchanged, its whole sequence is a slot-identical prefix of every holder (merge precondition
+  // proven on the host, kvcache.cpp:268-274).
   struct Lineage {
     uint64_t group;
     int32_t entries;
     int64_t tokens;
+    uint64_t src;
+    uint64_t src_version;
   };
   std::vector<Lineage> lineage;
   uint64_t version = 0;              // bumps whenever the table changes (decode plan cache)
+  uint64_t stamp = 0;                // per-call mark (duplicate handles in one append)
 
   int32_t n_entries() const { return (int32_t)cum.size() - 1; }
   int64_t n_tokens() const { return cum.back(); }
+};
+
+// Engine fast-path append descriptor (one token per handle, kvstore.cu).
+struct TokDesc {
+  int64_t idx;     // arena index of the entry to extend / create
+  int32_t fresh;   // 1 -> pop a page and create entry (page,0,1); 0 -> grow entry in place
+  int32_t cumv;    // cum value for a fresh entry
 };
 
 struct DecodePlanCache;  // decode.cu
@@ -79,7 +92,12 @@ class PagedStore {
   // scratch helpers shared with decode.cu
   void* pinned(size_t bytes);                 // host staging (grows; ordered by stream sync points)
   void* device_scratch(size_t bytes, int slot);
-  mv_status check_device_error(const char* what);  // syncs the stream
+  // Page reservation (CacheError::CapacityExceeded, kvcache.cpp:37-41): every page-popping call
+  // reserves its pages against a host lower bound of the device free stack BEFORE it touches any
+  // host or device state. Releases only raise the device count, so the bound stays valid without a
+  // sync; only when it says the pool may run out does the store synchronise and re-read the stack.
+  mv_status reserve_pages(int64_t m, const char* what);
+  void unreserve_pages(int64_t m) { free_lb_ += m; }
   DecodePlanCache* plan = nullptr;
 
  private:
@@ -95,7 +113,11 @@ class PagedStore {
   int32_t* d_refcnt_ = nullptr;
   int32_t* d_free_ = nullptr;      // free-page stack
   int32_t* d_free_top_ = nullptr;  // stack size (device scalar)
-  int32_t* d_err_ = nullptr;       // sticky device error bits (1 = out of pages)
+  int32_t* d_err_ = nullptr;       // device error bits (1 = a page pop failed: a reservation bug)
+  int64_t free_lb_ = 0;            // host lower bound of the device free-page count
+  uint64_t call_stamp_ = 0;
+  std::vector<HandleRec*> append_recs_;  // per-call scratch of append (kept to avoid reallocation)
+  std::vector<TokDesc> append_desc_;
   int32_t* d_slot_tok_ = nullptr;  // token id per slot
   uint8_t* d_records_ = nullptr;   // record_bytes per slot
   std::vector<__nv_bfloat16*> k_planes_, v_planes_;

@@ -613,20 +613,10 @@ extern "C" mv_status mv_tile_map(const int32_t* d_excl, int32_t n, int32_t max_d
 }
 
 namespace mv {
-mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t* d_count, int32_t* d_list,
-                    int32_t stride, cudaStream_t stream, int32_t* d_hcount, int32_t* d_hlist) {
+mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, uint8_t* d_status, int32_t* d_count,
+                    int32_t* d_list, int32_t stride, cudaStream_t stream, int32_t* d_hcount, int32_t* d_hlist) {
+  // statuses in the caller's workspace: a byte array [n_qp][stride]
   const int n_qp = (n + 255) / 256;
-  // statuses in a scratch byte array [n_qp][stride] (persistent per device, grown on demand)
-  static uint8_t* status_dev[kMaxDevices] = {};
-  static size_t status_bytes_dev[kMaxDevices] = {};
-  uint8_t*& d_status = status_dev[current_device()];
-  size_t& status_bytes = status_bytes_dev[current_device()];
-  const size_t need = (size_t)n_qp * stride;
-  if (need > status_bytes) {
-    if (d_status) MV_CUDA_TRY(cudaFree(d_status));
-    MV_CUDA_TRY(cudaMalloc(&d_status, need));
-    status_bytes = need;
-  }
   tile_status_kernel<<<dim3(n_qp, kTm2Split), 256, 0, stream>>>(d_excl, n, max_depth, d_status, stride);
   MV_LAUNCH_CHECK();
   tile_list_kernel<<<n_qp, kTm2Threads, 0, stream>>>(d_status, n, d_count, d_list, stride, d_hcount, d_hlist);
