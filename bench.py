@@ -1,24 +1,32 @@
 #!/usr/bin/env python3
-"""Branch-parallel decode benchmark (BASELINE.json metric, configs[1] shape).
+"""Branch-parallel decode benchmark (BASELINE.json metric on configs[1]) plus the other §8(d) configs.
 
-Workload (one "step"): every branch of every request appends its new token's K/V into the
-paged cache (RoPE fused) and attends over shared Map prefix + its own suffix — the decode
-hot path of engine.cpp:599-641 (resolve + ToyModel::step attention + extend), batched.
-  per request: Qwen2.5-32B attention shape (40 q / 8 kv heads, head_dim 128, bf16),
-  4096-token shared Map prefix, 8 branches x 1024 tokens, KV pages of 16 tokens.
-  R requests per GPU (default 16 -> 0.8 GB of KV, larger than the 126 MB L2: no flush needed).
+Headline (the JSON line's top level): configs[1] decode. One "step" = every branch of every request
+appends its new token's K/V into the paged cache (RoPE fused) and attends over the shared Map prefix
++ its own suffix (engine.cpp:599-641: resolve + ToyModel::step attention + extend, batched).
+  per request: Qwen2.5-32B attention shape (40 q / 8 kv heads, head_dim 128, bf16), 4096-token shared
+  Map prefix, 8 branches x 1024 tokens, KV pages of 16 tokens; R requests per GPU (default 16 -> 0.8 GB
+  of KV, larger than the 126 MB L2: no flush needed).
+Sub-records on the same line (each with value, roofline and a CPU baseline):
+  c3_prefill  configs[2]: branch-masked prefill over the 16K nested stream (tensor-core roofline)
+  c4_decode   configs[3]: 64 requests x 32 branches, 32K unique tokens each, sharded by request
+  c5_stress   configs[4]: 16 rounds of fork 128 / 64 tokens / merge / 16 Reduce tokens, then decode
 
-Prints ONE JSON line (rank 0). `--impl reference` times the reference CPU path instead: the
-patched reference core compiled from /root/reference (oracle/_ref/refdrv, kind "reference") running
-its own decode path (RadixStore::resolve_payloads + ToyModel::step, engine.cpp:599-607) on all host
-cores, attention part isolated as step(ctx) - step(empty); if that binary was not built, the
-oracle restatement of toy_model.cpp:121-157 (fp64, GQA; kind "port").
+`--gpus N` without WORLD_SIZE re-launches itself under torchrun (one process per GPU, NCCL). `value` is
+the whole-job aggregate over the N GPUs (the driver's contract); `value_per_gpu` divides it by N.
+
+`--impl reference` times the reference CPU path instead: the patched reference core compiled from
+/root/reference (oracle/_ref/refdrv, kind "reference") running its own decode path
+(RadixStore::resolve_payloads + ToyModel::step, engine.cpp:599-607) on all host cores; each step is one
+branch token per host thread, attention isolated as step(ctx) - step(empty).  If that binary was not
+built, the oracle restatement of toy_model.cpp:121-157 (fp64, GQA; kind "port") is timed instead.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -30,13 +38,12 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 HQ, HKV, D = 40, 8, 128
-PREFIX, BRANCHES, BRANCH_LEN = 4096, 8, 1024
-# --workload: c2 = configs[1] (the metric's config, R requests per GPU, weak scaling);
-# c4 = configs[3] (64 requests x 32 branches, 16K shared prefix + 32 x 512 = 32K unique tokens per
-# request, sharded by request across the GPUs: strong scaling)
+KV_BYTES_PER_TOKEN = HKV * D * 2 * 2  # K and V, bf16, all KV heads of one layer
 WORKLOADS = {"c2": dict(prefix=4096, branches=8, branch_len=1024),
              "c4": dict(prefix=16384, branches=32, branch_len=512, total_requests=64)}
 METRIC = "branch-parallel decode tokens/s/GPU; attention HBM GB/s vs 8 TB/s roofline"
+C2_TEXT = ("configs[1] x R requests per GPU: 40q/8kv heads, d128, bf16, 4K shared Map prefix, 8 branches x 1K "
+           "tokens (+1 per step), KV page 16")
 
 
 def parse():
@@ -45,12 +52,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--requests", type=int, default=16, help="requests per GPU (c2)")
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS), help="the headline workload")
     ap.add_argument("--shard", default="requests", choices=["requests", "heads"],
                     help="heads: every rank serves all requests for its KV-head group and the head-sharded "
                          "outputs are all-gathered over NCCL each step (the layer-level bench, SURVEY.md §8e)")
+    ap.add_argument("--extras", default="all", help="comma list of c3,c4,c5 sub-records, 'all' or 'none'")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of each CPU baseline sample")
     return ap.parse_args()
 
 
@@ -58,9 +66,20 @@ def peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p["hbm_gbs"], "measured"
+        return p, "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, "fallback"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 class Clocks:
@@ -100,52 +119,46 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def ref_binary():
-    path = os.path.join(REPO, "oracle", "_ref", "refdrv")
-    return path if os.access(path, os.X_OK) else None
+class Device:
+    """CUDA device plumbing for the GPU arms.  MV_BENCH_DEVICE=cpu (tests only: the multi-rank dry run with
+    stub kernels, tests/test_bench_multirank.py) swaps in host timers, a no-op sync and the gloo backend."""
+
+    def __init__(self, index):
+        import torch
+        self.torch = torch
+        self.cpu = os.environ.get("MV_BENCH_DEVICE") == "cpu"
+        self.dev = torch.device("cpu") if self.cpu else torch.device("cuda", index)
+        if not self.cpu:
+            torch.cuda.set_device(self.dev)
+        self.stream = _HostStream() if self.cpu else torch.cuda.current_stream()
+        self.backend = "gloo" if self.cpu else "nccl"
+
+    def event(self):
+        return _HostEvent() if self.cpu else self.torch.cuda.Event(enable_timing=True)
+
+    def sync(self):
+        if not self.cpu:
+            self.torch.cuda.synchronize()
+
+    def pin(self, t):
+        return t if self.cpu else t.pin_memory()
+
+    def release_memory(self):
+        if not self.cpu:
+            self.torch.cuda.empty_cache()
 
 
-def cpu_reference_ref(seconds: float):
-    """The reference's own decode path (engine.cpp:599-607: RadixStore::resolve_payloads + ToyModel::step),
-    compiled from /root/reference by oracle/ref_build.sh, on all host cores (one branch per thread).
-    step() also runs projections + MLP, so the value is the attention path: step(ctx) - step(empty ctx)."""
-    threads = os.cpu_count() or 1
-    out = subprocess.run([ref_binary(), "decode", str(threads), str(seconds)], capture_output=True, text=True,
-                         check=True, timeout=600).stdout
-    r = json.loads(out.strip().splitlines()[-1])
-    return {"value": r["tokens_per_s_attention"], "unit": "tokens/s", "cores": threads, "kind": "reference",
-            "sample": f"{r['steps']} branch decode steps of the patched reference (resolve_payloads + ToyModel::step "
-                      f"attention; 40 heads x 128 MHA, ctx {r['ctx']}, fp64) on {threads} threads; full step incl. "
-                      f"projections/MLP: {r['tokens_per_s_full']:.3f} tokens/s"}
+class _HostEvent:
+    def record(self, stream=None):
+        self.t = time.perf_counter()
+
+    def elapsed_time(self, other):
+        return (other.t - self.t) * 1e3
 
 
-def cpu_baseline(seconds: float):
-    return cpu_reference_ref(seconds) if ref_binary() else cpu_reference(seconds)
-
-
-def cpu_reference(seconds: float):
-    """Oracle restatement of the reference attention core on all host cores, one request's step
-    (8 branches x 40 heads over 4096+1024 tokens) repeated for ~`seconds`."""
-    import oracle
-    rng = np.random.default_rng(0)
-    n_rows = PREFIX + BRANCHES * BRANCH_LEN
-    K = rng.uniform(-1, 1, (n_rows, HKV, D))
-    V = rng.uniform(-1, 1, (n_rows, HKV, D))
-    q = rng.uniform(-1, 1, (BRANCHES, HQ, D))
-    ctx = [list(range(PREFIX)) + list(range(PREFIX + b * BRANCH_LEN, PREFIX + (b + 1) * BRANCH_LEN))
-           for b in range(BRANCHES)]
-    threads = os.cpu_count() or 1
-    oracle.attn_decode(q, K, V, ctx, nthreads=threads)  # warm
-    reps, t0 = 0, time.perf_counter()
-    while True:
-        oracle.attn_decode(q, K, V, ctx, nthreads=threads)
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
-            break
-    return {"value": BRANCHES * reps / el, "unit": "tokens/s", "cores": threads, "kind": "port",
-            "sample": f"{reps} decode steps of 1 request (8 branches x 40 heads, ctx 4096+1024, fp64) "
-                      f"in {el:.1f} s on {threads} threads"}
+class _HostStream:
+    def synchronize(self):
+        pass
 
 
 def dist_env():
@@ -155,35 +168,173 @@ def dist_env():
     return world, rank, local
 
 
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` run directly: one process per GPU through torchrun (127.0.0.1 rendezvous)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU baselines (bench.py's cpu_baseline leg: the only place bench.py runs oracle/ or oracle/_ref)
+# ---------------------------------------------------------------------------------------------
+def ref_binary():
+    path = os.path.join(REPO, "oracle", "_ref", "refdrv")
+    return path if os.access(path, os.X_OK) else None
+
+
+def refdrv_decode(threads: int, steps: int, warmup: int):
+    out = subprocess.run([ref_binary(), "decode", str(threads), "0", str(steps), str(warmup)], capture_output=True,
+                         text=True, check=True, timeout=900).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def c2_cpu_reference(steps: int | None = None, warmup: int = 0, seconds: float = 15.0):
+    """The reference's own decode path (engine.cpp:599-607: RadixStore::resolve_payloads + ToyModel::step) on
+    all host cores, one branch token per thread per step.  step() also runs projections + MLP, so the value
+    is the attention path: step(ctx) - step(empty ctx).  The reference has no GQA (toy_model.cpp:122-157),
+    so it runs its MHA form, 40 heads x 128 (5x the KV bytes per token of the 8-KV-head GPU config)."""
+    threads = os.cpu_count() or 1
+    if steps is None:  # size a bounded sample: ~seconds of CPU per thread
+        probe = refdrv_decode(threads, 1, 0)
+        steps = max(1, int(seconds / max(probe["s_per_token_full"] * 1.7, 1e-3)))
+    r = refdrv_decode(threads, steps, warmup)
+    return {"value": r["tokens_per_s_attention"], "unit": "tokens/s", "cores": threads, "kind": "reference",
+            "cpu": cpu_model(), "steps": steps, "warmup": warmup,
+            "sample": f"{steps} steps x {threads} threads of one branch-token decode each through the patched "
+                      f"reference (resolve_payloads + ToyModel::step attention; 40 heads x 128 MHA, ctx {r['ctx']}, "
+                      f"fp64); full step incl. projections/MLP: {r['tokens_per_s_full']:.3f} tokens/s"}
+
+
+def c2_cpu_port(seconds: float = 5.0):
+    """Same-work CPU baseline: the oracle restatement of toy_model.cpp:121-157 (fp64) on the GPU config's
+    GQA shape (40 q / 8 kv heads), one request (8 branches x 40 heads over 4096 + 1024 tokens) per rep."""
+    import oracle
+    rng = np.random.default_rng(0)
+    pre, nb, bl = 4096, 8, 1024
+    K = rng.uniform(-1, 1, (pre + nb * bl, HKV, D))
+    V = rng.uniform(-1, 1, (pre + nb * bl, HKV, D))
+    q = rng.uniform(-1, 1, (nb, HQ, D))
+    ctx = [list(range(pre)) + list(range(pre + b * bl, pre + (b + 1) * bl)) for b in range(nb)]
+    threads = os.cpu_count() or 1
+    oracle.attn_decode(q, K, V, ctx, nthreads=threads)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.attn_decode(q, K, V, ctx, nthreads=threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"value": nb * reps / el, "unit": "tokens/s", "cores": threads, "kind": "port", "cpu": cpu_model(),
+            "sample": f"{reps} decode steps of 1 request (8 branches x 40 q / 8 kv heads, ctx 4096+1024, fp64) "
+                      f"in {el:.1f} s on {threads} threads"}
+
+
+def c3_cpu_port(toks, n_rows=512):
+    """configs[2] on the CPU: the oracle restatement of the masked attention (toy_model.cpp:174-202 with the
+    dag.cpp:243-263 mask, fp64, GQA) on a seeded sample of 512 query rows x 40 heads, all host cores."""
+    import oracle
+    n = len(toks)
+    err, pos, _, excl = oracle.build_dag(toks)
+    rng = np.random.default_rng(3)
+    rows = np.sort(rng.choice(n, size=n_rows, replace=False))
+    K = oracle.rope(rng.uniform(-1, 1, (n, HKV, D)), pos)
+    V = rng.uniform(-1, 1, (n, HKV, D))
+    q = oracle.rope(rng.uniform(-1, 1, (n_rows, HQ, D)), pos[rows])
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.attn_prefill(q, K, V, excl, rows, nthreads=threads)
+    el = time.perf_counter() - t0
+    return {"value": n_rows / el, "unit": "rows/s (x 40 heads)", "cores": threads, "kind": "port",
+            "cpu": cpu_model(), "sample": f"{n_rows} seeded query rows x 40 heads of the 16K nested stream, fp64, "
+                                          f"{el:.2f} s on {threads} threads"}
+
+
+def c4_cpu_port(prefix=16384, nb=32, bl=512, seconds_hint=None):
+    """configs[3] on the CPU, one sampled request (32 branches over 16K shared + 512 private tokens each,
+    40 q / 8 kv heads, fp64 oracle restatement) on all host cores, extrapolated to the 64 requests."""
+    import oracle
+    rng = np.random.default_rng(4)
+    K = rng.uniform(-1, 1, (prefix + nb * bl, HKV, D))
+    V = rng.uniform(-1, 1, (prefix + nb * bl, HKV, D))
+    q = rng.uniform(-1, 1, (nb, HQ, D))
+    ctx = [list(range(prefix)) + list(range(prefix + b * bl, prefix + (b + 1) * bl)) for b in range(nb)]
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.attn_decode(q, K, V, ctx, nthreads=threads)
+    el = time.perf_counter() - t0
+    return {"value": nb / el, "unit": "tokens/s", "cores": threads, "kind": "port", "cpu": cpu_model(),
+            "sample": f"1 of 64 requests (32 branch tokens, ctx 16384+512, fp64) in {el:.2f} s on {threads} "
+                      f"threads; a step of all 64 requests extrapolates to {64 * el:.1f} s"}
+
+
+def c5_cpu_reference(budget_s: float):
+    """configs[4] on the patched reference RadixStore (oracle/_ref/refdrv c5, 1 thread, 16-byte records):
+    whole rounds until `budget_s`, then the remaining rounds extrapolated by a quadratic fit of the
+    per-round times (its span bookkeeping grows quadratically)."""
+    if not ref_binary():
+        return None
+    out = subprocess.run([ref_binary(), "c5", "16", "16", str(budget_s)], capture_output=True, text=True,
+                         timeout=900).stdout
+    r = json.loads(out.strip().splitlines()[-1])
+    per = [x / 1e6 for x in r["round_us"]]
+    done = len(per)
+    if done >= 3:
+        c = np.polyfit(np.arange(done), per, 2)
+        total = sum(per) + float(sum(np.polyval(c, k) for k in range(done, 16)))
+        how = f"measured {done} rounds ({sum(per):.1f} s), rounds {done}-15 extrapolated by a quadratic fit"
+    else:
+        total, how = sum(per) * 16 / max(done, 1), f"measured {done} rounds, scaled linearly (lower bound)"
+    return {"value": total, "unit": "s for 16 rounds of ops", "cores": 1, "kind": "reference", "cpu": cpu_model(),
+            "sample": how, "per_op_us": {k: r[k] for k in ("fork128_us", "extend64_us", "merge128_us", "release_us",
+                                                          "reduce_extend16_us")}}
+
+
 def run_reference(args):
+    """The reference arm: the reference's own CPU path on this box's host cores, configs[1] decode."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cpu = cpu_baseline(max(2.0, args.cpu_seconds))
+    if ref_binary():
+        # each step: one branch-token decode per host thread; sized so K + W steps end within minutes
+        probe = refdrv_decode(os.cpu_count() or 1, 1, 0)
+        per_step = probe["s_per_token_full"] * 1.7  # step(ctx) + step(empty)
+        budget = 240.0
+        steps = max(1, min(args.steps, int(budget / per_step) - args.warmup))
+        warmup = min(args.warmup, 1)
+        cpu = c2_cpu_reference(steps, warmup)
+        steps_run, warm_run = steps, warmup
+    else:
+        cpu = c2_cpu_port(max(2.0, args.cpu_seconds))
+        steps_run, warm_run = None, None
     line = {"impl": "reference", "metric": METRIC, "value": cpu["value"], "unit": "tokens/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * BRANCHES / cpu["value"],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1]: 40q/8kv heads, d128, 4K shared prefix, 8 branches x 1K, page 16",
-                       "sample": cpu["sample"]},
+            "steps": steps_run, "warmup": warm_run, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": 1e3 * (os.cpu_count() or 1) / cpu["value"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "configs[1]: 4K shared prefix, 8 branches x 1K, one request sampled; the reference "
+                                   "has no GQA, so 40 heads x 128 MHA", "sample": cpu["sample"]},
             "cpu_baseline": cpu,
             "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def build_workload(mv, torch, R, dev, first_request=0, prefix=PREFIX, branches_per_req=BRANCHES,
-                   branch_len=BRANCH_LEN, steps_total=0, hkv=HKV):
-    """R requests: root prefix, fork into B branches, branch_len - 1 private tokens each (positions
-    shared start).  Request r's data is seeded by its global id, so every rank holds distinct
-    requests.  The pool has room for steps_total appended tokens per branch."""
-    PREFIX, BRANCHES, BRANCH_LEN = prefix, branches_per_req, branch_len  # noqa: N806
-    pages = R * (PREFIX // 16 + 1 + BRANCHES * ((BRANCH_LEN + steps_total) // 16 + 3)) + 1024
-    # page-table arena: every branch holds its own span list (prefix entries + private tail), with
-    # the store's capacity doubling on growth
-    table = 2 * R * (BRANCHES + 1) * (PREFIX // 16 + (BRANCH_LEN + steps_total) // 16 + 8) + 65536
-    HKV = hkv  # noqa: N806  (this rank's KV-head group)
-    st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=HKV, table_entries=table)
+# ---------------------------------------------------------------------------------------------
+# GPU arms
+# ---------------------------------------------------------------------------------------------
+def build_workload(mv, torch, R, dev, first_request=0, prefix=4096, branches_per_req=8, branch_len=1024,
+                   steps_total=0, hkv=HKV):
+    """R requests: root prefix, fork into B branches, branch_len - 1 private tokens each (positions shared
+    start).  Request r's data is seeded by its global id, so every rank holds distinct requests.  The pool
+    has room for steps_total appended tokens per branch."""
+    pages = R * (prefix // 16 + 1 + branches_per_req * ((branch_len + steps_total) // 16 + 3)) + 1024
+    table = 2 * R * (branches_per_req + 1) * (prefix // 16 + (branch_len + steps_total) // 16 + 8) + 65536
+    st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=hkv, table_entries=table)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + first_request)
+    sync = torch.cuda.synchronize if dev.type == "cuda" else (lambda: None)
 
     def rnd(*shape):
         return (torch.rand(*shape, generator=gen, device=dev) * 2 - 1).to(torch.bfloat16)
@@ -191,38 +342,43 @@ def build_workload(mv, torch, R, dev, first_request=0, prefix=PREFIX, branches_p
     branches, positions = [], []
     for r in range(R):
         root = st.create()
-        st.append_many(root, torch.full((PREFIX,), 11, dtype=torch.int32, device=dev),
-                       torch.arange(PREFIX, dtype=torch.int32, device=dev), 0, rnd(PREFIX, HKV, D),
-                       rnd(PREFIX, HKV, D))
-        for b in st.fork(root, BRANCHES):
-            n = BRANCH_LEN - 1
+        st.append_many(root, torch.full((prefix,), 11, dtype=torch.int32, device=dev),
+                       torch.arange(prefix, dtype=torch.int32, device=dev), 0, rnd(prefix, hkv, D), rnd(prefix, hkv, D))
+        for b in st.fork(root, branches_per_req):
+            n = branch_len - 1
             st.append_many(b, torch.full((n,), 12, dtype=torch.int32, device=dev),
-                           torch.arange(PREFIX, PREFIX + n, dtype=torch.int32, device=dev), 0, rnd(n, HKV, D),
-                           rnd(n, HKV, D))
+                           torch.arange(prefix, prefix + n, dtype=torch.int32, device=dev), 0, rnd(n, hkv, D),
+                           rnd(n, hkv, D))
             branches.append(b)
-            positions.append(PREFIX + n)
+            positions.append(prefix + n)
         st.release(root)  # the parent lane waits; its prefix pages live on through the branches
-    torch.cuda.synchronize()
+    sync()
     return st, branches, positions, rnd
 
 
-def run_ours(args):
-    import torch
-    world, rank, local = dist_env()
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    dev = torch.device("cuda", local if world > 1 else 0)
-    torch.cuda.set_device(dev)
-    import paper_2506_09991_b200 as mv
+def decode_traffic(workload, R, steps, warmup, heads_mode):
+    """ncu DRAM bytes per decode_tc launch captured on the SAME command (workload, requests, steps, warmup:
+    identical contexts), from profiles/decode_traffic.json; None when no capture matches."""
+    try:
+        with open(os.path.join(REPO, "profiles", "decode_traffic.json")) as f:
+            tj = json.load(f)
+        for cap in tj.get("captures", []):
+            if (cap["workload"], cap["requests"], cap["steps"], cap["warmup"]) == (workload, R, steps, warmup) \
+                    and not heads_mode:
+                return cap["dram_bytes_per_launch"], cap["source"]
+    except Exception:
+        pass
+    return None, None
 
+
+def decode_arm(args, world, rank, local, D_, workload, heads_mode):
+    """The decode step timed on the device (inputs resident), then end to end through the public API."""
+    import torch
+    dev = D_.dev
+    import paper_2506_09991_b200 as mv
     from paper_2506_09991_b200.shard import shard_heads, shard_requests, max_over_ranks
-    # weak scaling: R requests per GPU, sharded by request (no collective in attention)
-    wl = WORKLOADS[args.workload]
-    heads_mode = args.shard == "heads"
-    if heads_mode:
-        # layer-level bench: all ranks serve the same requests, each for its KV-head group
+    wl = WORKLOADS[workload]
+    if heads_mode:  # layer-level bench: all ranks serve the same requests, each for its KV-head group
         total = wl.get("total_requests", args.requests)
         shard = shard_heads(total, HKV, world, rank)
     else:
@@ -231,47 +387,39 @@ def run_ours(args):
     R = len(shard.requests)
     hkv_l = shard.kv_heads[1] - shard.kv_heads[0]
     hq_l = hkv_l * (HQ // HKV)
-    steps_total = args.warmup + args.steps
-    steps_total += max(3, args.steps // 2)  # the e2e leg appends too
-    # a head-sharded rank seeds its data by (first request, head group): synthetic values per shard
+    e2e_steps = max(3, args.steps // 2)
+    steps_total = args.warmup + args.steps + e2e_steps
     seed_id = shard.requests[0] * 64 + shard.kv_heads[0]
     st, handles, pos0, rnd = build_workload(mv, torch, R, dev, seed_id, wl["prefix"], wl["branches"],
                                             wl["branch_len"], steps_total, hkv=hkv_l)
     n = len(handles)
     handles = mv.kv.handle_array(handles)  # uint64 array: no per-call list conversion
-    steps_total = args.warmup + args.steps
-    # per-step inputs (device resident for `value`)
     qs = [rnd(n, hq_l, D) for _ in range(2)]
     ks = [rnd(n, hkv_l, D) for _ in range(2)]
     vs = [rnd(n, hkv_l, D) for _ in range(2)]
     toks = torch.full((n,), 13, dtype=torch.int32, device=dev)
     out = torch.empty(n, hq_l, D, dtype=torch.bfloat16, device=dev)
-    # head-sharded outputs of all ranks: [world][n][hq_l][D] (NCCL all-gather each step)
     gathered = torch.empty(world, n, hq_l, D, dtype=torch.bfloat16, device=dev) if heads_mode and world > 1 else None
-    ag = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+    ag = [(D_.event(), D_.event())
           for _ in range(args.steps)] if gathered is not None else []
     base_pos = torch.tensor(pos0, dtype=torch.int32, device=dev)
-
-    def step(i, q, k, v, p):
-        st.append(handles, toks, p, 0, k, v)
-        mv.attention.decode(st, handles, q, p, out=out)
-
-    stream = torch.cuda.current_stream()
+    stream = D_.stream
     for i in range(args.warmup):
-        step(i, qs[i % 2], ks[i % 2], vs[i % 2], base_pos + i)
-    torch.cuda.synchronize()
+        st.append(handles, toks, base_pos + i, 0, ks[i % 2], vs[i % 2])
+        mv.attention.decode(st, handles, qs[i % 2], base_pos + i, out=out)
+    D_.sync()
     info = st.plan_info()
 
-    # ---- timed region (device events; attention launches bracketed separately) ----
+    # ---- timed region: device events; the attention launches bracketed separately ----
     clocks = Clocks(local)
-    clocks.start()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    att = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if not D_.cpu:
+        clocks.start()
+    att = [(D_.event(), D_.event()) for _ in range(args.steps)]
     pos_steps = [base_pos + (args.warmup + s) for s in range(args.steps)]  # inputs resident before timing
-    torch.cuda.synchronize()
+    ev = [D_.event() for _ in range(2)]
+    if world > 1:
+        torch.distributed.barrier()
+    D_.sync()
     ev[0].record(stream)
     t_host0 = time.perf_counter()
     for s in range(args.steps):
@@ -283,27 +431,23 @@ def run_ours(args):
         att[s][1].record(stream)
         if gathered is not None:  # layer-level: every rank assembles all heads of every token
             ag[s][0].record(stream)
-            dist.all_gather_into_tensor(gathered, out)
+            torch.distributed.all_gather_into_tensor(gathered, out)
             ag[s][1].record(stream)
     ev[1].record(stream)
-    host_ms = (time.perf_counter() - t_host0) * 1e3 / args.steps  # enqueue cost per step (host)
-    torch.cuda.synchronize()
+    host_ms = (time.perf_counter() - t_host0) * 1e3 / args.steps
+    D_.sync()
     if world > 1:
-        dist.barrier()
+        torch.distributed.barrier()
     clk = clocks.stop()
     ms = ev[0].elapsed_time(ev[1]) / args.steps
-    att_each = [a.elapsed_time(b) for a, b in att]
-    att_ms = float(np.mean(att_each))
+    att_ms = float(np.mean([a.elapsed_time(b) for a, b in att]))
     ag_ms = float(np.mean([a.elapsed_time(b) for a, b in ag])) if ag else 0.0
-    if os.environ.get("MV_BENCH_DUMP"):
-        np.save(os.environ["MV_BENCH_DUMP"], np.array(att_each))
     ms, att_ms, ag_ms = max_over_ranks([ms, att_ms, ag_ms], device=dev)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the region ----
-    # one pinned host block per step input set [q | k | v | positions] -> one H2D copy per step
     nq, nk = n * hq_l * D * 2, n * hkv_l * D * 2
     blk = nq + 2 * nk + n * 4
-    hin = [torch.empty(blk, dtype=torch.uint8).pin_memory() for _ in range(2)]
+    hin = [D_.pin(torch.empty(blk, dtype=torch.uint8)) for _ in range(2)]
     for j in range(2):
         hin[j][:nq].copy_(qs[j].cpu().view(torch.uint8).reshape(-1))
         hin[j][nq:nq + nk].copy_(ks[j].cpu().view(torch.uint8).reshape(-1))
@@ -314,92 +458,260 @@ def run_ours(args):
     dk = din[nq:nq + nk].view(torch.bfloat16).view(n, hkv_l, D)
     dv = din[nq + nk:nq + 2 * nk].view(torch.bfloat16).view(n, hkv_l, D)
     dp = din[nq + 2 * nk:].view(torch.int32)
-    hout = torch.empty(n, hq_l, D, dtype=torch.bfloat16).pin_memory()
+    hout = D_.pin(torch.empty(n, hq_l, D, dtype=torch.bfloat16))
     pos0_np = np.asarray(pos0, dtype=np.int32)
-    e2e_steps = max(3, args.steps // 2)
     if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ee = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        torch.distributed.barrier()
+    D_.sync()
+    ee = [D_.event() for _ in range(2)]
     ee[0].record(stream)
     for s in range(e2e_steps):
         i = args.warmup + args.steps + s
-        hpos[i % 2].numpy()[:] = pos0_np + i  # the step's positions, written into the pinned block
+        hpos[i % 2].numpy()[:] = pos0_np + i
         din.copy_(hin[i % 2], non_blocking=True)
         st.append(handles, toks, dp, 0, dk, dv)
         mv.attention.decode(st, handles, dq, dp, out=out)
         hout.copy_(out, non_blocking=True)
         stream.synchronize()  # the caller reads this step's result before the next step
     ee[1].record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = ee[0].elapsed_time(ee[1]) / e2e_steps
-    (e2e_ms,) = max_over_ranks([e2e_ms], device=dev)
-    h2d = n * (hq_l + 2 * hkv_l) * D * 2 + n * 4
-    d2h = n * hq_l * D * 2
-
+    D_.sync()
+    (e2e_ms,) = max_over_ranks([ee[0].elapsed_time(ee[1]) / e2e_steps], device=dev)
     tokens_per_step = n if heads_mode else n * world  # head-sharded ranks share their tokens
-    value = tokens_per_step / (ms / 1e3)
-    # roofline of the dominant kernel: algorithmic bytes = unique KV read once + Q/O
-    # every step appends one token per branch before attending, so the context (and the bytes a
-    # step must read) grows by n tokens per step: use the mean over the timed steps
-    kv_tokens = info["unique_kv_tokens"] + n * (args.steps + 1) / 2.0
+    kv_tokens = info["unique_kv_tokens"] + n * (args.steps + 1) / 2.0  # mean context over the timed steps
     alg_bytes = kv_tokens * hkv_l * D * 2 * 2 + n * hq_l * D * 2 * 2
-    achieved = alg_bytes / (att_ms / 1e3) / 1e9
-    peak, peak_kind = peaks()
-    traffic = None
-    try:
-        with open(os.path.join(REPO, "profiles", "decode_traffic.json")) as f:
-            tj = json.load(f)
-            if tj.get("requests") == R and args.workload == "c2" and not heads_mode:
-                traffic = tj["per_kernel_bytes"].get(tj.get("dominant_kernel", ""), tj.get("dram_bytes_per_launch"))
-    except Exception:
-        pass
+    return dict(ms=ms, att_ms=att_ms, ag_ms=ag_ms, e2e_ms=e2e_ms, host_ms=host_ms, clk=clk, info=info, n=n, R=R,
+                hkv_l=hkv_l, tokens_per_step=tokens_per_step, kv_tokens=kv_tokens, alg_bytes=alg_bytes,
+                h2d=n * (hq_l + 2 * hkv_l) * D * 2 + n * 4, d2h=n * hq_l * D * 2, store=st)
 
+
+def c3_prefill(dev, pk, iters=20):
+    """configs[2]: masked prefill over the 16K nested stream; FLOPs count visible pairs only."""
+    import torch
+    import paper_2506_09991_b200 as mv
+    from tools.workloads import nested_16k
+    toks = nested_16k()
+    n = len(toks)
+    g = torch.Generator(device=dev).manual_seed(0)
+    rnd = lambda *s: (torch.rand(*s, generator=g, device=dev) * 2 - 1).to(torch.bfloat16)  # noqa: E731
+    q, k, v = rnd(n, HQ, D), rnd(n, HKV, D), rnd(n, HKV, D)
+    spec = mv.dag.build_visibility(toks)
+    _, _, vis = mv.dag.tile_map(spec, 128)
+    pairs = int(vis.item())
+    out = torch.empty_like(q)
+    ws = torch.empty(mv.lib.mv_prefill_workspace_size(n, HQ, HKV), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > L2: every iteration starts cold
+    for _ in range(3):
+        mv.attention.prefill(q, k, v, spec.positions, spec.excl, out=out, workspace=ws)
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+    for a, b in evs:
+        flush.zero_()
+        a.record()
+        mv.attention.prefill(q, k, v, spec.positions, spec.excl, out=out, workspace=ws)
+        b.record()
+    torch.cuda.synchronize()
+    ms = float(np.median([a.elapsed_time(b) for a, b in evs]))
+    flops = 4.0 * D * HQ * pairs
+    tf = flops / ms / 1e9
+    # e2e: host (pinned) Q/K/V + tag stream in, host output back, mask built by K1 inside the region
+    hq_, hk_, hv_ = (t.cpu().pin_memory() for t in (q, k, v))
+    hout = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(3):
+        sp = mv.dag.build_visibility(toks)
+        mv.attention.prefill(hq_.to(dev, non_blocking=True), hk_.to(dev, non_blocking=True),
+                             hv_.to(dev, non_blocking=True), sp.positions, sp.excl, out=out, workspace=ws)
+        hout.copy_(out, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / 3
+    return {"workload": "configs[2]: n=16384 nested (outer 4 paths x inner 4 paths) structured stream, 40q/8kv, "
+                        "d128, bf16, K1 mask + RoPE + tile map + tcgen05 attention",
+            "metric": "masked prefill TFLOP/s on visible pairs (4 * 128 * Hq * popcount(mask))",
+            "value": tf, "unit": "TFLOP/s", "ms": ms, "visible_pairs": pairs, "density": pairs / (n * n),
+            "l2": "256 MiB flush before every timed iteration",
+            "e2e": {"value": n / (e2e_ms / 1e3), "unit": "rows/s", "ms": e2e_ms,
+                    "h2d_bytes": (HQ + 2 * HKV) * D * 2 * n + 4 * n, "d2h_bytes": HQ * D * 2 * n},
+            "roofline": {"bound": "tensor", "achieved": tf, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                         "frac": tf / pk["bf16_tflops"], "peak_kind": "burst (kernel timed alone)",
+                         "kernel": "prefill_tc3_kernel (+ rope_qk, tile map)", "traffic": None},
+            "rows_per_s": n / (ms / 1e3), "gpu_launches_per_iter": 5}
+
+
+def c5_stress(dev, pk, rounds=16, B=128, path=64, red=16, prefix=4096, decode_steps=256):
+    """configs[4]: fork 128 / append 64 per branch / ordinal merge / 16 Reduce tokens, x16, then decode.
+    Per-op latency = host wall clock around the call + a device sync (what an engine waits)."""
+    import torch
+    import paper_2506_09991_b200 as mv
+    total = prefix + rounds * (B * path + red)
+    pages = total // 16 + rounds * B * 2 + decode_steps // 16 + 4096
+    st = mv.kv.PagedStore(num_pages=pages, layers=1, kv_heads=HKV, table_entries=1 << 23)
+    g = torch.Generator(device=dev).manual_seed(5)
+    rnd = lambda *s: (torch.rand(*s, generator=g, device=dev) * 2 - 1).to(torch.bfloat16)  # noqa: E731
+    pool_k, pool_v = rnd(B * path, HKV, D), rnd(B * path, HKV, D)
+    tok = torch.full((B * path,), 11, dtype=torch.int32, device=dev)
+    t = {"fork": [], "append": [], "merge": [], "release": [], "reduce_append": []}
+    copied = 0
+
+    def timed(key, fn):
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        r = fn()
+        torch.cuda.synchronize()
+        t[key].append((time.perf_counter() - a) * 1e6)
+        return r
+
+    cur = st.create()
+    st.append_many(cur, tok[:1].expand(prefix).contiguous(), torch.arange(prefix, dtype=torch.int32, device=dev), 0,
+                   rnd(prefix, HKV, D), rnd(prefix, HKV, D))
+    L = prefix
+    torch.cuda.synchronize()
+    for r in range(rounds):
+        kids = timed("fork", lambda: st.fork(cur, B))
+        pos_path = torch.arange(L, L + path, dtype=torch.int32, device=dev)
+        for k, h in enumerate(kids):
+            timed("append", lambda: st.append_many(h, tok[:path], pos_path, 0, pool_k[k * path:(k + 1) * path],
+                                                   pool_v[k * path:(k + 1) * path]))
+        m = timed("merge", lambda: st.merge(cur, kids))
+        copied += st.stats().bytes_copied_on_last_op
+        for h in [cur] + kids:
+            timed("release", lambda: st.release(h))
+        L += path
+        pos_red = torch.arange(L, L + red, dtype=torch.int32, device=dev)
+        timed("reduce_append", lambda: st.append_many(m, tok[:red], pos_red, 0, pool_k[:red], pool_v[:red]))
+        L += red
+        cur = m
+    ops_s = sum(sum(v) for v in t.values()) / 1e6  # the ops alone (stats() probes excluded)
+    assert st.length(cur) == total
+    qs, ks, vs = rnd(2, HQ, D), rnd(2, HKV, D), rnd(2, HKV, D)
+    tok1 = torch.tensor([13], dtype=torch.int32, device=dev)
+    poss = [torch.tensor([L + s], dtype=torch.int32, device=dev) for s in range(decode_steps + 3)]
+    for s in range(3):
+        st.append([cur], tok1, poss[s], 0, ks[s % 2:s % 2 + 1], vs[s % 2:s % 2 + 1])
+        mv.attention.decode(st, [cur], qs[s % 2:s % 2 + 1], poss[s])
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record()
+    for s in range(3, decode_steps + 3):
+        st.append([cur], tok1, poss[s], 0, ks[s % 2:s % 2 + 1], vs[s % 2:s % 2 + 1])
+        mv.attention.decode(st, [cur], qs[s % 2:s % 2 + 1], poss[s])
+    ev[1].record()
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / decode_steps
+    ctx = total + 3 + decode_steps / 2
+    gbs = ctx * KV_BYTES_PER_TOKEN / (ms / 1e3) / 1e9
+    return {"workload": "configs[4]: prefix 4096, 16 rounds x {fork 128, 64 tokens per branch, ordinal merge, 16 "
+                        "Reduce tokens}, then 256 decode steps over the merged KV (40q/8kv, d128, bf16)",
+            "metric": "time of the 16 rounds of page-table ops (host clock around each op + a device sync)",
+            "value": ops_s, "unit": "s", "higher_is_better": False,
+            "final_context": total, "kv_bytes_copied_by_fork_and_merge": int(copied),
+            "us_per_op_median": {k: float(np.median(v)) for k, v in t.items()},
+            "decode": {"ms_per_step": ms, "achieved_gbs": gbs, "context_tokens": ctx},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / pk["hbm_gbs"], "kernel": "decode_tc_kernel over the merged 135K context"}}
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    D_ = Device(local if world > 1 else 0)
+    dev = D_.dev
+    if world > 1:
+        torch.distributed.init_process_group(D_.backend)
+    import paper_2506_09991_b200  # noqa: F401  (fails loudly without libmvb200.so: no CPU fallback)
+    pk, pk_src = peaks()
+    heads_mode = args.shard == "heads"
+    r = decode_arm(args, world, rank, local, D_, args.workload, heads_mode)
+    value = r["tokens_per_step"] / (r["ms"] / 1e3)
+    achieved = r["alg_bytes"] / (r["att_ms"] / 1e3) / 1e9
+    traffic, traffic_src = decode_traffic(args.workload, r["R"], args.steps, args.warmup, heads_mode)
+    del r["store"]
+    D_.release_memory()
+    extras = {"c3", "c4", "c5"} if args.extras == "all" else set() if args.extras == "none" else set(
+        args.extras.split(","))
+    sub = {}
+    if "c4" in extras and args.workload != "c4":
+        a4 = argparse.Namespace(**{**vars(args), "steps": min(args.steps, 10), "warmup": min(args.warmup, 3)})
+        r4 = decode_arm(a4, world, rank, local, D_, "c4", False)
+        v4 = r4["tokens_per_step"] / (r4["ms"] / 1e3)
+        a4b = r4["alg_bytes"] / (r4["att_ms"] / 1e3) / 1e9
+        sub["c4_decode"] = {
+            "workload": "configs[3]: 64 requests x 32 branches sharded by request over the GPUs, 40q/8kv, d128, "
+                        "bf16, 16K shared prefix + 32 x 512 branch tokens (32K unique per request), KV page 16",
+            "value": v4, "unit": "tokens/s", "value_per_gpu": v4 / world, "ms_per_step": r4["ms"],
+            "steps": a4.steps, "warmup": a4.warmup, "scaling": "strong",
+            "e2e": {"value": r4["tokens_per_step"] / (r4["e2e_ms"] / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": r4["h2d"], "d2h_bytes_per_step": r4["d2h"]},
+            "roofline": {"bound": "hbm", "achieved": a4b, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": a4b / pk["hbm_gbs"], "alg_bytes_per_launch": r4["alg_bytes"],
+                         "launch_ms": r4["att_ms"], "kernel": "decode_tc_kernel (+ rope_q_tile, combine)"},
+            "host_enqueue_ms_per_step": r4["host_ms"], "plan": r4["info"]}
+        del r4["store"]
+        D_.release_memory()
+    if rank == 0 and world == 1:
+        if "c3" in extras:
+            sub["c3_prefill"] = c3_prefill(dev, pk)
+        if "c5" in extras:
+            sub["c5_stress"] = c5_stress(dev, pk)
     if rank == 0:
-        cpu = cpu_baseline(args.cpu_seconds) if world == 1 and args.workload == "c2" else None
-        if args.workload == "c4":
-            wl_text = ("configs[3]: 64 requests x 32 branches sharded by request over the GPUs, 40q/8kv heads, "
-                       "d128, bf16, 16K shared prefix + 32 x 512 branch tokens (32K unique per request, +1 per "
-                       "branch per step), KV page 16")
-        else:
-            wl_text = ("configs[1] x R requests per GPU: 40q/8kv heads, d128, bf16, 4K shared Map prefix, 8 "
-                       "branches x 1K tokens (+1 per step), KV page 16")
+        cpu = c2_cpu_reference(seconds=args.cpu_seconds) if world == 1 and ref_binary() else None
+        if world == 1:
+            port = c2_cpu_port(min(args.cpu_seconds, 5.0))
+            if cpu is None:
+                cpu = port
+            else:
+                cpu["same_work_port"] = port
+            if "c3_prefill" in sub:
+                from tools.workloads import nested_16k
+                sub["c3_prefill"]["cpu_baseline"] = c3_cpu_port(nested_16k())
+            if "c4_decode" in sub:
+                sub["c4_decode"]["cpu_baseline"] = c4_cpu_port()
+            if "c5_stress" in sub:
+                sub["c5_stress"]["cpu_baseline"] = c5_cpu_reference(min(args.cpu_seconds, 20.0))
         line = {
-            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "value_per_gpu": value / world,
+            "value_is": "whole-job aggregate over n_gpus (bench contract); value_per_gpu = value / n_gpus",
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True,
             "scaling": "strong" if (args.workload == "c4" or heads_mode) else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": wl_text,
-                       "requests_per_gpu": R, "branches_per_gpu": n, "l2": "inputs 0.8+ GB > L2 (no flush)",
-                       "mean_kv_tokens_per_step": kv_tokens, "host_enqueue_ms_per_step": host_ms,
+            "config": {"workload": C2_TEXT if args.workload == "c2" else "configs[3] (see c4_decode)",
+                       "requests_per_gpu": r["R"], "branches_per_gpu": r["n"], "l2": "inputs 0.8+ GB > L2 (no flush)",
+                       "mean_kv_tokens_per_step": r["kv_tokens"], "host_enqueue_ms_per_step": r["host_ms"],
                        "parallelism": (f"kv-head groups x{world} + NCCL all-gather of outputs" if heads_mode
                                        else f"requests x{world}, no collective"),
-                       "kv_heads_per_gpu": hkv_l, "allgather_ms_per_step": ag_ms if heads_mode else None,
+                       "kv_heads_per_gpu": r["hkv_l"], "allgather_ms_per_step": r["ag_ms"] if heads_mode else None,
                        "step": "append 1 token K/V per branch (RoPE fused) + cascade decode attention"},
-            "e2e": {"value": tokens_per_step / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "decode_tc_kernel (+ rope_q_tile_kernel, combine_kernel)",
-                         "alg_bytes_per_launch": alg_bytes,
-                         "launch_ms": att_ms, "frac_of_8TBs": achieved / 8000.0},
+            "e2e": {"value": r["tokens_per_step"] / (r["e2e_ms"] / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": pk_src, "kernel": "decode_tc_kernel (+ rope_q_tile_kernel, combine_kernel)",
+                         "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["att_ms"],
+                         "frac_of_8TBs": achieved / 8000.0},
             "gpu_launches": 4 * args.steps,  # per step: k_append_one, rope_q_tile, decode_tc, combine
-            "clocks": clk,
-            "plan": info,
+            "clocks": r["clk"],
+            "plan": r["info"],
         }
         if cpu:
             line["cpu_baseline"] = cpu
+        line.update(sub)
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.destroy_process_group()
+        torch.distributed.destroy_process_group()
 
 
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
+    run_ours(args)
 
 
 if __name__ == "__main__":

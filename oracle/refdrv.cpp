@@ -535,7 +535,10 @@ int mode_forced_bench(int prompt_words, int path_words, int reps) {
 // RadixStore resolution is read-only and ToyModel::step is const).
 // step() also runs the QKV/O projections and the MLP, which are not part of the attention path,
 // so each sample also times step() with an empty context and reports the difference.
-int mode_decode_bench(int threads, double seconds) {
+// threads lanes decode in parallel; with steps >= 0 every thread runs exactly warmup + steps
+// branch-token decodes (a bench "step" = one token per thread) and only the last `steps` are timed,
+// else each runs for `seconds`.
+int mode_decode_bench(int threads, double seconds, int steps = -1, int warmup = 0) {
   toy::ToyModelConfig cfg;
   cfg.layers = 1;
   cfg.heads = 40;
@@ -576,7 +579,11 @@ int mode_decode_bench(int threads, double seconds) {
     pool.emplace_back([&, t] {
       const auto& h = br[t % nb];
       const int pos = static_cast<int>(prefix + blen);
-      while (std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count() < seconds || reps[t] == 0) {
+      for (int it = 0;; ++it) {
+        if (steps >= 0 ? it >= warmup + steps
+                       : (std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count() >= seconds &&
+                          reps[t] > 0))
+          break;
         auto a = std::chrono::steady_clock::now();
         auto ctx = store.resolve_payloads(h);
         auto out = model.step(std::span<const double>(reinterpret_cast<const double*>(ctx.data()), ctx.size() / sizeof(double)),
@@ -584,6 +591,7 @@ int mode_decode_bench(int threads, double seconds) {
         auto b = std::chrono::steady_clock::now();
         auto out0 = model.step(std::span<const double>(), 0, 13, pos);
         auto c = std::chrono::steady_clock::now();
+        if (steps >= 0 && it < warmup) continue;
         t_full[t] += std::chrono::duration<double>(b - a).count();
         t_empty[t] += std::chrono::duration<double>(c - b).count();
         reps[t] += 1;
@@ -605,7 +613,10 @@ int mode_decode_bench(int threads, double seconds) {
   return 0;
 }
 
-int mode_c5(int rounds, std::size_t rec) {
+// C5 op log on the reference RadixStore.  Stops after the round in which `budget_s` seconds have
+// elapsed (its bookkeeping grows quadratically with the rounds) and prints the
+// per-round op times so the caller can extrapolate the remaining rounds.
+int mode_c5(int rounds, std::size_t rec, double budget_s = 1e30) {
   using clk = std::chrono::steady_clock;
   kv::RadixStore store(rec, 1u << 20);
   std::vector<std::byte> zeros(rec * 4096);
@@ -619,8 +630,11 @@ int mode_c5(int rounds, std::size_t rec) {
   auto cur = store.extend(root, ids(4096, 0), std::span<const std::byte>(zeros.data(), rec * 4096));
   store.release(root);
   double t_fork = 0, t_ext = 0, t_merge = 0, t_rel = 0, t_red = 0;
-  int n_ext = 0, n_rel = 0;
+  int n_ext = 0, n_rel = 0, done = 0;
+  std::vector<double> round_us;
+  const auto t_start = clk::now();
   for (int r = 0; r < rounds; ++r) {
+    const auto r0 = clk::now();
     auto a = clk::now();
     auto kids = store.fork(cur, 128);
     auto b = clk::now();
@@ -647,10 +661,18 @@ int mode_c5(int rounds, std::size_t rec) {
     store.release(m);
     t_red += us(g, clk::now());
     cur = nm;
+    round_us.push_back(us(r0, clk::now()));
+    ++done;
+    if (std::chrono::duration<double>(clk::now() - t_start).count() > budget_s) break;
   }
+  rounds = done;
+  std::string per_round = "[";
+  for (std::size_t i = 0; i < round_us.size(); ++i) per_round += (i ? "," : "") + std::to_string(round_us[i]);
+  per_round += "]";
   std::printf("{\"kind\":\"c5\",\"rounds\":%d,\"final_len\":%zu,\"fork128_us\":%.3f,\"extend64_us\":%.3f,"
-              "\"merge128_us\":%.3f,\"release_us\":%.3f,\"reduce_extend16_us\":%.3f}\n",
-              rounds, cur.length, t_fork / rounds, t_ext / n_ext, t_merge / rounds, t_rel / n_rel, t_red / rounds);
+              "\"merge128_us\":%.3f,\"release_us\":%.3f,\"reduce_extend16_us\":%.3f,\"round_us\":%s}\n",
+              rounds, cur.length, t_fork / rounds, t_ext / n_ext, t_merge / rounds, t_rel / n_rel, t_red / rounds,
+              per_round.c_str());
   store.release(cur);
   return 0;
 }
@@ -668,7 +690,11 @@ int main(int argc, char** argv) {
     return mode_kv(std::stoull(argv[2]), std::stoi(argv[3]), static_cast<std::size_t>(std::stoul(argv[4])));
   if (mode == "toy") return mode_toy();
   if (mode == "forced" && argc >= 5) return mode_forced_bench(std::stoi(argv[2]), std::stoi(argv[3]), std::stoi(argv[4]));
+  if (mode == "decode" && argc >= 6)
+    return mode_decode_bench(std::stoi(argv[2]), std::stod(argv[3]), std::stoi(argv[4]), std::stoi(argv[5]));
   if (mode == "decode" && argc >= 4) return mode_decode_bench(std::stoi(argv[2]), std::stod(argv[3]));
+  if (mode == "c5" && argc >= 5)
+    return mode_c5(std::stoi(argv[2]), static_cast<std::size_t>(std::stoul(argv[3])), std::stod(argv[4]));
   if (mode == "c5" && argc >= 4) return mode_c5(std::stoi(argv[2]), static_cast<std::size_t>(std::stoul(argv[3])));
   std::fprintf(stderr, "bad arguments\n");
   return 1;

@@ -7,7 +7,7 @@ import torch
 
 import oracle
 from mvtest import bf16_to_f64, sym_bf16
-from test_visibility_gpu import nested_16k
+from tools.workloads import nested_16k
 
 pytestmark = pytest.mark.gpu
 TOL = 2e-3

@@ -15,7 +15,7 @@ sys.path.insert(0, os.path.join(REPO, "tests"))
 
 def main(iters=10):
     import paper_2506_09991_b200 as mv
-    from test_visibility_gpu import nested_16k
+    from tools.workloads import nested_16k
     toks = nested_16k()
     n, hq, hkv = len(toks), 40, 8
     g = torch.Generator(device="cuda").manual_seed(0)

@@ -9,7 +9,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, REPO)
 sys.path.insert(0, os.path.join(REPO, "tests"))
 import paper_2506_09991_b200 as mv  # noqa: E402
-from test_visibility_gpu import nested_16k  # noqa: E402
+from tools.workloads import nested_16k  # noqa: E402
 
 toks = nested_16k()
 t = torch.tensor(toks, dtype=torch.int32, device="cuda")
