@@ -50,6 +50,8 @@ def lib():
         L.mvo_attn_decode.argtypes = [P, P, P, i64, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int]
         L.mvo_attn_prefill.argtypes = [P, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P, i64, P,
                                        ctypes.c_int]
+        L.mvo_attn_prefill_mask.argtypes = [P, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, i64, P, i64, P,
+                                            ctypes.c_int]
         L.mvo_toy_new.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, u64, f64, f64]
         L.mvo_toy_new.restype = P
         L.mvo_toy_free.argtypes = [P]
@@ -139,6 +141,24 @@ def attn_prefill(q_rows, K, V, excl, rows, nthreads: int | None = None) -> np.nd
     out = np.zeros((len(r), hq, dh), np.float64)
     lib().mvo_attn_prefill(_p(q), _p(K), _p(V), hq, K.shape[1], dh, _p(ex), ex.shape[1], _p(r), len(r), _p(out),
                            nthreads or threads())
+    return out
+
+
+def attn_prefill_tokens(q_rows, K, V, tokens, rows, nthreads: int | None = None) -> np.ndarray:
+    """The prefill oracle with the mask built from the tag stream by the oracle's own build_mask restatement
+    (segment ancestry, dag.cpp:227-263; no interval form): independent of the device K1 builder."""
+    q = np.ascontiguousarray(q_rows, np.float64)
+    K = np.ascontiguousarray(K, np.float64)
+    V = np.ascontiguousarray(V, np.float64)
+    r = np.ascontiguousarray(rows, np.int32)
+    n = len(tokens)
+    bits = np.concatenate([np.unpackbits(mask_packed(tokens, int(i), int(i) + 1))[:n] for i in r]) if len(r) else \
+        np.zeros(0, np.uint8)
+    packed = np.ascontiguousarray(np.packbits(bits))
+    _, hq, dh = q.shape
+    out = np.zeros((len(r), hq, dh), np.float64)
+    lib().mvo_attn_prefill_mask(_p(q), _p(K), _p(V), hq, K.shape[1], dh, _p(packed), n, _p(r), len(r), _p(out),
+                                nthreads or threads())
     return out
 
 

@@ -13,6 +13,21 @@ GOLDEN = REPO / "tests" / "golden"
 
 
 
+def pytest_terminal_summary(terminalreporter):
+    """Numeric parity margins (max-abs error vs the test's tolerance) of the GPU tests that ran."""
+    try:
+        from mvtest import MARGINS
+    except Exception:
+        return
+    if not MARGINS:
+        return
+    terminalreporter.section("parity margins (max-abs error / tolerance)")
+    worst = max(MARGINS, key=lambda m: m[1] / m[2])
+    for name, err, tol in MARGINS:
+        terminalreporter.write_line(f"{err:.3e} / {tol:.0e}  ({err / tol:5.1%})  {name}")
+    terminalreporter.write_line(f"worst: {worst[0]} at {worst[1] / worst[2]:.1%} of its tolerance")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); runs through the C-ABI library")
 

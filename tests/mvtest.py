@@ -16,3 +16,11 @@ def sym_bf16(seed: int, shape) -> torch.Tensor:
 
 def bf16_to_f64(t: torch.Tensor) -> np.ndarray:
     return t.float().cpu().numpy().astype(np.float64)
+
+
+# max-abs error / tolerance of every numeric parity check, printed in pytest's terminal summary
+MARGINS: list[tuple[str, float, float]] = []
+
+
+def record_margin(name: str, err: float, tol: float) -> None:
+    MARGINS.append((name, float(err), float(tol)))

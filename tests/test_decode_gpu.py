@@ -6,7 +6,7 @@ import pytest
 import torch
 
 import oracle
-from mvtest import bf16_to_f64, sym_bf16
+from mvtest import bf16_to_f64, record_margin, sym_bf16
 
 pytestmark = pytest.mark.gpu
 TOL = 2e-3
@@ -87,6 +87,7 @@ def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1):
     ctx_full = [c + [base + i] for i, c in enumerate(ctx)]
     ref = oracle.attn_decode(qr, Kr, V, ctx_full)
     err = np.abs(out.float().cpu().numpy() - ref).max()
+    record_margin(f"decode {len(handles)} handles hq={hq}/{hkv}", err, TOL)
     # the bf16 output path: identical arithmetic plus the bf16 store rounding (<= 2^-9 |o|)
     out16 = mv.attention.decode(st, handles, q.cuda(), pos.cuda()).float().cpu().numpy()
     assert (np.abs(out16 - ref) <= TOL + np.abs(ref) * 2.0 ** -8).all()

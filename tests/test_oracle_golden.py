@@ -143,3 +143,22 @@ def test_kv_log_flat_mirror(log):
             assert m.seq[rv["id"]] == rv["tokens"]
     for rv in rows[-1]["final"]:
         assert m.seq[rv["id"]] == rv["tokens"]
+
+
+def test_prefill_oracle_from_tokens_matches_dense_rule():
+    """oracle.attn_prefill_tokens (mask from the oracle's build_mask rows, no intervals) equals a direct
+    numpy evaluation of ToyModel::forward's attention (toy_model.cpp:183-196) over the dense mask."""
+    import oracle
+    t1 = [10, 0, 2, 4, 11, 12, 5, 4, 13, 14, 5, 3, 6, 11, 15, 16, 7, 6, 13, 17, 18, 19, 7, 8, 20, 9, 1, 21]
+    n = len(t1)
+    rng = np.random.default_rng(0)
+    q, K, V = rng.uniform(-1, 1, (n, 4, 16)), rng.uniform(-1, 1, (n, 2, 16)), rng.uniform(-1, 1, (n, 2, 16))
+    rows = np.array([0, 5, 12, 16, 17, 22, 23, 27])
+    out = oracle.attn_prefill_tokens(q[rows], K, V, t1, rows)
+    M = oracle.mask_dense(t1)
+    for r, i in enumerate(rows):
+        ctx = [j for j in range(i) if M[i, j]] + [i]
+        for h in range(4):
+            s = np.array([q[i, h] @ K[j, h // 2] for j in ctx]) / 4.0
+            p = np.exp(s - s.max())
+            assert np.abs(out[r, h] - (p[:, None] * V[ctx, h // 2]).sum(0) / p.sum()).max() < 1e-12

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 import oracle
-from mvtest import bf16_to_f64, sym_bf16
+from mvtest import bf16_to_f64, record_margin, sym_bf16
 from tools.workloads import nested_16k
 
 pytestmark = pytest.mark.gpu
@@ -20,6 +20,9 @@ def mv():
 
 
 def run_prefill(mv, tokens, hq, hkv, rows=None, seed=3):
+    """Device prefill (K1 intervals -> K3) against the oracle built from the tag stream alone: the oracle's
+    own positions (dag.cpp:203-222 restated) and dense build_mask rows (dag.cpp:227-263), so a K1 bug cannot
+    be certified by this test."""
     n = len(tokens)
     spec = mv.dag.build_visibility(tokens)
     q = sym_bf16(seed * 10 + 1, (n, hq, 128))
@@ -27,13 +30,16 @@ def run_prefill(mv, tokens, hq, hkv, rows=None, seed=3):
     v = sym_bf16(seed * 10 + 3, (n, hkv, 128))
     out = mv.attention.prefill(q.cuda(), k.cuda(), v.cuda(), spec.positions, spec.excl, out_dtype=torch.float32)
     torch.cuda.synchronize()
-    pos = spec.positions.cpu().numpy()
+    err_code, pos, _, _ = oracle.build_dag(tokens)
+    assert err_code == 0
     rows = np.arange(n) if rows is None else np.asarray(rows)
     Kr = oracle.rope(bf16_to_f64(k), pos)
     qr = oracle.rope(bf16_to_f64(q)[rows], pos[rows])
-    ref = oracle.attn_prefill(qr, Kr, bf16_to_f64(v), spec.excl.cpu().numpy(), rows)
+    ref = oracle.attn_prefill_tokens(qr, Kr, bf16_to_f64(v), tokens, rows)
     got = out.cpu().numpy()[rows]
-    return float(np.abs(got - ref).max()), spec
+    err = float(np.abs(got - ref).max())
+    record_margin(f"prefill n={n} hq={hq}/{hkv} rows={len(rows)}", err, TOL)
+    return err, spec
 
 
 def test_t1_all_rows(mv, dag_golden):

@@ -13,6 +13,7 @@ import pytest
 import torch
 
 import oracle
+from mvtest import record_margin
 from paper_2506_09991_b200.host.tokenize import tokenize
 
 pytestmark = pytest.mark.gpu
@@ -37,6 +38,7 @@ def gpu_toy(mv, c):
 def check_logits(got, want, what):
     got = got.cpu().numpy().reshape(want.shape)
     err = np.abs(got - want).max()
+    record_margin(f"toy logits {what}", err, LOGIT_TOL)
     agree = (got.argmax(-1) == want.argmax(-1)).mean()
     assert err < LOGIT_TOL, (what, err)
     assert agree == 1.0, (what, agree)
