@@ -113,7 +113,7 @@ typedef struct mv_kv_store mv_kv_store;
 typedef struct {
   int32_t num_pages;      /* page pool size; tokens capacity = 16 * num_pages (CapacityExceeded beyond) */
   int32_t record_bytes;   /* opaque per-token payload record (RadixStore payload_record_size); 0 = none */
-  int32_t layers;         /* attention KV plane: bf16 K and V, [layer][page][kv_head][16][head_dim] */
+  int32_t layers;         /* attention KV planes: bf16 K and V per layer, head-major [kv_head][page][16][head_dim] */
   int32_t kv_heads;       /*   (0 = no attention plane) */
   int32_t head_dim;       /*   must be 128 when kv_heads > 0 */
   int64_t table_entries;  /* device page-table arena capacity in entries (0 = 4 * num_pages + 65536) */

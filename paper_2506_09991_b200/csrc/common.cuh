@@ -56,21 +56,22 @@ __host__ __device__ inline PageRef make_ref(int page, int begin, int count) {
 }
 
 // ---------------------------------------------------------------------------
-// KV page layout: [page][kv_head][4 KiB block]; the block holds token t, dim d at
-//   atom (t >> 3, d >> 6) of 1 KiB = 8 token rows x 128 B, atoms ordered [t >> 3][d >> 6],
-//   16-byte chunk c of row r stored at chunk c ^ r   (SWIZZLE_128B within each atom).
-// Consecutive page-head blocks of one KV head therefore form canonical UMMA operands with
-// one 1-D bulk copy per page: K-major for Q.K^T (N = tokens: 8-row groups 2048 B apart, dims
-// 64..127 at +1024 B) and MN-major for P.V (N = dims: atoms 1024 B apart, K = tokens: 8-row
-// groups 2048 B apart) — no shared-memory re-layout.
+// KV plane layout (one plane per layer for K, one for V): head-major [kv_head][page][4 KiB block];
+//   the block holds token t, dim d at atom (t >> 3, d >> 6) of 1 KiB = 8 token rows x 128 B, atoms
+//   ordered [t >> 3][d >> 6], 16-byte chunk c of row r stored at chunk c ^ r (SWIZZLE_128B per atom).
+// Consecutive page-head blocks of one KV head therefore form canonical UMMA operands with one 1-D bulk
+// copy per page: K-major for Q.K^T (N = tokens: 8-row groups 2048 B apart, dims 64..127 at +1024 B) and
+// MN-major for P.V (N = dims: atoms 1024 B apart, K = tokens: 8-row groups 2048 B apart) — no
+// shared-memory re-layout.  Head-major: pages p..p+3 of one head are 16 KiB of contiguous HBM, so a
+// table block of consecutive page ids (bulk allocations hand out ascending runs) is ONE bulk copy.
 // ---------------------------------------------------------------------------
 __host__ __device__ inline int swz_chunk(int token, int chunk) { return chunk ^ (token & 7); }
 // element offset of 16-byte chunk c (dims 8c..8c+7) of token slot t inside a page-head block
 __host__ __device__ inline int kv_chunk_offset(int t, int c) {
   return ((((t >> 3) * 2 + (c >> 3)) * 8 + (t & 7)) * 64) + ((((c & 7) ^ (t & 7))) << 3);
 }
-__host__ __device__ inline size_t kv_page_head_offset(int64_t page, int head, int kv_heads) {
-  return ((size_t)page * kv_heads + head) * (kPageTokens * kHeadDim);
+__host__ __device__ inline size_t kv_page_head_offset(int64_t page, int head, int64_t num_pages) {
+  return ((size_t)head * (size_t)num_pages + (size_t)page) * (kPageTokens * kHeadDim);
 }
 
 // ---------------------------------------------------------------------------
@@ -194,6 +195,16 @@ __device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// P for the P.V MMA: rounds a probability pair to bf16x2 and accumulates the ROUNDED values into
+// the row sum, so numerator (sum of rounded p * v) and denominator use the same weights: the result
+// is exact attention under score perturbations of at most 2^-9 (the unrounded sum adds the rounding
+// bias of every weight on top of that).
+__device__ __forceinline__ uint32_t pack_bf16_sum(float2 pp, float2& acc) {
+  const uint32_t u = pack_bf16(pp.x, pp.y);
+  acc = __fadd2_rn(acc, make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u)));
+  return u;
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {

@@ -126,6 +126,7 @@ struct DecodeParams {
   void* out;
   int out_f32;
   int kv_heads, q_heads, gqa, R;
+  int64_t num_pages;             // page pool size (head stride of the planes)
   float scale_log2;
 };
 
@@ -256,8 +257,7 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
           const float2 pp = (kDecPoly > 0 && k % kDecPoly == kDecPoly - 1)
                                 ? poly_exp2x2(xy)
                                 : make_float2(fast_exp2(xy.x), fast_exp2(xy.y));
-          la = __fadd2_rn(la, pp);
-          pk[k] = pack_bf16(pp.x, pp.y);
+          pk[k] = pack_bf16_sum(pp, la);
         }
         return la.x + la.y;
       };
@@ -437,15 +437,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
     }
   } else if (warp == kWarpTma) {
     // ---------------- TMA: keeps the K and V rings full across work units ----------------
-    // Two independent streams on two lanes (their issue latencies overlap): lane 0 copies K
-    // blocks, lane 1 V blocks (one 4 KiB bulk copy per page-head).  K slots free after Q.K^T,
-    // V slots after P.V.  L2 prefetching is the stager's job.
+    // K and V streams (lanes 0-7 K, 8-15 V).  K slots free after Q.K^T, V slots after P.V.
     if (lane < 4 * kTmaLanesPerBlkGroup * 2) {
-      // K and V streams, kTmaGroups 4-lane groups each; group j of a stream copies block g + j of
-      // every kTmaGroups-block step, lane p of a group page p (tools/microbench/mb_gather.cu:
-      // random 4 KiB bulk copies need several issuing lanes to approach the HBM bandwidth)
+      // kTmaGroups 4-lane groups per stream; group j copies block g + j of every kTmaGroups-block
+      // step.  A block whose 4 page ids are consecutive is 16 KiB of contiguous HBM in the
+      // head-major plane (common.cuh) and goes as ONE bulk copy; otherwise lane p copies page p
+      // (tools/microbench/mb_gather.cu: random 4 KiB copies need several issuing lanes to approach
+      // the HBM bandwidth, 16 KiB copies reach it from one)
       constexpr int kTmaGroups = kTmaLanesPerBlkGroup;
-      const size_t page_stride = (size_t)P.kv_heads * kPageTokens * kHeadDim;
+      const size_t head_stride = (size_t)P.num_pages * kPageTokens * kHeadDim;
       const bool is_k = lane < 4 * kTmaGroups;
       const int sl_lane = lane % (4 * kTmaGroups);
       const int sub = sl_lane & 3, grp = sl_lane >> 2;
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         if (!si->valid) break;
         const int n_ent = si->n_entries;
         const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
-        const size_t head_off = (size_t)si->kvh * kPageTokens * kHeadDim;
+        const __nv_bfloat16* hplane = plane + (size_t)si->kvh * head_stride;
         const PageRef* se = s_ent0 + buf * kMaxEntries;
         for (int blk = grp; blk < nblk; blk += kTmaGroups) {
           const int g = g0 + blk;
@@ -471,11 +471,16 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           const int sl = g % nsl, np = min(kBlkPages, n_ent - e0);
           if (g >= nsl) mbar_wait(&eb[sl], ((g / nsl) - 1) & 1);
           uint8_t* dst = rb + sl * kSlotBytes;
+          const int pg = sub < np ? se[e0 + sub].page : -1;
+          const int p0 = __shfl_sync(gmask, pg, lane & ~3);
+          const bool run = __all_sync(gmask, np == kBlkPages && pg == p0 + sub);
           if (sub == 0) mbar_arrive_expect_tx(&fb[sl], (uint32_t)np * kPageBytes);
           __syncwarp(gmask);  // the expected bytes are registered before any copy can complete
-          if (sub < np)
-            bulk_g2s(dst + sub * kPageBytes, plane + (size_t)se[e0 + sub].page * page_stride + head_off, kPageBytes,
-                     &fb[sl]);
+          if (run) {
+            if (sub == 0) bulk_g2s(dst, hplane + (size_t)p0 * (kPageTokens * kHeadDim), kSlotBytes, &fb[sl]);
+          } else if (sub < np) {
+            bulk_g2s(dst + sub * kPageBytes, hplane + (size_t)pg * (kPageTokens * kHeadDim), kPageBytes, &fb[sl]);
+          }
         }
         g0 += nblk;
         // every lane of the stream is done with the unit's entries before the slot is released
@@ -1139,6 +1144,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   P.out = d_out;
   P.out_f32 = out_dtype == 1;
   P.kv_heads = cfg.kv_heads;
+  P.num_pages = cfg.num_pages;
   P.q_heads = q_heads;
   P.gqa = gqa;
   P.R = R;

@@ -191,12 +191,13 @@ __device__ __forceinline__ void rope8(uint4& v, int pos, int chunk, const double
 }
 
 __device__ __forceinline__ void write_kv_token(__nv_bfloat16* kp, __nv_bfloat16* vp, int64_t page, int slot,
-                                               int kv_heads, const __nv_bfloat16* k, const __nv_bfloat16* v,
-                                               int pos, const double* inv, int lane, int nlanes, int first = 0) {
+                                               int kv_heads, int64_t npages, const __nv_bfloat16* k,
+                                               const __nv_bfloat16* v, int pos, const double* inv, int lane,
+                                               int nlanes, int first = 0) {
   // kv_heads * 16 chunks of 8 dims (from chunk `first`); K rotated, V verbatim; stored chunk-swizzled.
   for (int j = first + lane; j < kv_heads * 16; j += nlanes) {
     int h = j >> 4, c = j & 15;
-    size_t dst = kv_page_head_offset(page, h, kv_heads) + (size_t)kv_chunk_offset(slot, c);
+    size_t dst = kv_page_head_offset(page, h, npages) + (size_t)kv_chunk_offset(slot, c);
     uint4 kk = *reinterpret_cast<const uint4*>(k + (size_t)h * kHeadDim + c * 8);
     rope8(kk, pos, c, inv);
     *reinterpret_cast<uint4*>(kp + dst) = kk;
@@ -209,7 +210,7 @@ __global__ void k_append_data(AppendPlan pl, const int32_t* __restrict__ page_ou
                               const uint8_t* __restrict__ rec_in, uint8_t* __restrict__ records, int rec_bytes,
                               const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                               const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads,
-                              const RopeTable rt) {
+                              int64_t npages, const RopeTable rt) {
   __shared__ double s_inv[kHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   // one warp per token
@@ -233,7 +234,7 @@ __global__ void k_append_data(AppendPlan pl, const int32_t* __restrict__ page_ou
   if (rec_in && rec_bytes > 0)
     for (int b = lane; b < rec_bytes; b += 32) records[gslot * rec_bytes + b] = rec_in[(int64_t)t * rec_bytes + b];
   if (k && v)
-    write_kv_token(kp, vp, page, slot, kv_heads, k + (size_t)t * kv_heads * kHeadDim,
+    write_kv_token(kp, vp, page, slot, kv_heads, npages, k + (size_t)t * kv_heads * kHeadDim,
                    v + (size_t)t * kv_heads * kHeadDim, pos ? pos[t] : 0, inv, lane, 32);
 }
 
@@ -255,7 +256,8 @@ __device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef
                                                 int32_t* __restrict__ err, const int32_t* __restrict__ pos,
                                                 const __nv_bfloat16* __restrict__ k,
                                                 const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp,
-                                                __nv_bfloat16* vp, int kv_heads, const double* inv) {
+                                                __nv_bfloat16* vp, int kv_heads, int64_t npages,
+                                                const double* inv) {
   const int lane = threadIdx.x & 31;
   // programmatic launch: the inputs (k, v, positions, tokens) may be produced by the kernel
   // this one overlaps (e.g. the caller's projection GEMM), so nothing is read before this wait;
@@ -308,13 +310,13 @@ __device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef
   for (int u = 0; u < 4; ++u) {
     const int j = lane + 32 * u;
     if (j < nch) {
-      const size_t dst = kv_page_head_offset(page, j >> 4, kv_heads) + (size_t)kv_chunk_offset(slot, j & 15);
+      const size_t dst = kv_page_head_offset(page, j >> 4, npages) + (size_t)kv_chunk_offset(slot, j & 15);
       *reinterpret_cast<uint4*>(kp + dst) = kk[u];
       *reinterpret_cast<uint4*>(vp + dst) = vv[u];
     }
   }
   if (nch > 128)  // more than 8 kv heads: the remaining chunks after the destination is known
-    write_kv_token(kp, vp, page, slot, kv_heads, kt, vt, p, inv, lane, 32, 128);
+    write_kv_token(kp, vp, page, slot, kv_heads, npages, kt, vt, p, inv, lane, 32, 128);
 }
 
 __global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ cum, const TokDesc* __restrict__ d,
@@ -322,13 +324,13 @@ __global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ 
                              int32_t* __restrict__ refcnt, int32_t* __restrict__ free_stack,
                              int32_t* __restrict__ free_top, int32_t* __restrict__ err, const int32_t* __restrict__ pos,
                              const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
-                             __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, const RopeTable rt) {
+                             __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, int64_t npages, const RopeTable rt) {
   __shared__ double s_inv[kHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
   append_one_warp((threadIdx.x & 31) == 0 ? d[i] : TokDesc{0, 0, 0}, i, arena, cum, tokens, slot_tok, refcnt,
-                  free_stack, free_top, err, pos, k, v, kp, vp, kv_heads, inv);
+                  free_stack, free_top, err, pos, k, v, kp, vp, kv_heads, npages, inv);
 }
 __global__ void k_append_one_inline(PageRef* __restrict__ arena, int32_t* __restrict__ cum, const TokDescInline d,
                                     int n, const int32_t* __restrict__ tokens, int32_t* __restrict__ slot_tok,
@@ -336,7 +338,7 @@ __global__ void k_append_one_inline(PageRef* __restrict__ arena, int32_t* __rest
                                     int32_t* __restrict__ free_top, int32_t* __restrict__ err,
                                     const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                                     const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp,
-                                    int kv_heads, const RopeTable rt) {
+                                    int kv_heads, int64_t npages, const RopeTable rt) {
   // the RoPE pre-pass after this kernel may launch now: it waits (griddepcontrol.wait) for this
   // grid to complete before touching anything, and only then releases decode_tc
   pdl_launch_dependents();
@@ -345,20 +347,20 @@ __global__ void k_append_one_inline(PageRef* __restrict__ arena, int32_t* __rest
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
   append_one_warp(d.d[i], i, arena, cum, tokens, slot_tok, refcnt, free_stack, free_top, err, pos, k, v, kp, vp,
-                  kv_heads, inv);
+                  kv_heads, npages, inv);
 }
 
 // K/V of the last token of each handle (for layers > the one written at append).
 __global__ void k_write_last(const PageRef* __restrict__ arena, const int64_t* __restrict__ idx,
                              const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                              const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads,
-                             const RopeTable rt) {
+                             int64_t npages, const RopeTable rt) {
   __shared__ double s_inv[kHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int i = blockIdx.x;
   PageRef r = arena[idx[i]];
   int slot = ref_begin(r) + ref_count(r) - 1;
-  write_kv_token(kp, vp, r.page, slot, kv_heads, k + (size_t)i * kv_heads * kHeadDim,
+  write_kv_token(kp, vp, r.page, slot, kv_heads, npages, k + (size_t)i * kv_heads * kHeadDim,
                  v + (size_t)i * kv_heads * kHeadDim, pos[i], inv, threadIdx.x, blockDim.x);
 }
 
@@ -367,7 +369,7 @@ __global__ void k_resolve(const PageRef* __restrict__ arena, const int32_t* __re
                           const int32_t* __restrict__ slot_tok, const uint8_t* __restrict__ records, int rec_bytes,
                           int32_t* __restrict__ tok_out, uint8_t* __restrict__ rec_out, uint32_t* __restrict__ slot_out,
                           const __nv_bfloat16* __restrict__ kp, const __nv_bfloat16* __restrict__ vp, int kv_heads,
-                          __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out) {
+                          int64_t npages, __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out) {
   for (int e = blockIdx.x; e < n; e += gridDim.x) {
     PageRef r = arena[off + e];
     int c0 = cum[off + e];
@@ -384,7 +386,7 @@ __global__ void k_resolve(const PageRef* __restrict__ arena, const int32_t* __re
       for (int x = threadIdx.x; x < cnt * kv_heads * 16; x += blockDim.x) {
         int t = x / (kv_heads * 16), h = (x / 16) % kv_heads, c = x % 16;
         int slot = b + t;
-        size_t src = kv_page_head_offset(r.page, h, kv_heads) + (size_t)kv_chunk_offset(slot, c);
+        size_t src = kv_page_head_offset(r.page, h, npages) + (size_t)kv_chunk_offset(slot, c);
         size_t dst = ((size_t)(c0 + t) * kv_heads + h) * kHeadDim + c * 8;
         *reinterpret_cast<uint4*>(k_out + dst) = *reinterpret_cast<const uint4*>(kp + src);
         *reinterpret_cast<uint4*>(v_out + dst) = *reinterpret_cast<const uint4*>(vp + src);
@@ -416,8 +418,10 @@ __global__ void k_count(const uint32_t* __restrict__ bitmap, int64_t words, cons
   atomicAdd(&out[2], c);
 }
 
+// Ascending stack: a bulk pop of m pages (k_append_table takes stack[top - m .. top)) hands out an
+// ascending run of page ids, so a fresh pool stores a bulk append contiguously (16 KiB decode copies).
 __global__ void k_init_free(int32_t* free_stack, int n, int32_t* free_top) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) free_stack[i] = n - 1 - i;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) free_stack[i] = i;
   if (blockIdx.x == 0 && threadIdx.x == 0) *free_top = n;
 }
 
@@ -731,7 +735,7 @@ mv_status PagedStore::extend(uint64_t h, const int32_t* tokens, int64_t n, const
     int64_t threads = n * 32;
     k_append_data<<<(int)((threads + 255) / 256), 256, 0, stream_>>>(
         pl, d_pages, d_pages + new_pages, (const int32_t*)d_tok, d_slot_tok_, (const uint8_t*)d_rec, d_records_,
-        cfg_.record_bytes, nullptr, nullptr, nullptr, nullptr, nullptr, cfg_.kv_heads, rope_);
+        cfg_.record_bytes, nullptr, nullptr, nullptr, nullptr, nullptr, cfg_.kv_heads, cfg_.num_pages, rope_);
     MV_LAUNCH_CHECK();
     for (int64_t t = 0; t < fill; ++t) r.cum.back()++;
     for (int32_t k = 0; k < new_pages; ++k) {
@@ -906,7 +910,7 @@ mv_status PagedStore::resolve(uint64_t h, int32_t* tokens, void* payloads, uint3
   uint8_t* d_rec = pb ? d + tb + sb : nullptr;
   k_resolve<<<std::min(r->n_entries(), 148 * 16), 128, 0, stream_>>>(
       d_arena, d_cum, r->arena_off, r->n_entries(), d_slot_tok_, d_records_, cfg_.record_bytes, d_tok, d_rec, d_slot,
-      nullptr, nullptr, cfg_.kv_heads, nullptr, nullptr);
+      nullptr, nullptr, cfg_.kv_heads, (int64_t)cfg_.num_pages, nullptr, nullptr);
   MV_LAUNCH_CHECK();
   if (tb) MV_CUDA_TRY(cudaMemcpyAsync(tokens, d_tok, tb, cudaMemcpyDeviceToHost, stream_));
   if (sb) MV_CUDA_TRY(cudaMemcpyAsync(slots, d_slot, sb, cudaMemcpyDeviceToHost, stream_));
@@ -973,14 +977,15 @@ mv_status PagedStore::append(const uint64_t* hs, int32_t n, const int32_t* d_tok
     lc.numAttrs = 1;
     MV_CUDA_TRY(cudaLaunchKernelEx(&lc, k_append_one_inline, d_arena, d_cum, inl, n, d_tokens, d_slot_tok_, d_refcnt_,
                                    d_free_, d_free_top_, d_err_, d_pos, (const __nv_bfloat16*)d_k,
-                                   (const __nv_bfloat16*)d_v, kpl, vpl, (int)cfg_.kv_heads, rope_));
+                                   (const __nv_bfloat16*)d_v, kpl, vpl, (int)cfg_.kv_heads, (int64_t)cfg_.num_pages,
+                                   rope_));
   } else {
     void* d_desc;
     if (mv_status st = upload(desc.data(), sizeof(TokDesc) * n, &d_desc, 10)) return st;
     k_append_one<<<(n + 3) / 4, 128, 0, stream_>>>(d_arena, d_cum, (const TokDesc*)d_desc, n, d_tokens, d_slot_tok_,
                                                    d_refcnt_, d_free_, d_free_top_, d_err_, d_pos,
                                                    (const __nv_bfloat16*)d_k, (const __nv_bfloat16*)d_v, kpl, vpl,
-                                                   cfg_.kv_heads, rope_);
+                                                   cfg_.kv_heads, (int64_t)cfg_.num_pages, rope_);
   }
   MV_LAUNCH_CHECK();
   return MV_OK;
@@ -1002,7 +1007,7 @@ mv_status PagedStore::write_last(const uint64_t* hs, int32_t n, const int32_t* d
   if (mv_status st = upload(idx.data(), sizeof(int64_t) * n, &d_idx, 11)) return st;
   k_write_last<<<n, 128, 0, stream_>>>(d_arena, (const int64_t*)d_idx, d_pos, (const __nv_bfloat16*)d_k,
                                        (const __nv_bfloat16*)d_v, k_planes_[layer], v_planes_[layer], cfg_.kv_heads,
-                                       rope_);
+                                       (int64_t)cfg_.num_pages, rope_);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }
@@ -1038,7 +1043,7 @@ mv_status PagedStore::append_many(uint64_t h, int64_t n, const int32_t* d_tokens
   k_append_data<<<(int)((threads + 255) / 256), 256, 0, stream_>>>(
       pl, d_pages, d_pages + new_pages, d_tokens, d_slot_tok_, nullptr, d_records_, cfg_.record_bytes, d_pos,
       (const __nv_bfloat16*)d_k, (const __nv_bfloat16*)d_v, d_k ? k_planes_[layer] : nullptr,
-      d_k ? v_planes_[layer] : nullptr, cfg_.kv_heads, rope_);
+      d_k ? v_planes_[layer] : nullptr, cfg_.kv_heads, (int64_t)cfg_.num_pages, rope_);
   MV_LAUNCH_CHECK();
   r->cum.back() += fill;
   for (int32_t k = 0; k < new_pages; ++k) {
@@ -1060,7 +1065,8 @@ mv_status PagedStore::gather_kv(uint64_t h, int32_t layer, void* d_k, void* d_v)
   if (r->n_entries() == 0) return MV_OK;
   k_resolve<<<std::min(r->n_entries(), 148 * 16), 128, 0, stream_>>>(
       d_arena, d_cum, r->arena_off, r->n_entries(), d_slot_tok_, d_records_, cfg_.record_bytes, nullptr, nullptr,
-      nullptr, k_planes_[layer], v_planes_[layer], cfg_.kv_heads, (__nv_bfloat16*)d_k, (__nv_bfloat16*)d_v);
+      nullptr, k_planes_[layer], v_planes_[layer], cfg_.kv_heads, (int64_t)cfg_.num_pages, (__nv_bfloat16*)d_k,
+      (__nv_bfloat16*)d_v);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }

@@ -439,9 +439,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
             const float2 pp = (kPolyMod3 > 0 && u % kPolyMod3 == kPolyMod3 - 1)
                                   ? poly_exp2x2(xy)  // FMA pipe: relieves the 16/clk/SM MUFU
                                   : make_float2(fast_exp2(xy.x), fast_exp2(xy.y));
-            if (u & 1) lb = __fadd2_rn(lb, pp);
-            else la = __fadd2_rn(la, pp);
-            pk[u] = pack_bf16(pp.x, pp.y);
+            pk[u] = pack_bf16_sum(pp, (u & 1) ? lb : la);
           }
           // P for k tokens [64c, 64c + 64) -> packed columns [32c, 32c + 32) of the S buffer
           tc::tmem_stNu<16>(lane_base + s_col + c * 32 + c16 * 16, pk);
