@@ -79,6 +79,19 @@ MV_API mv_status mv_visibility(const int32_t* d_tokens, const int64_t* h_offsets
                         void* d_workspace, size_t workspace_bytes, mv_stream_t stream);
 
 /*
+ * Teacher-forced training batch (dag::build_training_batch, dag.hpp:124-139, dag.cpp:314-359) for a
+ * batch of tag streams: everything mv_visibility computes (token ids are the input; layout order is
+ * stream order) plus, per token, the next-token target (-1 where the row has none: a path's last
+ * token, unless its block has one path, and the sequence's last token) and the loss mask
+ * (target >= 0 and, unless tag_loss, a non-tag target; BatchOptions::tag_loss, dag.hpp:120-122).
+ *   d_targets int32[n_total]; d_loss_mask uint8[n_total]; same workspace as mv_visibility.
+ */
+MV_API mv_status mv_training_batch(const int32_t* d_tokens, const int64_t* h_offsets, int32_t n_seq, int32_t max_depth,
+                                   int32_t tag_loss, int32_t* d_positions, int32_t* d_excl, int32_t* d_targets,
+                                   uint8_t* d_loss_mask, int32_t* d_status, void* d_workspace, size_t workspace_bytes,
+                                   mv_stream_t stream);
+
+/*
  * Dense legacy dag::Mask (dag.hpp:59-73) from the intervals: rows [row0, row1) of one
  * sequence of length n, MSB-first packed bits, row-major ((row1-row0)*n bits).
  */

@@ -52,6 +52,7 @@ def lib():
                                        ctypes.c_int]
         L.mvo_attn_prefill_mask.argtypes = [P, P, P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, i64, P, i64, P,
                                             ctypes.c_int]
+        L.mvo_batch_targets.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P]
         L.mvo_toy_new.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, u64, f64, f64]
         L.mvo_toy_new.restype = P
         L.mvo_toy_free.argtypes = [P]
@@ -81,6 +82,16 @@ def build_dag(tokens):
     ns = np.zeros(1, np.int32)
     err = lib().mvo_build_dag(_p(t), n, _p(pos), _p(seg), _p(kind), _p(ns))
     return err, pos, seg, kind
+
+
+def batch_targets(tokens, tag_loss: bool = True):
+    """(err, target_ids, loss_mask) of build_training_batch (dag.cpp:326-357), restated over segments."""
+    t = np.ascontiguousarray(tokens, dtype=np.int32)
+    n = len(t)
+    tgt = np.full(max(n, 1), -1, np.int32)
+    loss = np.zeros(max(n, 1), np.uint8)
+    err = lib().mvo_batch_targets(_p(t), n, int(bool(tag_loss)), _p(tgt), _p(loss))
+    return err, tgt[:n], loss[:n]
 
 
 def mask_packed(tokens, row0: int = 0, row1: int | None = None) -> np.ndarray:

@@ -179,17 +179,19 @@ std::string mutate(synth::Rng& rng, const std::string& src, int* which) {
   }
 }
 
-int mode_dag(const std::string& fixdir) {
+// Every trajectory of the dag goldens: fixtures, seeded random trajectories, malformed mutants.
+template <typename F>
+void for_each_dag_case(const std::string& fixdir, F&& emit) {
   for (const char* f : {"t1.txt", "nested.txt", "collective_4path.txt", "selective_2path.txt",
                         "generation_collective.txt", "generation_selective.txt", "sequential.txt"}) {
-    emit_dag_case(std::string("fixture:") + f, read_file(fixdir + "/" + f), true);
+    emit(std::string("fixture:") + f, read_file(fixdir + "/" + f), true);
   }
   for (int seed = 0; seed < 300; ++seed) {
     synth::Rng rng(static_cast<std::uint64_t>(seed));
     synth::TrajectoryParams p;
     p.max_depth = 3;
     p.max_paths = 5;
-    emit_dag_case("random3x5:" + std::to_string(seed), synth::random_trajectory(rng, p), seed < 100);
+    emit("random3x5:" + std::to_string(seed), synth::random_trajectory(rng, p), seed < 100);
   }
   for (int seed = 0; seed < 40; ++seed) {
     synth::Rng rng(static_cast<std::uint64_t>(1000 + seed));
@@ -198,7 +200,7 @@ int mode_dag(const std::string& fixdir) {
     p.max_paths = 6;
     p.max_blocks = 3;
     p.nest_probability = 0.6;
-    emit_dag_case("random4x6:" + std::to_string(seed), synth::random_trajectory(rng, p), false);
+    emit("random4x6:" + std::to_string(seed), synth::random_trajectory(rng, p), false);
   }
   for (int seed = 0; seed < 200; ++seed) {
     synth::Rng rng(static_cast<std::uint64_t>(5000 + seed));
@@ -208,8 +210,42 @@ int mode_dag(const std::string& fixdir) {
     std::string src = synth::random_trajectory(rng, p);
     int which = 0;
     std::string bad = mutate(rng, src, &which);
-    emit_dag_case("mutant" + std::to_string(which) + ":" + std::to_string(seed), bad, false);
+    emit("mutant" + std::to_string(which) + ":" + std::to_string(seed), bad, false);
   }
+}
+
+int mode_dag(const std::string& fixdir) {
+  for_each_dag_case(fixdir, emit_dag_case);
+  return 0;
+}
+
+// Teacher-forced batch targets (dag.cpp:314-359): target ids and loss masks with and without
+// tag loss (BatchOptions::tag_loss), for every parse-valid trajectory of the dag goldens.
+void emit_batch_case(const std::string& name, const std::string& text, bool) {
+  try {
+    grammar::Trajectory traj = grammar::parse_text(text);
+    tok::Tokenizer tz;
+    dag::GenerationDag g = dag::build_dag(traj, tz);
+    dag::BatchOptions with_tags, no_tags;
+    no_tags.tag_loss = false;
+    dag::TrainingBatch a = dag::build_training_batch(g, with_tags);
+    dag::TrainingBatch b = dag::build_training_batch(g, no_tags);
+    std::vector<int> la(a.loss_mask.begin(), a.loss_mask.end()), lb(b.loss_mask.begin(), b.loss_mask.end());
+    std::printf("{\"kind\":\"batch\",\"name\":\"%s\",", name.c_str());
+    put_vec("tokens", a.token_ids);
+    std::printf(",");
+    put_vec("targets", a.target_ids);
+    std::printf(",");
+    put_vec("loss_mask", la);
+    std::printf(",");
+    put_vec("loss_mask_no_tags", lb);
+    std::printf("}\n");
+  } catch (const grammar::ParseError&) {
+  }
+}
+
+int mode_batch(const std::string& fixdir) {
+  for_each_dag_case(fixdir, emit_batch_case);
   return 0;
 }
 
@@ -686,6 +722,7 @@ int main(int argc, char** argv) {
   }
   std::string mode = argv[1];
   if (mode == "dag" && argc >= 3) return mode_dag(argv[2]);
+  if (mode == "batch" && argc >= 3) return mode_batch(argv[2]);
   if (mode == "kv" && argc >= 5)
     return mode_kv(std::stoull(argv[2]), std::stoi(argv[3]), static_cast<std::size_t>(std::stoul(argv[4])));
   if (mode == "toy") return mode_toy();

@@ -61,6 +61,7 @@ def _load():
         "mv_version": ([], ctypes.c_char_p),
         "mv_visibility_workspace_size": ([P, i32], sz),
         "mv_visibility": ([P, P, i32, i32, P, P, P, P, P, sz, P], ctypes.c_int),
+        "mv_training_batch": ([P, P, i32, i32, i32, P, P, P, P, P, P, sz, P], ctypes.c_int),
         "mv_mask_packed": ([P, i32, i32, i32, i32, P, P], ctypes.c_int),
         "mv_tile_map": ([P, i32, i32, i32, P, P, P, P], ctypes.c_int),
         "mv_kv_store_create": ([P, P], ctypes.c_int),
@@ -99,7 +100,8 @@ lib = _load()
 
 # C-ABI symbols declared in include/multiverse_b200.h (checked by tests/test_capi.py)
 EXPORTED = (
-    "mv_last_error", "mv_version", "mv_visibility_workspace_size", "mv_visibility", "mv_mask_packed", "mv_tile_map",
+    "mv_last_error", "mv_version", "mv_visibility_workspace_size", "mv_visibility", "mv_training_batch",
+    "mv_mask_packed", "mv_tile_map",
     "mv_kv_store_create", "mv_kv_store_destroy", "mv_kv_set_stream", "mv_kv_planes", "mv_kv_create", "mv_kv_extend",
     "mv_kv_fork", "mv_kv_merge", "mv_kv_release", "mv_kv_length", "mv_kv_stats_get", "mv_kv_resolve",
     "mv_kv_resolve_payloads", "mv_kv_resolve_slots", "mv_kv_append", "mv_kv_write_last", "mv_kv_append_many",

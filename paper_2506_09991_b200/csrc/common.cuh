@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -197,14 +198,12 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// P for the P.V MMA: rounds a probability pair to bf16x2 and accumulates the ROUNDED values into
-// the row sum, so numerator (sum of rounded p * v) and denominator use the same weights: the result
-// is exact attention under score perturbations of at most 2^-9 (the unrounded sum adds the rounding
-// bias of every weight on top of that).
-__device__ __forceinline__ uint32_t pack_bf16_sum(float2 pp, float2& acc) {
-  const uint32_t u = pack_bf16(pp.x, pp.y);
-  acc = __fadd2_rn(acc, make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xFFFF0000u)));
-  return u;
+// P for the P.V MMA as packed fp16x2 (idesc_f16a_bf16b): probabilities lie in (0, 2^8] under the
+// lazy softmax reference; fp16's 11-bit significand keeps the rounding error of every weight below
+// 2^-12 (bf16: 2^-9, which alone could approach the 2e-3 parity bound on short rows).
+__device__ __forceinline__ uint32_t pack_p(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {

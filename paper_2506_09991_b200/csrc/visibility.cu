@@ -44,17 +44,19 @@ struct SeqWs {
   int32_t* tag_node;  // [n] interval node applying from the k-th tag on (-1 none)
   int32_t* last_tag;  // [n] rank of the last tag at or before token i (-1 none)
   int4* nodes;        // [n] interval nodes {lo, hi, parent, depth}
+  int32_t* single;    // [n] per <Conclusion> tag rank: 1 if its block has exactly one path
 };
 
 __device__ inline SeqWs seq_ws(void* ws, int64_t off, int64_t n) {
-  // Each sequence owns a contiguous workspace slice of 8*n int32.
-  int32_t* base = reinterpret_cast<int32_t*>(ws) + off * 8;
+  // Each sequence owns a contiguous workspace slice of 9*n int32.
+  int32_t* base = reinterpret_cast<int32_t*>(ws) + off * 9;
   SeqWs w;
   w.tag_idx = base;
   w.tag_pos = base + n;
   w.tag_node = base + 2 * n;
   w.last_tag = base + 3 * n;
   w.nodes = reinterpret_cast<int4*>(base + 4 * n);
+  w.single = base + 8 * n;
   return w;
 }
 
@@ -221,6 +223,7 @@ __global__ void __launch_bounds__(kVisThreads) visibility_kernel(const int32_t* 
               err = MV_ERR_COUNT_MISMATCH;  // grammar.cpp:228-232
             } else if (t == kConcOpen) {
               pos = f->max_path_end + 1;  // Reduce = max path end + 1
+              w.single[k] = f->paths == 1;  // the Reduce segment's parents are the path tails
               cur_node = f->enclosing_node;
               f->phase = kInConclusion;
             } else {
@@ -293,7 +296,9 @@ __global__ void __launch_bounds__(kFillThreads) visibility_fill_kernel(const int
                                                                         int32_t* __restrict__ positions,
                                                                         int32_t* __restrict__ excl,
                                                                         const int32_t* __restrict__ status,
-                                                                        void* ws) {
+                                                                        void* ws, const int32_t* __restrict__ tokens,
+                                                                        int32_t* __restrict__ targets,
+                                                                        uint8_t* __restrict__ loss_mask, int tag_loss) {
   const int s = blockIdx.y;
   if (status[s] != MV_OK) return;
   const int64_t off = offsets[s];
@@ -315,6 +320,20 @@ __global__ void __launch_bounds__(kFillThreads) visibility_fill_kernel(const int
       node = w.tag_node[lt];
     }
     positions[off + i] = p;
+    if (targets) {
+      // build_training_batch (dag.cpp:326-357): layout rows are stream order and every segment is a
+      // contiguous run, so a row's target is the next token, except where the next segment is not
+      // its unique chain successor: a </Path> ends its path, and only a single-path block's Reduce
+      // has that path as its one parent; the last row has none.
+      int tgt = -1;
+      if (i + 1 < n) {
+        const int nx = tokens[off + i + 1];
+        tgt = nx;
+        if (tokens[off + i] == kPathClose && !(nx == kConcOpen && w.single[w.last_tag[i + 1]])) tgt = -1;
+      }
+      targets[off + i] = tgt;
+      loss_mask[off + i] = tgt >= 0 && (tag_loss || tgt >= kTagCount) ? 1 : 0;
+    }
     int32_t* e = excl + (off + i) * (int64_t)max_depth * 2;
     int d = node >= 0 ? w.nodes[node].w : 0;
     for (int q = d; q < max_depth; ++q) { e[2 * q] = 0; e[2 * q + 1] = 0; }
@@ -556,14 +575,17 @@ using namespace mv;
 
 extern "C" size_t mv_visibility_workspace_size(const int64_t* h_offsets, int32_t n_seq) {
   if (!h_offsets || n_seq <= 0) return 0;
-  return (size_t)h_offsets[n_seq] * 8 * sizeof(int32_t) + 256;
+  return (size_t)h_offsets[n_seq] * 9 * sizeof(int32_t) + 256;
 }
 
-extern "C" mv_status mv_visibility(const int32_t* d_tokens, const int64_t* h_offsets, int32_t n_seq, int32_t max_depth,
-                                   int32_t* d_positions, int32_t* d_seg_id, int32_t* d_excl, int32_t* d_status,
-                                   void* d_workspace, size_t workspace_bytes, mv_stream_t stream) {
+static mv_status visibility_impl(const int32_t* d_tokens, const int64_t* h_offsets, int32_t n_seq, int32_t max_depth,
+                                 int32_t* d_positions, int32_t* d_seg_id, int32_t* d_excl, int32_t* d_targets,
+                                 uint8_t* d_loss_mask, int tag_loss, int32_t* d_status, void* d_workspace,
+                                 size_t workspace_bytes, mv_stream_t stream) {
   if (n_seq <= 0 || !h_offsets || max_depth < 1 || !d_positions || !d_excl || !d_status)
     return fail(MV_ERR_INVALID_ARGUMENT, "mv_visibility: bad arguments");
+  if ((d_targets == nullptr) != (d_loss_mask == nullptr))
+    return fail(MV_ERR_INVALID_ARGUMENT, "mv_training_batch: targets and loss mask go together");
   if (workspace_bytes < mv_visibility_workspace_size(h_offsets, n_seq) || !d_workspace)
     return fail(MV_ERR_INVALID_ARGUMENT, "mv_visibility: workspace too small");
   for (int s = 0; s < n_seq; ++s)
@@ -571,7 +593,6 @@ extern "C" mv_status mv_visibility(const int32_t* d_tokens, const int64_t* h_off
       return fail(MV_ERR_INVALID_ARGUMENT, "mv_visibility: bad offsets");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int64_t* d_off = nullptr;
-  // Offsets travel inside the workspace tail? Keep it simple: a small async upload.
   MV_CUDA_TRY(cudaMallocAsync(&d_off, sizeof(int64_t) * (n_seq + 1), st));
   MV_CUDA_TRY(cudaMemcpyAsync(d_off, h_offsets, sizeof(int64_t) * (n_seq + 1), cudaMemcpyHostToDevice, st));
   visibility_kernel<<<n_seq, kVisThreads, 0, st>>>(d_tokens, d_off, max_depth, d_positions, d_seg_id, d_excl, d_status,
@@ -581,11 +602,27 @@ extern "C" mv_status mv_visibility(const int32_t* d_tokens, const int64_t* h_off
   for (int s = 0; s < n_seq; ++s) max_len = std::max<int64_t>(max_len, h_offsets[s + 1] - h_offsets[s]);
   if (max_len > 0) {
     visibility_fill_kernel<<<dim3((unsigned)((max_len + kFillTile - 1) / kFillTile), n_seq), kFillThreads, 0, st>>>(
-        d_off, max_depth, d_positions, d_excl, d_status, d_workspace);
+        d_off, max_depth, d_positions, d_excl, d_status, d_workspace, d_tokens, d_targets, d_loss_mask, tag_loss);
     MV_LAUNCH_CHECK();
   }
   MV_CUDA_TRY(cudaFreeAsync(d_off, st));
   return MV_OK;
+}
+
+extern "C" mv_status mv_visibility(const int32_t* d_tokens, const int64_t* h_offsets, int32_t n_seq, int32_t max_depth,
+                                   int32_t* d_positions, int32_t* d_seg_id, int32_t* d_excl, int32_t* d_status,
+                                   void* d_workspace, size_t workspace_bytes, mv_stream_t stream) {
+  return visibility_impl(d_tokens, h_offsets, n_seq, max_depth, d_positions, d_seg_id, d_excl, nullptr, nullptr, 1,
+                         d_status, d_workspace, workspace_bytes, stream);
+}
+
+extern "C" mv_status mv_training_batch(const int32_t* d_tokens, const int64_t* h_offsets, int32_t n_seq,
+                                       int32_t max_depth, int32_t tag_loss, int32_t* d_positions, int32_t* d_excl,
+                                       int32_t* d_targets, uint8_t* d_loss_mask, int32_t* d_status, void* d_workspace,
+                                       size_t workspace_bytes, mv_stream_t stream) {
+  if (!d_targets || !d_loss_mask) return fail(MV_ERR_INVALID_ARGUMENT, "mv_training_batch: null targets / loss mask");
+  return visibility_impl(d_tokens, h_offsets, n_seq, max_depth, d_positions, nullptr, d_excl, d_targets, d_loss_mask,
+                         tag_loss, d_status, d_workspace, workspace_bytes, stream);
 }
 
 extern "C" mv_status mv_mask_packed(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t row0, int32_t row1,

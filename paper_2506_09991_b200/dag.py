@@ -104,3 +104,39 @@ def tile_map(spec: VisibilitySpec, tile: int = 128):
     vis = torch.zeros(1, dtype=torch.int64, device=dev)
     check(lib.mv_tile_map(_ptr(spec.excl), n, spec.max_depth, tile, _ptr(count), _ptr(lst), _ptr(vis), _stream()))
     return count, lst, vis
+
+
+@dataclass
+class TrainingBatch:
+    """dag::TrainingBatch (dag.hpp:124-139) on the device; the mask in its compact interval form."""
+    token_ids: torch.Tensor   # int32 [n] (layout order = stream order)
+    positions: torch.Tensor   # int32 [n]
+    excl: torch.Tensor        # int32 [n, D, 2]
+    target_ids: torch.Tensor  # int32 [n], -1 where a row has no next-token target
+    loss_mask: torch.Tensor   # uint8 [n]
+    max_depth: int
+
+
+def build_training_batch(tokens, tag_loss: bool = True, max_depth: int = DEFAULT_MAX_DEPTH,
+                         device="cuda") -> TrainingBatch:
+    """dag::build_training_batch (dag.cpp:314-359) for one tag stream, in one K1 launch pair;
+    raises ParseError like grammar::parse."""
+    flat = (tokens.reshape(-1).to(device=device, dtype=torch.int32) if isinstance(tokens, torch.Tensor)
+            else torch.tensor([int(x) for x in tokens] or [0], dtype=torch.int32, device=device))
+    n = len(tokens)
+    h_offs = (ctypes.c_int64 * 2)(0, n)
+    m = max(n, 1)
+    pos = torch.empty(m, dtype=torch.int32, device=device)
+    excl = torch.empty((m, max_depth, 2), dtype=torch.int32, device=device)
+    tgt = torch.empty(m, dtype=torch.int32, device=device)
+    loss = torch.empty(m, dtype=torch.uint8, device=device)
+    status = torch.empty(1, dtype=torch.int32, device=device)
+    ws_bytes = lib.mv_visibility_workspace_size(h_offs, 1)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
+    check(lib.mv_training_batch(_ptr(flat), h_offs, 1, max_depth, int(bool(tag_loss)), _ptr(pos), _ptr(excl),
+                                _ptr(tgt), _ptr(loss), _ptr(status), _ptr(ws), ws_bytes, _stream()))
+    st = int(status.item())
+    if st != 0:
+        check(st) if st not in ParseError.KINDS else None
+        raise ParseError(st, f"tag stream rejected: {ParseError.KINDS.get(st, st)}")
+    return TrainingBatch(flat[:n], pos[:n], excl[:n], tgt[:n], loss[:n], max_depth)

@@ -29,6 +29,7 @@ def main():
     if not DRV.exists():
         sys.exit("build oracle/_ref first: ./oracle/ref_build.sh")
     run(["dag", str(FIX)], "dag.jsonl.gz")
+    run(["batch", str(FIX)], "batch.jsonl.gz")
     run(["toy"], "toy.jsonl.gz")
     logs = []
     for seed in range(1, 7):

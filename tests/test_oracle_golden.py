@@ -162,3 +162,16 @@ def test_prefill_oracle_from_tokens_matches_dense_rule():
             s = np.array([q[i, h] @ K[j, h // 2] for j in ctx]) / 4.0
             p = np.exp(s - s.max())
             assert np.abs(out[r, h] - (p[:, None] * V[ctx, h // 2]).sum(0) / p.sum()).max() < 1e-12
+
+
+def test_batch_targets_oracle_matches_reference():
+    """The oracle's build_training_batch restatement equals the reference's targets and loss masks
+    (tests/golden/batch.jsonl.gz: refdrv batch over every parse-valid dag-golden trajectory)."""
+    import oracle
+    rows = load_jsonl("batch.jsonl.gz")
+    assert len(rows) > 300
+    for r in rows:
+        err, tgt, loss = oracle.batch_targets(r["tokens"], True)
+        assert err == 0 and tgt.tolist() == r["targets"] and loss.tolist() == r["loss_mask"], r["name"]
+        _, _, loss2 = oracle.batch_targets(r["tokens"], False)
+        assert loss2.tolist() == r["loss_mask_no_tags"], r["name"]

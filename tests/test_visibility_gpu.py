@@ -96,3 +96,26 @@ def test_tile_map_counts_visible_pairs(mv):
         for kt in range(qt + 1):
             blk = dense_rows[qt * 128:(qt + 1) * 128, kt * 128:(kt + 1) * 128]
             assert (kt in listed) == bool(blk.any())
+
+
+def test_training_batch_targets_match_reference(mv):
+    """§8f-4: the device training batch (targets, loss masks with / without tag loss, positions) equals
+    the reference's build_training_batch on every parse-valid golden trajectory (tests/golden/batch.jsonl.gz)."""
+    from conftest import load_jsonl
+    rows = load_jsonl("batch.jsonl.gz")
+    for r in rows:
+        b = mv.dag.build_training_batch(r["tokens"], tag_loss=True, max_depth=8)
+        assert b.target_ids.cpu().tolist() == r["targets"], r["name"]
+        assert b.loss_mask.cpu().tolist() == r["loss_mask"], r["name"]
+        b2 = mv.dag.build_training_batch(r["tokens"], tag_loss=False, max_depth=8)
+        assert b2.loss_mask.cpu().tolist() == r["loss_mask_no_tags"], r["name"]
+        err, pos, _, _ = oracle.build_dag(r["tokens"])
+        assert b.positions.cpu().tolist() == pos.tolist(), r["name"]
+
+
+def test_training_batch_16k_against_oracle(mv):
+    toks = nested_16k()
+    b = mv.dag.build_training_batch(toks, tag_loss=False)
+    err, tgt, loss = oracle.batch_targets(toks, False)
+    assert err == 0
+    assert np.array_equal(b.target_ids.cpu().numpy(), tgt) and np.array_equal(b.loss_mask.cpu().numpy(), loss)
