@@ -2,7 +2,6 @@
 #pragma once
 
 #include <cuda_bf16.h>
-#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -195,14 +194,6 @@ __device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-
-// P for the P.V MMA as packed fp16x2 (idesc_f16a_bf16b): probabilities lie in (0, 2^8] under the
-// lazy softmax reference; fp16's 11-bit significand keeps the rounding error of every weight below
-// 2^-12 (bf16: 2^-9, which alone could approach the 2e-3 parity bound on short rows).
-__device__ __forceinline__ uint32_t pack_p(float lo, float hi) {
-  __half2 v = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
 

@@ -108,7 +108,7 @@ constexpr int kSmem = kOffTmem + 16 + 1024;  // + 1 KiB alignment slack
 static_assert(kSmem <= 227 * 1024, "decode smem");
 
 constexpr uint32_t kIdQK = tc::idesc_bf16(128, kBlkCols, 0, 0);  // S(128 x 64) = Q . K_blk^T
-constexpr uint32_t kIdPV = tc::idesc_f16a_bf16b(128, 128, 0, 1);  // O(128 x 128) += P_page (f16) . V_page
+constexpr uint32_t kIdPV = tc::idesc_bf16(128, 128, 0, 1);  // O(128 x 128) += P_page . V_page
 
 struct DecodeParams {
   const PageRef* arena;
@@ -258,7 +258,7 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
                                 ? poly_exp2x2(xy)
                                 : make_float2(fast_exp2(xy.x), fast_exp2(xy.y));
           la = __fadd2_rn(la, pp);
-          pk[k] = pack_p(pp.x, pp.y);
+          pk[k] = pack_bf16(pp.x, pp.y);
         }
         return la.x + la.y;
       };

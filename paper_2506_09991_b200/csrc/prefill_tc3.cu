@@ -50,7 +50,7 @@ constexpr int kOffX3 = kOffBar3 + 512;  // row max / sum exchange: [2 parity][2 
 constexpr int kSmem3 = kOffX3 + 2 * 2 * 128 * 4;
 static_assert(kSmem3 <= 227 * 1024, "prefill v3 smem");
 constexpr uint32_t kIdQK3 = tc::idesc_bf16(128, 128, 0, 0);
-constexpr uint32_t kIdPV3 = tc::idesc_f16a_bf16b(128, 128, 0, 1);  // O += P (f16, TMEM) . V (bf16)
+constexpr uint32_t kIdPV3 = tc::idesc_bf16(128, 128, 0, 1);
 constexpr float kLazy3 = 8.f;
 // TMEM columns: three S buffers (S(g) in buffer g % 3) and one O
 constexpr int kSB = 3;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
                                   : make_float2(fast_exp2(xy.x), fast_exp2(xy.y));
             if (u & 1) lb = __fadd2_rn(lb, pp);
             else la = __fadd2_rn(la, pp);
-            pk[u] = pack_p(pp.x, pp.y);
+            pk[u] = pack_bf16(pp.x, pp.y);
           }
           // P for k tokens [64c, 64c + 64) -> packed columns [32c, 32c + 32) of the S buffer
           tc::tmem_stNu<16>(lane_base + s_col + c * 32 + c16 * 16, pk);

@@ -41,14 +41,6 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_
          | ((uint32_t)(M >> 4) << 24);  // M / 16
 }
 
-// P.V with P in fp16 (A, from TMEM) and V in bf16 (B, shared memory): the kind::f16 instruction
-// descriptor types A and B separately.  fp16 keeps 3 more mantissa bits of the probabilities than
-// bf16 (P <= 2^8 under the lazy softmax reference, far inside fp16's range), which bounds the
-// P-rounding error of the output 8x tighter.
-__host__ __device__ constexpr uint32_t idesc_f16a_bf16b(int M, int N, int a_mn, int b_mn) {
-  return idesc_bf16(M, N, a_mn, b_mn) & ~(7u << 7);  // A format 0 = f16
-}
-
 // ---------------------------------------------------------------------------
 // tcgen05
 // ---------------------------------------------------------------------------
