@@ -192,6 +192,10 @@ MV_API mv_status mv_kv_write_last(mv_kv_store* s, const uint64_t* h_handles, int
  * d_k/d_v bf16[n][kv_heads][head_dim] at positions d_positions[n]. */
 MV_API mv_status mv_kv_append_many(mv_kv_store* s, uint64_t h, int64_t n, const int32_t* d_tokens,
                             const int32_t* d_positions, int32_t layer, const void* d_k, const void* d_v);
+/* K/V of tokens [first, first + n) of handle h for `layer` (bf16 [n][kv_heads][head_dim], K rotated at
+ * d_positions[i], or not at all when d_positions is NULL): the other layers of a bulk prefill. */
+MV_API mv_status mv_kv_write_range(mv_kv_store* s, uint64_t h, int64_t first, int64_t n, const int32_t* d_positions,
+                                   int32_t layer, const void* d_k, const void* d_v);
 /* Gather a handle's cached K and V (post-RoPE, bf16 [len][kv_heads][head_dim]) into device buffers. */
 MV_API mv_status mv_kv_gather_kv(mv_kv_store* s, uint64_t h, int32_t layer, void* d_k, void* d_v);
 
@@ -279,6 +283,44 @@ MV_API mv_status mv_interp_init(int32_t* d_state, int32_t n_lanes, const int32_t
 MV_API mv_status mv_interp_feed(int32_t* d_state, int32_t n_lanes, const int32_t* d_events, int32_t n_steps,
                                 int32_t* d_action, int32_t* d_arg, int32_t* d_spawns, int32_t* d_n_spawns,
                                 mv_stream_t stream);
+
+/* ======================================================================== */
+/* The reference's toy transformer on the device      */
+/* ======================================================================== */
+/*
+ * toy::ToyModel (toy_model.hpp:71-92, toy_model.cpp:45-221) with every layer op on the GPU: fp32
+ * projections / tanh MLP / unembed, fp64 RoPE at the token's position, attention through K4 / K3.
+ * Head dims below 128 ride the 128-wide attention kernels zero-padded.
+ * Weights: host fp64 in ToyModelWeights order (toy_model.cpp:58-68): embedding [V][D]; per layer
+ * wq, wk, wv, wo [D][D], w_up [4D][D], w_down [D][4D]; unembed [V][D]; mv_toy_weight_count doubles.
+ */
+typedef struct mv_toy mv_toy;
+typedef struct {
+  int32_t layers, heads, model_dim, vocab;
+  double rope_base; /* 0 = 10000 */
+} mv_toy_config;
+MV_API size_t mv_toy_weight_count(const mv_toy_config* cfg);
+MV_API mv_status mv_toy_create(const mv_toy_config* cfg, const double* h_weights, mv_toy** out);
+MV_API mv_status mv_toy_destroy(mv_toy* m);
+/*
+ * ToyModel::step for n lanes at once (engine.cpp:603-641 batched): each lane's token joins its cache
+ * (K/V of every layer appended in place into `s`, whose planes must be layers x heads x 128) and
+ * attends over it.  d_tokens / d_positions int32[n]; d_logits fp32 [n][V]; optional d_hidden fp32
+ * [n][D] and d_kv fp32 [n][2 * layers * D] (the reference's cache record: per layer rotated K | V).
+ * Runs on the store's stream.
+ */
+MV_API mv_status mv_toy_step(mv_toy* m, mv_kv_store* s, const uint64_t* h_handles, int32_t n, const int32_t* d_tokens,
+                             const int32_t* d_positions, float* d_logits, float* d_hidden, float* d_kv);
+/* Appends ctx_len tokens to handle h from the reference's host cache records (fp64 [ctx_len][2 * layers *
+ * D]; resolve_payloads of engine.cpp:603): the legacy ToyModel::step(context_kv, ...) entry point. */
+MV_API mv_status mv_toy_load_context(mv_toy* m, mv_kv_store* s, uint64_t h, const double* h_records, int64_t ctx_len);
+/* ToyModel::forward (toy_model.cpp:174-202) over one structured sequence: d_positions / d_excl from
+ * mv_visibility (or mv_training_batch); d_logits fp32 [n][V]; optional d_hidden fp32 [n][D]. */
+MV_API mv_status mv_toy_forward(mv_toy* m, const int32_t* d_tokens, int32_t n, const int32_t* d_positions,
+                                const int32_t* d_excl, int32_t max_depth, float* d_logits, float* d_hidden,
+                                mv_stream_t stream);
+/* Greedy sampling (engine.cpp:543-556): the first index of each row's maximum. */
+MV_API mv_status mv_argmax_rows(const float* d_x, int32_t n, int32_t cols, int32_t* d_idx, mv_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -364,6 +364,30 @@ __global__ void k_write_last(const PageRef* __restrict__ arena, const int64_t* _
                  v + (size_t)i * kv_heads * kHeadDim, pos[i], inv, threadIdx.x, blockDim.x);
 }
 
+// K/V of tokens [first, first + n) of one handle for one layer (multi-layer bulk prefill: layer 0 goes
+// with append_many, the other layers through this), one warp per token; the token's slot comes from
+// the handle's entries by binary search over the prefix sums.
+__global__ void k_write_range(const PageRef* __restrict__ arena, const int32_t* __restrict__ cum, int64_t off,
+                              int n_entries, int first, int n, const int32_t* __restrict__ pos,
+                              const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
+                              __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, int64_t npages, const RopeTable rt) {
+  __shared__ double s_inv[kHeadDim / 2];
+  const double* inv = rope_stage(rt, s_inv);
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const int t = first + w;
+  int lo = 0, hi = n_entries - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (cum[off + mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  const PageRef r = arena[off + lo];
+  write_kv_token(kp, vp, r.page, ref_begin(r) + (t - cum[off + lo]), kv_heads, npages,
+                 k + (size_t)w * kv_heads * kHeadDim, v + (size_t)w * kv_heads * kHeadDim, pos ? pos[w] : 0, inv,
+                 lane, 32);
+}
+
 // resolve / resolve_payloads / resolve_slots / gather_kv: one thread block per entry.
 __global__ void k_resolve(const PageRef* __restrict__ arena, const int32_t* __restrict__ cum, int64_t off, int n,
                           const int32_t* __restrict__ slot_tok, const uint8_t* __restrict__ records, int rec_bytes,
@@ -1057,6 +1081,23 @@ mv_status PagedStore::append_many(uint64_t h, int64_t n, const int32_t* d_tokens
   return MV_OK;
 }
 
+mv_status PagedStore::write_range(uint64_t h, int64_t first, int64_t n, const int32_t* d_pos, int32_t layer,
+                                  const void* d_k, const void* d_v) {
+  HandleRec* r = find(h);
+  if (!r) return unknown(h);
+  if (cfg_.kv_heads == 0 || layer < 0 || layer >= cfg_.layers || !d_k || !d_v)
+    return fail(MV_ERR_INVALID_ARGUMENT, "write_range: no attention plane for this layer / null K, V");
+  if (first < 0 || n < 0 || first + n > r->n_tokens())
+    return fail(MV_ERR_INVALID_ARGUMENT, "write_range: token range outside the handle");
+  if (n == 0) return MV_OK;
+  const int64_t threads = n * 32;
+  k_write_range<<<(int)((threads + 255) / 256), 256, 0, stream_>>>(
+      d_arena, d_cum, r->arena_off, r->n_entries(), (int)first, (int)n, d_pos, (const __nv_bfloat16*)d_k,
+      (const __nv_bfloat16*)d_v, k_planes_[layer], v_planes_[layer], cfg_.kv_heads, (int64_t)cfg_.num_pages, rope_);
+  MV_LAUNCH_CHECK();
+  return MV_OK;
+}
+
 mv_status PagedStore::gather_kv(uint64_t h, int32_t layer, void* d_k, void* d_v) {
   HandleRec* r = find(h);
   if (!r) return unknown(h);
@@ -1175,6 +1216,11 @@ extern "C" mv_status mv_kv_append_many(mv_kv_store* s, uint64_t h, int64_t n, co
                                        const int32_t* d_pos, int32_t layer, const void* d_k, const void* d_v) {
   STORE_OR_FAIL(s);
   return s->impl->append_many(h, n, d_tokens, d_pos, layer, d_k, d_v);
+}
+extern "C" mv_status mv_kv_write_range(mv_kv_store* s, uint64_t h, int64_t first, int64_t n, const int32_t* d_positions,
+                                       int32_t layer, const void* d_k, const void* d_v) {
+  STORE_OR_FAIL(s);
+  return s->impl->write_range(h, first, n, d_positions, layer, d_k, d_v);
 }
 extern "C" mv_status mv_kv_gather_kv(mv_kv_store* s, uint64_t h, int32_t layer, void* d_k, void* d_v) {
   STORE_OR_FAIL(s);

@@ -80,6 +80,8 @@ class PagedStore {
                        const void* d_v);
   mv_status append_many(uint64_t h, int64_t n, const int32_t* d_tokens, const int32_t* d_pos, int32_t layer,
                         const void* d_k, const void* d_v);
+  mv_status write_range(uint64_t h, int64_t first, int64_t n, const int32_t* d_pos, int32_t layer, const void* d_k,
+                        const void* d_v);
   mv_status gather_kv(uint64_t h, int32_t layer, void* d_k, void* d_v);
 
   HandleRec* find(uint64_t h);

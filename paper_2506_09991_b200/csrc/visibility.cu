@@ -48,8 +48,9 @@ struct SeqWs {
 };
 
 __device__ inline SeqWs seq_ws(void* ws, int64_t off, int64_t n) {
-  // Each sequence owns a contiguous workspace slice of 9*n int32.
-  int32_t* base = reinterpret_cast<int32_t*>(ws) + off * 9;
+  // Each sequence owns a contiguous workspace slice of 12*n int32 (a multiple of 4 int32 per token keeps
+  // the int4 node array 16-byte aligned for every sequence offset).
+  int32_t* base = reinterpret_cast<int32_t*>(ws) + off * 12;
   SeqWs w;
   w.tag_idx = base;
   w.tag_pos = base + n;
@@ -575,7 +576,7 @@ using namespace mv;
 
 extern "C" size_t mv_visibility_workspace_size(const int64_t* h_offsets, int32_t n_seq) {
   if (!h_offsets || n_seq <= 0) return 0;
-  return (size_t)h_offsets[n_seq] * 9 * sizeof(int32_t) + 256;
+  return (size_t)h_offsets[n_seq] * 12 * sizeof(int32_t) + 256;
 }
 
 static mv_status visibility_impl(const int32_t* d_tokens, const int64_t* h_offsets, int32_t n_seq, int32_t max_depth,
