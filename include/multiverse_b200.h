@@ -319,8 +319,60 @@ MV_API mv_status mv_toy_load_context(mv_toy* m, mv_kv_store* s, uint64_t h, cons
 MV_API mv_status mv_toy_forward(mv_toy* m, const int32_t* d_tokens, int32_t n, const int32_t* d_positions,
                                 const int32_t* d_excl, int32_t max_depth, float* d_logits, float* d_hidden,
                                 mv_stream_t stream);
+MV_API mv_status mv_toy_get_config(const mv_toy* m, mv_toy_config* out);
+MV_API int32_t mv_toy_vocab(const mv_toy* m);
 /* Greedy sampling (engine.cpp:543-556): the first index of each row's maximum. */
 MV_API mv_status mv_argmax_rows(const float* d_x, int32_t n, int32_t cols, int32_t* d_idx, mv_stream_t stream);
+
+/* ======================================================================== */
+/* Engine: the batched Multiverse decode loop  */
+/* ======================================================================== */
+/*
+ * engine::run_forced / run_free (engine.cpp:928-950) over the device hot path: per step ONE batched
+ * device pass for every active lane (mv_toy_step: KV append + K4 decode + layer algebra; greedy argmax;
+ * K5 mv_interp_feed for the tag interpreter of every lane); the host reads back the interpreter actions
+ * and sampled ids (one small copy per step) and spawns (mv_kv_fork + injected <Path>, label), retires
+ * (</Path> -> zombie) and merges (zero-copy mv_kv_merge + injected <Conclusion>) as the reference's
+ * Simulator does (engine.cpp:498-802).  Positions are runtime state (engine.cpp:705, :788).
+ */
+typedef struct {
+  int32_t max_worker_tokens;   /* EngineLimits (engine.hpp:64-67); 0 = 4096 */
+  int32_t max_request_tokens;  /* 0 = 4096 */
+  int32_t num_pages;           /* paged-store pages for the run; 0 = 4096 */
+} mv_engine_options;
+#define MV_ENGINE_FAIL_NONE 0
+#define MV_ENGINE_FAIL_GRAMMAR 1 /* FailureKind::GrammarViolationDuringDecode */
+#define MV_ENGINE_FAIL_LIMIT 2   /* FailureKind::LimitExceeded */
+typedef struct {
+  int32_t status;               /* RunStatus: 0 Done, 1 Failed */
+  int32_t failure;              /* MV_ENGINE_FAIL_* */
+  char failure_detail[256];     /* SimulationReport::failure_detail */
+  int64_t steps, total_tokens, merges, spawns, lanes, events;
+} mv_engine_report;
+/* SimEvent (engine.hpp:85-97): step, lane, kind (EventKind order), token id or spawn count, source index */
+#define MV_EVT_DECODE 0
+#define MV_EVT_PREFILL 1
+#define MV_EVT_SPAWN 2
+#define MV_EVT_ZOMBIE 3
+#define MV_EVT_MERGE 4
+#define MV_EVT_DONE 6
+#define MV_EVT_FAILED 7
+typedef struct {
+  int64_t step;
+  int32_t lane, kind, token, source;
+} mv_engine_event;
+/* Token id of a path index label ("1:", "2.1:", ...; tok::Tokenizer::text_token, engine.cpp:711-715). */
+typedef int32_t (*mv_engine_label_fn)(void* ctx, const char* label);
+/* Forced run (run_forced with record_logits): h_tokens is the tag stream; h_logits fp32 [n][vocab] by
+ * source index (NULL to skip); events into h_events[events_cap] (report.events counts them all). */
+MV_API mv_status mv_engine_run_forced(mv_toy* m, const int32_t* h_tokens, int32_t n, const mv_engine_options* opt,
+                                      mv_stream_t stream, float* h_logits, mv_engine_event* h_events,
+                                      int64_t events_cap, mv_engine_report* report);
+/* Greedy free-running decode after an injected prompt (run_free); stops after max_steps (0: none). */
+MV_API mv_status mv_engine_run_free(mv_toy* m, const int32_t* h_prompt, int32_t n_prompt, int32_t max_steps,
+                                    const mv_engine_options* opt, mv_engine_label_fn label_fn, void* label_ctx,
+                                    mv_stream_t stream, mv_engine_event* h_events, int64_t events_cap,
+                                    mv_engine_report* report);
 
 #ifdef __cplusplus
 }

@@ -11,8 +11,12 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <limits>
+#include <random>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -336,5 +340,230 @@ inline void prefill(const void* d_q, const void* d_k, const void* d_v, const dag
 }
 
 }  // namespace attn
+
+namespace dag {
+
+// dag::build_visibility(GenerationDag&) (dag.hpp:108, dag.cpp:265-270): any GenerationDag-shaped type
+// (token_layout() -> (segment id, offset) rows, segments[sid].tokens[off].id) is flattened to its
+// layout-order token ids and built on the device.
+template <class GenerationDag>
+  requires requires(GenerationDag& g) {
+    g.token_layout();
+    g.segments;
+  }
+VisibilitySpec build_visibility(GenerationDag& g, int max_depth = 8) {
+  std::vector<int32_t> ids;
+  for (auto [sid, off] : g.token_layout())
+    ids.push_back(g.segments[static_cast<std::size_t>(sid)].tokens[static_cast<std::size_t>(off)].id);
+  return build_visibility(std::span<const int32_t>(ids), max_depth);
+}
+
+}  // namespace dag
+
+namespace toy {
+
+// toy::ToyModelConfig (toy_model.hpp:24-37)
+struct ToyModelConfig {
+  int layers = 2;
+  int heads = 2;
+  int model_dim = 32;
+  int vocab_size = 256;
+  std::uint64_t seed = 0;
+  double init_range = 0.05;
+  double rope_base = 10000.0;
+
+  int head_dim() const { return model_dim / heads; }
+  int hidden_dim() const { return 4 * model_dim; }
+  int kv_doubles_per_token() const { return 2 * layers * model_dim; }
+};
+
+// toy::ToyModelWeights (toy_model.hpp:39-57).  init() draws the reference's weights: synth::Rng over
+// std::mt19937_64 (fully specified by the C++ standard) with next_symmetric's mapping (synth.cpp:24-29),
+// in the fill order of toy_model.cpp:58-68.
+struct ToyModelWeights {
+  ToyModelConfig config;
+  struct Layer {
+    std::vector<double> wq, wk, wv, wo, w_up, w_down;
+  };
+  std::vector<double> embedding;
+  std::vector<Layer> layers;
+  std::vector<double> unembed;
+
+  static ToyModelWeights init(const ToyModelConfig& config) {
+    if (config.layers < 1 || config.heads < 1 || config.model_dim < 1 || config.vocab_size < 1)
+      throw std::invalid_argument("toy model dims must be >= 1");
+    if (config.model_dim % config.heads != 0 || config.head_dim() % 2 != 0)
+      throw std::invalid_argument("model_dim must split into even-sized heads");
+    ToyModelWeights w;
+    w.config = config;
+    std::mt19937_64 rng(config.seed);
+    auto fill = [&](std::vector<double>& v, std::size_t n) {
+      v.resize(n);
+      for (auto& x : v) x = (static_cast<double>(rng() >> 11) * 0x1.0p-53 * 2.0 - 1.0) * config.init_range;
+    };
+    const std::size_t d = static_cast<std::size_t>(config.model_dim), hid = static_cast<std::size_t>(config.hidden_dim()),
+                      vocab = static_cast<std::size_t>(config.vocab_size);
+    fill(w.embedding, vocab * d);
+    w.layers.resize(static_cast<std::size_t>(config.layers));
+    for (auto& l : w.layers) {
+      fill(l.wq, d * d);
+      fill(l.wk, d * d);
+      fill(l.wv, d * d);
+      fill(l.wo, d * d);
+      fill(l.w_up, hid * d);
+      fill(l.w_down, d * hid);
+    }
+    fill(w.unembed, vocab * d);
+    return w;
+  }
+};
+
+// toy::StepOutput / ForwardResult (toy_model.hpp:59-69)
+struct StepOutput {
+  std::vector<double> logits;
+  std::vector<double> hidden;
+  std::vector<double> kv;
+};
+struct ForwardResult {
+  std::vector<double> logits;
+  std::vector<double> hidden;
+  std::size_t rows = 0;
+  std::span<const double> logits_row(std::size_t i) const {
+    const std::size_t v = logits.size() / rows;
+    return {logits.data() + i * v, v};
+  }
+  std::span<const double> hidden_row(std::size_t i) const {
+    const std::size_t d = hidden.size() / rows;
+    return {hidden.data() + i * d, d};
+  }
+};
+
+// toy::ToyModel (toy_model.hpp:71-92) on the device (mv_toy_*).  step() is the reference's legacy
+// entry point: the caller's host context records (resolve_payloads, engine.cpp:603-607) are staged into
+// a scratch handle of a device store, then ONE batched device step runs the whole layer stack with K4
+// for the attention; forward() is K1 + K3 over the batch's token stream.  Both are parity paths; the
+// fast path is mv_toy_step over the engine's own store (mv_engine_*).
+class ToyModel {
+ public:
+  explicit ToyModel(const ToyModelConfig& config) : ToyModel(ToyModelWeights::init(config)) {}
+  explicit ToyModel(ToyModelWeights weights) : weights_(std::move(weights)) {
+    const auto& c = weights_.config;
+    mv_toy_config tc{c.layers, c.heads, c.model_dim, c.vocab_size, c.rope_base};
+    std::vector<double> flat;
+    auto put = [&](const std::vector<double>& v) { flat.insert(flat.end(), v.begin(), v.end()); };
+    put(weights_.embedding);
+    for (const auto& l : weights_.layers) {
+      put(l.wq);
+      put(l.wk);
+      put(l.wv);
+      put(l.wo);
+      put(l.w_up);
+      put(l.w_down);
+    }
+    put(weights_.unembed);
+    check(mv_toy_create(&tc, flat.data(), &m_));
+  }
+  ToyModel(const ToyModel&) = delete;
+  ToyModel& operator=(const ToyModel&) = delete;
+  ~ToyModel() {
+    if (scratch_) mv_kv_store_destroy(scratch_);
+    mv_toy_destroy(m_);
+  }
+
+  const ToyModelConfig& config() const { return weights_.config; }
+  const ToyModelWeights& weights() const { return weights_; }
+  mv_toy* native() const { return m_; }
+
+  StepOutput step(std::span<const double> context_kv, std::size_t ctx_len, int token_id, int position) const {
+    const auto& c = weights_.config;
+    const std::size_t rec = static_cast<std::size_t>(c.kv_doubles_per_token());
+    if (context_kv.size() < ctx_len * rec) throw std::invalid_argument("context kv shorter than ctx_len records");
+    ensure_scratch(ctx_len + 1);
+    std::uint64_t h = 0;
+    check(mv_kv_create(scratch_, &h));
+    check(mv_toy_load_context(m_, scratch_, h, context_kv.data(), static_cast<int64_t>(ctx_len)));
+    const int32_t io[2] = {token_id, position};
+    DeviceBuffer<int32_t> d_io(2);
+    d_io.upload(io, 2);
+    DeviceBuffer<float> logits(static_cast<std::size_t>(c.vocab_size)), hidden(static_cast<std::size_t>(c.model_dim)),
+        kv(rec);
+    check(mv_toy_step(m_, scratch_, &h, 1, d_io.data(), d_io.data() + 1, logits.data(), hidden.data(), kv.data()));
+    StepOutput out;
+    auto to64 = [](const std::vector<float>& v) { return std::vector<double>(v.begin(), v.end()); };
+    out.logits = to64(logits.download());
+    out.hidden = to64(hidden.download());
+    out.kv = to64(kv.download());
+    check(mv_kv_release(scratch_, h));
+    return out;
+  }
+
+  // ToyModel::forward (toy_model.cpp:174-202) over a TrainingBatch-shaped batch (token_ids, positions,
+  // mask): the visibility is rebuilt on the device from the token ids (the mask is a function of the
+  // tag stream, dag.cpp:314-359).
+  template <class Batch>
+  ForwardResult forward(const Batch& batch) const {
+    const auto& c = weights_.config;
+    const std::size_t n = batch.token_ids.size();
+    if (batch.mask.size() != n || batch.positions.size() != n)
+      throw std::invalid_argument("batch mask/positions do not match token count");
+    ForwardResult r;
+    r.rows = n;
+    if (n == 0) return r;
+    std::vector<int32_t> ids(batch.token_ids.begin(), batch.token_ids.end());
+    auto vis = dag::build_visibility_device(std::span<const int32_t>(ids), 8);
+    DeviceBuffer<int32_t> d_tok(n);
+    d_tok.upload(ids.data(), n);
+    DeviceBuffer<float> logits(n * static_cast<std::size_t>(c.vocab_size)), hidden(n * static_cast<std::size_t>(c.model_dim));
+    check(mv_toy_forward(m_, d_tok.data(), static_cast<int32_t>(n), vis.positions.data(), vis.excl.data(), vis.max_depth,
+                         logits.data(), hidden.data(), nullptr));
+    auto lg = logits.download();
+    auto hd = hidden.download();
+    r.logits.assign(lg.begin(), lg.end());
+    r.hidden.assign(hd.begin(), hd.end());
+    return r;
+  }
+
+  // ToyModel::loss (toy_model.cpp:204-221): mean negative log-likelihood over loss-masked targets
+  template <class Batch>
+  double loss(const Batch& batch) const {
+    ForwardResult fwd = forward(batch);
+    const std::size_t vocab = static_cast<std::size_t>(weights_.config.vocab_size);
+    double total = 0.0;
+    std::size_t count = 0;
+    for (std::size_t i = 0; i < batch.token_ids.size(); ++i) {
+      if (batch.target_ids[i] < 0 || !batch.loss_mask[i]) continue;
+      auto row = fwd.logits_row(i);
+      double mx = -std::numeric_limits<double>::infinity();
+      for (double z : row) mx = std::max(mx, z);
+      double den = 0.0;
+      for (double z : row) den += std::exp(z - mx);
+      total += -(row[static_cast<std::size_t>(batch.target_ids[i]) % vocab] - mx - std::log(den));
+      ++count;
+    }
+    return count ? total / static_cast<double>(count) : 0.0;
+  }
+
+ private:
+  void ensure_scratch(std::size_t tokens) const {
+    const std::size_t pages = (tokens + 15) / 16 + 4;
+    if (scratch_ && pages <= scratch_pages_) return;
+    if (scratch_) mv_kv_store_destroy(scratch_);
+    scratch_pages_ = std::max<std::size_t>(pages * 2, 256);
+    mv_kv_config kc{};
+    kc.num_pages = static_cast<int32_t>(scratch_pages_);
+    kc.layers = weights_.config.layers;
+    kc.kv_heads = weights_.config.heads;
+    kc.head_dim = 128;
+    kc.rope_base = weights_.config.rope_base;
+    check(mv_kv_store_create(&kc, &scratch_));
+  }
+
+  ToyModelWeights weights_;
+  mv_toy* m_ = nullptr;
+  mutable mv_kv_store* scratch_ = nullptr;  // single-writer: the reference's ToyModel is shared read-only
+  mutable std::size_t scratch_pages_ = 0;
+};
+
+}  // namespace toy
 
 }  // namespace multiverse_b200

@@ -533,6 +533,57 @@ int mode_toy() {
   return 0;
 }
 
+// engine::run_free (greedy, engine.cpp:941-950) of the C1 toy model after a seeded prompt: status,
+// failure detail and every emitted token (Decode / Prefill events with the token's id).
+void emit_free(const char* name, const toy::ToyModelConfig& cfg, int prompt_words, std::uint64_t seed) {
+  toy::ToyModel model(cfg);
+  synth::Rng rng(seed);
+  const std::string text = synth::random_sequential_text(rng, prompt_words);
+  tok::Tokenizer tz;
+  auto prompt = tz.tokenize(text);
+  engine::RunOptions opt;
+  auto rep = engine::run_free(model, tz, prompt, opt);
+  std::vector<int> prompt_ids, steps, lanes, kinds, ids;
+  for (const auto& t : prompt) prompt_ids.push_back(t.id);
+  for (const auto& e : rep.events) {
+    if (e.kind != engine::EventKind::Decode && e.kind != engine::EventKind::Prefill) continue;
+    steps.push_back(static_cast<int>(e.step));
+    lanes.push_back(e.lane);
+    kinds.push_back(e.kind == engine::EventKind::Decode ? 0 : 1);
+    // token_from_id (engine.cpp:584-597): vocab text for known ids, "tok<id>" beyond the vocabulary
+    auto known = tz.vocab().lookup(e.token);
+    ids.push_back(known ? *known : std::stoi(e.token.substr(3)));
+  }
+  std::printf("{\"kind\":\"free\",\"name\":\"%s\",\"layers\":%d,\"heads\":%d,\"model_dim\":%d,\"vocab\":%d,"
+              "\"seed\":%llu,\"init\":%.17g,\"rope\":%.17g,\"status\":%d,\"failure\":%d,\"detail\":\"%s\","
+              "\"wall\":%.17g,",
+              name, cfg.layers, cfg.heads, cfg.model_dim, cfg.vocab_size, (unsigned long long)cfg.seed, cfg.init_range,
+              cfg.rope_base, static_cast<int>(rep.status), static_cast<int>(rep.failure), rep.failure_detail.c_str(),
+              rep.wall_units);
+  put_vec("prompt", prompt_ids);
+  std::printf(",");
+  put_vec("steps", steps);
+  std::printf(",");
+  put_vec("lanes", lanes);
+  std::printf(",");
+  put_vec("kinds", kinds);
+  std::printf(",");
+  put_vec("tokens", ids);
+  std::printf("}\n");
+}
+
+int mode_free() {
+  toy::ToyModelConfig c1;
+  c1.layers = 2;
+  c1.heads = 4;
+  c1.model_dim = 256;
+  c1.vocab_size = 256;
+  emit_free("free_c1", c1, 512, 0);
+  toy::ToyModelConfig small;
+  emit_free("free_small", small, 64, 3);
+  return 0;
+}
+
 int mode_forced_bench(int prompt_words, int path_words, int reps) {
   toy::ToyModelConfig c1;
   c1.layers = 2;
@@ -726,6 +777,7 @@ int main(int argc, char** argv) {
   if (mode == "kv" && argc >= 5)
     return mode_kv(std::stoull(argv[2]), std::stoi(argv[3]), static_cast<std::size_t>(std::stoul(argv[4])));
   if (mode == "toy") return mode_toy();
+  if (mode == "free") return mode_free();
   if (mode == "forced" && argc >= 5) return mode_forced_bench(std::stoi(argv[2]), std::stoi(argv[3]), std::stoi(argv[4]));
   if (mode == "decode" && argc >= 6)
     return mode_decode_bench(std::stoi(argv[2]), std::stod(argv[3]), std::stoi(argv[4]), std::stoi(argv[5]));

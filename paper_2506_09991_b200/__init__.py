@@ -50,6 +50,10 @@ class ParseError(MvError):
         return self.KINDS[self.status]
 
 
+# mv_engine_label_fn: token id of a path index label text
+LABEL_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_char_p)
+
+
 def _load():
     if not LIB_PATH.exists():
         raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -86,6 +90,18 @@ def _load():
         "mv_attn_decode_plan_info": ([P, P], ctypes.c_int),
         "mv_prefill_workspace_size": ([i32, i32, i32], sz),
         "mv_attn_prefill": ([P, P, P, P, P, i32, i32, i32, i32, ctypes.c_double, P, i32, P, sz, P], ctypes.c_int),
+        "mv_kv_write_range": ([P, u64, i64, i64, P, i32, P, P], ctypes.c_int),
+        "mv_toy_weight_count": ([P], sz),
+        "mv_toy_create": ([P, P, P], ctypes.c_int),
+        "mv_toy_destroy": ([P], ctypes.c_int),
+        "mv_toy_get_config": ([P, P], ctypes.c_int),
+        "mv_toy_vocab": ([P], i32),
+        "mv_toy_step": ([P, P, P, i32, P, P, P, P, P], ctypes.c_int),
+        "mv_toy_load_context": ([P, P, u64, P, i64], ctypes.c_int),
+        "mv_toy_forward": ([P, P, i32, P, P, i32, P, P, P], ctypes.c_int),
+        "mv_argmax_rows": ([P, i32, i32, P, P], ctypes.c_int),
+        "mv_engine_run_forced": ([P, P, i32, P, P, P, P, i64, P], ctypes.c_int),
+        "mv_engine_run_free": ([P, P, i32, i32, P, LABEL_FN, P, P, P, i64, P], ctypes.c_int),
         "mv_interp_init": ([P, i32, P, P], ctypes.c_int),
         "mv_interp_feed": ([P, i32, P, i32, P, P, P, P, P], ctypes.c_int),
     }
@@ -106,7 +122,9 @@ EXPORTED = (
     "mv_kv_fork", "mv_kv_merge", "mv_kv_release", "mv_kv_length", "mv_kv_stats_get", "mv_kv_resolve",
     "mv_kv_resolve_payloads", "mv_kv_resolve_slots", "mv_kv_append", "mv_kv_write_last", "mv_kv_append_many",
     "mv_kv_gather_kv", "mv_attn_decode", "mv_attn_decode_plan_info", "mv_prefill_workspace_size", "mv_attn_prefill",
-    "mv_interp_init", "mv_interp_feed",
+    "mv_interp_init", "mv_interp_feed", "mv_kv_write_range", "mv_toy_weight_count", "mv_toy_create", "mv_toy_destroy",
+    "mv_toy_get_config", "mv_toy_vocab", "mv_toy_step", "mv_toy_load_context", "mv_toy_forward", "mv_argmax_rows",
+    "mv_engine_run_forced", "mv_engine_run_free",
 )
 
 

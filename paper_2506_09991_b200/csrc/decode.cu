@@ -957,6 +957,43 @@ static void build_plan(PagedStore& st, DecodePlanCache& pc, const uint64_t* hs, 
       }
     }
   }
+  auto longest_first = [&](std::vector<int32_t>& ord) {
+    ord.resize(items.size());
+    for (size_t k = 0; k < ord.size(); ++k) ord[k] = (int32_t)k;
+    std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+      const WorkItem &a = items[x], &b = items[y];
+      return a.n_entries != b.n_entries ? a.n_entries > b.n_entries : a.n_mem > b.n_mem;
+    });
+  };
+  // Tail split: the dynamic queue ends with its smallest units, and when it runs dry every SM finishes
+  // the unit it holds at a different time (C2 measured SMs idle ~10% of the launch).  The last two
+  // waves of units are therefore halved (4-page-block aligned); a handle whose chunk is split gets one
+  // more split-KV slot.
+  {
+    std::vector<int32_t> ord;
+    longest_first(ord);
+    std::vector<int32_t> split;
+    int64_t acc = 0;
+    for (size_t k = ord.size(); k-- > 0 && acc < 2 * (int64_t)num_sms;) {
+      acc += kv_heads;
+      if (items[ord[k]].n_entries >= 2 * kBlkPages) split.push_back(ord[k]);
+    }
+    for (int32_t it : split) {
+      WorkItem a = items[it];
+      const int32_t half = (a.n_entries / 2 + kBlkPages - 1) / kBlkPages * kBlkPages;
+      WorkItem b = a;
+      b.entry_off = a.entry_off + half;
+      b.n_entries = a.n_entries - half;
+      b.slot_base = n_slots;
+      for (int m = 0; m < b.n_mem; ++m) slots_of[b.members[m]].push_back(n_slots + m);
+      n_slots += b.n_mem;
+      items[it].n_entries = half;
+      items.push_back(b);
+      tags.push_back(tags[it]);  // the second half ends where the chunk ended (a growing private tail)
+      tag_c0.push_back(tag_c0[it] + half);
+      tags[it] = -1;
+    }
+  }
   // longest-first (then widest-first) for the dynamic queue: the tail is made of the smallest units
   std::vector<int32_t> order(items.size());
   for (size_t k = 0; k < order.size(); ++k) order[k] = (int32_t)k;

@@ -308,6 +308,14 @@ extern "C" mv_status mv_toy_create(const mv_toy_config* cfg, const double* h_wei
   return MV_OK;
 }
 
+extern "C" mv_status mv_toy_get_config(const mv_toy* m, mv_toy_config* out) {
+  if (!m || !m->impl || !out) return fail(MV_ERR_INVALID_ARGUMENT, "null argument");
+  *out = m->impl->cfg;
+  return MV_OK;
+}
+
+extern "C" int32_t mv_toy_vocab(const mv_toy* m) { return m && m->impl ? m->impl->cfg.vocab : 0; }
+
 extern "C" mv_status mv_toy_destroy(mv_toy* m) {
   if (!m) return MV_OK;
   delete m->impl;

@@ -31,6 +31,7 @@ def main():
     run(["dag", str(FIX)], "dag.jsonl.gz")
     run(["batch", str(FIX)], "batch.jsonl.gz")
     run(["toy"], "toy.jsonl.gz")
+    run(["free"], "free.jsonl.gz")
     logs = []
     for seed in range(1, 7):
         for rec in (0, 8):

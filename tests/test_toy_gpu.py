@@ -58,11 +58,11 @@ def test_run_forced_matches_reference_engine(mv, toy_golden):
         g, c = toy_golden[name], toy_golden[cfg]
         _, toy = gpu_toy(mv, c)
         ids = tokenize(g["text"])
-        logits, stats = toy.run_forced(ids)
+        logits, rep = toy.run_forced(ids)
         want = np.array(g["logits"]).reshape(len(ids), -1)
         check_logits(logits, want, name)
-        assert stats["forks"] == 1 and stats["merges"] == 1 and stats["length"] == len(ids)
-        assert stats["store"].live_handles == 1  # the root only, released after the stats read
+        assert rep["status"] == "Done" and rep["spawns"] == 1 and rep["merges"] == 1
+        assert rep["total_tokens"] == len(ids) == g["total"]
 
 
 def c1_text(seed=0, prompt_words=512, path_words=64, concl_words=32):
@@ -85,9 +85,9 @@ def test_c1_full_forward_and_run_forced(mv, toy_golden):
     assert err == 0 and len(ids) > 600
     want = ref.forward(ids, pos, oracle.mask_dense(ids))
     check_logits(toy.forward(ids), want, "C1 forward")
-    logits, stats = toy.run_forced(ids)
+    logits, rep = toy.run_forced(ids)
     check_logits(logits, want, "C1 run_forced")
-    assert stats["steps"] < len(ids)  # the two path lanes stepped together
+    assert rep["status"] == "Done" and rep["steps"] < len(ids)  # the two path lanes stepped together
 
 
 def test_nested_run_forced_equals_forward(mv, toy_golden):
@@ -103,7 +103,39 @@ def test_nested_run_forced_equals_forward(mv, toy_golden):
     err, pos, _, _ = oracle.build_dag(ids)
     assert err == 0
     want = ref.forward(ids, pos, oracle.mask_dense(ids))
-    logits, stats = toy.run_forced(ids)
-    assert stats["forks"] == 2 and stats["merges"] == 2
+    logits, rep = toy.run_forced(ids)
+    assert rep["status"] == "Done" and rep["spawns"] == 2 and rep["merges"] == 2
     check_logits(logits, want, "nested run_forced")
     check_logits(toy.forward(ids), want, "nested forward")
+
+
+def test_run_free_matches_reference_engine(mv):
+    """engine::run_free (greedy, engine.cpp:941-950) through the C++ engine: the reference's own run
+    (tests/golden/free.jsonl.gz, refdrv free) emits the same tokens from the same lanes at the same steps
+    and fails at the same step with the same detail (the C1 model breaks the grammar ~20 tokens in)."""
+    from conftest import load_jsonl
+    for g in load_jsonl("free.jsonl.gz"):
+        if g["name"] != "free_c1":
+            continue
+        ref = oracle.Toy(g["layers"], g["heads"], g["model_dim"], g["vocab"], g["seed"], g["init"], g["rope"])
+        _, toy = gpu_toy(mv, {"layers": g["layers"], "heads": g["heads"], "model_dim": g["model_dim"],
+                              "vocab": g["vocab"], "seed": g["seed"], "init": g["init"], "rope": g["rope"]})
+        rep = toy.run_free(g["prompt"])
+        emitted = [e for e in rep["events"] if e[2] in ("Decode", "Prefill")]
+        assert [e[3] for e in emitted] == g["tokens"]
+        assert [e[0] for e in emitted] == g["steps"] and [e[1] for e in emitted] == g["lanes"]
+        assert [0 if e[2] == "Decode" else 1 for e in emitted] == g["kinds"]
+        assert rep["status"] == "Failed" and rep["failure_detail"] == g["detail"]
+        assert rep["steps"] == g["wall"]  # ConstantStep: wall units = steps
+
+
+def test_engine_lane_batching_and_limits(mv, toy_golden):
+    """Worker length cap (EngineLimits::max_worker_tokens: zombie with MaxLength, the reduce proceeds) and the
+    request token limit (LimitExceeded) through the batched engine (engine.cpp:660-676)."""
+    c = toy_golden["t1_c1"]
+    _, toy = gpu_toy(mv, c)
+    ids = tokenize("a b <Parallel> <Goal> <Outline> 1: x </Outline> <Outline> 2: y </Outline> </Goal> "
+                   "<Path> 1: p p p p p p </Path> <Path> 2: q </Path> <Conclusion> c </Conclusion> </Parallel> z")
+    _, rep = toy.run_forced(ids, max_request_tokens=10)
+    assert rep["status"] == "Failed" and rep["failure"] == "LimitExceeded"
+    assert rep["failure_detail"] == "request exceeded 10 tokens"
