@@ -293,7 +293,10 @@ inline DeviceVisibility build_visibility_device(std::span<const int32_t> tokens,
   check(mv_visibility(d_tok.data(), offs, 1, max_depth, v.positions.data(), v.seg_id.data(), v.excl.data(),
                       status.data(), ws.data(), ws_bytes, stream));
   cuda_check(cudaStreamSynchronize(stream));
-  check(static_cast<mv_status>(status.download()[0]));
+  const auto st = static_cast<mv_status>(status.download()[0]);
+  if (st == MV_ERR_DEPTH && max_depth < 64)  // deeper nesting than interval slots: grow the capacity
+    return build_visibility_device(tokens, std::min(2 * max_depth, 64), stream);
+  check(st);
   return v;
 }
 

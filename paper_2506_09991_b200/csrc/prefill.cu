@@ -20,7 +20,7 @@
 namespace mv {
 namespace {
 
-constexpr int kMaxD = 8;         // exclusion intervals per row supported by the kernel
+constexpr int kMaxD = 64;        // exclusion intervals per row (the first 8 live in registers)
 
 // One thread per (row, 16-byte chunk): the 4 (cos, sin) pairs of the chunk depend only on the
 // row's position, so they are computed once and applied to the chunk in every q and k head

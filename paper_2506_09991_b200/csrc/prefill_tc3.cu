@@ -384,6 +384,13 @@ __global__ void __launch_bounds__(kThreads3, 1)
 #pragma unroll
             for (int w = 0; w < 2; ++w) vm[w] &= ~bit_range3(a - (2 * c + w) * 32, b - (2 * c + w) * 32);
           }
+          for (int q = 8; q < P.D; ++q) {  // nesting deeper than 8: the rest from memory
+            const int2 e2 = __ldg(exr + q);
+            const int a = e2.x - j0, b = e2.y - j0;
+            if (a >= kT3 || b <= 0) continue;
+#pragma unroll
+            for (int w = 0; w < 2; ++w) vm[w] &= ~bit_range3(a - (2 * c + w) * 32, b - (2 * c + w) * 32);
+          }
 #pragma unroll
           for (int k = 0; k < 64; k += 2) {
             const uint32_t mm = vm[k >> 5] >> (k & 31);
@@ -499,7 +506,7 @@ mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_
                              const float2* cs, const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
                              int32_t kv_heads, void* d_out, int32_t out_dtype, const int32_t* hcount,
                              const int32_t* tlist, int32_t stride, int32_t* counters, cudaStream_t st) {
-  if (max_depth > 8) return fail(MV_ERR_INVALID_ARGUMENT, "prefill: max_depth > 8");
+  if (max_depth > 64) return fail(MV_ERR_INVALID_ARGUMENT, "prefill: max_depth > 64");
   CUtensorMap mq, mk, mvv;
   if (mv_status e = tc::make_rows_map(&mq, q_raw, n, q_heads, kT3)) return e;
   if (mv_status e = tc::make_rows_map(&mk, k_rot, n, kv_heads, kT3)) return e;

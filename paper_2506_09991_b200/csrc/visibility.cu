@@ -35,7 +35,8 @@ namespace {
 constexpr int kVisThreads = 512;
 constexpr int kVisItems = 8;                      // tokens per thread per tile
 constexpr int kVisTile = kVisThreads * kVisItems;  // 4096
-constexpr int kMaxFrames = 64;                    // open <Parallel> nesting handled by the walker
+constexpr int kMaxFrames = 256;                   // open <Parallel> nesting handled by the walker
+constexpr int kMaxIntervals = 64;                 // exclusion intervals per token the mask consumers accept
 constexpr int kSmemTags = 4096;                   // tags (and interval nodes) the walker reads from smem
 
 struct SeqWs {
@@ -403,6 +404,13 @@ __global__ void tile_map_kernel(const int32_t* __restrict__ excl, int n, int D, 
             touches = true;
           }
         }
+        for (int q = 8; q < D; ++q) {  // nesting deeper than 8: the rest from memory (intervals are disjoint)
+          const int a = max(excl[((int64_t)i * D + q) * 2], j0), b = min(excl[((int64_t)i * D + q) * 2 + 1], last + 1);
+          if (a < b) {
+            vis -= b - a;
+            touches = true;
+          }
+        }
         empty = vis == 0;
         full = !touches && (j1 - 1 <= i) && (j0 + tile <= n);  // tail tiles hold padding tokens
         vis_total += (unsigned long long)vis;
@@ -482,6 +490,10 @@ __global__ void __launch_bounds__(256) tile_status_kernel(const int32_t* __restr
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const int a = max(lo[q], j0), b = min(hi[q], lastc + 1);
+            if (a < b) { vis -= b - a; touches = true; }
+          }
+          for (int q = 8; q < D; ++q) {  // nesting deeper than 8: the rest from memory
+            const int a = max(excl[((int64_t)i * D + q) * 2], j0), b = min(excl[((int64_t)i * D + q) * 2 + 1], lastc + 1);
             if (a < b) { vis -= b - a; touches = true; }
           }
           empty = vis == 0;
@@ -641,7 +653,7 @@ extern "C" mv_status mv_mask_packed(const int32_t* d_excl, int32_t n, int32_t ma
 
 extern "C" mv_status mv_tile_map(const int32_t* d_excl, int32_t n, int32_t max_depth, int32_t tile, int32_t* d_count,
                                  int32_t* d_list, unsigned long long* d_visible_pairs, mv_stream_t stream) {
-  if (n <= 0 || tile <= 0 || tile > 1024 || (tile & 31) || max_depth < 1 || max_depth > 8)
+  if (n <= 0 || tile <= 0 || tile > 1024 || (tile & 31) || max_depth < 1 || max_depth > kMaxIntervals)
     return fail(MV_ERR_INVALID_ARGUMENT, "mv_tile_map: bad arguments");
   int n_qt = (n + tile - 1) / tile;
   tile_map_kernel<<<n_qt, tile, 0, reinterpret_cast<cudaStream_t>(stream)>>>(d_excl, n, max_depth, tile, d_count,

@@ -84,10 +84,17 @@ def build_visibility_batch(token_lists, max_depth: int = DEFAULT_MAX_DEPTH, devi
     return out, st
 
 
+MAX_DEPTH_LIMIT = 64  # the mask consumers' interval capacity (K3, tile maps)
+
+
 def build_visibility(tokens, max_depth: int = DEFAULT_MAX_DEPTH, device="cuda") -> VisibilitySpec:
-    """Positions + compact mask of one tag stream; raises ParseError like grammar::parse."""
-    res, st = build_visibility_batch([tokens if isinstance(tokens, torch.Tensor) else list(tokens)], max_depth,
-                                     device)
+    """Positions + compact mask of one tag stream; raises ParseError like grammar::parse.  The interval
+    capacity grows (doubling, up to MAX_DEPTH_LIMIT) when the stream nests deeper than `max_depth`."""
+    toks = tokens if isinstance(tokens, torch.Tensor) else list(tokens)
+    res, st = build_visibility_batch([toks], max_depth, device)
+    while st[0] == 9 and max_depth < MAX_DEPTH_LIMIT:  # MV_ERR_DEPTH: more nesting than interval slots
+        max_depth = min(2 * max_depth, MAX_DEPTH_LIMIT)
+        res, st = build_visibility_batch([toks], max_depth, device)
     if st[0] != 0:
         check(st[0]) if st[0] not in ParseError.KINDS else None
         raise ParseError(st[0], f"tag stream rejected: {ParseError.KINDS.get(st[0], st[0])}")

@@ -140,3 +140,29 @@ def test_32k_nested_sampled(mv):
     rows = np.sort(np.concatenate([rng.choice(n, 48, replace=False), [0, n - 1]]))
     err, spec = run_prefill(mv, toks, hq=40, hkv=8, rows=rows, seed=9)
     assert err < TOL, (n, err)
+
+
+def deep_chain(depth, seed=0):
+    """A tag stream nested `depth` blocks deep along one path per level (linear size): every row of the
+    innermost path carries `depth` exclusion intervals (the reference's recursion has no limit,
+    dag.cpp:117-187)."""
+    rng = np.random.default_rng(seed)
+    words = lambda k: [int(x) for x in 10 + rng.integers(0, 4000, size=k)]  # noqa: E731
+    P_OPEN, P_CLOSE, G_OPEN, G_CLOSE, O_OPEN, O_CLOSE, PATH, PATH_C, C_OPEN, C_CLOSE = range(10)
+
+    def block(d):
+        t = [P_OPEN, G_OPEN, O_OPEN] + words(2) + [O_CLOSE, O_OPEN] + words(2) + [O_CLOSE, G_CLOSE]
+        t += [PATH] + words(6) + [PATH_C]
+        t += [PATH] + words(5) + (block(d - 1) if d > 1 else []) + words(3) + [PATH_C]
+        return t + [C_OPEN] + words(3) + [C_CLOSE, P_CLOSE]
+
+    return words(40) + block(depth) + words(9)
+
+
+def test_nesting_deeper_than_eight(mv):
+    """12 nested blocks: K1 grows its interval capacity, the tile map and K3 read the intervals beyond 8
+    from memory; every row against the oracle's own mask."""
+    toks = deep_chain(12)
+    err, spec = run_prefill(mv, toks, hq=8, hkv=2, seed=12)
+    assert spec.excl.shape[1] >= 12
+    assert err < TOL, err
