@@ -63,10 +63,14 @@ __device__ __forceinline__ Act feed(int32_t* st, int ev) {
   const int f = st[1];
   const int phase = f & 7;
   const bool in_outline = (f >> 3) & 1, after_outline = (f >> 4) & 1;
-  // An if-chain over opaque copies, not a switch: nvcc lowers a switch (or a plain if-chain) over
-  // the phase to an indirect branch (BRX), and with divergent targets inside the multi-step
-  // loop lanes stopped writing for the rest of the launch (measured on B200: a worker lane in
-  // <Conclusion> beside warp-mates in other phases; one-step launches were exact).
+  // An if-chain over opaque copies, not a switch.  Root cause (tools/experiments/k5_multistep.py,
+  // B200, CUDA 12.9.86): ptxas lowers a switch or a plain if-chain over the phase to a jump table
+  // (`LDC c[0x2][idx]` + `BRX`); when the lanes of a warp sit in different phases that indirect
+  // branch is divergent, and every build that contains it (ptxas -O1 and -O3; one step per launch
+  // or a multi-step loop) corrupts the launch — illegal memory accesses, or, in round 1's variant,
+  // whole warps' stores lost — while the same PTX compiled without the jump table (ptxas -O0, -G)
+  // is exact, and the jump-table build is exact when all lanes share one phase.  opaque() hides
+  // the equality chain from that lowering: the SASS has compares and predicated branches only.
   if (opaque(phase) == AwaitGoal) {
     if (ev != GoalOpen) return violation(MV_VIOL_EXPECTED_GOAL);
     st[1] = (f & ~7) | Goal;
@@ -112,11 +116,9 @@ __device__ __forceinline__ Act feed(int32_t* st, int ev) {
 
 }  // namespace
 
-// One decode step per launch (step index `step` for the spawn list). A variant that walked all
-// n_steps inside one launch, state in registers, lost whole warps' stores after ~10 steps when
-// built with -O3 (B200, deterministic, data-dependent; exact under -G and at one step per
-// launch; tools/debug/interp_diag4.py) — root cause not isolated, so mv_interp_feed issues one
-// launch per step, which is also the engine's use (one sampled token per lane per step).
+// One decode step per launch (step index `step` for the spawn list): the engine's use, one sampled
+// token per lane per step.  (A multi-step loop is correct too once the phase dispatch avoids the
+// divergent jump table, see feed(); one launch per step keeps the spawn list ordered by step.)
 __global__ void interp_kernel(int32_t* __restrict__ state, int32_t n_lanes, const int32_t* __restrict__ events,
                               int32_t step, int32_t* __restrict__ action, int32_t* __restrict__ arg,
                               int32_t* __restrict__ spawns, int32_t* __restrict__ n_spawns) {
