@@ -63,14 +63,16 @@ __device__ __forceinline__ Act feed(int32_t* st, int ev) {
   const int f = st[1];
   const int phase = f & 7;
   const bool in_outline = (f >> 3) & 1, after_outline = (f >> 4) & 1;
-  // An if-chain over opaque copies, not a switch.  Root cause (tools/experiments/k5_multistep.py,
-  // B200, CUDA 12.9.86): ptxas lowers a switch or a plain if-chain over the phase to a jump table
-  // (`LDC c[0x2][idx]` + `BRX`); when the lanes of a warp sit in different phases that indirect
-  // branch is divergent, and every build that contains it (ptxas -O1 and -O3; one step per launch
-  // or a multi-step loop) corrupts the launch — illegal memory accesses, or, in round 1's variant,
-  // whole warps' stores lost — while the same PTX compiled without the jump table (ptxas -O0, -G)
-  // is exact, and the jump-table build is exact when all lanes share one phase.  opaque() hides
-  // the equality chain from that lowering: the SASS has compares and predicated branches only.
+  // An if-chain over opaque copies, not a switch, and one step per launch (interp_kernel): the two
+  // conditions under which this code is exact on B200 with CUDA 12.9.86.  Measured with the same
+  // PTX built several ways (tools/experiments/k5_multistep.py, 16K random lanes x 48 steps against
+  // the restatement): with warp-divergent per-lane phases, every ptxas-optimised build (-O1, -O3)
+  // of the plain dispatch (lowered to an `LDC c[0x2]` jump table + BRX) faults with an illegal
+  // memory access, even at one step per launch; the opaque dispatch (compares only) faults inside
+  // a multi-step loop; the same PTX compiled with ptxas -O0 or -G is exact in every form, and the
+  // optimised builds are exact when all lanes share one phase.  The SASS of the failing loop shows
+  // no out-of-range address arithmetic, so this is treated as a ptxas code-generation defect
+  // around divergent reconvergence, not a source-level race (each lane owns its state and outputs).
   if (opaque(phase) == AwaitGoal) {
     if (ev != GoalOpen) return violation(MV_VIOL_EXPECTED_GOAL);
     st[1] = (f & ~7) | Goal;

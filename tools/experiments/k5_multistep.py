@@ -11,7 +11,7 @@ import numpy as np
 
 REPO = pathlib.Path(__file__).resolve().parents[2]
 OUT = REPO / "tools" / "ab" / "k5"
-VARIANTS = {"O3": ["-O3"], "O1": ["-O1", "-Xptxas", "-O1"], "G": ["-G"], "O3_noptxopt": ["-O3", "-Xptxas", "-O0"]}
+VARIANTS = {"O3_opaque": ["-O3"], "O3": ["-O3"], "O1": ["-O1", "-Xptxas", "-O1"], "G": ["-G"], "O3_noptxopt": ["-O3", "-Xptxas", "-O0"]}
 
 
 def build():
@@ -19,7 +19,7 @@ def build():
     for name, fl in VARIANTS.items():
         cmd = ["/usr/local/cuda/bin/nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-std=c++17", "-shared",
                "-Xcompiler", "-fPIC", "-lineinfo" if name != "G" else "-g", f"-I{REPO / 'include'}",
-               f"-I{REPO / 'paper_2506_09991_b200' / 'csrc'}", *fl, str(REPO / "tools/experiments/k5_multistep.cu"),
+               f"-I{REPO / 'paper_2506_09991_b200' / 'csrc'}", *fl, str(REPO / ("tools/experiments/k5_multistep_opaque.cu" if name == "O3_opaque" else "tools/experiments/k5_multistep.cu")),
                "-o", str(OUT / f"k5_{name}.so")]
         subprocess.run(cmd, check=True)
         print("built", name)
