@@ -359,7 +359,7 @@ typedef struct {
 #define MV_EVT_FAILED 7
 typedef struct {
   int64_t step;
-  int32_t lane, kind, token, source;
+  int32_t request, lane, kind, token, source;  /* lane: index within its request */
 } mv_engine_event;
 /* Token id of a path index label ("1:", "2.1:", ...; tok::Tokenizer::text_token, engine.cpp:711-715). */
 typedef int32_t (*mv_engine_label_fn)(void* ctx, const char* label);
@@ -368,6 +368,13 @@ typedef int32_t (*mv_engine_label_fn)(void* ctx, const char* label);
 MV_API mv_status mv_engine_run_forced(mv_toy* m, const int32_t* h_tokens, int32_t n, const mv_engine_options* opt,
                                       mv_stream_t stream, float* h_logits, mv_engine_event* h_events,
                                       int64_t events_cap, mv_engine_report* report);
+/* A batch of forced requests in one engine (run_batch, engine.cpp:952-966, with the toy model attached):
+ * stream r is h_tokens[h_offsets[r], h_offsets[r+1]); every step is ONE device pass over the active
+ * lanes of ALL requests; h_logits fp32 [h_offsets[n_req]][vocab] by flat source index; the report
+ * carries the first failed request's kind and detail (finalize, engine.cpp:835-880). */
+MV_API mv_status mv_engine_run_batch(mv_toy* m, const int32_t* h_tokens, const int64_t* h_offsets, int32_t n_req,
+                                     const mv_engine_options* opt, mv_stream_t stream, float* h_logits,
+                                     mv_engine_event* h_events, int64_t events_cap, mv_engine_report* report);
 /* Greedy free-running decode after an injected prompt (run_free); stops after max_steps (0: none). */
 MV_API mv_status mv_engine_run_free(mv_toy* m, const int32_t* h_prompt, int32_t n_prompt, int32_t max_steps,
                                     const mv_engine_options* opt, mv_engine_label_fn label_fn, void* label_ctx,

@@ -101,6 +101,7 @@ def _load():
         "mv_toy_forward": ([P, P, i32, P, P, i32, P, P, P], ctypes.c_int),
         "mv_argmax_rows": ([P, i32, i32, P, P], ctypes.c_int),
         "mv_engine_run_forced": ([P, P, i32, P, P, P, P, i64, P], ctypes.c_int),
+        "mv_engine_run_batch": ([P, P, P, i32, P, P, P, P, i64, P], ctypes.c_int),
         "mv_engine_run_free": ([P, P, i32, i32, P, LABEL_FN, P, P, P, i64, P], ctypes.c_int),
         "mv_interp_init": ([P, i32, P, P], ctypes.c_int),
         "mv_interp_feed": ([P, i32, P, i32, P, P, P, P, P], ctypes.c_int),
@@ -124,7 +125,7 @@ EXPORTED = (
     "mv_kv_gather_kv", "mv_attn_decode", "mv_attn_decode_plan_info", "mv_prefill_workspace_size", "mv_attn_prefill",
     "mv_interp_init", "mv_interp_feed", "mv_kv_write_range", "mv_toy_weight_count", "mv_toy_create", "mv_toy_destroy",
     "mv_toy_get_config", "mv_toy_vocab", "mv_toy_step", "mv_toy_load_context", "mv_toy_forward", "mv_argmax_rows",
-    "mv_engine_run_forced", "mv_engine_run_free",
+    "mv_engine_run_forced", "mv_engine_run_batch", "mv_engine_run_free",
 )
 
 

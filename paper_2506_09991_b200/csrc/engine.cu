@@ -23,6 +23,7 @@
 // reference's comment at engine.cpp:505 states this; its loop lets pre-compiled children run in the
 // spawning step, SURVEY.md §0 "minor deviation").  Tokens, positions, contexts and logits are
 // unaffected; only the step count (wall units) differs on forced runs.
+#include <algorithm>
 #include <cstring>
 #include <deque>
 #include <string>
@@ -222,7 +223,7 @@ std::string label_to_prefix(const std::string& label) {  // engine.cpp:73-79
 
 struct Lane {
   enum State { Active, Waiting, Zombie, Done };
-  int id = 0, parent = -1, ordinal = 0;
+  int id = 0, req = 0, parent = -1, ordinal = 0;  // id: index in the engine's flat lane list (= K5 slot)
   State state = Active;
   uint64_t handle = 0;
   int next_position = 0;
@@ -238,6 +239,19 @@ struct Lane {
   bool has_logits = false;
   bool injected_now = false;
   Item now{};
+};
+
+// RequestRuntime (engine.cpp:417-428): one trajectory, its lanes (flat indices), its script.
+struct Request {
+  int base = 0;                    // flat index of its root lane (forced: lanes base .. base + script size)
+  const int32_t* src = nullptr;    // forced source stream
+  int n_src = 0;
+  int64_t logit_row0 = 0;          // first row of its logits in the caller's buffer
+  std::vector<ScriptLane> script;  // forced mode (stable: built before any lane points into it)
+  bool failed = false, done = false;
+  int failure = 0;
+  std::string detail;
+  int64_t emitted = 0;
 };
 
 class Engine {
@@ -257,9 +271,11 @@ class Engine {
     cudaFreeHost(h_logits_);
   }
 
-  mv_status run(const int32_t* src, int n, bool free_running, const int32_t* prompt, int n_prompt, int32_t max_steps,
-                mv_engine_label_fn label_fn, void* label_ctx, float* h_logits, mv_engine_event* events,
-                int64_t events_cap, mv_engine_report* rep) {
+  // Simulator::run (engine.cpp:481-485) over a batch of requests (run_batch, :952-966, with the toy
+  // model attached): forced requests when `offsets` is given, one free-running request otherwise.
+  mv_status run(const int32_t* src, const int64_t* offsets, int n_req, bool free_running, const int32_t* prompt,
+                int n_prompt, int32_t max_steps, mv_engine_label_fn label_fn, void* label_ctx, float* h_logits,
+                mv_engine_event* events, int64_t events_cap, mv_engine_report* rep) {
     std::memset(rep, 0, sizeof *rep);
     free_ = free_running;
     label_fn_ = label_fn;
@@ -271,38 +287,70 @@ class Engine {
     vocab_ = toy_cfg_vocab();
     PagedStore& st = *s_->impl;
     stream_ = st.stream();
-    if (!free_) {
-      std::string err;
-      if (!compile_script(src, n, script_, err)) return failed(MV_ENGINE_FAIL_GRAMMAR, err), MV_OK;
-      lanes_.resize(script_.size());
-      for (size_t i = 0; i < script_.size(); ++i) {
-        lanes_[i].id = (int)i;
-        lanes_[i].parent = script_[i].parent;
-        lanes_[i].ordinal = script_[i].ordinal;
-        lanes_[i].script = &script_[i];
-        lanes_[i].state = i == 0 ? Lane::Active : Lane::Done;
+    reqs_.resize(free_ ? 1 : n_req);
+    for (int r = 0; r < (int)reqs_.size(); ++r) {
+      Request& q = reqs_[r];
+      q.base = (int)lanes_.size();
+      if (!free_) {
+        q.src = src + offsets[r];
+        q.n_src = (int)(offsets[r + 1] - offsets[r]);
+        q.logit_row0 = offsets[r];
+        std::string err;
+        if (!compile_script(q.src, q.n_src, q.script, err)) {  // run_forced returns a failed report
+          fail(r, MV_ENGINE_FAIL_GRAMMAR, err);
+          lanes_.emplace_back();  // an inert root keeps the flat indexing simple
+          lanes_.back().id = q.base;
+          lanes_.back().req = r;
+          lanes_.back().state = Lane::Done;
+          continue;
+        }
+        for (size_t i = 0; i < q.script.size(); ++i) {
+          Lane l;
+          l.id = q.base + (int)i;
+          l.req = r;
+          l.parent = q.script[i].parent >= 0 ? q.base + q.script[i].parent : -1;
+          l.ordinal = q.script[i].ordinal;
+          l.script = &q.script[i];
+          l.state = i == 0 ? Lane::Active : Lane::Done;
+          lanes_.push_back(std::move(l));
+        }
+      } else {
+        if (n_prompt <= 0) {
+          fail(r, MV_ENGINE_FAIL_GRAMMAR, "free-running decode needs a non-empty prompt");
+          break;
+        }
+        Lane l;
+        l.id = q.base;
+        l.req = r;
+        for (int i = 0; i < n_prompt; ++i) l.inject.push_back({prompt[i], -1});
+        lanes_.push_back(std::move(l));
       }
-    } else {
-      if (n_prompt <= 0) return failed(MV_ENGINE_FAIL_GRAMMAR, "free-running decode needs a non-empty prompt"), MV_OK;
-      lanes_.resize(1);
-      for (int i = 0; i < n_prompt; ++i) lanes_[0].inject.push_back({prompt[i], -1});
     }
-    if (mv_status e = st.create(&lanes_[0].handle)) return e;
-    if (mv_status e = ensure_lanes(lanes_.size())) return e;
-    if (mv_status e = mv_interp_init(d_state_, 1, nullptr, stream_)) return e;
+    if (mv_status e = ensure_lanes(std::max<size_t>(lanes_.size(), 1))) return e;
+    for (Request& q : reqs_) {
+      if (q.failed) continue;
+      if (mv_status e = st.create(&lanes_[q.base].handle)) return e;
+      if (mv_status e = mv_interp_init(d_state_ + (size_t)q.base * MV_INTERP_STATE_WORDS, 1, nullptr, stream_))
+        return e;
+    }
     int64_t steps = 0;
     while (true) {
       bool progressed = false;
       if (mv_status e = step_once(&progressed)) return e;
       if (!progressed) break;
-      if (max_steps > 0 && ++steps >= max_steps) break;
+      if (max_steps > 0 && ++steps >= max_steps) {
+        for (int r = 0; r < (int)reqs_.size(); ++r)
+          if (!reqs_[r].failed && !reqs_[r].done) fail(r, MV_ENGINE_FAIL_LIMIT, "max_steps reached");
+        break;
+      }
     }
-    if (!failed_ && !done_) {  // the loop stopped with no active lane (or at max_steps)
-      bool active = false;
-      for (auto& l : lanes_) active = active || l.state == Lane::Active || l.state == Lane::Waiting;
-      if (active && max_steps > 0) failed(MV_ENGINE_FAIL_LIMIT, "max_steps reached");
-    }
-    rep_->status = failed_ ? 1 : 0;
+    // finalize (engine.cpp:835-880): the first failed request's kind and detail
+    for (const Request& q : reqs_)
+      if (q.failed && rep_->status == 0) {
+        rep_->status = 1;
+        rep_->failure = q.failure;
+        std::strncpy(rep_->failure_detail, q.detail.c_str(), sizeof rep_->failure_detail - 1);
+      }
     rep_->steps = step_;
     rep_->merges = merges_;
     rep_->spawns = spawns_;
@@ -317,17 +365,19 @@ class Engine {
  private:
   int toy_cfg_vocab();
 
-  void failed(int kind, const std::string& detail) {
-    failed_ = true;
-    rep_->failure = kind;
-    std::strncpy(rep_->failure_detail, detail.c_str(), sizeof rep_->failure_detail - 1);
+  // fail (engine.cpp:804-815): the request stops; other requests go on
+  void fail(int r, int kind, const std::string& detail) {
+    Request& q = reqs_[r];
+    q.failed = true;
+    q.failure = kind;
+    q.detail = detail;
     for (auto& l : lanes_)
-      if (l.state == Lane::Active || l.state == Lane::Waiting) l.state = Lane::Done;
-    log(MV_EVT_FAILED, 0, -1, -1);
+      if (l.req == r && (l.state == Lane::Active || l.state == Lane::Waiting)) l.state = Lane::Done;
+    log(MV_EVT_FAILED, r, q.base, -1, -1);
   }
 
-  void log(int kind, int lane, int token, int source) {
-    if (events_ && n_events_ < events_cap_) events_[n_events_] = {step_, lane, kind, token, source};
+  void log(int kind, int req, int lane, int token, int source) {
+    if (events_ && n_events_ < events_cap_) events_[n_events_] = {step_, req, lane - reqs_[req].base, kind, token, source};
     ++n_events_;
   }
 
@@ -381,19 +431,19 @@ class Engine {
     return MV_OK;
   }
 
-  // Simulator::step_once (engine.cpp:498-525) with step_lane (:528-582) and emit (:599-677) batched.
+  // Simulator::step_once (engine.cpp:498-525) with step_lane (:528-582) and emit (:599-677) batched over
+  // every active lane of every request.
   mv_status step_once(bool* progressed) {
     *progressed = false;
-    if (failed_ || done_) return MV_OK;
     std::vector<int> batch;
     const size_t count = lanes_.size();  // lanes spawned in this step start on the next one
     bool any = false;
     for (size_t li = 0; li < count; ++li) any = any || lanes_[li].state == Lane::Active;
     if (!any) return MV_OK;
     ++step_;
-    for (size_t li = 0; li < count && !failed_; ++li) {
+    for (size_t li = 0; li < count; ++li) {
       Lane& l = lanes_[li];
-      if (l.state != Lane::Active) continue;
+      if (l.state != Lane::Active || reqs_[l.req].failed) continue;
       Item it;
       bool injected = false;
       if (!l.inject.empty()) {
@@ -404,8 +454,8 @@ class Engine {
         it = l.script->items[l.next_item++];
       } else if (free_) {
         if (!l.has_logits) {
-          failed(MV_ENGINE_FAIL_GRAMMAR, "free-running lane has no context to decode from");
-          break;
+          fail(l.req, MV_ENGINE_FAIL_GRAMMAR, "free-running lane has no context to decode from");
+          continue;
         }
         it = {l.last_token, -1};
       } else {
@@ -416,11 +466,13 @@ class Engine {
       l.injected_now = injected;
       batch.push_back((int)li);
     }
-    if (failed_) return MV_OK;
     *progressed = true;
+    // a request that failed while the batch was being gathered emits nothing this step
+    batch.erase(std::remove_if(batch.begin(), batch.end(), [&](int li) { return reqs_[lanes_[li].req].failed; }),
+                batch.end());
     const int b = (int)batch.size();
     if (b > 0) {
-      // ---- device: one pass for every emitting lane ----
+      // ---- device: one pass for every emitting lane of every request ----
       std::vector<uint64_t> hs(b);
       for (int k = 0; k < b; ++k) {
         Lane& l = lanes_[batch[k]];
@@ -428,9 +480,9 @@ class Engine {
         h_io_[k] = l.now.token;
         h_io_[b + k] = l.next_position;
       }
-      for (size_t li = 0; li < lanes_.size(); ++li) h_io_[2 * b + li] = MV_INTERP_IDLE;
-      for (int k = 0; k < b; ++k) h_io_[2 * b + batch[k]] = lanes_[batch[k]].now.token;
       const size_t nl = lanes_.size();
+      for (size_t li = 0; li < nl; ++li) h_io_[2 * b + li] = MV_INTERP_IDLE;
+      for (int k = 0; k < b; ++k) h_io_[2 * b + batch[k]] = lanes_[batch[k]].now.token;
       MV_CUDA_TRY(cudaMemcpyAsync(d_io_, h_io_, sizeof(int32_t) * 2 * b, cudaMemcpyHostToDevice, stream_));
       MV_CUDA_TRY(cudaMemcpyAsync(d_events_, h_io_ + 2 * b, sizeof(int32_t) * nl, cudaMemcpyHostToDevice, stream_));
       if (mv_status e = mv_toy_step(toy_, s_, hs.data(), b, d_io_, d_io_ + b, d_logits_, nullptr, nullptr)) return e;
@@ -446,33 +498,35 @@ class Engine {
         MV_CUDA_TRY(cudaMemcpyAsync(h_logits_, d_logits_, sizeof(float) * b * vocab_, cudaMemcpyDeviceToHost, stream_));
       MV_CUDA_TRY(cudaStreamSynchronize(stream_));
       // ---- host: emit bookkeeping and interpreter actions, lane order (engine.cpp:643-677) ----
-      for (int k = 0; k < b && !failed_; ++k) {
+      for (int k = 0; k < b; ++k) {
         Lane& l = lanes_[batch[k]];
+        Request& q = reqs_[l.req];
+        if (q.failed) continue;  // an earlier lane of this request failed in this step
         if (h_logits_out_ && l.now.source >= 0)
-          std::memcpy(h_logits_out_ + (size_t)l.now.source * vocab_, h_logits_ + (size_t)k * vocab_,
+          std::memcpy(h_logits_out_ + (size_t)(q.logit_row0 + l.now.source) * vocab_, h_logits_ + (size_t)k * vocab_,
                       sizeof(float) * vocab_);
         l.last_token = h_back_[2 * cap_lanes_ + k];
         l.has_logits = true;
         ++l.next_position;
         ++l.emitted;
         ++total_tokens_;
-        ++req_emitted_;
-        log(l.injected_now ? MV_EVT_PREFILL : MV_EVT_DECODE, l.id, l.now.token, l.now.source);
-        if (req_emitted_ > (int64_t)max_request_tokens()) {
-          failed(MV_ENGINE_FAIL_LIMIT, "request exceeded " + std::to_string(max_request_tokens()) + " tokens");
-          break;
+        ++q.emitted;
+        log(l.injected_now ? MV_EVT_PREFILL : MV_EVT_DECODE, l.req, l.id, l.now.token, l.now.source);
+        if (q.emitted > (int64_t)max_request_tokens()) {
+          fail(l.req, MV_ENGINE_FAIL_LIMIT, "request exceeded " + std::to_string(max_request_tokens()) + " tokens");
+          continue;
         }
         const int act = h_back_[l.id], arg = h_back_[cap_lanes_ + l.id];
         if (act == MV_ACT_VIOLATION) {
-          failed(MV_ENGINE_FAIL_GRAMMAR, violation_text(arg, l.now.token));
-          break;
+          fail(l.req, MV_ENGINE_FAIL_GRAMMAR, violation_text(arg, l.now.token));
+          continue;
         }
         if (act == MV_ACT_WORKER_DONE) {
           enter_zombie(l);
           continue;
         }
         if (act == MV_ACT_SPAWN) {
-          if (mv_status e = spawn_children(l, arg)) return e;
+          if (mv_status e = spawn_children(batch[k], arg)) return e;
           continue;
         }
         if (l.parent >= 0 && l.state == Lane::Active && l.emitted >= (int64_t)max_worker_tokens()) enter_zombie(l);
@@ -482,11 +536,10 @@ class Engine {
           finish_lane(l);
       }
     }
-    if (failed_) return MV_OK;
     // ---- end of step: merge every waiting lane whose children are all zombies (engine.cpp:516-523) ----
     for (size_t li = 0; li < lanes_.size(); ++li)
-      if (lanes_[li].state == Lane::Waiting)
-        if (mv_status e = maybe_merge(lanes_[li])) return e;
+      if (lanes_[li].state == Lane::Waiting && !reqs_[lanes_[li].req].failed)
+        if (mv_status e = maybe_merge((int)li)) return e;
     return MV_OK;
   }
 
@@ -494,23 +547,27 @@ class Engine {
   size_t max_request_tokens() const { return opt_.max_request_tokens > 0 ? (size_t)opt_.max_request_tokens : 4096; }
 
   // spawn_children (engine.cpp:679-725): fork the lane's KV into `count` children that start at its
-  // next position with an injected <Path> and their index label.
-  mv_status spawn_children(Lane& l, int count) {
-    const int pid = l.id;  // lanes_ may grow below: the parent is re-fetched by index
+  // next position with an injected <Path> and their index label.  (lanes_ may grow: indices only.)
+  mv_status spawn_children(int pid, int count) {
     const ScriptLane::Spawn* sp = nullptr;
-    if (l.script && l.next_spawn < l.script->spawns.size()) sp = &l.script->spawns[l.next_spawn++];
+    {
+      Lane& l = lanes_[pid];
+      if (l.script && l.next_spawn < l.script->spawns.size()) sp = &l.script->spawns[l.next_spawn++];
+    }
     std::vector<uint64_t> forks(count);
-    if (mv_status e = s_->impl->fork(l.handle, count, forks.data())) return e;
-    const std::string prefix = l.label.empty() ? "" : label_to_prefix(l.label);
+    if (mv_status e = s_->impl->fork(lanes_[pid].handle, count, forks.data())) return e;
+    const int r = lanes_[pid].req, base = reqs_[r].base;
+    const std::string prefix = lanes_[pid].label.empty() ? "" : label_to_prefix(lanes_[pid].label);
     std::vector<int> kids;
     for (int k = 1; k <= count; ++k) {
       int cid;
       if (sp) {
-        cid = sp->children[k - 1];
+        cid = base + sp->children[k - 1];
       } else {
         cid = (int)lanes_.size();
         lanes_.emplace_back();
         lanes_.back().id = cid;
+        lanes_.back().req = r;
       }
       kids.push_back(cid);
     }
@@ -526,7 +583,7 @@ class Engine {
       if (c.label.empty()) c.label = prefix + std::to_string(k) + ":";
       const ScriptLane* cl = c.script;
       int label_tok;
-      if (cl && cl->label_source >= 0) label_tok = src_token(cl->label_source);
+      if (cl && cl->label_source >= 0) label_tok = reqs_[r].src[cl->label_source];
       else if (label_fn_) label_tok = label_fn_(label_ctx_, c.label.c_str());
       else label_tok = -1;
       c.inject.push_back({kPathOpen, cl ? cl->path_open_source : -1});
@@ -538,21 +595,20 @@ class Engine {
     p.waiting_on = p.spawn_children.size() - 1;
     p.state = Lane::Waiting;
     ++spawns_;
-    log(MV_EVT_SPAWN, p.id, count, -1);
+    log(MV_EVT_SPAWN, r, p.id, count, -1);
     return MV_OK;
   }
 
-  int src_token(int source) const { return source >= 0 && source < n_src_ ? src_[source] : -1; }
-
   void enter_zombie(Lane& l) {
     l.state = Lane::Zombie;
-    log(MV_EVT_ZOMBIE, l.id, -1, -1);
+    log(MV_EVT_ZOMBIE, l.req, l.id, -1, -1);
   }
 
   void finish_lane(Lane& l);
 
   // maybe_merge (engine.cpp:767-802)
-  mv_status maybe_merge(Lane& l) {
+  mv_status maybe_merge(int li) {
+    Lane& l = lanes_[li];
     const std::vector<int>& kids = l.spawn_children[l.waiting_on];
     std::vector<uint64_t> branches;
     for (int c : kids) {
@@ -581,20 +637,15 @@ class Engine {
     MV_CUDA_TRY(cudaStreamSynchronize(stream_));  // ev is pageable host memory
     l.inject.push_back({kConcOpen, l.spawn_conclusion[l.waiting_on]});
     l.state = Lane::Active;
-    log(MV_EVT_MERGE, l.id, -1, -1);
+    log(MV_EVT_MERGE, l.req, l.id, -1, -1);
     return MV_OK;
   }
 
- public:
-  const int32_t* src_ = nullptr;
-  int n_src_ = 0;
-
- private:
   mv_toy* toy_;
   mv_kv_store* s_;
   mv_engine_options opt_;
   cudaStream_t stream_ = nullptr;
-  bool free_ = false, failed_ = false, done_ = false;
+  bool free_ = false;
   mv_engine_label_fn label_fn_ = nullptr;
   void* label_ctx_ = nullptr;
   float* h_logits_out_ = nullptr;
@@ -602,9 +653,9 @@ class Engine {
   int64_t events_cap_ = 0, n_events_ = 0;
   mv_engine_report* rep_ = nullptr;
   int vocab_ = 0;
-  std::vector<ScriptLane> script_;
+  std::deque<Request> reqs_;  // stable addresses: lanes point into their request's script
   std::vector<Lane> lanes_;
-  int64_t step_ = 0, merges_ = 0, spawns_ = 0, total_tokens_ = 0, req_emitted_ = 0;
+  int64_t step_ = 0, merges_ = 0, spawns_ = 0, total_tokens_ = 0;
   size_t cap_lanes_ = 0;
   int32_t *d_state_ = nullptr, *d_ones_ = nullptr, *d_events_ = nullptr, *d_action_ = nullptr, *d_arg_ = nullptr;
   int32_t *d_io_ = nullptr, *d_ids_ = nullptr;
@@ -621,13 +672,13 @@ void Engine::finish_lane(Lane& l) {
     cudaMemcpyAsync(st, d_state_ + (size_t)l.id * MV_INTERP_STATE_WORDS, sizeof st, cudaMemcpyDeviceToHost, stream_);
     cudaStreamSynchronize(stream_);
     if ((st[0] & 0xff) == 0) {
-      done_ = true;
-      log(MV_EVT_DONE, l.id, -1, -1);
+      reqs_[l.req].done = true;
+      log(MV_EVT_DONE, l.req, l.id, -1, -1);
     } else {
-      failed(MV_ENGINE_FAIL_GRAMMAR, "stream ended inside an open block");
+      fail(l.req, MV_ENGINE_FAIL_GRAMMAR, "stream ended inside an open block");
     }
   } else {
-    failed(MV_ENGINE_FAIL_GRAMMAR, "worker stream ended early");
+    fail(l.req, MV_ENGINE_FAIL_GRAMMAR, "worker stream ended early");
   }
 }
 
@@ -650,10 +701,13 @@ static mv_status engine_store(mv_toy* toy, const mv_engine_options* opt, mv_kv_s
   return mv_kv_store_create(&kc, out);
 }
 
-extern "C" mv_status mv_engine_run_forced(mv_toy* toy, const int32_t* h_tokens, int32_t n,
-                                          const mv_engine_options* opt, mv_stream_t stream, float* h_logits,
-                                          mv_engine_event* h_events, int64_t events_cap, mv_engine_report* rep) {
-  if (!toy || !rep || (n > 0 && !h_tokens) || n < 0) return fail(MV_ERR_INVALID_ARGUMENT, "mv_engine_run_forced: bad arguments");
+extern "C" mv_status mv_engine_run_batch(mv_toy* toy, const int32_t* h_tokens, const int64_t* h_offsets, int32_t n_req,
+                                         const mv_engine_options* opt, mv_stream_t stream, float* h_logits,
+                                         mv_engine_event* h_events, int64_t events_cap, mv_engine_report* rep) {
+  if (!toy || !rep || n_req < 1 || !h_offsets || (h_offsets[n_req] > 0 && !h_tokens))
+    return fail(MV_ERR_INVALID_ARGUMENT, "mv_engine_run_batch: bad arguments");
+  for (int r = 0; r < n_req; ++r)
+    if (h_offsets[r + 1] < h_offsets[r]) return fail(MV_ERR_INVALID_ARGUMENT, "mv_engine_run_batch: bad offsets");
   mv_engine_options o{};
   if (opt) o = *opt;
   mv_kv_store* s = nullptr;
@@ -662,12 +716,19 @@ extern "C" mv_status mv_engine_run_forced(mv_toy* toy, const int32_t* h_tokens, 
   mv_status st;
   {
     Engine eng(toy, s, o);
-    eng.src_ = h_tokens;
-    eng.n_src_ = n;
-    st = eng.run(h_tokens, n, false, nullptr, 0, 0, nullptr, nullptr, h_logits, h_events, events_cap, rep);
+    st = eng.run(h_tokens, h_offsets, n_req, false, nullptr, 0, 0, nullptr, nullptr, h_logits, h_events, events_cap,
+                 rep);
   }
   mv_kv_store_destroy(s);
   return st;
+}
+
+extern "C" mv_status mv_engine_run_forced(mv_toy* toy, const int32_t* h_tokens, int32_t n,
+                                          const mv_engine_options* opt, mv_stream_t stream, float* h_logits,
+                                          mv_engine_event* h_events, int64_t events_cap, mv_engine_report* rep) {
+  if (n < 0) return fail(MV_ERR_INVALID_ARGUMENT, "mv_engine_run_forced: n < 0");
+  const int64_t offs[2] = {0, n};
+  return mv_engine_run_batch(toy, h_tokens, offs, 1, opt, stream, h_logits, h_events, events_cap, rep);
 }
 
 extern "C" mv_status mv_engine_run_free(mv_toy* toy, const int32_t* h_prompt, int32_t n_prompt, int32_t max_steps,
@@ -684,8 +745,8 @@ extern "C" mv_status mv_engine_run_free(mv_toy* toy, const int32_t* h_prompt, in
   mv_status st;
   {
     Engine eng(toy, s, o);
-    st = eng.run(nullptr, 0, true, h_prompt, n_prompt, max_steps, label_fn, label_ctx, nullptr, h_events, events_cap,
-                 rep);
+    st = eng.run(nullptr, nullptr, 1, true, h_prompt, n_prompt, max_steps, label_fn, label_ctx, nullptr, h_events,
+                 events_cap, rep);
   }
   mv_kv_store_destroy(s);
   return st;

@@ -39,8 +39,8 @@ class _Report(ctypes.Structure):
 
 
 class _Event(ctypes.Structure):
-    _fields_ = [("step", ctypes.c_int64), ("lane", ctypes.c_int32), ("kind", ctypes.c_int32),
-                ("token", ctypes.c_int32), ("source", ctypes.c_int32)]
+    _fields_ = [("step", ctypes.c_int64), ("request", ctypes.c_int32), ("lane", ctypes.c_int32),
+                ("kind", ctypes.c_int32), ("token", ctypes.c_int32), ("source", ctypes.c_int32)]
 
 
 EVENT_KINDS = {0: "Decode", 1: "Prefill", 2: "Spawn", 3: "ZombieEnter", 4: "Merge", 6: "Done", 7: "Failed"}
@@ -120,6 +120,25 @@ class ToyModel:
                                        logits.ctypes.data_as(ctypes.c_void_p), events, cap, ctypes.byref(rep)))
         return torch.from_numpy(logits[:n]), _report(rep, events, cap)
 
+    def run_batch(self, streams, num_pages: int = 4096, max_worker_tokens: int = 0, max_request_tokens: int = 0):
+        """engine::run_batch (with the toy model attached): every step one device pass over the active lanes
+        of ALL requests.  Returns ([logits [n_r, V] per request], report dict; events carry the request)."""
+        streams = [np.ascontiguousarray([int(i) for i in s_], dtype=np.int32) for s_ in streams]
+        offs = np.zeros(len(streams) + 1, np.int64)
+        offs[1:] = np.cumsum([len(s_) for s_ in streams])
+        flat = np.ascontiguousarray(np.concatenate(streams) if offs[-1] else np.zeros(1, np.int32))
+        logits = np.zeros((max(int(offs[-1]), 1), self.V), np.float32)
+        cap = 8 * int(offs[-1]) + 64 * len(streams)
+        events = (_Event * cap)()
+        rep = _Report()
+        opts = _EngineOpts(max_worker_tokens, max_request_tokens, num_pages)
+        check(lib.mv_engine_run_batch(self._h, flat.ctypes.data_as(ctypes.c_void_p),
+                                      offs.ctypes.data_as(ctypes.c_void_p), len(streams), ctypes.byref(opts),
+                                      _stream(), logits.ctypes.data_as(ctypes.c_void_p), events, cap,
+                                      ctypes.byref(rep)))
+        out = [torch.from_numpy(logits[offs[r]:offs[r + 1]]) for r in range(len(streams))]
+        return out, _report(rep, events, cap)
+
     def run_free(self, prompt, label_token=None, max_steps: int = 0, num_pages: int = 4096,
                  max_worker_tokens: int = 0, max_request_tokens: int = 0):
         """engine::run_free (greedy): the report dict, with the emitted tokens per event."""
@@ -136,7 +155,7 @@ class ToyModel:
 
 def _report(rep: _Report, events, cap) -> dict:
     ev = [(events[i].step, events[i].lane, EVENT_KINDS.get(events[i].kind, events[i].kind), events[i].token,
-           events[i].source) for i in range(min(rep.events, cap))]
+           events[i].source, events[i].request) for i in range(min(rep.events, cap))]
     return {"status": "Failed" if rep.status else "Done", "failure": FAILURES.get(rep.failure, rep.failure),
             "failure_detail": rep.failure_detail.decode(), "steps": rep.steps, "total_tokens": rep.total_tokens,
             "merges": rep.merges, "spawns": rep.spawns, "lanes": rep.lanes, "events": ev}

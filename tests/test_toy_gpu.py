@@ -139,3 +139,29 @@ def test_engine_lane_batching_and_limits(mv, toy_golden):
     _, rep = toy.run_forced(ids, max_request_tokens=10)
     assert rep["status"] == "Failed" and rep["failure"] == "LimitExceeded"
     assert rep["failure_detail"] == "request exceeded 10 tokens"
+
+
+def test_run_batch_many_requests_one_pass_per_step(mv, toy_golden):
+    """engine::run_batch with the toy model: three requests of different shapes advance together (one device
+    pass per step for the active lanes of all of them); each request's logits equal its own forced run,
+    and a malformed request fails alone (finalize reports the first failure, engine.cpp:835-880)."""
+    c = toy_golden["t1_c1"]
+    ref, toy = gpu_toy(mv, c)
+    texts = [c1_text(seed=1, prompt_words=40, path_words=12, concl_words=6),
+             "intro words here <Parallel> <Goal> <Outline> 1: a </Outline> <Outline> 2: b </Outline> "
+             "<Outline> 3: c </Outline> </Goal> <Path> 1: x x </Path> <Path> 2: z z z z </Path> <Path> 3: k </Path> "
+             "<Conclusion> done now </Conclusion> </Parallel> tail",
+             "plain sequential text only here"]
+    streams = [tokenize(t) for t in texts]
+    outs, rep = toy.run_batch(streams)
+    assert rep["status"] == "Done" and rep["spawns"] == 2 and rep["merges"] == 2
+    assert rep["total_tokens"] == sum(len(s) for s in streams)
+    longest_alone = max(toy.run_forced(s)[1]["steps"] for s in streams)
+    assert rep["steps"] == longest_alone  # the requests run concurrently
+    for s, got in zip(streams, outs):
+        err, pos, _, _ = oracle.build_dag(s)
+        check_logits(got, ref.forward(s, pos, oracle.mask_dense(s)), f"batch request of {len(s)} tokens")
+    bad = streams[1][:-6]  # the stream ends inside its block
+    outs, rep = toy.run_batch([streams[0], bad])
+    assert rep["status"] == "Failed" and "unterminated block" in rep["failure_detail"]
+    check_logits(outs[0], toy.run_forced(streams[0])[0].numpy(), "healthy request beside a failed one")

@@ -54,7 +54,15 @@ TRACE = [
 ]
 SB3 = ("constexpr int kSBufs = 5;", "constexpr int kSBufs = 3;")
 SB4 = ("constexpr int kSBufs = 5;", "constexpr int kSBufs = 4;")
-VARIANTS = {"sb3": [SB3], "sb4": [SB4], "trace": TRACE, "nopv": [PV], "noqk": [QK], "nosoft": [SOFT], "streamonly": [PV, QK, SOFT], "narrowF2": [F2],
+NOEXP = ("""          const float2 pp = (kDecPoly > 0 && k % kDecPoly == kDecPoly - 1)
+                                ? poly_exp2x2(xy)
+                                : make_float2(fast_exp2(xy.x), fast_exp2(xy.y));""", "          const float2 pp = xy;")
+ALLPOLY = ("""          const float2 pp = (kDecPoly > 0 && k % kDecPoly == kDecPoly - 1)""", """          const float2 pp = (true)""")
+NOSTORE = ("      tc::tmem_stNu<WP>(scol + part * WP, pk);", "      if (pk[0] == 0x7fffffffu) tc::tmem_stNu<WP>(scol + part * WP, pk);")
+POLY0 = ("constexpr int kDecPoly = 4;", "constexpr int kDecPoly = 0;")
+POLY8 = ("constexpr int kDecPoly = 4;", "constexpr int kDecPoly = 8;")
+POLY2 = ("constexpr int kDecPoly = 4;", "constexpr int kDecPoly = 2;")
+VARIANTS = {"poly0": [POLY0], "poly8": [POLY8], "poly2": [POLY2], "noexp": [NOEXP], "allpoly": [ALLPOLY], "nostore": [NOSTORE], "sb3": [SB3], "sb4": [SB4], "trace": TRACE, "nopv": [PV], "noqk": [QK], "nosoft": [SOFT], "streamonly": [PV, QK, SOFT], "narrowF2": [F2],
             "narrowF4": [F4, F4D]}
 
 
