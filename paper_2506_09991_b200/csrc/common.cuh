@@ -213,7 +213,9 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // 1.5 * 2^23 magic add, 2^f by a degree-3 minimax polynomial on [-0.5, 0.5] (relative error
 // 1.1e-4, below bf16's rounding of P), j added into the exponent field.
 __device__ __forceinline__ float2 poly_exp2x2(float2 x) {
-  x = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));  // keeps j + exponent(p) >= 0
+  // [-126, 64]: keeps j + exponent(p) inside the exponent field (an unclamped x >= 128 wraps into the
+  // sign bit and would hide a large score from the callers' softmax sum guards)
+  x = make_float2(fminf(fmaxf(x.x, -126.f), 64.f), fminf(fmaxf(x.y, -126.f), 64.f));
   const float2 t = __fadd2_rn(x, make_float2(12582912.f, 12582912.f));
   const float2 j = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));
   const float2 f = __ffma2_rn(j, make_float2(-1.f, -1.f), x);

@@ -21,12 +21,17 @@ def mv():
 class Req:
     """One request: shared prefix, fork into branches, per-branch private tokens, one decode step."""
 
-    def __init__(self, mv, st, rows, seed, prefix, branches, branch_len, hkv, nested=None):
+    def __init__(self, mv, st, rows, seed, prefix, branches, branch_len, hkv, nested=None, spike=False):
         self.st, self.rows = st, rows
         dev = "cuda"
 
-        def add(h, n, pos0):
+        def add(h, n, pos0, private=False):
             k = sym_bf16(seed * 1000 + len(rows["k"]) * 7 + 1, (n, hkv, 128))
+            if spike and private:
+                # the middle key of a branch's private run scores ~260 log2 units above the rest of the
+                # branch's context (dims 124-127 barely rotate: theta ~1e-4 rad per position)
+                k[n // 2, :, :] = 0.0
+                k[n // 2, :, 124:] = 512.0
             v = sym_bf16(seed * 1000 + len(rows["k"]) * 7 + 2, (n, hkv, 128))
             pos = torch.arange(pos0, pos0 + n, dtype=torch.int32)
             st.append_many(h, torch.full((n,), 11, dtype=torch.int32, device=dev), pos.to(dev), 0, k.to(dev),
@@ -52,17 +57,17 @@ class Req:
                     self.ctx.append(cc)
                     self.qpos.append(prefix + nested[0] + branch_len - 1)
                 continue
-            c = ctx_root + (add(h, branch_len - 1, prefix) if branch_len > 1 else [])
+            c = ctx_root + (add(h, branch_len - 1, prefix, private=True) if branch_len > 1 else [])
             self.handles.append(h)
             self.ctx.append(c)
             self.qpos.append(prefix + branch_len - 1)
         self.root, self.ctx_root = root, ctx_root
 
 
-def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1):
+def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1, spike=False):
     st = mv.kv.PagedStore(num_pages=num_pages, layers=1, kv_heads=hkv)
     rows = {"k": [], "v": [], "pos": []}
-    reqs = [Req(mv, st, rows, seed + i, *spec, hkv=hkv) if len(spec) == 3 else
+    reqs = [Req(mv, st, rows, seed + i, *spec, hkv=hkv, spike=spike) if len(spec) == 3 else
             Req(mv, st, rows, seed + i, *spec[:3], hkv=hkv, nested=spec[3]) for i, spec in enumerate(reqs_spec)]
     handles = [h for r in reqs for h in r.handles]
     ctx = [c for r in reqs for c in r.ctx]
@@ -72,6 +77,8 @@ def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1):
     knew = sym_bf16(seed * 77 + 5, (n, hkv, 128))
     vnew = sym_bf16(seed * 77 + 6, (n, hkv, 128))
     q = sym_bf16(seed * 77 + 7, (n, hq, 128))
+    if spike:
+        q[:, :, 124:] = 1.0
     pos = torch.tensor(qpos, dtype=torch.int32)
     st.append(handles, torch.full((n,), 12, dtype=torch.int32, device="cuda"), pos.cuda(), 0, knew.cuda(),
               vnew.cuda())
@@ -99,6 +106,14 @@ def test_small_gqa(mv):
     assert err < TOL, err
     info = st.plan_info()
     assert info["unique_kv_tokens"] < info["naive_kv_tokens"]  # the prefix is read once
+
+
+def test_score_spike(mv):
+    """One key in the middle of every branch's private run dwarfs the rest of its context: the softmax
+    reference must move (sum guard) even on polynomial-exp2 columns; branch lengths 600..615 walk the key
+    across the columns of its block."""
+    err, _ = run_case(mv, [(700, 2, 600 + i) for i in range(16)], hq=8, hkv=1, num_pages=2048, spike=True)
+    assert err < TOL, err
 
 
 def test_ragged_unaligned_prefix(mv):

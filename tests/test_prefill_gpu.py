@@ -19,7 +19,7 @@ def mv():
     return m
 
 
-def run_prefill(mv, tokens, hq, hkv, rows=None, seed=3):
+def run_prefill(mv, tokens, hq, hkv, rows=None, seed=3, spike=None):
     """Device prefill (K1 intervals -> K3) against the oracle built from the tag stream alone: the oracle's
     own positions (dag.cpp:203-222 restated) and dense build_mask rows (dag.cpp:227-263), so a K1 bug cannot
     be certified by this test."""
@@ -27,6 +27,11 @@ def run_prefill(mv, tokens, hq, hkv, rows=None, seed=3):
     spec = mv.dag.build_visibility(tokens)
     q = sym_bf16(seed * 10 + 1, (n, hq, 128))
     k = sym_bf16(seed * 10 + 2, (n, hkv, 128))
+    if spike is not None:
+        # one key whose score dwarfs every other (dims 124-127 barely rotate: theta ~1e-4 rad per position)
+        q[:, :, 124:] = 1.0
+        k[spike, :, :] = 0.0
+        k[spike, :, 124:] = 512.0
     v = sym_bf16(seed * 10 + 3, (n, hkv, 128))
     out = mv.attention.prefill(q.cuda(), k.cuda(), v.cuda(), spec.positions, spec.excl, out_dtype=torch.float32)
     torch.cuda.synchronize()
@@ -45,6 +50,16 @@ def run_prefill(mv, tokens, hq, hkv, rows=None, seed=3):
 def test_t1_all_rows(mv, dag_golden):
     t1 = next(c for c in dag_golden if c["name"] == "fixture:t1.txt")
     err, _ = run_prefill(mv, t1["tokens"], hq=8, hkv=2)
+    assert err < TOL, err
+
+
+@pytest.mark.parametrize("spike", [142, 174, 190, 206])
+def test_score_spike(mv, dag_golden, spike):
+    """A key ~260 log2 units above every other score, in a later key tile than the row's first: the
+    softmax reference must move (sum guard) even when the key sits on a polynomial-exp2 column
+    (key % 64 in {14, 15, 30, 31, 46, 47, 62, 63}); rows that see it return its value row exactly."""
+    nested = next(c for c in dag_golden if c["name"] == "fixture:nested.txt")
+    err, _ = run_prefill(mv, nested["tokens"], hq=8, hkv=2, spike=spike)
     assert err < TOL, err
 
 
