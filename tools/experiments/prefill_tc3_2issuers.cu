@@ -37,8 +37,9 @@ constexpr int kT3 = 128;
 constexpr int kQB3 = 2;                // Q tiles (item i uses tile i % kQB3; 3 Q tiles + 2 K slots measured 3% slower)
 constexpr int kKSt3 = 5 - kQB3;        // K ring slots (Q tiles + K slots share 5 x 32 KiB)
 constexpr int kVSt3 = 2;
-constexpr int kThreads3 = 384;   // 12 warps: loader, MMA, 8 softmax, 2 Q rotators
-constexpr int kRotWarp0 = 10;
+constexpr int kThreads3 = 384;   // 12 warps: loader, Q.K^T issuer, 8 softmax, Q rotator, P.V issuer
+constexpr int kRotWarp0 = 10;  // one Q rotator warp
+constexpr int kPvWarp = 11;    // the P.V issuer
 constexpr int kHalf3 = kT3 * 128;  // SW128 half tile: 128 rows x 64 dims
 constexpr int kTile3 = 2 * kHalf3;
 constexpr int kOffQ3 = 0;  // two Q tiles: item i loads and rotates into tile i & 1
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
   if (smem != smem_raw3) __trap();  // no slack was allocated for alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar3);
   uint64_t* q_loaded = bars;             // [kQB3] raw Q tile landed (tx)
-  uint64_t* q_full = q_loaded + kQB3;    // [kQB3] Q tile rotated (2 rotator warps)
+  uint64_t* q_full = q_loaded + kQB3;    // [kQB3] Q tile rotated (rotator warp)
   uint64_t* q_empty = q_full + kQB3;     // [kQB3] MMA commit after the item's last Q.K^T
   uint64_t* k_full = q_empty + kQB3;     // [kKSt3]
   uint64_t* k_empty = k_full + kKSt3;    // [3]
@@ -133,8 +134,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
   uint64_t* o_fin = p_full + kSB;        // O final for the item
   uint64_t* o_empty = o_fin + 1;         // epilogue read O (256 threads)
   uint64_t* item_full = o_empty + 1;     // [2]
-  uint64_t* slot_empty = item_full + 2;  // [2] V lane + MMA + 8 softmax warps
-  static_assert(3 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 2 * kSB + 6 <= 32, "barrier block");
+  uint64_t* slot_empty = item_full + 2;  // [2] V lane, 2 MMA issuers, 8 softmax warps, the rotator
+  uint64_t* pv_done = slot_empty + 2;    // [3] P.V(g) completed: S buffer g % 3 may take Q.K^T(g + 3)
+  static_assert(3 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 3 * kSB + 6 <= 32, "barrier block");
   Item3* s_item = reinterpret_cast<Item3*>(smem + kOffBar3 + 256);  // after <= 32 barriers, 16 B aligned
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_item + 2);
   float* s_x = reinterpret_cast<float*>(smem + kOffX3);
@@ -143,18 +145,19 @@ __global__ void __launch_bounds__(kThreads3, 1)
   if (threadIdx.x == 0) {
     for (int b = 0; b < kQB3; ++b) {
       mbar_init(&q_loaded[b], 1);
-      mbar_init(&q_full[b], 2);
+      mbar_init(&q_full[b], 1);
       mbar_init(&q_empty[b], 1);
     }
     mbar_init(o_fin, 1);
     mbar_init(o_empty, 256);
     for (int b = 0; b < kSB; ++b) {
+      mbar_init(&pv_done[b], 1);
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 256);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&item_full[b], 1);
-      mbar_init(&slot_empty[b], 12);  // V lane, MMA, 8 softmax warps, 2 rotator warps
+      mbar_init(&slot_empty[b], 12);  // V lane, 2 MMA issuers, 8 softmax warps, the rotator warp
     }
     for (int s = 0; s < kKSt3; ++s) {
       mbar_init(&k_full[s], 1);
@@ -243,78 +246,72 @@ __global__ void __launch_bounds__(kThreads3, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    // The whole warp runs the issue loop converged (waits, descriptors: warp-uniform values the
-    // compiler keeps in uniform registers) and one elected lane issues.  The issuer shares its
-    // SMSP with two busy softmax warps, so every instruction per MMA costs issue slots: a
-    // lane-0-only loop needed ~11 per MMA (descriptor R2UR + a waterfall per asm) and issued an
-    // MMA only every ~100 cycles, under the 64 an M=128 N=128 K=16 MMA takes.
-    const uint64_t qd0 = tc::sw128_desc(smem_u32(smem + kOffQ3), 16, 1024);
-    const uint64_t kd0 = tc::sw128_desc(smem_u32(smem + kOffK3), 16, 1024);
-    const uint64_t vd0 = tc::sw128_desc(smem_u32(smem + kOffV3), kHalf3, 1024);
-    int g = 0;  // processed k tiles so far (K/V ring index, S buffer = g % 3)
-    auto qk = [&](uint64_t qd, int gg) {  // S(gg % 3) = Q . K(gg)^T
-      mbar_wait(&k_full[gg % kKSt3], (gg / kKSt3) & 1);
-      tc::fence_after();
-      const uint64_t kd = kd0 + (uint64_t)(((gg % kKSt3) * kTile3) >> 4);
-      const int b = gg % kSB;
-      if (tc::elect_one()) {
-        if (b == 0) qk3<0>(qd, kd);
-        else if (b == 1) qk3<1>(qd, kd);
-        else if (kSB > 2) qk3<2 % kSB>(qd, kd);
-        tc::mma_commit(&s_full[b]);
-        tc::mma_commit(&k_empty[gg % kKSt3]);
+    // ---------------- MMA issuers: warp 1 Q.K^T, warp 11 P.V ----------------
+    // One thread issues a tcgen05.mma only every ~90 cycles (mb_umma), more than the
+    // 64 cycles an M=128 N=128 K=16 MMA takes: with one issuer the tensor core idled ~30%.  The
+    // two streams (separate warps: two lanes of one warp serialise) only meet at the S buffers: Q.K^T(g + 3) reuses buffer g % 3 once P.V(g) has
+    // completed (pv_done), P.V(g) waits for P(g) (softmax) and V(g).
+    if (lane == 0) {
+      const uint64_t qd0 = tc::sw128_desc(smem_u32(smem + kOffQ3), 16, 1024);
+      const uint64_t kd0 = tc::sw128_desc(smem_u32(smem + kOffK3), 16, 1024);
+      int g = 0;  // processed k tiles so far (K ring index, S buffer = g % 3)
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        mbar_wait(&item_full[buf], (i >> 1) & 1);
+        const Item3 it = s_item[buf];
+        mbar_arrive(&slot_empty[buf]);
+        if (!it.valid) break;
+        const int qb = i % kQB3;
+        const uint64_t qd = qd0 + (uint64_t)((qb * kTile3) >> 4);
+        mbar_wait(&q_full[qb], (i / kQB3) & 1);  // rotated by warp 10 (generic -> async proxy fenced)
+        for (int j = 0; j < it.m; ++j, ++g) {
+          const int b = g % kSB;
+          if (g >= kSB) mbar_wait(&pv_done[b], ((g / kSB) - 1) & 1);  // P.V(g - 3) read P from buffer b
+          mbar_wait(&k_full[g % kKSt3], (g / kKSt3) & 1);
+          tc::fence_after();
+          const uint64_t kd = kd0 + (uint64_t)(((g % kKSt3) * kTile3) >> 4);
+          if (b == 0) qk3<0>(qd, kd);
+          else if (b == 1) qk3<1>(qd, kd);
+          else qk3<2 % kSB>(qd, kd);
+          tc::mma_commit(&s_full[b]);
+          tc::mma_commit(&k_empty[g % kKSt3]);
+        }
+        tc::mma_commit(&q_empty[qb]);
       }
-      __syncwarp();
-    };
-    for (int i = 0;; ++i) {
-      const int buf = i & 1;
-      mbar_wait(&item_full[buf], (i >> 1) & 1);
-      const Item3 it = s_item[buf];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&slot_empty[buf]);
-      if (!it.valid) break;
-      const int m = it.m;
-      const int qb = i % kQB3;
-      const uint64_t qd = qd0 + (uint64_t)((qb * kTile3) >> 4);
-      mbar_wait(&q_full[qb], (i / kQB3) & 1);  // rotated by warps 10-11 (generic -> async proxy fenced)
-      for (int u = 0; u < kSB && u < m; ++u) qk(qd, g + u);
-      if (m <= kSB) {
-        if (tc::elect_one()) tc::mma_commit(&q_empty[qb]);
-        __syncwarp();
-      }
-      for (int j = 0; j < m; ++j, ++g) {
-        mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
-        mbar_wait(&p_full[g % kSB], (g / kSB) & 1);
-        if (j == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue of item i-1 read O
-        tc::fence_after();
-        const uint64_t vd = vd0 + (uint64_t)(((g % kVSt3) * kTile3) >> 4);
-        const int b = g % kSB;
-        if (tc::elect_one()) {
+    }
+  } else if (warp == kPvWarp) {
+    if (lane == 0) {
+      const uint64_t vd0 = tc::sw128_desc(smem_u32(smem + kOffV3), kHalf3, 1024);
+      int g = 0;
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        mbar_wait(&item_full[buf], (i >> 1) & 1);
+        const Item3 it = s_item[buf];
+        mbar_arrive(&slot_empty[buf]);
+        if (!it.valid) break;
+        for (int j = 0; j < it.m; ++j, ++g) {
+          mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
+          mbar_wait(&p_full[g % kSB], (g / kSB) & 1);
+          if (j == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue of item i-1 read O
+          tc::fence_after();
+          const uint64_t vd = vd0 + (uint64_t)(((g % kVSt3) * kTile3) >> 4);
+          const int b = g % kSB;
           if (b == 0) pv3<0>(vd, j == 0);
           else if (b == 1) pv3<1>(vd, j == 0);
-          else if (kSB > 2) pv3<2 % kSB>(vd, j == 0);
+          else pv3<2 % kSB>(vd, j == 0);
           tc::mma_commit(&v_empty[g % kVSt3]);
+          tc::mma_commit(&pv_done[b]);
         }
-        __syncwarp();
-        if (j + kSB < m) {
-          qk(qd, g + kSB);  // S buffer g % 3 again: in order behind P.V(g)
-          if (j + kSB + 1 == m) {
-            if (tc::elect_one()) tc::mma_commit(&q_empty[qb]);
-            __syncwarp();
-          }
-        }
+        if (it.m == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);
+        tc::mma_commit(o_fin);
       }
-      if (m == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);
-      if (tc::elect_one()) tc::mma_commit(o_fin);
-      __syncwarp();
     }
-  } else if (warp >= kRotWarp0) {
+  } else if (warp == kRotWarp0) {
     // ---------------- Q rotators: interleaved RoPE of the raw Q tile, in place ----------------
     // thread = 16-byte chunk (4 dim pairs) of a row; SW128: chunk c of row r sits at c ^ (r & 7)
     // of the row's 128 B in half c >> 3.  Same fp32 arithmetic as the pre-pass (rope_cs values
     // from the per-row table), so rotated Q is bit-identical to rope_qk_kernel's.
-    const int rt = threadIdx.x - kRotWarp0 * 32;  // 0..63
+    const int rt = lane;
     for (int it_i = 0;; ++it_i) {
       const int buf = it_i & 1;
       mbar_wait(&item_full[buf], (it_i >> 1) & 1);
@@ -328,12 +325,12 @@ __global__ void __launch_bounds__(kThreads3, 1)
       // 32 chunks per thread in 4 batches of 8: all table loads of a batch are in flight together
       // (the table comes from L2; a light item's rotation is otherwise on the MMA's critical path)
       constexpr int kBatch = 8;
-      for (int b0 = 0; b0 < kT3 * 16 / 64; b0 += kBatch) {
+      for (int b0 = 0; b0 < kT3 * 16 / 32; b0 += kBatch) {
         float4 t01[kBatch], t23[kBatch];
         uint4* q4[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
-          const int ch = rt + 64 * (b0 + u);
+          const int ch = rt + 32 * (b0 + u);
           const int row = ch >> 4, c = ch & 15;
           const int grow = min(it.t * kT3 + row, P.n - 1);  // rows past n are zero-filled: any angle
           q4[u] = reinterpret_cast<uint4*>(qt + (c >> 3) * kHalf3 + row * 128 + (((c & 7) ^ (row & 7)) << 4));

@@ -45,16 +45,16 @@ constexpr int kOffQ3 = 0;  // two Q tiles: item i loads and rotates into tile i 
 constexpr int kOffK3 = kOffQ3 + kQB3 * kTile3;
 constexpr int kOffV3 = kOffK3 + kKSt3 * kTile3;
 constexpr int kOffBar3 = kOffV3 + kVSt3 * kTile3;
-constexpr int kOffX3 = kOffBar3 + 512;  // row max / sum exchange: [2 parity][2 WG][128 rows] f32
+constexpr int kOffX3 = kOffBar3 + 512;  // epilogue (m, l) exchange: [2 parity][128 rows] float2
 // no alignment slack: the dynamic shared memory base is 1024-aligned here (checked at entry)
-constexpr int kSmem3 = kOffX3 + 2 * 2 * 128 * 4;
+constexpr int kSmem3 = kOffX3 + 2 * 128 * 8;
 static_assert(kSmem3 <= 227 * 1024, "prefill v3 smem");
 constexpr uint32_t kIdQK3 = tc::idesc_bf16(128, 128, 0, 0);
 constexpr uint32_t kIdPV3 = tc::idesc_bf16(128, 128, 0, 1);
 constexpr float kLazy3 = 8.f;
 // TMEM columns: three S buffers (S(g) in buffer g % 3) and one O
-constexpr int kSB = 3;
-constexpr uint32_t kS0 = 0, kO0 = kSB * 128;
+constexpr int kSB = 2;  // S / P buffer per tile parity
+constexpr uint32_t kS0 = 0, kO0 = kSB * 128;  // O accumulator per tile parity at kO0 + parity * 128
 
 struct Tc3Params {
   const int32_t* excl;
@@ -83,10 +83,11 @@ __device__ __forceinline__ void qk3(uint64_t qd, uint64_t kd) {
   }
 }
 template <int B>
-__device__ __forceinline__ void pv3(uint64_t vd, bool first) {
+__device__ __forceinline__ void pv3(uint64_t vd, bool first) {  // O(B) += P(B) . V
 #pragma unroll
   for (int k = 0; k < 8; ++k)
-    tc::mma_ts(kO0, kS0 + B * 128 + k * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV3, (!first || k > 0) ? 1u : 0u);
+    tc::mma_ts(kO0 + B * 128, kS0 + B * 128 + k * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV3,
+               (!first || k > 0) ? 1u : 0u);
 }
 
 // every kPolyMod3-th score pair takes poly_exp2x2: 1 pair in 8 gave +2.5% on C3 (16 and 4..6 no better)
@@ -112,7 +113,7 @@ __device__ __forceinline__ bool pair_any(int q, bool pred) {
       : "memory");
   return out != 0;
 }
-constexpr float kSumLimit3 = 64.f * 256.f;  // a 64-column half's P mass before the reference must move
+constexpr float kSumLimit3 = 32.f * 256.f;  // a 32-column chunk's P mass before the reference must move
 
 __global__ void __launch_bounds__(kThreads3, 1)
     prefill_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
   uint64_t* v_full = k_empty + kKSt3;    // [2]
   uint64_t* v_empty = v_full + kVSt3;    // [2] MMA commit after P.V (also certifies O for the rescale)
   uint64_t* s_full = v_empty + kVSt3;    // [3] S buffer b written
-  uint64_t* p_full = s_full + kSB;       // [3] 256 softmax threads wrote P into S buffer b
+  uint64_t* p_full = s_full + kSB;       // [2] the 128 softmax threads of parity b wrote P into S buffer b
   uint64_t* o_fin = p_full + kSB;        // O final for the item
   uint64_t* o_empty = o_fin + 1;         // epilogue read O (256 threads)
   uint64_t* item_full = o_empty + 1;     // [2]
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
   static_assert(3 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 2 * kSB + 6 <= 32, "barrier block");
   Item3* s_item = reinterpret_cast<Item3*>(smem + kOffBar3 + 256);  // after <= 32 barriers, 16 B aligned
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_item + 2);
-  float* s_x = reinterpret_cast<float*>(smem + kOffX3);
+  float2* s_x = reinterpret_cast<float2*>(smem + kOffX3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -150,7 +151,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
     mbar_init(o_empty, 256);
     for (int b = 0; b < kSB; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 256);
+      mbar_init(&p_full[b], 128);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&item_full[b], 1);
@@ -244,70 +245,50 @@ __global__ void __launch_bounds__(kThreads3, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    // The whole warp runs the issue loop converged (waits, descriptors: warp-uniform values the
-    // compiler keeps in uniform registers) and one elected lane issues.  The issuer shares its
-    // SMSP with two busy softmax warps, so every instruction per MMA costs issue slots: a
-    // lane-0-only loop needed ~11 per MMA (descriptor R2UR + a waterfall per asm) and issued an
-    // MMA only every ~100 cycles, under the 64 an M=128 N=128 K=16 MMA takes.
-    const uint64_t qd0 = tc::sw128_desc(smem_u32(smem + kOffQ3), 16, 1024);
-    const uint64_t kd0 = tc::sw128_desc(smem_u32(smem + kOffK3), 16, 1024);
-    const uint64_t vd0 = tc::sw128_desc(smem_u32(smem + kOffV3), kHalf3, 1024);
-    int g = 0;  // processed k tiles so far (K/V ring index, S buffer = g % 3)
-    auto qk = [&](uint64_t qd, int gg) {  // S(gg % 3) = Q . K(gg)^T
-      mbar_wait(&k_full[gg % kKSt3], (gg / kKSt3) & 1);
-      tc::fence_after();
-      const uint64_t kd = kd0 + (uint64_t)(((gg % kKSt3) * kTile3) >> 4);
-      const int b = gg % kSB;
-      if (tc::elect_one()) {
+    if (lane == 0) {
+      const uint64_t qd0 = tc::sw128_desc(smem_u32(smem + kOffQ3), 16, 1024);
+      const uint64_t kd0 = tc::sw128_desc(smem_u32(smem + kOffK3), 16, 1024);
+      const uint64_t vd0 = tc::sw128_desc(smem_u32(smem + kOffV3), kHalf3, 1024);
+      int g = 0;  // processed k tiles so far (K/V ring index, S buffer = g % 3)
+      auto qk = [&](uint64_t qd, int gg) {  // S(gg % 3) = Q . K(gg)^T
+        mbar_wait(&k_full[gg % kKSt3], (gg / kKSt3) & 1);
+        tc::fence_after();
+        const uint64_t kd = kd0 + (uint64_t)(((gg % kKSt3) * kTile3) >> 4);
+        const int b = gg & 1;
         if (b == 0) qk3<0>(qd, kd);
-        else if (b == 1) qk3<1>(qd, kd);
-        else if (kSB > 2) qk3<2 % kSB>(qd, kd);
+        else qk3<1>(qd, kd);
         tc::mma_commit(&s_full[b]);
         tc::mma_commit(&k_empty[gg % kKSt3]);
-      }
-      __syncwarp();
-    };
-    for (int i = 0;; ++i) {
-      const int buf = i & 1;
-      mbar_wait(&item_full[buf], (i >> 1) & 1);
-      const Item3 it = s_item[buf];
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&slot_empty[buf]);
-      if (!it.valid) break;
-      const int m = it.m;
-      const int qb = i % kQB3;
-      const uint64_t qd = qd0 + (uint64_t)((qb * kTile3) >> 4);
-      mbar_wait(&q_full[qb], (i / kQB3) & 1);  // rotated by warps 10-11 (generic -> async proxy fenced)
-      for (int u = 0; u < kSB && u < m; ++u) qk(qd, g + u);
-      if (m <= kSB) {
-        if (tc::elect_one()) tc::mma_commit(&q_empty[qb]);
-        __syncwarp();
-      }
-      for (int j = 0; j < m; ++j, ++g) {
-        mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
-        mbar_wait(&p_full[g % kSB], (g / kSB) & 1);
-        if (j == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue of item i-1 read O
-        tc::fence_after();
-        const uint64_t vd = vd0 + (uint64_t)(((g % kVSt3) * kTile3) >> 4);
-        const int b = g % kSB;
-        if (tc::elect_one()) {
-          if (b == 0) pv3<0>(vd, j == 0);
-          else if (b == 1) pv3<1>(vd, j == 0);
-          else if (kSB > 2) pv3<2 % kSB>(vd, j == 0);
+      };
+      for (int i = 0;; ++i) {
+        const int buf = i & 1;
+        mbar_wait(&item_full[buf], (i >> 1) & 1);
+        const Item3 it = s_item[buf];
+        mbar_arrive(&slot_empty[buf]);
+        if (!it.valid) break;
+        const int m = it.m;
+        const int qb = i % kQB3;
+        const uint64_t qd = qd0 + (uint64_t)((qb * kTile3) >> 4);
+        mbar_wait(&q_full[qb], (i / kQB3) & 1);  // rotated by warps 10-11 (generic -> async proxy fenced)
+        for (int u = 0; u < 2 && u < m; ++u) qk(qd, g + u);
+        if (m <= 2) tc::mma_commit(&q_empty[qb]);
+        for (int j = 0; j < m; ++j, ++g) {
+          mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
+          mbar_wait(&p_full[g & 1], (g >> 1) & 1);
+          if (j == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue of item i-1 read both O
+          tc::fence_after();
+          const uint64_t vd = vd0 + (uint64_t)(((g % kVSt3) * kTile3) >> 4);
+          if (g & 1) pv3<1>(vd, j < 2);  // the first tile of each parity starts its O
+          else pv3<0>(vd, j < 2);
           tc::mma_commit(&v_empty[g % kVSt3]);
-        }
-        __syncwarp();
-        if (j + kSB < m) {
-          qk(qd, g + kSB);  // S buffer g % 3 again: in order behind P.V(g)
-          if (j + kSB + 1 == m) {
-            if (tc::elect_one()) tc::mma_commit(&q_empty[qb]);
-            __syncwarp();
+          if (j + 2 < m) {
+            qk(qd, g + 2);  // S buffer g & 1 again: in order behind P.V(g)
+            if (j + 3 == m) tc::mma_commit(&q_empty[qb]);
           }
         }
+        if (m == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);
+        tc::mma_commit(o_fin);
       }
-      if (m == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);
-      if (tc::elect_one()) tc::mma_commit(o_fin);
-      __syncwarp();
     }
   } else if (warp >= kRotWarp0) {
     // ---------------- Q rotators: interleaved RoPE of the raw Q tile, in place ----------------
@@ -360,12 +341,16 @@ __global__ void __launch_bounds__(kThreads3, 1)
       if (lane == 0) mbar_arrive(&q_full[qb]);
     }
   } else {
-    // ---------------- softmax: warps 2-5 columns 0-63, warps 6-9 columns 64-127 ----------------
-    const int c = (warp - 2) >> 2;      // column half
+    // ---------------- softmax: warps 2-5 even tiles, warps 6-9 odd tiles ----------------
+    // Thread = row = TMEM lane, all 128 columns of its parity's tiles, 32 columns at a time.  The two
+    // warps of an SMSP (same lane quarter) work on different tiles, so one's exponentials overlap
+    // the other's TMEM traffic and barrier waits; each parity keeps its own reference / sum / O.
+    const int par = (warp - 2) >> 2;    // tile parity (global tile counter g & 1)
     const int quarter = warp & 3;       // TMEM lane quarter
     const int r = quarter * 32 + lane;  // row within the tile
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    int g = 0;
+    const uint32_t s_col = lane_base + kS0 + par * 128, o_col = lane_base + kO0 + par * 128;
+    int g = 0;  // global tile counter at the start of the item
     for (int it_i = 0;; ++it_i) {
       const int buf = it_i & 1;
       mbar_wait(&item_full[buf], (it_i >> 1) & 1);
@@ -374,6 +359,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       if (lane == 0) mbar_arrive(&slot_empty[buf]);
       if (!it.valid) break;
       const int i = it.t * kT3 + r;  // sequence row
+      const bool row_ok = i < P.n;
       const int2* exr = reinterpret_cast<const int2*>(P.excl) + (size_t)min(i, P.n - 1) * P.D;
       // the row's exclusion intervals, in registers for the whole item (partial tiles only use them)
       int2 exv[8];
@@ -381,59 +367,59 @@ __global__ void __launch_bounds__(kThreads3, 1)
       for (int q = 0; q < 8; ++q) exv[q] = q < P.D ? __ldg(exr + q) : make_int2(0, 0);
       const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
       const int sh = 20 + 2 * (it.t & 1);
-      const uint32_t o_col = kO0 + c * 64;
       float m_ref = -INFINITY, l = 0.f;
-      // the list entry of the next tile is loaded one tile ahead (its L2 latency used to sit
-      // between releasing P and waiting for the next S)
-      int nx = it.e0;
-      for (int done = 0; done < it.m; ++done, ++g) {
-        int e = nx;
-        nx = done + 1 < it.m ? lst[done + 1] : 0;
+      int j = (par - g) & 1;  // this parity's first tile of the item
+      // the list entry of the next tile is loaded one tile ahead
+      int nx = j < it.m ? (j == 0 ? it.e0 : lst[j]) : 0;
+      for (; j < it.m; j += 2) {
+        const int gg = g + j;
+        const int e = nx;
+        nx = j + 2 < it.m ? lst[j + 2] : 0;
         const int j0 = (e & 0xFFFFF) * kT3;
         const int status = (e >> sh) & 3;
-        const uint32_t s_col = kS0 + (g % kSB) * 128;
-        mbar_wait(&s_full[g % kSB], (g / kSB) & 1);
-        tc::fence_after();
-        float v[64];
-        tc::tmem_ld32(lane_base + s_col + c * 64, v);
-        tc::tmem_ld32(lane_base + s_col + c * 64 + 32, v + 32);
-        tc::tmem_wait_ld();
+        // visible columns of this row in the tile (partial tiles): 4 x 32-column masks
+        uint32_t vm[4] = {~0u, ~0u, ~0u, ~0u};
         if (status != 1) {
           const int lim = min(i, P.n - 1) - j0;  // last visible column
-          uint32_t vm[2];
 #pragma unroll
-          for (int w = 0; w < 2; ++w) vm[w] = bit_range3(0, lim + 1 - (2 * c + w) * 32);
+          for (int w = 0; w < 4; ++w) vm[w] = bit_range3(0, lim + 1 - w * 32);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             if (q >= P.D) break;
             const int a = exv[q].x - j0, b = exv[q].y - j0;
             if (a >= kT3 || b <= 0) continue;
 #pragma unroll
-            for (int w = 0; w < 2; ++w) vm[w] &= ~bit_range3(a - (2 * c + w) * 32, b - (2 * c + w) * 32);
+            for (int w = 0; w < 4; ++w) vm[w] &= ~bit_range3(a - w * 32, b - w * 32);
           }
           for (int q = 8; q < P.D; ++q) {  // nesting deeper than 8: the rest from memory
             const int2 e2 = __ldg(exr + q);
             const int a = e2.x - j0, b = e2.y - j0;
             if (a >= kT3 || b <= 0) continue;
 #pragma unroll
-            for (int w = 0; w < 2; ++w) vm[w] &= ~bit_range3(a - (2 * c + w) * 32, b - (2 * c + w) * 32);
-          }
-#pragma unroll
-          for (int k = 0; k < 64; k += 2) {
-            const uint32_t mm = vm[k >> 5] >> (k & 31);
-            v[k] = (mm & 1u) ? v[k] : -INFINITY;
-            v[k + 1] = (mm & 2u) ? v[k + 1] : -INFINITY;
+            for (int w = 0; w < 4; ++w) vm[w] &= ~bit_range3(a - w * 32, b - w * 32);
           }
         }
-        uint32_t pk[32];
+        const bool partial = status != 1;
+        auto mask = [&](float* x, int w) {
+          if (partial) {
+            // select, not index: a runtime w (slow path) must not push vm[] to local memory
+            const uint32_t mw = w == 0 ? vm[0] : w == 1 ? vm[1] : w == 2 ? vm[2] : vm[3];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) x[k] = ((mw >> k) & 1u) ? x[k] : -INFINITY;
+          }
+        };
+        mbar_wait(&s_full[par], (gg >> 1) & 1);
+        tc::fence_after();
+        float vc[32], vn[32];
+        uint32_t pk[16];
         auto exps = [&](float mu) {
           // FFMA2 scale, 1 pair in kPolyMod3 on the FMA pipe (relieves the 16/clk/SM MUFU), FADD2 sums
           const float2 sc2 = make_float2(P.scale_log2, P.scale_log2), nmu2 = make_float2(-mu, -mu);
           float2 la = make_float2(0.f, 0.f), lb = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int u = 0; u < 32; ++u) {
-            const float2 xy = __ffma2_rn(make_float2(v[2 * u], v[2 * u + 1]), sc2, nmu2);
-            const float2 pp = (kPolyMod3 > 0 && (u & 15) % kPolyMod3 == kPolyMod3 - 1)
+          for (int u = 0; u < 16; ++u) {
+            const float2 xy = __ffma2_rn(make_float2(vc[2 * u], vc[2 * u + 1]), sc2, nmu2);
+            const float2 pp = (kPolyMod3 > 0 && u % kPolyMod3 == kPolyMod3 - 1)
                                   ? poly_exp2x2(xy)
                                   : make_float2(fast_exp2(xy.x), fast_exp2(xy.y));
             if (u & 1) lb = __fadd2_rn(lb, pp);
@@ -442,83 +428,132 @@ __global__ void __launch_bounds__(kThreads3, 1)
           }
           return (la.x + lb.x) + (la.y + lb.y);
         };
-        // Fast path (no per-tile row max): exponentiate against the row's reference; it moves only on
-        // the item's first tile or when this half's mass exceeds kSumLimit3 (every P stays <= 2^14,
-        // exact enough in bf16 and far from fp32 overflow).  The OR-reduced pair barrier also orders
-        // both warps' S loads before either writes P into the S columns.
-        bool need = m_ref == -INFINITY;
-        float ls = 0.f;
-        if (!__any_sync(0xffffffffu, need)) {
-          ls = exps(m_ref);
-          need = !(ls <= kSumLimit3);  // also catches inf / NaN sums
-        }
-        if (pair_any(quarter, need)) {
-          // slow path: the row max over both column halves, move the reference, rescale O
-          float mx0 = -INFINITY, mx1 = -INFINITY;
+        float ls = 0.f;     // this tile's P mass (against m_ref)
+        bool dead = false;  // no visible column left in this tile for the row
+        tc::tmem_ld32(s_col, vc);
+        tc::tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 64; k += 2) {
-            mx0 = fmaxf(mx0, v[k]);
-            mx1 = fmaxf(mx1, v[k + 1]);
-          }
-          float* xs = s_x + (g & 1) * 256;
-          xs[c * 128 + r] = fmaxf(mx0, mx1);
-          pair_sync(quarter);
-          const float mx = fmaxf(xs[r], xs[128 + r]) * P.scale_log2;
-          const bool move = m_ref == -INFINITY || mx > m_ref + kLazy3;
-          const float nref = move ? fmaxf(m_ref, mx) : m_ref;
-          const float alpha = move && m_ref != -INFINITY ? fast_exp2(m_ref - nref) : 1.f;
-          if (done >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
-            // O holds P.V of the previous tile (g - 1): its V slot's release certifies it
-            mbar_wait(&v_empty[(g - 1) % kVSt3], ((g - 1) / kVSt3) & 1);
-            tc::fence_after();
-#pragma unroll 1
-            for (int cc = 0; cc < 2; ++cc) {
-              float o[32];
-              tc::tmem_ld32(lane_base + o_col + cc * 32, o);
-              tc::tmem_wait_ld();
+        for (int w = 0; w < 4; ++w) {
+          if (w < 3) tc::tmem_ld32(s_col + (w + 1) * 32, vn);  // in flight while chunk w is processed
+          mask(vc, w);
+          // Fast path: exponentiate against the row's reference; it moves only on the parity's first
+          // tile or when a chunk's mass exceeds kSumLimit3 (every P stays <= 2^13, exact enough in
+          // bf16 and far from fp32 overflow).  No per-tile row max.
+          float lc = exps(m_ref == -INFINITY ? 0.f : m_ref);
+          const bool need = row_ok && !dead && (m_ref == -INFINITY || !(lc <= kSumLimit3));
+          if (__any_sync(0xffffffffu, need)) {
+            // slow path: the row max over the chunks not yet exponentiated (S columns >= 32w are
+            // intact: P of chunks < w sits in columns < 16w), move the reference, rescale the P
+            // already stored, the tile's mass, l and this parity's O
+            tc::tmem_wait_ld();
+            float mx = -INFINITY;
 #pragma unroll
-              for (int k = 0; k < 32; ++k) o[k] *= alpha;
-              tc::tmem_st32(lane_base + o_col + cc * 32, o);
+            for (int k = 0; k < 32; ++k) mx = fmaxf(mx, vc[k]);
+            if (w < 3) {
+              mask(vn, w + 1);
+#pragma unroll
+              for (int k = 0; k < 32; ++k) mx = fmaxf(mx, vn[k]);
             }
+#pragma unroll 1
+            for (int w2 = w + 2; w2 < 4; ++w2) {
+              float t[32];
+              tc::tmem_ld32(s_col + w2 * 32, t);
+              tc::tmem_wait_ld();
+              mask(t, w2);
+#pragma unroll
+              for (int k = 0; k < 32; ++k) mx = fmaxf(mx, t[k]);
+            }
+            mx *= P.scale_log2;
+            const bool move = row_ok && !dead && (m_ref == -INFINITY ? mx != -INFINITY : mx > m_ref + kLazy3);
+            const float alpha = move && m_ref != -INFINITY ? fast_exp2(m_ref - mx) : 1.f;
+            if (__any_sync(0xffffffffu, alpha != 1.f)) {
+              if (w > 0) {
+                tc::tmem_wait_st();
+#pragma unroll 1
+                for (int w2 = 0; w2 < w; ++w2) {
+                  float t[16];
+                  tc::tmem_ldN<16>(s_col + w2 * 16, t);
+                  tc::tmem_wait_ld();
+                  uint32_t u16[16];
+#pragma unroll
+                  for (int k = 0; k < 16; ++k) {
+                    const uint32_t b = __float_as_uint(t[k]);
+                    u16[k] = pack_bf16(__uint_as_float(b << 16) * alpha, __uint_as_float(b & 0xFFFF0000u) * alpha);
+                  }
+                  tc::tmem_stNu<16>(s_col + w2 * 16, u16);
+                }
+              }
+              if (j >= 2) {
+                // O holds P.V of this parity's previous tile (gg - 2): its V slot's release certifies it
+                mbar_wait(&v_empty[(gg - 2) % kVSt3], ((gg - 2) / kVSt3) & 1);
+                tc::fence_after();
+#pragma unroll 1
+                for (int cc = 0; cc < 4; ++cc) {
+                  float o[32];
+                  tc::tmem_ld32(o_col + cc * 32, o);
+                  tc::tmem_wait_ld();
+#pragma unroll
+                  for (int k = 0; k < 32; ++k) o[k] *= alpha;
+                  tc::tmem_st32(o_col + cc * 32, o);
+                }
+              }
+            }
+            if (move) m_ref = mx;
+            l *= alpha;
+            ls *= alpha;
+            dead = dead || mx == -INFINITY;
+            lc = exps(m_ref == -INFINITY ? 0.f : m_ref);
           }
-          l *= alpha;
-          m_ref = nref;
-          ls = exps(m_ref == -INFINITY ? 0.f : m_ref);
+          // P of chunk w -> packed columns [16w, 16w + 16) of the S buffer (S columns already read)
+          tc::tmem_stNu<16>(s_col + w * 16, pk);
+          ls += lc;
+          if (w < 3) {
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int k = 0; k < 32; ++k) vc[k] = vn[k];
+          }
         }
-        // P for k tokens [64c, 64c + 64) -> packed columns [32c, 32c + 32) of the S buffer
-        tc::tmem_stNu<16>(lane_base + s_col + c * 32, pk);
-        tc::tmem_stNu<16>(lane_base + s_col + c * 32 + 16, pk + 16);
         l += ls;
         tc::tmem_wait_st();
         tc::fence_before();
-        mbar_arrive(&p_full[g % kSB]);
+        mbar_arrive(&p_full[par]);
       }
-      // epilogue: row sum over both halves, O / l for this warp's 64 dims
+      g += it.m;
+      // epilogue: combine the two parities' (reference, sum, O); this warp writes dims [64 par, 64 par + 64)
       mbar_wait(o_fin, it_i & 1);
       tc::fence_after();
-      float* ls = s_x + (g & 1) * 256;  // the next tile's max slot: free until this pair syncs again
-      ls[c * 128 + r] = l;
+      s_x[par * 128 + r] = make_float2(m_ref, l);
       pair_sync(quarter);
-      const float lt = ls[r] + ls[128 + r];
-      pair_sync(quarter);  // both read before the slot is reused by the next tile's max
+      const float2 ot = s_x[(par ^ 1) * 128 + r];
+      pair_sync(quarter);  // both read before the next item's exchange
+      const float mm = fmaxf(m_ref, ot.x);
+      const float a_me = m_ref == -INFINITY ? 0.f : fast_exp2(m_ref - mm);
+      const float a_ot = ot.x == -INFINITY ? 0.f : fast_exp2(ot.x - mm);
+      const float lt = l * a_me + ot.y * a_ot;
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      const float a0 = (par == 0 ? a_me : a_ot) * inv, a1 = (par == 0 ? a_ot : a_me) * inv;
 #pragma unroll 1
       for (int cc = 0; cc < 2; ++cc) {
-        float o[32];
-        tc::tmem_ld32(lane_base + o_col + cc * 32, o);
+        float o0[32], o1[32];
+        tc::tmem_ld32(lane_base + kO0 + par * 64 + cc * 32, o0);
+        tc::tmem_ld32(lane_base + kO0 + 128 + par * 64 + cc * 32, o1);
         tc::tmem_wait_ld();
-        if (i < P.n) {
-          const int d0 = c * 64 + cc * 32;
+        // a parity without tiles in this item (or a row it never saw) has a = 0 and an O that was
+        // not written for this item: select, never multiply, so stale values cannot leak
+#pragma unroll
+        for (int k = 0; k < 32; ++k) o0[k] = (a0 != 0.f ? o0[k] * a0 : 0.f) + (a1 != 0.f ? o1[k] * a1 : 0.f);
+        if (row_ok) {
+          const int d0 = par * 64 + cc * 32;
           if (P.out_f32) {
             float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + it.h) * kHeadDim + d0);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
+            for (int e = 0; e < 8; ++e) dst[e] = make_float4(o0[4 * e], o0[4 * e + 1], o0[4 * e + 2], o0[4 * e + 3]);
           } else {
             uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + ((size_t)i * P.hq + it.h) * kHeadDim + d0);
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-              dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
-                                  pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
+              dst[e] = make_uint4(pack_bf16(o0[8 * e], o0[8 * e + 1]), pack_bf16(o0[8 * e + 2], o0[8 * e + 3]),
+                                  pack_bf16(o0[8 * e + 4], o0[8 * e + 5]), pack_bf16(o0[8 * e + 6], o0[8 * e + 7]));
           }
         }
       }
