@@ -491,26 +491,32 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
     }
   } else if (warp == kWarpQk) {
     // ---------------- QK issuer: Q -> TMEM per unit, S_g = Q . K_g^T per block ----------------
-    if (lane == 0) {
-      const uint64_t qdesc0 = tc::sw128_desc(smem_u32(smem + kOffQ), 16, 1024);
-      const uint64_t kdesc0 = tc::sw128_desc(smem_u32(ring), 16, 2048);
-      int g = 0;
-      for (int i = 0;; ++i) {
-        const int ub = i & 1;
-        mbar_wait(&item_full[ub], (i >> 1) & 1);
-        const WorkItem* si = &s_item[ub];
-        if (!si->valid) break;
-        const int nblk = (si->n_entries + kBlkPages - 1) / kBlkPages;
-        tc::fence_after();
-        // the unit's Q tile smem -> TMEM (ordered after the previous unit's QK MMAs)
+    // Both issuers run converged with one elected lane issuing (prefill_tc3.cu: warp-uniform
+    // descriptors stay in uniform registers, no per-MMA waterfall on an SMSP shared with softmax warps).
+    const uint64_t qdesc0 = tc::sw128_desc(smem_u32(smem + kOffQ), 16, 1024);
+    const uint64_t kdesc0 = tc::sw128_desc(smem_u32(ring), 16, 2048);
+    int g = 0;
+    for (int i = 0;; ++i) {
+      const int ub = i & 1;
+      mbar_wait(&item_full[ub], (i >> 1) & 1);
+      const WorkItem* si = &s_item[ub];
+      const int valid = si->valid, n_ent = si->n_entries;
+      if (!valid) break;
+      const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
+      tc::fence_after();
+      // the unit's Q tile smem -> TMEM (ordered after the previous unit's QK MMAs)
+      if (tc::elect_one()) {
         issue_q_copy(qdesc0);
         tc::mma_commit(q_free);
-        for (int blk = 0; blk < nblk; ++blk, ++g) {
-          const int sb = g % kSBufs, sl = g % kKSlots;
-          if (g >= kSBufs) mbar_wait(&pv_done[sb], ((g - kSBufs) / kSBufs) & 1);  // P(g - kSBufs) consumed
-          mbar_wait(&kfull[sl], (g / kKSlots) & 1);
-          tc::fence_after();
-          const uint64_t kd = kdesc0 + (uint64_t)(sl * (kSlotBytes >> 4));
+      }
+      __syncwarp();
+      for (int blk = 0; blk < nblk; ++blk, ++g) {
+        const int sb = g % kSBufs, sl = g % kKSlots;
+        if (g >= kSBufs) mbar_wait(&pv_done[sb], ((g - kSBufs) / kSBufs) & 1);  // P(g - kSBufs) consumed
+        mbar_wait(&kfull[sl], (g / kKSlots) & 1);
+        tc::fence_after();
+        const uint64_t kd = kdesc0 + (uint64_t)(sl * (kSlotBytes >> 4));
+        if (tc::elect_one()) {
           switch (sb) {
             case 0: issue_qk_mmas<0>(kd); break;
             case 1: issue_qk_mmas<1>(kd); break;
@@ -521,31 +527,34 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           tc::mma_commit(&s_full[sb]);
           tc::mma_commit(&kempty[sl]);
         }
-        tc::mma_commit(&slot_empty[ub]);  // Q smem tile consumed
+        __syncwarp();
       }
+      if (tc::elect_one()) tc::mma_commit(&slot_empty[ub]);  // Q smem tile consumed
+      __syncwarp();
     }
   } else if (warp == kWarpPv) {
     // ---------------- PV issuer: O_par += P_g . V_g per block ----------------
-    if (lane == 0) {
-      const uint64_t vdesc0 = tc::sw128_desc(smem_u32(smem + kOffVRing), 1024, 2048);
-      int g = 0;
-      for (int i = 0;; ++i) {
-        const int ub = i & 1;
-        mbar_wait(&item_full[ub], (i >> 1) & 1);
-        const WorkItem* si = &s_item[ub];
-        const int valid = si->valid, n_ent = si->n_entries;
-        mbar_arrive(&slot_empty[ub]);  // header read
-        if (!valid) break;
-        const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
-        for (int blk = 0; blk < nblk; ++blk, ++g) {
-          const int sb = g % kSBufs;
-          mbar_wait(&p_full[sb], (g / kSBufs) & 1);
-          if (blk == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue drained O
-          mbar_wait(&vfull[g % kVSlots], (g / kVSlots) & 1);
-          tc::fence_after();
-          const uint64_t vd = vdesc0 + (uint64_t)((g % kVSlots) * (kSlotBytes >> 4));
-          const int np = n_ent - blk * kBlkPages;
-          const uint32_t acc0 = blk > 0 ? 1u : 0u;  // the unit's first block opens O
+    const uint64_t vdesc0 = tc::sw128_desc(smem_u32(smem + kOffVRing), 1024, 2048);
+    int g = 0;
+    for (int i = 0;; ++i) {
+      const int ub = i & 1;
+      mbar_wait(&item_full[ub], (i >> 1) & 1);
+      const WorkItem* si = &s_item[ub];
+      const int valid = si->valid, n_ent = si->n_entries;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&slot_empty[ub]);  // header read
+      if (!valid) break;
+      const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
+      for (int blk = 0; blk < nblk; ++blk, ++g) {
+        const int sb = g % kSBufs;
+        mbar_wait(&p_full[sb], (g / kSBufs) & 1);
+        if (blk == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue drained O
+        mbar_wait(&vfull[g % kVSlots], (g / kVSlots) & 1);
+        tc::fence_after();
+        const uint64_t vd = vdesc0 + (uint64_t)((g % kVSlots) * (kSlotBytes >> 4));
+        const int np = n_ent - blk * kBlkPages;
+        const uint32_t acc0 = blk > 0 ? 1u : 0u;  // the unit's first block opens O
+        if (tc::elect_one()) {
           switch (sb) {
             case 0: issue_pv_mmas<0>(vd, np, acc0); break;
             case 1: issue_pv_mmas<1>(vd, np, acc0); break;
@@ -557,6 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           tc::mma_commit(&pv_done[sb]);
           if (blk == nblk - 1) tc::mma_commit(o_full);
         }
+        __syncwarp();
       }
     }
   } else if (warp >= 4 && warp < 12) {
