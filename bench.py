@@ -46,6 +46,24 @@ C2_TEXT = ("configs[1] x R requests per GPU: 40q/8kv heads, d128, bf16, 4K share
            "tokens (+1 per step), KV page 16")
 
 
+def static_config(args, world):
+    """The workload description both arms print (identical `config` objects: what was measured, not how it
+    went; run-time facts such as the mean context or the host enqueue time go under `run`)."""
+    heads_mode = args.shard == "heads"
+    wl = WORKLOADS[args.workload]
+    if heads_mode:
+        R, hkv_l = wl.get("total_requests", args.requests), HKV // world
+    else:
+        R, hkv_l = wl.get("total_requests", args.requests * world) // world, HKV
+    return {"workload": C2_TEXT if args.workload == "c2" else "configs[3] (see c4_decode)",
+            "requests_per_gpu": R, "branches_per_gpu": R * wl.get("branches", 8),
+            "l2": "inputs 0.8+ GB > L2 (no flush)",
+            "parallelism": (f"kv-head groups x{world} + NCCL all-gather of outputs" if heads_mode
+                            else f"requests x{world}, no collective"),
+            "kv_heads_per_gpu": hkv_l,
+            "step": "append 1 token K/V per branch (RoPE fused) + cascade decode attention"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -314,8 +332,9 @@ def run_reference(args):
             "steps": steps_run, "warmup": warm_run, "steps_requested": args.steps, "warmup_requested": args.warmup,
             "ms_per_step": 1e3 * (os.cpu_count() or 1) / cpu["value"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "configs[1]: 4K shared prefix, 8 branches x 1K, one request sampled; the reference "
-                                   "has no GQA, so 40 heads x 128 MHA", "sample": cpu["sample"]},
+            "config": static_config(args, world),
+            "run": {"reference": "the reference's own CPU path on this host (no GQA in the reference: 40 heads x 128 "
+                                 "MHA), one request sampled", "sample": cpu["sample"]},
             "cpu_baseline": cpu,
             "e2e": {"value": cpu["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -678,13 +697,10 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms"], "higher_is_better": True,
             "scaling": "strong" if (args.workload == "c4" or heads_mode) else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": C2_TEXT if args.workload == "c2" else "configs[3] (see c4_decode)",
-                       "requests_per_gpu": r["R"], "branches_per_gpu": r["n"], "l2": "inputs 0.8+ GB > L2 (no flush)",
-                       "mean_kv_tokens_per_step": r["kv_tokens"], "host_enqueue_ms_per_step": r["host_ms"],
-                       "parallelism": (f"kv-head groups x{world} + NCCL all-gather of outputs" if heads_mode
-                                       else f"requests x{world}, no collective"),
-                       "kv_heads_per_gpu": r["hkv_l"], "allgather_ms_per_step": r["ag_ms"] if heads_mode else None,
-                       "step": "append 1 token K/V per branch (RoPE fused) + cascade decode attention"},
+            "config": static_config(args, world),
+            "run": {"requests_per_gpu": r["R"], "branches_per_gpu": r["n"], "kv_heads_per_gpu": r["hkv_l"],
+                    "mean_kv_tokens_per_step": r["kv_tokens"], "host_enqueue_ms_per_step": r["host_ms"],
+                    "allgather_ms_per_step": r["ag_ms"] if heads_mode else None},
             "e2e": {"value": r["tokens_per_step"] / (r["e2e_ms"] / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
