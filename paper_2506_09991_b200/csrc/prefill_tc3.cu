@@ -406,8 +406,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             if (q >= P.D) break;
+            // branch-free: bit_range3 clamps, so an interval outside this tile clears nothing
             const int a = exv[q].x - j0, b = exv[q].y - j0;
-            if (a >= kT3 || b <= 0) continue;
 #pragma unroll
             for (int w = 0; w < 2; ++w) vm[w] &= ~bit_range3(a - (2 * c + w) * 32, b - (2 * c + w) * 32);
           }
