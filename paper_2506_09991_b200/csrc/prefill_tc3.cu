@@ -91,6 +91,9 @@ __device__ __forceinline__ void pv3(uint64_t vd, bool first) {
 
 // every kPolyMod3-th score pair takes poly_exp2x2: 1 pair in 8 gave +2.5% on C3 (16 and 4..6 no better)
 constexpr int kPolyMod3 = 8;
+// exclusion intervals a softmax thread keeps in registers for its row (nesting depth); deeper ones
+// are read from L1 on partial tiles
+constexpr int kExvRegs = 4;
 
 __device__ __forceinline__ uint32_t bit_range3(int lo, int hi) {
   lo = max(lo, 0);
@@ -376,9 +379,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const int i = it.t * kT3 + r;  // sequence row
       const int2* exr = reinterpret_cast<const int2*>(P.excl) + (size_t)min(i, P.n - 1) * P.D;
       // the row's exclusion intervals, in registers for the whole item (partial tiles only use them)
-      int2 exv[8];
+      int2 exv[kExvRegs];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) exv[q] = q < P.D ? __ldg(exr + q) : make_int2(0, 0);
+      for (int q = 0; q < kExvRegs; ++q) exv[q] = q < P.D ? __ldg(exr + q) : make_int2(0, 0);
       const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
       const int sh = 20 + 2 * (it.t & 1);
       const uint32_t o_col = kO0 + c * 64;
@@ -404,17 +407,16 @@ __global__ void __launch_bounds__(kThreads3, 1)
 #pragma unroll
           for (int w = 0; w < 2; ++w) vm[w] = bit_range3(0, lim + 1 - (2 * c + w) * 32);
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
+          for (int q = 0; q < kExvRegs; ++q) {
             if (q >= P.D) break;
             // branch-free: bit_range3 clamps, so an interval outside this tile clears nothing
             const int a = exv[q].x - j0, b = exv[q].y - j0;
 #pragma unroll
             for (int w = 0; w < 2; ++w) vm[w] &= ~bit_range3(a - (2 * c + w) * 32, b - (2 * c + w) * 32);
           }
-          for (int q = 8; q < P.D; ++q) {  // nesting deeper than 8: the rest from memory
+          for (int q = kExvRegs; q < P.D; ++q) {  // deeper nesting: the rest from memory (L1)
             const int2 e2 = __ldg(exr + q);
             const int a = e2.x - j0, b = e2.y - j0;
-            if (a >= kT3 || b <= 0) continue;
 #pragma unroll
             for (int w = 0; w < 2; ++w) vm[w] &= ~bit_range3(a - (2 * c + w) * 32, b - (2 * c + w) * 32);
           }
