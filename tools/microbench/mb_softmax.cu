@@ -186,6 +186,86 @@ __global__ void __launch_bounds__(512, 1) bench(float* out, long long* cyc, floa
   (void)nw;
 }
 
+
+// Full-row softmax step (FA4-style: one warp per lane quarter holds whole rows): each warp
+// exponentiates its 32 rows x 128 columns per step as two 64-column halves (load, exponentials,
+// P store), no cross-warp barrier.  W warps: W / 4 independent rows sets per SMSP.
+template <int POLY>
+__global__ void __launch_bounds__(512, 1) bench_fullrow(float* out, long long* cyc, float scale) {
+  __shared__ uint32_t slot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) tc::tmem_alloc(&slot, 512);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const int quarter = warp & 3, grp = warp >> 2;  // grp: which S tile (one per warp on the SMSP)
+  const uint32_t base = slot + ((uint32_t)(quarter * 32) << 16) + grp * 128;
+  {
+    float init[32];
+#pragma unroll
+    for (int k = 0; k < 32; ++k) init[k] = (lane * 7 + k * 13 % 29) * 0.01f - 1.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tc::tmem_st32(base + c * 32, init);
+    tc::tmem_wait_st();
+  }
+  __syncthreads();
+  float l = 0.f, m_ref = 0.5f;
+  long long t0 = clock64();
+  for (int it = 0; it < kIters; ++it) {
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      float v[64];
+      tc::tmem_ld32(base + h * 64, v);
+      tc::tmem_ld32(base + h * 64 + 32, v + 32);
+      tc::tmem_wait_ld();
+      uint32_t pk[32];
+      const float2 sc2 = make_float2(scale, scale), nmu2 = make_float2(-m_ref, -m_ref);
+      float2 la = make_float2(0.f, 0.f), lb = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const float2 xy = __ffma2_rn(make_float2(v[2 * u], v[2 * u + 1]), sc2, nmu2);
+        const float2 pp = (POLY && (u & 7) == 7) ? poly_exp2x2(xy) : make_float2(fast_exp2(xy.x), fast_exp2(xy.y));
+        if (u & 1) lb = __fadd2_rn(lb, pp);
+        else la = __fadd2_rn(la, pp);
+        pk[u] = pack_bf16(pp.x, pp.y);
+      }
+      const float ls = (la.x + lb.x) + (la.y + lb.y);
+      if (__any_sync(0xffffffffu, !(ls <= 16384.f))) m_ref += 1.f;
+      l += ls;
+      // P of this half -> packed columns [32h, 32h + 32) (S columns < 64h + 64, already read)
+      tc::tmem_stNu<16>(base + h * 32, pk);
+      tc::tmem_stNu<16>(base + h * 32 + 16, pk + 16);
+    }
+    tc::tmem_wait_st();
+  }
+  long long t1 = clock64();
+  if (lane == 0) cyc[warp] = t1 - t0;
+  out[threadIdx.x] = l;
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(slot, 512);
+}
+
+template <int POLY>
+void run_fullrow(int warps, const char* name) {
+  float* out;
+  long long* cyc;
+  cudaMalloc(&out, 512 * 4);
+  cudaMalloc(&cyc, 32 * 8);
+  bench_fullrow<POLY><<<1, warps * 32>>>(out, cyc, 0.1275f);
+  bench_fullrow<POLY><<<1, warps * 32>>>(out, cyc, 0.1275f);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[32];
+  cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+  long long mx = 0;
+  for (int w = 0; w < warps; ++w) mx = h[w] > mx ? h[w] : mx;
+  // per SMSP: warps/4 warps x 4096 elements per step
+  printf("%-34s warps/SMSP=%d  %7.1f cyc/step(tile per warp)  %5.2f elem/cyc/SMSP  %s\n", name, warps / 4,
+         (double)mx / kIters, (warps / 4) * 4096.0 / ((double)mx / kIters), cudaGetErrorString(e));
+  cudaFree(out);
+  cudaFree(cyc);
+}
+
 template <int MODE>
 void run(int warps, const char* name) {
   float* out;
@@ -214,6 +294,9 @@ void run(int warps, const char* name) {
 }
 
 int main() {
+  run_fullrow<1>(4, "full rows, 1 warp/SMSP, poly");
+  run_fullrow<1>(8, "full rows, 2 warps/SMSP, poly");
+  run_fullrow<0>(4, "full rows, 1 warp/SMSP, MUFU only");
   run<12 | 2048>(8, "regs softmax + pipelined MMA");
   run<14 | 2048>(8, "TMEM softmax + pipelined MMA");
   run<15 | 2048>(8, "TMEM softmax pair bar + pipelined MMA");
