@@ -119,7 +119,8 @@ constexpr float kSumLimit3 = 64.f * 256.f;  // a 64-column half's P mass before 
 
 __global__ void __launch_bounds__(kThreads3, 1)
     prefill_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
-                       const __grid_constant__ CUtensorMap map_v, Tc3Params P) {
+                       const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_o,
+                       Tc3Params P) {
   extern __shared__ uint8_t smem_raw3[];
   uint8_t* smem = smem_align1024(smem_raw3);
   if (smem != smem_raw3) __trap();  // no slack was allocated for alignment
@@ -137,7 +138,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
   uint64_t* o_empty = o_fin + 1;         // epilogue read O (256 threads)
   uint64_t* item_full = o_empty + 1;     // [2]
   uint64_t* slot_empty = item_full + 2;  // [2] V lane + MMA + 8 softmax warps
-  static_assert(3 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 2 * kSB + 6 <= 32, "barrier block");
+  uint64_t* qbuf_free = slot_empty + 2;  // [kQB3] the epilogue's output store has read the Q buffer
+  static_assert(4 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 2 * kSB + 6 <= 32, "barrier block");
   Item3* s_item = reinterpret_cast<Item3*>(smem + kOffBar3 + 256);  // after <= 32 barriers, 16 B aligned
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_item + 2);
   float* s_x = reinterpret_cast<float*>(smem + kOffX3);
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       mbar_init(&q_loaded[b], 1);
       mbar_init(&q_full[b], 2);
       mbar_init(&q_empty[b], 1);
+      mbar_init(&qbuf_free[b], 1);
     }
     mbar_init(o_fin, 1);
     mbar_init(o_empty, 256);
@@ -204,7 +207,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
         claim(nxt);
         // raw (pre-RoPE) Q into tile buf once item i-2's last Q.K^T has read it
         const int qb = i % kQB3;
-        if (i >= kQB3) mbar_wait(&q_empty[qb], ((i / kQB3) - 1) & 1);
+        if (i >= kQB3) {
+          mbar_wait(&q_empty[qb], ((i / kQB3) - 1) & 1);
+          mbar_wait(&qbuf_free[qb], ((i / kQB3) - 1) & 1);  // item i-2's output staged through it
+        }
         mbar_arrive_expect_tx(&q_loaded[qb], kTile3);
         tc::tma_load_3d(smem + kOffQ3 + qb * kTile3, &map_q, 0, it.h, it.t * kT3, &q_loaded[qb]);
         tc::tma_load_3d(smem + kOffQ3 + qb * kTile3 + kHalf3, &map_q, 64, it.h, it.t * kT3, &q_loaded[qb]);
@@ -504,25 +510,42 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const float lt = ls[r] + ls[128 + r];
       pair_sync(quarter);  // both read before the slot is reused by the next tile's max
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      // bf16 output: stage the tile in this item's Q buffer (all its Q.K^T completed before o_fin) in
+      // the Q tile's SW128 layout and write it with two TMA stores (the per-thread row stores of a
+      // 128-row tile were 256 uncoalesced wavefronts per warp); fp32 output: direct row stores
+      const int qb_ep = it_i % kQB3;
+      uint8_t* stage = smem + kOffQ3 + qb_ep * kTile3 + c * kHalf3;
 #pragma unroll 1
       for (int cc = 0; cc < 2; ++cc) {
         float o[32];
         tc::tmem_ld32(lane_base + o_col + cc * 32, o);
         tc::tmem_wait_ld();
-        if (i < P.n) {
-          const int d0 = c * 64 + cc * 32;
-          if (P.out_f32) {
-            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + it.h) * kHeadDim + d0);
+        if (!P.out_f32) {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
-          } else {
-            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + ((size_t)i * P.hq + it.h) * kHeadDim + d0);
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
-                                  pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
+          for (int e = 0; e < 4; ++e) {
+            const int ch = cc * 4 + e;  // 16-byte chunk of this row's 128 B half
+            *reinterpret_cast<uint4*>(stage + r * 128 + ((ch ^ (r & 7)) << 4)) =
+                make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
+                           pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
           }
+        } else if (i < P.n) {
+          const int d0 = c * 64 + cc * 32;
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + it.h) * kHeadDim + d0);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
         }
+      }
+      if (!P.out_f32) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the TMA
+      asm volatile("bar.sync 5, 256;" ::: "memory");  // the 8 softmax warps staged their rows
+      if (warp == 2 && lane == 0) {
+        if (!P.out_f32) {
+          uint8_t* tile = smem + kOffQ3 + qb_ep * kTile3;
+          tc::tma_store_3d(&map_o, tile, 0, it.h, it.t * kT3);  // rows past n are clipped
+          tc::tma_store_3d(&map_o, tile + kHalf3, 64, it.h, it.t * kT3);
+          tc::bulk_commit_group();
+          tc::bulk_wait_group_read0();
+        }
+        mbar_arrive(&qbuf_free[qb_ep]);
       }
       tc::fence_before();
       mbar_arrive(o_empty);
@@ -544,8 +567,10 @@ mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_
                              int32_t kv_heads, void* d_out, int32_t out_dtype, const int32_t* hcount,
                              const int32_t* tlist, int32_t stride, int32_t* counters, cudaStream_t st) {
   if (max_depth > 64) return fail(MV_ERR_INVALID_ARGUMENT, "prefill: max_depth > 64");
-  CUtensorMap mq, mk, mvv;
+  CUtensorMap mq, mk, mvv, mo;
   if (mv_status e = tc::make_rows_map(&mq, q_raw, n, q_heads, kT3)) return e;
+  // bf16 output map (same [n][hq][128] shape and box as Q); unused for fp32 output
+  if (mv_status e = tc::make_rows_map(&mo, out_dtype == 1 ? (const void*)q_raw : d_out, n, q_heads, kT3)) return e;
   if (mv_status e = tc::make_rows_map(&mk, k_rot, n, kv_heads, kT3)) return e;
   if (mv_status e = tc::make_rows_map(&mvv, v, n, kv_heads, kT3)) return e;
   Tc3Params T;
@@ -575,7 +600,7 @@ mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_
   MV_CUDA_TRY(attr_err);
   const int num_sms = sms_dev[cur] > 0 ? sms_dev[cur] : 148;
   T.counters = counters;
-  prefill_tc3_kernel<<<std::min(T.n_items, num_sms), kThreads3, kSmem3, st>>>(mq, mk, mvv, T);
+  prefill_tc3_kernel<<<std::min(T.n_items, num_sms), kThreads3, kSmem3, st>>>(mq, mk, mvv, mo, T);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }

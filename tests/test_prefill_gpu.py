@@ -140,8 +140,19 @@ def test_sequence_lengths_around_tiles(mv):
     # lengths that leave a partial last q tile / k tile, including n < 128 and n = 128 * k + 1
     for n_extra in (0, 1, 127, 129, 255, 383):
         toks = nested_tokens(2, 2, 8, seed=n_extra, prefix=50 + n_extra)
-        err, _ = run_prefill(mv, toks, hq=8, hkv=2, seed=n_extra + 1)
+        err, spec = run_prefill(mv, toks, hq=8, hkv=2, seed=n_extra + 1)
         assert err < TOL, (len(toks), err)
+        # the bf16 output leaves through a TMA store of whole 128-row tiles: rows past n are clipped,
+        # rows before it equal the fp32 result up to the bf16 rounding
+        n = len(toks)
+        q, k, v = sym_bf16(n + 1, (n, 8, 128)).cuda(), sym_bf16(n + 2, (n, 2, 128)).cuda(), sym_bf16(n + 3, (n, 2, 128)).cuda()
+        guard = torch.full((n + 256, 8, 128), 7.0, dtype=torch.bfloat16, device="cuda")
+        o16 = guard[:n]
+        mv.attention.prefill(q, k, v, spec.positions, spec.excl, out=o16)
+        o32 = mv.attention.prefill(q, k, v, spec.positions, spec.excl, out_dtype=torch.float32)
+        d = (o16.float() - o32).abs()
+        assert bool((d <= o32.abs() * 2.0 ** -8 + 1e-6).all()), n
+        assert bool((guard[n:] == 7.0).all()), n  # nothing written past row n
 
 
 def test_32k_nested_sampled(mv):
