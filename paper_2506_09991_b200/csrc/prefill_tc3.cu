@@ -195,25 +195,32 @@ __global__ void __launch_bounds__(kThreads3, 1)
         it.e0 = it.valid ? P.tlist[(size_t)it.t * P.stride] : 0;
         it.pad0 = it.pad1 = it.pad2 = 0;
       };
+      // raw (pre-RoPE) Q tiles go out one item ahead: item i + 1's tile is loaded once item i's first
+      // K tiles are out (the buffer held item i - 1's Q and its staged output: q_empty and qbuf_free),
+      // so the rotator warps rotate it while item i runs instead of at the item transition
+      auto load_q = [&](const Item3& q_it, int qi) {
+        const int qb = qi % kQB3;
+        if (qi >= kQB3) {
+          mbar_wait(&q_empty[qb], ((qi / kQB3) - 1) & 1);
+          mbar_wait(&qbuf_free[qb], ((qi / kQB3) - 1) & 1);
+        }
+        mbar_arrive_expect_tx(&q_loaded[qb], kTile3);
+        tc::tma_load_3d(smem + kOffQ3 + qb * kTile3, &map_q, 0, q_it.h, q_it.t * kT3, &q_loaded[qb]);
+        tc::tma_load_3d(smem + kOffQ3 + qb * kTile3 + kHalf3, &map_q, 64, q_it.h, q_it.t * kT3, &q_loaded[qb]);
+      };
       Item3 nxt;
       claim(nxt);
+      if (nxt.valid) load_q(nxt, 0);
       for (int i = 0;; ++i) {
         const int buf = i & 1;
         if (i >= 2) mbar_wait(&slot_empty[buf], ((i >> 1) - 1) & 1);
-        const Item3 it = nxt;
+        Item3 it = nxt;
+        if (it.valid) claim(nxt);
+        it.pad0 = nxt.valid;  // the rotator warps rotate the next item's Q tile during this item
+        it.pad1 = nxt.t;
         s_item[buf] = it;
         mbar_arrive(&item_full[buf]);
         if (!it.valid) break;
-        claim(nxt);
-        // raw (pre-RoPE) Q into tile buf once item i-2's last Q.K^T has read it
-        const int qb = i % kQB3;
-        if (i >= kQB3) {
-          mbar_wait(&q_empty[qb], ((i / kQB3) - 1) & 1);
-          mbar_wait(&qbuf_free[qb], ((i / kQB3) - 1) & 1);  // item i-2's output staged through it
-        }
-        mbar_arrive_expect_tx(&q_loaded[qb], kTile3);
-        tc::tma_load_3d(smem + kOffQ3 + qb * kTile3, &map_q, 0, it.h, it.t * kT3, &q_loaded[qb]);
-        tc::tma_load_3d(smem + kOffQ3 + qb * kTile3 + kHalf3, &map_q, 64, it.h, it.t * kT3, &q_loaded[qb]);
         const int kvh = it.h / (P.hq / P.hkv);
         const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
         for (int j = 0; j < it.m; ++j) {
@@ -225,7 +232,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
           tc::tma_load_3d(smem + kOffK3 + s * kTile3, &map_k, 0, kvh, kt * kT3, &k_full[s]);
           tc::tma_load_3d(smem + kOffK3 + s * kTile3 + kHalf3, &map_k, 64, kvh, kt * kT3, &k_full[s]);
           ++gk;
+          if (j == min(kKSt3, it.m) - 1 && nxt.valid) load_q(nxt, i + 1);
         }
+        if (it.m == 0 && nxt.valid) load_q(nxt, i + 1);
       }
     } else if (lane == 1) {
       // ---------------- V loader ----------------
@@ -331,11 +340,16 @@ __global__ void __launch_bounds__(kThreads3, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&slot_empty[buf]);
       if (!it.valid) break;
-      const int qb = it_i % kQB3;
-      mbar_wait(&q_loaded[qb], (it_i / kQB3) & 1);
+      // item 0's tile first, then (every item) the next item's tile, loaded one item ahead
+#pragma unroll 1
+      for (int pass = it_i == 0 ? 0 : 1; pass < 2; ++pass) {
+      const int qi = it_i + pass;
+      if (pass == 1 && !it.pad0) break;
+      const int qt_t = pass == 0 ? it.t : it.pad1;
+      const int qb = qi % kQB3;
+      mbar_wait(&q_loaded[qb], (qi / kQB3) & 1);
       uint8_t* qt = smem + kOffQ3 + qb * kTile3;
       // 32 chunks per thread in 4 batches of 8: all table loads of a batch are in flight together
-      // (the table comes from L2; a light item's rotation is otherwise on the MMA's critical path)
       constexpr int kBatch = 8;
       for (int b0 = 0; b0 < kT3 * 16 / 64; b0 += kBatch) {
         float4 t01[kBatch], t23[kBatch];
@@ -344,7 +358,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
         for (int u = 0; u < kBatch; ++u) {
           const int ch = rt + 64 * (b0 + u);
           const int row = ch >> 4, c = ch & 15;
-          const int grow = min(it.t * kT3 + row, P.n - 1);  // rows past n are zero-filled: any angle
+          const int grow = min(qt_t * kT3 + row, P.n - 1);  // rows past n are zero-filled: any angle
           q4[u] = reinterpret_cast<uint4*>(qt + (c >> 3) * kHalf3 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
           const float4* tb = reinterpret_cast<const float4*>(P.cs + (size_t)grow * 64 + c * 4);
           t01[u] = __ldg(tb);
@@ -367,6 +381,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_full[qb]);
+      }
     }
   } else {
     // ---------------- softmax: warps 2-5 columns 0-63, warps 6-9 columns 64-127 ----------------
