@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
   uint64_t* item_full = o_empty + 1;     // [2]
   uint64_t* slot_empty = item_full + 2;  // [2] V lane + MMA + 8 softmax warps
   uint64_t* qbuf_free = slot_empty + 2;  // [kQB3] the epilogue's output store has read the Q buffer
-  static_assert(4 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 2 * kSB + 6 <= 32, "barrier block");
+  uint64_t* stage_full = qbuf_free + kQB3;  // [2] by item parity: the 8 softmax warps staged its output
+  static_assert(4 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 2 * kSB + 8 <= 32, "barrier block");
   Item3* s_item = reinterpret_cast<Item3*>(smem + kOffBar3 + 256);  // after <= 32 barriers, 16 B aligned
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_item + 2);
   float* s_x = reinterpret_cast<float*>(smem + kOffX3);
@@ -154,6 +155,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
     }
     mbar_init(o_fin, 1);
     mbar_init(o_empty, 256);
+    mbar_init(&stage_full[0], 8);
+    mbar_init(&stage_full[1], 8);
     for (int b = 0; b < kSB; ++b) {
       mbar_init(&s_full[b], 1);
       mbar_init(&p_full[b], 256);
@@ -382,7 +385,23 @@ __global__ void __launch_bounds__(kThreads3, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&q_full[qb]);
       }
+      // this item's output tile, staged by the softmax warps in its Q buffer: two TMA stores; the
+      // buffer returns to the loader once they have read it
+      if (warp == kRotWarp0 && lane == 0) {
+        mbar_wait(&stage_full[it_i & 1], (it_i >> 1) & 1);
+        const int qb_ep = it_i % kQB3;
+        if (!P.out_f32) {
+          const uint8_t* tile = smem + kOffQ3 + qb_ep * kTile3;
+          tc::tma_store_3d(&map_o, tile, 0, it.h, it.t * kT3);  // rows past n are clipped
+          tc::tma_store_3d(&map_o, tile + kHalf3, 64, it.h, it.t * kT3);
+          tc::bulk_commit_group();
+          tc::bulk_wait_group_read0();
+        }
+        mbar_arrive(&qbuf_free[qb_ep]);
+      }
+      __syncwarp();
     }
+    if (warp == kRotWarp0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores done
   } else {
     // ---------------- softmax: warps 2-5 columns 0-63, warps 6-9 columns 64-127 ----------------
     const int c = (warp - 2) >> 2;      // column half
@@ -516,18 +535,20 @@ __global__ void __launch_bounds__(kThreads3, 1)
         tc::fence_before();
         mbar_arrive(&p_full[g % kSB]);
       }
-      // epilogue: row sum over both halves, O / l for this warp's 64 dims
-      mbar_wait(o_fin, it_i & 1);
-      tc::fence_after();
+      // epilogue: row sum over both halves (exchanged while the last P.V runs), O / l for this
+      // warp's 64 dims
       float* ls = s_x + (g & 1) * 256;  // the next tile's max slot: free until this pair syncs again
       ls[c * 128 + r] = l;
       pair_sync(quarter);
       const float lt = ls[r] + ls[128 + r];
       pair_sync(quarter);  // both read before the slot is reused by the next tile's max
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      mbar_wait(o_fin, it_i & 1);
+      tc::fence_after();
       // bf16 output: stage the tile in this item's Q buffer (all its Q.K^T completed before o_fin) in
-      // the Q tile's SW128 layout and write it with two TMA stores (the per-thread row stores of a
-      // 128-row tile were 256 uncoalesced wavefronts per warp); fp32 output: direct row stores
+      // the Q tile's SW128 layout; rotator warp 10 writes it with two TMA stores and waits for their
+      // reads (~2,500 cycles, off the softmax warps' path).  The per-thread row stores this replaces
+      // were 256 uncoalesced wavefronts per warp.  fp32 output: direct row stores.
       const int qb_ep = it_i % kQB3;
       uint8_t* stage = smem + kOffQ3 + qb_ep * kTile3 + c * kHalf3;
 #pragma unroll 1
@@ -551,17 +572,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
         }
       }
       if (!P.out_f32) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the TMA
-      asm volatile("bar.sync 5, 256;" ::: "memory");  // the 8 softmax warps staged their rows
-      if (warp == 2 && lane == 0) {
-        if (!P.out_f32) {
-          uint8_t* tile = smem + kOffQ3 + qb_ep * kTile3;
-          tc::tma_store_3d(&map_o, tile, 0, it.h, it.t * kT3);  // rows past n are clipped
-          tc::tma_store_3d(&map_o, tile + kHalf3, 64, it.h, it.t * kT3);
-          tc::bulk_commit_group();
-          tc::bulk_wait_group_read0();
-        }
-        mbar_arrive(&qbuf_free[qb_ep]);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&stage_full[it_i & 1]);
       tc::fence_before();
       mbar_arrive(o_empty);
     }
