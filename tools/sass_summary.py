@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""SASS evidence per kernel of the built library: tcgen05 MMAs (UTCHMMA / UTCQMMA), TMA (UTMALDG),
+"""SASS evidence per kernel of the built library: tcgen05 MMAs (UTCHMMA / UTCQMMA), TMA loads / stores (UTMALDG / UTMASTG),
 bulk copies (UBLKCP), TMEM loads / stores (LDTM / STTM), tcgen05 commits (UTCBAR), MUFU.EX2, legacy
 HMMA (mma.sync) and local-memory traffic (LDL / STL).  usage: sass_summary.py [lib.so] > out.txt"""
 import collections
@@ -9,7 +9,7 @@ import sys
 
 lib = sys.argv[1] if len(sys.argv) > 1 else "paper_2506_09991_b200/libmvb200.so"
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
-keys = ["UTCHMMA", "UTCQMMA", "UTMALDG", "UBLKCP", "LDTM", "STTM", "UTCBAR", "UTCCP", "MUFU.EX2", "HMMA", "LDL", "STL",
+keys = ["UTCHMMA", "UTCQMMA", "UTMALDG", "UTMASTG", "UBLKCP", "LDTM", "STTM", "UTCBAR", "UTCCP", "MUFU.EX2", "HMMA", "LDL", "STL",
         "SYNCS.PHASECHK", "ELECT"]
 cur, counts, order = None, {}, []
 for line in sass.splitlines():
