@@ -86,7 +86,9 @@ template <int B>
 __device__ __forceinline__ void pv3(uint64_t vd, bool first) {
 #pragma unroll
   for (int k = 0; k < 8; ++k)
-    tc::mma_ts(kO0, kS0 + B * 128 + k * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV3, (!first || k > 0) ? 1u : 0u);
+    // P of k tokens [64h, 64h + 64) sits in packed columns [64h, 64h + 32) of the S buffer
+    tc::mma_ts(kO0, kS0 + B * 128 + (k >> 2) * 64 + (k & 3) * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV3,
+               (!first || k > 0) ? 1u : 0u);
 }
 
 // every kPolyMod3-th score pair takes poly_exp2x2: 1 pair in 8 gave +2.5% on C3 (16 and 4..6 no better)
@@ -486,13 +488,17 @@ __global__ void __launch_bounds__(kThreads3, 1)
         };
         // Fast path (no per-tile row max): exponentiate against the row's reference; it moves only on
         // the item's first tile or when this half's mass exceeds kSumLimit3 (every P stays <= 2^14,
-        // exact enough in bf16 and far from fp32 overflow).  The OR-reduced pair barrier also orders
-        // both warps' S loads before either writes P into the S columns.
+        // exact enough in bf16 and far from fp32 overflow).  P of this half goes into this warp's own
+        // S columns (packed [64c, 64c + 32)), so it is stored before the OR-reduced pair barrier
+        // (the store overlaps the wait); a move rewrites it.
         bool need = m_ref == -INFINITY;
         float ls = 0.f;
+        const uint32_t p_col = lane_base + s_col + c * 64;
         if (!__any_sync(0xffffffffu, need)) {
           ls = exps(m_ref);
           need = !(ls <= kSumLimit3);  // also catches inf / NaN sums
+          tc::tmem_stNu<16>(p_col, pk);
+          tc::tmem_stNu<16>(p_col + 16, pk + 16);
         }
         if (pair_any(quarter, need)) {
           // slow path: the row max over both column halves, move the reference, rescale O
@@ -526,10 +532,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
           l *= alpha;
           m_ref = nref;
           ls = exps(m_ref == -INFINITY ? 0.f : m_ref);
+          tc::tmem_stNu<16>(p_col, pk);
+          tc::tmem_stNu<16>(p_col + 16, pk + 16);
         }
-        // P for k tokens [64c, 64c + 64) -> packed columns [32c, 32c + 32) of the S buffer
-        tc::tmem_stNu<16>(lane_base + s_col + c * 32, pk);
-        tc::tmem_stNu<16>(lane_base + s_col + c * 32 + 16, pk + 16);
         l += ls;
         tc::tmem_wait_st();
         tc::fence_before();
