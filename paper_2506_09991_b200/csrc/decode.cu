@@ -167,13 +167,17 @@ __device__ __forceinline__ void issue_qk_mmas(uint64_t kd) {  // S_SB = Q . K_bl
     tc::mma_ts(kColS + SB * kBlkCols, kColQ + k * 8, kd + (uint64_t)(((k >> 2) * 1024 + (k & 3) * 32) >> 4), kIdQK,
                k > 0 ? 1u : 0u);
 }
+// P of a block: each softmax part (W = 64 / (2F) tokens) is packed into the first W / 2 of its own
+// S columns, so page k's 16 tokens sit at packed column (k >> 1) * 32 + (k & 1) * 8 (F = 1) or
+// k * 16 (F = 2)
 template <int SB>
-__device__ __forceinline__ void issue_pv_mmas(uint64_t vd, int np, uint32_t acc0) {  // O += P_SB . V_blk
+__device__ __forceinline__ void issue_pv_mmas(uint64_t vd, int np, uint32_t acc0, int copies) {  // O += P_SB . V_blk
   constexpr uint32_t ocol = kColO, pcol = kColS + SB * kBlkCols;
+  const uint32_t p1 = copies == 1 ? 8 : 16, p2 = 32, p3 = copies == 1 ? 40 : 48;
   tc::mma_ts(ocol, pcol, vd, kIdPV, acc0);
-  if (np > 1) tc::mma_ts(ocol, pcol + 8, vd + (uint64_t)(kPageBytes >> 4), kIdPV, 1u);
-  if (np > 2) tc::mma_ts(ocol, pcol + 16, vd + (uint64_t)((2 * kPageBytes) >> 4), kIdPV, 1u);
-  if (np > 3) tc::mma_ts(ocol, pcol + 24, vd + (uint64_t)((3 * kPageBytes) >> 4), kIdPV, 1u);
+  if (np > 1) tc::mma_ts(ocol, pcol + p1, vd + (uint64_t)(kPageBytes >> 4), kIdPV, 1u);
+  if (np > 2) tc::mma_ts(ocol, pcol + p2, vd + (uint64_t)((2 * kPageBytes) >> 4), kIdPV, 1u);
+  if (np > 3) tc::mma_ts(ocol, pcol + p3, vd + (uint64_t)((3 * kPageBytes) >> 4), kIdPV, 1u);
 }
 // named barrier over the softmax warps holding one logical row quadrant, OR-reducing a predicate
 __device__ __forceinline__ bool group_any(int id, int count, bool pred) {
@@ -267,11 +271,22 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
       // and far from fp32 overflow), so no per-block max is needed.
       bool need = row_active && m_ref == -INFINITY;
       float ls = 0.f;
+      // P of this part goes into its own S columns (packed [part W, part W + W/2)), the zeros into
+      // the other copies' parts of these rows: no warp's store touches S another warp still reads,
+      // so they are issued before the group barrier (which only decides a reference move)
+      if (F > 1) {
+        uint32_t z[WP];
+#pragma unroll
+        for (int k = 0; k < WP; ++k) z[k] = 0u;
+#pragma unroll
+        for (int c2 = 0; c2 < F; ++c2)
+          if (c2 != c) tc::tmem_stNu<WP>(scol + (c2 * 2 + half) * W, z);
+      }
       if (!__any_sync(0xffffffffu, need)) {
         ls = exp_part(row_active ? m_ref : 0.f);
         need = ls > kSumLimit / NP;
+        tc::tmem_stNu<WP>(scol + part * W, pk);
       }
-      // the barrier also orders every warp's S reads before any warp's P / zero stores
       if (group_any(bar_id, bar_cnt, need)) {
         // slow path (whole group): row max over all parts, move the reference, rescale O
         float mx = -INFINITY;
@@ -304,17 +319,9 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
         l *= alpha;
         m_ref = nref;
         ls = exp_part(m_ref == -INFINITY ? 0.f : m_ref);
+        tc::tmem_stNu<WP>(scol + part * W, pk);
       }
       l += ls;
-      tc::tmem_stNu<WP>(scol + part * WP, pk);
-      if (F > 1) {
-        uint32_t z[WP];
-#pragma unroll
-        for (int k = 0; k < WP; ++k) z[k] = 0u;
-#pragma unroll
-        for (int c2 = 0; c2 < F; ++c2)
-          if (c2 != c) tc::tmem_stNu<WP>(scol + (c2 * 2 + half) * WP, z);
-      }
       tc::tmem_wait_st();
     }
     tc::fence_before();
@@ -540,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       const int ub = i & 1;
       mbar_wait(&item_full[ub], (i >> 1) & 1);
       const WorkItem* si = &s_item[ub];
-      const int valid = si->valid, n_ent = si->n_entries;
+      const int valid = si->valid, n_ent = si->n_entries, copies = si->copies;
       __syncwarp();
       if (lane == 0) mbar_arrive(&slot_empty[ub]);  // header read
       if (!valid) break;
@@ -556,11 +563,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         const uint32_t acc0 = blk > 0 ? 1u : 0u;  // the unit's first block opens O
         if (tc::elect_one()) {
           switch (sb) {
-            case 0: issue_pv_mmas<0>(vd, np, acc0); break;
-            case 1: issue_pv_mmas<1>(vd, np, acc0); break;
-            case 2: issue_pv_mmas<2>(vd, np, acc0); break;
-            case 3: issue_pv_mmas<3>(vd, np, acc0); break;
-            default: issue_pv_mmas<4>(vd, np, acc0); break;
+            case 0: issue_pv_mmas<0>(vd, np, acc0, copies); break;
+            case 1: issue_pv_mmas<1>(vd, np, acc0, copies); break;
+            case 2: issue_pv_mmas<2>(vd, np, acc0, copies); break;
+            case 3: issue_pv_mmas<3>(vd, np, acc0, copies); break;
+            default: issue_pv_mmas<4>(vd, np, acc0, copies); break;
           }
           tc::mma_commit(&vempty[g % kVSlots]);  // also certifies PV(g) to the softmax (O rescale)
           tc::mma_commit(&pv_done[sb]);
