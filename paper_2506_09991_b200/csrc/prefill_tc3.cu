@@ -53,8 +53,8 @@ constexpr uint32_t kIdQK3 = tc::idesc_bf16(128, 128, 0, 0);
 constexpr uint32_t kIdPV3 = tc::idesc_bf16(128, 128, 0, 1);
 constexpr float kLazy3 = 8.f;
 // TMEM columns: three S buffers (S(g) in buffer g % 3) and one O
-constexpr int kSB = 3;
-constexpr uint32_t kS0 = 0, kO0 = kSB * 128;
+constexpr int kSB = 2;  // S / P buffers
+constexpr uint32_t kS0 = 0, kO0 = kSB * 128;  // O of column half c (all 128 dims) at kO0 + c * 128
 
 struct Tc3Params {
   const int32_t* excl;
@@ -82,12 +82,12 @@ __device__ __forceinline__ void qk3(uint64_t qd, uint64_t kd) {
     tc::mma_ss(kS0 + B * 128, qd + off, kd + off, kIdQK3, k > 0 ? 1u : 0u);
   }
 }
-template <int B>
+// O(h) += P(h) . V[64h, 64h + 64): P of column half h sits in packed columns [64h, 64h + 32)
+template <int B, int H>
 __device__ __forceinline__ void pv3(uint64_t vd, bool first) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
-    // P of k tokens [64h, 64h + 64) sits in packed columns [64h, 64h + 32) of the S buffer
-    tc::mma_ts(kO0, kS0 + B * 128 + (k >> 2) * 64 + (k & 3) * 8, vd + (uint64_t)((k * 2048) >> 4), kIdPV3,
+  for (int k = 0; k < 4; ++k)
+    tc::mma_ts(kO0 + H * 128, kS0 + B * 128 + H * 64 + k * 8, vd + (uint64_t)(((H * 4 + k) * 2048) >> 4), kIdPV3,
                (!first || k > 0) ? 1u : 0u);
 }
 
@@ -135,14 +135,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
   uint64_t* v_full = k_empty + kKSt3;    // [2]
   uint64_t* v_empty = v_full + kVSt3;    // [2] MMA commit after P.V (also certifies O for the rescale)
   uint64_t* s_full = v_empty + kVSt3;    // [3] S buffer b written
-  uint64_t* p_full = s_full + kSB;       // [3] 256 softmax threads wrote P into S buffer b
-  uint64_t* o_fin = p_full + kSB;        // O final for the item
+  uint64_t* p_full = s_full + kSB;       // [kSB][2] the 4 warps of column half h wrote P into S buffer b
+  uint64_t* o_fin = p_full + 2 * kSB;    // O final for the item
   uint64_t* o_empty = o_fin + 1;         // epilogue read O (256 threads)
   uint64_t* item_full = o_empty + 1;     // [2]
   uint64_t* slot_empty = item_full + 2;  // [2] V lane + MMA + 8 softmax warps
   uint64_t* qbuf_free = slot_empty + 2;  // [kQB3] the epilogue's output store has read the Q buffer
   uint64_t* stage_full = qbuf_free + kQB3;  // [2] by item parity: the 8 softmax warps staged its output
-  static_assert(4 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 2 * kSB + 8 <= 32, "barrier block");
+  static_assert(4 * kQB3 + 2 * kKSt3 + 2 * kVSt3 + 3 * kSB + 8 <= 32, "barrier block");
   Item3* s_item = reinterpret_cast<Item3*>(smem + kOffBar3 + 256);  // after <= 32 barriers, 16 B aligned
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_item + 2);
   float* s_x = reinterpret_cast<float*>(smem + kOffX3);
@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
     mbar_init(&stage_full[1], 8);
     for (int b = 0; b < kSB; ++b) {
       mbar_init(&s_full[b], 1);
-      mbar_init(&p_full[b], 256);
+      mbar_init(&p_full[2 * b], 128);
+      mbar_init(&p_full[2 * b + 1], 128);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&item_full[b], 1);
@@ -283,8 +284,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const int b = gg % kSB;
       if (tc::elect_one()) {
         if (b == 0) qk3<0>(qd, kd);
-        else if (b == 1) qk3<1>(qd, kd);
-        else if (kSB > 2) qk3<2 % kSB>(qd, kd);
+        else qk3<1>(qd, kd);
         tc::mma_commit(&s_full[b]);
         tc::mma_commit(&k_empty[gg % kKSt3]);
       }
@@ -308,20 +308,28 @@ __global__ void __launch_bounds__(kThreads3, 1)
       }
       for (int j = 0; j < m; ++j, ++g) {
         mbar_wait(&v_full[g % kVSt3], (g / kVSt3) & 1);
-        mbar_wait(&p_full[g % kSB], (g / kSB) & 1);
-        if (j == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue of item i-1 read O
-        tc::fence_after();
-        const uint64_t vd = vd0 + (uint64_t)(((g % kVSt3) * kTile3) >> 4);
         const int b = g % kSB;
-        if (tc::elect_one()) {
-          if (b == 0) pv3<0>(vd, j == 0);
-          else if (b == 1) pv3<1>(vd, j == 0);
-          else if (kSB > 2) pv3<2 % kSB>(vd, j == 0);
-          tc::mma_commit(&v_empty[g % kVSt3]);
+        if (j == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue of item i-1 read both O
+        const uint64_t vd = vd0 + (uint64_t)(((g % kVSt3) * kTile3) >> 4);
+        // each column half's P.V goes as soon as its four softmax warps released P
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          mbar_wait(&p_full[2 * b + h], (g / kSB) & 1);
+          tc::fence_after();
+          if (tc::elect_one()) {
+            if (b == 0) {
+              if (h == 0) pv3<0, 0>(vd, j == 0);
+              else pv3<0, 1>(vd, j == 0);
+            } else {
+              if (h == 0) pv3<1, 0>(vd, j == 0);
+              else pv3<1, 1>(vd, j == 0);
+            }
+            if (h == 1) tc::mma_commit(&v_empty[g % kVSt3]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
         if (j + kSB < m) {
-          qk(qd, g + kSB);  // S buffer g % 3 again: in order behind P.V(g)
+          qk(qd, g + kSB);  // S buffer g % 2 again: in order behind P.V(g)
           if (j + kSB + 1 == m) {
             if (tc::elect_one()) tc::mma_commit(&q_empty[qb]);
             __syncwarp();
@@ -426,7 +434,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       for (int q = 0; q < kExvRegs; ++q) exv[q] = q < P.D ? __ldg(exr + q) : make_int2(0, 0);
       const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
       const int sh = 20 + 2 * (it.t & 1);
-      const uint32_t o_col = kO0 + c * 64;
+      const uint32_t o_col = kO0 + c * 128;  // this column half's own O (all 128 dims)
       float m_ref = -INFINITY, l = 0.f;
       // the list entry of the next tile is loaded one tile ahead (its L2 latency used to sit
       // between releasing P and waiting for the next S)
@@ -500,27 +508,25 @@ __global__ void __launch_bounds__(kThreads3, 1)
           tc::tmem_stNu<16>(p_col, pk);
           tc::tmem_stNu<16>(p_col + 16, pk + 16);
         }
-        if (pair_any(quarter, need)) {
-          // slow path: the row max over both column halves, move the reference, rescale O
+        if (__any_sync(0xffffffffu, need)) {
+          // slow path (this warp only: each column half keeps its own reference, sum and O): the
+          // max over this half, move the reference, rescale this half's O
           float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
           for (int k = 0; k < 64; k += 2) {
             mx0 = fmaxf(mx0, v[k]);
             mx1 = fmaxf(mx1, v[k + 1]);
           }
-          float* xs = s_x + (g & 1) * 256;
-          xs[c * 128 + r] = fmaxf(mx0, mx1);
-          pair_sync(quarter);
-          const float mx = fmaxf(xs[r], xs[128 + r]) * P.scale_log2;
+          const float mx = fmaxf(mx0, mx1) * P.scale_log2;
           const bool move = m_ref == -INFINITY || mx > m_ref + kLazy3;
           const float nref = move ? fmaxf(m_ref, mx) : m_ref;
           const float alpha = move && m_ref != -INFINITY ? fast_exp2(m_ref - nref) : 1.f;
           if (done >= 1 && __any_sync(0xffffffffu, alpha != 1.f)) {
-            // O holds P.V of the previous tile (g - 1): its V slot's release certifies it
+            // O(c) holds P.V of the previous tile (g - 1): its V slot's release certifies it
             mbar_wait(&v_empty[(g - 1) % kVSt3], ((g - 1) / kVSt3) & 1);
             tc::fence_after();
 #pragma unroll 1
-            for (int cc = 0; cc < 2; ++cc) {
+            for (int cc = 0; cc < 4; ++cc) {
               float o[32];
               tc::tmem_ld32(lane_base + o_col + cc * 32, o);
               tc::tmem_wait_ld();
@@ -538,16 +544,21 @@ __global__ void __launch_bounds__(kThreads3, 1)
         l += ls;
         tc::tmem_wait_st();
         tc::fence_before();
-        mbar_arrive(&p_full[g % kSB]);
+        mbar_arrive(&p_full[2 * (g % kSB) + c]);
       }
-      // epilogue: row sum over both halves (exchanged while the last P.V runs), O / l for this
-      // warp's 64 dims
-      float* ls = s_x + (g & 1) * 256;  // the next tile's max slot: free until this pair syncs again
-      ls[c * 128 + r] = l;
+      // epilogue: combine the two column halves' (reference, sum, O), exchanged while the last P.V
+      // runs; this warp writes dims [64c, 64c + 64)
+      float2* xs2 = reinterpret_cast<float2*>(s_x);
+      xs2[c * 128 + r] = make_float2(m_ref, l);
       pair_sync(quarter);
-      const float lt = ls[r] + ls[128 + r];
-      pair_sync(quarter);  // both read before the slot is reused by the next tile's max
+      const float2 ot = xs2[(c ^ 1) * 128 + r];
+      pair_sync(quarter);  // both read before the next item's exchange
+      const float mm = fmaxf(m_ref, ot.x);
+      const float a_me = m_ref == -INFINITY ? 0.f : fast_exp2(m_ref - mm);
+      const float a_ot = ot.x == -INFINITY ? 0.f : fast_exp2(ot.x - mm);
+      const float lt = l * a_me + ot.y * a_ot;
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      const float a0 = (c == 0 ? a_me : a_ot) * inv, a1 = (c == 0 ? a_ot : a_me) * inv;
       mbar_wait(o_fin, it_i & 1);
       tc::fence_after();
       // bf16 output: stage the tile in this item's Q buffer (all its Q.K^T completed before o_fin) in
@@ -558,22 +569,25 @@ __global__ void __launch_bounds__(kThreads3, 1)
       uint8_t* stage = smem + kOffQ3 + qb_ep * kTile3 + c * kHalf3;
 #pragma unroll 1
       for (int cc = 0; cc < 2; ++cc) {
-        float o[32];
-        tc::tmem_ld32(lane_base + o_col + cc * 32, o);
+        float o[32], o1[32];
+        tc::tmem_ld32(lane_base + kO0 + c * 64 + cc * 32, o);
+        tc::tmem_ld32(lane_base + kO0 + 128 + c * 64 + cc * 32, o1);
         tc::tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 32; ++k) o[k] = (a0 != 0.f ? o[k] * a0 : 0.f) + (a1 != 0.f ? o1[k] * a1 : 0.f);
         if (!P.out_f32) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int ch = cc * 4 + e;  // 16-byte chunk of this row's 128 B half
             *reinterpret_cast<uint4*>(stage + r * 128 + ((ch ^ (r & 7)) << 4)) =
-                make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
-                           pack_bf16(o[8 * e + 4] * inv, o[8 * e + 5] * inv), pack_bf16(o[8 * e + 6] * inv, o[8 * e + 7] * inv));
+                make_uint4(pack_bf16(o[8 * e], o[8 * e + 1]), pack_bf16(o[8 * e + 2], o[8 * e + 3]),
+                           pack_bf16(o[8 * e + 4], o[8 * e + 5]), pack_bf16(o[8 * e + 6], o[8 * e + 7]));
           }
         } else if (i < P.n) {
           const int d0 = c * 64 + cc * 32;
           float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + it.h) * kHeadDim + d0);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
+          for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
         }
       }
       if (!P.out_f32) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the TMA
