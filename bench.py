@@ -38,6 +38,7 @@ REPO = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, REPO)
 
 HQ, HKV, D = 40, 8, 128
+HOST_STEPS = 6  # untimed steps after the timed region that time the host cost of a step's library calls
 KV_BYTES_PER_TOKEN = HKV * D * 2 * 2  # K and V, bf16, all KV heads of one layer
 WORKLOADS = {"c2": dict(prefix=4096, branches=8, branch_len=1024),
              "c4": dict(prefix=16384, branches=32, branch_len=512, total_requests=64)}
@@ -407,7 +408,7 @@ def decode_arm(args, world, rank, local, D_, workload, heads_mode):
     hkv_l = shard.kv_heads[1] - shard.kv_heads[0]
     hq_l = hkv_l * (HQ // HKV)
     e2e_steps = max(3, args.steps // 2)
-    steps_total = args.warmup + args.steps + e2e_steps
+    steps_total = args.warmup + args.steps + HOST_STEPS + e2e_steps
     seed_id = shard.requests[0] * 64 + shard.kv_heads[0]
     st, handles, pos0, rnd = build_workload(mv, torch, R, dev, seed_id, wl["prefix"], wl["branches"],
                                             wl["branch_len"], steps_total, hkv=hkv_l)
@@ -423,21 +424,10 @@ def decode_arm(args, world, rank, local, D_, workload, heads_mode):
           for _ in range(args.steps)] if gathered is not None else []
     base_pos = torch.tensor(pos0, dtype=torch.int32, device=dev)
     stream = D_.stream
-    # the last warm-up steps also time the host cost of a step's two library calls, synchronised first so
-    # no back-pressure wait is counted (the timed loop's host time includes the waits for a pinned staging
-    # buffer to come free, i.e. it tracks the device)
-    host_call = []
     for i in range(args.warmup):
-        timed = i >= max(1, args.warmup - 3)  # step 0 builds the plan
-        if timed:
-            D_.sync()
-        a = time.perf_counter()
         st.append(handles, toks, base_pos + i, 0, ks[i % 2], vs[i % 2])
         mv.attention.decode(st, handles, qs[i % 2], base_pos + i, out=out)
-        if timed:
-            host_call.append(time.perf_counter() - a)
     D_.sync()
-    host_call_ms = 1e3 * float(np.mean(host_call)) if host_call else None
     info = st.plan_info()
 
     # ---- timed region: device events; the attention launches bracketed separately ----
@@ -474,6 +464,20 @@ def decode_arm(args, world, rank, local, D_, workload, heads_mode):
     ag_ms = float(np.mean([a.elapsed_time(b) for a, b in ag])) if ag else 0.0
     ms, att_ms, ag_ms = max_over_ranks([ms, att_ms, ag_ms], device=dev)
 
+    # host cost of a step's two library calls, on untimed steps after the timed region (the plan is
+    # built and settled by then), each synchronised first so no back-pressure wait is counted (the timed
+    # loop's host time includes the waits for a pinned staging buffer to come free, i.e. tracks the device)
+    host_call = []
+    for s in range(HOST_STEPS):
+        i = args.warmup + args.steps + s
+        D_.sync()
+        a = time.perf_counter()
+        st.append(handles, toks, base_pos + i, 0, ks[i % 2], vs[i % 2])
+        mv.attention.decode(st, handles, qs[i % 2], base_pos + i, out=out)
+        host_call.append(time.perf_counter() - a)
+    D_.sync()
+    host_call_ms = 1e3 * float(np.median(host_call))
+
     # ---- e2e through the public API with host buffers (pinned), copies inside the region ----
     nq, nk = n * hq_l * D * 2, n * hkv_l * D * 2
     blk = nq + 2 * nk + n * 4
@@ -496,7 +500,7 @@ def decode_arm(args, world, rank, local, D_, workload, heads_mode):
     ee = [D_.event() for _ in range(2)]
     ee[0].record(stream)
     for s in range(e2e_steps):
-        i = args.warmup + args.steps + s
+        i = args.warmup + args.steps + HOST_STEPS + s
         hpos[i % 2].numpy()[:] = pos0_np + i
         din.copy_(hin[i % 2], non_blocking=True)
         st.append(handles, toks, dp, 0, dk, dv)
