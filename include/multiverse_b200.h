@@ -128,7 +128,7 @@ typedef struct {
   int32_t record_bytes;   /* opaque per-token payload record (RadixStore payload_record_size); 0 = none */
   int32_t layers;         /* attention KV planes: bf16 K and V per layer, head-major [kv_head][page][16][head_dim] */
   int32_t kv_heads;       /*   (0 = no attention plane) */
-  int32_t head_dim;       /*   must be 128 when kv_heads > 0 */
+  int32_t head_dim;       /*   64 or 128 when kv_heads > 0 (the attention kernels' native head dims) */
   int64_t table_entries;  /* device page-table arena capacity in entries (0 = 4 * num_pages + 65536) */
   double rope_base;       /* rotary base for K at append (toy_model.cpp:30-41); 0 = 10000 */
 } mv_kv_config;
@@ -245,6 +245,13 @@ MV_API mv_status mv_attn_prefill(const void* d_q, const void* d_k, const void* d
                           const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads, int32_t kv_heads,
                           double rope_base, void* d_out, int32_t out_dtype, void* d_workspace,
                           size_t workspace_bytes, mv_stream_t stream);
+/* The same with an explicit head dim (64 or 128; the two above are head_dim 128): every [..][128]
+ * above reads [..][head_dim].  ToyModel's d_h = model_dim / heads (toy_model.hpp:29) is 64 at C1. */
+MV_API size_t mv_prefill_workspace_size_hd(int32_t n, int32_t q_heads, int32_t kv_heads, int32_t head_dim);
+MV_API mv_status mv_attn_prefill_hd(const void* d_q, const void* d_k, const void* d_v, const int32_t* d_positions,
+                             const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
+                             int32_t kv_heads, int32_t head_dim, double rope_base, void* d_out, int32_t out_dtype,
+                             void* d_workspace, size_t workspace_bytes, mv_stream_t stream);
 
 /*
  * K5 — per-lane tag interpreter (replaces engine.cpp:323-415 feed_interpreter, with the BUG-2
@@ -302,9 +309,13 @@ typedef struct {
 MV_API size_t mv_toy_weight_count(const mv_toy_config* cfg);
 MV_API mv_status mv_toy_create(const mv_toy_config* cfg, const double* h_weights, mv_toy** out);
 MV_API mv_status mv_toy_destroy(mv_toy* m);
+/* The attention kernels' head dim for a model head dim: d_h itself when it is 64 or 128 (native
+ * kernels), else 128 (q / k / v zero-padded, q pre-scaled by sqrt(128 / d_h)).  Toy stores use it. */
+MV_API int32_t mv_attn_head_dim(int32_t model_head_dim);
 /*
  * ToyModel::step for n lanes at once (engine.cpp:603-641 batched): each lane's token joins its cache
- * (K/V of every layer appended in place into `s`, whose planes must be layers x heads x 128) and
+ * (K/V of every layer appended in place into `s`, whose planes must be layers x heads x
+ * mv_attn_head_dim(model_dim / heads)) and
  * attends over it.  d_tokens / d_positions int32[n]; d_logits fp32 [n][V]; optional d_hidden fp32
  * [n][D] and d_kv fp32 [n][2 * layers * D] (the reference's cache record: per layer rotated K | V).
  * Runs on the store's stream.

@@ -556,7 +556,7 @@ class ToyModel {
     kc.num_pages = static_cast<int32_t>(scratch_pages_);
     kc.layers = weights_.config.layers;
     kc.kv_heads = weights_.config.heads;
-    kc.head_dim = 128;
+    kc.head_dim = mv_attn_head_dim(weights_.config.head_dim());
     kc.rope_base = weights_.config.rope_base;
     check(mv_kv_store_create(&kc, &scratch_));
   }

@@ -90,6 +90,10 @@ def _load():
         "mv_attn_decode_plan_info": ([P, P], ctypes.c_int),
         "mv_prefill_workspace_size": ([i32, i32, i32], sz),
         "mv_attn_prefill": ([P, P, P, P, P, i32, i32, i32, i32, ctypes.c_double, P, i32, P, sz, P], ctypes.c_int),
+        "mv_prefill_workspace_size_hd": ([i32, i32, i32, i32], sz),
+        "mv_attn_prefill_hd": ([P, P, P, P, P, i32, i32, i32, i32, i32, ctypes.c_double, P, i32, P, sz, P],
+                               ctypes.c_int),
+        "mv_attn_head_dim": ([i32], i32),
         "mv_kv_write_range": ([P, u64, i64, i64, P, i32, P, P], ctypes.c_int),
         "mv_toy_weight_count": ([P], sz),
         "mv_toy_create": ([P, P, P], ctypes.c_int),
@@ -123,6 +127,7 @@ EXPORTED = (
     "mv_kv_fork", "mv_kv_merge", "mv_kv_release", "mv_kv_length", "mv_kv_stats_get", "mv_kv_resolve",
     "mv_kv_resolve_payloads", "mv_kv_resolve_slots", "mv_kv_append", "mv_kv_write_last", "mv_kv_append_many",
     "mv_kv_gather_kv", "mv_attn_decode", "mv_attn_decode_plan_info", "mv_prefill_workspace_size", "mv_attn_prefill",
+    "mv_prefill_workspace_size_hd", "mv_attn_prefill_hd", "mv_attn_head_dim",
     "mv_interp_init", "mv_interp_feed", "mv_kv_write_range", "mv_toy_weight_count", "mv_toy_create", "mv_toy_destroy",
     "mv_toy_get_config", "mv_toy_vocab", "mv_toy_step", "mv_toy_load_context", "mv_toy_forward", "mv_argmax_rows",
     "mv_engine_run_forced", "mv_engine_run_batch", "mv_engine_run_free",

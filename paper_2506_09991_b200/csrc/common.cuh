@@ -30,7 +30,9 @@ mv_status fail(mv_status st, const std::string& msg);
   } while (0)
 
 constexpr int kPageTokens = 16;   // tokens per KV page (BASELINE configs[1] "paged KV block 16")
-constexpr int kHeadDim = 128;     // Qwen2.5-32B head dim; the attention kernels are specialised for it
+constexpr int kHeadDim = 128;     // Qwen2.5-32B head dim (BASELINE configs[1..4])
+constexpr int kMaxHeadDim = 128;  // head dims with native kernels: 128 and 64 (the toy model's d_h, toy_model.hpp:29)
+__host__ __device__ constexpr bool head_dim_supported(int hd) { return hd == 64 || hd == 128; }
 constexpr int kTagCount = 10;     // grammar.hpp:47 kTagLiteralCount
 
 // Tag ids (tokenizer.cpp:56-63 / grammar.hpp:34-46).
@@ -56,22 +58,23 @@ __host__ __device__ inline PageRef make_ref(int page, int begin, int count) {
 }
 
 // ---------------------------------------------------------------------------
-// KV plane layout (one plane per layer for K, one for V): head-major [kv_head][page][4 KiB block];
-//   the block holds token t, dim d at atom (t >> 3, d >> 6) of 1 KiB = 8 token rows x 128 B, atoms
-//   ordered [t >> 3][d >> 6], 16-byte chunk c of row r stored at chunk c ^ r (SWIZZLE_128B per atom).
+// KV plane layout (one plane per layer for K, one for V): head-major [kv_head][page][16 x hd block]
+//   (hd = head dim, 128 or 64); the block holds token t, dim d at atom (t >> 3, d >> 6) of 1 KiB =
+//   8 token rows x 128 B, atoms ordered [t >> 3][d >> 6], 16-byte chunk c of row r stored at chunk
+//   c ^ r (SWIZZLE_128B per atom).
 // Consecutive page-head blocks of one KV head therefore form canonical UMMA operands with one 1-D bulk
-// copy per page: K-major for Q.K^T (N = tokens: 8-row groups 2048 B apart, dims 64..127 at +1024 B) and
-// MN-major for P.V (N = dims: atoms 1024 B apart, K = tokens: 8-row groups 2048 B apart) — no
-// shared-memory re-layout.  Head-major: pages p..p+3 of one head are 16 KiB of contiguous HBM, so a
-// table block of consecutive page ids (bulk allocations hand out ascending runs) is ONE bulk copy.
+// copy per page: K-major for Q.K^T (N = tokens: 8-row groups hd * 16 B apart, dims 64..127 at +1024 B)
+// and MN-major for P.V (N = dims: atoms 1024 B apart, K = tokens: 8-row groups hd * 16 B apart) — no
+// shared-memory re-layout.  Head-major: pages p..p+3 of one head are contiguous HBM, so a table block
+// of consecutive page ids (bulk allocations hand out ascending runs) is ONE bulk copy.
 // ---------------------------------------------------------------------------
 __host__ __device__ inline int swz_chunk(int token, int chunk) { return chunk ^ (token & 7); }
 // element offset of 16-byte chunk c (dims 8c..8c+7) of token slot t inside a page-head block
-__host__ __device__ inline int kv_chunk_offset(int t, int c) {
-  return ((((t >> 3) * 2 + (c >> 3)) * 8 + (t & 7)) * 64) + ((((c & 7) ^ (t & 7))) << 3);
+__host__ __device__ inline int kv_chunk_offset(int t, int c, int hd) {
+  return ((((t >> 3) * (hd >> 6) + (c >> 3)) * 8 + (t & 7)) * 64) + ((((c & 7) ^ (t & 7))) << 3);
 }
-__host__ __device__ inline size_t kv_page_head_offset(int64_t page, int head, int64_t num_pages) {
-  return ((size_t)head * (size_t)num_pages + (size_t)page) * (kPageTokens * kHeadDim);
+__host__ __device__ inline size_t kv_page_head_offset(int64_t page, int head, int64_t num_pages, int hd) {
+  return ((size_t)head * (size_t)num_pages + (size_t)page) * (size_t)(kPageTokens * hd);
 }
 
 // ---------------------------------------------------------------------------
@@ -226,16 +229,18 @@ __device__ __forceinline__ float2 poly_exp2x2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-// Interleaved rotary map (toy_model.cpp:30-41): pair t of a 128-dim head rotates by
+// Interleaved rotary map (toy_model.cpp:30-41): pair t of an hd-dim head rotates by
 // theta = pos * base^(-2t/dh). The inverse frequencies are computed on the host with the same
 // std::pow expression as the reference, theta is formed and range-reduced in fp64 (positions
 // reach 1e5 rad), and only the final sincos runs in fp32.
 struct RopeTable {
-  double inv[kHeadDim / 2];
+  double inv[kMaxHeadDim / 2];  // hd / 2 pairs used
+  int32_t hd;                   // head dim of the rotated vectors (and of the K/V rows the kernels write)
 };
-inline RopeTable make_rope_table(double base) {
+inline RopeTable make_rope_table(double base, int hd) {
   RopeTable t;
-  for (int i = 0; i < kHeadDim / 2; ++i) t.inv[i] = std::pow(base, -2.0 * (double)i / (double)kHeadDim);
+  t.hd = hd;
+  for (int i = 0; i < kMaxHeadDim / 2; ++i) t.inv[i] = i < hd / 2 ? std::pow(base, -2.0 * (double)i / (double)hd) : 0.0;
   return t;
 }
 // Stages the frequency table in shared memory.  Indexing the by-value kernel-parameter copy
@@ -243,7 +248,7 @@ inline RopeTable make_rope_table(double base) {
 // warp), which made the RoPE passes ~4x slower than their HBM bound.  Call before any early
 // return (it contains a block barrier).
 __device__ __forceinline__ const double* rope_stage(const RopeTable& rt, double* s_inv) {
-  for (int t = threadIdx.x; t < kHeadDim / 2; t += blockDim.x) s_inv[t] = rt.inv[t];
+  for (int t = threadIdx.x; t < kMaxHeadDim / 2; t += blockDim.x) s_inv[t] = rt.inv[t];
   __syncthreads();
   return s_inv;
 }

@@ -57,7 +57,9 @@ constexpr int kThreads = 512;                               // 16 warps
 // quadrant w % 4.  Query rows fill quadrants from 0, so the latency-critical MMA issuers sit on
 // sub-partitions 3 (QK) and 2 (PV), idle unless a unit has > 64 rows.
 constexpr int kWarpStage = 0, kWarpTma = 1, kWarpPv = 2, kWarpQk = 3;
-constexpr int kPageBytes = kPageTokens * kHeadDim * 2;      // 4 KiB page-head block
+constexpr int kPageBytes = kPageTokens * kHeadDim * 2;      // 4 KiB page-head block at head dim 128 (ring slots are sized
+                                                            // for it; head dim 64 fills half of each slot / Q tile)
+template <int HD> constexpr int page_bytes() { return kPageTokens * HD * 2; }
 constexpr int kBlkPages = 4;                                // pages per block (one QK MMA chain)
 constexpr int kBlkCols = kBlkPages * kPageTokens;           // 64 S columns per block
 constexpr int kKSlots = 5, kVSlots = 6;                     // K / V rings, one block (4 pages) per slot (5/6 measured best against 4/7, 6/5, 3/8)
@@ -108,13 +110,13 @@ constexpr int kSmem = kOffTmem + 16 + 1024;  // + 1 KiB alignment slack
 static_assert(kSmem <= 227 * 1024, "decode smem");
 
 constexpr uint32_t kIdQK = tc::idesc_bf16(128, kBlkCols, 0, 0);  // S(128 x 64) = Q . K_blk^T
-constexpr uint32_t kIdPV = tc::idesc_bf16(128, 128, 0, 1);  // O(128 x 128) += P_page . V_page
+template <int HD> constexpr uint32_t id_pv() { return tc::idesc_bf16(128, HD, 0, 1); }  // O(128 x HD) += P_page . V_page
 
 struct DecodeParams {
   const PageRef* arena;
   const __nv_bfloat16* kplane;
   const __nv_bfloat16* vplane;
-  const __nv_bfloat16* q_tile;  // [n][kv_heads][2][R][64] RoPE'd, swizzled (rope_q_tile_kernel)
+  const __nv_bfloat16* q_tile;  // [n][kv_heads][HD / 64][R][64] RoPE'd, swizzled (rope_q_tile_kernel)
   const WorkItem* units;
   int n_units;
   int* work_counter;
@@ -130,13 +132,14 @@ struct DecodeParams {
   float scale_log2;
 };
 
+template <int HD>
 __device__ __forceinline__ void store_row(const DecodeParams& P, int64_t row, int c, const float* o, float inv) {
   if (P.out_f32) {
-    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + row * kHeadDim + c * 32);
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + row * HD + c * 32);
 #pragma unroll
     for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
   } else {
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + row * kHeadDim + c * 32);
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + row * HD + c * 32);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
@@ -146,13 +149,14 @@ __device__ __forceinline__ void store_row(const DecodeParams& P, int64_t row, in
 
 // MMA issue helpers with compile-time TMEM operands: the issuing thread then needs no per-MMA
 // register -> uniform-register moves (which the compiler otherwise wraps in an ELECT loop).
+template <int HD>
 __device__ __forceinline__ void store_row16(const DecodeParams& P, int64_t row, int k, const float* o, float inv) {
   if (P.out_f32) {
-    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + row * kHeadDim + k * 16);
+    float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + row * HD + k * 16);
 #pragma unroll
     for (int e = 0; e < 4; ++e) dst[e] = make_float4(o[4 * e] * inv, o[4 * e + 1] * inv, o[4 * e + 2] * inv, o[4 * e + 3] * inv);
   } else {
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + row * kHeadDim + k * 16);
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(P.out) + row * HD + k * 16);
 #pragma unroll
     for (int e = 0; e < 2; ++e)
       dst[e] = make_uint4(pack_bf16(o[8 * e] * inv, o[8 * e + 1] * inv), pack_bf16(o[8 * e + 2] * inv, o[8 * e + 3] * inv),
@@ -160,24 +164,25 @@ __device__ __forceinline__ void store_row16(const DecodeParams& P, int64_t row, 
   }
 }
 
-template <int SB>
-__device__ __forceinline__ void issue_qk_mmas(uint64_t kd) {  // S_SB = Q . K_blk^T (A = Q in TMEM)
+template <int SB, int HD>
+__device__ __forceinline__ void issue_qk_mmas(uint64_t kd) {  // S_SB = Q . K_blk^T (A = Q in TMEM), HD / 16 K-steps
 #pragma unroll
-  for (int k = 0; k < 8; ++k)
+  for (int k = 0; k < HD / 16; ++k)
     tc::mma_ts(kColS + SB * kBlkCols, kColQ + k * 8, kd + (uint64_t)(((k >> 2) * 1024 + (k & 3) * 32) >> 4), kIdQK,
                k > 0 ? 1u : 0u);
 }
 // P of a block: each softmax part (W = 64 / (2F) tokens) is packed into the first W / 2 of its own
 // S columns, so page k's 16 tokens sit at packed column (k >> 1) * 32 + (k & 1) * 8 (F = 1) or
 // k * 16 (F = 2)
-template <int SB>
+template <int SB, int HD>
 __device__ __forceinline__ void issue_pv_mmas(uint64_t vd, int np, uint32_t acc0, int copies) {  // O += P_SB . V_blk
-  constexpr uint32_t ocol = kColO, pcol = kColS + SB * kBlkCols;
+  constexpr uint32_t ocol = kColO, pcol = kColS + SB * kBlkCols, id = id_pv<HD>();
+  constexpr int pb = page_bytes<HD>();
   const uint32_t p1 = copies == 1 ? 8 : 16, p2 = 32, p3 = copies == 1 ? 40 : 48;
-  tc::mma_ts(ocol, pcol, vd, kIdPV, acc0);
-  if (np > 1) tc::mma_ts(ocol, pcol + p1, vd + (uint64_t)(kPageBytes >> 4), kIdPV, 1u);
-  if (np > 2) tc::mma_ts(ocol, pcol + p2, vd + (uint64_t)((2 * kPageBytes) >> 4), kIdPV, 1u);
-  if (np > 3) tc::mma_ts(ocol, pcol + p3, vd + (uint64_t)((3 * kPageBytes) >> 4), kIdPV, 1u);
+  tc::mma_ts(ocol, pcol, vd, id, acc0);
+  if (np > 1) tc::mma_ts(ocol, pcol + p1, vd + (uint64_t)(pb >> 4), id, 1u);
+  if (np > 2) tc::mma_ts(ocol, pcol + p2, vd + (uint64_t)((2 * pb) >> 4), id, 1u);
+  if (np > 3) tc::mma_ts(ocol, pcol + p3, vd + (uint64_t)((3 * pb) >> 4), id, 1u);
 }
 // named barrier over the softmax warps holding one logical row quadrant, OR-reducing a predicate
 __device__ __forceinline__ bool group_any(int id, int count, bool pred) {
@@ -199,7 +204,7 @@ __device__ __forceinline__ void group_sync(int id, int count) {
 // into the other copies' parts of its rows, so every copy accumulates a disjoint slice of the
 // tokens into its own O rows (summed by the epilogue).  All 2F warps holding a logical row share
 // its reference max through one named barrier per block (OR-reduced "move" flag).
-template <int F>
+template <int F, int HD>
 __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int n_ent, int n_mem,
                                              const PageRef* se, int warp, int lane, uint32_t tmem, uint64_t* s_full,
                                              uint64_t* p_full, uint64_t* vempty, float* xmax, float& m_out,
@@ -213,7 +218,7 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
   const bool warp_active = lq * 32 < n_mem * P.R;  // uniform over the group
   const int part = c * 2 + half;
   const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-  const uint32_t ocol = lane_base + kColO + half * 64;
+  const uint32_t ocol = lane_base + kColO + half * (HD / 2);  // this warp half rescales HD / 2 O columns
   float* gmax = xmax + lq * (NP * 32);
   // named barrier per (copy layout, row quadrant group): units with different F never share an
   // id, so warps that run ahead into the next unit (inactive ones skip barriers) cannot mix
@@ -307,7 +312,7 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
           mbar_wait(&vempty[(g - 1) % kVSlots], ((g - 1) / kVSlots) & 1);
           tc::fence_after();
 #pragma unroll 1
-          for (int cc = 0; cc < 2; ++cc) {
+          for (int cc = 0; cc < HD / 64; ++cc) {
             float o[32];
             tc::tmem_ld32(ocol + cc * 32, o);
             tc::tmem_wait_ld();
@@ -331,12 +336,17 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
   m_out = m_ref;
   l_out = l;
 }
-__device__ __forceinline__ void issue_q_copy(uint64_t qd) {  // Q tile smem -> TMEM
+template <int HD>
+__device__ __forceinline__ void issue_q_copy(uint64_t qd) {  // Q tile smem -> TMEM (HD / 64 halves)
 #pragma unroll
-  for (int k = 0; k < 8; ++k) tc::cp_128x256b(kColQ + k * 8, qd + (uint64_t)(((k >> 2) * kQHalf + (k & 3) * 32) >> 4));
+  for (int k = 0; k < HD / 16; ++k) tc::cp_128x256b(kColQ + k * 8, qd + (uint64_t)(((k >> 2) * kQHalf + (k & 3) * 32) >> 4));
 }
 
+template <int HD>
 __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodeParams P) {
+  constexpr int kNH = HD / 64;                // Q / K / V 64-dim atoms per row
+  constexpr int kPB = page_bytes<HD>();       // page-head block bytes
+  constexpr int kRunBytes = kBlkPages * kPB;  // a 4-page block of consecutive pages
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
   uint8_t* ring = smem + kOffRing;
@@ -433,13 +443,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       if (i == 0) pdl_wait();  // the Q tile of this launch is complete and visible
       if (i >= 1) mbar_wait(q_free, (i - 1) & 1);  // the previous unit's Q tile is in TMEM
       const int copies = si->copies, rpc = 128 / copies;
-      if (lane == 0) mbar_arrive_expect_tx(&item_full[buf], 2u * half_bytes * (uint32_t)(n_mem * copies));
+      if (lane == 0) mbar_arrive_expect_tx(&item_full[buf], (uint32_t)kNH * half_bytes * (uint32_t)(n_mem * copies));
       __syncwarp();
-      if (lane < 2 * n_mem * copies) {  // (member, half, copy): n_mem * R * copies <= 128 rows
-        const int m = (lane >> 1) % n_mem, h = lane & 1, cp = (lane >> 1) / n_mem;
+      if (lane < kNH * n_mem * copies) {  // (member, half, copy): n_mem * R * copies <= 128 rows
+        const int m = (lane / kNH) % n_mem, h = lane % kNH, cp = (lane / kNH) / n_mem;
         const int b = si->members[m];
         uint8_t* dst = smem + kOffQ + h * kQHalf + (cp * rpc) * 128 + m * half_bytes;
-        const __nv_bfloat16* src = P.q_tile + (((size_t)b * P.kv_heads + kvh) * 2 + h) * (size_t)P.R * 64;
+        const __nv_bfloat16* src = P.q_tile + (((size_t)b * P.kv_heads + kvh) * kNH + h) * (size_t)P.R * 64;
         bulk_g2s(dst, src, half_bytes, &item_full[buf]);
       }
     }
@@ -453,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       // (tools/microbench/mb_gather.cu: random 4 KiB copies need several issuing lanes to approach
       // the HBM bandwidth, 16 KiB copies reach it from one)
       constexpr int kTmaGroups = kTmaLanesPerBlkGroup;
-      const size_t head_stride = (size_t)P.num_pages * kPageTokens * kHeadDim;
+      const size_t head_stride = (size_t)P.num_pages * kPageTokens * HD;
       const bool is_k = lane < 4 * kTmaGroups;
       const int sl_lane = lane % (4 * kTmaGroups);
       const int sub = sl_lane & 3, grp = sl_lane >> 2;
@@ -482,12 +492,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           const int pg = sub < np ? se[e0 + sub].page : -1;
           const int p0 = __shfl_sync(gmask, pg, lane & ~3);
           const bool run = __all_sync(gmask, np == kBlkPages && pg == p0 + sub);
-          if (sub == 0) mbar_arrive_expect_tx(&fb[sl], (uint32_t)np * kPageBytes);
+          if (sub == 0) mbar_arrive_expect_tx(&fb[sl], (uint32_t)np * kPB);
           __syncwarp(gmask);  // the expected bytes are registered before any copy can complete
           if (run) {
-            if (sub == 0) bulk_g2s(dst, hplane + (size_t)p0 * (kPageTokens * kHeadDim), kSlotBytes, &fb[sl]);
+            if (sub == 0) bulk_g2s(dst, hplane + (size_t)p0 * (kPageTokens * HD), kRunBytes, &fb[sl]);
           } else if (sub < np) {
-            bulk_g2s(dst + sub * kPageBytes, hplane + (size_t)pg * (kPageTokens * kHeadDim), kPageBytes, &fb[sl]);
+            bulk_g2s(dst + sub * kPB, hplane + (size_t)pg * (kPageTokens * HD), kPB, &fb[sl]);
           }
         }
         g0 += nblk;
@@ -501,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
     // Both issuers run converged with one elected lane issuing (prefill_tc3.cu: warp-uniform
     // descriptors stay in uniform registers, no per-MMA waterfall on an SMSP shared with softmax warps).
     const uint64_t qdesc0 = tc::sw128_desc(smem_u32(smem + kOffQ), 16, 1024);
-    const uint64_t kdesc0 = tc::sw128_desc(smem_u32(ring), 16, 2048);
+    const uint64_t kdesc0 = tc::sw128_desc(smem_u32(ring), 16, 16 * HD);  // 8-token groups 16 * HD bytes apart
     int g = 0;
     for (int i = 0;; ++i) {
       const int ub = i & 1;
@@ -513,7 +523,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       tc::fence_after();
       // the unit's Q tile smem -> TMEM (ordered after the previous unit's QK MMAs)
       if (tc::elect_one()) {
-        issue_q_copy(qdesc0);
+        issue_q_copy<HD>(qdesc0);
         tc::mma_commit(q_free);
       }
       __syncwarp();
@@ -525,11 +535,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         const uint64_t kd = kdesc0 + (uint64_t)(sl * (kSlotBytes >> 4));
         if (tc::elect_one()) {
           switch (sb) {
-            case 0: issue_qk_mmas<0>(kd); break;
-            case 1: issue_qk_mmas<1>(kd); break;
-            case 2: issue_qk_mmas<2>(kd); break;
-            case 3: issue_qk_mmas<3>(kd); break;
-            default: issue_qk_mmas<4>(kd); break;
+            case 0: issue_qk_mmas<0, HD>(kd); break;
+            case 1: issue_qk_mmas<1, HD>(kd); break;
+            case 2: issue_qk_mmas<2, HD>(kd); break;
+            case 3: issue_qk_mmas<3, HD>(kd); break;
+            default: issue_qk_mmas<4, HD>(kd); break;
           }
           tc::mma_commit(&s_full[sb]);
           tc::mma_commit(&kempty[sl]);
@@ -541,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
     }
   } else if (warp == kWarpPv) {
     // ---------------- PV issuer: O_par += P_g . V_g per block ----------------
-    const uint64_t vdesc0 = tc::sw128_desc(smem_u32(smem + kOffVRing), 1024, 2048);
+    const uint64_t vdesc0 = tc::sw128_desc(smem_u32(smem + kOffVRing), 1024, 16 * HD);
     int g = 0;
     for (int i = 0;; ++i) {
       const int ub = i & 1;
@@ -563,11 +573,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         const uint32_t acc0 = blk > 0 ? 1u : 0u;  // the unit's first block opens O
         if (tc::elect_one()) {
           switch (sb) {
-            case 0: issue_pv_mmas<0>(vd, np, acc0, copies); break;
-            case 1: issue_pv_mmas<1>(vd, np, acc0, copies); break;
-            case 2: issue_pv_mmas<2>(vd, np, acc0, copies); break;
-            case 3: issue_pv_mmas<3>(vd, np, acc0, copies); break;
-            default: issue_pv_mmas<4>(vd, np, acc0, copies); break;
+            case 0: issue_pv_mmas<0, HD>(vd, np, acc0, copies); break;
+            case 1: issue_pv_mmas<1, HD>(vd, np, acc0, copies); break;
+            case 2: issue_pv_mmas<2, HD>(vd, np, acc0, copies); break;
+            case 3: issue_pv_mmas<3, HD>(vd, np, acc0, copies); break;
+            default: issue_pv_mmas<4, HD>(vd, np, acc0, copies); break;
           }
           tc::mma_commit(&vempty[g % kVSlots]);  // also certifies PV(g) to the softmax (O rescale)
           tc::mma_commit(&pv_done[sb]);
@@ -597,9 +607,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       const PageRef* se = s_ent0 + buf * kMaxEntries;
       float m_ref, l;
       if (copies == 2)
-        softmax_unit<2>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
+        softmax_unit<2, HD>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
       else
-        softmax_unit<1>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
+        softmax_unit<1, HD>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
       // hand (m, l_half) and the unit header to the epilogue, release the unit slot
       if (i >= 1) mbar_wait(o_empty, (i - 1) & 1);
       s_stat[half * 128 + r] = make_float2(m_ref, l);
@@ -638,7 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       const float inv = ml.y > 0.f ? 1.f / ml.y : 0.f;
       if (F == 1) {
 #pragma unroll 1
-        for (int k = 0; k < 4; ++k) {  // 32-column chunks of O
+        for (int k = 0; k < HD / 32; ++k) {  // 32-column chunks of O
           float o[32];
           if (warp_active) {
             tc::tmem_ld32(lane_base + kColO + k * 32, o);
@@ -646,9 +656,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           }
           if (active) {
             if (nslots == 1) {
-              store_row(P, orow, k, o, inv);
+              store_row<HD>(P, orow, k, o, inv);
             } else {
-              float4* dst = reinterpret_cast<float4*>(P.part_o + (slot * P.q_heads + head) * kHeadDim + k * 32);
+              float4* dst = reinterpret_cast<float4*>(P.part_o + (slot * P.q_heads + head) * HD + k * 32);
 #pragma unroll
               for (int e = 0; e < 8; ++e) __stcg(dst + e, make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]));
             }
@@ -656,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         }
       } else {
 #pragma unroll 1
-        for (int k = 0; k < 8; ++k) {  // 16-column chunks of O
+        for (int k = 0; k < HD / 16; ++k) {  // 16-column chunks of O
           float o[16];
           if (warp_active) {
             tc::tmem_ldN<16>(lane_base + kColO + k * 16, o);
@@ -682,9 +692,9 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
           }
           if (active) {
             if (nslots == 1) {
-              store_row16(P, orow, k, o, inv);
+              store_row16<HD>(P, orow, k, o, inv);
             } else {
-              float4* dst = reinterpret_cast<float4*>(P.part_o + (slot * P.q_heads + head) * kHeadDim + k * 16);
+              float4* dst = reinterpret_cast<float4*>(P.part_o + (slot * P.q_heads + head) * HD + k * 16);
   #pragma unroll
               for (int e = 0; e < 4; ++e) __stcg(dst + e, make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]));
             }
@@ -720,7 +730,7 @@ constexpr int kCombineWarps = 4;
 __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(
     const float* __restrict__ part_o, const float2* __restrict__ part_ml, const int32_t* __restrict__ multi,
     int n_multi, const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ slot_idx, int q_heads,
-    void* __restrict__ out, int out_f32, int wide) {
+    void* __restrict__ out, int out_f32, int wide, int hd) {
   pdl_wait();  // programmatic launch behind decode_tc_kernel: its partials are visible after this
   pdl_launch_dependents();  // the next step's append may start its launch
   __shared__ float s_m[kCombineWarps], s_l[kCombineWarps];
@@ -741,13 +751,15 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(
     l = l * a + w * ml.y;
     m = nm;
   };
+  const bool dims = lane * 4 < hd;  // float4 of dims per lane (lanes 16-31 idle at head dim 64)
   for (int s = first; s < s1; s += 2 * step) {
     const int64_t sa = slot_idx[s];
     const bool two = s + step < s1;
     const int64_t sb = two ? slot_idx[s + step] : sa;
     const float2 mla = part_ml[sa * q_heads + h], mlb = part_ml[sb * q_heads + h];
-    const float4 va = *reinterpret_cast<const float4*>(&part_o[(sa * q_heads + h) * kHeadDim + lane * 4]);
-    const float4 vb = *reinterpret_cast<const float4*>(&part_o[(sb * q_heads + h) * kHeadDim + lane * 4]);
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 va = dims ? *reinterpret_cast<const float4*>(&part_o[(sa * q_heads + h) * hd + lane * 4]) : z4;
+    const float4 vb = dims ? *reinterpret_cast<const float4*>(&part_o[(sb * q_heads + h) * hd + lane * 4]) : z4;
     merge(mla, va);
     if (two) merge(mlb, vb);
   }
@@ -765,7 +777,8 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(
     for (int w = 0; w < kCombineWarps; ++w) merge(make_float2(s_m[w], s_l[w]), s_acc[w][lane]);
   }
   const float inv = l > 0.f ? 1.f / l : 0.f;
-  const int64_t at = ((int64_t)b * q_heads + h) * kHeadDim + lane * 4;
+  const int64_t at = ((int64_t)b * q_heads + h) * hd + lane * 4;
+  if (!dims) return;
   if (out_f32) {
     *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + at) =
         make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
@@ -778,7 +791,7 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(
 }
 
 // RoPE pre-pass: rotates every query once (toy_model.cpp:30-41 at the handle's position) and
-// writes it as the decode kernel's Q operand tile [n][kv_heads][2 halves][R rows][64 dims],
+// writes it as the decode kernel's Q operand tile [n][kv_heads][hd / 64 halves][R rows][64 dims],
 // SWIZZLE_128B (chunk c of row hl at c ^ (hl & 7)); rows hl >= gqa are zero.  One thread per
 // 16-byte chunk.
 __global__ void rope_q_tile_kernel(const __nv_bfloat16* __restrict__ q, const int32_t* __restrict__ pos, int n,
@@ -788,19 +801,20 @@ __global__ void rope_q_tile_kernel(const __nv_bfloat16* __restrict__ q, const in
   // own griddepcontrol.wait
   pdl_wait();
   pdl_launch_dependents();  // decode_tc may start its prologue (every CTA of this grid is running)
-  __shared__ double s_inv[kHeadDim / 2];
+  __shared__ double s_inv[kMaxHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
+  const int hd = rt.hd, lg = hd == 128 ? 4 : 3;  // log2 16-byte chunks per row
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)n * kv_heads * R * 16;
+  const int64_t total = ((int64_t)n * kv_heads * R) << lg;
   if (x >= total) return;
-  const int c = (int)(x & 15);           // 16-byte chunk of the 128-dim row
-  const int hl = (int)((x >> 4) % R);
-  const int64_t bk = (x >> 4) / R;       // b * kv_heads + kvh
+  const int c = (int)(x & ((1 << lg) - 1));  // 16-byte chunk of the hd-dim row
+  const int hl = (int)((x >> lg) % R);
+  const int64_t bk = (x >> lg) / R;          // b * kv_heads + kvh
   const int b = (int)(bk / kv_heads), kvh = (int)(bk % kv_heads);
   uint4 v = make_uint4(0, 0, 0, 0);
   if (hl < gqa) {
     const int head = kvh * gqa + hl;
-    v = *reinterpret_cast<const uint4*>(q + ((int64_t)b * kv_heads * gqa + head) * kHeadDim + c * 8);
+    v = *reinterpret_cast<const uint4*>(q + ((int64_t)b * kv_heads * gqa + head) * hd + c * 8);
     __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&v);
     const int p = pos[b];
 #pragma unroll
@@ -812,7 +826,7 @@ __global__ void rope_q_tile_kernel(const __nv_bfloat16* __restrict__ q, const in
     }
   }
   const int half = c >> 3, cc = c & 7;
-  const int64_t dst = ((bk * 2 + half) * R + hl) * 64 + ((cc ^ (hl & 7)) << 3);
+  const int64_t dst = ((bk * (hd >> 6) + half) * R + hl) * 64 + ((cc ^ (hl & 7)) << 3);
   *reinterpret_cast<uint4*>(tile + dst) = v;
 }
 
@@ -1074,7 +1088,8 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   if (!st.plan) st.plan = new DecodePlanCache();
   DecodePlanCache& pc = *st.plan;
   if (!pc.smem_set) {
-    MV_CUDA_TRY(cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    MV_CUDA_TRY(cudaFuncSetAttribute(decode_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    MV_CUDA_TRY(cudaFuncSetAttribute(decode_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
     int dev = 0;
     MV_CUDA_TRY(cudaGetDevice(&dev));
     MV_CUDA_TRY(cudaDeviceGetAttribute(&pc.num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1153,7 +1168,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     if (pc.cap_slots != old_slots || !pc.d_part_o) {
       cudaFree(pc.d_part_o);
       pc.d_part_o = nullptr;
-      MV_CUDA_TRY(cudaMalloc(&pc.d_part_o, sizeof(float) * pc.cap_slots * kHeadDim));
+      MV_CUDA_TRY(cudaMalloc(&pc.d_part_o, sizeof(float) * pc.cap_slots * kMaxHeadDim));
     }
     MV_CUDA_TRY(cudaMemcpyAsync(pc.d_units, pc.units.data(), sizeof(WorkItem) * pc.units.size(),
                                 cudaMemcpyHostToDevice, stream));
@@ -1167,9 +1182,10 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     // acceptable for a full re-plan; in-place updates above use pinned staging)
   }
   const int R = rows_per_member(gqa);
-  if (mv_status e = ensure_dev(pc.d_q_tile, pc.cap_q, (size_t)n * cfg.kv_heads * 2 * R * 64)) return e;
+  const int hd = cfg.head_dim;
+  if (mv_status e = ensure_dev(pc.d_q_tile, pc.cap_q, (size_t)n * cfg.kv_heads * R * hd)) return e;
   {
-    const int64_t chunks = (int64_t)n * cfg.kv_heads * R * 16;
+    const int64_t chunks = (int64_t)n * cfg.kv_heads * R * (hd / 8);
     cudaLaunchAttribute pdl[1];
     pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     pdl[0].val.programmaticStreamSerializationAllowed = 1;
@@ -1203,7 +1219,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   P.q_heads = q_heads;
   P.gqa = gqa;
   P.R = R;
-  P.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
+  P.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
   const int grid = std::min(P.n_units, pc.num_sms);
   // decode_tc and combine are launched programmatically dependent on the kernel before them
   // (PDL): their launch latency and prologue overlap the predecessor's tail
@@ -1217,7 +1233,8 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   lc.stream = stream;
   lc.attrs = pdl;
   lc.numAttrs = 1;
-  MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel, P));
+  if (hd == 128) MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel<128>, P));
+  else MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel<64>, P));
   MV_LAUNCH_CHECK();
   if (!pc.multi.empty()) {
     int max_slots = 0;
@@ -1229,7 +1246,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     lc.dynamicSmemBytes = 0;
     MV_CUDA_TRY(cudaLaunchKernelEx(&lc, combine_kernel, (const float*)pc.d_part_o, (const float2*)pc.d_part_ml,
                                    (const int32_t*)pc.d_multi, (int)pc.multi.size(), (const int32_t*)pc.d_slot_ptr,
-                                   (const int32_t*)pc.d_slot_idx, q_heads, d_out, (int)(out_dtype == 1), wide));
+                                   (const int32_t*)pc.d_slot_idx, q_heads, d_out, (int)(out_dtype == 1), wide, hd));
     MV_LAUNCH_CHECK();
   }
   return MV_OK;

@@ -696,7 +696,7 @@ static mv_status engine_store(mv_toy* toy, const mv_engine_options* opt, mv_kv_s
   kc.num_pages = opt && opt->num_pages > 0 ? opt->num_pages : 4096;
   kc.layers = c.layers;
   kc.kv_heads = c.heads;
-  kc.head_dim = kHeadDim;
+  kc.head_dim = mv_attn_head_dim(c.model_dim / c.heads);
   kc.rope_base = c.rope_base;
   return mv_kv_store_create(&kc, out);
 }

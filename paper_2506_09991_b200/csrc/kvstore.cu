@@ -193,15 +193,16 @@ __device__ __forceinline__ void rope8(uint4& v, int pos, int chunk, const double
 __device__ __forceinline__ void write_kv_token(__nv_bfloat16* kp, __nv_bfloat16* vp, int64_t page, int slot,
                                                int kv_heads, int64_t npages, const __nv_bfloat16* k,
                                                const __nv_bfloat16* v, int pos, const double* inv, int lane,
-                                               int nlanes, int first = 0) {
-  // kv_heads * 16 chunks of 8 dims (from chunk `first`); K rotated, V verbatim; stored chunk-swizzled.
-  for (int j = first + lane; j < kv_heads * 16; j += nlanes) {
-    int h = j >> 4, c = j & 15;
-    size_t dst = kv_page_head_offset(page, h, npages) + (size_t)kv_chunk_offset(slot, c);
-    uint4 kk = *reinterpret_cast<const uint4*>(k + (size_t)h * kHeadDim + c * 8);
+                                               int nlanes, int hd, int first = 0) {
+  // kv_heads * hd / 8 chunks of 8 dims (from chunk `first`); K rotated, V verbatim; stored chunk-swizzled.
+  const int lg = hd == 128 ? 4 : 3;  // log2 chunks per head
+  for (int j = first + lane; j < (kv_heads << lg); j += nlanes) {
+    int h = j >> lg, c = j & ((1 << lg) - 1);
+    size_t dst = kv_page_head_offset(page, h, npages, hd) + (size_t)kv_chunk_offset(slot, c, hd);
+    uint4 kk = *reinterpret_cast<const uint4*>(k + (size_t)h * hd + c * 8);
     rope8(kk, pos, c, inv);
     *reinterpret_cast<uint4*>(kp + dst) = kk;
-    *reinterpret_cast<uint4*>(vp + dst) = *reinterpret_cast<const uint4*>(v + (size_t)h * kHeadDim + c * 8);
+    *reinterpret_cast<uint4*>(vp + dst) = *reinterpret_cast<const uint4*>(v + (size_t)h * hd + c * 8);
   }
 }
 
@@ -211,7 +212,7 @@ __global__ void k_append_data(AppendPlan pl, const int32_t* __restrict__ page_ou
                               const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                               const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads,
                               int64_t npages, const RopeTable rt) {
-  __shared__ double s_inv[kHeadDim / 2];
+  __shared__ double s_inv[kMaxHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   // one warp per token
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -234,8 +235,8 @@ __global__ void k_append_data(AppendPlan pl, const int32_t* __restrict__ page_ou
   if (rec_in && rec_bytes > 0)
     for (int b = lane; b < rec_bytes; b += 32) records[gslot * rec_bytes + b] = rec_in[(int64_t)t * rec_bytes + b];
   if (k && v)
-    write_kv_token(kp, vp, page, slot, kv_heads, npages, k + (size_t)t * kv_heads * kHeadDim,
-                   v + (size_t)t * kv_heads * kHeadDim, pos ? pos[t] : 0, inv, lane, 32);
+    write_kv_token(kp, vp, page, slot, kv_heads, npages, k + (size_t)t * kv_heads * rt.hd,
+                   v + (size_t)t * kv_heads * rt.hd, pos ? pos[t] : 0, inv, lane, 32, rt.hd);
 }
 
 // Engine fast path: one token per handle, in place (one warp per handle, 4 per CTA).
@@ -257,16 +258,17 @@ __device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef
                                                 const __nv_bfloat16* __restrict__ k,
                                                 const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp,
                                                 __nv_bfloat16* vp, int kv_heads, int64_t npages,
-                                                const double* inv) {
+                                                const double* inv, int hd) {
   const int lane = threadIdx.x & 31;
   // programmatic launch: the inputs (k, v, positions, tokens) may be produced by the kernel
   // this one overlaps (e.g. the caller's projection GEMM), so nothing is read before this wait;
   // only the launch latency and the frequency staging overlap the predecessor
   pdl_wait();
   const bool kv = k && v;
-  const int nch = kv ? kv_heads * 16 : 0;  // 16-byte chunks of the token's K (and V)
-  const __nv_bfloat16* kt = kv ? k + (size_t)i * kv_heads * kHeadDim : nullptr;
-  const __nv_bfloat16* vt = kv ? v + (size_t)i * kv_heads * kHeadDim : nullptr;
+  const int lg = hd == 128 ? 4 : 3;  // log2 16-byte chunks per head
+  const int nch = kv ? kv_heads << lg : 0;  // 16-byte chunks of the token's K (and V)
+  const __nv_bfloat16* kt = kv ? k + (size_t)i * kv_heads * hd : nullptr;
+  const __nv_bfloat16* vt = kv ? v + (size_t)i * kv_heads * hd : nullptr;
   uint4 kk[4], vv[4];
   const int p = kv ? __ldg(pos + i) : 0;
 #pragma unroll
@@ -302,7 +304,7 @@ __device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef
   }
 #pragma unroll
   for (int u = 0; u < 4; ++u)
-    if (lane + 32 * u < nch) rope8(kk[u], p, (lane + 32 * u) & 15, inv);
+    if (lane + 32 * u < nch) rope8(kk[u], p, (lane + 32 * u) & ((1 << lg) - 1), inv);
   page = __shfl_sync(0xffffffffu, page, 0);
   slot = __shfl_sync(0xffffffffu, slot, 0);
   if (page < 0 || !kv) return;
@@ -310,13 +312,13 @@ __device__ __forceinline__ void append_one_warp(const TokDesc td, int i, PageRef
   for (int u = 0; u < 4; ++u) {
     const int j = lane + 32 * u;
     if (j < nch) {
-      const size_t dst = kv_page_head_offset(page, j >> 4, npages) + (size_t)kv_chunk_offset(slot, j & 15);
+      const size_t dst = kv_page_head_offset(page, j >> lg, npages, hd) + (size_t)kv_chunk_offset(slot, j & ((1 << lg) - 1), hd);
       *reinterpret_cast<uint4*>(kp + dst) = kk[u];
       *reinterpret_cast<uint4*>(vp + dst) = vv[u];
     }
   }
-  if (nch > 128)  // more than 8 kv heads: the remaining chunks after the destination is known
-    write_kv_token(kp, vp, page, slot, kv_heads, npages, kt, vt, p, inv, lane, 32, 128);
+  if (nch > 128)  // more than 128 chunks (8 kv heads at hd 128): the rest after the destination is known
+    write_kv_token(kp, vp, page, slot, kv_heads, npages, kt, vt, p, inv, lane, 32, hd, 128);
 }
 
 __global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ cum, const TokDesc* __restrict__ d,
@@ -325,12 +327,12 @@ __global__ void k_append_one(PageRef* __restrict__ arena, int32_t* __restrict__ 
                              int32_t* __restrict__ free_top, int32_t* __restrict__ err, const int32_t* __restrict__ pos,
                              const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                              __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, int64_t npages, const RopeTable rt) {
-  __shared__ double s_inv[kHeadDim / 2];
+  __shared__ double s_inv[kMaxHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
   append_one_warp((threadIdx.x & 31) == 0 ? d[i] : TokDesc{0, 0, 0}, i, arena, cum, tokens, slot_tok, refcnt,
-                  free_stack, free_top, err, pos, k, v, kp, vp, kv_heads, npages, inv);
+                  free_stack, free_top, err, pos, k, v, kp, vp, kv_heads, npages, inv, rt.hd);
 }
 __global__ void k_append_one_inline(PageRef* __restrict__ arena, int32_t* __restrict__ cum, const TokDescInline d,
                                     int n, const int32_t* __restrict__ tokens, int32_t* __restrict__ slot_tok,
@@ -342,12 +344,12 @@ __global__ void k_append_one_inline(PageRef* __restrict__ arena, int32_t* __rest
   // the RoPE pre-pass after this kernel may launch now: it waits (griddepcontrol.wait) for this
   // grid to complete before touching anything, and only then releases decode_tc
   pdl_launch_dependents();
-  __shared__ double s_inv[kHeadDim / 2];
+  __shared__ double s_inv[kMaxHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
   append_one_warp(d.d[i], i, arena, cum, tokens, slot_tok, refcnt, free_stack, free_top, err, pos, k, v, kp, vp,
-                  kv_heads, npages, inv);
+                  kv_heads, npages, inv, rt.hd);
 }
 
 // K/V of the last token of each handle (for layers > the one written at append).
@@ -355,13 +357,13 @@ __global__ void k_write_last(const PageRef* __restrict__ arena, const int64_t* _
                              const int32_t* __restrict__ pos, const __nv_bfloat16* __restrict__ k,
                              const __nv_bfloat16* __restrict__ v, __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads,
                              int64_t npages, const RopeTable rt) {
-  __shared__ double s_inv[kHeadDim / 2];
+  __shared__ double s_inv[kMaxHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int i = blockIdx.x;
   PageRef r = arena[idx[i]];
   int slot = ref_begin(r) + ref_count(r) - 1;
-  write_kv_token(kp, vp, r.page, slot, kv_heads, npages, k + (size_t)i * kv_heads * kHeadDim,
-                 v + (size_t)i * kv_heads * kHeadDim, pos[i], inv, threadIdx.x, blockDim.x);
+  write_kv_token(kp, vp, r.page, slot, kv_heads, npages, k + (size_t)i * kv_heads * rt.hd,
+                 v + (size_t)i * kv_heads * rt.hd, pos[i], inv, threadIdx.x, blockDim.x, rt.hd);
 }
 
 // K/V of tokens [first, first + n) of one handle for one layer (multi-layer bulk prefill: layer 0 goes
@@ -371,7 +373,7 @@ __global__ void k_write_range(const PageRef* __restrict__ arena, const int32_t* 
                               int n_entries, int first, int n, const int32_t* __restrict__ pos,
                               const __nv_bfloat16* __restrict__ k, const __nv_bfloat16* __restrict__ v,
                               __nv_bfloat16* kp, __nv_bfloat16* vp, int kv_heads, int64_t npages, const RopeTable rt) {
-  __shared__ double s_inv[kHeadDim / 2];
+  __shared__ double s_inv[kMaxHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (w >= n) return;
@@ -384,8 +386,8 @@ __global__ void k_write_range(const PageRef* __restrict__ arena, const int32_t* 
   }
   const PageRef r = arena[off + lo];
   write_kv_token(kp, vp, r.page, ref_begin(r) + (t - cum[off + lo]), kv_heads, npages,
-                 k + (size_t)w * kv_heads * kHeadDim, v + (size_t)w * kv_heads * kHeadDim, pos ? pos[w] : 0, inv,
-                 lane, 32);
+                 k + (size_t)w * kv_heads * rt.hd, v + (size_t)w * kv_heads * rt.hd, pos ? pos[w] : 0, inv,
+                 lane, 32, rt.hd);
 }
 
 // resolve / resolve_payloads / resolve_slots / gather_kv: one thread block per entry.
@@ -393,7 +395,8 @@ __global__ void k_resolve(const PageRef* __restrict__ arena, const int32_t* __re
                           const int32_t* __restrict__ slot_tok, const uint8_t* __restrict__ records, int rec_bytes,
                           int32_t* __restrict__ tok_out, uint8_t* __restrict__ rec_out, uint32_t* __restrict__ slot_out,
                           const __nv_bfloat16* __restrict__ kp, const __nv_bfloat16* __restrict__ vp, int kv_heads,
-                          int64_t npages, __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out) {
+                          int64_t npages, __nv_bfloat16* __restrict__ k_out, __nv_bfloat16* __restrict__ v_out,
+                          int hd) {
   for (int e = blockIdx.x; e < n; e += gridDim.x) {
     PageRef r = arena[off + e];
     int c0 = cum[off + e];
@@ -407,11 +410,12 @@ __global__ void k_resolve(const PageRef* __restrict__ arena, const int32_t* __re
       for (int x = threadIdx.x; x < cnt * rec_bytes; x += blockDim.x)
         rec_out[(int64_t)c0 * rec_bytes + x] = records[((int64_t)r.page * kPageTokens + b) * rec_bytes + x];
     if (k_out)
-      for (int x = threadIdx.x; x < cnt * kv_heads * 16; x += blockDim.x) {
-        int t = x / (kv_heads * 16), h = (x / 16) % kv_heads, c = x % 16;
+      for (int x = threadIdx.x; x < cnt * kv_heads * (hd / 8); x += blockDim.x) {
+        const int ch = hd / 8;
+        int t = x / (kv_heads * ch), h = (x / ch) % kv_heads, c = x % ch;
         int slot = b + t;
-        size_t src = kv_page_head_offset(r.page, h, npages) + (size_t)kv_chunk_offset(slot, c);
-        size_t dst = ((size_t)(c0 + t) * kv_heads + h) * kHeadDim + c * 8;
+        size_t src = kv_page_head_offset(r.page, h, npages, hd) + (size_t)kv_chunk_offset(slot, c, hd);
+        size_t dst = ((size_t)(c0 + t) * kv_heads + h) * hd + c * 8;
         *reinterpret_cast<uint4*>(k_out + dst) = *reinterpret_cast<const uint4*>(kp + src);
         *reinterpret_cast<uint4*>(v_out + dst) = *reinterpret_cast<const uint4*>(vp + src);
       }
@@ -465,7 +469,7 @@ int32_t pow2_cap(int32_t need) {
 PagedStore::PagedStore(const mv_kv_config& cfg) : cfg_(cfg) {
   if (cfg_.table_entries <= 0) cfg_.table_entries = 4 * (int64_t)cfg_.num_pages + 65536;
   if (cfg_.rope_base <= 0) cfg_.rope_base = 10000.0;
-  rope_ = make_rope_table(cfg_.rope_base);
+  rope_ = make_rope_table(cfg_.rope_base, cfg_.head_dim > 0 ? cfg_.head_dim : kHeadDim);
 }
 
 PagedStore::~PagedStore() {
@@ -493,8 +497,8 @@ PagedStore::~PagedStore() {
 mv_status PagedStore::init() {
   if (cfg_.num_pages <= 0 || cfg_.record_bytes < 0 || cfg_.layers < 0 || cfg_.kv_heads < 0)
     return fail(MV_ERR_INVALID_ARGUMENT, "mv_kv_store_create: bad config");
-  if (cfg_.kv_heads > 0 && (cfg_.head_dim != kHeadDim || cfg_.layers < 1))
-    return fail(MV_ERR_INVALID_ARGUMENT, "mv_kv_store_create: attention plane needs head_dim 128 and layers >= 1");
+  if (cfg_.kv_heads > 0 && (!head_dim_supported(cfg_.head_dim) || cfg_.layers < 1))
+    return fail(MV_ERR_INVALID_ARGUMENT, "mv_kv_store_create: attention plane needs head_dim 64 or 128 and layers >= 1");
   const int64_t slots = (int64_t)cfg_.num_pages * kPageTokens;
   MV_CUDA_TRY(cudaMalloc(&d_arena, sizeof(PageRef) * cfg_.table_entries));
   MV_CUDA_TRY(cudaMalloc(&d_cum, sizeof(int32_t) * cfg_.table_entries));
@@ -507,7 +511,7 @@ mv_status PagedStore::init() {
   MV_CUDA_TRY(cudaMalloc(&d_slot_tok_, sizeof(int32_t) * slots));
   if (cfg_.record_bytes > 0) MV_CUDA_TRY(cudaMalloc(&d_records_, (size_t)slots * cfg_.record_bytes));
   if (cfg_.kv_heads > 0) {
-    size_t plane = (size_t)slots * cfg_.kv_heads * kHeadDim * sizeof(__nv_bfloat16);
+    size_t plane = (size_t)slots * cfg_.kv_heads * cfg_.head_dim * sizeof(__nv_bfloat16);
     for (int l = 0; l < cfg_.layers; ++l) {
       __nv_bfloat16 *k = nullptr, *v = nullptr;
       MV_CUDA_TRY(cudaMalloc(&k, plane));
@@ -934,7 +938,7 @@ mv_status PagedStore::resolve(uint64_t h, int32_t* tokens, void* payloads, uint3
   uint8_t* d_rec = pb ? d + tb + sb : nullptr;
   k_resolve<<<std::min(r->n_entries(), 148 * 16), 128, 0, stream_>>>(
       d_arena, d_cum, r->arena_off, r->n_entries(), d_slot_tok_, d_records_, cfg_.record_bytes, d_tok, d_rec, d_slot,
-      nullptr, nullptr, cfg_.kv_heads, (int64_t)cfg_.num_pages, nullptr, nullptr);
+      nullptr, nullptr, cfg_.kv_heads, (int64_t)cfg_.num_pages, nullptr, nullptr, rope_.hd);
   MV_LAUNCH_CHECK();
   if (tb) MV_CUDA_TRY(cudaMemcpyAsync(tokens, d_tok, tb, cudaMemcpyDeviceToHost, stream_));
   if (sb) MV_CUDA_TRY(cudaMemcpyAsync(slots, d_slot, sb, cudaMemcpyDeviceToHost, stream_));
@@ -1107,7 +1111,7 @@ mv_status PagedStore::gather_kv(uint64_t h, int32_t layer, void* d_k, void* d_v)
   k_resolve<<<std::min(r->n_entries(), 148 * 16), 128, 0, stream_>>>(
       d_arena, d_cum, r->arena_off, r->n_entries(), d_slot_tok_, d_records_, cfg_.record_bytes, nullptr, nullptr,
       nullptr, k_planes_[layer], v_planes_[layer], cfg_.kv_heads, (int64_t)cfg_.num_pages, (__nv_bfloat16*)d_k,
-      (__nv_bfloat16*)d_v);
+      (__nv_bfloat16*)d_v, rope_.hd);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }

@@ -33,17 +33,18 @@ __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __res
                                                       int32_t* __restrict__ counters) {
   // re-arm the attention kernel's work queue (it runs after this kernel on the same stream)
   if (counters && blockIdx.x == 0 && threadIdx.x < 2) counters[threadIdx.x] = 0;
-  __shared__ double s_inv[kHeadDim / 2];
+  __shared__ double s_inv[kMaxHeadDim / 2];
   const double* inv = rope_stage(rt, s_inv);
+  const int hd = rt.hd, lg = hd == 128 ? 4 : 3, ch = 1 << lg;  // 16-byte chunks per head row
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (x >= (int64_t)n * 16) return;
-  const int row = (int)(x >> 4), c = (int)(x & 15);
+  if (x >= ((int64_t)n << lg)) return;
+  const int row = (int)(x >> lg), c = (int)(x & (ch - 1));
   const int p = __ldg(pos + row);
   float cs[4], sn[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) rope_cs(p, inv[c * 4 + j], cs[j], sn[j]);
   if (table) {  // (cos, sin) per row and pair for the prefill kernel's in-place Q rotation
-    float4* tb = reinterpret_cast<float4*>(table + (size_t)row * 64 + c * 4);
+    float4* tb = reinterpret_cast<float4*>(table + (size_t)row * (hd / 2) + c * 4);
     tb[0] = make_float4(cs[0], sn[0], cs[1], sn[1]);
     tb[1] = make_float4(cs[2], sn[2], cs[3], sn[3]);
   }
@@ -56,11 +57,11 @@ __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __res
     }
     return v;
   };
-  const uint4* qs = reinterpret_cast<const uint4*>(q + (size_t)row * hq * kHeadDim) + c;
-  uint4* qd = reinterpret_cast<uint4*>(q_rot + (size_t)row * hq * kHeadDim) + c;
+  const uint4* qs = reinterpret_cast<const uint4*>(q + (size_t)row * hq * hd) + c;
+  uint4* qd = reinterpret_cast<uint4*>(q_rot + (size_t)row * hq * hd) + c;
   // q heads then k heads as one sequence of 16-byte chunks, 8 independent loads in flight
-  const uint4* ks = reinterpret_cast<const uint4*>(k + (size_t)row * hkv * kHeadDim) + c;
-  uint4* kd = reinterpret_cast<uint4*>(k_rot + (size_t)row * hkv * kHeadDim) + c;
+  const uint4* ks = reinterpret_cast<const uint4*>(k + (size_t)row * hkv * hd) + c;
+  uint4* kd = reinterpret_cast<uint4*>(k_rot + (size_t)row * hkv * hd) + c;
   const int nq = q_rot ? hq : 0;  // without q_rot only K is rotated (Q rotates in the kernel)
   const int nh = nq + hkv;
   for (int h0 = 0; h0 < nh; h0 += 8) {
@@ -68,12 +69,12 @@ __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __res
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int h = h0 + u;
-      if (h < nh) v[u] = __ldg(h < nq ? qs + h * 16 : ks + (h - nq) * 16);
+      if (h < nh) v[u] = __ldg(h < nq ? qs + h * ch : ks + (h - nq) * ch);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int h = h0 + u;
-      if (h < nh) *(h < nq ? qd + h * 16 : kd + (h - nq) * 16) = rot(v[u]);
+      if (h < nh) *(h < nq ? qd + h * ch : kd + (h - nq) * ch) = rot(v[u]);
     }
   }
 }
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(256) rope_qk_kernel(const __nv_bfloat16* __res
 namespace mv {
 mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
                              const float2* cs, const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
-                             int32_t kv_heads, void* d_out, int32_t out_dtype, const int32_t* hcount,
+                             int32_t kv_heads, int32_t head_dim, void* d_out, int32_t out_dtype, const int32_t* hcount,
                              const int32_t* tlist, int32_t stride, int32_t* counters, cudaStream_t st);
 mv_status tile_map2(const int32_t* d_excl, int32_t n, int32_t max_depth, uint8_t* d_status, int32_t* d_count,
                     int32_t* d_list, int32_t stride, cudaStream_t stream, int32_t* d_hcount, int32_t* d_hlist);
@@ -98,8 +99,8 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // Workspace carve-up (all per call: two prefills on different streams share nothing).
 struct PrefillWs {
-  float2* cs;         // [n][64] RoPE (cos, sin) per row and pair
-  __nv_bfloat16* k_rot;  // [n][kv_heads][128]
+  float2* cs;         // [n][head_dim / 2] RoPE (cos, sin) per row and pair
+  __nv_bfloat16* k_rot;  // [n][kv_heads][head_dim]
   int32_t* count;     // [n_qp] pair counts, then [2 n_qp] per-128-row-tile counts
   int32_t* list;      // [n_qp][stride] pair lists, then [2 n_qp][stride] per-tile lists
   uint8_t* status;    // [n_qp][stride] tile statuses
@@ -107,7 +108,7 @@ struct PrefillWs {
   size_t bytes;
 };
 
-PrefillWs carve(void* base, int32_t n, int32_t kv_heads) {
+PrefillWs carve(void* base, int32_t n, int32_t kv_heads, int32_t hd) {
   const size_t n_qp = (size_t)(n + 255) / 256, stride = (size_t)(n + 127) / 128;
   PrefillWs w;
   uint8_t* p = reinterpret_cast<uint8_t*>(base);
@@ -117,8 +118,8 @@ PrefillWs carve(void* base, int32_t n, int32_t kv_heads) {
     off += align256(bytes);
     return r;
   };
-  w.cs = reinterpret_cast<float2*>(take((size_t)n * 64 * sizeof(float2)));
-  w.k_rot = reinterpret_cast<__nv_bfloat16*>(take((size_t)n * kv_heads * kHeadDim * 2));
+  w.cs = reinterpret_cast<float2*>(take((size_t)n * (hd / 2) * sizeof(float2)));
+  w.k_rot = reinterpret_cast<__nv_bfloat16*>(take((size_t)n * kv_heads * hd * 2));
   w.count = reinterpret_cast<int32_t*>(take(3 * n_qp * 4));
   w.list = reinterpret_cast<int32_t*>(take(3 * n_qp * stride * 4));
   w.status = take(n_qp * stride);
@@ -151,27 +152,32 @@ mv_status side_for(cudaStream_t st, Side* out) {
 
 }  // namespace
 
-extern "C" size_t mv_prefill_workspace_size(int32_t n, int32_t q_heads, int32_t kv_heads) {
+extern "C" size_t mv_prefill_workspace_size_hd(int32_t n, int32_t q_heads, int32_t kv_heads, int32_t head_dim) {
   (void)q_heads;
-  return n > 0 ? carve(nullptr, n, kv_heads).bytes : 0;
+  return n > 0 && head_dim_supported(head_dim) ? carve(nullptr, n, kv_heads, head_dim).bytes : 0;
+}
+extern "C" size_t mv_prefill_workspace_size(int32_t n, int32_t q_heads, int32_t kv_heads) {
+  return mv_prefill_workspace_size_hd(n, q_heads, kv_heads, kHeadDim);
 }
 
-extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const void* d_v, const int32_t* d_positions,
-                                     const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
-                                     int32_t kv_heads, double rope_base, void* d_out, int32_t out_dtype,
-                                     void* d_workspace, size_t workspace_bytes, mv_stream_t stream) {
+extern "C" mv_status mv_attn_prefill_hd(const void* d_q, const void* d_k, const void* d_v, const int32_t* d_positions,
+                                        const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
+                                        int32_t kv_heads, int32_t head_dim, double rope_base, void* d_out,
+                                        int32_t out_dtype, void* d_workspace, size_t workspace_bytes,
+                                        mv_stream_t stream) {
   if (n <= 0) return n == 0 ? MV_OK : fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_prefill: n < 0");
   if (q_heads <= 0 || kv_heads <= 0 || q_heads % kv_heads)
     return fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_prefill: q_heads must be a multiple of kv_heads");
+  if (!head_dim_supported(head_dim)) return fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_prefill: head_dim must be 64 or 128");
   if (max_depth < 1 || max_depth > kMaxD)
     return fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_prefill: max_depth in 1.." + std::to_string(kMaxD));
   if (out_dtype != 0 && out_dtype != 1) return fail(MV_ERR_INVALID_ARGUMENT, "out_dtype must be 0 (bf16) or 1 (fp32)");
   if (!d_q || !d_k || !d_v || !d_positions || !d_excl || !d_out || !d_workspace)
     return fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_prefill: null buffer");
-  if (workspace_bytes < mv_prefill_workspace_size(n, q_heads, kv_heads))
+  if (workspace_bytes < mv_prefill_workspace_size_hd(n, q_heads, kv_heads, head_dim))
     return fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_prefill: workspace too small");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const PrefillWs ws = carve(d_workspace, n, kv_heads);
+  const PrefillWs ws = carve(d_workspace, n, kv_heads, head_dim);
   const int n_qp = (n + 255) / 256, stride = (n + 127) / 128;
   int32_t* hcount = ws.count + n_qp;                      // per-128-row-tile counts after the pair counts
   int32_t* hlist = ws.list + (size_t)n_qp * stride;       // per-128-row-tile lists after the pair lists
@@ -183,11 +189,19 @@ extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const voi
     return e;
   MV_CUDA_TRY(cudaEventRecord(side.join, side.stream));
   // K rotated once; Q is rotated inside the attention kernel from the per-row (cos, sin) table
-  rope_qk_kernel<<<(unsigned)(((int64_t)n * 16 + 255) / 256), 256, 0, st>>>(
+  rope_qk_kernel<<<(unsigned)(((int64_t)n * (head_dim / 8) + 255) / 256), 256, 0, st>>>(
       (const __nv_bfloat16*)d_q, (const __nv_bfloat16*)d_k, d_positions, n, q_heads, kv_heads,
-      make_rope_table(rope_base > 0 ? rope_base : 10000.0), nullptr, ws.k_rot, ws.cs, ws.counters);
+      make_rope_table(rope_base > 0 ? rope_base : 10000.0, head_dim), nullptr, ws.k_rot, ws.cs, ws.counters);
   MV_LAUNCH_CHECK();
   MV_CUDA_TRY(cudaStreamWaitEvent(st, side.join, 0));
   return prefill_tc3_launch((const __nv_bfloat16*)d_q, ws.k_rot, (const __nv_bfloat16*)d_v, ws.cs, d_excl, max_depth, n,
-                            q_heads, kv_heads, d_out, out_dtype, hcount, hlist, stride, ws.counters, st);
+                            q_heads, kv_heads, head_dim, d_out, out_dtype, hcount, hlist, stride, ws.counters, st);
+}
+
+extern "C" mv_status mv_attn_prefill(const void* d_q, const void* d_k, const void* d_v, const int32_t* d_positions,
+                                     const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
+                                     int32_t kv_heads, double rope_base, void* d_out, int32_t out_dtype,
+                                     void* d_workspace, size_t workspace_bytes, mv_stream_t stream) {
+  return mv_attn_prefill_hd(d_q, d_k, d_v, d_positions, d_excl, max_depth, n, q_heads, kv_heads, kHeadDim, rope_base,
+                            d_out, out_dtype, d_workspace, workspace_bytes, stream);
 }

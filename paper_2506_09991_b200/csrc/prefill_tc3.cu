@@ -50,11 +50,11 @@ constexpr int kOffX3 = kOffBar3 + 512;  // row max / sum exchange: [2 parity][2 
 constexpr int kSmem3 = kOffX3 + 2 * 2 * 128 * 4;
 static_assert(kSmem3 <= 227 * 1024, "prefill v3 smem");
 constexpr uint32_t kIdQK3 = tc::idesc_bf16(128, 128, 0, 0);
-constexpr uint32_t kIdPV3 = tc::idesc_bf16(128, 128, 0, 1);
+template <int HD> constexpr uint32_t id_pv3() { return tc::idesc_bf16(128, HD, 0, 1); }
 constexpr float kLazy3 = 8.f;
 // TMEM columns: three S buffers (S(g) in buffer g % 3) and one O
 constexpr int kSB = 2;  // S / P buffers
-constexpr uint32_t kS0 = 0, kO0 = kSB * 128;  // O of column half c (all 128 dims) at kO0 + c * 128
+constexpr uint32_t kS0 = 0, kO0 = kSB * 128;  // O of column half c (all HD dims) at kO0 + c * HD
 
 struct Tc3Params {
   const int32_t* excl;
@@ -74,20 +74,20 @@ struct __align__(16) Item3 {
   int e0, pad0, pad1, pad2;  // e0: first raw entry of the tile's pair list (read ahead by the scheduler)
 };
 
-template <int B>
+template <int B, int HD>
 __device__ __forceinline__ void qk3(uint64_t qd, uint64_t kd) {
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < HD / 16; ++k) {
     const uint64_t off = (uint64_t)(((k >> 2) * kHalf3 + (k & 3) * 32) >> 4);
     tc::mma_ss(kS0 + B * 128, qd + off, kd + off, kIdQK3, k > 0 ? 1u : 0u);
   }
 }
 // O(h) += P(h) . V[64h, 64h + 64): P of column half h sits in packed columns [64h, 64h + 32)
-template <int B, int H>
+template <int B, int H, int HD>
 __device__ __forceinline__ void pv3(uint64_t vd, bool first) {
 #pragma unroll
   for (int k = 0; k < 4; ++k)
-    tc::mma_ts(kO0 + H * 128, kS0 + B * 128 + H * 64 + k * 8, vd + (uint64_t)(((H * 4 + k) * 2048) >> 4), kIdPV3,
+    tc::mma_ts(kO0 + H * HD, kS0 + B * 128 + H * 64 + k * 8, vd + (uint64_t)(((H * 4 + k) * 2048) >> 4), id_pv3<HD>(),
                (!first || k > 0) ? 1u : 0u);
 }
 
@@ -119,6 +119,7 @@ __device__ __forceinline__ bool pair_any(int q, bool pred) {
 }
 constexpr float kSumLimit3 = 64.f * 256.f;  // a 64-column half's P mass before the reference must move
 
+template <int HD>
 __global__ void __launch_bounds__(kThreads3, 1)
     prefill_tc3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k,
                        const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_o,
@@ -126,6 +127,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
   extern __shared__ uint8_t smem_raw3[];
   uint8_t* smem = smem_align1024(smem_raw3);
   if (smem != smem_raw3) __trap();  // no slack was allocated for alignment
+  constexpr int kNH = HD / 64;              // 64-dim SW128 halves per row (head dim 64: one)
+  constexpr uint32_t kTileTx = kNH * kHalf3;  // bytes of one Q / K / V tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar3);
   uint64_t* q_loaded = bars;             // [kQB3] raw Q tile landed (tx)
   uint64_t* q_full = q_loaded + kQB3;    // [kQB3] Q tile rotated (2 rotator warps)
@@ -210,9 +213,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
           mbar_wait(&q_empty[qb], ((qi / kQB3) - 1) & 1);
           mbar_wait(&qbuf_free[qb], ((qi / kQB3) - 1) & 1);
         }
-        mbar_arrive_expect_tx(&q_loaded[qb], kTile3);
-        tc::tma_load_3d(smem + kOffQ3 + qb * kTile3, &map_q, 0, q_it.h, q_it.t * kT3, &q_loaded[qb]);
-        tc::tma_load_3d(smem + kOffQ3 + qb * kTile3 + kHalf3, &map_q, 64, q_it.h, q_it.t * kT3, &q_loaded[qb]);
+        mbar_arrive_expect_tx(&q_loaded[qb], kTileTx);
+#pragma unroll
+        for (int hh = 0; hh < kNH; ++hh)
+          tc::tma_load_3d(smem + kOffQ3 + qb * kTile3 + hh * kHalf3, &map_q, 64 * hh, q_it.h, q_it.t * kT3, &q_loaded[qb]);
       };
       Item3 nxt;
       claim(nxt);
@@ -234,9 +238,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
           const int s = gk % kKSt3;
           if (gk >= kKSt3) mbar_wait(&k_empty[s], ((gk / kKSt3) - 1) & 1);
           const int kt = e & 0xFFFFF;
-          mbar_arrive_expect_tx(&k_full[s], kTile3);
-          tc::tma_load_3d(smem + kOffK3 + s * kTile3, &map_k, 0, kvh, kt * kT3, &k_full[s]);
-          tc::tma_load_3d(smem + kOffK3 + s * kTile3 + kHalf3, &map_k, 64, kvh, kt * kT3, &k_full[s]);
+          mbar_arrive_expect_tx(&k_full[s], kTileTx);
+#pragma unroll
+          for (int hh = 0; hh < kNH; ++hh)
+            tc::tma_load_3d(smem + kOffK3 + s * kTile3 + hh * kHalf3, &map_k, 64 * hh, kvh, kt * kT3, &k_full[s]);
           ++gk;
           if (j == min(kKSt3, it.m) - 1 && nxt.valid) load_q(nxt, i + 1);
         }
@@ -259,9 +264,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
           const int s = gv % kVSt3;
           if (gv >= kVSt3) mbar_wait(&v_empty[s], ((gv / kVSt3) - 1) & 1);
           const int kt = e & 0xFFFFF;
-          mbar_arrive_expect_tx(&v_full[s], kTile3);
-          tc::tma_load_3d(smem + kOffV3 + s * kTile3, &map_v, 0, kvh, kt * kT3, &v_full[s]);
-          tc::tma_load_3d(smem + kOffV3 + s * kTile3 + kHalf3, &map_v, 64, kvh, kt * kT3, &v_full[s]);
+          mbar_arrive_expect_tx(&v_full[s], kTileTx);
+#pragma unroll
+          for (int hh = 0; hh < kNH; ++hh)
+            tc::tma_load_3d(smem + kOffV3 + s * kTile3 + hh * kHalf3, &map_v, 64 * hh, kvh, kt * kT3, &v_full[s]);
           ++gv;
         }
       }
@@ -283,8 +289,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
       const uint64_t kd = kd0 + (uint64_t)(((gg % kKSt3) * kTile3) >> 4);
       const int b = gg % kSB;
       if (tc::elect_one()) {
-        if (b == 0) qk3<0>(qd, kd);
-        else qk3<1>(qd, kd);
+        if (b == 0) qk3<0, HD>(qd, kd);
+        else qk3<1, HD>(qd, kd);
         tc::mma_commit(&s_full[b]);
         tc::mma_commit(&k_empty[gg % kKSt3]);
       }
@@ -318,11 +324,11 @@ __global__ void __launch_bounds__(kThreads3, 1)
           tc::fence_after();
           if (tc::elect_one()) {
             if (b == 0) {
-              if (h == 0) pv3<0, 0>(vd, j == 0);
-              else pv3<0, 1>(vd, j == 0);
+              if (h == 0) pv3<0, 0, HD>(vd, j == 0);
+              else pv3<0, 1, HD>(vd, j == 0);
             } else {
-              if (h == 0) pv3<1, 0>(vd, j == 0);
-              else pv3<1, 1>(vd, j == 0);
+              if (h == 0) pv3<1, 0, HD>(vd, j == 0);
+              else pv3<1, 1, HD>(vd, j == 0);
             }
             if (h == 1) tc::mma_commit(&v_empty[g % kVSt3]);
           }
@@ -364,16 +370,17 @@ __global__ void __launch_bounds__(kThreads3, 1)
       uint8_t* qt = smem + kOffQ3 + qb * kTile3;
       // 32 chunks per thread in 4 batches of 8: all table loads of a batch are in flight together
       constexpr int kBatch = 8;
-      for (int b0 = 0; b0 < kT3 * 16 / 64; b0 += kBatch) {
+      constexpr int kCh = HD / 8, kLg = HD == 128 ? 4 : 3;  // 16-byte chunks per row
+      for (int b0 = 0; b0 < kT3 * kCh / 64; b0 += kBatch) {
         float4 t01[kBatch], t23[kBatch];
         uint4* q4[kBatch];
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
           const int ch = rt + 64 * (b0 + u);
-          const int row = ch >> 4, c = ch & 15;
+          const int row = ch >> kLg, c = ch & (kCh - 1);
           const int grow = min(qt_t * kT3 + row, P.n - 1);  // rows past n are zero-filled: any angle
           q4[u] = reinterpret_cast<uint4*>(qt + (c >> 3) * kHalf3 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
-          const float4* tb = reinterpret_cast<const float4*>(P.cs + (size_t)grow * 64 + c * 4);
+          const float4* tb = reinterpret_cast<const float4*>(P.cs + (size_t)grow * (HD / 2) + c * 4);
           t01[u] = __ldg(tb);
           t23[u] = __ldg(tb + 1);
         }
@@ -402,8 +409,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
         const int qb_ep = it_i % kQB3;
         if (!P.out_f32) {
           const uint8_t* tile = smem + kOffQ3 + qb_ep * kTile3;
-          tc::tma_store_3d(&map_o, tile, 0, it.h, it.t * kT3);  // rows past n are clipped
-          tc::tma_store_3d(&map_o, tile + kHalf3, 64, it.h, it.t * kT3);
+#pragma unroll
+          for (int hh = 0; hh < kNH; ++hh)  // rows past n are clipped
+            tc::tma_store_3d(&map_o, tile + hh * kHalf3, 64 * hh, it.h, it.t * kT3);
           tc::bulk_commit_group();
           tc::bulk_wait_group_read0();
         }
@@ -434,7 +442,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
       for (int q = 0; q < kExvRegs; ++q) exv[q] = q < P.D ? __ldg(exr + q) : make_int2(0, 0);
       const int32_t* lst = P.tlist + (size_t)it.t * P.stride;
       const int sh = 20 + 2 * (it.t & 1);
-      const uint32_t o_col = kO0 + c * 128;  // this column half's own O (all 128 dims)
+      const uint32_t o_col = kO0 + c * HD;  // this column half's own O (all HD dims)
       float m_ref = -INFINITY, l = 0.f;
       // the list entry of the next tile is loaded one tile ahead (its L2 latency used to sit
       // between releasing P and waiting for the next S)
@@ -526,7 +534,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
             mbar_wait(&v_empty[(g - 1) % kVSt3], ((g - 1) / kVSt3) & 1);
             tc::fence_after();
 #pragma unroll 1
-            for (int cc = 0; cc < 4; ++cc) {
+            for (int cc = 0; cc < HD / 32; ++cc) {
               float o[32];
               tc::tmem_ld32(lane_base + o_col + cc * 32, o);
               tc::tmem_wait_ld();
@@ -547,7 +555,7 @@ __global__ void __launch_bounds__(kThreads3, 1)
         mbar_arrive(&p_full[2 * (g % kSB) + c]);
       }
       // epilogue: combine the two column halves' (reference, sum, O), exchanged while the last P.V
-      // runs; this warp writes dims [64c, 64c + 64)
+      // runs; this warp writes dims [c HD/2, (c + 1) HD/2)
       float2* xs2 = reinterpret_cast<float2*>(s_x);
       xs2[c * 128 + r] = make_float2(m_ref, l);
       pair_sync(quarter);
@@ -566,26 +574,26 @@ __global__ void __launch_bounds__(kThreads3, 1)
       // reads (~2,500 cycles, off the softmax warps' path).  The per-thread row stores this replaces
       // were 256 uncoalesced wavefronts per warp.  fp32 output: direct row stores.
       const int qb_ep = it_i % kQB3;
-      uint8_t* stage = smem + kOffQ3 + qb_ep * kTile3 + c * kHalf3;
 #pragma unroll 1
-      for (int cc = 0; cc < 2; ++cc) {
+      for (int cc = 0; cc < HD / 64; ++cc) {
+        const int d0 = c * (HD / 2) + cc * 32;  // first of the 32 dims of this pass
+        uint8_t* stage = smem + kOffQ3 + qb_ep * kTile3 + (d0 >> 6) * kHalf3;
         float o[32], o1[32];
-        tc::tmem_ld32(lane_base + kO0 + c * 64 + cc * 32, o);
-        tc::tmem_ld32(lane_base + kO0 + 128 + c * 64 + cc * 32, o1);
+        tc::tmem_ld32(lane_base + kO0 + d0, o);
+        tc::tmem_ld32(lane_base + kO0 + HD + d0, o1);
         tc::tmem_wait_ld();
 #pragma unroll
         for (int k = 0; k < 32; ++k) o[k] = (a0 != 0.f ? o[k] * a0 : 0.f) + (a1 != 0.f ? o1[k] * a1 : 0.f);
         if (!P.out_f32) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int ch = cc * 4 + e;  // 16-byte chunk of this row's 128 B half
+            const int ch = ((d0 & 63) >> 3) + e;  // 16-byte chunk of this row's 128 B half
             *reinterpret_cast<uint4*>(stage + r * 128 + ((ch ^ (r & 7)) << 4)) =
                 make_uint4(pack_bf16(o[8 * e], o[8 * e + 1]), pack_bf16(o[8 * e + 2], o[8 * e + 3]),
                            pack_bf16(o[8 * e + 4], o[8 * e + 5]), pack_bf16(o[8 * e + 6], o[8 * e + 7]));
           }
         } else if (i < P.n) {
-          const int d0 = c * 64 + cc * 32;
-          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + it.h) * kHeadDim + d0);
+          float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + ((size_t)i * P.hq + it.h) * HD + d0);
 #pragma unroll
           for (int e = 0; e < 8; ++e) dst[e] = make_float4(o[4 * e], o[4 * e + 1], o[4 * e + 2], o[4 * e + 3]);
         }
@@ -610,15 +618,16 @@ __global__ void __launch_bounds__(kThreads3, 1)
 // v3 launch on rotated q/k and the caller's v; tcount / tlist / hcount from tile_map2.
 mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_rot, const __nv_bfloat16* v,
                              const float2* cs, const int32_t* d_excl, int32_t max_depth, int32_t n, int32_t q_heads,
-                             int32_t kv_heads, void* d_out, int32_t out_dtype, const int32_t* hcount,
+                             int32_t kv_heads, int32_t head_dim, void* d_out, int32_t out_dtype, const int32_t* hcount,
                              const int32_t* tlist, int32_t stride, int32_t* counters, cudaStream_t st) {
   if (max_depth > 64) return fail(MV_ERR_INVALID_ARGUMENT, "prefill: max_depth > 64");
   CUtensorMap mq, mk, mvv, mo;
-  if (mv_status e = tc::make_rows_map(&mq, q_raw, n, q_heads, kT3)) return e;
+  if (mv_status e = tc::make_rows_map(&mq, q_raw, n, q_heads, kT3, head_dim)) return e;
   // bf16 output map (same [n][hq][128] shape and box as Q); unused for fp32 output
-  if (mv_status e = tc::make_rows_map(&mo, out_dtype == 1 ? (const void*)q_raw : d_out, n, q_heads, kT3)) return e;
-  if (mv_status e = tc::make_rows_map(&mk, k_rot, n, kv_heads, kT3)) return e;
-  if (mv_status e = tc::make_rows_map(&mvv, v, n, kv_heads, kT3)) return e;
+  if (mv_status e = tc::make_rows_map(&mo, out_dtype == 1 ? (const void*)q_raw : d_out, n, q_heads, kT3, head_dim))
+    return e;
+  if (mv_status e = tc::make_rows_map(&mk, k_rot, n, kv_heads, kT3, head_dim)) return e;
+  if (mv_status e = tc::make_rows_map(&mvv, v, n, kv_heads, kT3, head_dim)) return e;
   Tc3Params T;
   T.excl = d_excl;
   T.hcount = hcount;
@@ -632,7 +641,7 @@ mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_
   T.D = max_depth;
   T.n_qt = (n + kT3 - 1) / kT3;
   T.stride = stride;
-  T.scale_log2 = 1.4426950408889634f / sqrtf((float)kHeadDim);
+  T.scale_log2 = 1.4426950408889634f / sqrtf((float)head_dim);
   T.n_items = T.n_qt * q_heads;
   static std::once_flag attr_once[kMaxDevices];
   static int sms_dev[kMaxDevices] = {};
@@ -641,12 +650,15 @@ mv_status prefill_tc3_launch(const __nv_bfloat16* q_raw, const __nv_bfloat16* k_
   std::call_once(attr_once[cur], [&] {
     attr_err = cudaDeviceGetAttribute(&sms_dev[cur], cudaDevAttrMultiProcessorCount, cur);
     if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(prefill_tc3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem3);
+      attr_err = cudaFuncSetAttribute(prefill_tc3_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem3);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(prefill_tc3_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem3);
   });
   MV_CUDA_TRY(attr_err);
   const int num_sms = sms_dev[cur] > 0 ? sms_dev[cur] : 148;
   T.counters = counters;
-  prefill_tc3_kernel<<<std::min(T.n_items, num_sms), kThreads3, kSmem3, st>>>(mq, mk, mvv, mo, T);
+  if (head_dim == 128) prefill_tc3_kernel<128><<<std::min(T.n_items, num_sms), kThreads3, kSmem3, st>>>(mq, mk, mvv, mo, T);
+  else prefill_tc3_kernel<64><<<std::min(T.n_items, num_sms), kThreads3, kSmem3, st>>>(mq, mk, mvv, mo, T);
   MV_LAUNCH_CHECK();
   return MV_OK;
 }

@@ -219,7 +219,7 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
 
 // Host: a [n][heads][128] bf16 tensor as a 3-D TMA map with a (64 dims x 1 head x box_rows) box
 // and 128 B swizzle: one load lands one K-major SW128 half-tile [box_rows][64].
-mv_status make_rows_map(CUtensorMap* map, const void* base, int n, int heads, int box_rows);
+mv_status make_rows_map(CUtensorMap* map, const void* base, int n, int heads, int box_rows, int hd);
 
 }  // namespace tc
 }  // namespace mv

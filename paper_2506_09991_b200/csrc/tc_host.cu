@@ -23,11 +23,11 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-mv_status make_rows_map(CUtensorMap* map, const void* base, int n, int heads, int box_rows) {
+mv_status make_rows_map(CUtensorMap* map, const void* base, int n, int heads, int box_rows, int hd) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return fail(MV_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)kHeadDim, (cuuint64_t)heads, (cuuint64_t)n};
-  cuuint64_t strides[2] = {(cuuint64_t)kHeadDim * 2, (cuuint64_t)heads * kHeadDim * 2};
+  cuuint64_t dims[3] = {(cuuint64_t)hd, (cuuint64_t)heads, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)hd * 2, (cuuint64_t)heads * hd * 2};
   cuuint32_t box[3] = {64, 1, (cuuint32_t)box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,

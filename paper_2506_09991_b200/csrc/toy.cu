@@ -10,8 +10,9 @@
 // reference's own frequency expression, attention through K4 (mv_toy_step, one launch for all lanes,
 // K/V appended into the paged store) or K3 (mv_toy_forward, masked prefill).
 //
-// Head dims below 128 (C1: 4 heads x 64) ride the 128-wide attention kernels zero-padded: zero q/k
-// dims add nothing to q.k, zero v dims give zero outputs that are dropped, and q is pre-scaled by
+// Head dims 64 (C1: 4 heads x 64) and 128 run on the attention kernels' native head dims
+// (mv_attn_head_dim).  Any other even head dim below 128 rides the 128-wide kernels zero-padded: zero
+// q/k dims add nothing to q.k, zero v dims give zero outputs that are dropped, and q is pre-scaled by
 // sqrt(128 / dh) so the kernels' 1/sqrt(128) becomes 1/sqrt(dh).  The rotation uses dh's frequencies,
 // so q and k are rotated here and the kernels see position 0 (their identity rotation).
 #include <cmath>
@@ -83,11 +84,11 @@ __global__ void toy_embed_kernel(const int32_t* __restrict__ tokens, int n, cons
   for (int d = threadIdx.x; d < D; d += blockDim.x) x[(size_t)i * D + d] = emb[(size_t)id * D + d];
 }
 
-// qkv [n][3D] -> q, k, v bf16 [n][H][128] (zero-padded), q and k rotated at pos with dh's
-// frequencies (fp64 angle and sincos, toy_model.cpp:30-41), q scaled by sqrt(128 / dh).  Optionally the
+// qkv [n][3D] -> q, k, v bf16 [n][H][ad] (ad = attention head dim, zero-padded past dh), q and k rotated
+// at pos with dh's frequencies (fp64 angle and sincos, toy_model.cpp:30-41), q scaled by sqrt(ad / dh).  Optionally the
 // reference's cache record of the token for this layer: kv_rec[n][rec] at layer_off = [K (rotated) | V].
 __global__ void toy_qkv_post_kernel(const float* __restrict__ qkv, const int32_t* __restrict__ pos, int n, int H,
-                                    int dh, const double* __restrict__ inv, float qscale,
+                                    int dh, int ad, const double* __restrict__ inv, float qscale,
                                     __nv_bfloat16* __restrict__ q, __nv_bfloat16* __restrict__ k,
                                     __nv_bfloat16* __restrict__ v, float* __restrict__ kv_rec, int rec, int layer_off) {
   const int i = blockIdx.x;
@@ -95,9 +96,9 @@ __global__ void toy_qkv_post_kernel(const float* __restrict__ qkv, const int32_t
   const int D = H * dh;
   const float* row = qkv + (size_t)i * 3 * D;
   const int p = pos[i];
-  for (int e = threadIdx.x; e < H * 64; e += blockDim.x) {  // (head, pair of the padded 128 dims)
-    const int h = e >> 6, t = e & 63;
-    const size_t o = ((size_t)i * H + h) * 128 + 2 * t;
+  for (int e = threadIdx.x; e < H * (ad / 2); e += blockDim.x) {  // (head, pair of the ad dims)
+    const int h = e / (ad / 2), t = e % (ad / 2);
+    const size_t o = ((size_t)i * H + h) * ad + 2 * t;
     if (2 * t >= dh) {
       q[o] = q[o + 1] = k[o] = k[o + 1] = v[o] = v[o + 1] = __float2bfloat16(0.f);
       continue;
@@ -124,24 +125,25 @@ __global__ void toy_qkv_post_kernel(const float* __restrict__ qkv, const int32_t
   }
 }
 
-// attention output [n][H][128] fp32 -> [n][D] (the first dh dims of each head)
-__global__ void toy_gather_heads_kernel(const float* __restrict__ att, int n, int H, int dh, float* __restrict__ a) {
+// attention output [n][H][ad] fp32 -> [n][D] (the first dh dims of each head)
+__global__ void toy_gather_heads_kernel(const float* __restrict__ att, int n, int H, int dh, int ad,
+                                        float* __restrict__ a) {
   const int i = blockIdx.x;
   if (i >= n) return;
-  for (int e = threadIdx.x; e < H * dh; e += blockDim.x) a[(size_t)i * H * dh + e] = att[((size_t)i * H + e / dh) * 128 + e % dh];
+  for (int e = threadIdx.x; e < H * dh; e += blockDim.x) a[(size_t)i * H * dh + e] = att[((size_t)i * H + e / dh) * ad + e % dh];
 }
 
-// reference cache records (fp64 [ctx][rec], per layer [K | V]) -> bf16 padded K, V of one layer
+// reference cache records (fp64 [ctx][rec], per layer [K | V]) -> bf16 K, V [ctx][H][ad] of one layer
 __global__ void toy_records_kernel(const double* __restrict__ recs, int n, int rec, int layer_off, int H, int dh,
-                                   __nv_bfloat16* __restrict__ k, __nv_bfloat16* __restrict__ v) {
+                                   int ad, __nv_bfloat16* __restrict__ k, __nv_bfloat16* __restrict__ v) {
   const int i = blockIdx.x;
   if (i >= n) return;
   const int D = H * dh;
-  for (int e = threadIdx.x; e < H * 128; e += blockDim.x) {
-    const int h = e >> 7, d = e & 127;
+  for (int e = threadIdx.x; e < H * ad; e += blockDim.x) {
+    const int h = e / ad, d = e % ad;
     const bool in = d < dh;
-    k[(size_t)i * H * 128 + e] = __float2bfloat16(in ? (float)recs[(size_t)i * rec + layer_off + h * dh + d] : 0.f);
-    v[(size_t)i * H * 128 + e] = __float2bfloat16(in ? (float)recs[(size_t)i * rec + layer_off + D + h * dh + d] : 0.f);
+    k[(size_t)i * H * ad + e] = __float2bfloat16(in ? (float)recs[(size_t)i * rec + layer_off + h * dh + d] : 0.f);
+    v[(size_t)i * H * ad + e] = __float2bfloat16(in ? (float)recs[(size_t)i * rec + layer_off + D + h * dh + d] : 0.f);
   }
 }
 
@@ -181,7 +183,7 @@ void linear(const float* x, const float* W, float* y, int n, int M, int K, cudaS
 
 struct ToyDev {
   mv_toy_config cfg{};
-  int D = 0, dh = 0, hidden = 0;
+  int D = 0, dh = 0, ad = 0, hidden = 0;  // ad: the attention kernels' head dim (mv_attn_head_dim(dh))
   float *emb = nullptr, *unemb = nullptr;
   std::vector<float*> wqkv, wo, up, down;  // per layer, device
   double* inv = nullptr;                   // [dh / 2] RoPE inverse frequencies
@@ -219,12 +221,12 @@ struct ToyDev {
     const int H = cfg.heads;
     MV_CUDA_TRY(cudaMalloc(&x, sizeof(float) * c * D));
     MV_CUDA_TRY(cudaMalloc(&qkv, sizeof(float) * c * 3 * D));
-    MV_CUDA_TRY(cudaMalloc(&att, sizeof(float) * c * H * 128));
+    MV_CUDA_TRY(cudaMalloc(&att, sizeof(float) * c * H * ad));
     MV_CUDA_TRY(cudaMalloc(&a, sizeof(float) * c * D));
     MV_CUDA_TRY(cudaMalloc(&h, sizeof(float) * c * hidden));
-    MV_CUDA_TRY(cudaMalloc(&q, sizeof(__nv_bfloat16) * c * H * 128));
-    MV_CUDA_TRY(cudaMalloc(&k, sizeof(__nv_bfloat16) * c * H * 128));
-    MV_CUDA_TRY(cudaMalloc(&v, sizeof(__nv_bfloat16) * c * H * 128));
+    MV_CUDA_TRY(cudaMalloc(&q, sizeof(__nv_bfloat16) * c * H * ad));
+    MV_CUDA_TRY(cudaMalloc(&k, sizeof(__nv_bfloat16) * c * H * ad));
+    MV_CUDA_TRY(cudaMalloc(&v, sizeof(__nv_bfloat16) * c * H * ad));
     MV_CUDA_TRY(cudaMalloc(&zero_pos, sizeof(int32_t) * c));
     MV_CUDA_TRY(cudaMemset(zero_pos, 0, sizeof(int32_t) * c));
     cap_rows = c;
@@ -232,7 +234,7 @@ struct ToyDev {
   }
   // post-attention half of a layer: x += Wo a; x += W_down tanh(W_up x)
   void finish_layer(int l, int n, cudaStream_t st) {
-    toy_gather_heads_kernel<<<n, 128, 0, st>>>(att, n, cfg.heads, dh, a);
+    toy_gather_heads_kernel<<<n, 128, 0, st>>>(att, n, cfg.heads, dh, ad, a);
     linear<1>(a, wo[l], x, n, D, D, st);
     linear<2>(x, up[l], h, n, hidden, D, st);
     linear<1>(h, down[l], x, n, D, hidden, st);
@@ -267,6 +269,7 @@ extern "C" mv_status mv_toy_create(const mv_toy_config* cfg, const double* h_wei
   if (m->cfg.rope_base <= 0) m->cfg.rope_base = 10000.0;
   m->D = cfg->model_dim;
   m->dh = cfg->model_dim / cfg->heads;
+  m->ad = mv_attn_head_dim(m->dh);
   m->hidden = 4 * cfg->model_dim;
   const size_t D = m->D, V = cfg->vocab, Hd = m->hidden;
   auto up32 = [&](const double* src, size_t count, float** dst) -> mv_status {
@@ -316,6 +319,10 @@ extern "C" mv_status mv_toy_get_config(const mv_toy* m, mv_toy_config* out) {
 
 extern "C" int32_t mv_toy_vocab(const mv_toy* m) { return m && m->impl ? m->impl->cfg.vocab : 0; }
 
+extern "C" int32_t mv_attn_head_dim(int32_t model_head_dim) {
+  return head_dim_supported(model_head_dim) ? model_head_dim : kHeadDim;
+}
+
 extern "C" mv_status mv_toy_destroy(mv_toy* m) {
   if (!m) return MV_OK;
   delete m->impl;
@@ -326,8 +333,9 @@ extern "C" mv_status mv_toy_destroy(mv_toy* m) {
 static mv_status check_store(const ToyDev& m, mv_kv_store* s) {
   if (!s || !s->impl) return fail(MV_ERR_INVALID_ARGUMENT, "null store");
   const mv_kv_config& c = s->impl->cfg();
-  if (c.kv_heads != m.cfg.heads || c.layers != m.cfg.layers)
-    return fail(MV_ERR_INVALID_ARGUMENT, "store attention planes do not match the toy model (layers x heads x 128)");
+  if (c.kv_heads != m.cfg.heads || c.layers != m.cfg.layers || c.head_dim != m.ad)
+    return fail(MV_ERR_INVALID_ARGUMENT,
+                "store attention planes do not match the toy model (layers x heads x mv_attn_head_dim(d_h))");
   return MV_OK;
 }
 
@@ -343,12 +351,12 @@ extern "C" mv_status mv_toy_step(mv_toy* tm, mv_kv_store* s, const uint64_t* h_h
   cudaStream_t cs = st.stream();
   if (mv_status e = m.ensure_rows(n)) return e;
   const int H = m.cfg.heads, D = m.D, L = m.cfg.layers, rec = 2 * L * D;
-  const float qscale = sqrtf((float)kHeadDim / (float)m.dh);
+  const float qscale = sqrtf((float)m.ad / (float)m.dh);
   toy_embed_kernel<<<n, 128, 0, cs>>>(d_tokens, n, m.emb, m.cfg.vocab, D, m.x);
   MV_LAUNCH_CHECK();
   for (int l = 0; l < L; ++l) {
     linear<0>(m.x, m.wqkv[l], m.qkv, n, 3 * D, D, cs);
-    toy_qkv_post_kernel<<<n, 128, 0, cs>>>(m.qkv, d_positions, n, H, m.dh, m.inv, qscale, m.q, m.k, m.v, d_kv, rec,
+    toy_qkv_post_kernel<<<n, 128, 0, cs>>>(m.qkv, d_positions, n, H, m.dh, m.ad, m.inv, qscale, m.q, m.k, m.v, d_kv, rec,
                                             l * 2 * D);
     MV_LAUNCH_CHECK();
     // engine.cpp:639-641 (extend + release) in place: the token joins each lane's cache, K already
@@ -383,7 +391,7 @@ extern "C" mv_status mv_toy_load_context(mv_toy* tm, mv_kv_store* s, uint64_t h,
   int64_t base = 0;
   if (mv_status e = st.length(h, &base)) return e;
   for (int l = 0; l < L; ++l) {
-    toy_records_kernel<<<(unsigned)ctx_len, 128, 0, cs>>>(d_rec, (int)ctx_len, rec, l * 2 * D, H, m.dh, m.k, m.v);
+    toy_records_kernel<<<(unsigned)ctx_len, 128, 0, cs>>>(d_rec, (int)ctx_len, rec, l * 2 * D, H, m.dh, m.ad, m.k, m.v);
     MV_LAUNCH_CHECK();
     // the records hold post-RoPE K: positions 0 (identity) for the store's rotation
     mv_status e = l == 0 ? st.append_many(h, ctx_len, nullptr, m.zero_pos, 0, m.k, m.v)
@@ -404,24 +412,24 @@ extern "C" mv_status mv_toy_forward(mv_toy* tm, const int32_t* d_tokens, int32_t
   cudaStream_t cs = reinterpret_cast<cudaStream_t>(stream);
   if (mv_status e = m.ensure_rows(n)) return e;
   const int H = m.cfg.heads, D = m.D, L = m.cfg.layers;
-  const size_t ws = mv_prefill_workspace_size(n, H, H);
+  const size_t ws = mv_prefill_workspace_size_hd(n, H, H, m.ad);
   if (ws > m.ws_bytes) {
     cudaFree(m.ws);
     m.ws = nullptr;
     MV_CUDA_TRY(cudaMalloc(&m.ws, ws));
     m.ws_bytes = ws;
   }
-  const float qscale = sqrtf((float)kHeadDim / (float)m.dh);
+  const float qscale = sqrtf((float)m.ad / (float)m.dh);
   toy_embed_kernel<<<n, 128, 0, cs>>>(d_tokens, n, m.emb, m.cfg.vocab, D, m.x);
   MV_LAUNCH_CHECK();
   for (int l = 0; l < L; ++l) {
     linear<0>(m.x, m.wqkv[l], m.qkv, n, 3 * D, D, cs);
-    toy_qkv_post_kernel<<<n, 128, 0, cs>>>(m.qkv, d_positions, n, H, m.dh, m.inv, qscale, m.q, m.k, m.v, nullptr, 0,
+    toy_qkv_post_kernel<<<n, 128, 0, cs>>>(m.qkv, d_positions, n, H, m.dh, m.ad, m.inv, qscale, m.q, m.k, m.v, nullptr, 0,
                                             0);
     MV_LAUNCH_CHECK();
     // ToyModel::forward (toy_model.cpp:174-202): every row over its mask-visible rows, then self
-    if (mv_status e = mv_attn_prefill(m.q, m.k, m.v, m.zero_pos, d_excl, max_depth, n, H, H, m.cfg.rope_base, m.att,
-                                      1, m.ws, m.ws_bytes, stream))
+    if (mv_status e = mv_attn_prefill_hd(m.q, m.k, m.v, m.zero_pos, d_excl, max_depth, n, H, H, m.ad, m.cfg.rope_base,
+                                         m.att, 1, m.ws, m.ws_bytes, stream))
       return e;
     m.finish_layer(l, n, cs);
     MV_LAUNCH_CHECK();

@@ -62,7 +62,7 @@ class PagedStore:
         self._h = ctypes.c_void_p()
         check(lib.mv_kv_store_create(ctypes.byref(cfg), ctypes.byref(self._h)))
         self.record_bytes = record_bytes
-        self.layers, self.kv_heads = layers, kv_heads
+        self.layers, self.kv_heads, self.head_dim = layers, kv_heads, head_dim
         self.set_stream(torch.cuda.current_stream())
 
     def close(self):

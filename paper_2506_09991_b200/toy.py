@@ -10,7 +10,8 @@ Binds three parts of libmvb200 (include/multiverse_b200.h):
   engine of `mv_engine_*` (engine.cu): one batched device pass per step for every active lane, the K5 tag
   interpreter on the device, fork / zero-copy merge of the paged store on spawn / reduce.
 
-Head dims below 128 ride the 128-wide attention kernels zero-padded (toy.cu).
+Head dims 64 and 128 run on native attention kernels; other head dims ride the 128-wide kernels
+zero-padded (toy.cu, mv_attn_head_dim).
 """
 from __future__ import annotations
 

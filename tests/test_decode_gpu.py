@@ -21,18 +21,18 @@ def mv():
 class Req:
     """One request: shared prefix, fork into branches, per-branch private tokens, one decode step."""
 
-    def __init__(self, mv, st, rows, seed, prefix, branches, branch_len, hkv, nested=None, spike=False):
+    def __init__(self, mv, st, rows, seed, prefix, branches, branch_len, hkv, nested=None, spike=False, d=128):
         self.st, self.rows = st, rows
         dev = "cuda"
 
         def add(h, n, pos0, private=False):
-            k = sym_bf16(seed * 1000 + len(rows["k"]) * 7 + 1, (n, hkv, 128))
+            k = sym_bf16(seed * 1000 + len(rows["k"]) * 7 + 1, (n, hkv, d))
             if spike and private:
                 # the middle key of a branch's private run scores ~260 log2 units above the rest of the
                 # branch's context (dims 124-127 barely rotate: theta ~1e-4 rad per position)
                 k[n // 2, :, :] = 0.0
-                k[n // 2, :, 124:] = 512.0
-            v = sym_bf16(seed * 1000 + len(rows["k"]) * 7 + 2, (n, hkv, 128))
+                k[n // 2, :, d - 4:] = 512.0
+            v = sym_bf16(seed * 1000 + len(rows["k"]) * 7 + 2, (n, hkv, d))
             pos = torch.arange(pos0, pos0 + n, dtype=torch.int32)
             st.append_many(h, torch.full((n,), 11, dtype=torch.int32, device=dev), pos.to(dev), 0, k.to(dev),
                            v.to(dev))
@@ -64,21 +64,21 @@ class Req:
         self.root, self.ctx_root = root, ctx_root
 
 
-def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1, spike=False):
-    st = mv.kv.PagedStore(num_pages=num_pages, layers=1, kv_heads=hkv)
+def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1, spike=False, d=128):
+    st = mv.kv.PagedStore(num_pages=num_pages, layers=1, kv_heads=hkv, head_dim=d)
     rows = {"k": [], "v": [], "pos": []}
-    reqs = [Req(mv, st, rows, seed + i, *spec, hkv=hkv, spike=spike) if len(spec) == 3 else
-            Req(mv, st, rows, seed + i, *spec[:3], hkv=hkv, nested=spec[3]) for i, spec in enumerate(reqs_spec)]
+    reqs = [Req(mv, st, rows, seed + i, *spec, hkv=hkv, spike=spike, d=d) if len(spec) == 3 else
+            Req(mv, st, rows, seed + i, *spec[:3], hkv=hkv, nested=spec[3], d=d) for i, spec in enumerate(reqs_spec)]
     handles = [h for r in reqs for h in r.handles]
     ctx = [c for r in reqs for c in r.ctx]
     qpos = [p for r in reqs for p in r.qpos]
     n = len(handles)
     # the decode step: append each branch's new token (K/V), then attend
-    knew = sym_bf16(seed * 77 + 5, (n, hkv, 128))
-    vnew = sym_bf16(seed * 77 + 6, (n, hkv, 128))
-    q = sym_bf16(seed * 77 + 7, (n, hq, 128))
+    knew = sym_bf16(seed * 77 + 5, (n, hkv, d))
+    vnew = sym_bf16(seed * 77 + 6, (n, hkv, d))
+    q = sym_bf16(seed * 77 + 7, (n, hq, d))
     if spike:
-        q[:, :, 124:] = 1.0
+        q[:, :, d - 4:] = 1.0
     pos = torch.tensor(qpos, dtype=torch.int32)
     st.append(handles, torch.full((n,), 12, dtype=torch.int32, device="cuda"), pos.cuda(), 0, knew.cuda(),
               vnew.cuda())
@@ -94,7 +94,7 @@ def run_case(mv, reqs_spec, hq, hkv, num_pages, seed=1, spike=False):
     ctx_full = [c + [base + i] for i, c in enumerate(ctx)]
     ref = oracle.attn_decode(qr, Kr, V, ctx_full)
     err = np.abs(out.float().cpu().numpy() - ref).max()
-    record_margin(f"decode {len(handles)} handles hq={hq}/{hkv}", err, TOL)
+    record_margin(f"decode {len(handles)} handles hq={hq}/{hkv}" + (f" d={d}" if d != 128 else ""), err, TOL)
     # the bf16 output path: identical arithmetic plus the bf16 store rounding (<= 2^-9 |o|)
     out16 = mv.attention.decode(st, handles, q.cuda(), pos.cuda()).float().cpu().numpy()
     assert (np.abs(out16 - ref) <= TOL + np.abs(ref) * 2.0 ** -8).all()
@@ -453,3 +453,33 @@ def test_device_produced_inputs_without_sync(mv):
         ref = oracle.attn_decode(oracle.rope(bf16_to_f64(qs[s]), pos.numpy()), oracle.rope(K, P), V, ctx)
         err = np.abs(outs[s].cpu().numpy() - ref).max()
         assert err < TOL, (s, err)
+
+
+# ---- head dim 64 (the toy model's d_h, toy_model.hpp:29): native decode_tc_kernel<64> ----
+@pytest.mark.parametrize("spec,hq,hkv", [
+    ([(100, 3, 20)], 40, 8),                          # plain units, ragged pages
+    ([(1000, 8, 300), (64, 2, 17)], 40, 8),           # F = 2 row copies (8 x 5 rows)
+    ([(4096, 32, 100)], 40, 8),                       # > 16 members: member groups
+    ([(16, 1, 9000)], 40, 8),                         # split-KV slots + combine
+    ([(333, 4, 70), (50, 2, 5, (20, 3))], 4, 4),      # MHA (C1's 4 heads), nested lineage
+])
+def test_head_dim_64(mv, spec, hq, hkv):
+    err, _ = run_case(mv, spec, hq, hkv, 4096, seed=11, d=64)
+    assert err < TOL
+
+
+def test_head_dim_64_score_spike(mv):
+    err, _ = run_case(mv, [(300, 4, 40)], 40, 8, 512, seed=12, spike=True, d=64)
+    assert err < TOL
+
+
+def test_head_dim_mismatch_raises(mv):
+    st = mv.kv.PagedStore(num_pages=16, layers=1, kv_heads=2, head_dim=64)
+    h = st.create()
+    k = sym_bf16(1, (3, 2, 64)).cuda()
+    st.append_many(h, torch.full((3,), 11, dtype=torch.int32, device="cuda"),
+                   torch.arange(3, dtype=torch.int32, device="cuda"), 0, k, k)
+    with pytest.raises(ValueError):
+        mv.attention.decode(st, [h], sym_bf16(2, (1, 4, 128)).cuda(), torch.tensor([3], dtype=torch.int32).cuda())
+    with pytest.raises(ValueError):  # MV_ERR_INVALID_ARGUMENT: no kernel for head dim 96
+        mv.kv.PagedStore(num_pages=16, layers=1, kv_heads=2, head_dim=96)

@@ -19,20 +19,20 @@ def mv():
     return m
 
 
-def run_prefill(mv, tokens, hq, hkv, rows=None, seed=3, spike=None):
+def run_prefill(mv, tokens, hq, hkv, rows=None, seed=3, spike=None, d=128):
     """Device prefill (K1 intervals -> K3) against the oracle built from the tag stream alone: the oracle's
     own positions (dag.cpp:203-222 restated) and dense build_mask rows (dag.cpp:227-263), so a K1 bug cannot
     be certified by this test."""
     n = len(tokens)
     spec = mv.dag.build_visibility(tokens)
-    q = sym_bf16(seed * 10 + 1, (n, hq, 128))
-    k = sym_bf16(seed * 10 + 2, (n, hkv, 128))
+    q = sym_bf16(seed * 10 + 1, (n, hq, d))
+    k = sym_bf16(seed * 10 + 2, (n, hkv, d))
     if spike is not None:
         # one key whose score dwarfs every other (dims 124-127 barely rotate: theta ~1e-4 rad per position)
-        q[:, :, 124:] = 1.0
+        q[:, :, d - 4:] = 1.0
         k[spike, :, :] = 0.0
-        k[spike, :, 124:] = 512.0
-    v = sym_bf16(seed * 10 + 3, (n, hkv, 128))
+        k[spike, :, d - 4:] = 512.0
+    v = sym_bf16(seed * 10 + 3, (n, hkv, d))
     out = mv.attention.prefill(q.cuda(), k.cuda(), v.cuda(), spec.positions, spec.excl, out_dtype=torch.float32)
     torch.cuda.synchronize()
     err_code, pos, _, _ = oracle.build_dag(tokens)
@@ -43,7 +43,7 @@ def run_prefill(mv, tokens, hq, hkv, rows=None, seed=3, spike=None):
     ref = oracle.attn_prefill_tokens(qr, Kr, bf16_to_f64(v), tokens, rows)
     got = out.cpu().numpy()[rows]
     err = float(np.abs(got - ref).max())
-    record_margin(f"prefill n={n} hq={hq}/{hkv} rows={len(rows)}", err, TOL)
+    record_margin(f"prefill n={n} hq={hq}/{hkv} rows={len(rows)}" + (f" d={d}" if d != 128 else ""), err, TOL)
     return err, spec
 
 
@@ -192,3 +192,39 @@ def test_nesting_deeper_than_eight(mv):
     err, spec = run_prefill(mv, toks, hq=8, hkv=2, seed=12)
     assert spec.excl.shape[1] >= 12
     assert err < TOL, err
+
+
+# ---- head dim 64 (the toy model's d_h, toy_model.hpp:29): native prefill_tc3_kernel<64> ----
+def test_head_dim_64_t1_and_trajectories(mv, dag_golden):
+    t1 = next(c for c in dag_golden if c["name"] == "fixture:t1.txt")["tokens"]
+    err, _ = run_prefill(mv, t1, 4, 4, d=64)
+    assert err < TOL, err
+    for c in [c for c in dag_golden if c["name"].startswith("random4x6") and c["error"] == -1][:6]:
+        err, _ = run_prefill(mv, c["tokens"], 40, 8, d=64, seed=len(c["tokens"]))
+        assert err < TOL, (c["name"], err)
+
+
+@pytest.mark.parametrize("depth,paths,pw", [(2, 3, 40), (3, 2, 60)])
+def test_head_dim_64_nested(mv, depth, paths, pw):
+    err, _ = run_prefill(mv, nested_tokens(depth, paths, pw, seed=depth), 40, 8, d=64)
+    assert err < TOL
+
+
+def test_head_dim_64_spike_and_tiles(mv, dag_golden):
+    toks = nested_tokens(2, 3, 40, seed=9)
+    err, _ = run_prefill(mv, toks, 8, 2, spike=len(toks) // 2, d=64)
+    assert err < TOL
+    for n in (1, 127, 129, 300):
+        err, _ = run_prefill(mv, list(range(30, 30 + n)), 8, 2, d=64, seed=n)
+        assert err < TOL
+
+
+def test_head_dim_64_bf16_output(mv):
+    toks = nested_tokens(2, 3, 40, seed=13)
+    n = len(toks)
+    spec = mv.dag.build_visibility(toks)
+    q, k, v = sym_bf16(81, (n, 8, 64)).cuda(), sym_bf16(82, (n, 2, 64)).cuda(), sym_bf16(83, (n, 2, 64)).cuda()
+    o32 = mv.attention.prefill(q, k, v, spec.positions, spec.excl, out_dtype=torch.float32)
+    o16 = mv.attention.prefill(q, k, v, spec.positions, spec.excl)
+    d = (o16.float() - o32).abs()
+    assert bool((d <= o32.abs() * 2.0 ** -8 + 1e-6).all())
