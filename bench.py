@@ -408,7 +408,8 @@ def decode_arm(args, world, rank, local, D_, workload, heads_mode):
     hkv_l = shard.kv_heads[1] - shard.kv_heads[0]
     hq_l = hkv_l * (HQ // HKV)
     e2e_steps = max(3, args.steps // 2)
-    steps_total = args.warmup + args.steps + HOST_STEPS + e2e_steps
+    k_steps = min(args.steps, 10)  # decode_tc launches timed alone (kernel-timing hook)
+    steps_total = args.warmup + args.steps + HOST_STEPS + k_steps + e2e_steps
     seed_id = shard.requests[0] * 64 + shard.kv_heads[0]
     st, handles, pos0, rnd = build_workload(mv, torch, R, dev, seed_id, wl["prefix"], wl["branches"],
                                             wl["branch_len"], steps_total, hkv=hkv_l)
@@ -478,6 +479,16 @@ def decode_arm(args, world, rank, local, D_, workload, heads_mode):
     D_.sync()
     host_call_ms = 1e3 * float(np.median(host_call))
 
+    # the dominant kernel alone: the library records an event pair around each decode_tc launch (the RoPE
+    # pre-pass and the combine outside it; decode_tc then does not overlap its prologue with the RoPE pass)
+    st.decode_kernel_timing(k_steps)
+    for s in range(k_steps):
+        i = args.warmup + args.steps + HOST_STEPS + s
+        st.append(handles, toks, base_pos + i, 0, ks[i % 2], vs[i % 2])
+        mv.attention.decode(st, handles, qs[i % 2], base_pos + i, out=out)
+    kern = st.decode_kernel_timing(0)
+    (kern_ms,) = max_over_ranks([float(np.mean(kern))], device=dev)
+
     # ---- e2e through the public API with host buffers (pinned), copies inside the region ----
     nq, nk = n * hq_l * D * 2, n * hkv_l * D * 2
     blk = nq + 2 * nk + n * 4
@@ -500,7 +511,7 @@ def decode_arm(args, world, rank, local, D_, workload, heads_mode):
     ee = [D_.event() for _ in range(2)]
     ee[0].record(stream)
     for s in range(e2e_steps):
-        i = args.warmup + args.steps + HOST_STEPS + s
+        i = args.warmup + args.steps + HOST_STEPS + k_steps + s
         hpos[i % 2].numpy()[:] = pos0_np + i
         din.copy_(hin[i % 2], non_blocking=True)
         st.append(handles, toks, dp, 0, dk, dv)
@@ -513,7 +524,9 @@ def decode_arm(args, world, rank, local, D_, workload, heads_mode):
     tokens_per_step = n if heads_mode else n * world  # head-sharded ranks share their tokens
     kv_tokens = info["unique_kv_tokens"] + n * (args.steps + 1) / 2.0  # mean context over the timed steps
     alg_bytes = kv_tokens * hkv_l * D * 2 * 2 + n * hq_l * D * 2 * 2
-    return dict(ms=ms, att_ms=att_ms, ag_ms=ag_ms, e2e_ms=e2e_ms, host_ms=host_ms, host_call_ms=host_call_ms, clk=clk, info=info, n=n, R=R,
+    kv_tokens_k = info["unique_kv_tokens"] + n * (args.steps + HOST_STEPS + (k_steps + 1) / 2.0)
+    alg_bytes_k = kv_tokens_k * hkv_l * D * 2 * 2 + n * hq_l * D * 2 * 2
+    return dict(kern_ms=kern_ms, alg_bytes_k=alg_bytes_k, ms=ms, att_ms=att_ms, ag_ms=ag_ms, e2e_ms=e2e_ms, host_ms=host_ms, host_call_ms=host_call_ms, clk=clk, info=info, n=n, R=R,
                 hkv_l=hkv_l, tokens_per_step=tokens_per_step, kv_tokens=kv_tokens, alg_bytes=alg_bytes,
                 h2d=n * (hq_l + 2 * hkv_l) * D * 2 + n * 4, d2h=n * hq_l * D * 2, store=st)
 
@@ -661,7 +674,8 @@ def run_ours(args):
     heads_mode = args.shard == "heads"
     r = decode_arm(args, world, rank, local, D_, args.workload, heads_mode)
     value = r["tokens_per_step"] / (r["ms"] / 1e3)
-    achieved = r["alg_bytes"] / (r["att_ms"] / 1e3) / 1e9
+    achieved = r["alg_bytes_k"] / (r["kern_ms"] / 1e3) / 1e9  # decode_tc alone
+    achieved_win = r["alg_bytes"] / (r["att_ms"] / 1e3) / 1e9  # RoPE pass + decode_tc + combine, in the timed loop
     traffic, traffic_src = decode_traffic(args.workload, r["R"], args.steps, args.warmup, heads_mode)
     del r["store"]
     D_.release_memory()
@@ -672,7 +686,8 @@ def run_ours(args):
         a4 = argparse.Namespace(**{**vars(args), "steps": min(args.steps, 10), "warmup": min(args.warmup, 3)})
         r4 = decode_arm(a4, world, rank, local, D_, "c4", False)
         v4 = r4["tokens_per_step"] / (r4["ms"] / 1e3)
-        a4b = r4["alg_bytes"] / (r4["att_ms"] / 1e3) / 1e9
+        a4b = r4["alg_bytes_k"] / (r4["kern_ms"] / 1e3) / 1e9
+        a4w = r4["alg_bytes"] / (r4["att_ms"] / 1e3) / 1e9
         sub["c4_decode"] = {
             "workload": "configs[3]: 64 requests x 32 branches sharded by request over the GPUs, 40q/8kv, d128, "
                         "bf16, 16K shared prefix + 32 x 512 branch tokens (32K unique per request), KV page 16",
@@ -681,8 +696,11 @@ def run_ours(args):
             "e2e": {"value": r4["tokens_per_step"] / (r4["e2e_ms"] / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": r4["h2d"], "d2h_bytes_per_step": r4["d2h"]},
             "roofline": {"bound": "hbm", "achieved": a4b, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": a4b / pk["hbm_gbs"], "alg_bytes_per_launch": r4["alg_bytes"],
-                         "launch_ms": r4["att_ms"], "kernel": "decode_tc_kernel (+ rope_q_tile, combine)"},
+                         "frac": a4b / pk["hbm_gbs"], "alg_bytes_per_launch": r4["alg_bytes_k"],
+                         "launch_ms": r4["kern_ms"], "kernel": "decode_tc_kernel",
+                         "window": {"kernels": "rope_q_tile + decode_tc + combine (timed loop)",
+                                    "launch_ms": r4["att_ms"], "alg_bytes": r4["alg_bytes"],
+                                    "frac": a4w / pk["hbm_gbs"]}},
             "host_call_ms_per_step": r4["host_call_ms"], "host_loop_ms_per_step": r4["host_ms"],
             "plan": r4["info"]}
         del r4["store"]
@@ -722,9 +740,15 @@ def run_ours(args):
                     "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
-                         "peak_source": pk_src, "kernel": "decode_tc_kernel (+ rope_q_tile_kernel, combine_kernel)",
-                         "alg_bytes_per_launch": r["alg_bytes"], "launch_ms": r["att_ms"],
-                         "frac_of_8TBs": achieved / 8000.0},
+                         "peak_source": pk_src, "kernel": "decode_tc_kernel",
+                         "alg_bytes_per_launch": r["alg_bytes_k"], "launch_ms": r["kern_ms"],
+                         "launch_timing": "CUDA events recorded by the library around each decode_tc launch "
+                                          "(mv_attn_decode_kernel_timing), 10 steps after the timed loop",
+                         "frac_of_8TBs": achieved / 8000.0,
+                         "window": {"kernels": "rope_q_tile + decode_tc + combine (events around each "
+                                               "mv_attn_decode call in the timed loop)",
+                                    "launch_ms": r["att_ms"], "alg_bytes": r["alg_bytes"],
+                                    "frac": achieved_win / pk["hbm_gbs"]}},
             "gpu_launches": 4 * args.steps,  # per step: k_append_one, rope_q_tile, decode_tc, combine
             "clocks": r["clk"],
             "plan": r["info"],

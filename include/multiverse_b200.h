@@ -228,6 +228,11 @@ typedef struct {
   int64_t naive_kv_tokens;    /* tokens a per-branch decode would read (sum of lengths) */
 } mv_decode_plan_info;
 MV_API mv_status mv_attn_decode_plan_info(mv_kv_store* s, mv_decode_plan_info* out);
+/* Measurement hook: with max_calls > 0, the next max_calls mv_attn_decode calls on this store record a CUDA
+ * event pair around the decode_tc launch alone (the RoPE pre-pass and the split-KV combine outside it).
+ * A call with h_n != NULL first writes the recorded launches' durations (ms) to h_ms[0..*h_n) (waiting for
+ * them); every call re-arms the recording for max_calls more calls (0 = off). */
+MV_API mv_status mv_attn_decode_kernel_timing(mv_kv_store* s, int32_t max_calls, float* h_ms, int32_t* h_n);
 
 /* ======================================================================== */
 /* K3 — branch-masked prefill attention (tcgen05 / TMEM / TMA)               */

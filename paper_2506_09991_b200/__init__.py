@@ -88,6 +88,7 @@ def _load():
         "mv_kv_gather_kv": ([P, u64, i32, P, P], ctypes.c_int),
         "mv_attn_decode": ([P, i32, P, i32, i32, P, P, P, i32], ctypes.c_int),
         "mv_attn_decode_plan_info": ([P, P], ctypes.c_int),
+        "mv_attn_decode_kernel_timing": ([P, i32, P, P], ctypes.c_int),
         "mv_prefill_workspace_size": ([i32, i32, i32], sz),
         "mv_attn_prefill": ([P, P, P, P, P, i32, i32, i32, i32, ctypes.c_double, P, i32, P, sz, P], ctypes.c_int),
         "mv_prefill_workspace_size_hd": ([i32, i32, i32, i32], sz),
@@ -126,7 +127,8 @@ EXPORTED = (
     "mv_kv_store_create", "mv_kv_store_destroy", "mv_kv_set_stream", "mv_kv_planes", "mv_kv_create", "mv_kv_extend",
     "mv_kv_fork", "mv_kv_merge", "mv_kv_release", "mv_kv_length", "mv_kv_stats_get", "mv_kv_resolve",
     "mv_kv_resolve_payloads", "mv_kv_resolve_slots", "mv_kv_append", "mv_kv_write_last", "mv_kv_append_many",
-    "mv_kv_gather_kv", "mv_attn_decode", "mv_attn_decode_plan_info", "mv_prefill_workspace_size", "mv_attn_prefill",
+    "mv_kv_gather_kv", "mv_attn_decode", "mv_attn_decode_plan_info",
+    "mv_attn_decode_kernel_timing", "mv_prefill_workspace_size", "mv_attn_prefill",
     "mv_prefill_workspace_size_hd", "mv_attn_prefill_hd", "mv_attn_head_dim",
     "mv_interp_init", "mv_interp_feed", "mv_kv_write_range", "mv_toy_weight_count", "mv_toy_create", "mv_toy_destroy",
     "mv_toy_get_config", "mv_toy_vocab", "mv_toy_step", "mv_toy_load_context", "mv_toy_forward", "mv_argmax_rows",

@@ -852,6 +852,9 @@ struct DecodePlanCache {
   bool smem_set = false;
   int num_sms = 148;
   int* d_counter = nullptr;
+  // optional kernel timing (mv_attn_decode_kernel_timing): an event pair around decode_tc per call
+  std::vector<cudaEvent_t> t_begin, t_end;
+  int t_used = 0;
   // pinned double-buffered staging for in-place plan updates (no implicit stream sync)
   WorkItem* h_stage[2] = {nullptr, nullptr};
   size_t cap_stage = 0;
@@ -863,6 +866,8 @@ struct DecodePlanCache {
       if (stage_ev[k]) cudaEventDestroy(stage_ev[k]);
     }
     cudaFree(d_counter);
+    for (auto e : t_begin) cudaEventDestroy(e);
+    for (auto e : t_end) cudaEventDestroy(e);
     cudaFree(d_units);
     cudaFree(d_q_tile);
     cudaFree(d_slot_ptr);
@@ -1233,8 +1238,13 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
   lc.stream = stream;
   lc.attrs = pdl;
   lc.numAttrs = 1;
+  // kernel timing: the events sit between the RoPE pass and decode_tc (which then cannot overlap its
+  // prologue with the RoPE pass), so this measures the whole decode_tc launch
+  const bool timed = pc.t_used < (int)pc.t_begin.size();
+  if (timed) MV_CUDA_TRY(cudaEventRecord(pc.t_begin[pc.t_used], stream));
   if (hd == 128) MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel<128>, P));
   else MV_CUDA_TRY(cudaLaunchKernelEx(&lc, decode_tc_kernel<64>, P));
+  if (timed) MV_CUDA_TRY(cudaEventRecord(pc.t_end[pc.t_used++], stream));
   MV_LAUNCH_CHECK();
   if (!pc.multi.empty()) {
     int max_slots = 0;
@@ -1259,5 +1269,35 @@ extern "C" mv_status mv_attn_decode_plan_info(mv_kv_store* s, mv_decode_plan_inf
     return MV_OK;
   }
   *out = s->impl->plan->info;
+  return MV_OK;
+}
+
+extern "C" mv_status mv_attn_decode_kernel_timing(mv_kv_store* s, int32_t max_calls, float* h_ms, int32_t* h_n) {
+  if (!s || !s->impl) return fail(MV_ERR_INVALID_ARGUMENT, "null store");
+  if (!s->impl->plan) s->impl->plan = new DecodePlanCache();
+  DecodePlanCache& pc = *s->impl->plan;
+  if (h_n) {  // read back the recorded calls (waits for the last one)
+    const int n = pc.t_used;
+    for (int k = 0; k < n; ++k) {
+      MV_CUDA_TRY(cudaEventSynchronize(pc.t_end[k]));
+      MV_CUDA_TRY(cudaEventElapsedTime(h_ms + k, pc.t_begin[k], pc.t_end[k]));
+    }
+    *h_n = n;
+  }
+  if (max_calls < 0) return fail(MV_ERR_INVALID_ARGUMENT, "max_calls < 0");
+  while ((int)pc.t_begin.size() < max_calls) {
+    cudaEvent_t a, b;
+    MV_CUDA_TRY(cudaEventCreate(&a));
+    MV_CUDA_TRY(cudaEventCreate(&b));
+    pc.t_begin.push_back(a);
+    pc.t_end.push_back(b);
+  }
+  while ((int)pc.t_begin.size() > max_calls) {
+    cudaEventDestroy(pc.t_begin.back());
+    cudaEventDestroy(pc.t_end.back());
+    pc.t_begin.pop_back();
+    pc.t_end.pop_back();
+  }
+  pc.t_used = 0;
   return MV_OK;
 }

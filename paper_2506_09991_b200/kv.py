@@ -159,6 +159,14 @@ class PagedStore:
         check(lib.mv_kv_gather_kv(self._h, h, layer, _p(k), _p(v)))
         return k, v
 
+    def decode_kernel_timing(self, max_calls: int) -> list[float]:
+        """Durations (ms) of the decode_tc launches recorded since the last call, then record the next
+        max_calls mv_attn_decode calls (0 = off)."""
+        ms = (ctypes.c_float * 1024)()
+        n = ctypes.c_int32(0)
+        check(lib.mv_attn_decode_kernel_timing(self._h, min(max_calls, 1024), ms, ctypes.byref(n)))
+        return [float(ms[i]) for i in range(n.value)]
+
     def plan_info(self) -> dict:
         s = _PlanInfo()
         check(lib.mv_attn_decode_plan_info(self._h, ctypes.byref(s)))
