@@ -25,7 +25,7 @@
 //                     slots (mbarrier complete_tx).  Runs ahead across work units.
 //   warp 3  QK      : one thread.  Per unit: Q smem -> TMEM (tcgen05.cp).  Per block:
 //                     S = Q.K_blk^T (M=128 query rows, N=64 tokens, K=128; A = Q from TMEM) into
-//                     one of 5 TMEM S buffers.
+//                     one of 3 TMEM S buffers.
 //   warp 2  PV      : one thread.  After the softmax, per page O += P_page.V_page (TS: P read
 //                     from TMEM, aliasing S; N=128 dims).
 //   warps 4-11 softmax: thread = query row = TMEM lane; the two warps of a lane quadrant split
@@ -33,7 +33,9 @@
 //                     Masks ragged page slots, log2-domain softmax against a lazily moved
 //                     reference (no per-block max), one score pair in four on the FMA pipe,
 //                     P as packed bf16 back into TMEM.
-//   warps 12-15 epilogue: sums row copies; O row from TMEM -> final output (single-chunk
+//   warps 12-15 epilogue: O is double-buffered by unit parity (TMEM: 3 S + 2 O + Q = 512 columns), so the
+//                     epilogue of unit i drains O[i & 1] while unit i + 1 accumulates into the other.
+//                     Sums row copies; O row from TMEM -> final output (single-chunk
 //                     handles) or an fp32 split-KV partial, merged afterwards by combine_kernel
 //                     (log-sum-exp over the handle's chunks, one CTA per (handle, q head)).
 // Query rows: member m of a unit owns TMEM lanes [m*R, m*R + gqa), R = gqa rounded up to a
@@ -70,14 +72,14 @@ constexpr int kMaxMem = 16;                                 // handles per work 
 constexpr int kQHalf = 128 * 128;                           // [128 rows][64 dims] bf16
 constexpr int kQBytes = 2 * kQHalf;
 constexpr float kSumLimit = 4096.f;                        // block mass that moves the softmax reference
-constexpr int kSBufs = 5;                                   // S / P buffers in flight
+constexpr int kSBufs = 3;                                   // S / P buffers in flight (3 leaves room for two O)
 // every kDecPoly-th score pair on the FMA pipe: C2 +4.5% (1/8: +2.4%, 1/3 ~ 1/4, 1/2 no gain);
 // C4: 1/2 -3.5%, 1/3 -0.5%, 1/6 -2%
 constexpr int kDecPoly = 4;
 constexpr int kTmaLanesPerBlkGroup = 2;  // 4-lane copy groups per stream (blocks in flight per step): C2 +1.4% over 1
-constexpr int kColS = 0;                                    // TMEM: S0..S4 (64 cols each)
-constexpr int kColO = kSBufs * kBlkCols;                    //       O (128 cols)
-constexpr int kColQ = kColO + 128;                          //       Q (64 cols: 128 bf16 dims)
+constexpr int kColS = 0;                                    // TMEM: S0..S2 (64 cols each)
+constexpr int kColO = kSBufs * kBlkCols;                    //       O of even / odd units (2 x 128 cols)
+constexpr int kColQ = kColO + 2 * 128;                      //       Q (64 cols: 128 bf16 dims)
 static_assert(kColQ + 64 <= 512, "TMEM budget");
 constexpr int kTmemCols = 512;
 
@@ -101,12 +103,13 @@ constexpr int kOffEnt = kOffVRing + kVSlots * kSlotBytes;
 constexpr int kOffItem = kOffEnt + 2 * kMaxEntries * 8;
 constexpr int kOffEp = kOffItem + 2 * sizeof(WorkItem);
 constexpr int kOffStat = kOffEp + 2 * sizeof(WorkItem);
-constexpr int kOffFlag = kOffStat + 2 * 128 * 8;  // softmax group max exchange [4][8][32] floats
+constexpr int kOffFlag = kOffStat + 2 * 2 * 128 * 8;  // (reference, sum) per unit parity, warp half, row  // softmax group max exchange [4][8][32] floats
 constexpr int kOffXch = kOffFlag + 4 * 8 * 32 * 4;  // epilogue copy merge [3][32][16] floats
 constexpr int kOffBar = kOffXch + 3 * 32 * 16 * 4;
-constexpr int kNumBars = 4 + 2 * (kKSlots + kVSlots) + 3 * kSBufs + 4 + 2;
+constexpr int kNumBars = 4 + 2 * (kKSlots + kVSlots) + 3 * kSBufs + 7 + 2;
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
-constexpr int kSmem = kOffTmem + 16 + 1024;  // + 1 KiB alignment slack
+// no alignment slack: with no static shared memory the dynamic base is 1024-aligned (checked at entry)
+constexpr int kSmem = kOffTmem + 16;
 static_assert(kSmem <= 227 * 1024, "decode smem");
 
 constexpr uint32_t kIdQK = tc::idesc_bf16(128, kBlkCols, 0, 0);  // S(128 x 64) = Q . K_blk^T
@@ -175,8 +178,8 @@ __device__ __forceinline__ void issue_qk_mmas(uint64_t kd) {  // S_SB = Q . K_bl
 // S columns, so page k's 16 tokens sit at packed column (k >> 1) * 32 + (k & 1) * 8 (F = 1) or
 // k * 16 (F = 2)
 template <int SB, int HD>
-__device__ __forceinline__ void issue_pv_mmas(uint64_t vd, int np, uint32_t acc0, int copies) {  // O += P_SB . V_blk
-  constexpr uint32_t ocol = kColO, pcol = kColS + SB * kBlkCols, id = id_pv<HD>();
+__device__ __forceinline__ void issue_pv_mmas(uint64_t vd, int np, uint32_t acc0, int copies, uint32_t ocol) {  // O += P_SB . V_blk
+  constexpr uint32_t pcol = kColS + SB * kBlkCols, id = id_pv<HD>();
   constexpr int pb = page_bytes<HD>();
   const uint32_t p1 = copies == 1 ? 8 : 16, p2 = 32, p3 = copies == 1 ? 40 : 48;
   tc::mma_ts(ocol, pcol, vd, id, acc0);
@@ -208,7 +211,7 @@ template <int F, int HD>
 __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int n_ent, int n_mem,
                                              const PageRef* se, int warp, int lane, uint32_t tmem, uint64_t* s_full,
                                              uint64_t* p_full, uint64_t* vempty, float* xmax, float& m_out,
-                                             float& l_out) {
+                                             float& l_out, int ob) {
   constexpr int QPC = 4 / F, RPC = 32 * QPC, NP = 2 * F, W = kBlkCols / NP, WP = W / 2;
   const int q = warp & 3, half = (warp - 4) >> 2;
   const int c = q / QPC, lq = q % QPC;
@@ -218,7 +221,7 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
   const bool warp_active = lq * 32 < n_mem * P.R;  // uniform over the group
   const int part = c * 2 + half;
   const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
-  const uint32_t ocol = lane_base + kColO + half * (HD / 2);  // this warp half rescales HD / 2 O columns
+  const uint32_t ocol = lane_base + kColO + ob * 128 + half * (HD / 2);  // this warp half rescales HD / 2 O columns
   float* gmax = xmax + lq * (NP * 32);
   // named barrier per (copy layout, row quadrant group): units with different F never share an
   // id, so warps that run ahead into the next unit (inactive ones skip barriers) cannot mix
@@ -349,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
   constexpr int kRunBytes = kBlkPages * kPB;  // a 4-page block of consecutive pages
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_align1024(smem_raw);
+  if (smem != smem_raw) __trap();  // no slack was allocated for alignment
   uint8_t* ring = smem + kOffRing;
   WorkItem* s_item = reinterpret_cast<WorkItem*>(smem + kOffItem);
   WorkItem* s_ep = reinterpret_cast<WorkItem*>(smem + kOffEp);
@@ -364,10 +368,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
   uint64_t* s_full = vempty + kVSlots;    // [kSBufs] QK commit -> softmax
   uint64_t* p_full = s_full + kSBufs;     // [kSBufs] 8 softmax warps -> PV issuer
   uint64_t* pv_done = p_full + kSBufs;    // [kSBufs] PV commit -> QK issuer (S buffer free)
-  uint64_t* o_full = pv_done + kSBufs;    // PV commit -> epilogue (unit's O final)
-  uint64_t* o_empty = o_full + 1;         // epilogue warps -> PV issuer / softmax
-  uint64_t* stat_full = o_empty + 1;      // 8 softmax warps -> epilogue
-  uint64_t* q_free = stat_full + 1;       // QK issuer commit (Q tile copied to TMEM) -> stager
+  // O is double-buffered by unit parity: unit i accumulates into O[i & 1] while the epilogue drains unit i - 1
+  uint64_t* o_full = pv_done + kSBufs;    // [2] PV commit -> epilogue (unit's O final)
+  uint64_t* o_empty = o_full + 2;         // [2] epilogue warps -> PV issuer / softmax (O, stats, header read)
+  uint64_t* stat_full = o_empty + 2;      // [2] 8 softmax warps -> epilogue
+  uint64_t* q_free = stat_full + 2;       // QK issuer commit (Q tile copied to TMEM) -> stager
   uint64_t* ent_full = q_free + 1;        // [2] stager -> TMA lanes: header + page entries staged (no Q)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffTmem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -383,9 +388,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       mbar_init(&p_full[b], 8);
       mbar_init(&pv_done[b], 1);
     }
-    mbar_init(o_full, 1);
-    mbar_init(o_empty, 4);
-    mbar_init(stat_full, 8);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&o_full[b], 1);
+      mbar_init(&o_empty[b], 4);
+      mbar_init(&stat_full[b], 8);
+    }
     mbar_init(q_free, 1);
     for (int s = 0; s < kKSlots; ++s) {
       mbar_init(&kfull[s], 1);
@@ -565,23 +572,24 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       for (int blk = 0; blk < nblk; ++blk, ++g) {
         const int sb = g % kSBufs;
         mbar_wait(&p_full[sb], (g / kSBufs) & 1);
-        if (blk == 0 && i >= 1) mbar_wait(o_empty, (i - 1) & 1);  // epilogue drained O
+        if (blk == 0 && i >= 2) mbar_wait(&o_empty[i & 1], ((i >> 1) - 1) & 1);  // epilogue drained O[i & 1]
         mbar_wait(&vfull[g % kVSlots], (g / kVSlots) & 1);
         tc::fence_after();
         const uint64_t vd = vdesc0 + (uint64_t)((g % kVSlots) * (kSlotBytes >> 4));
         const int np = n_ent - blk * kBlkPages;
         const uint32_t acc0 = blk > 0 ? 1u : 0u;  // the unit's first block opens O
+        const uint32_t ocol = kColO + (uint32_t)(i & 1) * 128u;
         if (tc::elect_one()) {
           switch (sb) {
-            case 0: issue_pv_mmas<0, HD>(vd, np, acc0, copies); break;
-            case 1: issue_pv_mmas<1, HD>(vd, np, acc0, copies); break;
-            case 2: issue_pv_mmas<2, HD>(vd, np, acc0, copies); break;
-            case 3: issue_pv_mmas<3, HD>(vd, np, acc0, copies); break;
-            default: issue_pv_mmas<4, HD>(vd, np, acc0, copies); break;
+            case 0: issue_pv_mmas<0, HD>(vd, np, acc0, copies, ocol); break;
+            case 1: issue_pv_mmas<1, HD>(vd, np, acc0, copies, ocol); break;
+            case 2: issue_pv_mmas<2, HD>(vd, np, acc0, copies, ocol); break;
+            case 3: issue_pv_mmas<3, HD>(vd, np, acc0, copies, ocol); break;
+            default: issue_pv_mmas<4, HD>(vd, np, acc0, copies, ocol); break;
           }
           tc::mma_commit(&vempty[g % kVSlots]);  // also certifies PV(g) to the softmax (O rescale)
           tc::mma_commit(&pv_done[sb]);
-          if (blk == nblk - 1) tc::mma_commit(o_full);
+          if (blk == nblk - 1) tc::mma_commit(&o_full[i & 1]);
         }
         __syncwarp();
       }
@@ -597,26 +605,27 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       mbar_wait(&item_full[buf], (i >> 1) & 1);
       const WorkItem* si = &s_item[buf];
       if (!si->valid) {
-        if (i >= 1) mbar_wait(o_empty, (i - 1) & 1);
-        if (warp == 4 && lane == 0) s_ep->valid = 0;
+        if (i >= 2) mbar_wait(&o_empty[i & 1], ((i >> 1) - 1) & 1);
+        if (warp == 4 && lane == 0) s_ep[i & 1].valid = 0;
         __syncwarp();
-        if (lane == 0) mbar_arrive(stat_full);
+        if (lane == 0) mbar_arrive(&stat_full[i & 1]);
         break;
       }
       const int n_ent = si->n_entries, n_mem = si->n_mem, copies = si->copies;
       const PageRef* se = s_ent0 + buf * kMaxEntries;
       float m_ref, l;
       if (copies == 2)
-        softmax_unit<2, HD>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
+        softmax_unit<2, HD>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l, i & 1);
       else
-        softmax_unit<1, HD>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l);
+        softmax_unit<1, HD>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l, i & 1);
       // hand (m, l_half) and the unit header to the epilogue, release the unit slot
-      if (i >= 1) mbar_wait(o_empty, (i - 1) & 1);
-      s_stat[half * 128 + r] = make_float2(m_ref, l);
-      if (warp == 4 && lane < kItemInts) reinterpret_cast<int*>(s_ep)[lane] = reinterpret_cast<const int*>(si)[lane];
+      // unit i - 2's epilogue read the stats / header slot of this parity
+      if (i >= 2) mbar_wait(&o_empty[i & 1], ((i >> 1) - 1) & 1);
+      s_stat[(i & 1) * 256 + half * 128 + r] = make_float2(m_ref, l);
+      if (warp == 4 && lane < kItemInts) reinterpret_cast<int*>(s_ep + (i & 1))[lane] = reinterpret_cast<const int*>(si)[lane];
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(stat_full);
+        mbar_arrive(&stat_full[i & 1]);
         mbar_arrive(&slot_empty[buf]);
       }
     }
@@ -627,20 +636,24 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16);
     float* xch = reinterpret_cast<float*>(smem + kOffXch);  // [copy - 1][row in copy][16]
     for (int i = 0;; ++i) {
-      mbar_wait(stat_full, i & 1);
-      if (!s_ep->valid) break;
-      const int n_mem = s_ep->n_mem, kvh = s_ep->kvh, F = s_ep->copies;
+      const int par = i & 1;
+      mbar_wait(&stat_full[par], (i >> 1) & 1);
+      const WorkItem* ep = s_ep + par;
+      const float2* st2 = s_stat + par * 256;
+      if (!ep->valid) break;
+      const int n_mem = ep->n_mem, kvh = ep->kvh, F = ep->copies;
       const int qpc = 4 / F, rpc = 32 * qpc;
       const int c = q / qpc, lq = q % qpc, lr = r - c * rpc;
       const int mi = lr / P.R, hl = lr % P.R;
       const bool warp_active = lq * 32 < n_mem * P.R;
       const bool active = c == 0 && mi < n_mem && hl < P.gqa;
-      const int b = active ? s_ep->members[mi] : 0;
-      const int64_t slot = s_ep->slot_base + mi;
+      const int b = active ? ep->members[mi] : 0;
+      const int64_t slot = ep->slot_base + mi;
       // every copy and warp half shares the reference; the row's mass is the sum of the parts
-      float2 ml = make_float2(s_stat[lr].x, 0.f);
-      for (int cc = 0; cc < F; ++cc) ml.y += s_stat[cc * rpc + lr].y + s_stat[128 + cc * rpc + lr].y;
-      mbar_wait(o_full, i & 1);
+      float2 ml = make_float2(st2[lr].x, 0.f);
+      for (int cc = 0; cc < F; ++cc) ml.y += st2[cc * rpc + lr].y + st2[128 + cc * rpc + lr].y;
+      mbar_wait(&o_full[par], (i >> 1) & 1);
+      const uint32_t ocol = lane_base + kColO + par * 128;
       tc::fence_after();
       const int head = kvh * P.gqa + hl;
       const int nslots = active ? P.slot_cnt[b] : 0;
@@ -651,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         for (int k = 0; k < HD / 32; ++k) {  // 32-column chunks of O
           float o[32];
           if (warp_active) {
-            tc::tmem_ld32(lane_base + kColO + k * 32, o);
+            tc::tmem_ld32(ocol + k * 32, o);
             tc::tmem_wait_ld();
           }
           if (active) {
@@ -669,7 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
         for (int k = 0; k < HD / 16; ++k) {  // 16-column chunks of O
           float o[16];
           if (warp_active) {
-            tc::tmem_ldN<16>(lane_base + kColO + k * 16, o);
+            tc::tmem_ldN<16>(ocol + k * 16, o);
             tc::tmem_wait_ld();
           }
           if (F > 1) {
@@ -703,7 +716,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       }
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(o_empty);
+      if (lane == 0) mbar_arrive(&o_empty[par]);
       if (active && nslots > 1) __stcg(P.part_ml + slot * P.q_heads + head, ml);
     }
   }

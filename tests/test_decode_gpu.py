@@ -116,6 +116,18 @@ def test_score_spike(mv):
     assert err < TOL, err
 
 
+@pytest.mark.parametrize("blen", [1, 17, 33, 49, 65, 130, 257])
+def test_narrow_units(mv, blen):
+    """Private tails of 1..17 blocks (<= 32 query rows in one lane quadrant), including units shorter than the
+    S ring; the single-context case (no prefix) is written by the epilogue directly, the forked ones through
+    the split-KV combine."""
+    err, _ = run_case(mv, [(0, 1, blen), (64, 3, blen), (500, 2, blen + 3)], hq=40, hkv=8, num_pages=512,
+                      seed=blen)
+    assert err < TOL, err
+    err, _ = run_case(mv, [(40, 2, blen)], hq=16, hkv=1, num_pages=256, seed=blen + 1)  # R = 16 rows per member
+    assert err < TOL, err
+
+
 def test_ragged_unaligned_prefix(mv):
     # prefix length not a multiple of 16: the shared tail page is partial (SURVEY.md §7 H1)
     err, _ = run_case(mv, [(77, 4, 19), (5, 2, 3), (0, 2, 1)], hq=40, hkv=8, num_pages=256)
