@@ -495,3 +495,23 @@ def test_head_dim_mismatch_raises(mv):
         mv.attention.decode(st, [h], sym_bf16(2, (1, 4, 128)).cuda(), torch.tensor([3], dtype=torch.int32).cuda())
     with pytest.raises(ValueError):  # MV_ERR_INVALID_ARGUMENT: no kernel for head dim 96
         mv.kv.PagedStore(num_pages=16, layers=1, kv_heads=2, head_dim=96)
+
+
+def test_decode_kernel_timing_hook(mv):
+    """mv_attn_decode_kernel_timing records one event pair per decode_tc launch (bench.py's roofline timing):
+    as many durations as recorded calls, each positive, and recording off once re-armed with 0."""
+    err, st = run_case(mv, [(300, 3, 37)], hq=8, hkv=2, num_pages=256)
+    st.decode_kernel_timing(4)
+    assert st.decode_kernel_timing(4) == []  # nothing recorded yet
+    h = st.create()
+    k = sym_bf16(5, (40, 2, 128)).cuda()
+    st.append_many(h, torch.full((40,), 11, dtype=torch.int32, device="cuda"),
+                   torch.arange(40, dtype=torch.int32, device="cuda"), 0, k, k)
+    q = sym_bf16(6, (1, 8, 128)).cuda()
+    p = torch.tensor([40], dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        mv.attention.decode(st, [h], q, p)
+    ms = st.decode_kernel_timing(0)
+    assert len(ms) == 3 and all(0.0 < x < 100.0 for x in ms)
+    mv.attention.decode(st, [h], q, p)
+    assert st.decode_kernel_timing(0) == []

@@ -10,7 +10,7 @@ python bench.py --gpus 1 --steps 20 --warmup 5 > $o/bench_s20w5.json 2> $o/bench
 bash tools/run_all_benches.sh $o/summary > $o/summary.log 2>&1; echo "summary rc=$?" >> $o/rc.txt
 python bench.py --steps 20 --warmup 5 --extras none > $o/plain.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-      -k regex:"decode_tc|k_append|rope_q_tile|combine" -c 100 --csv --log-file $o/decode_launches.csv \
+      -k regex:"decode_tc|k_append_one|rope_q_tile|combine" -c 120 --csv --log-file $o/decode_launches.csv \
       python bench.py --steps 20 --warmup 5 --extras none > $o/ncu_launches.log 2>&1; echo "launches rc=$?" >> $o/rc.txt
 python bench.py --workload c4 --steps 3 --warmup 3 --extras none --cpu-seconds 0 > $o/c4_plain.json 2>&1 && \
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
