@@ -239,7 +239,10 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
       tc::tmem_ldN<W>(scol + part * W, v);
       // valid slots of this part's tokens (ragged unit head / tail pages, partial pages)
       const int t0 = part * W;
-      uint32_t vm = 0u;
+      constexpr uint32_t kFull = W == 32 ? 0xFFFFFFFFu : ((1u << W) - 1u);
+      // padding rows (GQA heads past gqa, lanes past the unit's members) take no mask: their exponentials
+      // run against an infinite reference (P = 0), so only a ragged page costs the select below
+      uint32_t vm = row_active ? 0u : kFull;
       if (row_active) {
 #pragma unroll
         for (int p = 0; p < (W + 15) / 16; ++p) {
@@ -251,7 +254,6 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
           }
         }
       }
-      constexpr uint32_t kFull = W == 32 ? 0xFFFFFFFFu : ((1u << W) - 1u);
       tc::tmem_wait_ld();
       if (!__all_sync(0xffffffffu, vm == kFull)) {
 #pragma unroll
@@ -291,7 +293,7 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
           if (c2 != c) tc::tmem_stNu<WP>(scol + (c2 * 2 + half) * W, z);
       }
       if (!__any_sync(0xffffffffu, need)) {
-        ls = exp_part(row_active ? m_ref : 0.f);
+        ls = exp_part(row_active ? m_ref : INFINITY);
         need = ls > kSumLimit / NP;
         tc::tmem_stNu<WP>(scol + part * W, pk);
       }
@@ -326,7 +328,7 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
         }
         l *= alpha;
         m_ref = nref;
-        ls = exp_part(m_ref == -INFINITY ? 0.f : m_ref);
+        ls = exp_part(!row_active ? INFINITY : (m_ref == -INFINITY ? 0.f : m_ref));
         tc::tmem_stNu<WP>(scol + part * W, pk);
       }
       l += ls;
