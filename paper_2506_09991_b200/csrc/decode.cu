@@ -103,8 +103,12 @@ constexpr int kOffEnt = kOffVRing + kVSlots * kSlotBytes;
 constexpr int kOffItem = kOffEnt + 2 * kMaxEntries * 8;
 constexpr int kOffEp = kOffItem + 2 * sizeof(WorkItem);
 constexpr int kOffStat = kOffEp + 2 * sizeof(WorkItem);
-constexpr int kOffFlag = kOffStat + 2 * 2 * 128 * 8;  // (reference, sum) per unit parity, warp half, row  // softmax group max exchange [4][8][32] floats
-constexpr int kOffXch = kOffFlag + 4 * 8 * 32 * 4;  // epilogue copy merge [3][32][16] floats
+// (reference, sum) per unit parity, warp half, row
+constexpr int kOffFlag = kOffStat + 2 * 2 * 128 * 8;  // softmax group max exchange: QPC x NP x 32 = 256 floats for every F
+constexpr int kOffRag = kOffFlag + 256 * 4;           // per item buffer: bit b = block b has a ragged page [2][4] words
+constexpr int kRagWords = (kMaxEntries / kBlkPages + 31) / 32;
+static_assert(kRagWords <= 4, "ragged-block bitmask");
+constexpr int kOffXch = kOffRag + 2 * 4 * 4;          // epilogue copy merge [3][32][16] floats
 constexpr int kOffBar = kOffXch + 3 * 32 * 16 * 4;
 constexpr int kNumBars = 4 + 2 * (kKSlots + kVSlots) + 3 * kSBufs + 7 + 2;
 constexpr int kOffTmem = kOffBar + kNumBars * 8;
@@ -209,7 +213,8 @@ __device__ __forceinline__ void group_sync(int id, int count) {
 // its reference max through one named barrier per block (OR-reduced "move" flag).
 template <int F, int HD>
 __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int n_ent, int n_mem,
-                                             const PageRef* se, int warp, int lane, uint32_t tmem, uint64_t* s_full,
+                                             const PageRef* se, const uint32_t* rag, int warp, int lane, uint32_t tmem,
+                                             uint64_t* s_full,
                                              uint64_t* p_full, uint64_t* vempty, float* xmax, float& m_out,
                                              float& l_out, int ob) {
   constexpr int QPC = 4 / F, RPC = 32 * QPC, NP = 2 * F, W = kBlkCols / NP, WP = W / 2;
@@ -243,7 +248,8 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
       // padding rows (GQA heads past gqa, lanes past the unit's members) take no mask: their exponentials
       // run against an infinite reference (P = 0), so only a ragged page costs the select below
       uint32_t vm = row_active ? 0u : kFull;
-      if (row_active) {
+      if (row_active && !((rag[blk >> 5] >> (blk & 31)) & 1u)) vm = kFull;  // every page of the block full
+      if (vm != kFull) {
 #pragma unroll
         for (int p = 0; p < (W + 15) / 16; ++p) {
           const int pg = blk * kBlkPages + t0 / 16 + p;
@@ -442,9 +448,15 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       const int n_ent = si->n_entries, n_mem = si->n_mem, kvh = si->kvh;
       const int64_t eoff = si->entry_off;
       PageRef* se = s_ent0 + buf * kMaxEntries;
+      uint32_t* rag = reinterpret_cast<uint32_t*>(smem + kOffRag) + buf * 4;
+      if (lane < 4) rag[lane] = 0u;
+      __syncwarp();
       for (int j = lane; j < n_ent; j += 32) {
         const PageRef ref = P.arena[eoff + j];
         se[j] = ref.page >= 0 ? ref : make_ref(0, 0, 0);  // an unset entry reads no token (never expected)
+        // a block with a page that is not 16 full slots from slot 0 (or past the unit's end) needs slot masks
+        if (ref.page < 0 || ref_begin(ref) != 0 || ref_count(ref) != kPageTokens || ((j + 1 == n_ent) && (n_ent & 3)))
+          atomicOr(&rag[(j >> 2) >> 5], 1u << ((j >> 2) & 31));
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&ent_full[buf]);  // the TMA lanes may stream this unit's pages
@@ -615,11 +627,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
       }
       const int n_ent = si->n_entries, n_mem = si->n_mem, copies = si->copies;
       const PageRef* se = s_ent0 + buf * kMaxEntries;
+      const uint32_t* rag = reinterpret_cast<const uint32_t*>(smem + kOffRag) + buf * 4;
       float m_ref, l;
       if (copies == 2)
-        softmax_unit<2, HD>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l, i & 1);
+        softmax_unit<2, HD>(P, g, n_ent, n_mem, se, rag, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l, i & 1);
       else
-        softmax_unit<1, HD>(P, g, n_ent, n_mem, se, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l, i & 1);
+        softmax_unit<1, HD>(P, g, n_ent, n_mem, se, rag, warp, lane, tmem, s_full, p_full, vempty, xmax, m_ref, l, i & 1);
       // hand (m, l_half) and the unit header to the epilogue, release the unit slot
       // unit i - 2's epilogue read the stats / header slot of this parity
       if (i >= 2) mbar_wait(&o_empty[i & 1], ((i >> 1) - 1) & 1);
