@@ -446,10 +446,16 @@ __global__ void __launch_bounds__(kThreads3, 1)
       float m_ref = -INFINITY, l = 0.f;
       // the list entry of the next tile is loaded one tile ahead (its L2 latency used to sit
       // between releasing P and waiting for the next S)
-      int nx = it.e0;
+      // the item's tile list in a register window: lane k holds entry w0 + k, one coalesced load per 32
+      // tiles, issued a window ahead (a per-tile load of the next entry stalled ~6% of the softmax samples)
+      int win = lane < it.m ? __ldg(lst + lane) : 0;
+      int win_next = 32 + lane < it.m ? __ldg(lst + 32 + lane) : 0;
       for (int done = 0; done < it.m; ++done, ++g) {
-        int e = nx;
-        nx = done + 1 < it.m ? lst[done + 1] : 0;
+        if (done > 0 && (done & 31) == 0) {
+          win = win_next;
+          win_next = done + 32 + lane < it.m ? __ldg(lst + done + 32 + lane) : 0;
+        }
+        const int e = __shfl_sync(0xffffffffu, win, done & 31);
         const int j0 = (e & 0xFFFFF) * kT3;
         const int status = (e >> sh) & 3;
         const uint32_t s_col = kS0 + (g % kSB) * 128;
