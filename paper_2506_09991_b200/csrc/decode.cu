@@ -233,6 +233,7 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
   // arrivals of differently sized barriers (ids 2-5: F = 1, 6-7: F = 2, 8: F = 4; 1: epilogue)
   const int bar_id = (F == 1 ? 2 : (F == 2 ? 6 : 8)) + lq, bar_cnt = 64 * F;
   const int nblk = (n_ent + kBlkPages - 1) / kBlkPages;
+  const uint32_t rg0 = rag[0], rg1 = rag[1], rg2 = rag[2], rg3 = rag[3];  // ragged-block bits in registers
   float m_ref = -INFINITY, l = 0.f;
   for (int blk = 0; blk < nblk; ++blk, ++g) {
     const int sb = g % kSBufs;
@@ -248,7 +249,8 @@ __device__ __forceinline__ void softmax_unit(const DecodeParams& P, int& g, int 
       // padding rows (GQA heads past gqa, lanes past the unit's members) take no mask: their exponentials
       // run against an infinite reference (P = 0), so only a ragged page costs the select below
       uint32_t vm = row_active ? 0u : kFull;
-      if (row_active && !((rag[blk >> 5] >> (blk & 31)) & 1u)) vm = kFull;  // every page of the block full
+      const uint32_t rw = blk < 32 ? rg0 : (blk < 64 ? rg1 : (blk < 96 ? rg2 : rg3));
+      if (row_active && !((rw >> (blk & 31)) & 1u)) vm = kFull;  // every page of the block full
       if (vm != kFull) {
 #pragma unroll
         for (int p = 0; p < (W + 15) / 16; ++p) {
