@@ -1308,6 +1308,7 @@ extern "C" mv_status mv_attn_decode_kernel_timing(mv_kv_store* s, int32_t max_ca
   DecodePlanCache& pc = *s->impl->plan;
   if (h_n) {  // read back the recorded calls (waits for the last one)
     const int n = pc.t_used;
+    if (n > 0 && !h_ms) return fail(MV_ERR_INVALID_ARGUMENT, "mv_attn_decode_kernel_timing: null h_ms");
     for (int k = 0; k < n; ++k) {
       MV_CUDA_TRY(cudaEventSynchronize(pc.t_end[k]));
       MV_CUDA_TRY(cudaEventElapsedTime(h_ms + k, pc.t_begin[k], pc.t_end[k]));
