@@ -752,25 +752,27 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
 // Split-KV combine for handles with more than one partial slot: one warp per (handle, q head),
 // float4 per lane, log-sum-exp over the handle's slots (single-slot handles were written by the
 // decode epilogue directly).
-constexpr int kCombineWarps = 4;
+constexpr int kCombineWarps = 4;       // narrow mode: pairs per CTA
+constexpr int kCombineWideWarps = 16;  // wide mode: warps merging one pair's slots (a 135K context has 68+ slots)
 // Split-KV combine.  wide = 1: one CTA per (handle, q head), warp w merges slots w, w + 4, ...
 // online (log-sum-exp), two slots' loads in flight, then warp 0 merges the four partial states
 // (a long single context has one slot per chunk: 132 at the 135K-token C5 context).  wide = 0
 // (every handle has few slots, e.g. C2's prefix + private chunk): one warp per (handle, q head).
-__global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(
+__global__ void __launch_bounds__(32 * kCombineWideWarps) combine_kernel(
     const float* __restrict__ part_o, const float2* __restrict__ part_ml, const int32_t* __restrict__ multi,
     int n_multi, const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ slot_idx, int q_heads,
     void* __restrict__ out, int out_f32, int wide, int hd) {
   pdl_wait();  // programmatic launch behind decode_tc_kernel: its partials are visible after this
   pdl_launch_dependents();  // the next step's append may start its launch
-  __shared__ float s_m[kCombineWarps], s_l[kCombineWarps];
-  __shared__ float4 s_acc[kCombineWarps][32];
+  __shared__ float s_m[kCombineWideWarps], s_l[kCombineWideWarps];
+  __shared__ float4 s_acc[kCombineWideWarps][32];
+  const int nwarps = (int)(blockDim.x >> 5);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = wide ? blockIdx.x : blockIdx.x * kCombineWarps + warp;
   if (pair >= n_multi * q_heads) return;  // narrow mode only (warp-uniform)
   const int b = multi[pair / q_heads], h = pair % q_heads;
   const int s0 = slot_ptr[b], s1 = slot_ptr[b + 1];
-  const int first = wide ? s0 + warp : s0, step = wide ? kCombineWarps : 1;
+  const int first = wide ? s0 + warp : s0, step = wide ? nwarps : 1;
   float m = -INFINITY, l = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   auto merge = [&](float2 ml, float4 v) {
@@ -804,7 +806,7 @@ __global__ void __launch_bounds__(32 * kCombineWarps) combine_kernel(
     m = -INFINITY;
     l = 0.f;
     acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int w = 0; w < kCombineWarps; ++w) merge(make_float2(s_m[w], s_l[w]), s_acc[w][lane]);
+    for (int w = 0; w < nwarps; ++w) merge(make_float2(s_m[w], s_l[w]), s_acc[w][lane]);
   }
   const float inv = l > 0.f ? 1.f / l : 0.f;
   const int64_t at = ((int64_t)b * q_heads + h) * hd + lane * 4;
@@ -1282,7 +1284,7 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     const int wide = max_slots > 8 ? 1 : 0;
     const size_t pairs = pc.multi.size() * (size_t)q_heads;
     lc.gridDim = dim3((unsigned)(wide ? pairs : (pairs + kCombineWarps - 1) / kCombineWarps));
-    lc.blockDim = dim3(32 * kCombineWarps);
+    lc.blockDim = dim3(32 * (wide ? kCombineWideWarps : kCombineWarps));
     lc.dynamicSmemBytes = 0;
     MV_CUDA_TRY(cudaLaunchKernelEx(&lc, combine_kernel, (const float*)pc.d_part_o, (const float2*)pc.d_part_ml,
                                    (const int32_t*)pc.d_multi, (int)pc.multi.size(), (const int32_t*)pc.d_slot_ptr,
