@@ -753,7 +753,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_tc_kernel(const DecodePara
 // float4 per lane, log-sum-exp over the handle's slots (single-slot handles were written by the
 // decode epilogue directly).
 constexpr int kCombineWarps = 4;       // narrow mode: pairs per CTA
-constexpr int kCombineWideWarps = 16;  // wide mode: warps merging one pair's slots (a 135K context has 68+ slots)
+constexpr int kCombineWideWarps = 16;
+constexpr int kMultiRec = 10;          // ints per multi-slot handle: b, slot count, up to 8 slots (narrow mode)  // wide mode: warps merging one pair's slots (a 135K context has 68+ slots)
 // Split-KV combine.  wide = 1: one CTA per (handle, q head), warp w merges slots w, w + 4, ...
 // online (log-sum-exp), two slots' loads in flight, then warp 0 merges the four partial states
 // (a long single context has one slot per chunk: 132 at the 135K-token C5 context).  wide = 0
@@ -770,7 +771,52 @@ __global__ void __launch_bounds__(32 * kCombineWideWarps) combine_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = wide ? blockIdx.x : blockIdx.x * kCombineWarps + warp;
   if (pair >= n_multi * q_heads) return;  // narrow mode only (warp-uniform)
-  const int b = multi[pair / q_heads], h = pair % q_heads;
+  const int h = pair % q_heads;
+  const bool dims = lane * 4 < hd;  // float4 of dims per lane (lanes 16-31 idle at head dim 64)
+  // multi: per handle {b, slot count, its <= 8 slots} (kMultiRec ints), so the narrow path needs one load
+  // before the partials' (instead of multi -> slot_ptr -> slot_idx -> partials)
+  const int rv = lane < kMultiRec ? __ldg(multi + (size_t)(pair / q_heads) * kMultiRec + lane) : 0;
+  const int b = __shfl_sync(0xffffffffu, rv, 0);
+  if (!wide) {
+    const int ns = __shfl_sync(0xffffffffu, rv, 1);
+    float2 ml[kMultiRec - 2];
+    float4 v[kMultiRec - 2];
+#pragma unroll
+    for (int u = 0; u < kMultiRec - 2; ++u) {
+      const int64_t sl = __shfl_sync(0xffffffffu, rv, 2 + u);
+      ml[u] = make_float2(-INFINITY, 0.f);
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (u < ns) {
+        ml[u] = part_ml[sl * q_heads + h];
+        if (dims) v[u] = *reinterpret_cast<const float4*>(&part_o[(sl * q_heads + h) * hd + lane * 4]);
+      }
+    }
+    float m = -INFINITY;
+#pragma unroll
+    for (int u = 0; u < kMultiRec - 2; ++u) m = fmaxf(m, ml[u].x);
+    float l = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < kMultiRec - 2; ++u)
+      if (ml[u].x != -INFINITY) {
+        const float w = fast_exp2(ml[u].x - m);
+        l += w * ml[u].y;
+        acc = make_float4(acc.x + w * v[u].x, acc.y + w * v[u].y, acc.z + w * v[u].z, acc.w + w * v[u].w);
+      }
+    if (!dims) return;
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    const int64_t at = ((int64_t)b * q_heads + h) * hd + lane * 4;
+    if (out_f32) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + at) =
+          make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+    } else {
+      uint2 pk;
+      pk.x = pack_bf16(acc.x * inv, acc.y * inv);
+      pk.y = pack_bf16(acc.z * inv, acc.w * inv);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + at) = pk;
+    }
+    return;
+  }
   const int s0 = slot_ptr[b], s1 = slot_ptr[b + 1];
   const int first = wide ? s0 + warp : s0, step = wide ? nwarps : 1;
   float m = -INFINITY, l = 0.f;
@@ -783,7 +829,6 @@ __global__ void __launch_bounds__(32 * kCombineWideWarps) combine_kernel(
     l = l * a + w * ml.y;
     m = nm;
   };
-  const bool dims = lane * 4 < hd;  // float4 of dims per lane (lanes 16-31 idle at head dim 64)
   for (int s = first; s < s1; s += 2 * step) {
     const int64_t sa = slot_idx[s];
     const bool two = s + step < s1;
@@ -871,6 +916,7 @@ struct DecodePlanCache {
   // host plan
   std::vector<WorkItem> units;
   std::vector<int32_t> slot_ptr, slot_idx, slot_cnt, multi;  // multi: handles with > 1 slot
+  std::vector<int32_t> multi_rec;  // per multi handle: b, slot count, its first 8 slots (combine_kernel)
   std::vector<int32_t> tail_item, tail_c0;  // per handle: item holding its private tail chunk (-1 none)
   int32_t n_slots = 0;
   mv_decode_plan_info info{};
@@ -1194,10 +1240,19 @@ extern "C" mv_status mv_attn_decode(mv_kv_store* s, int32_t layer, const uint64_
     if (mv_status e = ensure_dev(pc.d_slot_ptr, pc.cap_ptr, pc.slot_ptr.size())) return e;
     if (mv_status e = ensure_dev(pc.d_slot_idx, pc.cap_idx, std::max<size_t>(1, pc.slot_idx.size()))) return e;
     if (mv_status e = ensure_dev(pc.d_slot_cnt, pc.cap_cnt, pc.slot_cnt.size())) return e;
-    if (mv_status e = ensure_dev(pc.d_multi, pc.cap_multi, std::max<size_t>(1, pc.multi.size()))) return e;
-    if (!pc.multi.empty())
-      MV_CUDA_TRY(cudaMemcpyAsync(pc.d_multi, pc.multi.data(), sizeof(int32_t) * pc.multi.size(),
+    if (mv_status e = ensure_dev(pc.d_multi, pc.cap_multi, std::max<size_t>(1, pc.multi.size() * kMultiRec))) return e;
+    if (!pc.multi.empty()) {
+      pc.multi_rec.assign(pc.multi.size() * kMultiRec, 0);
+      for (size_t k = 0; k < pc.multi.size(); ++k) {
+        const int32_t b = pc.multi[k], ns = pc.slot_cnt[b];
+        int32_t* rec = pc.multi_rec.data() + k * kMultiRec;
+        rec[0] = b;
+        rec[1] = ns;
+        for (int j = 0; j < ns && j < kMultiRec - 2; ++j) rec[2 + j] = pc.slot_idx[pc.slot_ptr[b] + j];
+      }
+      MV_CUDA_TRY(cudaMemcpyAsync(pc.d_multi, pc.multi_rec.data(), sizeof(int32_t) * pc.multi_rec.size(),
                                   cudaMemcpyHostToDevice, stream));
+    }
     const size_t old_slots = pc.cap_slots;
     // 2x headroom: later re-plans split growing tails into more chunks (more partial slots)
     if (mv_status e = ensure_dev(pc.d_part_ml, pc.cap_slots, std::max<size_t>(1, (size_t)pc.n_slots * q_heads * 2)))
